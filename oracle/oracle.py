@@ -1,0 +1,363 @@
+"""ctypes view of the CPU oracle (oracle/_build/liboracle.so).
+
+TEST INFRASTRUCTURE ONLY — imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` leg. The product package
+(paper_2201_05752_b200) never imports this module.
+
+Every function mirrors a reference symbol; see moses_oracle.hpp for the
+file:line each one restates.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "liboracle.so")
+
+# moseslab::ErrorCode ordinals (errors.hpp:10-36)
+ERROR_NAMES = [
+    "invalid-task", "invalid-config", "space-too-large", "immutable-space", "bad-dims",
+    "dim-mismatch", "shape-mismatch", "version-mismatch", "corrupt-stream", "empty-dataset",
+    "invalid-ratio", "unnormalized-threshold", "adversary-disabled", "unstable-decay",
+    "infeasible-split", "zero-mean", "insufficient-batches", "budget-infeasible",
+    "missing-reference-strategy", "mismatched-runs", "empty-rows", "parse-error",
+    "missing-field", "io-error", "usage-error",
+]
+
+THRESHOLD, RATIO = 1, 2
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = ERROR_NAMES[code - 1] if 1 <= code <= len(ERROR_NAMES) else f"status-{code}"
+        super().__init__(f"{self.code}: {msg}")
+
+
+def build() -> str:
+    if not os.path.exists(_SO) or any(
+        os.path.getmtime(os.path.join(_HERE, f)) > os.path.getmtime(_SO)
+        for f in ("moses_oracle.hpp", "oracle_capi.cpp")
+    ):
+        subprocess.check_call(["make", "-s", "-C", _HERE])
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build() if not os.path.exists(_SO) else None
+        _lib = C.CDLL(_SO)
+        _lib.orc_last_error.restype = C.c_char_p
+        for name in ("orc_splitmix_draw", "orc_splitmix_at", "orc_fnv_u64s", "orc_fnv_str", "orc_fnv_u64_str"):
+            getattr(_lib, name).restype = C.c_uint64
+        _lib.orc_splitmix_draw.argtypes = [C.c_uint64, C.c_int]
+        _lib.orc_splitmix_at.argtypes = [C.c_uint64, C.c_uint64]
+        _lib.orc_fnv_u64_str.argtypes = [C.c_uint64, C.c_char_p]
+        _lib.orc_uniform01_first.restype = C.c_double
+        _lib.orc_uniform01_first.argtypes = [C.c_uint64]
+        _lib.orc_gaussian_first.restype = C.c_double
+        _lib.orc_gaussian_first.argtypes = [C.c_uint64]
+        for name in ("orc_param_count", "orc_ranking_terms_f64", "orc_ranking_terms_f32", "orc_ratio_keep",
+                     "orc_serialize", "orc_write_mask_bytes"):
+            getattr(_lib, name).restype = C.c_longlong
+        _lib.orc_ratio_keep.argtypes = [C.c_double, C.c_longlong]
+        _lib.orc_init_random.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int, C.c_void_p]
+        for s in ("f64", "f32"):
+            rt = C.c_double if s == "f64" else C.c_float
+            getattr(_lib, f"orc_disc_ce_{s}").restype = rt
+            getattr(_lib, f"orc_mmd2_{s}").restype = rt
+            getattr(_lib, f"orc_mmd2_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, rt]
+            getattr(_lib, f"orc_gradients_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                           C.c_int, C.c_void_p, rt, C.c_void_p, C.c_int, rt,
+                                                           C.c_void_p, C.c_void_p, C.c_int]
+            getattr(_lib, f"orc_objective_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                           C.c_int, C.c_void_p, rt, C.c_void_p, C.c_int, rt,
+                                                           C.c_void_p]
+            getattr(_lib, f"orc_apply_update_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                                                              C.c_double, C.c_double, C.c_void_p, C.c_int]
+            getattr(_lib, f"orc_xi_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_void_p]
+            getattr(_lib, f"orc_partition_{s}").argtypes = [C.c_void_p, C.c_longlong, C.c_int, C.c_int, C.c_double,
+                                                            C.c_void_p]
+            getattr(_lib, f"orc_variant_decay_{s}").argtypes = [C.c_void_p, C.c_longlong, C.c_void_p, C.c_double,
+                                                               C.c_double]
+            getattr(_lib, f"orc_adversarial_term_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                                                  C.c_void_p, C.c_int, C.c_int, rt, C.c_void_p]
+            getattr(_lib, f"orc_topk_{s}").argtypes = [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p]
+            getattr(_lib, f"orc_segment_sum_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_longlong,
+                                                             C.c_void_p]
+            getattr(_lib, f"orc_adam_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                                                      C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double,
+                                                      C.c_int]
+        _lib.orc_synth_features.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_int, C.c_void_p]
+        _lib.orc_synth_labels.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_void_p]
+        _lib.orc_synth_offsets.argtypes = [C.c_uint64, C.c_longlong, C.c_int, C.c_void_p]
+        _lib.orc_serialize.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong]
+        _lib.orc_write_mask_bytes.argtypes = [C.c_void_p, C.c_longlong, C.c_uint, C.c_int, C.c_double, C.c_void_p,
+                                              C.c_longlong]
+        _lib.orc_train_step_f64.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().orc_last_error().decode())
+
+
+def _sfx(dtype):
+    return "f64" if np.dtype(dtype) == np.float64 else "f32"
+
+
+def _dims(dims):
+    return np.ascontiguousarray(dims, dtype=np.int32)
+
+
+# ---------------------------------------------------------------- rng
+def splitmix_draw(seed: int, k: int) -> int:
+    return lib().orc_splitmix_draw(seed, k)
+
+
+def uniform01_first(seed: int) -> float:
+    return lib().orc_uniform01_first(seed)
+
+
+def gaussian_first(seed: int) -> float:
+    return lib().orc_gaussian_first(seed)
+
+
+def fnv_u64s(vals) -> int:
+    a = np.ascontiguousarray(vals, dtype=np.uint64)
+    return lib().orc_fnv_u64s(_p(a), len(a))
+
+
+def fnv_str(s: str) -> int:
+    return lib().orc_fnv_str(s.encode())
+
+
+# ---------------------------------------------------------------- model
+def param_count(dims) -> int:
+    d = _dims(dims)
+    return lib().orc_param_count(_p(d), len(d))
+
+
+def init_random(dims, seed: int, strict: bool = True) -> np.ndarray:
+    d = _dims(dims)
+    out = np.zeros(param_count(dims), dtype=np.float64)
+    _check(lib().orc_init_random(_p(d), len(d), seed, int(strict), _p(out)))
+    return out
+
+
+def forward(dims, w, x, threads: int = 1):
+    """Returns (scores n, penultimate n x dims[-2])."""
+    d = _dims(dims)
+    w = np.ascontiguousarray(w)
+    x = np.ascontiguousarray(x, dtype=w.dtype)
+    n = x.shape[0]
+    s = np.zeros(n, dtype=w.dtype)
+    h = np.zeros((n, dims[-2]), dtype=w.dtype)
+    _check(getattr(lib(), f"orc_forward_{_sfx(w.dtype)}")(_p(d), len(d), _p(w), _p(x), n, _p(s), _p(h), threads))
+    return s, h
+
+
+def ranking_terms(scores, labels):
+    s = np.ascontiguousarray(scores)
+    y = np.ascontiguousarray(labels, dtype=s.dtype)
+    loss = np.zeros(1, dtype=s.dtype)
+    gs = np.zeros(len(s), dtype=s.dtype)
+    pairs = getattr(lib(), f"orc_ranking_terms_{_sfx(s.dtype)}")(_p(s), _p(y), len(s), _p(loss), _p(gs))
+    return float(loss[0]), gs, pairs
+
+
+def gradients(dims, w, x, y, adv=None, beta=0.0, want_loss=True, threads=1):
+    """adv = (weight, bias, replay) or None. Returns (g_flat, loss)."""
+    d = _dims(dims)
+    w = np.ascontiguousarray(w)
+    dt = w.dtype
+    x = np.ascontiguousarray(x, dtype=dt)
+    y = np.ascontiguousarray(y, dtype=dt)
+    g = np.zeros_like(w)
+    loss = np.zeros(1, dtype=dt)
+    rt = C.c_double if dt == np.float64 else C.c_float
+    if adv is not None:
+        aw = np.ascontiguousarray(adv[0], dtype=dt)
+        rep = np.ascontiguousarray(adv[2], dtype=dt)
+        args = (_p(aw), rt(adv[1]), _p(rep), rep.shape[0])
+    else:
+        args = (None, rt(0.0), None, 0)
+    _check(getattr(lib(), f"orc_gradients_{_sfx(dt)}")(_p(d), len(d), _p(w), _p(x), _p(y), x.shape[0], *args,
+                                                      rt(beta), _p(g), _p(loss) if want_loss else None, threads))
+    return g, float(loss[0])
+
+
+def objective(dims, w, x, y, adv=None, beta=0.0):
+    d = _dims(dims)
+    w = np.ascontiguousarray(w)
+    dt = w.dtype
+    x = np.ascontiguousarray(x, dtype=dt)
+    y = np.ascontiguousarray(y, dtype=dt)
+    out = np.zeros(1, dtype=dt)
+    rt = C.c_double if dt == np.float64 else C.c_float
+    if adv is not None:
+        aw = np.ascontiguousarray(adv[0], dtype=dt)
+        rep = np.ascontiguousarray(adv[2], dtype=dt)
+        args = (_p(aw), rt(adv[1]), _p(rep), rep.shape[0])
+    else:
+        args = (None, rt(0.0), None, 0)
+    _check(getattr(lib(), f"orc_objective_{_sfx(dt)}")(_p(d), len(d), _p(w), _p(x), _p(y), x.shape[0], *args,
+                                                      rt(beta), _p(out)))
+    return float(out[0])
+
+
+def apply_update(w, mom, g, lr, mu=0.9, mask=None, use_momentum=False):
+    """In place on copies; returns (w, mom)."""
+    w = np.array(w, copy=True)
+    mom = np.array(mom, copy=True, dtype=w.dtype)
+    g = np.ascontiguousarray(g, dtype=w.dtype)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+    getattr(lib(), f"orc_apply_update_{_sfx(w.dtype)}")(_p(w), _p(mom), _p(g), len(w), lr, mu, _p(m),
+                                                        int(use_momentum))
+    return w, mom
+
+
+def xi_scores(w, g, normalize):
+    w = np.ascontiguousarray(w)
+    g = np.ascontiguousarray(g, dtype=w.dtype)
+    out = np.zeros_like(w)
+    getattr(lib(), f"orc_xi_{_sfx(w.dtype)}")(_p(w), _p(g), len(w), int(normalize), _p(out))
+    return out
+
+
+def partition(xi, normalized, mode, value):
+    xi = np.ascontiguousarray(xi)
+    out = np.zeros(len(xi), dtype=np.uint8)
+    _check(getattr(lib(), f"orc_partition_{_sfx(xi.dtype)}")(_p(xi), len(xi), int(normalized), mode, value, _p(out)))
+    return out.astype(bool)
+
+
+def ratio_keep(value, n):
+    return lib().orc_ratio_keep(value, n)
+
+
+def variant_decay(w, mask, alpha, lam):
+    w = np.array(w, copy=True)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    _check(getattr(lib(), f"orc_variant_decay_{_sfx(w.dtype)}")(_p(w), len(w), _p(m), alpha, lam))
+    return w
+
+
+def accuracy_counts(scores, labels):
+    s = np.ascontiguousarray(scores)
+    y = np.ascontiguousarray(labels, dtype=s.dtype)
+    pairs = C.c_longlong(0)
+    conc = C.c_longlong(0)
+    getattr(lib(), f"orc_accuracy_counts_{_sfx(s.dtype)}")(_p(s), _p(y), len(s), C.byref(pairs), C.byref(conc))
+    return pairs.value, conc.value
+
+
+def disc_ce(zs, zt):
+    zs = np.ascontiguousarray(zs)
+    zt = np.ascontiguousarray(zt, dtype=zs.dtype)
+    return getattr(lib(), f"orc_disc_ce_{_sfx(zs.dtype)}")(_p(zs), len(zs), _p(zt), len(zt))
+
+
+def adversarial_term(weight, bias, hs, ht, step=0.1):
+    """Returns (new_weight, new_bias, discriminator_loss)."""
+    aw = np.array(weight, copy=True)
+    dt = aw.dtype
+    rt = C.c_double if dt == np.float64 else C.c_float
+    ab = np.array([bias], dtype=dt)
+    hs = np.ascontiguousarray(hs, dtype=dt)
+    ht = np.ascontiguousarray(ht, dtype=dt)
+    loss = np.zeros(1, dtype=dt)
+    _check(getattr(lib(), f"orc_adversarial_term_{_sfx(dt)}")(_p(aw), _p(ab), _p(hs), hs.shape[0], _p(ht),
+                                                              ht.shape[0], len(aw), rt(step), _p(loss)))
+    return aw, float(ab[0]), float(loss[0])
+
+
+def topk(scores, k):
+    s = np.ascontiguousarray(scores)
+    k = min(k, len(s))
+    out = np.zeros(k, dtype=np.int64)
+    getattr(lib(), f"orc_topk_{_sfx(s.dtype)}")(_p(s), len(s), k, _p(out))
+    return out
+
+
+def segment_sum(h, offsets):
+    h = np.ascontiguousarray(h)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = np.zeros((len(off) - 1, h.shape[1]), dtype=h.dtype)
+    getattr(lib(), f"orc_segment_sum_{_sfx(h.dtype)}")(_p(h), h.shape[1], _p(off), len(off) - 1, _p(out))
+    return out
+
+
+def mmd2(xs, xt, sigma):
+    xs = np.ascontiguousarray(xs)
+    xt = np.ascontiguousarray(xt, dtype=xs.dtype)
+    return getattr(lib(), f"orc_mmd2_{_sfx(xs.dtype)}")(_p(xs), xs.shape[0], _p(xt), xt.shape[0], xs.shape[1],
+                                                       sigma)
+
+
+def adam(w, m1, m2, g, lr, b1, b2, eps, t, mask=None):
+    w, m1, m2 = (np.array(a, copy=True) for a in (w, m1, m2))
+    g = np.ascontiguousarray(g, dtype=w.dtype)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+    getattr(lib(), f"orc_adam_{_sfx(w.dtype)}")(_p(w), _p(m1), _p(m2), _p(g), len(w), _p(m), lr, b1, b2, eps, t)
+    return w, m1, m2
+
+
+def synth_features(seed, row0, rows, D):
+    out = np.zeros((rows, D), dtype=np.float64)
+    lib().orc_synth_features(seed, row0, rows, D, _p(out))
+    return out
+
+
+def synth_labels(seed, row0, rows):
+    out = np.zeros(rows, dtype=np.float64)
+    lib().orc_synth_labels(seed, row0, rows, _p(out))
+    return out
+
+
+def synth_offsets(seed, programs, max_stmts=8):
+    out = np.zeros(programs + 1, dtype=np.int64)
+    lib().orc_synth_offsets(seed, programs, max_stmts, _p(out))
+    return out
+
+
+def serialize(dims, w, mom=None):
+    d = _dims(dims)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    mom = np.zeros_like(w) if mom is None else np.ascontiguousarray(mom, dtype=np.float64)
+    n = lib().orc_serialize(_p(d), len(d), _p(w), _p(mom), None, 0)
+    if n < 0:
+        raise OracleError(-n, lib().orc_last_error().decode())
+    buf = C.create_string_buffer(n)
+    lib().orc_serialize(_p(d), len(d), _p(w), _p(mom), buf, n)
+    return buf.raw
+
+
+def write_mask_bytes(mask, phase, mode, value):
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    n = lib().orc_write_mask_bytes(_p(m), len(m), phase, mode, value, None, 0)
+    buf = C.create_string_buffer(n)
+    lib().orc_write_mask_bytes(_p(m), len(m), phase, mode, value, buf, n)
+    return buf.raw
+
+
+def train_step_f64(dims, w, mom, x, y, lr=0.001, mu=0.9, threads=1):
+    """In place on w, mom (float64 arrays). Returns the batch loss."""
+    d = _dims(dims)
+    loss = np.zeros(1)
+    _check(lib().orc_train_step_f64(_p(d), len(d), _p(w), _p(mom), _p(np.ascontiguousarray(x)),
+                                    _p(np.ascontiguousarray(y)), x.shape[0], lr, mu, _p(loss), threads))
+    return float(loss[0])
