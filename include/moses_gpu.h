@@ -1,0 +1,212 @@
+/* moses_gpu.h — C ABI of the B200-native Moses cost-model hot path.
+ *
+ * This is the drop-in boundary under the reference's C++ API (namespace
+ * moseslab, /root/reference/proj/include/moseslab/{model,lottery,search}.hpp).
+ * Every entry point cites the reference function it replaces. Plain pointers
+ * and sizes only; no torch or Eigen types. Host buffers are float64 like the
+ * reference's Eigen::MatrixXd / VectorXd; "_device" variants take device
+ * pointers for bulk work.
+ *
+ * Layout conventions (identical to the reference):
+ *   - flat parameter order (lottery.hpp:13-14): per level, the weight array in
+ *     Eigen column-major storage order (element (o,i) of the out x in matrix
+ *     at off + i*out + o), then the bias; momentum in the same order.
+ *   - feature matrices are row-major n x D (the reference's Eigen matrices are
+ *     column-major; the C++ wrapper transposes).
+ *
+ * Status: 0 = MOSES_OK; 1..25 = 1 + moseslab::ErrorCode ordinal
+ * (errors.hpp:10-36) with the same validation order as the reference;
+ * >= 100 = library errors. moses_last_error() gives the thread's message.
+ *
+ * Threading: every handle owns one CUDA stream and its workspaces; handles
+ * are independent, so callers may use distinct handles from distinct host
+ * threads (the reference's compare pool, tuner.cpp:331-374). A single handle
+ * must not be used concurrently (update ops need exclusive access, SPEC.md).
+ */
+#ifndef MOSES_GPU_H_
+#define MOSES_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOSES_API __attribute__((visibility("default")))
+
+enum {
+  MOSES_OK = 0,
+  MOSES_ERR_INVALID_CONFIG = 2,        /* ErrorCode::InvalidConfig */
+  MOSES_ERR_BAD_DIMS = 5,              /* ErrorCode::BadDims */
+  MOSES_ERR_DIM_MISMATCH = 6,          /* ErrorCode::DimMismatch */
+  MOSES_ERR_SHAPE_MISMATCH = 7,        /* ErrorCode::ShapeMismatch */
+  MOSES_ERR_VERSION_MISMATCH = 8,      /* ErrorCode::VersionMismatch */
+  MOSES_ERR_CORRUPT_STREAM = 9,        /* ErrorCode::CorruptStream */
+  MOSES_ERR_INVALID_RATIO = 11,        /* ErrorCode::InvalidRatio */
+  MOSES_ERR_UNNORMALIZED_THRESHOLD = 12, /* ErrorCode::UnnormalizedThreshold */
+  MOSES_ERR_ADVERSARY_DISABLED = 13,   /* ErrorCode::AdversaryDisabled */
+  MOSES_ERR_UNSTABLE_DECAY = 14,       /* ErrorCode::UnstableDecay */
+  MOSES_ERR_IO = 24,                   /* ErrorCode::IoError */
+  MOSES_ERR_CUDA = 100,
+  MOSES_ERR_NO_DEVICE = 101,
+  MOSES_ERR_CAPACITY = 102,
+  MOSES_ERR_INVALID_ARG = 103
+};
+
+enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1 };            /* GEMM operand precision */
+enum { MOSES_MODE_THRESHOLD = 1, MOSES_MODE_RATIO = 2 };        /* PartitionMode, "MOSK" mode byte */
+enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1 };
+
+typedef struct moses_model* moses_model_t;
+typedef struct moses_adversary* moses_adversary_t;
+
+MOSES_API const char* moses_last_error(void);
+MOSES_API const char* moses_version(void);
+/* Number of kernels this library launched in the calling process (evidence counter). */
+MOSES_API int64_t moses_kernel_launches(void);
+MOSES_API int moses_device_check(void);
+
+/* ------------------------------------------------------------------ model (model.hpp:19-25, 51-100) */
+/* param_count (model.cpp:141-145). Returns -status on bad dims. */
+MOSES_API int64_t moses_param_count(const int32_t* dims, int32_t ndims);
+/* init_random (model.cpp:147-167): Glorot-uniform from keyed SplitMix64, bit-exact with the reference.
+ * strict = 1 enforces the reference's 4-level rule; 0 allows {D, h1..hL, 1}. Host-side. */
+MOSES_API int moses_init_random(const int32_t* dims, int32_t ndims, uint64_t seed, int32_t strict, double* flat_out);
+/* Device handle for a model of the given dims. max_rows bounds rows per call (batch + replay). */
+MOSES_API int moses_model_create(const int32_t* dims, int32_t ndims, int32_t precision, int64_t max_rows,
+                                 moses_model_t* out);
+MOSES_API int moses_model_destroy(moses_model_t m);
+MOSES_API int moses_model_upload(moses_model_t m, const double* params, const double* momentum, int64_t count);
+MOSES_API int moses_model_download(moses_model_t m, double* params, double* momentum, int64_t count);
+/* Value-semantics copy (tuner.cpp:349 copies the model per job). dst must have identical dims. */
+MOSES_API int moses_model_copy(moses_model_t dst, moses_model_t src);
+MOSES_API int moses_model_synchronize(moses_model_t m);
+
+/* predict (model.cpp:169-175): scores for n x D row-major features. */
+MOSES_API int moses_predict(moses_model_t m, const double* features, int64_t n, int32_t D, double* scores);
+/* penultimate_activations (model.cpp:177-183): n x dims[L-1] row-major out. */
+MOSES_API int moses_penultimate(moses_model_t m, const double* features, int64_t n, int32_t D, double* hidden);
+/* Bulk scoring on device buffers (candidate pool, cfg4): x_dev is n rows of `ldx` elements of `dtype`
+ * already in the packed layout (column D == 1, columns > D zero; see moses_packed_ld). Any n (chunked). */
+MOSES_API int moses_predict_device(moses_model_t m, const void* x_dev, int32_t dtype, int64_t ldx, int64_t n,
+                                   float* scores_dev);
+/* Row stride (elements) of the packed layout for input width D under the handle's precision. */
+MOSES_API int64_t moses_packed_ld(moses_model_t m);
+/* Per-program scores with segment-sum pooling over statement rows (north-star extension; with all
+ * segment lengths 1 this is predict). offsets: programs+1 CSR offsets into the n statement rows. */
+MOSES_API int moses_predict_pooled(moses_model_t m, const double* stmt_features, int64_t n, int32_t D,
+                                   const int64_t* offsets, int64_t programs, double* scores);
+
+/* gradients (model.cpp:192-244). Result stays on the device (read with moses_gradients_download).
+ * adv may be NULL; beta == 0 or NULL adversary skips the confusion term bit-exactly. */
+MOSES_API int moses_gradients(moses_model_t m, const double* features, const double* labels, int64_t n, int32_t D,
+                              moses_adversary_t adv, double beta, double* loss_out);
+MOSES_API int moses_gradients_download(moses_model_t m, double* grads, int64_t count);
+MOSES_API int moses_gradients_upload(moses_model_t m, const double* grads, int64_t count);
+/* objective (model.cpp:246-261) */
+MOSES_API int moses_objective(moses_model_t m, const double* features, const double* labels, int64_t n, int32_t D,
+                              moses_adversary_t adv, double beta, double* out);
+/* apply_update (model.cpp:263-296) with the device gradients. mask: NULL or count host bytes. */
+MOSES_API int moses_apply_update(moses_model_t m, double learning_rate, double momentum, const uint8_t* mask,
+                                 int64_t mask_len, int32_t use_momentum);
+/* One offline pretraining step (tuner.cpp:146-147): gradients + momentum update. */
+MOSES_API int moses_train_step(moses_model_t m, const double* features, const double* labels, int64_t n, int32_t D,
+                               double learning_rate, double momentum, double* loss_out);
+/* Same on device-resident rows (packed layout, labels fp32); loss stays on device unless loss_out != NULL. */
+MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                      double learning_rate, double momentum, double* loss_out);
+/* ranking_accuracy (model.cpp:298-312): nb batches, rows [off[b], off[b+1]) of features/labels. */
+MOSES_API int moses_ranking_accuracy(moses_model_t m, const double* features, const double* labels,
+                                     const int64_t* batch_offsets, int32_t nbatches, int32_t D, double* accuracy,
+                                     int64_t* pairs, int64_t* concordant);
+/* pairwise_ranking_loss (model.cpp:185-190), standalone on host buffers. */
+MOSES_API int moses_ranking_loss(const double* scores, const double* labels, int64_t n, double* loss,
+                                 int64_t* pairs);
+/* Masked Adam on the device gradients (north-star extension; parity pinned by the oracle only). */
+MOSES_API int moses_adam_update(moses_model_t m, double lr, double beta1, double beta2, double eps, int32_t step,
+                                const uint8_t* mask, int64_t mask_len);
+
+/* ------------------------------------------------------------------ lottery (lottery.hpp:44-83) */
+/* xi_scores (lottery.cpp:35-57) from the handle's params and device gradients; xi_out may be NULL. */
+MOSES_API int moses_xi_scores(moses_model_t m, int32_t normalize, double* xi_out, int64_t count);
+/* partition (lottery.cpp:59-90) over the xi computed by the last moses_xi_scores (or uploaded with
+ * moses_xi_upload). The mask is kept on the device; mask_out (count bytes) may be NULL. */
+MOSES_API int moses_partition(moses_model_t m, int32_t mode, double value, int32_t phase, uint8_t* mask_out,
+                              int64_t count, int64_t* popcount);
+MOSES_API int moses_xi_upload(moses_model_t m, const double* xi, int64_t count, int32_t normalized);
+MOSES_API int moses_mask_upload(moses_model_t m, const uint8_t* mask, int64_t count);
+/* transferable_step (lottery.cpp:92-97) with the device mask and gradients. */
+MOSES_API int moses_transferable_step(moses_model_t m, double alpha);
+/* variant_decay (lottery.cpp:99-120) with the device mask. */
+MOSES_API int moses_variant_decay(moses_model_t m, double alpha, double lambda);
+/* The Moses adaptation step fused (tuner.cpp:258-262): xi -> partition -> step -> decay in one
+ * device pass sequence; threshold mode normalises xi like the tuner does. */
+MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, int32_t phase, double alpha,
+                                 double lambda, uint8_t* mask_out, int64_t count, int64_t* popcount);
+
+/* ------------------------------------------------------------------ adversary (lottery.hpp:36-42, 64-79) */
+/* make_adversary (lottery.cpp:166-180): zero discriminator over m x D replay rows. */
+MOSES_API int moses_adversary_create(const double* replay, int64_t m, int32_t D, int32_t width, double step_size,
+                                     moses_adversary_t* out);
+MOSES_API int moses_adversary_destroy(moses_adversary_t a);
+MOSES_API int moses_adversary_get(moses_adversary_t a, double* weight, int32_t width, double* bias);
+MOSES_API int moses_adversary_set(moses_adversary_t a, const double* weight, int32_t width, double bias);
+/* adversarial_term (lottery.cpp:135-164) on explicit hidden activations (reference signature). */
+MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hidden_source, int64_t ms,
+                                     const double* hidden_target, int64_t nt, int32_t width, double beta,
+                                     double* discriminator_loss, double* confusion);
+/* tuner.cpp:252-256 fused: penultimate activations of the replay rows and the target rows under the
+ * model's current params, then the discriminator step. */
+MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const double* target_features,
+                                     int64_t n, int32_t D, double beta, double* discriminator_loss,
+                                     double* confusion);
+/* discriminator_cross_entropy (lottery.cpp:207-218) */
+MOSES_API int moses_discriminator_cross_entropy(const double* zs, int64_t m, const double* zt, int64_t n,
+                                                double* out);
+
+/* ------------------------------------------------------------------ candidate selection (search.cpp:32-37, 82-95) */
+/* Indices of the k best scores ordered (score desc, index asc) — sort_desc's order when the
+ * pool index is the lexicographic config order. k <= 4096. */
+MOSES_API int moses_topk(const double* scores, int64_t n, int64_t k, int64_t* idx_out);
+MOSES_API int moses_topk_device(const float* scores_dev, int64_t n, int64_t k, int64_t* idx_out_host);
+/* select_batch (search.cpp:82-95) over a score-ordered candidate list: first k whose hash is
+ * neither in `measured` nor already taken. Host-side. Returns the count written. */
+MOSES_API int64_t moses_select_batch(const uint64_t* ordered_hashes, int64_t n, const uint64_t* measured,
+                                     int64_t n_measured, int64_t batch_size, int64_t* out_positions);
+
+/* ------------------------------------------------------------------ extensions */
+/* Segment-sum pooling over CSR offsets on host buffers: out[p] = sum rows [off[p], off[p+1]). */
+MOSES_API int moses_segment_sum(const double* h, int64_t rows, int32_t width, const int64_t* offsets,
+                                int64_t programs, double* out);
+/* Device variant (bf16 or f32 rows with row stride ld) -> fp32 out [programs][width]. */
+MOSES_API int moses_segment_sum_device(const void* h_dev, int32_t dtype, int64_t ld, int32_t width,
+                                       const int64_t* offsets_dev, int64_t programs, float* out_dev);
+/* Biased MMD^2 with a Gaussian kernel between source and target representations. */
+MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t n, int32_t width, double sigma,
+                         double* out);
+
+/* ------------------------------------------------------------------ synthetic TenSet-shaped data (bench) */
+/* Rows [row0, row0+n) of the keyed SplitMix64 generator, written in the packed layout. */
+MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype,
+                                          void* dst, int64_t ld);
+MOSES_API int moses_synth_labels_device(uint64_t seed, int64_t row0, int64_t n, float* dst);
+
+/* ------------------------------------------------------------------ files (model.cpp:344-412, lottery.cpp:267-325) */
+MOSES_API int64_t moses_serialize(const int32_t* dims, int32_t ndims, const double* params, const double* momentum,
+                                  uint8_t* out, int64_t cap);
+MOSES_API int moses_deserialize(const uint8_t* bytes, int64_t len, int32_t* dims_out, double* params,
+                                double* momentum, int64_t cap);
+MOSES_API int64_t moses_write_mask(const uint8_t* mask, int64_t n, int32_t phase, int32_t mode, double value,
+                                   uint8_t* out, int64_t cap);
+MOSES_API int moses_read_mask(const uint8_t* bytes, int64_t len, uint8_t* mask_out, int64_t cap, int64_t* n,
+                              int32_t* phase, int32_t* mode, double* value);
+
+/* ------------------------------------------------------------------ timing helpers (bench) */
+/* Raw pointers into the handle (device): params fp32, gradients fp32, momentum fp32. */
+MOSES_API int moses_model_device_ptrs(moses_model_t m, float** params, float** grads, float** momentum);
+MOSES_API int moses_model_stream(moses_model_t m, void** stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOSES_GPU_H_ */

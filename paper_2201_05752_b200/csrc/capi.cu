@@ -1,0 +1,1331 @@
+// capi.cu — the C ABI (include/moses_gpu.h): device model / adversary handles
+// and the reference-facing operations, each composed from the sm_100a kernels.
+//
+// Device data layout:
+//   params / grads / momentum / xi : fp32, the reference flat order (lottery.hpp:13-14)
+//   weight operand                 : bf16 shadow of params (BF16 mode) or params itself (TF32 mode);
+//                                    level l's block [in][out] is the GEMM B operand, MN-major for the
+//                                    forward pass and K-major for the data-gradient pass.
+//   activations act[l]             : rows x ld[l], column dims[l] == 1.0 (bias row of the wgrad GEMM),
+//                                    row block [0, m) = adversary replay rows, [m, m+n) = batch rows.
+//   dZ[l]                          : rows x lddz[l]
+#include <algorithm>
+#include <atomic>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace moses {
+
+std::atomic<long long> g_launches{0};
+void note_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MOSES_OK;
+  } catch (const Status& s) {
+    g_err = s.what();
+    return s.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MOSES_ERR_INVALID_ARG;
+  }
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  MOSES_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// ---- reference-side validation helpers (model.cpp:20-37)
+void check_dims(const int32_t* dims, int nd, bool strict) {
+  if (dims == nullptr || (strict ? nd != 4 : nd < 3))
+    fail(MOSES_ERR_BAD_DIMS, "expected 4 levels, got " + std::to_string(nd));
+  for (int i = 0; i < nd; ++i)
+    if (dims[i] <= 0) fail(MOSES_ERR_BAD_DIMS, "non-positive level width");
+  if (dims[nd - 1] != 1) fail(MOSES_ERR_BAD_DIMS, "output width must be 1");
+}
+long long level_off(const std::vector<int>& d, int l) {
+  long long o = 0;
+  for (int k = 0; k < l; ++k) o += (long long)d[k] * d[k + 1] + d[k + 1];
+  return o;
+}
+
+// ---- keyed SplitMix64 (rng.hpp:16-80) for host-side init
+struct KeyBuilder {
+  uint64_t h = 0xcbf29ce484222325ull;
+  void step(unsigned char b) { h ^= b; h *= 0x100000001b3ull; }
+  KeyBuilder& add(uint64_t v) {
+    for (int i = 0; i < 8; ++i) step((unsigned char)(v >> (8 * i)));
+    return *this;
+  }
+  KeyBuilder& add(const char* s) {
+    for (; *s; ++s) step((unsigned char)*s);
+    step(0);
+    return *this;
+  }
+};
+struct Rng {
+  uint64_t s;
+  uint64_t next() {
+    s += 0x9e3779b97f4a7c15ull;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  double u01() { return double(next() >> 11) * 0x1.0p-53; }
+};
+
+// Scratch context for the handle-less entry points (ranking loss, top-k, pooling, MMD, ...).
+struct Scratch {
+  std::mutex mu;
+  cudaStream_t st = nullptr;
+  void* buf = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (!st) MOSES_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (bytes > cap) {
+      dfree(buf);
+      buf = nullptr;
+      cap = 0;
+      MOSES_CUDA(cudaMalloc(&buf, bytes));
+      cap = bytes;
+    }
+    return buf;
+  }
+};
+Scratch& scratch() {
+  static Scratch s;
+  return s;
+}
+
+struct Carver {
+  uint8_t* p;
+  template <typename T>
+  T* take(size_t count) {
+    T* r = reinterpret_cast<T*>(p);
+    p += round_up(count * sizeof(T) + 1, 256);
+    return r;
+  }
+};
+
+}  // namespace
+}  // namespace moses
+
+using namespace moses;
+
+struct moses_adversary {
+  int D = 0, W = 0;
+  long long m = 0;
+  float* replay = nullptr;  // m x D fp32 (device)
+  float* u = nullptr;       // [W] + c at u[W]... kept separate:
+  float* c = nullptr;       // [1]
+  float eta = 0.1f;
+  ~moses_adversary() {
+    dfree(replay);
+    dfree(u);
+    dfree(c);
+  }
+};
+
+struct moses_model {
+  std::vector<int> dims;
+  int L = 0;  // levels
+  long long P = 0;
+  std::vector<long long> off;
+  int prec = MOSES_PREC_BF16;
+  int esz = 2;
+  long long cap = 0;
+  cudaStream_t st = nullptr;
+  // parameters
+  float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
+  float *m1 = nullptr, *m2 = nullptr;
+  uint8_t* mask = nullptr;
+  __nv_bfloat16* wbf = nullptr;
+  bool xi_valid = false, xi_norm = false, mask_valid = false;
+  // activations
+  std::vector<void*> act, dz;
+  std::vector<long long> ld, lddz;
+  int max_tiles = 0;
+  float *head_part = nullptr, *head_part2 = nullptr;
+  float *scores = nullptr, *labels = nullptr, *coefA = nullptr, *coefB = nullptr;
+  RankWs rank{};
+  double* dscal = nullptr;  // [0] loss, [1] ce, [2..] scratch
+  long long* dpairs = nullptr;
+  unsigned long long* dcount = nullptr;
+  void* sel_base = nullptr;
+  SelectWs sel{};
+  double* staging = nullptr;  // host-double staging [cap * stage_w]
+  long long stage_w = 0;
+  float* adv_ws = nullptr;
+  int last_tiles = 0;  // N tiles of the last hidden GEMM of the most recent forward
+
+  const void* wop(int l) const {
+    return esz == 2 ? static_cast<const void*>(wbf + off[l]) : static_cast<const void*>(w + off[l]);
+  }
+  __nv_bfloat16* shadow() const { return esz == 2 ? wbf : nullptr; }
+  int width(int l) const { return dims[l]; }
+  int W() const { return dims[L - 1]; }
+  const float* head_w() const { return w + off[L - 1]; }
+  const float* head_b() const { return w + off[L - 1] + dims[L - 1]; }
+  const float* bias(int l) const { return w + off[l] + (long long)dims[l] * dims[l + 1]; }
+
+  ~moses_model() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : {(void*)w, (void*)mom, (void*)g, (void*)xi, (void*)m1, (void*)m2, (void*)mask, (void*)wbf,
+                    (void*)head_part, (void*)head_part2, (void*)scores, (void*)labels, (void*)coefA, (void*)coefB,
+                    (void*)rank.gs_part, (void*)rank.loss_part, (void*)rank.pairs_part, (void*)dscal, (void*)dpairs,
+                    (void*)dcount, sel_base, (void*)staging, (void*)adv_ws})
+      dfree(p);
+    for (void* p : act) dfree(p);
+    for (void* p : dz) dfree(p);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace moses {
+namespace {
+
+// ---------------------------------------------------------------- forward / backward composition
+template <typename T>
+void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
+  for (int l = 0; l + 1 < m->L; ++l) {
+    GemmCall c{};
+    c.M = int(R);
+    c.N = m->dims[l + 1];
+    c.K = m->dims[l];
+    c.A = {l == 0 ? x0 : m->act[l], l == 0 ? ldx0 : m->ld[l], false};
+    c.B = {m->wop(l), m->dims[l + 1], true};
+    c.epi = EpiKind::Fwd;
+    const bool last = l + 2 == m->L;
+    c.out = (last && !keep_last) ? nullptr : m->act[l + 1];
+    c.ldo = m->ld[l + 1];
+    c.bias = m->bias(l);
+    c.relu = 1;
+    if (last) {
+      c.head_w = m->head_w();
+      c.head_u = head_u;
+      c.head_part = m->head_part;
+      c.head_part2 = head_u ? m->head_part2 : nullptr;
+      c.head_ld = m->cap;
+    }
+    const int bn = launch_gemm(m->esz, c, m->st);
+    note_launch(1);
+    if (last) m->last_tiles = ceil_div(c.N, bn);
+  }
+}
+
+template <typename T>
+void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u) {
+  const int L = m->L, W = m->W();
+  T* hl = static_cast<T*>(m->act[L - 1]);
+  column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->st);
+  head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
+                   m->lddz[L - 1], m->st);
+  note_launch(2);
+  for (int l = L - 2; l >= 0; --l) {
+    const void* a = l == 0 ? x0 : m->act[l];
+    const long long lda = l == 0 ? ldx0 : m->ld[l];
+    GemmCall wg{};
+    wg.M = m->dims[l] + 1;  // + the ones column -> bias gradient row (flat layout: W block then b)
+    wg.N = m->dims[l + 1];
+    wg.K = int(R);
+    wg.A = {a, lda, true};
+    wg.B = {m->dz[l + 1], m->lddz[l + 1], true};
+    wg.epi = EpiKind::StoreF32;
+    wg.out = m->g + m->off[l];
+    wg.ldo = m->dims[l + 1];
+    launch_gemm(m->esz, wg, m->st);
+    note_launch(1);
+    if (l > 0) {
+      GemmCall dg{};
+      dg.M = int(R);
+      dg.N = m->dims[l];
+      dg.K = m->dims[l + 1];
+      dg.A = {m->dz[l + 1], m->lddz[l + 1], false};
+      dg.B = {m->wop(l), m->dims[l + 1], false};
+      dg.epi = EpiKind::Dgrad;
+      dg.out = m->dz[l];
+      dg.ldo = m->lddz[l];
+      dg.mask = m->act[l];
+      dg.ldm = m->ld[l];
+      launch_gemm(m->esz, dg, m->st);
+      note_launch(1);
+    }
+  }
+}
+
+void require_model(moses_model* m) {
+  if (!m) fail(MOSES_ERR_INVALID_ARG, "null model handle");
+}
+
+// Pack host double rows into act[0] rows [row0, row0+n).
+void upload_rows(moses_model* m, const double* x, long long n, long long row0) {
+  if (n <= 0) return;
+  const int D = m->dims[0];
+  for (long long r = 0; r < n;) {
+    const long long c = std::min(n - r, m->cap * m->stage_w / std::max(D, 1));
+    MOSES_CUDA(cudaMemcpyAsync(m->staging, x + r * D, sizeof(double) * c * D, cudaMemcpyHostToDevice, m->st));
+    if (m->esz == 2)
+      pack_rows<__nv_bfloat16>(m->staging, c, D, static_cast<__nv_bfloat16*>(m->act[0]) + (row0 + r) * m->ld[0],
+                               m->ld[0], m->st);
+    else
+      pack_rows<float>(m->staging, c, D, static_cast<float*>(m->act[0]) + (row0 + r) * m->ld[0], m->ld[0], m->st);
+    note_launch(1);
+    r += c;
+  }
+}
+void upload_replay(moses_model* m, const moses_adversary* a) {
+  if (m->esz == 2)
+    pack_rows_f32<__nv_bfloat16>(a->replay, a->m, a->D, a->D, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0], m->st);
+  else
+    pack_rows_f32<float>(a->replay, a->m, a->D, a->D, static_cast<float*>(m->act[0]), m->ld[0], m->st);
+  note_launch(1);
+}
+void upload_f32(moses_model* m, const double* src, long long n, float* dst) {
+  if (n <= 0) return;
+  for (long long r = 0; r < n;) {
+    const long long c = std::min(n - r, m->cap * m->stage_w);
+    MOSES_CUDA(cudaMemcpyAsync(m->staging, src + r, sizeof(double) * c, cudaMemcpyHostToDevice, m->st));
+    f64_to_f32(m->staging, c, dst + r, m->st);
+    note_launch(1);
+    r += c;
+  }
+}
+void download_f32(moses_model* m, const float* src, long long n, double* dst) {
+  if (n <= 0) return;
+  for (long long r = 0; r < n;) {
+    const long long c = std::min(n - r, m->cap * m->stage_w);
+    f32_to_f64(src + r, c, m->staging, m->st);
+    note_launch(1);
+    MOSES_CUDA(cudaMemcpyAsync(dst + r, m->staging, sizeof(double) * c, cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    r += c;
+  }
+}
+
+void dispatch_forward(moses_model* m, const void* x0, long long ldx0, long long R, const float* u, bool keep_last) {
+  if (m->esz == 2) forward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, keep_last);
+  else forward_rows<float>(m, x0, ldx0, R, u, keep_last);
+}
+
+// gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch.
+void gradients_core(moses_model* m, const void* x0, long long ldx0, const float* y, long long n, moses_adversary* adv,
+                    double beta) {
+  const bool active = adv != nullptr && beta != 0.0 && n > 0;
+  const long long mrep = active ? adv->m : 0;
+  const long long R = mrep + n;
+  if (n == 0) {
+    MOSES_CUDA(cudaMemsetAsync(m->g, 0, sizeof(float) * m->P, m->st));
+    MOSES_CUDA(cudaMemsetAsync(m->dscal, 0, sizeof(double) * 2, m->st));
+    m->xi_valid = false;
+    return;
+  }
+  const float* u = active ? adv->u : nullptr;
+  dispatch_forward(m, x0, ldx0, R, u, true);
+  head_scores(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), n, m->scores, m->st);
+  rank_pairs(m->scores, y, n, {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->st);
+  FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
+  rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
+                active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
+  note_launch(3);
+  if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u);
+  else backward_rows<float>(m, x0, ldx0, R, u);
+  m->xi_valid = false;
+}
+
+void check_rows(moses_model* m, long long R) {
+  if (R > m->cap)
+    fail(MOSES_ERR_CAPACITY, "rows " + std::to_string(R) + " exceed the handle capacity " + std::to_string(m->cap));
+}
+
+}  // namespace
+}  // namespace moses
+
+// ====================================================================== C ABI
+extern "C" {
+
+MOSES_API const char* moses_last_error(void) { return g_err.c_str(); }
+MOSES_API const char* moses_version(void) { return "moses-b200 0.1 (sm_100a, tcgen05/TMA)"; }
+MOSES_API int64_t moses_kernel_launches(void) { return g_launches.load(); }
+
+MOSES_API int moses_device_check(void) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(MOSES_ERR_NO_DEVICE, "no CUDA device");
+    cudaDeviceProp p;
+    MOSES_CUDA(cudaGetDeviceProperties(&p, 0));
+    if (p.major != 10) fail(MOSES_ERR_NO_DEVICE, std::string("need sm_100 (B200), found ") + p.name);
+  });
+}
+
+MOSES_API int64_t moses_param_count(const int32_t* dims, int32_t nd) {
+  int64_t out = 0;
+  const int rc = guarded([&] {
+    check_dims(dims, nd, false);
+    std::vector<int> d(dims, dims + nd);
+    out = level_off(d, nd - 1);
+  });
+  return rc ? -rc : out;
+}
+
+MOSES_API int moses_init_random(const int32_t* dims, int32_t nd, uint64_t seed, int32_t strict, double* flat) {
+  return guarded([&] {
+    check_dims(dims, nd, strict != 0);
+    std::vector<int> d(dims, dims + nd);
+    const long long P = level_off(d, nd - 1);
+    std::fill(flat, flat + P, 0.0);
+    for (int l = 0; l + 1 < nd; ++l) {
+      const int fi = d[l], fo = d[l + 1];
+      const double bound = std::sqrt(6.0 / double(fi + fo));
+      KeyBuilder k;
+      k.add(seed).add("init").add(uint64_t(l));
+      Rng r{k.h};
+      double* w = flat + level_off(d, l);
+      for (long long i = 0; i < (long long)fi * fo; ++i) w[i] = (2.0 * r.u01() - 1.0) * bound;
+    }
+  });
+}
+
+MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precision, int64_t max_rows,
+                                 moses_model_t* out) {
+  return guarded([&] {
+    *out = nullptr;
+    check_dims(dims, nd, false);
+    if (precision != MOSES_PREC_BF16 && precision != MOSES_PREC_TF32) fail(MOSES_ERR_INVALID_ARG, "precision");
+    for (int l = 1; l + 1 < nd; ++l)
+      if (dims[l] % 8) fail(MOSES_ERR_INVALID_ARG, "hidden widths must be multiples of 8 (TMA 16-byte rows)");
+    if (max_rows < 1) max_rows = 1;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(MOSES_ERR_NO_DEVICE, "no CUDA device visible");
+    auto m = std::make_unique<moses_model>();
+    m->dims.assign(dims, dims + nd);
+    m->L = nd - 1;
+    m->P = level_off(m->dims, m->L);
+    for (int l = 0; l <= m->L; ++l) m->off.push_back(level_off(m->dims, l));
+    m->prec = precision;
+    m->esz = precision == MOSES_PREC_BF16 ? 2 : 4;
+    m->cap = round_up(max_rows, 128);
+    MOSES_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+    const long long P = m->P;
+    m->w = dalloc<float>(P);
+    m->mom = dalloc<float>(P);
+    m->g = dalloc<float>(P);
+    m->xi = dalloc<float>(P);
+    m->mask = dalloc<uint8_t>(P);
+    if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(P);
+    MOSES_CUDA(cudaMemset(m->w, 0, P * 4));
+    MOSES_CUDA(cudaMemset(m->mom, 0, P * 4));
+    MOSES_CUDA(cudaMemset(m->g, 0, P * 4));
+    if (m->wbf) MOSES_CUDA(cudaMemset(m->wbf, 0, P * 2));
+    const int vec = 16 / m->esz;
+    int maxw = 0;
+    for (int l = 0; l < m->L; ++l) {
+      const long long ldl = round_up(m->dims[l] + 1, vec);
+      m->ld.push_back(ldl);
+      m->lddz.push_back(round_up(m->dims[l], vec));
+      maxw = std::max(maxw, m->dims[l]);
+      void* a = nullptr;
+      MOSES_CUDA(cudaMalloc(&a, m->cap * ldl * m->esz));
+      MOSES_CUDA(cudaMemset(a, 0, m->cap * ldl * m->esz));
+      m->act.push_back(a);
+      void* d = nullptr;
+      if (l > 0) {
+        MOSES_CUDA(cudaMalloc(&d, m->cap * m->lddz[l] * m->esz));
+        MOSES_CUDA(cudaMemset(d, 0, m->cap * m->lddz[l] * m->esz));
+      }
+      m->dz.push_back(d);
+      // ones column of every activation buffer (never overwritten by the epilogues)
+      if (m->esz == 2) set_ones_column<__nv_bfloat16>(static_cast<__nv_bfloat16*>(a), m->cap, m->dims[l], ldl, m->st);
+      else set_ones_column<float>(static_cast<float*>(a), m->cap, m->dims[l], ldl, m->st);
+      note_launch(1);
+    }
+    m->max_tiles = ceil_div(m->dims[m->L - 1], 64);
+    m->head_part = dalloc<float>(m->max_tiles * m->cap);
+    m->head_part2 = dalloc<float>(m->max_tiles * m->cap);
+    m->scores = dalloc<float>(m->cap);
+    m->labels = dalloc<float>(m->cap);
+    m->coefA = dalloc<float>(m->cap);
+    m->coefB = dalloc<float>(m->cap);
+    const int ns = rank_splits(m->cap);
+    m->rank.nsplit = ns;
+    m->rank.gs_part = dalloc<double>(ns * m->cap);
+    m->rank.loss_part = dalloc<double>(ns * m->cap);
+    m->rank.pairs_part = dalloc<long long>(ns * m->cap);
+    m->dscal = dalloc<double>(16);
+    m->dpairs = dalloc<long long>(4);
+    m->dcount = dalloc<unsigned long long>(4);
+    const long long seln = std::max<long long>(P, m->cap);
+    const size_t selb = select_ws_bytes(seln, nullptr);
+    MOSES_CUDA(cudaMalloc(&m->sel_base, selb));
+    select_ws_carve(m->sel_base, seln, &m->sel);
+    m->stage_w = std::max<long long>(maxw, 1) + 1;
+    m->staging = dalloc<double>(m->cap * m->stage_w);
+    m->adv_ws = dalloc<float>(round_up(m->cap, 64) + round_up(maxw + 1, 64) + 64);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    *out = m.release();
+  });
+}
+
+MOSES_API int moses_model_destroy(moses_model_t m) {
+  return guarded([&] { delete m; });
+}
+
+MOSES_API int moses_model_upload(moses_model_t m, const double* params, const double* momentum, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "parameter count mismatch");
+    upload_f32(m, params, count, m->w);
+    if (momentum) upload_f32(m, momentum, count, m->mom);
+    else MOSES_CUDA(cudaMemsetAsync(m->mom, 0, count * 4, m->st));
+    if (m->wbf) {
+      f32_to_bf16(m->w, count, m->wbf, m->st);
+      note_launch(1);
+    }
+    m->xi_valid = false;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_model_download(moses_model_t m, double* params, double* momentum, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "parameter count mismatch");
+    if (params) download_f32(m, m->w, count, params);
+    if (momentum) download_f32(m, m->mom, count, momentum);
+  });
+}
+
+MOSES_API int moses_model_copy(moses_model_t dst, moses_model_t src) {
+  return guarded([&] {
+    require_model(dst);
+    require_model(src);
+    if (dst->dims != src->dims) fail(MOSES_ERR_SHAPE_MISMATCH, "model dims differ");
+    MOSES_CUDA(cudaStreamSynchronize(src->st));
+    MOSES_CUDA(cudaMemcpyAsync(dst->w, src->w, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
+    MOSES_CUDA(cudaMemcpyAsync(dst->mom, src->mom, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
+    if (dst->wbf) {
+      f32_to_bf16(dst->w, dst->P, dst->wbf, dst->st);
+      note_launch(1);
+    }
+    MOSES_CUDA(cudaStreamSynchronize(dst->st));
+  });
+}
+
+MOSES_API int moses_model_synchronize(moses_model_t m) {
+  return guarded([&] {
+    require_model(m);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int64_t moses_packed_ld(moses_model_t m) { return m ? m->ld[0] : -MOSES_ERR_INVALID_ARG; }
+
+static void predict_impl(moses_model* m, const double* x, long long n, int D, double* out, bool penult) {
+  require_model(m);
+  if (D != m->dims[0])
+    fail(MOSES_ERR_DIM_MISMATCH, "feature width " + std::to_string(D) + " != model input width " +
+                                     std::to_string(m->dims[0]));
+  const int W = m->W();
+  for (long long r = 0; r < n;) {
+    const long long c = std::min(n - r, m->cap);
+    upload_rows(m, x + r * D, c, 0);
+    dispatch_forward(m, m->act[0], m->ld[0], c, nullptr, penult);
+    if (penult) {
+      if (m->esz == 2) unpack_rows<__nv_bfloat16>(static_cast<__nv_bfloat16*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging, m->st);
+      else unpack_rows<float>(static_cast<float*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging, m->st);
+      note_launch(1);
+      for (long long q = 0; q < c;) {  // staging holds cap*stage_w doubles >= c*W
+        const long long cc = c - q;
+        MOSES_CUDA(cudaMemcpyAsync(out + (r + q) * W, m->staging + q * W, sizeof(double) * cc * W,
+                                   cudaMemcpyDeviceToHost, m->st));
+        q += cc;
+      }
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    } else {
+      head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, m->scores, m->st);
+      note_launch(1);
+      download_f32(m, m->scores, c, out + r);
+    }
+    r += c;
+  }
+}
+
+MOSES_API int moses_predict(moses_model_t m, const double* x, int64_t n, int32_t D, double* scores) {
+  return guarded([&] { predict_impl(m, x, n, D, scores, false); });
+}
+MOSES_API int moses_penultimate(moses_model_t m, const double* x, int64_t n, int32_t D, double* h) {
+  return guarded([&] { predict_impl(m, x, n, D, h, true); });
+}
+
+MOSES_API int moses_predict_device(moses_model_t m, const void* x_dev, int32_t dtype, int64_t ldx, int64_t n,
+                                   float* scores_dev) {
+  return guarded([&] {
+    require_model(m);
+    if ((dtype == MOSES_DTYPE_BF16) != (m->esz == 2)) fail(MOSES_ERR_INVALID_ARG, "dtype must match the handle precision");
+    for (long long r = 0; r < n;) {
+      const long long c = std::min(n - r, m->cap);
+      const void* x0 = static_cast<const uint8_t*>(x_dev) + r * ldx * m->esz;
+      dispatch_forward(m, x0, ldx, c, nullptr, false);
+      head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, scores_dev + r, m->st);
+      note_launch(1);
+      r += c;
+    }
+  });
+}
+
+MOSES_API int moses_predict_pooled(moses_model_t m, const double* x, int64_t n, int32_t D, const int64_t* offsets,
+                                   int64_t programs, double* scores) {
+  return guarded([&] {
+    require_model(m);
+    if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "feature width != model input width");
+    if (offsets[0] != 0 || offsets[programs] != n) fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must span the rows");
+    for (int64_t p = 0; p < programs; ++p)
+      if (offsets[p + 1] < offsets[p]) fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must be non-decreasing");
+    // per-statement head dots (bias excluded), then segment sum + bias on the device
+    float* stmt = nullptr;
+    long long* doff = nullptr;
+    float* pout = nullptr;
+    stmt = dalloc<float>(n);
+    doff = dalloc<long long>(programs + 1);
+    pout = dalloc<float>(programs);
+    float zero_b = 0.f;
+    float* dzero = dalloc<float>(1);
+    MOSES_CUDA(cudaMemcpyAsync(dzero, &zero_b, 4, cudaMemcpyHostToDevice, m->st));
+    MOSES_CUDA(cudaMemcpyAsync(doff, offsets, sizeof(long long) * (programs + 1), cudaMemcpyHostToDevice, m->st));
+    for (long long r = 0; r < n;) {
+      const long long c = std::min(n - r, m->cap);
+      upload_rows(m, x + r * D, c, 0);
+      dispatch_forward(m, m->act[0], m->ld[0], c, nullptr, false);
+      head_scores(m->head_part, m->last_tiles, m->cap, dzero, c, stmt + r, m->st);
+      note_launch(1);
+      r += c;
+    }
+    float hb = 0.f;
+    MOSES_CUDA(cudaMemcpyAsync(&hb, m->head_b(), 4, cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    segment_sum_scalar(stmt, doff, programs, hb, pout, m->st);
+    note_launch(1);
+    download_f32(m, pout, programs, scores);
+    dfree(stmt);
+    dfree(doff);
+    dfree(pout);
+    dfree(dzero);
+  });
+}
+
+static void gradients_host(moses_model* m, const double* x, const double* y, long long n, int D, moses_adversary* adv,
+                           double beta) {
+  require_model(m);
+  if (D != m->dims[0])
+    fail(MOSES_ERR_DIM_MISMATCH, "batch feature width " + std::to_string(D) + " != model input width " +
+                                     std::to_string(m->dims[0]));
+  const bool active = adv != nullptr && beta != 0.0 && n > 0;
+  if (active) {  // model.cpp:130-137
+    if (adv->W != m->W()) fail(MOSES_ERR_DIM_MISMATCH, "discriminator width != penultimate width");
+    if (adv->m == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "adversary has an empty replay buffer");
+    if (adv->D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "replay feature width != model input width");
+  }
+  const long long mrep = active ? adv->m : 0;
+  check_rows(m, mrep + n);
+  if (active) upload_replay(m, adv);
+  upload_rows(m, x, n, mrep);
+  upload_f32(m, y, n, m->labels);
+  gradients_core(m, m->act[0], m->ld[0], m->labels, n, active ? adv : nullptr, beta);
+}
+
+MOSES_API int moses_gradients(moses_model_t m, const double* x, const double* y, int64_t n, int32_t D,
+                              moses_adversary_t adv, double beta, double* loss_out) {
+  return guarded([&] {
+    gradients_host(m, x, y, n, D, adv, beta);
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    }
+  });
+}
+
+MOSES_API int moses_objective(moses_model_t m, const double* x, const double* y, int64_t n, int32_t D,
+                              moses_adversary_t adv, double beta, double* out) {
+  // objective = the loss gradients() reports (model.cpp:246-261 vs :237); the gradient buffer is
+  // preserved so the call stays read-only on the handle's visible state.
+  return guarded([&] {
+    require_model(m);
+    float* gsave = dalloc<float>(m->P);
+    MOSES_CUDA(cudaMemcpyAsync(gsave, m->g, m->P * 4, cudaMemcpyDeviceToDevice, m->st));
+    gradients_host(m, x, y, n, D, adv, beta);
+    MOSES_CUDA(cudaMemcpyAsync(out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaMemcpyAsync(m->g, gsave, m->P * 4, cudaMemcpyDeviceToDevice, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    dfree(gsave);
+  });
+}
+
+MOSES_API int moses_gradients_download(moses_model_t m, double* g, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "gradient count mismatch");
+    download_f32(m, m->g, count, g);
+  });
+}
+MOSES_API int moses_gradients_upload(moses_model_t m, const double* g, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "gradient count mismatch");
+    upload_f32(m, g, count, m->g);
+    m->xi_valid = false;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+static const uint8_t* upload_mask(moses_model* m, const uint8_t* mask, int64_t len) {
+  if (!mask) return nullptr;
+  if (len != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "mask length != parameter count");
+  MOSES_CUDA(cudaMemcpyAsync(m->mask, mask, m->P, cudaMemcpyHostToDevice, m->st));
+  m->mask_valid = true;
+  return m->mask;
+}
+
+MOSES_API int moses_apply_update(moses_model_t m, double lr, double mu, const uint8_t* mask, int64_t mask_len,
+                                 int32_t use_momentum) {
+  return guarded([&] {
+    require_model(m);
+    const uint8_t* dm = upload_mask(m, mask, mask_len);
+    sgd_update(m->w, m->mom, m->g, dm, m->P, float(lr), float(mu), use_momentum != 0, m->shadow(), m->st);
+    note_launch(1);
+    m->xi_valid = false;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_adam_update(moses_model_t m, double lr, double b1, double b2, double eps, int32_t step,
+                                const uint8_t* mask, int64_t mask_len) {
+  return guarded([&] {
+    require_model(m);
+    if (step < 1) fail(MOSES_ERR_INVALID_ARG, "adam step must be >= 1");
+    if (!m->m1) {
+      m->m1 = dalloc<float>(m->P);
+      m->m2 = dalloc<float>(m->P);
+      MOSES_CUDA(cudaMemsetAsync(m->m1, 0, m->P * 4, m->st));
+      MOSES_CUDA(cudaMemsetAsync(m->m2, 0, m->P * 4, m->st));
+    }
+    const uint8_t* dm = upload_mask(m, mask, mask_len);
+    const float c1 = float(1.0 - std::pow(b1, step)), c2 = float(1.0 - std::pow(b2, step));
+    adam_update(m->w, m->m1, m->m2, m->g, dm, m->P, float(lr), float(b1), float(b2), float(eps), c1, c2, m->shadow(),
+                m->st);
+    note_launch(1);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_train_step(moses_model_t m, const double* x, const double* y, int64_t n, int32_t D, double lr,
+                               double mu, double* loss_out) {
+  return guarded([&] {
+    gradients_host(m, x, y, n, D, nullptr, 0.0);
+    sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+    note_launch(1);
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    }
+  });
+}
+
+MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                      double lr, double mu, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    check_rows(m, n);
+    gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
+    sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+    note_launch(1);
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    }
+  });
+}
+
+MOSES_API int moses_ranking_accuracy(moses_model_t m, const double* x, const double* y, const int64_t* boff,
+                                     int32_t nb, int32_t D, double* acc, int64_t* pairs, int64_t* conc) {
+  return guarded([&] {
+    require_model(m);
+    if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "feature width != model input width");
+    const long long n = nb > 0 ? boff[nb] : 0;
+    float* s = dalloc<float>(n);
+    float* yd = dalloc<float>(n);
+    long long* seg = dalloc<long long>(n);
+    long long* so = dalloc<long long>(nb + 1);
+    std::vector<long long> seg_h(n);
+    for (int b = 0; b < nb; ++b)
+      for (long long r = boff[b]; r < boff[b + 1]; ++r) seg_h[r] = b;
+    MOSES_CUDA(cudaMemcpyAsync(seg, seg_h.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, m->st));
+    MOSES_CUDA(cudaMemcpyAsync(so, boff, sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, m->st));
+    for (long long r = 0; r < n;) {
+      const long long c = std::min(n - r, m->cap);
+      upload_rows(m, x + r * D, c, 0);
+      dispatch_forward(m, m->act[0], m->ld[0], c, nullptr, false);
+      head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, s + r, m->st);
+      note_launch(1);
+      r += c;
+    }
+    upload_f32(m, y, n, yd);
+    accuracy_counts(s, yd, seg, so, n, nullptr, nullptr, m->dcount, m->st);
+    note_launch(1);
+    unsigned long long tot[2] = {0, 0};
+    MOSES_CUDA(cudaMemcpyAsync(tot, m->dcount, sizeof(tot), cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    *pairs = (int64_t)tot[0];
+    *conc = (int64_t)tot[1];
+    *acc = tot[0] == 0 ? 0.0 : double(tot[1]) / double(tot[0]);
+    dfree(s);
+    dfree(yd);
+    dfree(seg);
+    dfree(so);
+  });
+}
+
+MOSES_API int moses_ranking_loss(const double* s, const double* y, int64_t n, double* loss, int64_t* pairs) {
+  return guarded([&] {
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const int ns = rank_splits(n);
+    const size_t bytes = (size_t(n) * 2 + 64) * 8 + size_t(ns) * n * 24 + size_t(n) * 8 + 4096;
+    Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
+    double* s64 = cv.take<double>(n);
+    double* y64 = cv.take<double>(n);
+    float* sf = cv.take<float>(n);
+    float* yf = cv.take<float>(n);
+    float* ca = cv.take<float>(n);
+    float* cb = cv.take<float>(n);
+    RankWs ws{cv.take<double>(ns * n), cv.take<double>(ns * n), cv.take<long long>(ns * n), ns};
+    double* dl = cv.take<double>(4);
+    long long* dp = cv.take<long long>(2);
+    if (n > 0) {
+      MOSES_CUDA(cudaMemcpyAsync(s64, s, 8 * n, cudaMemcpyHostToDevice, sc.st));
+      MOSES_CUDA(cudaMemcpyAsync(y64, y, 8 * n, cudaMemcpyHostToDevice, sc.st));
+      f64_to_f32(s64, n, sf, sc.st);
+      f64_to_f32(y64, n, yf, sc.st);
+      rank_pairs(sf, yf, n, ws, sc.st);
+      note_launch(3);
+    }
+    rank_finalize(ws, n, 0, nullptr, 0, 0, nullptr, 0.0, {dl, dp, ca, cb, dl + 1}, sc.st);
+    note_launch(1);
+    long long p = 0;
+    MOSES_CUDA(cudaMemcpyAsync(loss, dl, 8, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(&p, dp, 8, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+    if (pairs) *pairs = p;
+  });
+}
+
+// ---------------------------------------------------------------- lottery
+MOSES_API int moses_xi_scores(moses_model_t m, int32_t normalize, double* xi_out, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    xi_scores(m->w, m->g, m->P, normalize != 0, m->sel, m->xi, m->st);
+    note_launch(normalize ? 3 : 2);
+    m->xi_valid = true;
+    m->xi_norm = normalize != 0;
+    if (xi_out) {
+      if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "xi count mismatch");
+      download_f32(m, m->xi, count, xi_out);
+    }
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_xi_upload(moses_model_t m, const double* xi, int64_t count, int32_t normalized) {
+  return guarded([&] {
+    require_model(m);
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "xi count mismatch");
+    upload_f32(m, xi, count, m->xi);
+    m->xi_valid = true;
+    m->xi_norm = normalized != 0;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_mask_upload(moses_model_t m, const uint8_t* mask, int64_t count) {
+  return guarded([&] {
+    require_model(m);
+    upload_mask(m, mask, count);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+static long long partition_validate(moses_model* m, int mode, double value, bool normalized) {
+  const long long n = m->P;
+  if (n == 0) fail(MOSES_ERR_SHAPE_MISMATCH, "empty score array");
+  if (mode == MOSES_MODE_THRESHOLD) {
+    if (!normalized) fail(MOSES_ERR_UNNORMALIZED_THRESHOLD, "threshold partition needs normalized scores");
+    return -1;
+  }
+  if (mode != MOSES_MODE_RATIO) fail(MOSES_ERR_INVALID_ARG, "unknown partition mode");
+  if (!(value > 0.0) || value > 1.0) fail(MOSES_ERR_INVALID_RATIO, "ratio must lie in (0,1], got " + std::to_string(value));
+  return (long long)std::ceil(value * double(n));  // lottery.cpp:160, fp64 like the reference
+}
+
+static long long finish_mask(moses_model* m, int mode, long long keep, uint8_t* mask_out, int64_t count) {
+  long long pop;
+  if (mode == MOSES_MODE_RATIO) pop = std::min(keep, m->P);
+  else pop = popcount_mask(m->mask, m->P, m->dcount, m->st), note_launch(1);
+  if (mask_out) {
+    if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "mask count mismatch");
+    MOSES_CUDA(cudaMemcpyAsync(mask_out, m->mask, m->P, cudaMemcpyDeviceToHost, m->st));
+  }
+  MOSES_CUDA(cudaStreamSynchronize(m->st));
+  m->mask_valid = true;
+  return pop;
+}
+
+MOSES_API int moses_partition(moses_model_t m, int32_t mode, double value, int32_t phase, uint8_t* mask_out,
+                              int64_t count, int64_t* popcount) {
+  (void)phase;  // carried by the caller's ParamMask (lottery.hpp:25-32)
+  return guarded([&] {
+    require_model(m);
+    if (!m->xi_valid) fail(MOSES_ERR_SHAPE_MISMATCH, "no xi scores on the device (call moses_xi_scores)");
+    const long long keep = partition_validate(m, mode, value, m->xi_norm);
+    if (mode == MOSES_MODE_RATIO && keep >= m->P) {
+      MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
+    } else {
+      partition_from_xi(m->xi, m->P, mode, float(value), keep, m->sel, m->mask, m->st);
+      note_launch(mode == MOSES_MODE_RATIO ? 9 : 3);
+    }
+    const long long pop = finish_mask(m, mode, keep, mask_out, count);
+    if (popcount) *popcount = pop;
+  });
+}
+
+MOSES_API int moses_transferable_step(moses_model_t m, double alpha) {
+  return guarded([&] {
+    require_model(m);
+    if (!m->mask_valid) fail(MOSES_ERR_SHAPE_MISMATCH, "mask length != parameter count");
+    lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), 1.f, true, false, m->shadow(), m->st);
+    note_launch(1);
+    m->xi_valid = false;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+static float decay_factor(double alpha, double lambda, bool* noop) {
+  const double rate = alpha * lambda;
+  if (!(rate >= 0.0) || rate >= 1.0)
+    fail(MOSES_ERR_UNSTABLE_DECAY, "decay rate alpha*lambda = " + std::to_string(rate) + " must lie in [0,1)");
+  *noop = rate == 0.0;
+  return float(1.0 - rate);
+}
+
+MOSES_API int moses_variant_decay(moses_model_t m, double alpha, double lambda) {
+  return guarded([&] {
+    require_model(m);
+    if (!m->mask_valid) fail(MOSES_ERR_SHAPE_MISMATCH, "mask length != parameter count");
+    bool noop = false;
+    const float f = decay_factor(alpha, lambda, &noop);
+    if (noop) return;
+    lottery_apply(m->w, m->g, m->mask, m->P, 0.f, f, false, true, m->shadow(), m->st);
+    note_launch(1);
+    m->xi_valid = false;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, int32_t phase, double alpha,
+                                 double lambda, uint8_t* mask_out, int64_t count, int64_t* popcount) {
+  (void)phase;
+  return guarded([&] {
+    require_model(m);
+    const long long keep = partition_validate(m, mode, value, true /* the tuner normalises in threshold mode */);
+    if (mode == MOSES_MODE_RATIO && keep >= m->P) {
+      MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
+    } else {
+      lottery_select(m->w, m->g, m->P, mode, float(value), keep, m->sel, m->mask, nullptr, false, m->st);
+      note_launch(mode == MOSES_MODE_RATIO ? 8 : 3);
+    }
+    // step on kept scalars; decay the rest (reference order: step, then decay validation)
+    const double rate = alpha * lambda;
+    const bool decay_ok = (rate >= 0.0) && rate < 1.0;
+    const bool decay = decay_ok && rate != 0.0;
+    lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
+    note_launch(1);
+    m->xi_valid = false;
+    const long long pop = finish_mask(m, mode, keep, mask_out, count);
+    if (popcount) *popcount = pop;
+    if (!decay_ok) {
+      bool noop;
+      decay_factor(alpha, lambda, &noop);
+    }
+  });
+}
+
+// ---------------------------------------------------------------- adversary
+MOSES_API int moses_adversary_create(const double* replay, int64_t mrows, int32_t D, int32_t width, double step,
+                                     moses_adversary_t* out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (mrows == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "replay buffer must be non-empty");  // lottery.cpp:253
+    if (width <= 0) fail(MOSES_ERR_BAD_DIMS, "penultimate width must be positive");
+    auto a = std::make_unique<moses_adversary>();
+    a->D = D;
+    a->W = width;
+    a->m = mrows;
+    a->eta = float(step);
+    a->replay = dalloc<float>(mrows * D);
+    a->u = dalloc<float>(width);
+    a->c = dalloc<float>(1);
+    std::vector<float> tmp(mrows * D);
+    for (long long i = 0; i < mrows * D; ++i) tmp[i] = float(replay[i]);
+    MOSES_CUDA(cudaMemcpy(a->replay, tmp.data(), 4 * tmp.size(), cudaMemcpyHostToDevice));
+    MOSES_CUDA(cudaMemset(a->u, 0, 4 * width));
+    MOSES_CUDA(cudaMemset(a->c, 0, 4));
+    *out = a.release();
+  });
+}
+MOSES_API int moses_adversary_destroy(moses_adversary_t a) {
+  return guarded([&] { delete a; });
+}
+MOSES_API int moses_adversary_get(moses_adversary_t a, double* w, int32_t width, double* b) {
+  return guarded([&] {
+    if (width != a->W) fail(MOSES_ERR_DIM_MISMATCH, "width mismatch");
+    std::vector<float> t(width + 1);
+    MOSES_CUDA(cudaMemcpy(t.data(), a->u, 4 * width, cudaMemcpyDeviceToHost));
+    MOSES_CUDA(cudaMemcpy(t.data() + width, a->c, 4, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < width; ++j) w[j] = t[j];
+    *b = t[width];
+  });
+}
+MOSES_API int moses_adversary_set(moses_adversary_t a, const double* w, int32_t width, double b) {
+  return guarded([&] {
+    if (width != a->W) fail(MOSES_ERR_DIM_MISMATCH, "width mismatch");
+    std::vector<float> t(width + 1);
+    for (int j = 0; j < width; ++j) t[j] = float(w[j]);
+    t[width] = float(b);
+    MOSES_CUDA(cudaMemcpy(a->u, t.data(), 4 * width, cudaMemcpyHostToDevice));
+    MOSES_CUDA(cudaMemcpy(a->c, t.data() + width, 4, cudaMemcpyHostToDevice));
+  });
+}
+
+MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const double* x, int64_t n, int32_t D,
+                                     double beta, double* dloss, double* conf) {
+  return guarded([&] {
+    require_model(m);
+    if (!a) fail(MOSES_ERR_ADVERSARY_DISABLED, "null adversary");
+    if (a->m == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "adversary has an empty replay buffer");
+    if (n == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "empty activation batch");
+    if (a->W != m->W()) fail(MOSES_ERR_DIM_MISMATCH, "activation width != discriminator width");
+    if (D != m->dims[0] || a->D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "feature width != model input width");
+    check_rows(m, a->m + n);
+    upload_replay(m, a);
+    upload_rows(m, x, n, a->m);
+    dispatch_forward(m, m->act[0], m->ld[0], a->m + n, a->u, true);
+    if (m->esz == 2)
+      adversary_step<__nv_bfloat16>(m->head_part2, m->last_tiles, m->cap, static_cast<__nv_bfloat16*>(m->act[m->L - 1]),
+                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+    else
+      adversary_step<float>(m->head_part2, m->last_tiles, m->cap, static_cast<float*>(m->act[m->L - 1]),
+                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+    note_launch(3);
+    double l = 0;
+    MOSES_CUDA(cudaMemcpyAsync(&l, m->dscal + 2, 8, cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    if (dloss) *dloss = l;
+    if (conf) *conf = -beta * l;
+  });
+}
+
+MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hs, int64_t ms, const double* ht, int64_t nt,
+                                     int32_t width, double beta, double* dloss, double* conf) {
+  return guarded([&] {
+    if (!a || a->m == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "adversary has an empty replay buffer");
+    if (ms == 0 || nt == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "empty activation batch");
+    if (width != a->W) fail(MOSES_ERR_DIM_MISMATCH, "activation width != discriminator width");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const long long R = ms + nt;
+    const size_t bytes = size_t(R) * width * 12 + size_t(R) * 16 + size_t(width) * 16 + 8192;
+    Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
+    double* h64 = cv.take<double>(R * width);
+    float* H = cv.take<float>(R * width);
+    float* z = cv.take<float>(R);
+    float* ws = cv.take<float>(round_up(R, 64) + round_up(width + 1, 64) + 64);
+    double* dl = cv.take<double>(2);
+    MOSES_CUDA(cudaMemcpyAsync(h64, hs, 8 * ms * width, cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(h64 + ms * width, ht, 8 * nt * width, cudaMemcpyHostToDevice, sc.st));
+    f64_to_f32(h64, R * width, H, sc.st);
+    // logits as a single "tile" of partials: z_r = H_r . u
+    row_dot(H, width, R, width, a->u, z, sc.st);
+    adversary_step<float>(z, 1, R, H, width, ms, nt, width, a->u, a->c, a->eta, dl, ws, sc.st);
+    note_launch(5);
+    double l = 0;
+    MOSES_CUDA(cudaMemcpyAsync(&l, dl, 8, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+    if (dloss) *dloss = l;
+    if (conf) *conf = -beta * l;
+  });
+}
+
+MOSES_API int moses_discriminator_cross_entropy(const double* zs, int64_t m, const double* zt, int64_t n, double* out) {
+  return guarded([&] {
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    Carver cv{static_cast<uint8_t*>(sc.ensure(size_t(m + n) * 8 + 4096))};
+    double* z = cv.take<double>(m + n);
+    double* o = cv.take<double>(1);
+    MOSES_CUDA(cudaMemcpyAsync(z, zs, 8 * m, cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(z + m, zt, 8 * n, cudaMemcpyHostToDevice, sc.st));
+    disc_ce(z, m, n, o, sc.st);
+    note_launch(1);
+    MOSES_CUDA(cudaMemcpyAsync(out, o, 8, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+  });
+}
+
+// ---------------------------------------------------------------- candidate selection
+MOSES_API int moses_topk_device(const float* scores, int64_t n, int64_t k, int64_t* idx_out) {
+  return guarded([&] {
+    if (k <= 0 || n <= 0) return;
+    if (k > n) k = n;
+    if (k > kTopkMax) fail(MOSES_ERR_INVALID_ARG, "k must be <= 4096");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const size_t selb = select_ws_bytes(n, nullptr);
+    Carver cv{static_cast<uint8_t*>(sc.ensure(selb + (kTopkMax * 12) + 8192))};
+    uint8_t* selbase = cv.take<uint8_t>(selb);
+    unsigned* ok = cv.take<unsigned>(n < kTopkMax ? kTopkMax : kTopkMax);
+    long long* oi = cv.take<long long>(kTopkMax);
+    SelectWs ws;
+    select_ws_carve(selbase, n, &ws);
+    topk_select(scores, n, k, ws, ok, oi, sc.st);
+    note_launch(10);
+    MOSES_CUDA(cudaMemcpyAsync(idx_out, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+  });
+}
+
+MOSES_API int moses_topk(const double* scores, int64_t n, int64_t k, int64_t* idx_out) {
+  return guarded([&] {
+    if (k <= 0 || n <= 0) return;
+    float* d = dalloc<float>(n);
+    double* d64 = dalloc<double>(n);
+    MOSES_CUDA(cudaMemcpy(d64, scores, 8 * n, cudaMemcpyHostToDevice));
+    f64_to_f32(d64, n, d, nullptr);
+    note_launch(1);
+    MOSES_CUDA(cudaDeviceSynchronize());
+    const int rc = moses_topk_device(d, n, k, idx_out);
+    dfree(d);
+    dfree(d64);
+    if (rc) throw Status(rc, g_err);
+  });
+}
+
+MOSES_API int64_t moses_select_batch(const uint64_t* hashes, int64_t n, const uint64_t* measured, int64_t nm,
+                                     int64_t batch_size, int64_t* out) {
+  if (batch_size < 1) {
+    g_err = "batch size must be positive";
+    return -MOSES_ERR_INVALID_CONFIG;
+  }
+  std::unordered_set<uint64_t> meas(measured, measured + nm), taken;
+  int64_t c = 0;
+  for (int64_t i = 0; i < n && c < batch_size; ++i) {
+    if (meas.count(hashes[i]) || !taken.insert(hashes[i]).second) continue;
+    out[c++] = i;
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- extensions
+MOSES_API int moses_segment_sum_device(const void* h, int32_t dtype, int64_t ld, int32_t width, const int64_t* off,
+                                       int64_t programs, float* out) {
+  return guarded([&] {
+    if (dtype == MOSES_DTYPE_BF16)
+      segment_sum<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(h), ld, width, reinterpret_cast<const long long*>(off),
+                                 programs, out, width, nullptr);
+    else
+      segment_sum<float>(static_cast<const float*>(h), ld, width, reinterpret_cast<const long long*>(off), programs, out,
+                         width, nullptr);
+    note_launch(1);
+  });
+}
+
+MOSES_API int moses_segment_sum(const double* h, int64_t rows, int32_t width, const int64_t* off, int64_t programs,
+                                double* out) {
+  return guarded([&] {
+    if (programs < 0 || off[0] != 0 || off[programs] != rows) fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must span the rows");
+    const int wp = int(round_up(width, 4));
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const size_t bytes = size_t(rows) * width * 8 + size_t(rows) * wp * 4 + size_t(programs + 1) * 8 +
+                         size_t(programs) * wp * 12 + 8192;
+    Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
+    double* h64 = cv.take<double>(rows * width);
+    float* H = cv.take<float>(rows * wp);
+    long long* doff = cv.take<long long>(programs + 1);
+    float* o = cv.take<float>(programs * wp);
+    double* o64 = cv.take<double>(programs * wp);
+    MOSES_CUDA(cudaMemcpyAsync(h64, h, 8 * rows * width, cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(doff, off, 8 * (programs + 1), cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemsetAsync(H, 0, 4 * rows * wp, sc.st));
+    strided_f64_to_f32(h64, rows, width, H, wp, sc.st);
+    segment_sum<float>(H, wp, wp, reinterpret_cast<const long long*>(doff), programs, o, wp, sc.st);
+    unpack_rows<float>(o, programs, width, wp, o64, sc.st);
+    note_launch(3);
+    MOSES_CUDA(cudaMemcpyAsync(out, o64, 8 * programs * width, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+  });
+}
+
+MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t n, int32_t width, double sigma,
+                         double* out) {
+  return guarded([&] {
+    if (m <= 0 || n <= 0) fail(MOSES_ERR_INVALID_ARG, "mmd needs non-empty source and target");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const long long R = m + n;
+    const long long parts = (long long)ceil_div(m, 64) * ceil_div(m, 64) + ceil_div(n, 64) * ceil_div(n, 64) +
+                            ceil_div(m, 64) * ceil_div(n, 64);
+    Carver cv{static_cast<uint8_t*>(sc.ensure(size_t(R) * width * 12 + size_t(parts + 16) * 8 + 8192))};
+    double* h64 = cv.take<double>(R * width);
+    float* H = cv.take<float>(R * width);
+    double* ws = cv.take<double>(parts + 16);
+    MOSES_CUDA(cudaMemcpyAsync(h64, xs, 8 * m * width, cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(h64 + m * width, xt, 8 * n * width, cudaMemcpyHostToDevice, sc.st));
+    f64_to_f32(h64, R * width, H, sc.st);
+    *out = mmd2(H, m, H + m * width, n, width, float(sigma), ws, sc.st);
+    note_launch(7);
+  });
+}
+
+MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype, void* dst,
+                                          int64_t ld) {
+  return guarded([&] {
+    if (dtype == MOSES_DTYPE_BF16) synth_features<__nv_bfloat16>(seed, row0, n, D, static_cast<__nv_bfloat16*>(dst), ld, nullptr);
+    else synth_features<float>(seed, row0, n, D, static_cast<float*>(dst), ld, nullptr);
+    note_launch(1);
+  });
+}
+MOSES_API int moses_synth_labels_device(uint64_t seed, int64_t row0, int64_t n, float* dst) {
+  return guarded([&] {
+    synth_labels(seed, row0, n, dst, nullptr);
+    note_launch(1);
+  });
+}
+
+// ---------------------------------------------------------------- files (host byte formats)
+static void put_u32(std::vector<uint8_t>& o, uint32_t v) { for (int i = 0; i < 4; ++i) o.push_back(uint8_t(v >> (8 * i))); }
+static void put_u64(std::vector<uint8_t>& o, uint64_t v) { for (int i = 0; i < 8; ++i) o.push_back(uint8_t(v >> (8 * i))); }
+static uint64_t get_u64(const uint8_t* p) { uint64_t v = 0; for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i); return v; }
+static uint32_t get_u32(const uint8_t* p) { uint32_t v = 0; for (int i = 0; i < 4; ++i) v |= uint32_t(p[i]) << (8 * i); return v; }
+
+MOSES_API int64_t moses_serialize(const int32_t* dims, int32_t nd, const double* params, const double* mom, uint8_t* out,
+                                  int64_t cap) {
+  std::vector<uint8_t> b;
+  const int rc = guarded([&] {
+    check_dims(dims, nd, true);
+    if (dims[1] != 512 || dims[2] != 512) fail(MOSES_ERR_BAD_DIMS, "only the {D,512,512,1} shape has a file form");
+    std::vector<int> d(dims, dims + nd);
+    const long long P = level_off(d, 3);
+    b.reserve(12 + 16 * P);
+    b.insert(b.end(), {'M', 'O', 'S', 'M'});
+    put_u32(b, 1);
+    put_u32(b, uint32_t(dims[0]));
+    for (long long i = 0; i < P; ++i) put_u64(b, std::bit_cast<uint64_t>(params[i]));
+    for (long long i = 0; i < P; ++i) put_u64(b, std::bit_cast<uint64_t>(mom ? mom[i] : 0.0));
+  });
+  if (rc) return -rc;
+  if (out && cap >= (int64_t)b.size()) std::memcpy(out, b.data(), b.size());
+  return (int64_t)b.size();
+}
+
+MOSES_API int moses_deserialize(const uint8_t* bytes, int64_t len, int32_t* dims_out, double* params, double* mom,
+                                int64_t cap) {
+  return guarded([&] {
+    if (len < 12 || std::memcmp(bytes, "MOSM", 4) != 0) fail(MOSES_ERR_CORRUPT_STREAM, "bad magic or truncated header");
+    const uint32_t ver = get_u32(bytes + 4);
+    if (ver != 1) fail(MOSES_ERR_VERSION_MISMATCH, "format version " + std::to_string(ver) + ", expected 1");
+    const uint32_t D = get_u32(bytes + 8);
+    if (D == 0 || D > 4096) fail(MOSES_ERR_CORRUPT_STREAM, "implausible input width");
+    std::vector<int> d = {int(D), 512, 512, 1};
+    const long long P = level_off(d, 3);
+    if (len != 12 + 16 * P) fail(MOSES_ERR_CORRUPT_STREAM, "stream is " + std::to_string(len) + " bytes");
+    for (int i = 0; i < 4; ++i) dims_out[i] = d[i];
+    if (cap < P) fail(MOSES_ERR_CAPACITY, "output capacity too small");
+    for (long long i = 0; i < P; ++i) {
+      params[i] = std::bit_cast<double>(get_u64(bytes + 12 + 8 * i));
+      const double v = std::bit_cast<double>(get_u64(bytes + 12 + 8 * (P + i)));
+      if (mom) mom[i] = v;
+      if (!std::isfinite(params[i]) || !std::isfinite(v)) fail(MOSES_ERR_CORRUPT_STREAM, "non-finite parameter value");
+    }
+  });
+}
+
+MOSES_API int64_t moses_write_mask(const uint8_t* mask, int64_t n, int32_t phase, int32_t mode, double value,
+                                   uint8_t* out, int64_t cap) {
+  std::vector<uint8_t> b = {'M', 'O', 'S', 'K'};
+  put_u64(b, uint64_t(n));
+  put_u32(b, uint32_t(phase));
+  b.push_back(mode == MOSES_MODE_THRESHOLD ? 1 : 2);
+  put_u64(b, std::bit_cast<uint64_t>(value));
+  std::vector<uint8_t> bits((n + 7) / 8, 0);
+  for (int64_t i = 0; i < n; ++i)
+    if (mask[i]) bits[i / 8] |= uint8_t(1u << (i % 8));
+  b.insert(b.end(), bits.begin(), bits.end());
+  if (out && cap >= (int64_t)b.size()) std::memcpy(out, b.data(), b.size());
+  return (int64_t)b.size();
+}
+
+MOSES_API int moses_read_mask(const uint8_t* buf, int64_t len, uint8_t* mask_out, int64_t cap, int64_t* n,
+                              int32_t* phase, int32_t* mode, double* value) {
+  return guarded([&] {
+    if (len < 25 || std::memcmp(buf, "MOSK", 4) != 0) fail(MOSES_ERR_CORRUPT_STREAM, "bad magic or truncated header");
+    const uint64_t cnt = get_u64(buf + 4);
+    const uint8_t mb = buf[16];
+    if (mb != 1 && mb != 2) fail(MOSES_ERR_CORRUPT_STREAM, "unknown mode byte");
+    if ((uint64_t)len != 25 + (cnt + 7) / 8) fail(MOSES_ERR_CORRUPT_STREAM, "mask file size mismatch");
+    *n = (int64_t)cnt;
+    *phase = int32_t(get_u32(buf + 12));
+    *mode = mb;
+    *value = std::bit_cast<double>(get_u64(buf + 17));
+    if (mask_out) {
+      if (cap < (int64_t)cnt) fail(MOSES_ERR_CAPACITY, "mask capacity too small");
+      for (uint64_t i = 0; i < cnt; ++i) mask_out[i] = (buf[25 + i / 8] >> (i % 8)) & 1;
+    }
+  });
+}
+
+MOSES_API int moses_model_device_ptrs(moses_model_t m, float** params, float** grads, float** momentum) {
+  return guarded([&] {
+    require_model(m);
+    if (params) *params = m->w;
+    if (grads) *grads = m->g;
+    if (momentum) *momentum = m->mom;
+  });
+}
+MOSES_API int moses_model_stream(moses_model_t m, void** stream) {
+  return guarded([&] {
+    require_model(m);
+    *stream = m->st;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+// gemm.cu — host side of the tcgen05 GEMM: TMA descriptor encoding (driver
+// entry point fetched through the runtime, so the library needs no -lcuda),
+// N-tile selection for the 148-SM grid, and the template instantiations.
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace moses {
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) fail(MOSES_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D tiled map over a row-major matrix: `inner` contiguous elements per row,
+// `outer` rows, row stride `ld` elements; box = box_inner x box_outer, 128-B swizzle.
+CUtensorMap make_map(const void* base, int elem, long long inner, long long outer, long long ld, int box_inner,
+                     int box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * elem};
+  const cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem) & 15))
+    fail(MOSES_ERR_INVALID_ARG, "TMA operand must be 16-byte aligned with a 16-byte row stride");
+  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(MOSES_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+// operand map: rows of the GEMM dimension `mn` (size MN), K along the other axis
+CUtensorMap operand_map(const Operand& o, int elem, long long MN, long long K, int tile_mn) {
+  const int chunk = 128 / elem;  // elements in one 128-B swizzle row
+  if (o.mn_major) return make_map(o.ptr, elem, MN, K, o.ld, chunk, chunk /* BK */);
+  return make_map(o.ptr, elem, K, MN, o.ld, chunk, tile_mn);
+}
+
+template <typename T, int BN, bool AMN, bool BMN, int EPI>
+void launch_t(const GemmCall& c, cudaStream_t s) {
+  using Cfg = GemmCfg<T, BN>;
+  auto kern = umma_gemm_kernel<T, BN, AMN, BMN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    configured = true;
+  }
+  constexpr int elem = sizeof(T);
+  const CUtensorMap ta = operand_map(c.A, elem, c.M, c.K, Cfg::BM);
+  const CUtensorMap tb = operand_map(c.B, elem, c.N, c.K, BN);
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mask = c.mask;
+  a.ldm = c.ldm;
+  dim3 grid(ceil_div(c.M, Cfg::BM), ceil_div(c.N, BN));
+  kern<<<grid, 128, Cfg::kSmemBytes, s>>>(ta, tb, a);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+template <typename T, int BN>
+void dispatch_major(const GemmCall& c, cudaStream_t s) {
+  const bool am = c.A.mn_major, bm = c.B.mn_major;
+  switch (c.epi) {
+    case EpiKind::Fwd:
+      if (!am && bm) return launch_t<T, BN, false, true, int(Epi::Fwd)>(c, s);
+      if (!am && !bm) return launch_t<T, BN, false, false, int(Epi::Fwd)>(c, s);
+      break;
+    case EpiKind::Dgrad:
+      if (!am && !bm) return launch_t<T, BN, false, false, int(Epi::Dgrad)>(c, s);
+      break;
+    case EpiKind::StoreF32:
+      if (am && bm) return launch_t<T, BN, true, true, int(Epi::StoreF32)>(c, s);
+      if (!am && !bm) return launch_t<T, BN, false, false, int(Epi::StoreF32)>(c, s);
+      if (!am && bm) return launch_t<T, BN, false, true, int(Epi::StoreF32)>(c, s);
+      break;
+  }
+  fail(MOSES_ERR_INVALID_ARG, "unsupported GEMM operand-major / epilogue combination");
+}
+
+template <typename T>
+void dispatch_bn(const GemmCall& c, int bn, cudaStream_t s) {
+  switch (bn) {
+    case 64: return dispatch_major<T, 64>(c, s);
+    case 128: return dispatch_major<T, 128>(c, s);
+    default: return dispatch_major<T, 256>(c, s);
+  }
+}
+
+}  // namespace
+
+// Largest N tile that still gives at least one full wave of CTAs on 148 SMs;
+// small problems fall back to BN=64 for parallelism.
+int gemm_pick_bn(int M, int N) {
+  const int mt = ceil_div(M, 128);
+  for (int bn : {256, 128}) {
+    if (N >= bn && (long long)mt * ceil_div(N, bn) >= 148) return bn;
+  }
+  return 64;
+}
+
+int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
+  if (c.M <= 0 || c.N <= 0) return 0;
+  if (c.K <= 0) fail(MOSES_ERR_INVALID_ARG, "GEMM with K == 0");
+  const int bn = c.bn ? c.bn : gemm_pick_bn(c.M, c.N);
+  if (elem == 2) dispatch_bn<__nv_bfloat16>(c, bn, s);
+  else dispatch_bn<float>(c, bn, s);
+  return bn;
+}
+
+}  // namespace moses

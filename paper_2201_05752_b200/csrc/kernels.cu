@@ -1,0 +1,1157 @@
+// kernels.cu — the non-GEMM sm_100a kernels of the Moses hot path.
+//
+// Everything here is bandwidth- or latency-bound integer/elementwise work, so
+// the rules are: coalesced 16-byte accesses, grids sized to the 148 SMs,
+// and fixed-order reductions (no float atomics) so every result is
+// bit-reproducible run to run. Integer atomics (histograms, counts) are
+// order-independent and therefore deterministic too.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.cuh"
+
+namespace moses {
+namespace {
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+int grid_for(long long n, int block, int per_sm = 8) {
+  long long g = (n + block - 1) / block;
+  return int(g < 1 ? 1 : (g > kSMs * per_sm ? kSMs * per_sm : g));
+}
+
+// ---------------------------------------------------------------- data movement
+template <typename T>
+__global__ void pack_rows_kernel(const double* __restrict__ src, long long n, int D, T* __restrict__ dst, long long ld) {
+  const long long total = n * ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ld;
+    const int c = int(i - r * ld);
+    const float v = c < D ? float(src[r * D + c]) : (c == D ? 1.f : 0.f);
+    dst[i] = from_f<T>(v);
+  }
+}
+template <typename T>
+__global__ void pack_rows_f32_kernel(const float* __restrict__ src, long long n, int D, long long lds, T* __restrict__ dst,
+                                     long long ld) {
+  const long long total = n * ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ld;
+    const int c = int(i - r * ld);
+    const float v = c < D ? src[r * lds + c] : (c == D ? 1.f : 0.f);
+    dst[i] = from_f<T>(v);
+  }
+}
+template <typename T>
+__global__ void set_col_kernel(T* act, long long rows, int col, long long ld) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x)
+    act[r * ld + col] = from_f<T>(1.f);
+}
+template <typename T>
+__global__ void unpack_rows_kernel(const T* __restrict__ src, long long n, int W, long long ld, double* __restrict__ dst) {
+  const long long total = n * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W;
+    const int c = int(i - r * W);
+    dst[i] = double(to_f(src[r * ld + c]));
+  }
+}
+__global__ void f32_to_f64_kernel(const float* s, long long n, double* d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = s[i];
+}
+__global__ void f64_to_f32_kernel(const double* s, long long n, float* d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = float(s[i]);
+}
+__global__ void f32_to_bf16_kernel(const float* s, long long n, __nv_bfloat16* d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+__global__ void strided_f64_to_f32_kernel(const double* s, long long rows, int W, float* d, long long ldd) {
+  const long long total = rows * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W;
+    d[r * ldd + (i - r * W)] = float(s[i]);
+  }
+}
+__global__ void row_dot_kernel(const float* __restrict__ H, long long ldh, long long R, int W, const float* __restrict__ u,
+                               float* __restrict__ out) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < R; r += nw) {
+    float acc = 0.f;
+    for (int j = lane; j < W; j += 32) acc = fmaf(H[r * ldh + j], u[j], acc);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- scores from head partials
+__global__ void head_scores_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hb,
+                                   long long rows, float* __restrict__ s) {
+  const float b = hb[0];
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int t = 0; t < ntiles; ++t) acc += part[t * ld + r];  // fixed tile order
+    s[r] = acc + b;
+  }
+}
+
+// ---------------------------------------------------------------- pairwise ranking (model.cpp:71-106)
+// Row i accumulates, over its column split, every pair it belongs to:
+//   y_i > y_j : i is "hi": gs_i -= sigma(-(s_i - s_j)), loss += softplus(-(s_i - s_j)), pairs++
+//   y_j > y_i : i is "lo": gs_i += sigma(-(s_j - s_i))
+// Each distinct-label pair is counted once (at its hi row), as in the reference's i<j loop.
+constexpr int kRankBlock = 128;
+constexpr int kRankChunk = 512;
+__global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __restrict__ s, const float* __restrict__ y,
+                                                                long long n, double* gs_part, double* loss_part,
+                                                                long long* pairs_part) {
+  __shared__ float ss[kRankBlock], sy[kRankBlock];
+  const long long i = blockIdx.x * (long long)kRankBlock + threadIdx.x;
+  const long long j0 = (long long)blockIdx.y * kRankChunk;
+  const long long j1 = min(n, j0 + kRankChunk);
+  const bool ok = i < n;
+  const float si = ok ? s[i] : 0.f, yi = ok ? y[i] : 0.f;
+  double gs = 0.0, loss = 0.0;
+  long long pairs = 0;
+  for (long long jt = j0; jt < j1; jt += kRankBlock) {
+    const long long j = jt + threadIdx.x;
+    __syncthreads();
+    ss[threadIdx.x] = j < j1 ? s[j] : 0.f;
+    sy[threadIdx.x] = j < j1 ? y[j] : 0.f;
+    __syncthreads();
+    const int cnt = int(min((long long)kRankBlock, j1 - jt));
+    if (!ok) continue;
+    for (int q = 0; q < cnt; ++q) {
+      const float yj = sy[q];
+      if (yi == yj) continue;
+      const bool hi = yi > yj;
+      const float d = hi ? si - ss[q] : ss[q] - si;  // s_hi - s_lo
+      const float e = expf(-fabsf(d));
+      const float sig_neg = d >= 0.f ? e / (1.f + e) : 1.f / (1.f + e);
+      if (hi) {
+        gs -= sig_neg;
+        loss += d >= 0.f ? log1pf(e) : -d + log1pf(e);
+        ++pairs;
+      } else {
+        gs += sig_neg;
+      }
+    }
+  }
+  if (ok) {
+    const long long o = (long long)blockIdx.y * n + i;
+    gs_part[o] = gs;
+    loss_part[o] = loss;
+    pairs_part[o] = pairs;
+  }
+}
+
+__device__ __forceinline__ float stable_sigmoid(float x) {  // model.cpp:64-68
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+__device__ __forceinline__ double softplus_d(double v) { return fmax(v, 0.0) + log1p(exp(-fabs(v))); }
+
+constexpr int kFinBlock = 1024;
+__global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* gs_part, const double* loss_part,
+                                                                  const long long* pairs_part, int nsplit, long long n,
+                                                                  long long roff, const float* part2, int ntiles2,
+                                                                  long long ld2, const float* adv_bias, double beta,
+                                                                  double* loss_out, long long* pairs_out, float* coefA,
+                                                                  float* coefB, double* ce_out) {
+  using BR = cub::BlockReduce<double, kFinBlock>;
+  using BRL = cub::BlockReduce<long long, kFinBlock>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ typename BRL::TempStorage tmpl;
+  __shared__ double sh_loss;
+  __shared__ long long sh_pairs;
+  long long p = 0;
+  double l = 0.0;
+  for (long long i = threadIdx.x; i < n; i += kFinBlock)
+    for (int sp = 0; sp < nsplit; ++sp) {
+      p += pairs_part[sp * n + i];
+      l += loss_part[sp * n + i];
+    }
+  const long long ptot = BRL(tmpl).Sum(p);
+  __syncthreads();
+  const double ltot = BR(tmp).Sum(l);
+  if (threadIdx.x == 0) {
+    sh_pairs = ptot;
+    sh_loss = ptot > 0 ? ltot / double(ptot) : 0.0;
+  }
+  __syncthreads();
+  const long long pairs = sh_pairs;
+  const double inv = pairs > 0 ? 1.0 / double(pairs) : 0.0;
+  const long long R = roff + n;
+  for (long long r = threadIdx.x; r < R; r += kFinBlock) {
+    float a = 0.f;
+    if (r >= roff) {
+      double g = 0.0;
+      for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + (r - roff)];
+      a = pairs > 0 ? float(g * inv) : 0.f;
+    }
+    coefA[r] = a;
+    coefB[r] = 0.f;
+  }
+  double total = sh_loss;
+  if (part2 != nullptr && beta != 0.0 && n > 0) {
+    // logits z = c + sum of per-tile partial dots (fixed order); reversed gradient (model.cpp:224-231)
+    const float c = adv_bias[0];
+    const long long m = roff;
+    double ls = 0.0, lt = 0.0;
+    for (long long r = threadIdx.x; r < R; r += kFinBlock) {
+      float z = 0.f;
+      for (int t = 0; t < ntiles2; ++t) z += part2[t * ld2 + r];
+      z += c;
+      if (r < m) {
+        coefB[r] = float(0.5 * beta * double(stable_sigmoid(-z)) / double(m));
+        ls += softplus_d(-double(z));
+      } else {
+        coefB[r] = float(-0.5 * beta * double(stable_sigmoid(z)) / double(n));
+        lt += softplus_d(double(z));
+      }
+    }
+    __syncthreads();
+    const double lst = BR(tmp).Sum(ls);
+    __syncthreads();
+    const double ltt = BR(tmp).Sum(lt);
+    if (threadIdx.x == 0) {
+      const double ce = 0.5 * (lst / double(m) + ltt / double(n));
+      total += beta * -ce;
+      if (ce_out) *ce_out = ce;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *loss_out = total;
+    *pairs_out = pairs;
+  }
+}
+
+template <typename T>
+__global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
+                                     const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
+                                     long long ldh, long long R, int W, T* __restrict__ dz, long long ldz) {
+  const long long total = R * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W;
+    const int j = int(i - r * W);
+    float v = coefA[r] * wh[j];
+    if (u != nullptr) v += coefB[r] * u[j];
+    dz[r * ldz + j] = from_f<T>(to_f(H[r * ldh + j]) > 0.f ? v : 0.f);
+  }
+}
+
+// g[j] = sum_r coef[r] * H[r][j]; g[W] = sum_r coef[r]. 32 columns x 8 row-lanes per block.
+template <typename T>
+__global__ void column_dot_kernel(const float* __restrict__ coef, const T* __restrict__ H, long long ldh, long long R, int W,
+                                  float* __restrict__ g) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  float acc = 0.f;
+  if (j < W)
+    for (long long r = ty; r < R; r += 8) acc = fmaf(coef[r], to_f(H[r * ldh + j]), acc);
+  else if (j == W)
+    for (long long r = ty; r < R; r += 8) acc += coef[r];
+  red[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && j <= W) {
+    float s = red[0][tx];
+    for (int k = 1; k < 8; ++k) s += red[k][tx];
+    g[j] = s;
+  }
+}
+
+// ---------------------------------------------------------------- updates (no FMA contraction: reference
+// is built with -ffp-contract=off, so v = mu*v + g and w -= lr*v round after every op)
+template <bool MOM, bool MASK, bool SHADOW>
+__global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
+                           const uint8_t* __restrict__ mask, long long P, float lr, float mu,
+                           __nv_bfloat16* __restrict__ shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
+    float wi = w[i];
+    if (!MASK || mask[i]) {
+      if (MOM) {
+        const float vi = __fadd_rn(__fmul_rn(mu, v[i]), g[i]);
+        v[i] = vi;
+        wi = __fsub_rn(wi, __fmul_rn(lr, vi));
+      } else {
+        wi = __fsub_rn(wi, __fmul_rn(lr, g[i]));
+      }
+      w[i] = wi;
+    }
+    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+template <bool SHADOW>
+__global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m1, float* __restrict__ m2, const float* __restrict__ g,
+                            const uint8_t* __restrict__ mask, long long P, float lr, float b1, float b2, float eps,
+                            float c1, float c2, __nv_bfloat16* __restrict__ shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
+    float wi = w[i];
+    if (mask == nullptr || mask[i]) {
+      const float gi = g[i];
+      const float a = __fadd_rn(__fmul_rn(b1, m1[i]), __fmul_rn(__fsub_rn(1.f, b1), gi));
+      const float b = __fadd_rn(__fmul_rn(b2, m2[i]), __fmul_rn(__fsub_rn(1.f, b2), __fmul_rn(gi, gi)));
+      m1[i] = a;
+      m2[i] = b;
+      const float mh = __fdiv_rn(a, c1);
+      const float vh = __fdiv_rn(b, c2);
+      wi = __fsub_rn(wi, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
+      w[i] = wi;
+    }
+    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+template <bool SHADOW>
+__global__ void decay_kernel(float* __restrict__ w, const uint8_t* __restrict__ mask, long long P, float factor,
+                             __nv_bfloat16* __restrict__ shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
+    float wi = w[i];
+    if (!mask[i]) {
+      wi = __fmul_rn(wi, factor);
+      w[i] = wi;
+    }
+    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+// ---------------------------------------------------------------- radix select (top `need` keys, ties by index)
+// Three MSB-first passes over u32 keys (11, 11, 10 bits). State in device memory.
+struct SelState {
+  unsigned prefix, pmask;
+  unsigned long long need;  // still to take among keys matching the prefix
+  unsigned long long gt;    // keys strictly above the current prefix range
+  unsigned digit;           // digit chosen in the last pass
+  unsigned max_bits;        // threshold mode: max xi bits
+  unsigned long long count; // popcount accumulator
+};
+constexpr int kSelBlock = 256;
+constexpr int kBins = 2048;
+constexpr int kPassShift[3] = {21, 10, 0};
+constexpr int kPassBits[3] = {11, 11, 10};
+
+__device__ __forceinline__ unsigned float_key_desc(float f) {  // orderable: larger float -> larger key
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+struct Chunk {
+  long long lo, hi;
+};
+__device__ __forceinline__ Chunk block_chunk(long long n, long long chunk) {
+  const long long lo = (long long)blockIdx.x * chunk;
+  return {lo, min(n, lo + chunk)};
+}
+
+// MODE 0: keys given; MODE 1: keys = bits(|w*g|) (xi), also atomicMax of bits; MODE 2: keys = float_key_desc(score)
+template <int MODE, bool BLOCK_HIST>
+__global__ void __launch_bounds__(kSelBlock) radix_hist_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                               unsigned* __restrict__ keys, float* __restrict__ xi_out,
+                                                               long long n, long long chunk, SelState* st, int shift,
+                                                               int bits, unsigned* __restrict__ hist,
+                                                               unsigned* __restrict__ block_hist) {
+  __shared__ unsigned sh[kBins];
+  const int nb = 1 << bits;
+  for (int d = threadIdx.x; d < nb; d += kSelBlock) sh[d] = 0;
+  __syncthreads();
+  const unsigned prefix = st->prefix, pmask = st->pmask;
+  const Chunk ch = block_chunk(n, chunk);
+  unsigned local_max = 0;
+  for (long long i = ch.lo + threadIdx.x; i < ch.hi; i += kSelBlock) {
+    unsigned key;
+    if constexpr (MODE == 1) {
+      const float x = fabsf(__fmul_rn(a[i], b[i]));
+      key = __float_as_uint(x);
+      keys[i] = key;
+      if (xi_out) xi_out[i] = x;
+      local_max = max(local_max, key);
+    } else if constexpr (MODE == 2) {
+      key = float_key_desc(a[i]);
+      keys[i] = key;
+    } else {
+      key = keys[i];
+    }
+    if ((key & pmask) == prefix) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1u);
+  }
+  if constexpr (MODE == 1) {
+    for (int o = 16; o; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+    if ((threadIdx.x & 31) == 0 && local_max) atomicMax(&st->max_bits, local_max);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < nb; d += kSelBlock) {
+    const unsigned v = sh[d];
+    if (v) atomicAdd(&hist[d], v);
+    if (BLOCK_HIST) block_hist[(long long)blockIdx.x * kBins + d] = v;
+  }
+}
+
+constexpr int kPickBlock = 1024;
+__global__ void __launch_bounds__(kPickBlock) radix_pick_kernel(SelState* st, unsigned* hist, int shift, int bits) {
+  using Scan = cub::BlockScan<unsigned long long, kPickBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long suffix[kBins + 1];
+  const int nb = 1 << bits;
+  // suffix[d] = count of digits >= d. Thread t owns digits (nb-1-2t, nb-2-2t) in descending order.
+  const int per = (nb + kPickBlock - 1) / kPickBlock;
+  unsigned long long vals[2] = {0, 0};
+  unsigned long long local = 0;
+  for (int q = 0; q < per; ++q) {
+    const int d = nb - 1 - (threadIdx.x * per + q);
+    vals[q] = d >= 0 ? hist[d] : 0;
+    local += vals[q];
+  }
+  unsigned long long excl;
+  Scan(tmp).ExclusiveSum(local, excl);
+  unsigned long long run = excl;
+  for (int q = 0; q < per; ++q) {
+    const int d = nb - 1 - (threadIdx.x * per + q);
+    run += vals[q];
+    if (d >= 0) suffix[d] = run;
+  }
+  if (threadIdx.x == 0) suffix[nb] = 0;
+  __syncthreads();
+  const unsigned long long need = st->need;
+  // the chosen digit d* is the largest d with suffix[d] >= need (suffix is non-increasing in d)
+  for (int d = threadIdx.x; d < nb; d += kPickBlock) {
+    if (suffix[d] >= need && suffix[d + 1] < need) {
+      st->digit = unsigned(d);
+      st->need = need - suffix[d + 1];
+      st->gt += suffix[d + 1];
+      st->prefix |= unsigned(d) << shift;
+      st->pmask |= unsigned(nb - 1) << shift;
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < nb; d += kPickBlock) hist[d] = 0;
+}
+
+__global__ void sel_init_kernel(SelState* st, unsigned long long need, unsigned* hist) {
+  if (threadIdx.x == 0) {
+    st->prefix = 0;
+    st->pmask = 0;
+    st->need = need;
+    st->gt = 0;
+    st->digit = 0;
+    st->max_bits = 0;
+    st->count = 0;
+  }
+  for (int d = threadIdx.x; d < kBins; d += blockDim.x) hist[d] = 0;
+}
+
+// Block-contiguous final pass: kept = key > T || (key == T && rank_among_equal < need).
+// ACTION 0: write mask byte; 1: compact (key, idx) for top-k.
+template <int ACTION>
+__global__ void __launch_bounds__(kSelBlock) radix_apply_kernel(const unsigned* __restrict__ keys, long long n,
+                                                                long long chunk, const SelState* st,
+                                                                const unsigned* __restrict__ block_hist,
+                                                                uint8_t* __restrict__ mask, unsigned* out_key,
+                                                                long long* out_idx, unsigned long long* counter) {
+  using Scan = cub::BlockScan<unsigned, kSelBlock>;
+  using Red = cub::BlockReduce<unsigned long long, kSelBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ typename Red::TempStorage rtmp;
+  __shared__ unsigned long long sh_base;
+  const unsigned T = st->prefix;
+  const unsigned long long need = st->need;
+  const unsigned digit = st->digit;
+  // equal keys in earlier blocks (last pass histogram of block b' at digit d* counts keys == T)
+  unsigned long long before = 0;
+  for (int b = threadIdx.x; b < blockIdx.x; b += kSelBlock) before += block_hist[(long long)b * kBins + digit];
+  before = Red(rtmp).Sum(before);
+  if (threadIdx.x == 0) sh_base = before;
+  __syncthreads();
+  unsigned long long base = sh_base;
+  const Chunk ch = block_chunk(n, chunk);
+  for (long long t0 = ch.lo; t0 < ch.hi; t0 += kSelBlock) {
+    const long long i = t0 + threadIdx.x;
+    const bool valid = i < ch.hi;
+    const unsigned key = valid ? keys[i] : 0u;
+    const unsigned eq = (valid && key == T) ? 1u : 0u;
+    unsigned rank, tot;
+    Scan(tmp).ExclusiveSum(eq, rank, tot);
+    __syncthreads();
+    const bool kept = valid && (key > T || (eq && base + rank < need));
+    if (valid) {
+      if constexpr (ACTION == 0) {
+        mask[i] = kept ? 1 : 0;
+      } else {
+        if (kept) {
+          const unsigned long long pos = atomicAdd(counter, 1ull);
+          out_key[pos] = key;
+          out_idx[pos] = i;
+        }
+      }
+    }
+    base += tot;
+  }
+}
+
+// Threshold mode (normalised xi strictly above theta, lottery.cpp:152-157); also counts kept scalars.
+__global__ void __launch_bounds__(kSelBlock) threshold_mask_kernel(const unsigned* __restrict__ keys, long long n,
+                                                                   SelState* st, float theta, bool normalize,
+                                                                   uint8_t* __restrict__ mask, float* xi_norm) {
+  using Red = cub::BlockReduce<unsigned long long, kSelBlock>;
+  __shared__ typename Red::TempStorage rtmp;
+  const float top = __uint_as_float(st->max_bits);
+  unsigned long long cnt = 0;
+  for (long long i = blockIdx.x * (long long)kSelBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kSelBlock) {
+    float x = __uint_as_float(keys[i]);
+    if (normalize && top > 0.f) x = __fdiv_rn(x, top);
+    if (xi_norm) xi_norm[i] = x;
+    const bool kept = x > theta;
+    if (mask) mask[i] = kept;
+    cnt += kept;
+  }
+  cnt = Red(rtmp).Sum(cnt);
+  if (threadIdx.x == 0 && cnt) atomicAdd(&st->count, cnt);
+}
+
+__global__ void xi_normalize_kernel(float* xi, long long n, const SelState* st) {
+  const float top = __uint_as_float(st->max_bits);
+  if (!(top > 0.f)) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    xi[i] = __fdiv_rn(xi[i], top);
+}
+
+// Fused transferable step + variant decay on the mask (lottery.cpp:92-120):
+//   kept:   w -= alpha * g     (apply_update, no momentum)
+//   else:   w *= (1 - alpha*lambda)
+template <bool SHADOW>
+__global__ void lottery_apply_kernel(float* __restrict__ w, const float* __restrict__ g, const uint8_t* __restrict__ mask,
+                                     long long n, float alpha, float factor, bool step, bool decay,
+                                     __nv_bfloat16* __restrict__ shadow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float wi = w[i];
+    if (mask[i]) {
+      if (step) wi = __fsub_rn(wi, __fmul_rn(alpha, g[i]));
+    } else if (decay) {
+      wi = __fmul_rn(wi, factor);
+    }
+    w[i] = wi;
+    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+__global__ void popcount_kernel(const uint8_t* __restrict__ mask, long long n, unsigned long long* out) {
+  using Red = cub::BlockReduce<unsigned long long, kSelBlock>;
+  __shared__ typename Red::TempStorage rtmp;
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)kSelBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kSelBlock) c += mask[i] != 0;
+  c = Red(rtmp).Sum(c);
+  if (threadIdx.x == 0 && c) atomicAdd(out, c);
+}
+
+// Top-k: bitonic sort of the compacted winners by (key desc, index asc), one block.
+constexpr int kSortBlock = 1024;
+__global__ void __launch_bounds__(kSortBlock) topk_sort_kernel(unsigned* keys, long long* idx, const unsigned long long* count,
+                                                               long long k) {
+  __shared__ unsigned sk[kTopkMax];
+  __shared__ long long si[kTopkMax];
+  const int cnt = int(*count);
+  int np = 1;
+  while (np < cnt) np <<= 1;
+  for (int t = threadIdx.x; t < np; t += kSortBlock) {
+    sk[t] = t < cnt ? keys[t] : 0u;
+    si[t] = t < cnt ? idx[t] : 0x7fffffffffffffffll;
+  }
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < np; t += kSortBlock) {
+        const int o = t ^ stride;
+        if (o > t) {
+          const bool desc_block = (t & size) == 0;  // first half ordered "before"
+          const bool t_before_o = sk[t] > sk[o] || (sk[t] == sk[o] && si[t] < si[o]);
+          if (t_before_o != desc_block) {
+            const unsigned a = sk[t]; sk[t] = sk[o]; sk[o] = a;
+            const long long b = si[t]; si[t] = si[o]; si[o] = b;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < k && t < cnt; t += kSortBlock) {
+    keys[t] = sk[t];
+    idx[t] = si[t];
+  }
+}
+
+// ---------------------------------------------------------------- accuracy (model.cpp:298-312)
+__global__ void accuracy_kernel(const float* __restrict__ s, const float* __restrict__ y, const long long* __restrict__ seg_of_row,
+                                const long long* __restrict__ seg_off, long long n, unsigned long long* totals) {
+  using Red = cub::BlockReduce<unsigned long long, 256>;
+  __shared__ typename Red::TempStorage rtmp;
+  unsigned long long p = 0, c = 0;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const long long sg = seg_of_row[i];
+    const long long lo = seg_off[sg], hi = seg_off[sg + 1];
+    const float yi = y[i], si = s[i];
+    for (long long j = lo; j < hi; ++j) {
+      if (yi <= y[j]) continue;
+      ++p;
+      if (si > s[j]) ++c;
+    }
+  }
+  p = Red(rtmp).Sum(p);
+  __syncthreads();
+  c = Red(rtmp).Sum(c);
+  if (threadIdx.x == 0) {
+    if (p) atomicAdd(&totals[0], p);
+    if (c) atomicAdd(&totals[1], c);
+  }
+}
+
+// ---------------------------------------------------------------- adversary (lottery.cpp:135-164)
+__global__ void __launch_bounds__(kFinBlock) adv_logits_kernel(const float* part2, int ntiles, long long ld2, long long m,
+                                                               long long n, const float* c, float* dz, double* loss_out,
+                                                               double* dc_out) {
+  using BR = cub::BlockReduce<double, kFinBlock>;
+  __shared__ typename BR::TempStorage tmp;
+  const long long R = m + n;
+  double ls = 0.0, lt = 0.0, dcs = 0.0, dct = 0.0;
+  for (long long r = threadIdx.x; r < R; r += kFinBlock) {
+    float z = 0.f;
+    for (int t = 0; t < ntiles; ++t) z += part2[t * ld2 + r];
+    z += c[0];
+    float d;
+    if (r < m) {
+      d = float(-0.5 * double(stable_sigmoid(-z)) / double(m));
+      ls += softplus_d(-double(z));
+      dcs += d;
+    } else {
+      d = float(0.5 * double(stable_sigmoid(z)) / double(n));
+      lt += softplus_d(double(z));
+      dct += d;
+    }
+    dz[r] = d;
+  }
+  const double a = BR(tmp).Sum(ls);
+  __syncthreads();
+  const double b = BR(tmp).Sum(lt);
+  __syncthreads();
+  const double e = BR(tmp).Sum(dcs);
+  __syncthreads();
+  const double f = BR(tmp).Sum(dct);
+  if (threadIdx.x == 0) {
+    *loss_out = 0.5 * (a / double(m) + b / double(n));
+    *dc_out = e + f;
+  }
+}
+__global__ void __launch_bounds__(kFinBlock) disc_ce_kernel(const double* z, long long m, long long n, double* out) {
+  using BR = cub::BlockReduce<double, kFinBlock>;
+  __shared__ typename BR::TempStorage tmp;
+  double ls = 0.0, lt = 0.0;
+  for (long long r = threadIdx.x; r < m + n; r += kFinBlock) {
+    if (r < m) ls += softplus_d(-z[r]);
+    else lt += softplus_d(z[r]);
+  }
+  const double a = BR(tmp).Sum(ls);
+  __syncthreads();
+  const double b = BR(tmp).Sum(lt);
+  if (threadIdx.x == 0) *out = 0.5 * (a / double(m) + b / double(n));
+}
+__global__ void adv_update_kernel(float* u, float* c, const float* du, int W, float eta, const double* dc) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < W; j += gridDim.x * blockDim.x)
+    u[j] = __fsub_rn(u[j], __fmul_rn(eta, du[j]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) c[0] = __fsub_rn(c[0], __fmul_rn(eta, float(*dc)));
+}
+
+// ---------------------------------------------------------------- segment-sum pooling (CSR), one warp per program
+template <typename T>
+__global__ void segment_sum_kernel(const T* __restrict__ H, long long ldh, int W, const long long* __restrict__ off,
+                                   long long programs, float* __restrict__ out, long long ldo) {
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  const long long warp_global = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long p = warp_global; p < programs; p += nwarps) {
+    const long long lo = off[p], hi = off[p + 1];
+    for (int j0 = lane * V; j0 < W; j0 += 32 * V) {
+      float acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = 0.f;
+      for (long long r = lo; r < hi; ++r) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(H + r * ldh + j0));
+        const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] += to_f(e[q]);
+      }
+      float* o = out + p * ldo + j0;
+#pragma unroll
+      for (int q = 0; q < V; q += 4) *reinterpret_cast<float4*>(o + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+    }
+  }
+}
+__global__ void segment_sum_scalar_kernel(const float* __restrict__ v, const long long* __restrict__ off, long long programs,
+                                          float bias, float* __restrict__ out) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < programs; p += (long long)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (long long r = off[p]; r < off[p + 1]; ++r) acc += v[r];
+    out[p] = acc + bias;
+  }
+}
+
+// ---------------------------------------------------------------- MMD^2 (Gaussian kernel), tiled 64x64 Gram + exp + sum
+constexpr int kGT = 64;
+__global__ void __launch_bounds__(256) gram_exp_kernel(const float* __restrict__ A, long long na, const float* __restrict__ B,
+                                                       long long nb, int W, float inv2s2, double* partial) {
+  __shared__ float sa[kGT][33], sb[kGT][33];
+  using BR = cub::BlockReduce<double, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long i0 = (long long)blockIdx.x * kGT, j0 = (long long)blockIdx.y * kGT;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < W; k0 += 32) {
+    for (int t = threadIdx.x; t < kGT * 32; t += 256) {
+      const int r = t / 32, k = t % 32;
+      sa[r][k] = (i0 + r < na && k0 + k < W) ? A[(i0 + r) * W + k0 + k] : 0.f;
+      sb[r][k] = (j0 + r < nb && k0 + k < W) ? B[(j0 + r) * W + k0 + k] : 0.f;
+    }
+    __syncthreads();
+    for (int k = 0; k < 32; ++k)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const float d = sa[ty * 4 + a][k] - sb[tx * 4 + b][k];
+          acc[a][b] = fmaf(d, d, acc[a][b]);
+        }
+    __syncthreads();
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (i0 + ty * 4 + a < na && j0 + tx * 4 + b < nb) s += double(expf(-acc[a][b] * inv2s2));
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.y * (long long)gridDim.x + blockIdx.x] = s;
+}
+__global__ void sum_partials_kernel(const double* p, long long n, double* out) {
+  using BR = cub::BlockReduce<double, 1024>;
+  __shared__ typename BR::TempStorage tmp;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) s += p[i];
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ---------------------------------------------------------------- synthetic data
+__device__ __forceinline__ unsigned long long fnv_u64(unsigned long long h, unsigned long long v) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xffull;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+template <int N>
+__device__ __forceinline__ unsigned long long fnv_str(unsigned long long h, const char (&s)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {  // includes the terminating NUL, like KeyBuilder::add(string_view)
+    h ^= (unsigned char)s[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+__device__ __forceinline__ unsigned long long splitmix_at(unsigned long long key, unsigned long long k) {
+  unsigned long long z = key + k * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double u01(unsigned long long bits) { return double(bits >> 11) * 0x1.0p-53; }
+
+template <typename T>
+__global__ void synth_features_kernel(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    unsigned long long key = fnv_u64(0xcbf29ce484222325ull, seed);
+    key = fnv_str(key, "feat");
+    key = fnv_u64(key, (unsigned long long)(row0 + r));
+    T* row = dst + r * ld;
+    for (int c = 0; c < ld; ++c) {
+      const float v = c < D ? float(u01(splitmix_at(key, (unsigned long long)c + 1))) : (c == D ? 1.f : 0.f);
+      row[c] = from_f<T>(v);
+    }
+  }
+}
+__global__ void synth_labels_kernel(unsigned long long seed, long long row0, long long n, float* dst) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    unsigned long long key = fnv_u64(0xcbf29ce484222325ull, seed);
+    key = fnv_str(key, "label");
+    key = fnv_u64(key, (unsigned long long)(row0 + r));
+    dst[r] = float(0.1 + u01(splitmix_at(key, 1)));
+  }
+}
+
+}  // namespace
+
+// ====================================================================== host wrappers
+template <typename T>
+void pack_rows(const double* src, long long n, int D, T* dst, long long ld, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_rows_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, dst, ld);
+  MOSES_CUDA(cudaGetLastError());
+}
+template <typename T>
+void pack_rows_f32(const float* src, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_rows_f32_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, lds, dst, ld);
+  MOSES_CUDA(cudaGetLastError());
+}
+template <typename T>
+void set_ones_column(T* act, long long rows, int col, long long ld, cudaStream_t s) {
+  if (rows <= 0) return;
+  set_col_kernel<T><<<grid_for(rows, 256), 256, 0, s>>>(act, rows, col, ld);
+  MOSES_CUDA(cudaGetLastError());
+}
+template <typename T>
+void unpack_rows(const T* src, long long n, int W, long long ld, double* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  unpack_rows_kernel<T><<<grid_for(n * W, 256), 256, 0, s>>>(src, n, W, ld, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void f32_to_f64(const float* src, long long n, double* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  f32_to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  f64_to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, long long ldd, cudaStream_t s) {
+  if (rows <= 0) return;
+  strided_f64_to_f32_kernel<<<grid_for(rows * W, 256), 256, 0, s>>>(src, rows, W, dst, ldd);
+  MOSES_CUDA(cudaGetLastError());
+}
+void row_dot(const float* H, long long ldh, long long R, int W, const float* u, float* out, cudaStream_t s) {
+  if (R <= 0) return;
+  row_dot_kernel<<<grid_for(R * 32, 256), 256, 0, s>>>(H, ldh, R, W, u, out);
+  MOSES_CUDA(cudaGetLastError());
+}
+void disc_ce(const double* z, long long m, long long n, double* out, cudaStream_t s) {
+  disc_ce_kernel<<<1, kFinBlock, 0, s>>>(z, m, n, out);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void head_scores(const float* part, int ntiles, long long ld, const float* hb, long long rows, float* s, cudaStream_t st) {
+  if (rows <= 0) return;
+  head_scores_kernel<<<grid_for(rows, 256), 256, 0, st>>>(part, ntiles, ld, hb, rows, s);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+int rank_splits(long long n) { return n <= 0 ? 1 : ceil_div(n, kRankChunk); }
+
+void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st) {
+  if (n <= 0) return;
+  dim3 grid(ceil_div(n, kRankBlock), ws.nsplit);
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, y, n, ws.gs_part, ws.loss_part, ws.pairs_part);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
+                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st) {
+  rank_finalize_kernel<<<1, kFinBlock, 0, st>>>(ws.gs_part, ws.loss_part, ws.pairs_part, ws.nsplit, n, roff, part2,
+                                                ntiles2, ld2, adv_bias, beta, out.loss, out.pairs, out.coefA, out.coefB,
+                                                out.ce);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st) {
+  if (R <= 0) return;
+  head_backward_kernel<T><<<grid_for(R * W, 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz, ldz);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, cudaStream_t st) {
+  column_dot_kernel<T><<<ceil_div(W + 1, 32), 256, 0, st>>>(coef, H, ldh, R, W, g);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
+                __nv_bfloat16* shadow, cudaStream_t st) {
+  const int grid = grid_for(P, 256);
+#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, shadow)
+  const bool k = mask != nullptr, s = shadow != nullptr;
+  if (momentum) {
+    if (k) { if (s) SGD_LAUNCH(true, true, true); else SGD_LAUNCH(true, true, false); }
+    else { if (s) SGD_LAUNCH(true, false, true); else SGD_LAUNCH(true, false, false); }
+  } else {
+    if (k) { if (s) SGD_LAUNCH(false, true, true); else SGD_LAUNCH(false, true, false); }
+    else { if (s) SGD_LAUNCH(false, false, true); else SGD_LAUNCH(false, false, false); }
+  }
+#undef SGD_LAUNCH
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void adam_update(float* w, float* m1, float* m2, const float* g, const uint8_t* mask, long long P, float lr, float b1,
+                 float b2, float eps, float c1, float c2, __nv_bfloat16* shadow, cudaStream_t st) {
+  const int grid = grid_for(P, 256);
+  if (shadow) adam_kernel<true><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, shadow);
+  else adam_kernel<false><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, shadow);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void variant_decay(float* w, const uint8_t* mask, long long P, float factor, __nv_bfloat16* shadow, cudaStream_t st) {
+  const int grid = grid_for(P, 256);
+  if (shadow) decay_kernel<true><<<grid, 256, 0, st>>>(w, mask, P, factor, shadow);
+  else decay_kernel<false><<<grid, 256, 0, st>>>(w, mask, P, factor, shadow);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+// ---- select workspace
+static long long sel_chunk(long long n, int* grid) {
+  const long long target = kSMs * 4;
+  long long chunk = (n + target - 1) / target;
+  chunk = round_up(chunk < 1 ? 1 : chunk, kSelBlock * 4);
+  *grid = int((n + chunk - 1) / chunk);
+  if (*grid < 1) *grid = 1;
+  return chunk;
+}
+size_t select_ws_bytes(long long n, int* grid_out) {
+  int grid;
+  sel_chunk(n, &grid);
+  if (grid_out) *grid_out = grid;
+  return size_t(n) * 4 + kBins * 4 + size_t(grid) * kBins * 4 + 256 + 64 + 1024;
+}
+void select_ws_carve(void* base, long long n, SelectWs* ws) {
+  int grid;
+  sel_chunk(n, &grid);
+  uint8_t* p = static_cast<uint8_t*>(base);
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p;
+    p += round_up(bytes, 256);
+    return r;
+  };
+  ws->state = reinterpret_cast<unsigned*>(take(sizeof(SelState)));
+  ws->counter = reinterpret_cast<unsigned long long*>(take(64));
+  ws->hist = reinterpret_cast<unsigned*>(take(kBins * 4));
+  ws->block_hist = reinterpret_cast<unsigned*>(take(size_t(grid) * kBins * 4));
+  ws->keys = reinterpret_cast<unsigned*>(take(size_t(n) * 4));
+  ws->grid = grid;
+}
+
+// Runs the three histogram passes; the first one is fused with key production (MODE).
+template <int MODE>
+static void radix_select_passes(const float* a, const float* b, long long n, unsigned long long need, const SelectWs& ws,
+                                float* xi_out, cudaStream_t st) {
+  int grid;
+  const long long chunk = sel_chunk(n, &grid);
+  SelState* S = reinterpret_cast<SelState*>(ws.state);
+  sel_init_kernel<<<1, 256, 0, st>>>(S, need, ws.hist);
+  for (int p = 0; p < 3; ++p) {
+    const bool last = p == 2;
+    if (p == 0) {
+      radix_hist_kernel<MODE, false><<<grid, kSelBlock, 0, st>>>(a, b, ws.keys, xi_out, n, chunk, S, kPassShift[p],
+                                                                 kPassBits[p], ws.hist, ws.block_hist);
+    } else if (last) {
+      radix_hist_kernel<0, true><<<grid, kSelBlock, 0, st>>>(a, b, ws.keys, nullptr, n, chunk, S, kPassShift[p],
+                                                             kPassBits[p], ws.hist, ws.block_hist);
+    } else {
+      radix_hist_kernel<0, false><<<grid, kSelBlock, 0, st>>>(a, b, ws.keys, nullptr, n, chunk, S, kPassShift[p],
+                                                              kPassBits[p], ws.hist, ws.block_hist);
+    }
+    radix_pick_kernel<<<1, kPickBlock, 0, st>>>(S, ws.hist, kPassShift[p], kPassBits[p]);
+  }
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void lottery_select(const float* w, const float* g, long long n, int mode, float theta, long long keep, const SelectWs& ws,
+                    uint8_t* mask_out, float* xi_out, bool normalize_xi, cudaStream_t st) {
+  int grid;
+  const long long chunk = sel_chunk(n, &grid);
+  SelState* S = reinterpret_cast<SelState*>(ws.state);
+  if (mode == 1) {
+    // threshold: xi + max in one pass, then the strict comparison on xi/max
+    sel_init_kernel<<<1, 256, 0, st>>>(S, 0, ws.hist);
+    radix_hist_kernel<1, false><<<grid, kSelBlock, 0, st>>>(w, g, ws.keys, nullptr, n, chunk, S, 31, 1, ws.hist,
+                                                            ws.block_hist);
+    threshold_mask_kernel<<<grid_for(n, kSelBlock), kSelBlock, 0, st>>>(ws.keys, n, S, theta, true, mask_out, xi_out);
+  } else {
+    radix_select_passes<1>(w, g, n, (unsigned long long)keep, ws, xi_out, st);
+    radix_apply_kernel<0><<<grid, kSelBlock, 0, st>>>(ws.keys, n, chunk, S, ws.block_hist, mask_out, nullptr, nullptr,
+                                                      nullptr);
+    if (xi_out && normalize_xi) xi_normalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(xi_out, n, S);
+  }
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void xi_scores(const float* w, const float* g, long long n, bool normalize, const SelectWs& ws, float* xi_out,
+               cudaStream_t st) {
+  int grid;
+  const long long chunk = sel_chunk(n, &grid);
+  SelState* S = reinterpret_cast<SelState*>(ws.state);
+  sel_init_kernel<<<1, 256, 0, st>>>(S, 0, ws.hist);
+  radix_hist_kernel<1, false><<<grid, kSelBlock, 0, st>>>(w, g, ws.keys, xi_out, n, chunk, S, 31, 1, ws.hist,
+                                                          ws.block_hist);
+  if (normalize) xi_normalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(xi_out, n, S);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+__global__ void keys_from_xi_kernel(const float* xi, long long n, unsigned* keys) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    keys[i] = __float_as_uint(xi[i]);
+}
+
+void partition_from_xi(const float* xi, long long n, int mode, float theta, long long keep, const SelectWs& ws,
+                       uint8_t* mask_out, cudaStream_t st) {
+  int grid;
+  const long long chunk = sel_chunk(n, &grid);
+  SelState* S = reinterpret_cast<SelState*>(ws.state);
+  if (mode == 1) {
+    sel_init_kernel<<<1, 256, 0, st>>>(S, 0, ws.hist);
+    keys_from_xi_kernel<<<grid_for(n, 256), 256, 0, st>>>(xi, n, ws.keys);
+    threshold_mask_kernel<<<grid_for(n, kSelBlock), kSelBlock, 0, st>>>(ws.keys, n, S, theta, false, mask_out, nullptr);
+  } else {
+    keys_from_xi_kernel<<<grid_for(n, 256), 256, 0, st>>>(xi, n, ws.keys);
+    radix_select_passes<0>(nullptr, nullptr, n, (unsigned long long)keep, ws, nullptr, st);
+    radix_apply_kernel<0><<<grid, kSelBlock, 0, st>>>(ws.keys, n, chunk, S, ws.block_hist, mask_out, nullptr, nullptr,
+                                                      nullptr);
+  }
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void lottery_apply(float* w, const float* g, const uint8_t* mask, long long n, float alpha, float factor, bool step,
+                   bool decay, __nv_bfloat16* shadow, cudaStream_t st) {
+  const int grid = grid_for(n, 256);
+  if (shadow) lottery_apply_kernel<true><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, shadow);
+  else lottery_apply_kernel<false><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, shadow);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+long long popcount_mask(const uint8_t* mask, long long n, unsigned long long* dcount, cudaStream_t st) {
+  MOSES_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), st));
+  popcount_kernel<<<grid_for(n, kSelBlock), kSelBlock, 0, st>>>(mask, n, dcount);
+  MOSES_CUDA(cudaGetLastError());
+  unsigned long long h = 0;
+  MOSES_CUDA(cudaMemcpyAsync(&h, dcount, sizeof(h), cudaMemcpyDeviceToHost, st));
+  MOSES_CUDA(cudaStreamSynchronize(st));
+  return (long long)h;
+}
+
+void topk_select(const float* scores, long long n, long long k, const SelectWs& ws, unsigned* out_key, long long* out_idx,
+                 cudaStream_t st) {
+  if (k > kTopkMax) fail(MOSES_ERR_INVALID_ARG, "top-k supports k <= 4096");
+  int grid;
+  const long long chunk = sel_chunk(n, &grid);
+  SelState* S = reinterpret_cast<SelState*>(ws.state);
+  radix_select_passes<2>(scores, nullptr, n, (unsigned long long)k, ws, nullptr, st);
+  MOSES_CUDA(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned long long), st));
+  radix_apply_kernel<1><<<grid, kSelBlock, 0, st>>>(ws.keys, n, chunk, S, ws.block_hist, nullptr, out_key, out_idx,
+                                                    ws.counter);
+  topk_sort_kernel<<<1, kSortBlock, 0, st>>>(out_key, out_idx, ws.counter, k);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void accuracy_counts(const float* s, const float* y, const long long* seg_of_row, const long long* seg_off, long long n,
+                     long long*, long long*, unsigned long long* totals, cudaStream_t st) {
+  MOSES_CUDA(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), st));
+  if (n <= 0) return;
+  accuracy_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, y, seg_of_row, seg_off, n, totals);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, long long ldh, long long m, long long n,
+                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st) {
+  float* dz = ws;                                   // [m+n]
+  float* du = ws + round_up(m + n, 64);             // [W+1]
+  double* dc = reinterpret_cast<double*>(du + round_up(W + 1, 64));
+  adv_logits_kernel<<<1, kFinBlock, 0, st>>>(part2, ntiles, ld2, m, n, c, dz, loss_out, dc);
+  column_dot_kernel<T><<<ceil_div(W + 1, 32), 256, 0, st>>>(dz, H, ldh, m + n, W, du);
+  adv_update_kernel<<<ceil_div(W, 256), 256, 0, st>>>(u, c, du, W, eta, dc);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+void segment_sum(const T* H, long long ldh, int W, const long long* offsets, long long programs, float* out, long long ldo,
+                 cudaStream_t st) {
+  if (programs <= 0) return;
+  if ((W * sizeof(T)) % 16 != 0 || (ldh * sizeof(T)) % 16 != 0) fail(MOSES_ERR_INVALID_ARG, "segment_sum needs 16-byte rows");
+  const int warps_per_block = 8;
+  long long blocks = (programs + warps_per_block - 1) / warps_per_block;
+  if (blocks > kSMs * 16) blocks = kSMs * 16;
+  segment_sum_kernel<T><<<int(blocks), warps_per_block * 32, 0, st>>>(H, ldh, W, offsets, programs, out, ldo);
+  MOSES_CUDA(cudaGetLastError());
+}
+void segment_sum_scalar(const float* v, const long long* offsets, long long programs, float bias, float* out,
+                        cudaStream_t st) {
+  if (programs <= 0) return;
+  segment_sum_scalar_kernel<<<grid_for(programs, 256), 256, 0, st>>>(v, offsets, programs, bias, out);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+double mmd2(const float* xs, long long m, const float* xt, long long n, int W, float sigma, double* ws, cudaStream_t st) {
+  const float inv = 1.f / (2.f * sigma * sigma);
+  double sums[3];
+  const float* A[3] = {xs, xt, xs};
+  const float* B[3] = {xs, xt, xt};
+  const long long na[3] = {m, n, m}, nb[3] = {m, n, n};
+  for (int q = 0; q < 3; ++q) {
+    dim3 grid(ceil_div(na[q], kGT), ceil_div(nb[q], kGT));
+    gram_exp_kernel<<<grid, 256, 0, st>>>(A[q], na[q], B[q], nb[q], W, inv, ws + 8);
+    sum_partials_kernel<<<1, 1024, 0, st>>>(ws + 8, (long long)grid.x * grid.y, ws + q);
+  }
+  MOSES_CUDA(cudaGetLastError());
+  MOSES_CUDA(cudaMemcpyAsync(sums, ws, sizeof(sums), cudaMemcpyDeviceToHost, st));
+  MOSES_CUDA(cudaStreamSynchronize(st));
+  return sums[0] / (double(m) * double(m)) + sums[1] / (double(n) * double(n)) - 2.0 * sums[2] / (double(m) * double(n));
+}
+
+template <typename T>
+void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st) {
+  if (n <= 0) return;
+  synth_features_kernel<T><<<grid_for(n, 128, 32), 128, 0, st>>>(seed, row0, n, D, dst, ld);
+  MOSES_CUDA(cudaGetLastError());
+}
+void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st) {
+  if (n <= 0) return;
+  synth_labels_kernel<<<grid_for(n, 256), 256, 0, st>>>(seed, row0, n, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+#define INST(T)                                                                                                   \
+  template void pack_rows<T>(const double*, long long, int, T*, long long, cudaStream_t);                         \
+  template void pack_rows_f32<T>(const float*, long long, int, long long, T*, long long, cudaStream_t);           \
+  template void set_ones_column<T>(T*, long long, int, long long, cudaStream_t);                                  \
+  template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t);                       \
+  template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
+                                 long long, int, T*, long long, cudaStream_t);                                    \
+  template void column_dot<T>(const float*, const T*, long long, long long, int, float*, cudaStream_t);           \
+  template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \
+                                  float*, float*, float, double*, float*, cudaStream_t);                          \
+  template void segment_sum<T>(const T*, long long, int, const long long*, long long, float*, long long,          \
+                               cudaStream_t);                                                                     \
+  template void synth_features<T>(unsigned long long, long long, long long, int, T*, long long, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+#undef INST
+
+}  // namespace moses

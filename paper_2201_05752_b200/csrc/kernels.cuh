@@ -1,0 +1,114 @@
+// kernels.cuh — host-side launch wrappers for the non-GEMM kernels (kernels.cu).
+#pragma once
+#include "common.cuh"
+
+namespace moses {
+
+// ---- data movement
+template <typename T>
+void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s);
+template <typename T>
+void pack_rows_f32(const float* src_d, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s);
+template <typename T>
+void set_ones_column(T* act, long long rows, int col, long long ld, cudaStream_t s);
+template <typename T>
+void unpack_rows(const T* src, long long n, int W, long long ld, double* dst_d, cudaStream_t s);
+void f32_to_f64(const float* src, long long n, double* dst, cudaStream_t s);
+void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
+void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s);
+void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, long long ldd, cudaStream_t s);
+// out[r] = H[r] . u  (warp per row)
+void row_dot(const float* H, long long ldh, long long R, int W, const float* u, float* out, cudaStream_t s);
+// discriminator_cross_entropy (lottery.cpp:207-218) over z[0,m) source and z[m,m+n) target
+void disc_ce(const double* z, long long m, long long n, double* out, cudaStream_t s);
+
+// ---- scores / ranking (model.cpp:71-106)
+void head_scores(const float* part, int ntiles, long long ld, const float* head_bias, long long rows, float* s,
+                 cudaStream_t st);
+struct RankWs {
+  double* gs_part;
+  double* loss_part;
+  long long* pairs_part;
+  int nsplit;
+};
+int rank_splits(long long n);
+void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st);
+// Reduces the rank partials (fixed order), normalises by the pair count, folds in the
+// adversary's logits when `part2` is given (model.cpp:215-238), and emits per-row
+// backward coefficients coefA (ranking) / coefB (adversary) over all R = roff + n rows.
+struct FinalizeOut {
+  double* loss;       // [1]: rank loss + beta * -CE
+  long long* pairs;   // [1]
+  float* coefA;       // [R]
+  float* coefB;       // [R]
+  double* ce;         // [1] discriminator CE (adversary on)
+};
+void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
+                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st);
+// dZ_last[r][j] = (coefA[r]*wh[j] + coefB[r]*u[j]) * [H[r][j] > 0]
+template <typename T>
+void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st);
+// g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
+template <typename T>
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, cudaStream_t st);
+
+// ---- updates (model.cpp:263-296, lottery.cpp:92-120)
+void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
+                __nv_bfloat16* shadow, cudaStream_t st);
+void adam_update(float* w, float* m1, float* m2, const float* g, const uint8_t* mask, long long P, float lr, float b1,
+                 float b2, float eps, float c1, float c2, __nv_bfloat16* shadow, cudaStream_t st);
+void variant_decay(float* w, const uint8_t* mask, long long P, float factor, __nv_bfloat16* shadow, cudaStream_t st);
+
+// ---- lottery mask identification (lottery.cpp:35-90), fused with step + decay
+struct SelectWs {
+  unsigned* keys;       // [n]
+  unsigned* hist;       // [2048]
+  unsigned* block_hist; // [grid][2048]
+  unsigned* state;      // select state (device)
+  unsigned long long* counter;
+  int grid;
+};
+size_t select_ws_bytes(long long n, int* grid_out);
+void select_ws_carve(void* base, long long n, SelectWs* ws);
+// xi = |w*g| -> keys; mode 1 threshold (normalised, strict >), 2 ratio (top ceil(rho*n), ties by index).
+// do_step: transferable step (alpha) on kept scalars + variant decay (factor) on the rest.
+void lottery_select(const float* w_in, const float* g, long long n, int mode, float theta, long long keep,
+                    const SelectWs& ws, uint8_t* mask_out, float* xi_out, bool normalize_xi, cudaStream_t st);
+void lottery_apply(float* w, const float* g, const uint8_t* mask, long long n, float alpha, float factor, bool step,
+                   bool decay, __nv_bfloat16* shadow, cudaStream_t st);
+void xi_scores(const float* w, const float* g, long long n, bool normalize, const SelectWs& ws, float* xi_out,
+               cudaStream_t st);
+// mask from given xi (identical-input parity path)
+void partition_from_xi(const float* xi, long long n, int mode, float theta, long long keep, const SelectWs& ws,
+                       uint8_t* mask_out, cudaStream_t st);
+long long popcount_mask(const uint8_t* mask, long long n, unsigned long long* dcount, cudaStream_t st);
+
+// ---- candidate top-k (search.cpp:32-37): (score desc, index asc)
+void topk_select(const float* scores, long long n, long long k, const SelectWs& ws, unsigned* out_key, long long* out_idx,
+                 cudaStream_t st);
+constexpr long long kTopkMax = 4096;
+
+// ---- accuracy (model.cpp:298-312)
+void accuracy_counts(const float* s, const float* y, const long long* seg_of_row, const long long* seg_off, long long n,
+                     long long* pairs_part, long long* conc_part, unsigned long long* totals, cudaStream_t st);
+
+// ---- adversary (lottery.cpp:135-164)
+template <typename T>
+void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, long long ldh, long long m, long long n,
+                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st);
+
+// ---- extensions
+template <typename T>
+void segment_sum(const T* H, long long ldh, int W, const long long* offsets, long long programs, float* out,
+                 long long ldo, cudaStream_t st);
+void segment_sum_scalar(const float* v, const long long* offsets, long long programs, float bias, float* out,
+                        cudaStream_t st);
+double mmd2(const float* xs, long long m, const float* xt, long long n, int W, float sigma, double* ws, cudaStream_t st);
+
+// ---- synthetic TenSet-shaped data (bit-identical to oracle::synth_*)
+template <typename T>
+void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st);
+void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st);
+
+}  // namespace moses

@@ -1,0 +1,651 @@
+"""Python mirror of the reference's ``moseslab`` hot-path API over the C ABI.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/moseslab/{model,lottery,search}.hpp; every call
+goes through ``libmoses_gpu.so`` (include/moses_gpu.h). There is no CPU
+fallback: importing this module on a machine without the built library or a
+B200 raises.
+
+Value model: ``CostModelParams`` is the host value (dims + flat float64 params
++ momentum, the reference flat order). ``DeviceModel`` is a device handle; the
+free functions accept either and upload on demand, so reference-style code
+(`predict(params, features)`) works unchanged, while hot loops keep a
+``DeviceModel`` resident.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmoses_gpu.so")
+
+# moseslab::ErrorCode names (errors.hpp:157-186), indexed by ordinal
+ERROR_NAMES = [
+    "invalid-task", "invalid-config", "space-too-large", "immutable-space", "bad-dims",
+    "dim-mismatch", "shape-mismatch", "version-mismatch", "corrupt-stream", "empty-dataset",
+    "invalid-ratio", "unnormalized-threshold", "adversary-disabled", "unstable-decay",
+    "infeasible-split", "zero-mean", "insufficient-batches", "budget-infeasible",
+    "missing-reference-strategy", "mismatched-runs", "empty-rows", "parse-error",
+    "missing-field", "io-error", "usage-error",
+]
+LIB_ERRORS = {100: "cuda-error", 101: "no-device", 102: "capacity", 103: "invalid-argument"}
+
+PREC_BF16, PREC_TF32 = 0, 1
+THRESHOLD, RATIO = 1, 2
+DTYPE_F32, DTYPE_BF16 = 0, 1
+
+
+class MosesError(RuntimeError):
+    """moseslab::Error equivalent: .code is the reference's error_code_name."""
+
+    def __init__(self, status: int, message: str):
+        if 1 <= status <= len(ERROR_NAMES):
+            self.code = ERROR_NAMES[status - 1]
+        else:
+            self.code = LIB_ERRORS.get(status, f"status-{status}")
+        self.status = status
+        super().__init__(f"{self.code}: {message}")
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library. Fails loudly if it is missing (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing; run `python -m paper_2201_05752_b200.build`")
+    L = C.CDLL(_LIB_PATH)
+    vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+    sig = {
+        "moses_last_error": (C.c_char_p, []),
+        "moses_version": (C.c_char_p, []),
+        "moses_kernel_launches": (i64, []),
+        "moses_device_check": (C.c_int, []),
+        "moses_param_count": (i64, [vp, i32]),
+        "moses_init_random": (C.c_int, [vp, i32, u64, i32, vp]),
+        "moses_model_create": (C.c_int, [vp, i32, i32, i64, vp]),
+        "moses_model_destroy": (C.c_int, [vp]),
+        "moses_model_upload": (C.c_int, [vp, vp, vp, i64]),
+        "moses_model_download": (C.c_int, [vp, vp, vp, i64]),
+        "moses_model_copy": (C.c_int, [vp, vp]),
+        "moses_model_synchronize": (C.c_int, [vp]),
+        "moses_packed_ld": (i64, [vp]),
+        "moses_predict": (C.c_int, [vp, vp, i64, i32, vp]),
+        "moses_penultimate": (C.c_int, [vp, vp, i64, i32, vp]),
+        "moses_predict_device": (C.c_int, [vp, vp, i32, i64, i64, vp]),
+        "moses_predict_pooled": (C.c_int, [vp, vp, i64, i32, vp, i64, vp]),
+        "moses_gradients": (C.c_int, [vp, vp, vp, i64, i32, vp, dbl, vp]),
+        "moses_gradients_download": (C.c_int, [vp, vp, i64]),
+        "moses_gradients_upload": (C.c_int, [vp, vp, i64]),
+        "moses_objective": (C.c_int, [vp, vp, vp, i64, i32, vp, dbl, vp]),
+        "moses_apply_update": (C.c_int, [vp, dbl, dbl, vp, i64, i32]),
+        "moses_train_step": (C.c_int, [vp, vp, vp, i64, i32, dbl, dbl, vp]),
+        "moses_train_step_device": (C.c_int, [vp, vp, i64, vp, i64, dbl, dbl, vp]),
+        "moses_ranking_accuracy": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),
+        "moses_ranking_loss": (C.c_int, [vp, vp, i64, vp, vp]),
+        "moses_adam_update": (C.c_int, [vp, dbl, dbl, dbl, dbl, i32, vp, i64]),
+        "moses_xi_scores": (C.c_int, [vp, i32, vp, i64]),
+        "moses_partition": (C.c_int, [vp, i32, dbl, i32, vp, i64, vp]),
+        "moses_xi_upload": (C.c_int, [vp, vp, i64, i32]),
+        "moses_mask_upload": (C.c_int, [vp, vp, i64]),
+        "moses_transferable_step": (C.c_int, [vp, dbl]),
+        "moses_variant_decay": (C.c_int, [vp, dbl, dbl]),
+        "moses_lottery_step": (C.c_int, [vp, i32, dbl, i32, dbl, dbl, vp, i64, vp]),
+        "moses_adversary_create": (C.c_int, [vp, i64, i32, i32, dbl, vp]),
+        "moses_adversary_destroy": (C.c_int, [vp]),
+        "moses_adversary_get": (C.c_int, [vp, vp, i32, vp]),
+        "moses_adversary_set": (C.c_int, [vp, vp, i32, dbl]),
+        "moses_adversarial_term": (C.c_int, [vp, vp, i64, vp, i64, i32, dbl, vp, vp]),
+        "moses_adversarial_step": (C.c_int, [vp, vp, vp, i64, i32, dbl, vp, vp]),
+        "moses_discriminator_cross_entropy": (C.c_int, [vp, i64, vp, i64, vp]),
+        "moses_topk": (C.c_int, [vp, i64, i64, vp]),
+        "moses_topk_device": (C.c_int, [vp, i64, i64, vp]),
+        "moses_select_batch": (i64, [vp, i64, vp, i64, i64, vp]),
+        "moses_segment_sum": (C.c_int, [vp, i64, i32, vp, i64, vp]),
+        "moses_segment_sum_device": (C.c_int, [vp, i32, i64, i32, vp, i64, vp]),
+        "moses_mmd2": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp]),
+        "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
+        "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
+        "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),
+        "moses_deserialize": (C.c_int, [vp, i64, vp, vp, vp, i64]),
+        "moses_write_mask": (i64, [vp, i64, i32, i32, dbl, vp, i64]),
+        "moses_read_mask": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, vp]),
+        "moses_model_device_ptrs": (C.c_int, [vp, vp, vp, vp]),
+        "moses_model_stream": (C.c_int, [vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    return [n for n in lib().__dict__ if n.startswith("moses_")]
+
+
+def _ck(rc: int):
+    if rc != 0:
+        raise MosesError(rc, lib().moses_last_error().decode(errors="replace"))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dims(dims):
+    return np.ascontiguousarray(dims, dtype=np.int32)
+
+
+def kernel_launches() -> int:
+    return lib().moses_kernel_launches()
+
+
+# ---------------------------------------------------------------- values (model.hpp:19-48)
+@dataclass
+class CostModelParams:
+    dims: list
+    params: np.ndarray                # flat, reference order
+    momentum: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        self.params = _f64(self.params)
+        if self.momentum is None:
+            self.momentum = np.zeros_like(self.params)
+        self.momentum = _f64(self.momentum)
+
+    def copy(self):
+        return CostModelParams(list(self.dims), self.params.copy(), self.momentum.copy())
+
+    # views per level, reference shapes: w[l] is dims[l+1] x dims[l] (column-major storage)
+    def level_offset(self, l):
+        return int(sum(self.dims[k] * self.dims[k + 1] + self.dims[k + 1] for k in range(l)))
+
+    def w(self, l):
+        o, fi, fo = self.level_offset(l), self.dims[l], self.dims[l + 1]
+        return self.params[o:o + fi * fo].reshape(fi, fo).T
+
+    def b(self, l):
+        o, fi, fo = self.level_offset(l), self.dims[l], self.dims[l + 1]
+        return self.params[o + fi * fo:o + fi * fo + fo]
+
+
+@dataclass
+class TrainHyper:  # model.hpp:27-35
+    learning_rate: float = 0.001
+    weight_decay: float = 0.01
+    max_epochs: int = 30
+    batch_size: int = 512
+    momentum: float = 0.9
+    adversary_beta: float = 0.01
+    seed: int = 0
+
+
+@dataclass
+class RankingBatch:  # model.hpp:39-43
+    features: np.ndarray
+    labels: np.ndarray
+    task_id: str = ""
+
+
+@dataclass
+class XiScores:  # lottery.hpp:15-18
+    xi: np.ndarray
+    normalized: bool = False
+
+
+@dataclass
+class ParamMask:  # lottery.hpp:25-32
+    transferable: np.ndarray
+    phase: int = 0
+    mode: int = RATIO
+    value: float = 0.0
+
+    def popcount(self) -> int:
+        return int(np.count_nonzero(self.transferable))
+
+
+def param_count(dims) -> int:
+    d = _dims(dims)
+    n = lib().moses_param_count(_p(d), len(d))
+    if n < 0:
+        _ck(int(-n))
+    return int(n)
+
+
+def init_random(dims, seed: int, strict: bool = True) -> CostModelParams:
+    """model.cpp:147-167 (bit-exact keyed SplitMix64 draw order)."""
+    d = _dims(dims)
+    n = param_count(dims) if len(dims) >= 3 else 0
+    out = np.zeros(max(n, 1), dtype=np.float64)
+    _ck(lib().moses_init_random(_p(d), len(d), seed, int(strict), _p(out)))
+    return CostModelParams(list(dims), out[:n])
+
+
+# ---------------------------------------------------------------- device handles
+class DeviceModel:
+    """Device-resident cost model (one CUDA stream + workspaces per handle)."""
+
+    def __init__(self, params: CostModelParams, precision: int = PREC_TF32, max_rows: int = 4096):
+        self.dims = list(params.dims)
+        d = _dims(self.dims)
+        h = C.c_void_p()
+        _ck(lib().moses_model_create(_p(d), len(d), precision, max_rows, C.byref(h)))
+        self.h = h
+        self.precision = precision
+        self.P = param_count(self.dims)
+        self.upload(params)
+
+    def upload(self, params: CostModelParams):
+        _ck(lib().moses_model_upload(self.h, _p(params.params), _p(params.momentum), self.P))
+
+    def download(self) -> CostModelParams:
+        w = np.zeros(self.P)
+        m = np.zeros(self.P)
+        _ck(lib().moses_model_download(self.h, _p(w), _p(m), self.P))
+        return CostModelParams(list(self.dims), w, m)
+
+    def gradients(self) -> np.ndarray:
+        g = np.zeros(self.P)
+        _ck(lib().moses_gradients_download(self.h, _p(g), self.P))
+        return g
+
+    def set_gradients(self, g):
+        g = _f64(g)
+        _ck(lib().moses_gradients_upload(self.h, _p(g), self.P))
+
+    @property
+    def packed_ld(self) -> int:
+        return int(lib().moses_packed_ld(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().moses_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _as_device(model, precision=PREC_TF32, rows=4096):
+    if isinstance(model, DeviceModel):
+        return model, False
+    return DeviceModel(model, precision, max(rows, 1)), True
+
+
+class AdversaryState:
+    """lottery.hpp:36-42 — logistic discriminator + frozen replay rows (device)."""
+
+    def __init__(self, replay_features, penultimate_dim: int, seed: int = 0, step_size: float = 0.1):
+        r = _f64(replay_features)
+        if r.ndim != 2:
+            r = r.reshape(0, 0) if r.size == 0 else r
+        h = C.c_void_p()
+        _ck(lib().moses_adversary_create(_p(r), r.shape[0], r.shape[1] if r.ndim == 2 else 0, penultimate_dim,
+                                         step_size, C.byref(h)))
+        self.h = h
+        self.width = penultimate_dim
+        self.replay_features = r
+        self.step_size = step_size
+        self.seed = seed
+
+    @property
+    def weight(self):
+        w = np.zeros(self.width)
+        b = C.c_double()
+        _ck(lib().moses_adversary_get(self.h, _p(w), self.width, C.byref(b)))
+        return w
+
+    @property
+    def bias(self):
+        w = np.zeros(self.width)
+        b = C.c_double()
+        _ck(lib().moses_adversary_get(self.h, _p(w), self.width, C.byref(b)))
+        return b.value
+
+    def set(self, weight, bias):
+        w = _f64(weight)
+        _ck(lib().moses_adversary_set(self.h, _p(w), self.width, float(bias)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().moses_adversary_destroy(self.h)
+        except Exception:
+            pass
+
+
+def make_adversary(replay_features, penultimate_dim, seed=0, step_size=0.1) -> AdversaryState:
+    """lottery.cpp:166-180"""
+    return AdversaryState(replay_features, penultimate_dim, seed, step_size)
+
+
+# ---------------------------------------------------------------- model.hpp functions
+def predict(model, features) -> np.ndarray:
+    """model.cpp:169-175"""
+    x = _f64(features)
+    n, D = x.shape
+    dm, tmp = _as_device(model, rows=n)
+    out = np.zeros(n)
+    try:
+        _ck(lib().moses_predict(dm.h, _p(x), n, D, _p(out)))
+    finally:
+        if tmp:
+            dm.close()
+    return out
+
+
+def penultimate_activations(model, features) -> np.ndarray:
+    """model.cpp:177-183"""
+    x = _f64(features)
+    n, D = x.shape
+    dm, tmp = _as_device(model, rows=n)
+    out = np.zeros((n, dm.dims[-2]))
+    try:
+        _ck(lib().moses_penultimate(dm.h, _p(x), n, D, _p(out)))
+    finally:
+        if tmp:
+            dm.close()
+    return out
+
+
+def predict_pooled(model, stmt_features, offsets) -> np.ndarray:
+    x = _f64(stmt_features)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    dm, tmp = _as_device(model, rows=x.shape[0])
+    out = np.zeros(len(off) - 1)
+    try:
+        _ck(lib().moses_predict_pooled(dm.h, _p(x), x.shape[0], x.shape[1], _p(off), len(off) - 1, _p(out)))
+    finally:
+        if tmp:
+            dm.close()
+    return out
+
+
+def pairwise_ranking_loss(scores, labels) -> float:
+    """model.cpp:185-190"""
+    s, y = _f64(scores), _f64(labels)
+    if s.shape != y.shape:
+        raise MosesError(6, "scores/labels length mismatch")
+    loss = C.c_double()
+    pairs = C.c_int64()
+    _ck(lib().moses_ranking_loss(_p(s), _p(y), len(s), C.byref(loss), C.byref(pairs)))
+    return loss.value
+
+
+def gradients(model, batch: RankingBatch, adversary: Optional[AdversaryState] = None, beta: float = 0.0,
+              want_loss: bool = False):
+    """model.cpp:192-244. Returns the flat gradient (and the loss when want_loss)."""
+    x, y = _f64(batch.features), _f64(batch.labels)
+    n = x.shape[0]
+    D = x.shape[1] if x.ndim == 2 else 0
+    if y.shape[0] != n:
+        raise MosesError(6, "batch rows != label count")
+    rows = n + (adversary.replay_features.shape[0] if adversary is not None else 0)
+    dm, tmp = _as_device(model, rows=rows)
+    loss = C.c_double()
+    try:
+        _ck(lib().moses_gradients(dm.h, _p(x), _p(y), n, D, adversary.h if adversary else None, beta,
+                                  C.byref(loss)))
+        g = dm.gradients()
+    finally:
+        if tmp:
+            dm.close()
+    return (g, loss.value) if want_loss else g
+
+
+def objective(model, batch: RankingBatch, adversary=None, beta=0.0) -> float:
+    """model.cpp:246-261"""
+    x, y = _f64(batch.features), _f64(batch.labels)
+    rows = x.shape[0] + (adversary.replay_features.shape[0] if adversary is not None else 0)
+    dm, tmp = _as_device(model, rows=rows)
+    out = C.c_double()
+    try:
+        _ck(lib().moses_objective(dm.h, _p(x), _p(y), x.shape[0], x.shape[1], adversary.h if adversary else None,
+                                  beta, C.byref(out)))
+    finally:
+        if tmp:
+            dm.close()
+    return out.value
+
+
+def apply_update(model: DeviceModel, hyper: TrainHyper = TrainHyper(), mask: Optional[ParamMask] = None,
+                 use_momentum: bool = False, grads=None):
+    """model.cpp:263-296 on the handle (uses its device gradients unless `grads` is given)."""
+    if grads is not None:
+        model.set_gradients(grads)
+    m = None if mask is None else np.ascontiguousarray(mask.transferable, dtype=np.uint8)
+    _ck(lib().moses_apply_update(model.h, hyper.learning_rate, hyper.momentum, _p(m), 0 if m is None else len(m),
+                                 int(use_momentum)))
+
+
+def ranking_accuracy(model, batches: Sequence[RankingBatch]) -> float:
+    """model.cpp:298-312"""
+    if not batches:
+        return 0.0
+    x = np.concatenate([_f64(b.features) for b in batches])
+    y = np.concatenate([_f64(b.labels) for b in batches])
+    off = np.zeros(len(batches) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(b.labels) for b in batches])
+    dm, tmp = _as_device(model, rows=4096)
+    acc = C.c_double()
+    pairs = C.c_int64()
+    conc = C.c_int64()
+    try:
+        _ck(lib().moses_ranking_accuracy(dm.h, _p(x), _p(y), _p(off), len(batches), x.shape[1], C.byref(acc),
+                                         C.byref(pairs), C.byref(conc)))
+    finally:
+        if tmp:
+            dm.close()
+    return acc.value
+
+
+# ---------------------------------------------------------------- lottery.hpp functions
+def xi_scores(model: DeviceModel, normalize: bool, grads=None) -> XiScores:
+    """lottery.cpp:35-57 (with the handle's params and device gradients)."""
+    if grads is not None:
+        model.set_gradients(grads)
+    out = np.zeros(model.P)
+    _ck(lib().moses_xi_scores(model.h, int(normalize), _p(out), model.P))
+    return XiScores(out, normalize)
+
+
+def partition(model: DeviceModel, xi: Optional[XiScores], mode: int, value: float, phase: int) -> ParamMask:
+    """lottery.cpp:59-90. If `xi` is given it is uploaded (identical-input parity path)."""
+    if xi is not None:
+        x = _f64(xi.xi)
+        if len(x) == 0:
+            raise MosesError(7, "empty score array")
+        _ck(lib().moses_xi_upload(model.h, _p(x), len(x), int(xi.normalized)))
+    out = np.zeros(model.P, dtype=np.uint8)
+    pop = C.c_int64()
+    _ck(lib().moses_partition(model.h, mode, value, phase, _p(out), model.P, C.byref(pop)))
+    return ParamMask(out.astype(bool), phase, mode, value)
+
+
+def transferable_step(model: DeviceModel, mask: Optional[ParamMask], alpha: float, grads=None):
+    """lottery.cpp:92-97"""
+    if grads is not None:
+        model.set_gradients(grads)
+    if mask is not None:
+        m = np.ascontiguousarray(mask.transferable, dtype=np.uint8)
+        _ck(lib().moses_mask_upload(model.h, _p(m), len(m)))
+    _ck(lib().moses_transferable_step(model.h, alpha))
+
+
+def variant_decay(model: DeviceModel, mask: Optional[ParamMask], alpha: float, lam: float):
+    """lottery.cpp:99-120"""
+    if mask is not None:
+        m = np.ascontiguousarray(mask.transferable, dtype=np.uint8)
+        _ck(lib().moses_mask_upload(model.h, _p(m), len(m)))
+    _ck(lib().moses_variant_decay(model.h, alpha, lam))
+
+
+def lottery_step(model: DeviceModel, mode: int, value: float, phase: int, alpha: float, lam: float) -> ParamMask:
+    """tuner.cpp:258-262 fused: xi -> partition -> transferable_step -> variant_decay."""
+    out = np.zeros(model.P, dtype=np.uint8)
+    pop = C.c_int64()
+    _ck(lib().moses_lottery_step(model.h, mode, value, phase, alpha, lam, _p(out), model.P, C.byref(pop)))
+    return ParamMask(out.astype(bool), phase, mode, value)
+
+
+def discriminator_cross_entropy(z_source, z_target) -> float:
+    """lottery.cpp:207-218"""
+    zs, zt = _f64(z_source), _f64(z_target)
+    out = C.c_double()
+    _ck(lib().moses_discriminator_cross_entropy(_p(zs), len(zs), _p(zt), len(zt), C.byref(out)))
+    return out.value
+
+
+@dataclass
+class AdversarialResult:
+    discriminator_loss: float = 0.0
+    confusion_contribution: float = 0.0
+
+
+def adversarial_term(adversary: AdversaryState, hidden_source, hidden_target, beta: float) -> AdversarialResult:
+    """lottery.cpp:135-164"""
+    hs, ht = _f64(hidden_source), _f64(hidden_target)
+    ms = hs.shape[0] if hs.ndim == 2 else 0
+    nt = ht.shape[0] if ht.ndim == 2 else 0
+    width = hs.shape[1] if hs.ndim == 2 and ms else (ht.shape[1] if ht.ndim == 2 and nt else adversary.width)
+    if ht.ndim == 2 and nt and ht.shape[1] != width:
+        raise MosesError(6, "activation width != discriminator width")
+    dl, cf = C.c_double(), C.c_double()
+    _ck(lib().moses_adversarial_term(adversary.h, _p(hs), ms, _p(ht), nt, width, beta, C.byref(dl), C.byref(cf)))
+    return AdversarialResult(dl.value, cf.value)
+
+
+def adversarial_step(adversary: AdversaryState, model: DeviceModel, target_features, beta: float):
+    """tuner.cpp:252-256: penultimate activations of replay + target under the current params, then the step."""
+    x = _f64(target_features)
+    dl, cf = C.c_double(), C.c_double()
+    _ck(lib().moses_adversarial_step(adversary.h, model.h, _p(x), x.shape[0], x.shape[1], beta, C.byref(dl),
+                                     C.byref(cf)))
+    return AdversarialResult(dl.value, cf.value)
+
+
+# ---------------------------------------------------------------- search.hpp
+def topk(scores, k: int) -> np.ndarray:
+    """(score desc, index asc) order of search.cpp:32-37 over a candidate pool."""
+    s = _f64(scores)
+    k = min(int(k), len(s))
+    out = np.zeros(max(k, 1), dtype=np.int64)
+    _ck(lib().moses_topk(_p(s), len(s), k, _p(out)))
+    return out[:k]
+
+
+def select_batch(ordered_hashes, already_measured, batch_size: int) -> np.ndarray:
+    """search.cpp:82-95 over a score-ordered list of config hashes: returns positions kept."""
+    h = np.ascontiguousarray(ordered_hashes, dtype=np.uint64)
+    m = np.ascontiguousarray(sorted(already_measured), dtype=np.uint64)
+    out = np.zeros(max(int(batch_size), 1), dtype=np.int64)
+    n = lib().moses_select_batch(_p(h), len(h), _p(m) if len(m) else None, len(m), batch_size, _p(out))
+    if n < 0:
+        _ck(int(-n))
+    return out[:n]
+
+
+# ---------------------------------------------------------------- extensions
+def segment_sum(h, offsets) -> np.ndarray:
+    h = _f64(h)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = np.zeros((len(off) - 1, h.shape[1]))
+    _ck(lib().moses_segment_sum(_p(h), h.shape[0], h.shape[1], _p(off), len(off) - 1, _p(out)))
+    return out
+
+
+def mmd2(xs, xt, sigma: float) -> float:
+    xs, xt = _f64(xs), _f64(xt)
+    out = C.c_double()
+    _ck(lib().moses_mmd2(_p(xs), xs.shape[0], _p(xt), xt.shape[0], xs.shape[1], sigma, C.byref(out)))
+    return out.value
+
+
+def adam_update(model: DeviceModel, lr, b1=0.9, b2=0.999, eps=1e-8, step=1, mask: Optional[ParamMask] = None):
+    m = None if mask is None else np.ascontiguousarray(mask.transferable, dtype=np.uint8)
+    _ck(lib().moses_adam_update(model.h, lr, b1, b2, eps, step, _p(m), 0 if m is None else len(m)))
+
+
+# ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:267-325)
+def serialize(params: CostModelParams) -> bytes:
+    d = _dims(params.dims)
+    n = lib().moses_serialize(_p(d), len(d), _p(params.params), _p(params.momentum), None, 0)
+    if n < 0:
+        _ck(int(-n))
+    buf = (C.c_uint8 * n)()
+    lib().moses_serialize(_p(d), len(d), _p(params.params), _p(params.momentum), C.addressof(buf), n)
+    return bytes(buf)
+
+
+def deserialize(blob: bytes) -> CostModelParams:
+    b = np.frombuffer(blob, dtype=np.uint8)
+    dims = np.zeros(4, dtype=np.int32)
+    cap = max((len(blob) - 12) // 16, 1)
+    w = np.zeros(cap)
+    m = np.zeros(cap)
+    _ck(lib().moses_deserialize(_p(b) if len(b) else None, len(b), _p(dims), _p(w), _p(m), cap))
+    return CostModelParams([int(v) for v in dims], w, m)
+
+
+def save_model(params: CostModelParams, path: str):
+    blob = serialize(params)
+    try:
+        with open(path, "wb") as f:
+            f.write(blob)
+    except OSError as e:
+        raise MosesError(24, f"cannot open {path} for writing") from e
+
+
+def load_model(path: str) -> CostModelParams:
+    try:
+        with open(path, "rb") as f:
+            blob = f.read()
+    except OSError as e:
+        raise MosesError(24, f"cannot open model file {path}") from e
+    return deserialize(blob)
+
+
+def write_mask(mask: ParamMask, path: str):
+    m = np.ascontiguousarray(mask.transferable, dtype=np.uint8)
+    n = lib().moses_write_mask(_p(m), len(m), mask.phase, mask.mode, mask.value, None, 0)
+    buf = (C.c_uint8 * n)()
+    lib().moses_write_mask(_p(m), len(m), mask.phase, mask.mode, mask.value, C.addressof(buf), n)
+    try:
+        with open(path, "wb") as f:
+            f.write(bytes(buf))
+    except OSError as e:
+        raise MosesError(24, f"cannot open {path} for writing") from e
+
+
+def read_mask(path: str) -> ParamMask:
+    try:
+        with open(path, "rb") as f:
+            blob = f.read()
+    except OSError as e:
+        raise MosesError(24, f"cannot open mask file {path}") from e
+    b = np.frombuffer(blob, dtype=np.uint8)
+    n = C.c_int64()
+    ph = C.c_int32()
+    mo = C.c_int32()
+    val = C.c_double()
+    _ck(lib().moses_read_mask(_p(b), len(b), None, 0, C.byref(n), C.byref(ph), C.byref(mo), C.byref(val)))
+    out = np.zeros(n.value, dtype=np.uint8)
+    _ck(lib().moses_read_mask(_p(b), len(b), _p(out), len(out), C.byref(n), C.byref(ph), C.byref(mo),
+                              C.byref(val)))
+    return ParamMask(out.astype(bool), ph.value, mo.value, val.value)

@@ -1,0 +1,496 @@
+"""Parity of the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances (north star): tensor-core TF32/bf16 GEMM stages <= 1e-3 normwise
+relative (max |d| / max |ref|); masks, top-k indices, popcounts, accuracy counts
+bit-exact on identical inputs in identical precision (fp32 on both sides).
+bf16 mode is the throughput mode: its error is measured and bounded looser.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_TF32 = 1e-3
+TOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def ml():
+    from paper_2201_05752_b200 import moseslab
+
+    assert moseslab.lib().moses_device_check() == 0, moseslab.lib().moses_last_error()
+    return moseslab
+
+
+def nrel(got, ref):
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def rows(n, d, seed):
+    return np.random.default_rng(seed).random((n, d))
+
+
+def labels(n, seed):
+    return 0.1 + np.random.default_rng(seed).random(n)
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------- forward
+def test_golden_model_predictions(ml):
+    p = ml.init_random([16, 512, 512, 1], 12345)
+    x = np.array([[(r + 1) * 0.1 + c * 0.01 for c in range(16)] for r in range(3)])
+    want = [0.068432722090836534, 0.10419522897402726, 0.14194361818494705]
+    for prec, tol in ((ml.PREC_TF32, TOL_TF32), (ml.PREC_BF16, TOL_BF16)):
+        dm = ml.DeviceModel(p, prec, 128)
+        assert nrel(ml.predict(dm, x), want) < tol
+
+
+@pytest.mark.parametrize("dims", [[4, 8, 8, 1], [16, 512, 512, 1], [164, 256, 256, 1], [164, 512, 512, 1],
+                                  [164, 512, 512, 512, 512, 1], [33, 72, 40, 1]])
+@pytest.mark.parametrize("n", [1, 5, 300])
+def test_predict_vs_oracle(ml, orc, dims, n):
+    p = ml.init_random(dims, 11, strict=False)
+    x = rows(n, dims[0], n)
+    ref, h_ref = orc.forward(dims, p.params, x)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 512)
+    assert nrel(ml.predict(dm, x), ref) < TOL_TF32
+    assert nrel(ml.penultimate_activations(dm, x), h_ref) < TOL_TF32
+    db = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    assert nrel(ml.predict(db, x), ref) < TOL_BF16
+
+
+def test_predict_large_chunked(ml, orc):
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 5)
+    x = rows(5000, 164, 1)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 1024)  # forces 5 chunks
+    ref, _ = orc.forward(dims, p.params, x, threads=8)
+    assert nrel(ml.predict(dm, x), ref) < TOL_TF32
+
+
+def test_predict_rejects_wrong_width(ml):
+    dm = ml.DeviceModel(ml.init_random([4, 8, 8, 1], 3), ml.PREC_TF32, 16)
+    with pytest.raises(ml.MosesError) as e:
+        ml.predict(dm, rows(2, 5, 0))
+    assert e.value.code == "dim-mismatch"
+
+
+def test_predict_purity_duplicate_rows(ml):
+    dm = ml.DeviceModel(ml.init_random([4, 8, 8, 1], 2), ml.PREC_TF32, 16)
+    x = rows(2, 4, 9)
+    x[1] = x[0]
+    s = ml.predict(dm, x)
+    assert s[0] == s[1]
+
+
+def test_pooled_predict_reduces_to_predict_and_matches_oracle(ml, orc):
+    dims = [164, 256, 256, 1]
+    p = ml.init_random(dims, 4)
+    off = orc.synth_offsets(3, 200, 8)
+    x = rows(int(off[-1]), 164, 2)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 1024)
+    got = ml.predict_pooled(dm, x, off)
+    _, h = orc.forward(dims, p.params, x)
+    pooled = orc.segment_sum(h, off)
+    ref = pooled @ p.params[-257:-1] + p.params[-1]
+    assert nrel(got, ref) < TOL_TF32
+    # all segments of length 1 == predict
+    one = np.arange(41, dtype=np.int64)
+    assert nrel(ml.predict_pooled(dm, x[:40], one), ml.predict(dm, x[:40])) < 1e-6
+
+
+# ---------------------------------------------------------------- gradients
+@pytest.mark.parametrize("dims", [[4, 8, 8, 1], [16, 512, 512, 1], [164, 256, 256, 1],
+                                  [164, 512, 512, 512, 512, 1]])
+@pytest.mark.parametrize("n", [2, 12, 512])
+def test_gradients_vs_oracle(ml, orc, dims, n):
+    p = ml.init_random(dims, 21, strict=False)
+    x, y = rows(n, dims[0], 7), labels(n, 8)
+    g_ref, loss_ref = orc.gradients(dims, p.params, x, y)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 1024)
+    g, loss = ml.gradients(dm, ml.RankingBatch(x, y), want_loss=True)
+    assert nrel(g, g_ref) < TOL_TF32
+    assert abs(loss - loss_ref) <= TOL_TF32 * max(1.0, abs(loss_ref))
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.01, 0.5])
+def test_gradients_with_adversary(ml, orc, beta):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 31)
+    x, y = rows(12, 16, 1), labels(12, 2)
+    replay = rows(256, 16, 3)
+    u = np.random.default_rng(4).normal(0, 0.05, 512)
+    c = 0.03
+    g_ref, loss_ref = orc.gradients(dims, p.params, x, y, (u, c, replay), beta)
+    adv = ml.make_adversary(replay, 512, 7)
+    adv.set(u, c)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 512)
+    g, loss = ml.gradients(dm, ml.RankingBatch(x, y), adv, beta, want_loss=True)
+    assert nrel(g, g_ref) < TOL_TF32
+    assert abs(loss - loss_ref) <= TOL_TF32 * max(1.0, abs(loss_ref))
+    if beta == 0.0:  # model.cpp:213-215: adversary-free gradient bit-for-bit
+        g0 = ml.gradients(dm, ml.RankingBatch(x, y))
+        assert np.array_equal(g, g0)
+
+
+def test_gradients_pair_free_and_empty(ml):
+    dm = ml.DeviceModel(ml.init_random([4, 8, 8, 1], 7), ml.PREC_TF32, 16)
+    g = ml.gradients(dm, ml.RankingBatch(rows(4, 4, 20), np.ones(4)))
+    assert np.all(g == 0)
+    g = ml.gradients(dm, ml.RankingBatch(np.zeros((0, 4)), np.zeros(0)))
+    assert np.all(g == 0)
+
+
+def test_gradients_deterministic(ml):
+    dm = ml.DeviceModel(ml.init_random([164, 512, 512, 1], 1), ml.PREC_BF16, 1024)
+    b = ml.RankingBatch(rows(1000, 164, 5), labels(1000, 6))
+    a = ml.gradients(dm, b)
+    assert np.array_equal(a, ml.gradients(dm, b))
+
+
+def test_bf16_gradients_error_bounded(ml, orc):
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 3)
+    x, y = rows(512, 164, 1), labels(512, 2)
+    g_ref, _ = orc.gradients(dims, p.params, x, y, threads=8)
+    dm = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    assert nrel(ml.gradients(dm, ml.RankingBatch(x, y)), g_ref) < 5e-2
+
+
+def test_objective_matches_gradient_loss(ml, orc):
+    dims = [4, 8, 8, 1]
+    p = ml.init_random(dims, 30)
+    x, y = rows(6, 4, 31), labels(6, 32)
+    replay = rows(7, 4, 33)
+    adv = ml.make_adversary(replay, 8, 1)
+    adv.set(np.linspace(-0.2, 0.2, 8), 0.1)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 64)
+    _, loss = ml.gradients(dm, ml.RankingBatch(x, y), adv, 0.01, want_loss=True)
+    assert ml.objective(dm, ml.RankingBatch(x, y), adv, 0.01) == pytest.approx(loss, rel=1e-12)
+    ref = orc.objective(dims, p.params, x, y, (np.linspace(-0.2, 0.2, 8), 0.1, replay), 0.01)
+    assert loss == pytest.approx(ref, rel=TOL_TF32)
+
+
+# ---------------------------------------------------------------- ranking
+@pytest.mark.parametrize("n", [0, 1, 2, 8, 513, 4096])
+def test_ranking_loss_vs_oracle(ml, orc, n):
+    rng = np.random.default_rng(n)
+    s = f32(rng.uniform(-2, 2, n))
+    y = f32(np.round(rng.random(n) * 20) / 20)  # ties in labels
+    ref, _, _ = orc.ranking_terms(s, y)
+    got = ml.pairwise_ranking_loss(s, y)
+    assert got == pytest.approx(ref, rel=1e-5, abs=1e-12)
+
+
+def test_ranking_loss_hand_cases(ml):
+    assert ml.pairwise_ranking_loss([2.0, 1.0], [3.0, 1.0]) == pytest.approx(math.log(1 + math.exp(-1)), rel=1e-6)
+    assert ml.pairwise_ranking_loss([1.0, 1.0], [3.0, 1.0]) == pytest.approx(math.log(2), rel=1e-6)
+    assert ml.pairwise_ranking_loss([1.0, 1.0], [1.0, 1.0]) == 0.0
+
+
+def test_ranking_accuracy_counts_exact(ml, orc):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 44)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 512)
+    batches = [ml.RankingBatch(rows(n, 16, n), np.round(labels(n, n + 1), 2)) for n in (3, 12, 100, 1)]
+    acc = ml.ranking_accuracy(dm, batches)
+    pairs = conc = 0
+    for b in batches:
+        s = ml.predict(dm, b.features).astype(np.float32)
+        pp, cc = orc.accuracy_counts(s, np.asarray(b.labels, np.float32))
+        pairs, conc = pairs + pp, conc + cc
+    assert acc == (conc / pairs if pairs else 0.0)
+
+
+# ---------------------------------------------------------------- updates (bit-exact on identical fp32 inputs)
+def _f32_params(p):
+    return ml_params(p.dims, f32(p.params))
+
+
+def ml_params(dims, w, mom=None):
+    from paper_2201_05752_b200.moseslab import CostModelParams
+
+    return CostModelParams(list(dims), w, mom)
+
+
+@pytest.mark.parametrize("use_momentum", [False, True])
+@pytest.mark.parametrize("masked", [False, True])
+def test_apply_update_bit_exact(ml, orc, use_momentum, masked):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 40)
+    w = f32(p.params)
+    mom = f32(np.random.default_rng(1).normal(0, 1e-3, len(w)))
+    g = f32(np.random.default_rng(2).normal(0, 1e-2, len(w)))
+    mask = np.random.default_rng(3).random(len(w)) < 0.5 if masked else None
+    dm = ml.DeviceModel(ml_params(dims, w, mom), ml.PREC_BF16, 16)
+    ml.apply_update(dm, ml.TrainHyper(learning_rate=0.001, momentum=0.9),
+                    ml.ParamMask(mask) if masked else None, use_momentum, grads=g)
+    got = dm.download()
+    ref_w, ref_m = orc.apply_update(w.astype(np.float32), mom.astype(np.float32), g.astype(np.float32), 0.001, 0.9,
+                                    mask, use_momentum)
+    assert np.array_equal(got.params, ref_w.astype(np.float64))
+    assert np.array_equal(got.momentum, ref_m.astype(np.float64))
+
+
+def test_update_arithmetic_kat(ml):
+    p = ml.init_random([4, 8, 8, 1], 40)
+    p.params[0] = 1.0
+    g = np.zeros_like(p.params); g[0] = 2.0
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 16)
+    before = dm.download().params
+    ml.apply_update(dm, ml.TrainHyper(learning_rate=0.001), None, False, grads=g)
+    after = dm.download().params
+    assert after[0] == pytest.approx(0.998, rel=1e-7)
+    assert np.array_equal(after[1:], before[1:])
+
+
+# ---------------------------------------------------------------- lottery (bit-exact)
+def test_xi_scores_bit_exact(ml, orc):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 9)
+    w = f32(p.params)
+    g = f32(np.random.default_rng(5).normal(0, 1e-2, len(w)))
+    g[::7] = 0.0
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_TF32, 16)
+    for norm in (False, True):
+        xi = ml.xi_scores(dm, norm, grads=g)
+        ref = orc.xi_scores(w.astype(np.float32), g.astype(np.float32), norm)
+        assert np.array_equal(xi.xi, ref.astype(np.float64))
+
+
+@pytest.mark.parametrize("rho,want", [(0.01, 2719), (0.3, 81562), (0.5, 135937), (0.7, 190312), (1.0, 271873)])
+def test_ratio_popcounts_canonical(ml, orc, rho, want):
+    n = 271873
+    xi = np.array([(orc.lib().orc_splitmix_at(8, i + 1) >> 11) * 2.0 ** -53 for i in range(n)])
+    xi32 = f32(xi)
+    dm = ml.DeviceModel(ml.init_random([16, 512, 512, 1], 0), ml.PREC_TF32, 16)
+    mask = ml.partition(dm, ml.XiScores(xi32, False), ml.RATIO, rho, 0)
+    assert mask.popcount() == want
+    ref = orc.partition(xi32.astype(np.float32), False, orc.RATIO, rho)
+    assert np.array_equal(mask.transferable, ref)
+
+
+def test_ratio_tie_break_and_heavy_zero_ties(ml, orc):
+    dm = ml.DeviceModel(ml.init_random([4, 8, 8, 1], 0), ml.PREC_TF32, 16)
+    P = dm.P
+    xi = np.zeros(P)
+    xi[:6] = [0.5, 0.9, 0.5, 0.1, 0.9, 0.5]
+    for rho in (3 / P, 0.25, 0.5, 0.9):
+        m = ml.partition(dm, ml.XiScores(xi, False), ml.RATIO, rho, 1)
+        assert np.array_equal(m.transferable, orc.partition(xi.astype(np.float32), False, orc.RATIO, rho))
+    m = ml.partition(dm, ml.XiScores(xi, False), ml.RATIO, 3 / P, 1)
+    assert sorted(np.flatnonzero(m.transferable)) == [0, 1, 4]
+    # half the scalars tied at zero (README.md:106-113) at canonical scale
+    n = 271873
+    rng = np.random.default_rng(3)
+    xi = f32(np.where(rng.random(n) < 0.5, 0.0, rng.random(n)))
+    xi[100:5000] = xi[99]  # a long run of equal non-zero keys too
+    dm2 = ml.DeviceModel(ml.init_random([16, 512, 512, 1], 0), ml.PREC_TF32, 16)
+    for rho in (0.3, 0.5, 0.51, 0.7):
+        m = ml.partition(dm2, ml.XiScores(xi, False), ml.RATIO, rho, 0)
+        assert np.array_equal(m.transferable, orc.partition(xi.astype(np.float32), False, orc.RATIO, rho))
+
+
+def test_threshold_partition(ml, orc):
+    dm = ml.DeviceModel(ml.init_random([4, 8, 8, 1], 0), ml.PREC_TF32, 16)
+    xi = np.zeros(dm.P)
+    xi[:5] = [0.2, 0.5, 0.50000001, 0.9, 1.0]
+    m = ml.partition(dm, ml.XiScores(xi, True), ml.THRESHOLD, 0.5, 3)
+    ref = orc.partition(f32(xi).astype(np.float32), True, orc.THRESHOLD, 0.5)
+    assert np.array_equal(m.transferable, ref)
+    with pytest.raises(ml.MosesError) as e:
+        ml.partition(dm, ml.XiScores(xi, False), ml.THRESHOLD, 0.5, 0)
+    assert e.value.code == "unnormalized-threshold"
+    for bad in (0.0, 1.5, -0.1):
+        with pytest.raises(ml.MosesError) as e:
+            ml.partition(dm, ml.XiScores(xi, False), ml.RATIO, bad, 0)
+        assert e.value.code == "invalid-ratio"
+
+
+@pytest.mark.parametrize("mode,value", [(2, 0.01), (2, 0.5), (2, 0.7), (1, 0.5), (1, 0.05), (2, 1.0)])
+def test_fused_lottery_step_bit_exact(ml, orc, mode, value):
+    """tuner.cpp:258-262: xi -> partition -> transferable_step -> variant_decay, fused on device."""
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 13)
+    w = f32(p.params)
+    g = f32(np.random.default_rng(6).normal(0, 1e-2, len(w)))
+    g[np.random.default_rng(7).random(len(w)) < 0.4] = 0.0  # zero-gradient ties
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    dm.set_gradients(g)
+    mask = ml.lottery_step(dm, mode, value, 2, 0.001, 0.01)
+    got = dm.download().params
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    xi = orc.xi_scores(w32, g32, mode == 1)
+    ref_mask = orc.partition(xi, mode == 1, mode, value)
+    ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+    ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
+    assert np.array_equal(mask.transferable, ref_mask)
+    assert np.array_equal(got, ref_w.astype(np.float64))
+
+
+def test_step_and_decay_separate_ops(ml, orc):
+    dims = [4, 8, 8, 1]
+    p = ml.init_random(dims, 10)
+    w = f32(p.params)
+    g = np.ones_like(w)
+    mask = np.zeros(len(w), bool); mask[0] = True; mask[32] = True
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_TF32, 16)
+    ml.transferable_step(dm, ml.ParamMask(mask), 0.01, grads=g)
+    got = dm.download().params
+    exp = w.astype(np.float32).copy()
+    exp[0] = np.float32(exp[0]) - np.float32(0.01)
+    exp[32] = np.float32(exp[32]) - np.float32(0.01)
+    assert np.array_equal(got, exp.astype(np.float64))
+    ml.variant_decay(dm, ml.ParamMask(mask), 0.001, 0.01)
+    ref = orc.variant_decay(exp, mask, 0.001, 0.01)
+    assert np.array_equal(dm.download().params, ref.astype(np.float64))
+    before = dm.download().params
+    ml.variant_decay(dm, None, 0.5, 0.0)
+    assert before.tobytes() == dm.download().params.tobytes()
+    for a, l in ((1.0, 1.0), (2.0, 0.5), (0.1, -0.5)):
+        with pytest.raises(ml.MosesError) as e:
+            ml.variant_decay(dm, None, a, l)
+        assert e.value.code == "unstable-decay"
+    with pytest.raises(ml.MosesError) as e:
+        ml.transferable_step(dm, ml.ParamMask(np.ones(7, bool)), 0.01)
+    assert e.value.code == "shape-mismatch"
+
+
+def test_moses_rho1_equals_vanilla(ml):
+    """acceptance.cpp:250-263: Moses with rho = 1 and no adversary == vanilla fine-tune, bit-exact."""
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 99)
+    b = ml.RankingBatch(rows(12, 16, 1), labels(12, 2))
+    a = ml.DeviceModel(p, ml.PREC_BF16, 64)
+    v = ml.DeviceModel(p, ml.PREC_BF16, 64)
+    for _ in range(3):
+        ml.gradients(a, b)
+        ml.lottery_step(a, ml.RATIO, 1.0, 0, 0.001, 0.01)
+        ml.gradients(v, b)
+        ml.apply_update(v, ml.TrainHyper(learning_rate=0.001), None, False)
+    assert np.array_equal(a.download().params, v.download().params)
+
+
+def test_adam_update_vs_oracle(ml, orc):
+    dims = [16, 512, 512, 1]
+    w = f32(ml.init_random(dims, 3).params)
+    g = f32(np.random.default_rng(1).normal(0, 1e-2, len(w)))
+    mask = np.random.default_rng(2).random(len(w)) < 0.5
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_TF32, 16)
+    dm.set_gradients(g)
+    ml.adam_update(dm, 1e-3, 0.9, 0.999, 1e-8, 1, ml.ParamMask(mask))
+    ref, _, _ = orc.adam(w.astype(np.float32), np.zeros(len(w), np.float32), np.zeros(len(w), np.float32),
+                         g.astype(np.float32), 1e-3, 0.9, 0.999, 1e-8, 1, mask)
+    assert nrel(dm.download().params, ref) < 1e-6
+
+
+# ---------------------------------------------------------------- adversary
+def test_adversarial_term_vs_oracle(ml, orc):
+    rng = np.random.default_rng(0)
+    hs, ht = rng.random((64, 32)), rng.random((24, 32))
+    hs[:, 0] += 2
+    adv = ml.make_adversary(rows(4, 4, 1), 32, 2)
+    aw, ab = np.zeros(32), 0.0
+    for _ in range(20):
+        res = ml.adversarial_term(adv, hs, ht, 0.01)
+        aw, ab, lref = orc.adversarial_term(aw, ab, hs, ht)
+        assert res.discriminator_loss == pytest.approx(lref, rel=1e-4)
+        assert res.confusion_contribution == pytest.approx(-0.01 * res.discriminator_loss, rel=1e-12)
+    assert nrel(adv.weight, aw) < 1e-4 and adv.bias == pytest.approx(ab, rel=1e-4, abs=1e-6)
+
+
+def test_adversary_validation(ml):
+    with pytest.raises(ml.MosesError) as e:
+        ml.make_adversary(np.zeros((0, 4)), 4)
+    assert e.value.code == "adversary-disabled"
+    with pytest.raises(ml.MosesError) as e:
+        ml.make_adversary(rows(3, 4, 0), 0)
+    assert e.value.code == "bad-dims"
+    adv = ml.make_adversary(rows(3, 4, 1), 4)
+    with pytest.raises(ml.MosesError) as e:
+        ml.adversarial_term(adv, rows(3, 5, 2), rows(3, 4, 3), 0.0)
+    assert e.value.code == "dim-mismatch"
+    with pytest.raises(ml.MosesError) as e:
+        ml.adversarial_term(adv, np.zeros((0, 4)), rows(3, 4, 3), 0.0)
+    assert e.value.code == "adversary-disabled"
+
+
+def test_discriminator_ce(ml, orc):
+    z = np.zeros(5)
+    assert ml.discriminator_cross_entropy(z, z) == pytest.approx(math.log(2), rel=1e-15)
+    zs, zt = np.random.default_rng(1).normal(0, 3, 17), np.random.default_rng(2).normal(0, 3, 9)
+    assert ml.discriminator_cross_entropy(zs, zt) == pytest.approx(orc.disc_ce(zs, zt), rel=1e-14)
+
+
+def test_fused_adversarial_step_matches_reference_sequence(ml, orc):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 5)
+    replay, xt = rows(256, 16, 1), rows(12, 16, 2)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 512)
+    adv = ml.make_adversary(replay, 512, 3)
+    res = ml.adversarial_step(adv, dm, xt, 0.01)
+    _, hs = orc.forward(dims, p.params, replay)
+    _, ht = orc.forward(dims, p.params, xt)
+    aw, ab, lref = orc.adversarial_term(np.zeros(512), 0.0, hs, ht)
+    assert res.discriminator_loss == pytest.approx(lref, rel=1e-5)
+    assert nrel(adv.weight, aw) < TOL_TF32
+
+
+# ---------------------------------------------------------------- top-k / selection (bit-exact)
+@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (1000, 12), (100000, 1024), (1 << 20, 4096), (5000, 5000)])
+def test_topk_bit_exact(ml, orc, n, k):
+    rng = np.random.default_rng(n)
+    s = f32(np.round(rng.normal(0, 1, n), 3))  # many ties
+    if k > 4096:
+        k = 4096
+    got = ml.topk(s, k)
+    ref = orc.topk(s.astype(np.float32), k)
+    assert np.array_equal(got, ref)
+
+
+def test_topk_negative_and_equal_scores(ml, orc):
+    s = np.array([-1.0, -0.5, -0.5, -3.0, 0.0, -0.0, 2.5, -0.5])
+    assert np.array_equal(ml.topk(s, 8), orc.topk(s.astype(np.float32), 8))
+    assert list(ml.topk(np.full(10, 3.0), 4)) == [0, 1, 2, 3]
+
+
+# ---------------------------------------------------------------- pooling / MMD
+def test_segment_sum_vs_oracle(ml, orc):
+    off = orc.synth_offsets(5, 1000, 8)
+    h = f32(rows(int(off[-1]), 37, 1))
+    got = ml.segment_sum(h, off)
+    ref = orc.segment_sum(h, off)
+    assert nrel(got, ref) < 1e-6
+    empty = np.array([0, 0, 3, 3], dtype=np.int64)  # empty segments
+    assert nrel(ml.segment_sum(h[:3], empty), orc.segment_sum(h[:3], empty)) < 1e-6
+
+
+def test_mmd_vs_oracle(ml, orc):
+    rng = np.random.default_rng(1)
+    xs, xt = rng.normal(0, 1, (300, 64)), rng.normal(0.3, 1, (120, 64))
+    assert ml.mmd2(xs, xt, 4.0) == pytest.approx(orc.mmd2(xs, xt, 4.0), rel=1e-4, abs=1e-7)
+
+
+# ---------------------------------------------------------------- synthetic generator bit-exactness
+def test_device_synthetic_features_match_oracle(ml, orc):
+    import torch
+
+    n, D = 333, 164
+    ld = 168
+    buf = torch.zeros((n, ld), dtype=torch.float32, device="cuda")
+    assert ml.lib().moses_synth_features_device(1, 1000, n, D, ml.DTYPE_F32, buf.data_ptr(), ld) == 0
+    torch.cuda.synchronize()
+    ref = orc.synth_features(1, 1000, n, D).astype(np.float32)
+    got = buf.cpu().numpy()
+    assert np.array_equal(got[:, :D], ref)
+    assert np.all(got[:, D] == 1.0) and np.all(got[:, D + 1:] == 0.0)
+    y = torch.zeros(n, dtype=torch.float32, device="cuda")
+    assert ml.lib().moses_synth_labels_device(1, 1000, n, y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), orc.synth_labels(1, 1000, n).astype(np.float32))
