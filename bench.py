@@ -1,0 +1,424 @@
+"""Benchmark of the B200 Moses cost-model hot path (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1]): source-device pre-training of the cost model
+{164, 512, 512, 512, 512, 1} ("4x512 hidden") on 200k synthetic TenSet-shaped
+programs, batch 512 per GPU, momentum SGD (tuner.cpp:130-156 loop body:
+gradients + apply_update). A step = one batch: forward (tcgen05 GEMMs),
+pairwise ranking loss, backward (dgrad/wgrad GEMMs), momentum update.
+Metric: train samples/s (whole job). N > 1: data parallel, one process per GPU,
+NCCL average of the gradient buffer between gradients and update (weak scaling,
+each rank its own 512-row batch of its own shard).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the reference's CPU path (the fp64 C++ oracle restating
+model.cpp; the reference itself cannot be built here) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cost-model programs/sec (infer) & train samples/sec, 1–8 B200 vs CPU"
+DIMS = [164, 512, 512, 512, 512, 1]
+PROGRAMS = 200_000
+BATCH = 512
+SEED_DATA, SEED_MODEL = 1, 12345
+LR, MU = 0.001, 0.9
+
+
+def train_flops_per_sample(dims):
+    """Algorithmic FLOPs per training sample: forward + weight-grad + data-grad (levels >= 1)."""
+    L = len(dims) - 1
+    fwd = sum(2 * dims[l] * dims[l + 1] for l in range(L))
+    wgrad = sum(2 * dims[l] * dims[l + 1] for l in range(L))
+    dgrad = sum(2 * dims[l] * dims[l + 1] for l in range(1, L - 1))
+    return fwd, wgrad, dgrad
+
+
+def gemm_flops_per_step(dims, n):
+    L = len(dims) - 1
+    fwd = sum(2 * n * dims[l] * dims[l + 1] for l in range(L - 1))
+    wgrad = sum(2 * n * dims[l] * dims[l + 1] for l in range(L - 1))
+    dgrad = sum(2 * n * dims[l] * dims[l + 1] for l in range(1, L - 1))
+    return fwd + wgrad + dgrad
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(steps_budget_s: float = 15.0, threads: int | None = None):
+    """Reference CPU path (fp64 oracle, reference formulas) on a bounded sample of the workload."""
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    threads = threads or os.cpu_count() or 1
+    w = orc.init_random(DIMS, SEED_MODEL, strict=False)
+    mom = np.zeros_like(w)
+    x = orc.synth_features(SEED_DATA, 0, BATCH, DIMS[0])
+    y = orc.synth_labels(SEED_DATA, 0, BATCH)
+    orc.train_step_f64(DIMS, w, mom, x, y, LR, MU, threads)  # warm
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        orc.train_step_f64(DIMS, w, mom, x, y, LR, MU, threads)
+        n += 1
+        if time.perf_counter() - t0 > steps_budget_s or n >= 2000:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * BATCH / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{n} fp64 training steps of batch {BATCH} on {DIMS} ({dt:.1f} s), "
+                      f"oracle/moses_oracle.hpp restating model.cpp:192-296"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps_s = 0.0
+    base = cpu_baseline(steps_budget_s=max(5.0, min(30.0, 0.05 * (args.steps + args.warmup))))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / base["value"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (keyed SplitMix64 TenSet-shaped features, labels 0.1+U)",
+        "config": {"workload": f"cfg2 pretrain {DIMS} on {PROGRAMS} programs, batch {BATCH}, momentum SGD",
+                   "programs": PROGRAMS, "global_batch": BATCH, "parallelism": "host threads"},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    del steps_s
+
+
+def bench_infer(ml, L, local, programs, peaks, reps=3):
+    """cfg4 at one GPU: score a device-resident pool of `programs` synthetic programs with the
+    4x512 model and select the top-1024 (score desc, index asc). programs/s and the forward
+    GEMM roofline; features generated on device (PCIe would otherwise dominate)."""
+    import ctypes as C
+
+    import torch
+
+    chunk = 65536
+    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
+    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=chunk)
+    ld = dm.packed_ld
+    X = torch.empty((programs, ld), dtype=torch.bfloat16, device="cuda")
+    S = torch.empty(programs, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(SEED_DATA + 100, 0, programs, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    torch.cuda.synchronize()
+    idx = (C.c_int64 * 1024)()
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+
+    def run():
+        rc = L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
+        if rc:
+            raise RuntimeError(L.moses_last_error().decode())
+        torch.cuda.synchronize()
+        rc = L.moses_topk_device(S.data_ptr(), programs, 1024, idx)
+        if rc:
+            raise RuntimeError(L.moses_last_error().decode())
+
+    run()
+    times, fwd_ms = [], []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record(stream)
+            rc = L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
+            b.record(stream)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L.moses_topk_device(S.data_ptr(), programs, 1024, idx)
+            t_topk = time.perf_counter() - t0
+            times.append(a.elapsed_time(b) / 1000.0 + t_topk)
+            fwd_ms.append(a.elapsed_time(b))
+    ml.profile_begin()
+    with torch.cuda.stream(stream):
+        L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
+        torch.cuda.synchronize()
+    prof = ml.profile_end()
+    best = min(times)
+    flops_prog = sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 1))
+    gemm_s = prof["gemm_fwd"][0] / 1000.0
+    gemm_flops = programs * sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 2))
+    peak = peaks.get("bf16_tflops_sustained", 1408.7)
+    ach = gemm_flops / gemm_s / 1e12 if gemm_s else None
+    del X
+    torch.cuda.empty_cache()
+    return {"metric": "cost-model programs/sec (infer)", "value": programs / best, "unit": "programs/s",
+            "workload": f"cfg4 @1 GPU: score {programs} synthetic programs with {DIMS} (bf16), top-1024",
+            "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms), "flops_per_program": flops_prog,
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak if ach else None, "kernel": "umma_gemm_kernel forward (Fwd epilogue)",
+                         "gemm_ms": prof["gemm_fwd"][0], "gemm_launches": prof["gemm_fwd"][1]},
+            "inputs": "device-resident bf16 packed features (3.4 GB > L2)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--no-infer", action="store_true")
+    ap.add_argument("--infer-programs", type=int, default=10_000_000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_05752_b200 import moseslab as ml
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = ml.lib()
+    if L.moses_device_check() != 0:
+        raise SystemExit("moses: " + L.moses_last_error().decode())
+
+    # ---------------- model + device-resident dataset (this rank's shard)
+    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
+    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=BATCH)
+    ld = dm.packed_ld
+    shard = PROGRAMS // world if world > 1 else PROGRAMS
+    row0 = rank * shard
+    X = torch.empty((shard, ld), dtype=torch.bfloat16, device="cuda")
+    Y = torch.empty(shard, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(SEED_DATA, row0, shard, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(SEED_DATA, row0, shard, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    nb = shard // BATCH
+
+    import ctypes as C
+
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    gptr = C.POINTER(C.c_float)()
+    L.moses_model_device_ptrs(dm.h, None, C.byref(gptr), None)
+
+    class _CAI:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+    grads = torch.as_tensor(_CAI(C.cast(gptr, C.c_void_p).value, dm.P), device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    L.moses_set_async(1)
+    row_bytes = ld * 2
+
+    def step(b):
+        xb = X.data_ptr() + (b % nb) * BATCH * row_bytes
+        yb = Y.data_ptr() + (b % nb) * BATCH * 4
+        if world == 1:
+            rc = L.moses_train_step_device(dm.h, xb, ld, yb, BATCH, LR, MU, None)
+            if rc:
+                raise RuntimeError(L.moses_last_error().decode())
+        else:
+            rc = L.moses_gradients_device(dm.h, xb, ld, yb, BATCH, None)
+            if rc:
+                raise RuntimeError(L.moses_last_error().decode())
+            dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+            rc = L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
+            if rc:
+                raise RuntimeError(L.moses_last_error().decode())
+
+    with torch.cuda.stream(stream):
+        for b in range(args.warmup):
+            step(b)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # ---------------- timed region: K steps, L2 flushed between steps (outside the step brackets)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        launches0 = ml.kernel_launches()
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                evs[k][0].record(stream)
+                step(args.warmup + k)
+                evs[k][1].record(stream)
+            torch.cuda.synchronize()
+        launches = ml.kernel_launches() - launches0
+        total_ms = sum(a.elapsed_time(b) for a, b in evs)
+        if world > 1:
+            t = torch.tensor([total_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+            dist.barrier()
+        ms_step = total_ms / args.steps
+        value = world * BATCH / (ms_step / 1000.0)
+
+        # ---------------- device-time attribution (separate pass; events perturb timing)
+        ml.profile_begin()
+        for k in range(args.profile_steps):
+            step(k)
+        torch.cuda.synchronize()
+        prof = ml.profile_end()
+
+        # ---------------- end to end through the reference-facing C ABI with host buffers
+        x_host = torch.from_numpy(np.ascontiguousarray(
+            np.random.default_rng(rank).random((BATCH, DIMS[0])))).pin_memory()
+        y_host = torch.from_numpy(0.1 + np.random.default_rng(rank + 7).random(BATCH)).pin_memory()
+        loss = C.c_double()
+        L.moses_set_async(0)
+
+        def e2e_step():
+            rc = L.moses_gradients(dm.h, x_host.data_ptr(), y_host.data_ptr(), BATCH, DIMS[0], None, 0.0, C.byref(loss))
+            if rc:
+                raise RuntimeError(L.moses_last_error().decode())
+            if world > 1:
+                dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+            L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e2e_steps = max(10, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+    e2e_value = world * BATCH * e2e_steps / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel class
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
+    gemm_launches = sum(prof[c][1] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
+    flops = gemm_flops_per_step(DIMS, BATCH)
+    peak = peaks.get("bf16_tflops_sustained", 1408.7)
+    achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("gemm_bytes_per_launch")
+    except Exception:
+        pass
+    step_prof_ms = sum(v[0] for v in prof.values()) / args.profile_steps
+    fwd, wg, dg = train_flops_per_sample(DIMS)
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (keyed SplitMix64 TenSet-shaped features 164-d, labels 0.1+U; random-init model)",
+        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} programs, batch {BATCH}/GPU, "
+                               f"momentum SGD lr={LR} mu={MU}", "model": "moses-mlp-4x512", "programs": PROGRAMS,
+                   "global_batch": BATCH * world, "seq_len": None, "parallelism": f"dp{world}",
+                   "statements_per_program": 1,
+                   "l2": "flushed (256 MiB write) between timed steps, outside the per-step CUDA-event brackets"},
+        "e2e": {"value": e2e_value, "unit": "samples/s",
+                "h2d_bytes_per_step": BATCH * DIMS[0] * 8 + BATCH * 8, "d2h_bytes_per_step": 8,
+                "path": "moses_gradients + moses_apply_update (C ABI, pinned host float64 buffers)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "umma_gemm_kernel (tcgen05 bf16, all fwd/dgrad/wgrad launches of a step)",
+                     "flops_per_step": flops, "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+        "step_breakdown_ms": {k: v[0] / args.profile_steps for k, v in prof.items() if v[1]},
+        "step_device_ms_profiled": step_prof_ms,
+        "algorithmic_flops_per_sample": {"fwd": fwd, "wgrad": wg, "dgrad": dg},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_infer:
+        line["infer"] = bench_infer(ml, L, local, args.infer_programs, peaks)
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(15.0)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

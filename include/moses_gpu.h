@@ -101,6 +101,9 @@ MOSES_API int moses_predict_pooled(moses_model_t m, const double* stmt_features,
  * adv may be NULL; beta == 0 or NULL adversary skips the confusion term bit-exactly. */
 MOSES_API int moses_gradients(moses_model_t m, const double* features, const double* labels, int64_t n, int32_t D,
                               moses_adversary_t adv, double beta, double* loss_out);
+/* gradients() on device-resident packed rows (x_dev, ldx) and fp32 labels; no adversary. */
+MOSES_API int moses_gradients_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                     double* loss_out);
 MOSES_API int moses_gradients_download(moses_model_t m, double* grads, int64_t count);
 MOSES_API int moses_gradients_upload(moses_model_t m, const double* grads, int64_t count);
 /* objective (model.cpp:246-261) */
@@ -202,9 +205,20 @@ MOSES_API int moses_read_mask(const uint8_t* bytes, int64_t len, uint8_t* mask_o
                               int32_t* phase, int32_t* mode, double* value);
 
 /* ------------------------------------------------------------------ timing helpers (bench) */
+/* Calling thread: make moses_apply_update asynchronous on the handle's stream (device-resident loops). */
+MOSES_API int moses_set_async(int32_t on);
+/* Device-time attribution: CUDA-event brackets per kernel class between begin and end.
+ * Classes: 0 gemm_fwd, 1 gemm_dgrad, 2 gemm_wgrad, 3 rank, 4 head, 5 update, 6 select, 7 topk, 8 other. */
+MOSES_API int moses_profile_begin(void);
+MOSES_API int moses_profile_end(double* ms_by_cat, int64_t* count_by_cat, int32_t ncat);
 /* Raw pointers into the handle (device): params fp32, gradients fp32, momentum fp32. */
 MOSES_API int moses_model_device_ptrs(moses_model_t m, float** params, float** grads, float** momentum);
 MOSES_API int moses_model_stream(moses_model_t m, void** stream);
+/* Test hook: one raw tcgen05 GEMM C = A * B^T on device buffers (elem 2 = bf16, 4 = tf32;
+ * epi 0 = bias/ReLU store, 1 = ReLU'-masked store, 2 = fp32 store; bn 0 = auto). */
+MOSES_API int moses_debug_gemm(int elem, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B,
+                               long long ldb, int b_mn, int epi, void* out, long long ldo, const float* bias, int relu,
+                               int bn, const void* mask, long long ldm);
 
 #ifdef __cplusplus
 }

@@ -182,45 +182,79 @@ Params<R> cast_params(const Params<S>& p) {
 }
 
 // ---------------------------------------------------------------- dense kernels
-// C[M][N] (row-major) = A[M][K] * B[K][N]   (both row-major). Parallel over M.
+// C[M][N] (row-major) = A * B with general strides: A(m,k) = A[m*sam + k*sak],
+// B(k,n) = B[k*sbk + n*sbn]. Parallel over M; B is packed into 16-column panels.
 template <class R>
-void gemm_nn(int M, int N, int K, const R* A, const R* B, R* C, int threads) {
+void gemm_general(int M, int N, int K, const R* A, std::int64_t sam, std::int64_t sak, const R* B, std::int64_t sbk,
+                  std::int64_t sbn, R* C, int threads) {
 #if defined(ORACLE_AVX2)
   if constexpr (std::is_same_v<R, double>) {
+    // Register-blocked 4 x 16 micro-kernel (explicit FMA, as Eigen's GEBP does), full tiles fully
+    // unrolled so the 16 accumulators stay in ymm registers; edges fall back to scalar FMA.
     const int Nv = N & ~15;
+    const int Mv = M & ~3;
+    std::vector<double> Bp(std::size_t(K) * Nv);
+#pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
+    for (int n0 = 0; n0 < Nv; n0 += 16)
+      for (int k = 0; k < K; ++k) {
+        double* dst = &Bp[std::size_t(n0) * K + std::size_t(k) * 16];
+        const double* src = B + std::int64_t(k) * sbk + std::int64_t(n0) * sbn;
+        if (sbn == 1) std::memcpy(dst, src, 16 * sizeof(double));
+        else
+          for (int j = 0; j < 16; ++j) dst[j] = src[j * sbn];
+      }
 #pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
     for (int m0 = 0; m0 < M; m0 += 4) {
-      const int mr = std::min(4, M - m0);
-      for (int n0 = 0; n0 < Nv; n0 += 16) {
-        __m256d acc[4][4];
-        for (int r = 0; r < 4; ++r)
-          for (int c = 0; c < 4; ++c) acc[r][c] = _mm256_setzero_pd();
-        for (int k = 0; k < K; ++k) {
-          const double* b = B + std::int64_t(k) * N + n0;
-          const __m256d b0 = _mm256_loadu_pd(b), b1 = _mm256_loadu_pd(b + 4),
-                        b2 = _mm256_loadu_pd(b + 8), b3 = _mm256_loadu_pd(b + 12);
-          for (int r = 0; r < mr; ++r) {
-            const __m256d a = _mm256_broadcast_sd(A + std::int64_t(m0 + r) * K + k);
-            acc[r][0] = _mm256_fmadd_pd(a, b0, acc[r][0]);
-            acc[r][1] = _mm256_fmadd_pd(a, b1, acc[r][1]);
-            acc[r][2] = _mm256_fmadd_pd(a, b2, acc[r][2]);
-            acc[r][3] = _mm256_fmadd_pd(a, b3, acc[r][3]);
+      if (m0 < Mv) {
+        const double* a0 = A + std::int64_t(m0) * sam;
+        const double* a1 = a0 + sam;
+        const double* a2 = a1 + sam;
+        const double* a3 = a2 + sam;
+        for (int n0 = 0; n0 < Nv; n0 += 16) {
+          __m256d c00 = _mm256_setzero_pd(), c01 = c00, c02 = c00, c03 = c00;
+          __m256d c10 = c00, c11 = c00, c12 = c00, c13 = c00;
+          __m256d c20 = c00, c21 = c00, c22 = c00, c23 = c00;
+          __m256d c30 = c00, c31 = c00, c32 = c00, c33 = c00;
+          const double* b = Bp.data() + std::size_t(n0) * K;
+          for (int k = 0; k < K; ++k, b += 16) {
+            const std::int64_t ko = std::int64_t(k) * sak;
+            const __m256d b0 = _mm256_loadu_pd(b), b1 = _mm256_loadu_pd(b + 4), b2 = _mm256_loadu_pd(b + 8),
+                          b3 = _mm256_loadu_pd(b + 12);
+            __m256d a = _mm256_broadcast_sd(a0 + ko);
+            c00 = _mm256_fmadd_pd(a, b0, c00); c01 = _mm256_fmadd_pd(a, b1, c01);
+            c02 = _mm256_fmadd_pd(a, b2, c02); c03 = _mm256_fmadd_pd(a, b3, c03);
+            a = _mm256_broadcast_sd(a1 + ko);
+            c10 = _mm256_fmadd_pd(a, b0, c10); c11 = _mm256_fmadd_pd(a, b1, c11);
+            c12 = _mm256_fmadd_pd(a, b2, c12); c13 = _mm256_fmadd_pd(a, b3, c13);
+            a = _mm256_broadcast_sd(a2 + ko);
+            c20 = _mm256_fmadd_pd(a, b0, c20); c21 = _mm256_fmadd_pd(a, b1, c21);
+            c22 = _mm256_fmadd_pd(a, b2, c22); c23 = _mm256_fmadd_pd(a, b3, c23);
+            a = _mm256_broadcast_sd(a3 + ko);
+            c30 = _mm256_fmadd_pd(a, b0, c30); c31 = _mm256_fmadd_pd(a, b1, c31);
+            c32 = _mm256_fmadd_pd(a, b2, c32); c33 = _mm256_fmadd_pd(a, b3, c33);
           }
-        }
-        for (int r = 0; r < mr; ++r) {
-          double* c = C + std::int64_t(m0 + r) * N + n0;
-          _mm256_storeu_pd(c, acc[r][0]);
-          _mm256_storeu_pd(c + 4, acc[r][1]);
-          _mm256_storeu_pd(c + 8, acc[r][2]);
-          _mm256_storeu_pd(c + 12, acc[r][3]);
+          double* c = C + std::int64_t(m0) * N + n0;
+          _mm256_storeu_pd(c, c00); _mm256_storeu_pd(c + 4, c01); _mm256_storeu_pd(c + 8, c02); _mm256_storeu_pd(c + 12, c03);
+          c += N;
+          _mm256_storeu_pd(c, c10); _mm256_storeu_pd(c + 4, c11); _mm256_storeu_pd(c + 8, c12); _mm256_storeu_pd(c + 12, c13);
+          c += N;
+          _mm256_storeu_pd(c, c20); _mm256_storeu_pd(c + 4, c21); _mm256_storeu_pd(c + 8, c22); _mm256_storeu_pd(c + 12, c23);
+          c += N;
+          _mm256_storeu_pd(c, c30); _mm256_storeu_pd(c + 4, c31); _mm256_storeu_pd(c + 8, c32); _mm256_storeu_pd(c + 12, c33);
         }
       }
-      for (int r = 0; r < mr; ++r)
-        for (int n = Nv; n < N; ++n) {
-          double s = 0.0;
-          for (int k = 0; k < K; ++k) s = std::fma(A[std::int64_t(m0 + r) * K + k], B[std::int64_t(k) * N + n], s);
-          C[std::int64_t(m0 + r) * N + n] = s;
+      const int r0 = m0 < Mv ? 4 : 0;
+      const int mr = std::min(4, M - m0);
+      for (int r = 0; r < mr; ++r) {
+        double* c = C + std::int64_t(m0 + r) * N;
+        const int nlo = r < r0 ? Nv : 0;  // full 4-row tiles already covered [0, Nv)
+        for (int n = nlo; n < N; ++n) {
+          double acc = 0.0;
+          for (int k = 0; k < K; ++k)
+            acc = std::fma(A[std::int64_t(m0 + r) * sam + std::int64_t(k) * sak], B[std::int64_t(k) * sbk + std::int64_t(n) * sbn], acc);
+          c[n] = acc;
         }
+      }
     }
     return;
   }
@@ -230,18 +264,26 @@ void gemm_nn(int M, int N, int K, const R* A, const R* B, R* C, int threads) {
     R* c = C + std::int64_t(m) * N;
     for (int n = 0; n < N; ++n) c[n] = R(0);
     for (int k = 0; k < K; ++k) {
-      const R a = A[std::int64_t(m) * K + k];
-      const R* b = B + std::int64_t(k) * N;
-      for (int n = 0; n < N; ++n) c[n] = std::fma(a, b[n], c[n]);
+      const R a = A[std::int64_t(m) * sam + std::int64_t(k) * sak];
+      for (int n = 0; n < N; ++n) c[n] = std::fma(a, B[std::int64_t(k) * sbk + std::int64_t(n) * sbn], c[n]);
     }
   }
+}
+
+// C[M][N] = A[M][K] * B[K][N], all row-major.
+template <class R>
+void gemm_nn(int M, int N, int K, const R* A, const R* B, R* C, int threads) {
+  gemm_general<R>(M, N, K, A, K, 1, B, N, 1, C, threads);
 }
 
 template <class R>
 std::vector<R> transpose(const R* A, int rows, int cols) {
   std::vector<R> T(std::size_t(rows) * cols);
-  for (int r = 0; r < rows; ++r)
-    for (int c = 0; c < cols; ++c) T[std::size_t(c) * rows + r] = A[std::size_t(r) * cols + c];
+  constexpr int kB = 32;  // cache-blocked
+  for (int r0 = 0; r0 < rows; r0 += kB)
+    for (int c0 = 0; c0 < cols; c0 += kB)
+      for (int r = r0; r < std::min(rows, r0 + kB); ++r)
+        for (int c = c0; c < std::min(cols, c0 + kB); ++c) T[std::size_t(c) * rows + r] = A[std::size_t(r) * cols + c];
   return T;
 }
 
@@ -354,9 +396,8 @@ void backprop_from_penultimate(const Params<R>& p, const Forward<R>& f, const R*
     for (std::size_t i = 0; i < dz.size(); ++i) dz[i] = dh[i] * (z[i] > R(0) ? R(1) : R(0));
     const R* in = l == 0 ? x : f.h[l - 1].data();
     // gW (flat [in][out]) += in^T * dz ; gb += colsum(dz)
-    std::vector<R> inT = transpose(in, n, di);
     std::vector<R> gw(std::size_t(di) * dout);
-    gemm_nn<R>(di, dout, n, inT.data(), dz.data(), gw.data(), threads);
+    gemm_general<R>(di, dout, n, in, 1, di, dz.data(), dout, 1, gw.data(), threads);  // in^T * dz
     R* G = g.data() + level_offset(p.dims, l);
     for (std::size_t i = 0; i < gw.size(); ++i) G[i] += gw[i];
     std::vector<R> gb(dout, R(0));
@@ -366,9 +407,8 @@ void backprop_from_penultimate(const Params<R>& p, const Forward<R>& f, const R*
     for (int o = 0; o < dout; ++o) GB[o] += gb[o];
     if (l > 0) {
       // dh_prev = dz * W  (W is out x in; flat block is [in][out] = W^T)
-      std::vector<R> Wt = transpose(p.W(l), di, dout);  // -> [out][in]
       std::vector<R> nd(std::size_t(n) * di);
-      gemm_nn<R>(n, di, dout, dz.data(), Wt.data(), nd.data(), threads);
+      gemm_general<R>(n, di, dout, dz.data(), dout, 1, p.W(l), 1, dout, nd.data(), threads);  // dz * W
       dh = std::move(nd);
     }
   }

@@ -60,6 +60,9 @@ def lib():
         _lib.orc_splitmix_draw.argtypes = [C.c_uint64, C.c_int]
         _lib.orc_splitmix_at.argtypes = [C.c_uint64, C.c_uint64]
         _lib.orc_fnv_u64_str.argtypes = [C.c_uint64, C.c_char_p]
+        _lib.orc_fnv_u64s.argtypes = [C.c_void_p, C.c_int]
+        _lib.orc_fnv_str.argtypes = [C.c_char_p]
+        _lib.orc_param_count.argtypes = [C.c_void_p, C.c_int]
         _lib.orc_uniform01_first.restype = C.c_double
         _lib.orc_uniform01_first.argtypes = [C.c_uint64]
         _lib.orc_gaussian_first.restype = C.c_double
@@ -71,6 +74,13 @@ def lib():
         _lib.orc_init_random.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int, C.c_void_p]
         for s in ("f64", "f32"):
             rt = C.c_double if s == "f64" else C.c_float
+            getattr(_lib, f"orc_forward_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                                         C.c_void_p, C.c_void_p, C.c_int]
+            getattr(_lib, f"orc_ranking_terms_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                                               C.c_void_p]
+            getattr(_lib, f"orc_accuracy_counts_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                                                 C.c_void_p]
+            getattr(_lib, f"orc_disc_ce_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
             getattr(_lib, f"orc_disc_ce_{s}").restype = rt
             getattr(_lib, f"orc_mmd2_{s}").restype = rt
             getattr(_lib, f"orc_mmd2_{s}").argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, rt]

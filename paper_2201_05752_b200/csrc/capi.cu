@@ -28,6 +28,40 @@ namespace moses {
 std::atomic<long long> g_launches{0};
 void note_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// ---- profiler
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+};
+static Profiler& prof() {
+  static Profiler p;
+  return p;
+}
+ProfScope::ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
+  Profiler& p = prof();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> lk(p.mu);
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  if (!p.pool.empty()) {
+    ev = p.pool.back();
+    p.pool.pop_back();
+  } else {
+    cudaEventCreate(&ev.first);
+    cudaEventCreate(&ev.second);
+  }
+  idx = int(p.rec.size());
+  p.rec.push_back({c, ev});
+  cudaEventRecord(ev.first, s);
+}
+ProfScope::~ProfScope() {
+  if (idx < 0) return;
+  Profiler& p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  cudaEventRecord(p.rec[idx].second.second, st);
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -162,7 +196,8 @@ struct moses_model {
   float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
   float *m1 = nullptr, *m2 = nullptr;
   uint8_t* mask = nullptr;
-  __nv_bfloat16* wbf = nullptr;
+  __nv_bfloat16* wbf = nullptr;  // bf16 operand shadow (BF16 mode)
+  float* wtf = nullptr;          // tf32-rounded operand shadow (TF32 mode)
   bool xi_valid = false, xi_norm = false, mask_valid = false;
   // activations
   std::vector<void*> act, dz;
@@ -182,9 +217,9 @@ struct moses_model {
   int last_tiles = 0;  // N tiles of the last hidden GEMM of the most recent forward
 
   const void* wop(int l) const {
-    return esz == 2 ? static_cast<const void*>(wbf + off[l]) : static_cast<const void*>(w + off[l]);
+    return esz == 2 ? static_cast<const void*>(wbf + off[l]) : static_cast<const void*>(wtf + off[l]);
   }
-  __nv_bfloat16* shadow() const { return esz == 2 ? wbf : nullptr; }
+  Shadow shadow() const { return esz == 2 ? Shadow{wbf, 1} : Shadow{wtf, 2}; }
   int width(int l) const { return dims[l]; }
   int W() const { return dims[L - 1]; }
   const float* head_w() const { return w + off[L - 1]; }
@@ -193,7 +228,7 @@ struct moses_model {
 
   ~moses_model() {
     if (st) cudaStreamSynchronize(st);
-    for (void* p : {(void*)w, (void*)mom, (void*)g, (void*)xi, (void*)m1, (void*)m2, (void*)mask, (void*)wbf,
+    for (void* p : {(void*)w, (void*)mom, (void*)g, (void*)xi, (void*)m1, (void*)m2, (void*)mask, (void*)wbf, (void*)wtf,
                     (void*)head_part, (void*)head_part2, (void*)scores, (void*)labels, (void*)coefA, (void*)coefB,
                     (void*)rank.gs_part, (void*)rank.loss_part, (void*)rank.pairs_part, (void*)dscal, (void*)dpairs,
                     (void*)dcount, sel_base, (void*)staging, (void*)adv_ws})
@@ -223,6 +258,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     c.ldo = m->ld[l + 1];
     c.bias = m->bias(l);
     c.relu = 1;
+    c.round_out = !last;  // the last hidden layer is never a GEMM operand: keep it full fp32
     if (last) {
       c.head_w = m->head_w();
       c.head_u = head_u;
@@ -230,7 +266,11 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
       c.head_part2 = head_u ? m->head_part2 : nullptr;
       c.head_ld = m->cap;
     }
-    const int bn = launch_gemm(m->esz, c, m->st);
+    int bn;
+    {
+      ProfScope ps(P_GEMM_FWD, m->st);
+      bn = launch_gemm(m->esz, c, m->st);
+    }
     note_launch(1);
     if (last) m->last_tiles = ceil_div(c.N, bn);
   }
@@ -240,9 +280,12 @@ template <typename T>
 void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u) {
   const int L = m->L, W = m->W();
   T* hl = static_cast<T*>(m->act[L - 1]);
-  column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->st);
-  head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
-                   m->lddz[L - 1], m->st);
+  {
+    ProfScope ps(P_HEAD, m->st);
+    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st);
+    head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
+                     m->lddz[L - 1], m->st);
+  }
   note_launch(2);
   for (int l = L - 2; l >= 0; --l) {
     const void* a = l == 0 ? x0 : m->act[l];
@@ -256,7 +299,10 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     wg.epi = EpiKind::StoreF32;
     wg.out = m->g + m->off[l];
     wg.ldo = m->dims[l + 1];
-    launch_gemm(m->esz, wg, m->st);
+    {
+      ProfScope ps(P_GEMM_WGRAD, m->st);
+      launch_gemm(m->esz, wg, m->st);
+    }
     note_launch(1);
     if (l > 0) {
       GemmCall dg{};
@@ -270,11 +316,19 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       dg.ldo = m->lddz[l];
       dg.mask = m->act[l];
       dg.ldm = m->ld[l];
-      launch_gemm(m->esz, dg, m->st);
+      {
+        ProfScope ps(P_GEMM_DGRAD, m->st);
+        launch_gemm(m->esz, dg, m->st);
+      }
       note_launch(1);
     }
   }
 }
+
+// apply_update is synchronous for host callers (reference value semantics); the device-resident
+// DP loop (bench, moses_set_async) keeps it asynchronous on the handle's stream.
+thread_local bool g_async = false;
+bool sync_updates() { return !g_async; }
 
 void require_model(moses_model* m) {
   if (!m) fail(MOSES_ERR_INVALID_ARG, "null model handle");
@@ -344,12 +398,15 @@ void gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   }
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
+  ProfScope ps(P_RANK, m->st);
   head_scores(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), n, m->scores, m->st);
   rank_pairs(m->scores, y, n, {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->st);
   FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
   rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
                 active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
   note_launch(3);
+  ps.~ProfScope();
+  ps.idx = -1;
   if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u);
   else backward_rows<float>(m, x0, ldx0, R, u);
   m->xi_valid = false;
@@ -435,10 +492,12 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->xi = dalloc<float>(P);
     m->mask = dalloc<uint8_t>(P);
     if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(P);
+    else m->wtf = dalloc<float>(P);
     MOSES_CUDA(cudaMemset(m->w, 0, P * 4));
     MOSES_CUDA(cudaMemset(m->mom, 0, P * 4));
     MOSES_CUDA(cudaMemset(m->g, 0, P * 4));
     if (m->wbf) MOSES_CUDA(cudaMemset(m->wbf, 0, P * 2));
+    if (m->wtf) MOSES_CUDA(cudaMemset(m->wtf, 0, P * 4));
     const int vec = 16 / m->esz;
     int maxw = 0;
     for (int l = 0; l < m->L; ++l) {
@@ -482,7 +541,8 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     select_ws_carve(m->sel_base, seln, &m->sel);
     m->stage_w = std::max<long long>(maxw, 1) + 1;
     m->staging = dalloc<double>(m->cap * m->stage_w);
-    m->adv_ws = dalloc<float>(round_up(m->cap, 64) + round_up(maxw + 1, 64) + 64);
+    m->adv_ws = dalloc<float>(round_up(m->cap, 64) + round_up(maxw + 1, 64) + 64 + 16 +
+                              column_dot_ws_floats(m->cap, maxw) + 64);
     MOSES_CUDA(cudaStreamSynchronize(m->st));
     *out = m.release();
   });
@@ -499,10 +559,8 @@ MOSES_API int moses_model_upload(moses_model_t m, const double* params, const do
     upload_f32(m, params, count, m->w);
     if (momentum) upload_f32(m, momentum, count, m->mom);
     else MOSES_CUDA(cudaMemsetAsync(m->mom, 0, count * 4, m->st));
-    if (m->wbf) {
-      f32_to_bf16(m->w, count, m->wbf, m->st);
-      note_launch(1);
-    }
+    refresh_shadow(m->w, count, m->shadow(), m->st);
+    note_launch(1);
     m->xi_valid = false;
     MOSES_CUDA(cudaStreamSynchronize(m->st));
   });
@@ -525,10 +583,8 @@ MOSES_API int moses_model_copy(moses_model_t dst, moses_model_t src) {
     MOSES_CUDA(cudaStreamSynchronize(src->st));
     MOSES_CUDA(cudaMemcpyAsync(dst->w, src->w, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
     MOSES_CUDA(cudaMemcpyAsync(dst->mom, src->mom, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
-    if (dst->wbf) {
-      f32_to_bf16(dst->w, dst->P, dst->wbf, dst->st);
-      note_launch(1);
-    }
+    refresh_shadow(dst->w, dst->P, dst->shadow(), dst->st);
+    note_launch(1);
     MOSES_CUDA(cudaStreamSynchronize(dst->st));
   });
 }
@@ -682,6 +738,55 @@ MOSES_API int moses_objective(moses_model_t m, const double* x, const double* y,
   });
 }
 
+MOSES_API int moses_gradients_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                     double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    check_rows(m, n);
+    gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    }
+  });
+}
+
+MOSES_API int moses_set_async(int32_t on) {
+  g_async = on != 0;
+  return MOSES_OK;
+}
+
+MOSES_API int moses_profile_begin(void) {
+  return guarded([&] {
+    Profiler& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    for (auto& r : p.rec) p.pool.push_back(r.second);
+    p.rec.clear();
+    p.on = true;
+  });
+}
+
+MOSES_API int moses_profile_end(double* ms_by_cat, int64_t* count_by_cat, int32_t ncat) {
+  return guarded([&] {
+    Profiler& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.on = false;
+    for (int c = 0; c < ncat; ++c) {
+      ms_by_cat[c] = 0.0;
+      count_by_cat[c] = 0;
+    }
+    for (auto& r : p.rec) {
+      MOSES_CUDA(cudaEventSynchronize(r.second.second));
+      float ms = 0.f;
+      MOSES_CUDA(cudaEventElapsedTime(&ms, r.second.first, r.second.second));
+      if (r.first < ncat) {
+        ms_by_cat[r.first] += ms;
+        count_by_cat[r.first] += 1;
+      }
+    }
+  });
+}
+
 MOSES_API int moses_gradients_download(moses_model_t m, double* g, int64_t count) {
   return guarded([&] {
     require_model(m);
@@ -712,10 +817,13 @@ MOSES_API int moses_apply_update(moses_model_t m, double lr, double mu, const ui
   return guarded([&] {
     require_model(m);
     const uint8_t* dm = upload_mask(m, mask, mask_len);
-    sgd_update(m->w, m->mom, m->g, dm, m->P, float(lr), float(mu), use_momentum != 0, m->shadow(), m->st);
+    {
+      ProfScope ps(P_UPDATE, m->st);
+      sgd_update(m->w, m->mom, m->g, dm, m->P, float(lr), float(mu), use_momentum != 0, m->shadow(), m->st);
+    }
     note_launch(1);
     m->xi_valid = false;
-    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    if (sync_updates()) MOSES_CUDA(cudaStreamSynchronize(m->st));
   });
 }
 
@@ -758,6 +866,7 @@ MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_
     require_model(m);
     check_rows(m, n);
     gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
+    ProfScope ps(P_UPDATE, m->st);
     sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
     note_launch(1);
     if (loss_out) {
@@ -811,7 +920,7 @@ MOSES_API int moses_ranking_loss(const double* s, const double* y, int64_t n, do
     Scratch& sc = scratch();
     std::lock_guard<std::mutex> lk(sc.mu);
     const int ns = rank_splits(n);
-    const size_t bytes = (size_t(n) * 2 + 64) * 8 + size_t(ns) * n * 24 + size_t(n) * 8 + 4096;
+    const size_t bytes = size_t(n) * 48 + size_t(ns) * n * 24 + 8192;
     Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
     double* s64 = cv.take<double>(n);
     double* y64 = cv.take<double>(n);
@@ -960,6 +1069,7 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
     if (mode == MOSES_MODE_RATIO && keep >= m->P) {
       MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
     } else {
+      ProfScope ps(P_SELECT, m->st);
       lottery_select(m->w, m->g, m->P, mode, float(value), keep, m->sel, m->mask, nullptr, false, m->st);
       note_launch(mode == MOSES_MODE_RATIO ? 8 : 3);
     }
@@ -1063,12 +1173,12 @@ MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hs, int6
     Scratch& sc = scratch();
     std::lock_guard<std::mutex> lk(sc.mu);
     const long long R = ms + nt;
-    const size_t bytes = size_t(R) * width * 12 + size_t(R) * 16 + size_t(width) * 16 + 8192;
+    const size_t bytes = size_t(R) * width * 12 + size_t(R) * 16 + size_t(width) * 16 + column_dot_ws_floats(R, width) * 4 + 16384;
     Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
     double* h64 = cv.take<double>(R * width);
     float* H = cv.take<float>(R * width);
     float* z = cv.take<float>(R);
-    float* ws = cv.take<float>(round_up(R, 64) + round_up(width + 1, 64) + 64);
+    float* ws = cv.take<float>(round_up(R, 64) + round_up(width + 1, 64) + 64 + 16 + column_dot_ws_floats(R, width) + 64);
     double* dl = cv.take<double>(2);
     MOSES_CUDA(cudaMemcpyAsync(h64, hs, 8 * ms * width, cudaMemcpyHostToDevice, sc.st));
     MOSES_CUDA(cudaMemcpyAsync(h64 + ms * width, ht, 8 * nt * width, cudaMemcpyHostToDevice, sc.st));
@@ -1116,7 +1226,10 @@ MOSES_API int moses_topk_device(const float* scores, int64_t n, int64_t k, int64
     long long* oi = cv.take<long long>(kTopkMax);
     SelectWs ws;
     select_ws_carve(selbase, n, &ws);
-    topk_select(scores, n, k, ws, ok, oi, sc.st);
+    {
+      ProfScope ps(P_TOPK, sc.st);
+      topk_select(scores, n, k, ws, ok, oi, sc.st);
+    }
     note_launch(10);
     MOSES_CUDA(cudaMemcpyAsync(idx_out, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
     MOSES_CUDA(cudaStreamSynchronize(sc.st));
@@ -1329,3 +1442,39 @@ MOSES_API int moses_model_stream(moses_model_t m, void** stream) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- test hook: one raw GEMM on device buffers
+extern "C" MOSES_API int moses_debug_gemm(int elem, int M, int N, int K, const void* A, long long lda, int a_mn,
+                                          const void* B, long long ldb, int b_mn, int epi, void* out, long long ldo,
+                                          const float* bias, int relu, int bn, const void* mask, long long ldm) {
+  return guarded([&] {
+    GemmCall c{};
+    c.M = M;
+    c.N = N;
+    c.K = K;
+    c.A = {A, lda, a_mn != 0};
+    c.B = {B, ldb, b_mn != 0};
+    c.epi = EpiKind(epi);
+    c.out = out;
+    c.ldo = ldo;
+    c.bias = bias;
+    c.relu = relu;
+    c.bn = bn;
+    c.mask = mask;
+    c.ldm = ldm;
+    launch_gemm(elem, c, nullptr);
+    note_launch(1);
+    MOSES_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+namespace moses {
+extern int g_mn_swz[2], g_mn_layout[2], g_mn_sbo[2], g_mn_kstep[2];
+}
+extern "C" MOSES_API int moses_debug_set_mn(int which, int swz, int layout, int sbo, int kstep) {
+  moses::g_mn_swz[which] = swz;
+  moses::g_mn_layout[which] = layout;
+  moses::g_mn_sbo[which] = sbo;
+  moses::g_mn_kstep[which] = kstep;
+  return 0;
+}

@@ -55,6 +55,21 @@ struct GemmCall {
   const void* mask = nullptr;
   long long ldm = 0;
   int bn = 0;  // 0 = auto
+  int round_out = 1;  // fp32 outputs: round to tf32 (operand of the next kind::tf32 GEMM)
+};
+
+// ---------------------------------------------------------------- device-time profiler (capi.cu)
+// Optional per-category CUDA-event brackets around launches (off by default; a separate
+// profiling pass of bench.py turns it on to attribute step time to kernel classes).
+enum ProfCat : int {
+  P_GEMM_FWD = 0, P_GEMM_DGRAD, P_GEMM_WGRAD, P_RANK, P_HEAD, P_UPDATE, P_SELECT, P_TOPK, P_OTHER, P_NCAT
+};
+struct ProfScope {
+  int cat;
+  cudaStream_t st;
+  int idx = -1;
+  ProfScope(int c, cudaStream_t s);
+  ~ProfScope();
 };
 
 // elem = 2 (bf16, kind::f16) or 4 (fp32 operands, kind::tf32). Returns the N tile used.

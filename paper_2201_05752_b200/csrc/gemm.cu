@@ -7,6 +7,15 @@
 #include "gemm.cuh"
 
 namespace moses {
+// MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
+// swizzle (8 K-rows per 1024-B atom). 32-bit MN-major operands need the 32-byte-atom variant: TMA
+// SWIZZLE_128B_ATOM_32B on the load side and descriptor layout SWIZZLE_128B_BASE32B (type 1) with
+// 4-row (512-B) K atoms on the MMA side — the plain 128-B swizzle makes kind::tf32 read zeros
+// (measured on B200, tools/debug_tf32mn.py).
+int g_mn_swz[2] = {int(CU_TENSOR_MAP_SWIZZLE_128B), int(CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)};
+int g_mn_layout[2] = {2, 1};
+int g_mn_sbo[2] = {1024, 512};
+int g_mn_kstep[2] = {16 * 128, 8 * 128};
 namespace {
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -30,7 +39,7 @@ EncodeTiledFn encode_fn() {
 // 2-D tiled map over a row-major matrix: `inner` contiguous elements per row,
 // `outer` rows, row stride `ld` elements; box = box_inner x box_outer, 128-B swizzle.
 CUtensorMap make_map(const void* base, int elem, long long inner, long long outer, long long ld, int box_inner,
-                     int box_outer) {
+                     int box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
   const cuuint64_t strides[1] = {cuuint64_t(ld) * elem};
@@ -40,7 +49,7 @@ CUtensorMap make_map(const void* base, int elem, long long inner, long long oute
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem) & 15))
     fail(MOSES_ERR_INVALID_ARG, "TMA operand must be 16-byte aligned with a 16-byte row stride");
   const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(MOSES_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return m;
@@ -49,7 +58,8 @@ CUtensorMap make_map(const void* base, int elem, long long inner, long long oute
 // operand map: rows of the GEMM dimension `mn` (size MN), K along the other axis
 CUtensorMap operand_map(const Operand& o, int elem, long long MN, long long K, int tile_mn) {
   const int chunk = 128 / elem;  // elements in one 128-B swizzle row
-  if (o.mn_major) return make_map(o.ptr, elem, MN, K, o.ld, chunk, chunk /* BK */);
+  if (o.mn_major)
+    return make_map(o.ptr, elem, MN, K, o.ld, chunk, chunk /* BK */, CUtensorMapSwizzle(g_mn_swz[elem == 4]));
   return make_map(o.ptr, elem, K, MN, o.ld, chunk, tile_mn);
 }
 
@@ -80,6 +90,10 @@ void launch_t(const GemmCall& c, cudaStream_t s) {
   a.head_ld = c.head_ld;
   a.mask = c.mask;
   a.ldm = c.ldm;
+  a.mn_layout = g_mn_layout[elem == 4];
+  a.mn_sbo = g_mn_sbo[elem == 4];
+  a.mn_kstep = g_mn_kstep[elem == 4];
+  a.round_out = c.round_out;
   dim3 grid(ceil_div(c.M, Cfg::BM), ceil_div(c.N, BN));
   kern<<<grid, 128, Cfg::kSmemBytes, s>>>(ta, tb, a);
   MOSES_CUDA(cudaGetLastError());

@@ -41,7 +41,17 @@ struct GemmArgs {
   long long head_ld;
   const void* mask;     // Dgrad: T*, ReLU' source H_prev[m * ldm + n]
   long long ldm;
+  int mn_layout;        // descriptor layout type for MN-major operands (2 = SW128, 1 = SW128_BASE32B)
+  int mn_sbo;           // SBO bytes for MN-major operands
+  int mn_kstep;         // bytes advanced per MMA K step for MN-major operands
+  int round_out;        // fp32 Fwd/Dgrad outputs rounded to tf32 (next GEMM operand)
 };
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 template <typename T>
 struct UmmaType;
@@ -146,9 +156,9 @@ __global__ void __launch_bounds__(128, 1)
         const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
-          const uint64_t ad = A_MN ? ptx::sw128_desc(sa + kk * UK * 128, BK * 128, 1024)
+          const uint64_t ad = A_MN ? ptx::sw128_desc(sa + kk * args.mn_kstep, BK * 128, args.mn_sbo, args.mn_layout)
                                    : ptx::sw128_desc(sa + kk * UK * int(sizeof(T)), 16, 1024);
-          const uint64_t bd = B_MN ? ptx::sw128_desc(sb + kk * UK * 128, BK * 128, 1024)
+          const uint64_t bd = B_MN ? ptx::sw128_desc(sb + kk * args.mn_kstep, BK * 128, args.mn_sbo, args.mn_layout)
                                    : ptx::sw128_desc(sb + kk * UK * int(sizeof(T)), 16, 1024);
           const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
           if constexpr (sizeof(T) == 2) ptx::umma_f16(tmem_base, ad, bd, kIdesc, acc);
@@ -243,6 +253,10 @@ __global__ void __launch_bounds__(128, 1)
             if (j < nvalid) orow[j] = __float2bfloat16_rn(v[j]);
         }
       } else {
+        if (args.round_out) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = tf32_round(v[j]);  // next layer's kind::tf32 operand
+        }
         if (nvalid == 32) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);

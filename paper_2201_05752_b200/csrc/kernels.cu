@@ -19,10 +19,25 @@ __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <typename T>
 __device__ __forceinline__ T from_f(float v);
+__device__ __forceinline__ float tf32_rna(float x);
 template <>
-__device__ __forceinline__ float from_f<float>(float v) { return v; }
+__device__ __forceinline__ float from_f<float>(float v) { return tf32_rna(v); }  // fp32 activations feed kind::tf32
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Round-to-nearest tf32 (the tensor core drops the low 13 mantissa bits of a kind::tf32
+// operand; pre-rounding keeps the error unbiased).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// operand shadow of the master parameters: 0 none, 1 bf16, 2 tf32-rounded fp32
+template <int KIND>
+__device__ __forceinline__ void store_shadow(void* sh, long long i, float w) {
+  if constexpr (KIND == 1) static_cast<__nv_bfloat16*>(sh)[i] = __float2bfloat16_rn(w);
+  if constexpr (KIND == 2) static_cast<float*>(sh)[i] = tf32_rna(w);
+}
 
 int grid_for(long long n, int block, int per_sm = 8) {
   long long g = (n + block - 1) / block;
@@ -113,47 +128,59 @@ __global__ void head_scores_kernel(const float* __restrict__ part, int ntiles, l
 //   y_j > y_i : i is "lo": gs_i += sigma(-(s_j - s_i))
 // Each distinct-label pair is counted once (at its hi row), as in the reference's i<j loop.
 constexpr int kRankBlock = 128;
-constexpr int kRankChunk = 512;
+constexpr int kRankChunk = 32;  // j columns per block: n=512 -> 4 x 16 blocks, n=4096 -> 32 x 128
 __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __restrict__ s, const float* __restrict__ y,
                                                                 long long n, double* gs_part, double* loss_part,
                                                                 long long* pairs_part) {
-  __shared__ float ss[kRankBlock], sy[kRankBlock];
+  __shared__ float ss[kRankChunk], sy[kRankChunk];
   const long long i = blockIdx.x * (long long)kRankBlock + threadIdx.x;
   const long long j0 = (long long)blockIdx.y * kRankChunk;
-  const long long j1 = min(n, j0 + kRankChunk);
-  const bool ok = i < n;
-  const float si = ok ? s[i] : 0.f, yi = ok ? y[i] : 0.f;
-  double gs = 0.0, loss = 0.0;
-  long long pairs = 0;
-  for (long long jt = j0; jt < j1; jt += kRankBlock) {
-    const long long j = jt + threadIdx.x;
-    __syncthreads();
-    ss[threadIdx.x] = j < j1 ? s[j] : 0.f;
-    sy[threadIdx.x] = j < j1 ? y[j] : 0.f;
-    __syncthreads();
-    const int cnt = int(min((long long)kRankBlock, j1 - jt));
-    if (!ok) continue;
-    for (int q = 0; q < cnt; ++q) {
-      const float yj = sy[q];
-      if (yi == yj) continue;
-      const bool hi = yi > yj;
-      const float d = hi ? si - ss[q] : ss[q] - si;  // s_hi - s_lo
-      const float e = expf(-fabsf(d));
-      const float sig_neg = d >= 0.f ? e / (1.f + e) : 1.f / (1.f + e);
-      if (hi) {
-        gs -= sig_neg;
-        loss += d >= 0.f ? log1pf(e) : -d + log1pf(e);
-        ++pairs;
-      } else {
-        gs += sig_neg;
-      }
+  const int cnt = int(min((long long)kRankChunk, n - j0));
+  if (threadIdx.x < cnt) {
+    ss[threadIdx.x] = s[j0 + threadIdx.x];
+    sy[threadIdx.x] = y[j0 + threadIdx.x];
+  }
+  __syncthreads();
+  if (i >= n) return;
+  const float si = s[i], yi = y[i];
+  float gs = 0.f, loss = 0.f;
+  int pairs = 0;
+#pragma unroll 4
+  for (int q = 0; q < cnt; ++q) {
+    const float yj = sy[q];
+    if (yi == yj) continue;
+    const bool hi = yi > yj;
+    const float d = hi ? si - ss[q] : ss[q] - si;  // s_hi - s_lo
+    const float e = __expf(-fabsf(d));
+    const float inv = __frcp_rn(1.f + e);
+    const float sig_neg = d >= 0.f ? e * inv : inv;  // sigma(-d)
+    if (hi) {
+      gs -= sig_neg;
+      loss += (d >= 0.f ? 0.f : -d) + log1pf(e);
+      ++pairs;
+    } else {
+      gs += sig_neg;
     }
   }
-  if (ok) {
-    const long long o = (long long)blockIdx.y * n + i;
-    gs_part[o] = gs;
-    loss_part[o] = loss;
-    pairs_part[o] = pairs;
+  const long long o = (long long)blockIdx.y * n + i;
+  gs_part[o] = gs;
+  loss_part[o] = loss;
+  pairs_part[o] = pairs;
+}
+
+// per-row reduction of the split partials (fixed split order)
+__global__ void rank_rows_kernel(double* gs_part, double* loss_part, long long* pairs_part, int nsplit, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double g = 0.0, l = 0.0;
+    long long p = 0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      g += gs_part[sp * n + i];
+      l += loss_part[sp * n + i];
+      p += pairs_part[sp * n + i];
+    }
+    gs_part[i] = g;
+    loss_part[i] = l;
+    pairs_part[i] = p;
   }
 }
 
@@ -179,11 +206,10 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   __shared__ long long sh_pairs;
   long long p = 0;
   double l = 0.0;
-  for (long long i = threadIdx.x; i < n; i += kFinBlock)
-    for (int sp = 0; sp < nsplit; ++sp) {
-      p += pairs_part[sp * n + i];
-      l += loss_part[sp * n + i];
-    }
+  for (long long i = threadIdx.x; i < n; i += kFinBlock) {  // rows already reduced over splits
+    p += pairs_part[i];
+    l += loss_part[i];
+  }
   const long long ptot = BRL(tmpl).Sum(p);
   __syncthreads();
   const double ltot = BR(tmp).Sum(l);
@@ -197,11 +223,7 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   const long long R = roff + n;
   for (long long r = threadIdx.x; r < R; r += kFinBlock) {
     float a = 0.f;
-    if (r >= roff) {
-      double g = 0.0;
-      for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + (r - roff)];
-      a = pairs > 0 ? float(g * inv) : 0.f;
-    }
+    if (r >= roff) a = pairs > 0 ? float(gs_part[r - roff] * inv) : 0.f;
     coefA[r] = a;
     coefB[r] = 0.f;
   }
@@ -253,33 +275,42 @@ __global__ void head_backward_kernel(const float* __restrict__ coefA, const floa
   }
 }
 
-// g[j] = sum_r coef[r] * H[r][j]; g[W] = sum_r coef[r]. 32 columns x 8 row-lanes per block.
+// g[j] = sum_r coef[r] * H[r][j]; g[W] = sum_r coef[r]. Pass 1: block (32 columns x 8 row-lanes) over a
+// 64-row slab -> partial[slab][j]; pass 2 sums the slabs in order. Deterministic.
+constexpr int kColSlab = 64;
 template <typename T>
 __global__ void column_dot_kernel(const float* __restrict__ coef, const T* __restrict__ H, long long ldh, long long R, int W,
-                                  float* __restrict__ g) {
+                                  float* __restrict__ part) {
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
+  const long long r0 = (long long)blockIdx.y * kColSlab, r1 = min(R, r0 + kColSlab);
   float acc = 0.f;
   if (j < W)
-    for (long long r = ty; r < R; r += 8) acc = fmaf(coef[r], to_f(H[r * ldh + j]), acc);
+    for (long long r = r0 + ty; r < r1; r += 8) acc = fmaf(coef[r], to_f(H[r * ldh + j]), acc);
   else if (j == W)
-    for (long long r = ty; r < R; r += 8) acc += coef[r];
+    for (long long r = r0 + ty; r < r1; r += 8) acc += coef[r];
   red[ty][tx] = acc;
   __syncthreads();
   if (ty == 0 && j <= W) {
     float s = red[0][tx];
     for (int k = 1; k < 8; ++k) s += red[k][tx];
+    part[(long long)blockIdx.y * (W + 1) + j] = s;
+  }
+}
+__global__ void column_sum_kernel(const float* __restrict__ part, int slabs, int W1, float* __restrict__ g) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < W1; j += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < slabs; ++q) s += part[(long long)q * W1 + j];
     g[j] = s;
   }
 }
 
 // ---------------------------------------------------------------- updates (no FMA contraction: reference
 // is built with -ffp-contract=off, so v = mu*v + g and w -= lr*v round after every op)
-template <bool MOM, bool MASK, bool SHADOW>
+template <bool MOM, bool MASK, int SHADOW>
 __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
-                           const uint8_t* __restrict__ mask, long long P, float lr, float mu,
-                           __nv_bfloat16* __restrict__ shadow) {
+                           const uint8_t* __restrict__ mask, long long P, float lr, float mu, void* __restrict__ shadow) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
     if (!MASK || mask[i]) {
@@ -292,14 +323,14 @@ __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const f
       }
       w[i] = wi;
     }
-    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+    store_shadow<SHADOW>(shadow, i, wi);
   }
 }
 
-template <bool SHADOW>
+template <int SHADOW>
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m1, float* __restrict__ m2, const float* __restrict__ g,
                             const uint8_t* __restrict__ mask, long long P, float lr, float b1, float b2, float eps,
-                            float c1, float c2, __nv_bfloat16* __restrict__ shadow) {
+                            float c1, float c2, void* __restrict__ shadow) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
     if (mask == nullptr || mask[i]) {
@@ -313,20 +344,20 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m1, float
       wi = __fsub_rn(wi, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
       w[i] = wi;
     }
-    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+    store_shadow<SHADOW>(shadow, i, wi);
   }
 }
 
-template <bool SHADOW>
+template <int SHADOW>
 __global__ void decay_kernel(float* __restrict__ w, const uint8_t* __restrict__ mask, long long P, float factor,
-                             __nv_bfloat16* __restrict__ shadow) {
+                             void* __restrict__ shadow) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
     if (!mask[i]) {
       wi = __fmul_rn(wi, factor);
       w[i] = wi;
     }
-    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+    store_shadow<SHADOW>(shadow, i, wi);
   }
 }
 
@@ -531,10 +562,10 @@ __global__ void xi_normalize_kernel(float* xi, long long n, const SelState* st) 
 // Fused transferable step + variant decay on the mask (lottery.cpp:92-120):
 //   kept:   w -= alpha * g     (apply_update, no momentum)
 //   else:   w *= (1 - alpha*lambda)
-template <bool SHADOW>
+template <int SHADOW>
 __global__ void lottery_apply_kernel(float* __restrict__ w, const float* __restrict__ g, const uint8_t* __restrict__ mask,
                                      long long n, float alpha, float factor, bool step, bool decay,
-                                     __nv_bfloat16* __restrict__ shadow) {
+                                     void* __restrict__ shadow) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
     if (mask[i]) {
@@ -543,8 +574,17 @@ __global__ void lottery_apply_kernel(float* __restrict__ w, const float* __restr
       wi = __fmul_rn(wi, factor);
     }
     w[i] = wi;
-    if (SHADOW) shadow[i] = __float2bfloat16_rn(wi);
+    store_shadow<SHADOW>(shadow, i, wi);
   }
+}
+
+__global__ void shadow_kernel1(const float* w, long long n, void* sh) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    store_shadow<1>(sh, i, w[i]);
+}
+__global__ void shadow_kernel2(const float* w, long long n, void* sh) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    store_shadow<2>(sh, i, w[i]);
 }
 
 __global__ void popcount_kernel(const uint8_t* __restrict__ mask, long long n, unsigned long long* out) {
@@ -787,7 +827,8 @@ __global__ void synth_features_kernel(unsigned long long seed, long long row0, l
     T* row = dst + r * ld;
     for (int c = 0; c < ld; ++c) {
       const float v = c < D ? float(u01(splitmix_at(key, (unsigned long long)c + 1))) : (c == D ? 1.f : 0.f);
-      row[c] = from_f<T>(v);
+      if constexpr (sizeof(T) == 4) row[c] = v;  // bit-identical to the oracle generator
+      else row[c] = from_f<T>(v);
     }
   }
 }
@@ -837,6 +878,12 @@ void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s) {
   f64_to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
   MOSES_CUDA(cudaGetLastError());
 }
+void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s) {
+  if (n <= 0 || sh.kind == 0) return;
+  if (sh.kind == 1) shadow_kernel1<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
+  else shadow_kernel2<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
+  MOSES_CUDA(cudaGetLastError());
+}
 void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s) {
   if (n <= 0) return;
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
@@ -868,8 +915,9 @@ int rank_splits(long long n) { return n <= 0 ? 1 : ceil_div(n, kRankChunk); }
 
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st) {
   if (n <= 0) return;
-  dim3 grid(ceil_div(n, kRankBlock), ws.nsplit);
+  dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
   rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, y, n, ws.gs_part, ws.loss_part, ws.pairs_part);
+  rank_rows_kernel<<<grid_for(n, 256), 256, 0, st>>>(ws.gs_part, ws.loss_part, ws.pairs_part, int(grid.y), n);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -890,39 +938,49 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
 }
 
 template <typename T>
-void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, cudaStream_t st) {
-  column_dot_kernel<T><<<ceil_div(W + 1, 32), 256, 0, st>>>(coef, H, ldh, R, W, g);
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st) {
+  const int slabs = R > 0 ? ceil_div(R, kColSlab) : 1;
+  if (R <= 0) {
+    MOSES_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (W + 1), st));
+    return;
+  }
+  column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(coef, H, ldh, R, W, ws);
+  column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(ws, slabs, W + 1, g);
   MOSES_CUDA(cudaGetLastError());
 }
+size_t column_dot_ws_floats(long long R, int W) { return size_t(R > 0 ? ceil_div(R, kColSlab) : 1) * (W + 1); }
 
 void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
-                __nv_bfloat16* shadow, cudaStream_t st) {
+                Shadow sh, cudaStream_t st) {
   const int grid = grid_for(P, 256);
-#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, shadow)
-  const bool k = mask != nullptr, s = shadow != nullptr;
+#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr)
+#define SGD_K(M, K) \
+  if (sh.kind == 1) SGD_LAUNCH(M, K, 1); else if (sh.kind == 2) SGD_LAUNCH(M, K, 2); else SGD_LAUNCH(M, K, 0)
+  const bool k = mask != nullptr;
   if (momentum) {
-    if (k) { if (s) SGD_LAUNCH(true, true, true); else SGD_LAUNCH(true, true, false); }
-    else { if (s) SGD_LAUNCH(true, false, true); else SGD_LAUNCH(true, false, false); }
+    if (k) { SGD_K(true, true); } else { SGD_K(true, false); }
   } else {
-    if (k) { if (s) SGD_LAUNCH(false, true, true); else SGD_LAUNCH(false, true, false); }
-    else { if (s) SGD_LAUNCH(false, false, true); else SGD_LAUNCH(false, false, false); }
+    if (k) { SGD_K(false, true); } else { SGD_K(false, false); }
   }
+#undef SGD_K
 #undef SGD_LAUNCH
   MOSES_CUDA(cudaGetLastError());
 }
 
 void adam_update(float* w, float* m1, float* m2, const float* g, const uint8_t* mask, long long P, float lr, float b1,
-                 float b2, float eps, float c1, float c2, __nv_bfloat16* shadow, cudaStream_t st) {
+                 float b2, float eps, float c1, float c2, Shadow sh, cudaStream_t st) {
   const int grid = grid_for(P, 256);
-  if (shadow) adam_kernel<true><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, shadow);
-  else adam_kernel<false><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, shadow);
+  if (sh.kind == 1) adam_kernel<1><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, sh.ptr);
+  else if (sh.kind == 2) adam_kernel<2><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, sh.ptr);
+  else adam_kernel<0><<<grid, 256, 0, st>>>(w, m1, m2, g, mask, P, lr, b1, b2, eps, c1, c2, sh.ptr);
   MOSES_CUDA(cudaGetLastError());
 }
 
-void variant_decay(float* w, const uint8_t* mask, long long P, float factor, __nv_bfloat16* shadow, cudaStream_t st) {
+void variant_decay(float* w, const uint8_t* mask, long long P, float factor, Shadow sh, cudaStream_t st) {
   const int grid = grid_for(P, 256);
-  if (shadow) decay_kernel<true><<<grid, 256, 0, st>>>(w, mask, P, factor, shadow);
-  else decay_kernel<false><<<grid, 256, 0, st>>>(w, mask, P, factor, shadow);
+  if (sh.kind == 1) decay_kernel<1><<<grid, 256, 0, st>>>(w, mask, P, factor, sh.ptr);
+  else if (sh.kind == 2) decay_kernel<2><<<grid, 256, 0, st>>>(w, mask, P, factor, sh.ptr);
+  else decay_kernel<0><<<grid, 256, 0, st>>>(w, mask, P, factor, sh.ptr);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -1039,10 +1097,11 @@ void partition_from_xi(const float* xi, long long n, int mode, float theta, long
 }
 
 void lottery_apply(float* w, const float* g, const uint8_t* mask, long long n, float alpha, float factor, bool step,
-                   bool decay, __nv_bfloat16* shadow, cudaStream_t st) {
+                   bool decay, Shadow sh, cudaStream_t st) {
   const int grid = grid_for(n, 256);
-  if (shadow) lottery_apply_kernel<true><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, shadow);
-  else lottery_apply_kernel<false><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, shadow);
+  if (sh.kind == 1) lottery_apply_kernel<1><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, sh.ptr);
+  else if (sh.kind == 2) lottery_apply_kernel<2><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, sh.ptr);
+  else lottery_apply_kernel<0><<<grid, 256, 0, st>>>(w, g, mask, n, alpha, factor, step, decay, sh.ptr);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -1085,7 +1144,13 @@ void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, l
   float* du = ws + round_up(m + n, 64);             // [W+1]
   double* dc = reinterpret_cast<double*>(du + round_up(W + 1, 64));
   adv_logits_kernel<<<1, kFinBlock, 0, st>>>(part2, ntiles, ld2, m, n, c, dz, loss_out, dc);
-  column_dot_kernel<T><<<ceil_div(W + 1, 32), 256, 0, st>>>(dz, H, ldh, m + n, W, du);
+  {
+    const long long R = m + n;
+    const int slabs = ceil_div(R, kColSlab);
+    float* part = reinterpret_cast<float*>(dc + 8);
+    column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(dz, H, ldh, R, W, part);
+    column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(part, slabs, W + 1, du);
+  }
   adv_update_kernel<<<ceil_div(W, 256), 256, 0, st>>>(u, c, du, W, eta, dc);
   MOSES_CUDA(cudaGetLastError());
 }
@@ -1144,7 +1209,7 @@ void synth_labels(unsigned long long seed, long long row0, long long n, float* d
   template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t);                       \
   template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
                                  long long, int, T*, long long, cudaStream_t);                                    \
-  template void column_dot<T>(const float*, const T*, long long, long long, int, float*, cudaStream_t);           \
+  template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t);   \
   template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \
                                   float*, float*, float, double*, float*, cudaStream_t);                          \
   template void segment_sum<T>(const T*, long long, int, const long long*, long long, float*, long long,          \

@@ -4,6 +4,14 @@
 
 namespace moses {
 
+// Operand shadow of the fp32 master parameters written by every update kernel:
+// kind 0 none, 1 bf16 (kind::f16 operand), 2 tf32-rounded fp32 (kind::tf32 operand).
+struct Shadow {
+  void* ptr;
+  int kind;
+};
+void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s);
+
 // ---- data movement
 template <typename T>
 void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s);
@@ -51,14 +59,15 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
                    long long R, int W, T* dz, long long ldz, cudaStream_t st);
 // g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
 template <typename T>
-void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, cudaStream_t st);
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st);
+size_t column_dot_ws_floats(long long R, int W);
 
 // ---- updates (model.cpp:263-296, lottery.cpp:92-120)
 void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
-                __nv_bfloat16* shadow, cudaStream_t st);
+                Shadow shadow, cudaStream_t st);
 void adam_update(float* w, float* m1, float* m2, const float* g, const uint8_t* mask, long long P, float lr, float b1,
-                 float b2, float eps, float c1, float c2, __nv_bfloat16* shadow, cudaStream_t st);
-void variant_decay(float* w, const uint8_t* mask, long long P, float factor, __nv_bfloat16* shadow, cudaStream_t st);
+                 float b2, float eps, float c1, float c2, Shadow shadow, cudaStream_t st);
+void variant_decay(float* w, const uint8_t* mask, long long P, float factor, Shadow shadow, cudaStream_t st);
 
 // ---- lottery mask identification (lottery.cpp:35-90), fused with step + decay
 struct SelectWs {
@@ -76,7 +85,7 @@ void select_ws_carve(void* base, long long n, SelectWs* ws);
 void lottery_select(const float* w_in, const float* g, long long n, int mode, float theta, long long keep,
                     const SelectWs& ws, uint8_t* mask_out, float* xi_out, bool normalize_xi, cudaStream_t st);
 void lottery_apply(float* w, const float* g, const uint8_t* mask, long long n, float alpha, float factor, bool step,
-                   bool decay, __nv_bfloat16* shadow, cudaStream_t st);
+                   bool decay, Shadow shadow, cudaStream_t st);
 void xi_scores(const float* w, const float* g, long long n, bool normalize, const SelectWs& ws, float* xi_out,
                cudaStream_t st);
 // mask from given xi (identical-input parity path)

@@ -82,6 +82,10 @@ def lib():
         "moses_predict_device": (C.c_int, [vp, vp, i32, i64, i64, vp]),
         "moses_predict_pooled": (C.c_int, [vp, vp, i64, i32, vp, i64, vp]),
         "moses_gradients": (C.c_int, [vp, vp, vp, i64, i32, vp, dbl, vp]),
+        "moses_gradients_device": (C.c_int, [vp, vp, i64, vp, i64, vp]),
+        "moses_set_async": (C.c_int, [i32]),
+        "moses_profile_begin": (C.c_int, []),
+        "moses_profile_end": (C.c_int, [vp, vp, i32]),
         "moses_gradients_download": (C.c_int, [vp, vp, i64]),
         "moses_gradients_upload": (C.c_int, [vp, vp, i64]),
         "moses_objective": (C.c_int, [vp, vp, vp, i64, i32, vp, dbl, vp]),
@@ -119,6 +123,8 @@ def lib():
         "moses_read_mask": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, vp]),
         "moses_model_device_ptrs": (C.c_int, [vp, vp, vp, vp]),
         "moses_model_stream": (C.c_int, [vp, vp]),
+        "moses_debug_gemm": (C.c_int, [C.c_int] * 4 + [vp, C.c_longlong, C.c_int, vp, C.c_longlong, C.c_int, C.c_int,
+                                                       vp, C.c_longlong, vp, C.c_int, C.c_int, vp, C.c_longlong]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -151,6 +157,20 @@ def _dims(dims):
 
 def kernel_launches() -> int:
     return lib().moses_kernel_launches()
+
+
+PROFILE_CATS = ["gemm_fwd", "gemm_dgrad", "gemm_wgrad", "rank", "head", "update", "select", "topk", "other"]
+
+
+def profile_begin():
+    _ck(lib().moses_profile_begin())
+
+
+def profile_end() -> dict:
+    ms = np.zeros(len(PROFILE_CATS))
+    cnt = np.zeros(len(PROFILE_CATS), dtype=np.int64)
+    _ck(lib().moses_profile_end(_p(ms), _p(cnt), len(PROFILE_CATS)))
+    return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROFILE_CATS)}
 
 
 # ---------------------------------------------------------------- values (model.hpp:19-48)
