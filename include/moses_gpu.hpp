@@ -1,0 +1,301 @@
+// moses_gpu.hpp — header-only C++ host layer over the C ABI (moses_gpu.h).
+//
+// Mirrors the reference's namespace moseslab hot-path API
+// (/root/reference/proj/include/moseslab/{model,lottery,search}.hpp): same function
+// names, argument meaning and error behaviour (throws moseslab_gpu::Error carrying the
+// reference's ErrorCode). Eigen is not a dependency: matrices are row-major
+// std::vector<double> views; CostModelParams keeps the reference's flat parameter order
+// (lottery.hpp:13-14), so a caller holding Eigen data maps it without reordering
+// weights (only feature matrices are transposed, column-major -> row-major).
+//
+// Link: -L<pkg> -lmoses_gpu   (paper_2201_05752_b200/libmoses_gpu.so)
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <utility>
+#include <vector>
+
+#include "moses_gpu.h"
+
+namespace moseslab_gpu {
+
+// moseslab::ErrorCode (errors.hpp:10-36)
+enum class ErrorCode {
+  InvalidTask, InvalidConfig, SpaceTooLarge, ImmutableSpace, BadDims, DimMismatch, ShapeMismatch,
+  VersionMismatch, CorruptStream, EmptyDataset, InvalidRatio, UnnormalizedThreshold, AdversaryDisabled,
+  UnstableDecay, InfeasibleSplit, ZeroMean, InsufficientBatches, BudgetInfeasible, MissingReferenceStrategy,
+  MismatchedRuns, EmptyRows, ParseError, MissingField, IoError, UsageError,
+  // library-side (not in the reference)
+  Cuda = 100, NoDevice, Capacity, InvalidArgument
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(int status, const std::string& msg)
+      : std::runtime_error(msg), code_(status < 100 ? ErrorCode(status - 1) : ErrorCode(status)) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+inline void check(int status) {
+  if (status != MOSES_OK) throw Error(status, moses_last_error());
+}
+
+struct Matrix {  // row-major n x d
+  int64_t rows = 0;
+  int32_t cols = 0;
+  std::vector<double> data;
+  Matrix() = default;
+  Matrix(int64_t r, int32_t c) : rows(r), cols(c), data(size_t(r) * c, 0.0) {}
+  double& operator()(int64_t r, int32_t c) { return data[size_t(r) * cols + c]; }
+  double operator()(int64_t r, int32_t c) const { return data[size_t(r) * cols + c]; }
+};
+
+struct CostModelParams {  // model.hpp:19-25, flat reference order
+  std::vector<int32_t> dims;
+  std::vector<double> params;
+  std::vector<double> momentum;
+};
+
+struct TrainHyper {  // model.hpp:27-35
+  double learning_rate = 0.001;
+  double weight_decay = 0.01;
+  int max_epochs = 30;
+  int batch_size = 512;
+  double momentum = 0.9;
+  double adversary_beta = 0.01;
+  uint64_t seed = 0;
+};
+
+struct RankingBatch {  // model.hpp:39-43
+  Matrix features;
+  std::vector<double> labels;
+  std::string task_id;
+};
+
+enum class PartitionMode { Threshold = MOSES_MODE_THRESHOLD, Ratio = MOSES_MODE_RATIO };
+
+struct XiScores {  // lottery.hpp:15-18
+  std::vector<double> xi;
+  bool normalized = false;
+};
+
+struct ParamMask {  // lottery.hpp:25-32
+  std::vector<uint8_t> transferable;
+  int phase = 0;
+  PartitionMode mode = PartitionMode::Ratio;
+  double value = 0.0;
+  int64_t popcount() const {
+    int64_t c = 0;
+    for (uint8_t b : transferable) c += b != 0;
+    return c;
+  }
+};
+
+inline int64_t param_count(const std::vector<int32_t>& dims) {
+  const int64_t n = moses_param_count(dims.data(), int32_t(dims.size()));
+  if (n < 0) check(int(-n));
+  return n;
+}
+
+inline CostModelParams init_random(const std::vector<int32_t>& dims, uint64_t seed, bool strict = true) {
+  CostModelParams p;
+  p.dims = dims;
+  const int64_t P = param_count(dims);  // validates dims (BadDims)
+  p.params.assign(size_t(P), 0.0);
+  p.momentum.assign(size_t(P), 0.0);
+  check(moses_init_random(dims.data(), int32_t(dims.size()), seed, strict ? 1 : 0, p.params.data()));
+  return p;
+}
+
+// Device-resident model: one CUDA stream and workspaces per handle.
+class DeviceModel {
+ public:
+  explicit DeviceModel(const CostModelParams& p, int precision = MOSES_PREC_TF32, int64_t max_rows = 4096)
+      : dims_(p.dims), P_(param_count(p.dims)) {
+    moses_model_t h = nullptr;
+    check(moses_model_create(dims_.data(), int32_t(dims_.size()), precision, max_rows, &h));
+    h_.reset(h);
+    upload(p);
+  }
+  void upload(const CostModelParams& p) {
+    check(moses_model_upload(h_.get(), p.params.data(), p.momentum.empty() ? nullptr : p.momentum.data(), P_));
+  }
+  CostModelParams download() const {
+    CostModelParams p{dims_, std::vector<double>(size_t(P_)), std::vector<double>(size_t(P_))};
+    check(moses_model_download(h_.get(), p.params.data(), p.momentum.data(), P_));
+    return p;
+  }
+  std::vector<double> gradients() const {
+    std::vector<double> g(static_cast<size_t>(P_));
+    check(moses_gradients_download(h_.get(), g.data(), P_));
+    return g;
+  }
+  moses_model_t handle() const { return h_.get(); }
+  const std::vector<int32_t>& dims() const { return dims_; }
+  int64_t size() const { return P_; }
+
+ private:
+  struct Del {
+    void operator()(moses_model_t h) const { moses_model_destroy(h); }
+  };
+  std::vector<int32_t> dims_;
+  int64_t P_;
+  std::unique_ptr<moses_model, Del> h_;
+};
+
+class AdversaryState {  // lottery.hpp:36-42
+ public:
+  AdversaryState(const Matrix& replay, int penultimate_dim, double step_size = 0.1) : width_(penultimate_dim) {
+    moses_adversary_t h = nullptr;
+    check(moses_adversary_create(replay.data.data(), replay.rows, replay.cols, penultimate_dim, step_size, &h));
+    h_.reset(h);
+  }
+  std::vector<double> weight() const {
+    std::vector<double> w(static_cast<size_t>(width_));
+    double b = 0;
+    check(moses_adversary_get(h_.get(), w.data(), width_, &b));
+    return w;
+  }
+  double bias() const {
+    std::vector<double> w(static_cast<size_t>(width_));
+    double b = 0;
+    check(moses_adversary_get(h_.get(), w.data(), width_, &b));
+    return b;
+  }
+  moses_adversary_t handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(moses_adversary_t h) const { moses_adversary_destroy(h); }
+  };
+  int width_;
+  std::unique_ptr<moses_adversary, Del> h_;
+};
+
+// ---- model.hpp
+inline std::vector<double> predict(DeviceModel& m, const Matrix& x) {  // model.cpp:169-175
+  std::vector<double> s(static_cast<size_t>(x.rows));
+  check(moses_predict(m.handle(), x.data.data(), x.rows, x.cols, s.data()));
+  return s;
+}
+inline Matrix penultimate_activations(DeviceModel& m, const Matrix& x) {  // model.cpp:177-183
+  Matrix h(x.rows, m.dims()[m.dims().size() - 2]);
+  check(moses_penultimate(m.handle(), x.data.data(), x.rows, x.cols, h.data.data()));
+  return h;
+}
+inline double pairwise_ranking_loss(const std::vector<double>& s, const std::vector<double>& y) {
+  if (s.size() != y.size()) throw Error(1 + int(ErrorCode::DimMismatch), "scores/labels length mismatch");
+  double loss = 0;
+  int64_t pairs = 0;
+  check(moses_ranking_loss(s.data(), y.data(), int64_t(s.size()), &loss, &pairs));
+  return loss;
+}
+inline std::vector<double> gradients(DeviceModel& m, const RankingBatch& b, const AdversaryState* adv = nullptr,
+                                     double beta = 0.0, double* loss_out = nullptr) {  // model.cpp:192-244
+  if (int64_t(b.labels.size()) != b.features.rows)
+    throw Error(1 + int(ErrorCode::DimMismatch), "batch rows != label count");
+  check(moses_gradients(m.handle(), b.features.data.data(), b.labels.data(), b.features.rows, b.features.cols,
+                        adv ? adv->handle() : nullptr, beta, loss_out));
+  return m.gradients();
+}
+inline double objective(DeviceModel& m, const RankingBatch& b, const AdversaryState* adv = nullptr, double beta = 0.0) {
+  double out = 0;
+  check(moses_objective(m.handle(), b.features.data.data(), b.labels.data(), b.features.rows, b.features.cols,
+                        adv ? adv->handle() : nullptr, beta, &out));
+  return out;
+}
+// Uses the handle's device gradients (from the last gradients() call, or upload them first).
+inline void apply_update(DeviceModel& m, const TrainHyper& h, const ParamMask* mask = nullptr,
+                         bool use_momentum = false) {  // model.cpp:263-296
+  check(moses_apply_update(m.handle(), h.learning_rate, h.momentum, mask ? mask->transferable.data() : nullptr,
+                           mask ? int64_t(mask->transferable.size()) : 0, use_momentum ? 1 : 0));
+}
+inline double ranking_accuracy(DeviceModel& m, const std::vector<RankingBatch>& batches) {  // model.cpp:298-312
+  if (batches.empty()) return 0.0;
+  std::vector<double> x, y;
+  std::vector<int64_t> off{0};
+  const int32_t D = batches[0].features.cols;
+  for (const auto& b : batches) {
+    x.insert(x.end(), b.features.data.begin(), b.features.data.end());
+    y.insert(y.end(), b.labels.begin(), b.labels.end());
+    off.push_back(off.back() + b.features.rows);
+  }
+  double acc = 0;
+  int64_t pairs = 0, conc = 0;
+  check(moses_ranking_accuracy(m.handle(), x.data(), y.data(), off.data(), int32_t(batches.size()), D, &acc, &pairs,
+                               &conc));
+  return acc;
+}
+
+// ---- lottery.hpp
+inline XiScores xi_scores(DeviceModel& m, bool normalize) {  // lottery.cpp:35-57
+  XiScores out{std::vector<double>(size_t(m.size())), normalize};
+  check(moses_xi_scores(m.handle(), normalize ? 1 : 0, out.xi.data(), m.size()));
+  return out;
+}
+inline ParamMask partition(DeviceModel& m, const XiScores& xi, PartitionMode mode, double value, int phase) {
+  check(moses_xi_upload(m.handle(), xi.xi.data(), int64_t(xi.xi.size()), xi.normalized ? 1 : 0));
+  ParamMask mask{std::vector<uint8_t>(xi.xi.size()), phase, mode, value};
+  int64_t pop = 0;
+  check(moses_partition(m.handle(), int(mode), value, phase, mask.transferable.data(), int64_t(xi.xi.size()), &pop));
+  return mask;
+}
+inline void transferable_step(DeviceModel& m, const ParamMask& mask, double alpha) {  // lottery.cpp:92-97
+  check(moses_mask_upload(m.handle(), mask.transferable.data(), int64_t(mask.transferable.size())));
+  check(moses_transferable_step(m.handle(), alpha));
+}
+inline void variant_decay(DeviceModel& m, const ParamMask& mask, double alpha, double lambda) {  // lottery.cpp:99-120
+  check(moses_mask_upload(m.handle(), mask.transferable.data(), int64_t(mask.transferable.size())));
+  check(moses_variant_decay(m.handle(), alpha, lambda));
+}
+// tuner.cpp:258-262 fused on device: xi -> partition -> transferable_step -> variant_decay
+inline ParamMask lottery_step(DeviceModel& m, PartitionMode mode, double value, int phase, double alpha,
+                              double lambda) {
+  ParamMask mask{std::vector<uint8_t>(size_t(m.size())), phase, mode, value};
+  int64_t pop = 0;
+  check(moses_lottery_step(m.handle(), int(mode), value, phase, alpha, lambda, mask.transferable.data(), m.size(),
+                           &pop));
+  return mask;
+}
+inline double discriminator_cross_entropy(const std::vector<double>& zs, const std::vector<double>& zt) {
+  double out = 0;
+  check(moses_discriminator_cross_entropy(zs.data(), int64_t(zs.size()), zt.data(), int64_t(zt.size()), &out));
+  return out;
+}
+struct AdversarialResult {
+  double discriminator_loss = 0.0;
+  double confusion_contribution = 0.0;
+};
+inline AdversarialResult adversarial_term(AdversaryState& a, const Matrix& hs, const Matrix& ht, double beta) {
+  AdversarialResult r;
+  check(moses_adversarial_term(a.handle(), hs.data.data(), hs.rows, ht.data.data(), ht.rows,
+                               hs.rows ? hs.cols : ht.cols, beta, &r.discriminator_loss, &r.confusion_contribution));
+  return r;
+}
+
+// ---- search.hpp: candidate order (score desc, pool index asc) and select_batch
+inline std::vector<int64_t> topk(const std::vector<double>& scores, int64_t k) {
+  if (k > int64_t(scores.size())) k = int64_t(scores.size());
+  std::vector<int64_t> idx(static_cast<size_t>(k));
+  check(moses_topk(scores.data(), int64_t(scores.size()), k, idx.data()));
+  return idx;
+}
+inline std::vector<int64_t> select_batch(const std::vector<uint64_t>& ordered_hashes,
+                                         const std::unordered_set<uint64_t>& already_measured, int64_t batch_size) {
+  std::vector<uint64_t> meas(already_measured.begin(), already_measured.end());
+  std::vector<int64_t> out(static_cast<size_t>(batch_size > 0 ? batch_size : 1));
+  const int64_t n = moses_select_batch(ordered_hashes.data(), int64_t(ordered_hashes.size()), meas.data(),
+                                       int64_t(meas.size()), batch_size, out.data());
+  if (n < 0) check(int(-n));
+  out.resize(size_t(n));
+  return out;
+}
+
+}  // namespace moseslab_gpu

@@ -68,6 +68,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    # C++ drop-in API check (tests/cpp/test_api.cpp over include/moses_gpu.hpp)
+    src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
+    exe = os.path.join(OBJ, "test_api")
+    if os.path.exists(src) and (force or _stale(exe, [src, LIB, os.path.join(ROOT, "include", "moses_gpu.hpp")])):
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        cmd = [cxx, "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", exe, f"-L{PKG}",
+               "-lmoses_gpu", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/.."]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ API test build failed:\n{r.stderr[-4000:]}")
     if verbose:
         print(LIB)
     return LIB

@@ -1,0 +1,132 @@
+// C++ drop-in check: reference test bodies (test_model.cpp, test_lottery.cpp, test_search.cpp)
+// re-pointed at the B200 library through include/moses_gpu.hpp. Built by build(), run by
+// tests/test_cpp_api.py on a GPU box. Prints one line per case, exits non-zero on failure.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "moses_gpu.hpp"
+
+using namespace moseslab_gpu;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #cond);      \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+
+template <class F>
+static void expect_error(ErrorCode code, F&& f) {  // test_util.hpp:13-23
+  try {
+    f();
+    std::printf("FAIL expected error %d, nothing thrown\n", int(code));
+    ++failures;
+  } catch (const Error& e) {
+    if (e.code() != code) {
+      std::printf("FAIL expected error %d got %d (%s)\n", int(code), int(e.code()), e.what());
+      ++failures;
+    }
+  }
+}
+
+static uint64_t splitmix(uint64_t& s) {
+  s += 0x9e3779b97f4a7c15ull;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static double u01(uint64_t& s) { return double(splitmix(s) >> 11) * 0x1.0p-53; }
+
+int main() {
+  // test_model.cpp:77-81
+  CHECK(param_count({16, 512, 512, 1}) == 271873);
+  // test_model.cpp:100-104
+  expect_error(ErrorCode::BadDims, [] { init_random({16, 512, 1}, 0); });
+  expect_error(ErrorCode::BadDims, [] { init_random({16, 512, 512, 2}, 0); });
+  // test_model.cpp:387-398 (golden predictions; TF32 tolerance)
+  {
+    DeviceModel m(init_random({16, 512, 512, 1}, 12345), MOSES_PREC_TF32, 128);
+    Matrix x(3, 16);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 16; ++c) x(r, c) = (r + 1) * 0.1 + c * 0.01;
+    const auto s = predict(m, x);
+    const double want[3] = {0.068432722090836534, 0.10419522897402726, 0.14194361818494705};
+    for (int i = 0; i < 3; ++i) CHECK(std::abs(s[i] - want[i]) < 2e-3 * 0.142);
+  }
+  // test_model.cpp:136-139
+  {
+    DeviceModel m(init_random({4, 8, 8, 1}, 3), MOSES_PREC_TF32, 16);
+    expect_error(ErrorCode::DimMismatch, [&] { predict(m, Matrix(2, 5)); });
+  }
+  // test_model.cpp:155-165
+  CHECK(std::abs(pairwise_ranking_loss({2.0, 1.0}, {3.0, 1.0}) - std::log(1.0 + std::exp(-1.0))) < 1e-6);
+  CHECK(std::abs(pairwise_ranking_loss({1.0, 1.0}, {3.0, 1.0}) - std::log(2.0)) < 1e-6);
+  CHECK(pairwise_ranking_loss({1.0, 1.0}, {1.0, 1.0}) == 0.0);
+  // test_model.cpp:205-211 pair-free batch -> zero gradient
+  {
+    DeviceModel m(init_random({4, 8, 8, 1}, 7), MOSES_PREC_TF32, 16);
+    RankingBatch b{Matrix(4, 4), {1.0, 1.0, 1.0, 1.0}, "t"};
+    uint64_t s = 20;
+    for (auto& v : b.features.data) v = u01(s);
+    for (double g : gradients(m, b)) CHECK(g == 0.0);
+  }
+  // test_model.cpp:267-292 update arithmetic (fp32 device arithmetic)
+  {
+    CostModelParams p = init_random({4, 8, 8, 1}, 40);
+    p.params[0] = 1.0;
+    DeviceModel m(p, MOSES_PREC_TF32, 16);
+    std::vector<double> g(p.params.size(), 0.0);
+    g[0] = 2.0;
+    check(moses_gradients_upload(m.handle(), g.data(), int64_t(g.size())));
+    TrainHyper h;
+    apply_update(m, h, nullptr, false);
+    CHECK(std::abs(m.download().params[0] - 0.998) < 1e-7);
+  }
+  // test_lottery.cpp:138-150 canonical ratio popcounts
+  {
+    DeviceModel m(init_random({16, 512, 512, 1}, 0), MOSES_PREC_TF32, 16);
+    XiScores xi{std::vector<double>(271873), false};
+    uint64_t s = 8;
+    for (auto& v : xi.xi) v = double(float(u01(s)));
+    CHECK(partition(m, xi, PartitionMode::Ratio, 0.01, 0).popcount() == 2719);
+    CHECK(partition(m, xi, PartitionMode::Ratio, 0.3, 0).popcount() == 81562);
+    CHECK(partition(m, xi, PartitionMode::Ratio, 0.5, 0).popcount() == 135937);
+    CHECK(partition(m, xi, PartitionMode::Ratio, 0.7, 0).popcount() == 190312);
+    CHECK(partition(m, xi, PartitionMode::Ratio, 1.0, 0).popcount() == 271873);
+    expect_error(ErrorCode::InvalidRatio, [&] { partition(m, xi, PartitionMode::Ratio, 1.5, 0); });
+    expect_error(ErrorCode::UnnormalizedThreshold, [&] { partition(m, xi, PartitionMode::Threshold, 0.5, 0); });
+  }
+  // test_lottery.cpp:152-166 ties -> ascending index
+  {
+    DeviceModel m(init_random({4, 8, 8, 1}, 0), MOSES_PREC_TF32, 16);
+    XiScores xi{std::vector<double>(size_t(m.size()), 0.0), false};
+    const double v[6] = {0.5, 0.9, 0.5, 0.1, 0.9, 0.5};
+    for (int i = 0; i < 6; ++i) xi.xi[i] = v[i];
+    const ParamMask mk = partition(m, xi, PartitionMode::Ratio, 3.0 / double(m.size()), 0);
+    CHECK(mk.popcount() == 3 && mk.transferable[0] && mk.transferable[1] && mk.transferable[4]);
+  }
+  // test_lottery.cpp:256-263
+  {
+    DeviceModel m(init_random({4, 8, 8, 1}, 15), MOSES_PREC_TF32, 16);
+    ParamMask mk{std::vector<uint8_t>(size_t(m.size()), 0)};
+    expect_error(ErrorCode::UnstableDecay, [&] { variant_decay(m, mk, 1.0, 1.0); });
+  }
+  // test_lottery.cpp:265-274
+  CHECK(std::abs(discriminator_cross_entropy({0, 0, 0}, {0, 0}) - std::log(2.0)) < 1e-15);
+  // test_search.cpp:161-172 select_batch dedup
+  {
+    const auto pos = select_batch({11, 22, 11, 33}, {22}, 10);
+    CHECK(pos.size() == 2 && pos[0] == 0 && pos[1] == 3);
+  }
+  // search.cpp:32-37 order
+  {
+    const auto idx = topk({0.5, 0.9, 0.5, 0.1, 0.9, 0.5}, 4);
+    CHECK(idx.size() == 4 && idx[0] == 1 && idx[1] == 4 && idx[2] == 0 && idx[3] == 2);
+  }
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
