@@ -283,21 +283,22 @@ def main():
     L.moses_set_async(1)
     row_bytes = ld * 2
 
+    # One CUDA graph per step: device-side batch gather -> gradients [-> update].
+    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, BATCH, LR, MU, int(world == 1)))
+
     def step(b):
+        ml._ck(L.moses_train_graph_launch(dm.h, 1))
+        if world > 1:
+            dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+            ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
+
+    def step_eager(b):  # profiling pass: same work without the graph (per-kernel-class events)
         xb = X.data_ptr() + (b % nb) * BATCH * row_bytes
         yb = Y.data_ptr() + (b % nb) * BATCH * 4
-        if world == 1:
-            rc = L.moses_train_step_device(dm.h, xb, ld, yb, BATCH, LR, MU, None)
-            if rc:
-                raise RuntimeError(L.moses_last_error().decode())
-        else:
-            rc = L.moses_gradients_device(dm.h, xb, ld, yb, BATCH, None)
-            if rc:
-                raise RuntimeError(L.moses_last_error().decode())
+        ml._ck(L.moses_gradients_device(dm.h, xb, ld, yb, BATCH, None))
+        if world > 1:
             dist.all_reduce(grads, op=dist.ReduceOp.AVG)
-            rc = L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
-            if rc:
-                raise RuntimeError(L.moses_last_error().decode())
+        ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
 
     with torch.cuda.stream(stream):
         for b in range(args.warmup):
@@ -328,7 +329,7 @@ def main():
         # ---------------- device-time attribution (separate pass; events perturb timing)
         ml.profile_begin()
         for k in range(args.profile_steps):
-            step(k)
+            step_eager(k)
         torch.cuda.synchronize()
         prof = ml.profile_end()
 

@@ -118,6 +118,15 @@ MOSES_API int moses_train_step(moses_model_t m, const double* features, const do
 /* Same on device-resident rows (packed layout, labels fp32); loss stays on device unless loss_out != NULL. */
 MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
                                       double learning_rate, double momentum, double* loss_out);
+/* CUDA graph of one device-resident training step over a packed dataset of n_batches x batch rows
+ * (row stride = moses_packed_ld): gather batch (device-side index) -> gradients [-> momentum update].
+ * with_update = 0 leaves the update to the caller (data parallel: all-reduce the gradients first).
+ * Each launch replays `steps` steps; the batch index advances on the device. */
+MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                       int64_t n_batches, int64_t batch, double learning_rate, double momentum,
+                                       int32_t with_update);
+MOSES_API int moses_train_graph_launch(moses_model_t m, int64_t steps);
+MOSES_API int moses_train_graph_kernels(void);
 /* ranking_accuracy (model.cpp:298-312): nb batches, rows [off[b], off[b+1]) of features/labels. */
 MOSES_API int moses_ranking_accuracy(moses_model_t m, const double* features, const double* labels,
                                      const int64_t* batch_offsets, int32_t nbatches, int32_t D, double* accuracy,

@@ -192,6 +192,11 @@ struct moses_model {
   int esz = 2;
   long long cap = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;      // weight-gradient side stream
+  std::vector<cudaEvent_t> evs;   // fork / dz-ready / join events of the two-stream backward
+  // CUDA graph of one device-resident training step (moses_train_graph_*)
+  cudaGraphExec_t train_exec = nullptr;
+  long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
   // parameters
   float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
   float *m1 = nullptr, *m2 = nullptr;
@@ -235,6 +240,10 @@ struct moses_model {
       dfree(p);
     for (void* p : act) dfree(p);
     for (void* p : dz) dfree(p);
+    if (train_exec) cudaGraphExecDestroy(train_exec);
+    dfree(dcounter);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -278,14 +287,25 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
 
 template <typename T>
 void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u) {
+  // Two streams: the data-gradient chain (head backward -> dgrad(L-2) -> ... -> dgrad(1)) runs on
+  // st; every weight-gradient GEMM (and the head-gradient column reduction) runs on st2 as soon
+  // as its dZ is ready. At batch 512 each GEMM fills only 16-40 of the 148 SMs, so the two
+  // chains overlap almost perfectly.
   const int L = m->L, W = m->W();
   T* hl = static_cast<T*>(m->act[L - 1]);
+  cudaEvent_t* ev = m->evs.data();  // ev[0] fork, ev[1 + l] "dz[l] ready", ev[L + 1] join
+  MOSES_CUDA(cudaEventRecord(ev[0], m->st));
+  MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[0], 0));
+  {
+    ProfScope ps(P_HEAD, m->st2);
+    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2);
+  }
   {
     ProfScope ps(P_HEAD, m->st);
-    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st);
     head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
                      m->lddz[L - 1], m->st);
   }
+  MOSES_CUDA(cudaEventRecord(ev[1 + (L - 1)], m->st));
   note_launch(2);
   for (int l = L - 2; l >= 0; --l) {
     const void* a = l == 0 ? x0 : m->act[l];
@@ -299,9 +319,10 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     wg.epi = EpiKind::StoreF32;
     wg.out = m->g + m->off[l];
     wg.ldo = m->dims[l + 1];
+    MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (l + 1)], 0));
     {
-      ProfScope ps(P_GEMM_WGRAD, m->st);
-      launch_gemm(m->esz, wg, m->st);
+      ProfScope ps(P_GEMM_WGRAD, m->st2);
+      launch_gemm(m->esz, wg, m->st2);
     }
     note_launch(1);
     if (l > 0) {
@@ -320,9 +341,12 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
         ProfScope ps(P_GEMM_DGRAD, m->st);
         launch_gemm(m->esz, dg, m->st);
       }
+      MOSES_CUDA(cudaEventRecord(ev[1 + l], m->st));
       note_launch(1);
     }
   }
+  MOSES_CUDA(cudaEventRecord(ev[L + 1], m->st2));
+  MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 1], 0));
 }
 
 // apply_update is synchronous for host callers (reference value semantics); the device-resident
@@ -485,6 +509,9 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->esz = precision == MOSES_PREC_BF16 ? 2 : 4;
     m->cap = round_up(max_rows, 128);
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+    MOSES_CUDA(cudaStreamCreateWithFlags(&m->st2, cudaStreamNonBlocking));
+    m->evs.resize(m->L + 4);
+    for (auto& e : m->evs) MOSES_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const long long P = m->P;
     m->w = dalloc<float>(P);
     m->mom = dalloc<float>(P);
@@ -859,6 +886,68 @@ MOSES_API int moses_train_step(moses_model_t m, const double* x, const double* y
     }
   });
 }
+
+// ---- CUDA graph of one device-resident training step: gather batch (device counter) ->
+// gradients -> momentum update -> advance counter. Replayed with one cudaGraphLaunch per step.
+static long long g_graph_kernels = 0;
+MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                       int64_t n_batches, int64_t batch, double lr, double mu, int32_t with_update) {
+  return guarded([&] {
+    require_model(m);
+    check_rows(m, batch);
+    if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
+    if (n_batches < 1) fail(MOSES_ERR_INVALID_ARG, "n_batches must be >= 1");
+    if (m->train_exec) {
+      cudaGraphExecDestroy(m->train_exec);
+      m->train_exec = nullptr;
+    }
+    if (!m->dcounter) m->dcounter = dalloc<long long>(1);
+    MOSES_CUDA(cudaMemsetAsync(m->dcounter, 0, sizeof(long long), m->st));
+    const long long row_bytes = ldx * m->esz;
+    auto body = [&] {
+      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
+      gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
+      if (with_update) sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      advance_counter(m->dcounter, m->st);
+    };
+    {  // eager warm-up without the update (configures kernels, validates shapes; params untouched)
+      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
+      gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
+    }
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    cudaGraph_t graph;
+    MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(m->st, &graph);
+      throw;
+    }
+    MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+    size_t nodes = 0;
+    MOSES_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
+    std::vector<cudaGraphNode_t> nv(nodes);
+    MOSES_CUDA(cudaGraphGetNodes(graph, nv.data(), &nodes));
+    long long kernels = 0;
+    for (auto n : nv) {
+      cudaGraphNodeType t;
+      MOSES_CUDA(cudaGraphNodeGetType(n, &t));
+      kernels += t == cudaGraphNodeTypeKernel;
+    }
+    g_graph_kernels = kernels;
+    MOSES_CUDA(cudaGraphInstantiate(&m->train_exec, graph, 0));
+    MOSES_CUDA(cudaGraphDestroy(graph));
+  });
+}
+MOSES_API int moses_train_graph_launch(moses_model_t m, int64_t steps) {
+  return guarded([&] {
+    require_model(m);
+    if (!m->train_exec) fail(MOSES_ERR_INVALID_ARG, "no training graph (moses_train_graph_create)");
+    for (int64_t i = 0; i < steps; ++i) MOSES_CUDA(cudaGraphLaunch(m->train_exec, m->st));
+    note_launch(steps * g_graph_kernels);
+  });
+}
+MOSES_API int moses_train_graph_kernels(void) { return int(g_graph_kernels); }
 
 MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
                                       double lr, double mu, double* loss_out) {

@@ -111,6 +111,23 @@ __global__ void row_dot_kernel(const float* __restrict__ H, long long ldh, long 
   }
 }
 
+// ---------------------------------------------------------------- device-resident batch gather (graph replay)
+__global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
+                                    const long long* __restrict__ counter, long long nb, long long batch,
+                                    uint8_t* __restrict__ dst, float* __restrict__ ydst) {
+  const long long b = (*counter) % nb;
+  const uint4* src = reinterpret_cast<const uint4*>(x_base + b * batch * row_bytes);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const long long n16 = batch * row_bytes / 16;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
+    d[i] = src[i];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < batch; i += (long long)gridDim.x * blockDim.x)
+    ydst[i] = y_base[b * batch + i];
+}
+__global__ void advance_counter_kernel(long long* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *c += 1;
+}
+
 // ---------------------------------------------------------------- scores from head partials
 __global__ void head_scores_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hb,
                                    long long rows, float* __restrict__ s) {
@@ -887,6 +904,18 @@ void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s) {
 void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s) {
   if (n <= 0) return;
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
+                  long long batch, void* dst, float* ydst, cudaStream_t s) {
+  if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
+  gather_batch_kernel<<<grid_for(batch * row_bytes / 16, 256), 256, 0, s>>>(
+      static_cast<const uint8_t*>(x_base), row_bytes, y_base, counter, nb, batch, static_cast<uint8_t*>(dst), ydst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void advance_counter(long long* c, cudaStream_t s) {
+  advance_counter_kernel<<<1, 32, 0, s>>>(c);
   MOSES_CUDA(cudaGetLastError());
 }
 

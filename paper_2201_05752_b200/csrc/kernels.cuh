@@ -25,6 +25,10 @@ void f32_to_f64(const float* src, long long n, double* dst, cudaStream_t s);
 void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
 void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s);
 void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, long long ldd, cudaStream_t s);
+// batch b = (*counter % nb): rows [b*batch, (b+1)*batch) of a packed dataset -> dst, labels -> ydst
+void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
+                  long long batch, void* dst, float* ydst, cudaStream_t s);
+void advance_counter(long long* c, cudaStream_t s);
 // out[r] = H[r] . u  (warp per row)
 void row_dot(const float* H, long long ldh, long long R, int W, const float* u, float* out, cudaStream_t s);
 // discriminator_cross_entropy (lottery.cpp:207-218) over z[0,m) source and z[m,m+n) target

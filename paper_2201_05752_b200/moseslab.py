@@ -84,6 +84,9 @@ def lib():
         "moses_gradients": (C.c_int, [vp, vp, vp, i64, i32, vp, dbl, vp]),
         "moses_gradients_device": (C.c_int, [vp, vp, i64, vp, i64, vp]),
         "moses_set_async": (C.c_int, [i32]),
+        "moses_train_graph_create": (C.c_int, [vp, vp, i64, vp, i64, i64, dbl, dbl, i32]),
+        "moses_train_graph_launch": (C.c_int, [vp, i64]),
+        "moses_train_graph_kernels": (C.c_int, []),
         "moses_profile_begin": (C.c_int, []),
         "moses_profile_end": (C.c_int, [vp, vp, i32]),
         "moses_gradients_download": (C.c_int, [vp, vp, i64]),

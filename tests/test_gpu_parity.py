@@ -555,3 +555,32 @@ def test_device_synthetic_features_match_oracle(ml, orc):
     assert ml.lib().moses_synth_labels_device(1, 1000, n, y.data_ptr()) == 0
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), orc.synth_labels(1, 1000, n).astype(np.float32))
+
+
+# ---------------------------------------------------------------- CUDA-graph training step
+def test_train_graph_matches_eager_steps(ml):
+    """moses_train_graph_* (device gather + gradients + update, replayed) == eager steps, bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 2)
+    L = ml.lib()
+    a = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    b = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    ld = a.packed_ld
+    nb, batch = 3, 256
+    X = torch.empty((nb * batch, ld), dtype=torch.bfloat16, device="cuda")
+    Y = torch.empty(nb * batch, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(1, 0, nb * batch, dims[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(1, 0, nb * batch, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    ml._ck(L.moses_train_graph_create(a.h, X.data_ptr(), ld, Y.data_ptr(), nb, batch, 0.001, 0.9, 1))
+    ml._ck(L.moses_train_graph_launch(a.h, 5))
+    for s in range(5):
+        r = s % nb
+        ml._ck(L.moses_train_step_device(b.h, X.data_ptr() + r * batch * ld * 2, ld, Y.data_ptr() + r * batch * 4,
+                                         batch, 0.001, 0.9, None))
+    pa, pb = a.download(), b.download()
+    assert np.array_equal(pa.params, pb.params) and np.array_equal(pa.momentum, pb.momentum)
