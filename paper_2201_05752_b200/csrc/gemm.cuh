@@ -76,7 +76,8 @@ struct GemmCfg {
   static constexpr int kStages = (200 * 1024 / kStageBytes) > 6 ? 6 : (200 * 1024 / kStageBytes);
   static constexpr int kMNChunk = 128 / int(sizeof(T));  // elements per 128-byte MN row
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kVecBytes = 3 * BN * 4;  // bias / head_w / head_u slices of this CTA's N range
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kVecBytes;
 };
 
 template <typename T, int BN, bool A_MN, bool B_MN, int EPI>
@@ -94,6 +95,9 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* accum_bar = empty_bar + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  float* s_bias = reinterpret_cast<float*>(smem + STAGES * Cfg::kStageBytes + 256);
+  float* s_hw = s_bias + BN;
+  float* s_hu = s_hw + BN;
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -110,6 +114,15 @@ __global__ void __launch_bounds__(128, 1)
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if constexpr (EPI == int(Epi::Fwd)) {
+    for (int j = threadIdx.x; j < BN; j += 128) {
+      const int n = n0 + j;
+      const bool ok = n < args.N;
+      s_bias[j] = (ok && args.bias) ? __ldg(args.bias + n) : 0.f;
+      s_hw[j] = (ok && args.head_w) ? __ldg(args.head_w + n) : 0.f;
+      s_hu[j] = (ok && args.head_u) ? __ldg(args.head_u + n) : 0.f;
+    }
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -173,13 +186,38 @@ __global__ void __launch_bounds__(128, 1)
   }
 
   // ---------------- epilogue: all 4 warps, one accumulator row per thread
-  ptx::mbar_wait(accum_bar, 0);
-  ptx::tc_fence_after();
   const int row = warp * 32 + lane;
   const int m = m0 + row;
   const bool row_ok = m < args.M;
   const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
   float hp = 0.f, hp2 = 0.f;
+  // ReLU' source for the Dgrad epilogue: 16-byte vector loads, chunk 0 prefetched while the MMAs run
+  constexpr int kMaskVec = 32 * int(sizeof(T)) / 16;
+  uint4 mk[kMaskVec];
+  auto load_mask = [&](int c) {
+    if constexpr (EPI == int(Epi::Dgrad)) {
+      const int nb = n0 + c * 32;
+      if (row_ok && nb + 32 <= args.N) {
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(args.mask) + (long long)m * args.ldm + nb);
+#pragma unroll
+        for (int q = 0; q < kMaskVec; ++q) mk[q] = __ldg(src + q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kMaskVec; ++q) mk[q] = make_uint4(0, 0, 0, 0);
+        if (row_ok && nb < args.N) {
+          const T* mrow = reinterpret_cast<const T*>(args.mask) + (long long)m * args.ldm + nb;
+          T* dst = reinterpret_cast<T*>(mk);
+          const int cnt = args.N - nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < cnt) dst[j] = mrow[j];
+        }
+      }
+    }
+  };
+  load_mask(0);
+  ptx::mbar_wait(accum_bar, 0);
+  ptx::tc_fence_after();
 
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
@@ -187,35 +225,35 @@ __global__ void __launch_bounds__(128, 1)
     ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
     ptx::tmem_ld_wait();
     const int nb = n0 + c * 32;
-    if (!row_ok || nb >= args.N) continue;
-    const int nvalid = min(32, args.N - nb);
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if constexpr (EPI == int(Epi::Dgrad)) {
+      const T* mv = reinterpret_cast<const T*>(mk);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = static_cast<float>(mv[j]) > 0.f ? v[j] : 0.f;
+      if (c + 1 < BN / 32) load_mask(c + 1);
+    }
+    if (!row_ok || nb >= args.N) continue;
+    const int nvalid = min(32, args.N - nb);
 
     if constexpr (EPI == int(Epi::Fwd)) {
-      if (args.bias != nullptr) {
+      const float* sb = s_bias + c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += (j < nvalid) ? __ldg(args.bias + nb + j) : 0.f;
-      }
+      for (int j = 0; j < 32; ++j) v[j] += sb[j];
       if (args.relu) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
       }
       if (args.head_w != nullptr) {
+        const float* hw = s_hw + c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) hp = fmaf(v[j], (j < nvalid) ? __ldg(args.head_w + nb + j) : 0.f, hp);
+        for (int j = 0; j < 32; ++j) hp = fmaf(v[j], hw[j], hp);
       }
       if (args.head_u != nullptr) {
+        const float* hu = s_hu + c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], (j < nvalid) ? __ldg(args.head_u + nb + j) : 0.f, hp2);
-      }
-    } else if constexpr (EPI == int(Epi::Dgrad)) {
-      const T* mrow = reinterpret_cast<const T*>(args.mask) + (long long)m * args.ldm + nb;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float h = (j < nvalid) ? static_cast<float>(mrow[j]) : 0.f;
-        v[j] = h > 0.f ? v[j] : 0.f;
+        for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], hu[j], hp2);
       }
     }
 
