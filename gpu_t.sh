@@ -1,6 +1,7 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2 3; do timeout 300 python -m pytest "tests/test_gpu_parity.py::test_gradients_vs_precision_model" -q -m gpu 2>&1 | tail -3; done
-timeout 900 python -m pytest tests/ -q -m gpu --timeout 300 > gpurun_out/pytest10.log 2>&1; echo pytest rc=$?
-grep -E "passed|failed|FAILED" gpurun_out/pytest10.log | tail -30
-timeout 900 python bench.py --steps 100 --warmup 10 > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo bench rc=$?
-tail -3 gpurun_out/bench5.err; cat gpurun_out/bench5.json
+timeout 900 python -m pytest tests/ -q -m gpu --timeout 300 > gpurun_out/pytest11.log 2>&1; echo pytest rc=$?
+grep -E "passed|failed|FAILED" gpurun_out/pytest11.log | tail -30
+timeout 900 python bench.py > gpurun_out/bench6.json 2> gpurun_out/bench6.err; echo bench rc=$?
+tail -3 gpurun_out/bench6.err; python -c "
+import json; d=json.load(open('gpurun_out/bench6.json'))
+print(d['value'], d['ms_per_step']); print(d['step_breakdown_ms']); print(d['e2e']); print(d['infer']['value'], d['infer']['roofline']); print(d['cpu_baseline']['value'], d['gpu_launches'], d['clocks'])"

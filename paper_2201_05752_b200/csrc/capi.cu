@@ -423,12 +423,12 @@ void gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
   ProfScope ps(P_RANK, m->st);
-  head_scores(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), n, m->scores, m->st);
-  rank_pairs(m->scores, y, n, {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->st);
+  rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), y, n,
+                   {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->scores, m->st);
   FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
   rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
                 active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
-  note_launch(3);
+  note_launch(2);
   ps.~ProfScope();
   ps.idx = -1;
   if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u);
@@ -1026,7 +1026,7 @@ MOSES_API int moses_ranking_loss(const double* s, const double* y, int64_t n, do
       f64_to_f32(s64, n, sf, sc.st);
       f64_to_f32(y64, n, yf, sc.st);
       rank_pairs(sf, yf, n, ws, sc.st);
-      note_launch(3);
+      note_launch(3);  // two conversions + pairs
     }
     rank_finalize(ws, n, 0, nullptr, 0, 0, nullptr, 0.0, {dl, dp, ca, cb, dl + 1}, sc.st);
     note_launch(1);

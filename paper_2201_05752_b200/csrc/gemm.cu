@@ -94,9 +94,17 @@ void launch_t(const GemmCall& c, cudaStream_t s) {
   a.mn_sbo = g_mn_sbo[elem == 4];
   a.mn_kstep = g_mn_kstep[elem == 4];
   a.round_out = c.round_out;
-  dim3 grid(ceil_div(c.M, Cfg::BM), ceil_div(c.N, BN));
-  kern<<<grid, 128, Cfg::kSmemBytes, s>>>(ta, tb, a);
-  MOSES_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ceil_div(c.M, Cfg::BM), ceil_div(c.N, BN));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: prologue overlaps the previous kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
 }
 
 template <typename T, int BN>

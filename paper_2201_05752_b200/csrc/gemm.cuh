@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int num_kb = (args.K + BK - 1) / BK;
+  ptx::pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -114,6 +115,8 @@ __global__ void __launch_bounds__(128, 1)
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  // everything above overlaps the previous kernel's tail (PDL); operands/params are read below
+  ptx::pdl_wait();
   if constexpr (EPI == int(Epi::Fwd)) {
     for (int j = threadIdx.x; j < BN; j += 128) {
       const int n = n0 + j;

@@ -9,6 +9,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace moses {
 namespace {
@@ -47,6 +48,7 @@ int grid_for(long long n, int block, int per_sm = 8) {
 // ---------------------------------------------------------------- data movement
 template <typename T>
 __global__ void pack_rows_kernel(const double* __restrict__ src, long long n, int D, T* __restrict__ dst, long long ld) {
+  ptx::pdl_launch_dependents();
   const long long total = n * ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / ld;
@@ -115,6 +117,7 @@ __global__ void row_dot_kernel(const float* __restrict__ H, long long ldh, long 
 __global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
                                     const long long* __restrict__ counter, long long nb, long long batch,
                                     uint8_t* __restrict__ dst, float* __restrict__ ydst) {
+  ptx::pdl_launch_dependents();
   const long long b = (*counter) % nb;
   const uint4* src = reinterpret_cast<const uint4*>(x_base + b * batch * row_bytes);
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -146,20 +149,33 @@ __global__ void head_scores_kernel(const float* __restrict__ part, int ntiles, l
 // Each distinct-label pair is counted once (at its hi row), as in the reference's i<j loop.
 constexpr int kRankBlock = 128;
 constexpr int kRankChunk = 32;  // j columns per block: n=512 -> 4 x 16 blocks, n=4096 -> 32 x 128
-__global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __restrict__ s, const float* __restrict__ y,
-                                                                long long n, double* gs_part, double* loss_part,
-                                                                long long* pairs_part) {
+// Scores come either from `s` or, fused, from the last forward epilogue's per-N-tile partials
+// (s_r = b + sum_t part[t][r], the same fixed order as head_scores_kernel).
+__device__ __forceinline__ float score_of(const float* __restrict__ s, const float* __restrict__ part, int ntiles,
+                                          long long ld, float hb, long long r) {
+  if (part == nullptr) return s[r];
+  float acc = 0.f;
+  for (int t = 0; t < ntiles; ++t) acc += part[t * ld + r];
+  return acc + hb;
+}
+__global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __restrict__ s, const float* __restrict__ part,
+                                                                int ntiles, long long ld, const float* __restrict__ hbp,
+                                                                const float* __restrict__ y, long long n, double* gs_part,
+                                                                double* loss_part, long long* pairs_part,
+                                                                float* __restrict__ s_out) {
   __shared__ float ss[kRankChunk], sy[kRankChunk];
+  const float hb = part ? hbp[0] : 0.f;
   const long long i = blockIdx.x * (long long)kRankBlock + threadIdx.x;
   const long long j0 = (long long)blockIdx.y * kRankChunk;
   const int cnt = int(min((long long)kRankChunk, n - j0));
   if (threadIdx.x < cnt) {
-    ss[threadIdx.x] = s[j0 + threadIdx.x];
+    ss[threadIdx.x] = score_of(s, part, ntiles, ld, hb, j0 + threadIdx.x);
     sy[threadIdx.x] = y[j0 + threadIdx.x];
   }
   __syncthreads();
   if (i >= n) return;
-  const float si = s[i], yi = y[i];
+  const float si = score_of(s, part, ntiles, ld, hb, i), yi = y[i];
+  if (s_out != nullptr && blockIdx.y == 0) s_out[i] = si;
   float gs = 0.f, loss = 0.f;
   int pairs = 0;
 #pragma unroll 4
@@ -215,6 +231,7 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
                                                                   long long ld2, const float* adv_bias, double beta,
                                                                   double* loss_out, long long* pairs_out, float* coefA,
                                                                   float* coefB, double* ce_out) {
+  ptx::pdl_launch_dependents();
   using BR = cub::BlockReduce<double, kFinBlock>;
   using BRL = cub::BlockReduce<long long, kFinBlock>;
   __shared__ typename BR::TempStorage tmp;
@@ -223,10 +240,11 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   __shared__ long long sh_pairs;
   long long p = 0;
   double l = 0.0;
-  for (long long i = threadIdx.x; i < n; i += kFinBlock) {  // rows already reduced over splits
-    p += pairs_part[i];
-    l += loss_part[i];
-  }
+  for (long long i = threadIdx.x; i < n; i += kFinBlock)  // fixed order: row-major over (row, split)
+    for (int sp = 0; sp < nsplit; ++sp) {
+      p += pairs_part[sp * n + i];
+      l += loss_part[sp * n + i];
+    }
   const long long ptot = BRL(tmpl).Sum(p);
   __syncthreads();
   const double ltot = BR(tmp).Sum(l);
@@ -240,7 +258,11 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   const long long R = roff + n;
   for (long long r = threadIdx.x; r < R; r += kFinBlock) {
     float a = 0.f;
-    if (r >= roff) a = pairs > 0 ? float(gs_part[r - roff] * inv) : 0.f;
+    if (r >= roff) {
+      double g = 0.0;
+      for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + (r - roff)];
+      a = pairs > 0 ? float(g * inv) : 0.f;
+    }
     coefA[r] = a;
     coefB[r] = 0.f;
   }
@@ -282,6 +304,7 @@ template <typename T>
 __global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
                                      const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
                                      long long ldh, long long R, int W, T* __restrict__ dz, long long ldz) {
+  ptx::pdl_launch_dependents();
   const long long total = R * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / W;
@@ -328,6 +351,7 @@ __global__ void column_sum_kernel(const float* __restrict__ part, int slabs, int
 template <bool MOM, bool MASK, int SHADOW>
 __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
                            const uint8_t* __restrict__ mask, long long P, float lr, float mu, void* __restrict__ shadow) {
+  ptx::pdl_launch_dependents();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
     if (!MASK || mask[i]) {
@@ -945,8 +969,16 @@ int rank_splits(long long n) { return n <= 0 ? 1 : ceil_div(n, kRankChunk); }
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st) {
   if (n <= 0) return;
   dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
-  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, y, n, ws.gs_part, ws.loss_part, ws.pairs_part);
-  rank_rows_kernel<<<grid_for(n, 256), 256, 0, st>>>(ws.gs_part, ws.loss_part, ws.pairs_part, int(grid.y), n);
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, nullptr, 0, 0, nullptr, y, n, ws.gs_part, ws.loss_part,
+                                                 ws.pairs_part, nullptr);
+  MOSES_CUDA(cudaGetLastError());
+}
+void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const float* y, long long n,
+                      const RankWs& ws, float* s_out, cudaStream_t st) {
+  if (n <= 0) return;
+  dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(nullptr, part, ntiles, ld, hb, y, n, ws.gs_part, ws.loss_part,
+                                                 ws.pairs_part, s_out);
   MOSES_CUDA(cudaGetLastError());
 }
 

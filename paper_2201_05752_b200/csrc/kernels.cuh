@@ -45,6 +45,9 @@ struct RankWs {
 };
 int rank_splits(long long n);
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st);
+// same, scores summed from the forward's per-N-tile head partials (+ head bias); s_out optional
+void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const float* y, long long n,
+                      const RankWs& ws, float* s_out, cudaStream_t st);
 // Reduces the rank partials (fixed order), normalises by the pair count, folds in the
 // adversary's logits when `part2` is given (model.cpp:215-238), and emits per-row
 // backward coefficients coefA (ranking) / coefB (adversary) over all R = roff + n rows.
