@@ -34,6 +34,7 @@ PROGRAMS = 200_000
 BATCH = 512
 SEED_DATA, SEED_MODEL = 1, 12345
 LR, MU = 0.001, 0.9
+MAX_STMTS = 8  # statements per program: 1 + below(8), mean 4.5
 
 
 def train_flops_per_sample(dims):
@@ -119,20 +120,27 @@ def cpu_baseline(steps_budget_s: float = 15.0, threads: int | None = None):
     threads = threads or os.cpu_count() or 1
     w = orc.init_random(DIMS, SEED_MODEL, strict=False)
     mom = np.zeros_like(w)
-    x = orc.synth_features(SEED_DATA, 0, BATCH, DIMS[0])
+    off = orc.synth_offsets(SEED_DATA, BATCH, MAX_STMTS)
+    x = orc.synth_features(SEED_DATA, 0, int(off[-1]), DIMS[0])
     y = orc.synth_labels(SEED_DATA, 0, BATCH)
-    orc.train_step_f64(DIMS, w, mom, x, y, LR, MU, threads)  # warm
+
+    def step():  # tuner.cpp:146-147 with segment-sum pooling over each program's statements
+        nonlocal w, mom
+        g, _ = orc.gradients_pooled(DIMS, w, x, off, y, threads)
+        w, mom = orc.apply_update(w, mom, g, LR, MU, None, True)
+
+    step()  # warm
     t0 = time.perf_counter()
     n = 0
     while True:
-        orc.train_step_f64(DIMS, w, mom, x, y, LR, MU, threads)
+        step()
         n += 1
         if time.perf_counter() - t0 > steps_budget_s or n >= 2000:
             break
     dt = time.perf_counter() - t0
     return {"value": n * BATCH / dt, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{n} fp64 training steps of batch {BATCH} on {DIMS} ({dt:.1f} s), "
-                      f"oracle/moses_oracle.hpp restating model.cpp:192-296"}
+            "sample": f"{n} fp64 training steps of {BATCH} TenSet-shaped programs ({int(off[-1])} statements) on "
+                      f"{DIMS} ({dt:.1f} s), oracle/moses_oracle.hpp restating model.cpp:192-296 + pooling"}
 
 
 def run_reference(args, rank, world):
@@ -145,7 +153,9 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / base["value"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (keyed SplitMix64 TenSet-shaped features, labels 0.1+U)",
-        "config": {"workload": f"cfg2 pretrain {DIMS} on {PROGRAMS} programs, batch {BATCH}, momentum SGD",
+        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} TenSet-shaped programs "
+                               f"(segment-sum pooling over statements), batch {BATCH} programs, momentum SGD "
+                               f"lr={LR} mu={MU}",
                    "programs": PROGRAMS, "global_batch": BATCH, "parallelism": "host threads"},
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -253,38 +263,40 @@ def main():
     if L.moses_device_check() != 0:
         raise SystemExit("moses: " + L.moses_last_error().decode())
 
-    # ---------------- model + device-resident dataset (this rank's shard)
+    # ---------------- model + device-resident TenSet-shaped dataset (this rank's shard of programs)
+    from paper_2201_05752_b200.distributed import device_gradient_tensor, shard_range
+
     params = ml.init_random(DIMS, SEED_MODEL, strict=False)
-    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=BATCH)
+    off_all = ml.synth_offsets(SEED_DATA, PROGRAMS, MAX_STMTS)
+    p_lo, p_hi = shard_range(PROGRAMS, rank, world)
+    nb = (p_hi - p_lo) // BATCH
+    p_hi = p_lo + nb * BATCH
+    off = off_all[p_lo:p_hi + 1] - off_all[p_lo]
+    row0, n_rows = int(off_all[p_lo]), int(off[-1])
+    batch_rows = np.diff(off[::BATCH])
+    rows_pad = int((batch_rows.max() + 127) // 128 * 128)
+    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=rows_pad)
     ld = dm.packed_ld
-    shard = PROGRAMS // world if world > 1 else PROGRAMS
-    row0 = rank * shard
-    X = torch.empty((shard, ld), dtype=torch.bfloat16, device="cuda")
-    Y = torch.empty(shard, dtype=torch.float32, device="cuda")
-    assert L.moses_synth_features_device(SEED_DATA, row0, shard, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
-    assert L.moses_synth_labels_device(SEED_DATA, row0, shard, Y.data_ptr()) == 0
+    X = torch.empty((n_rows, ld), dtype=torch.bfloat16, device="cuda")
+    Y = torch.empty(nb * BATCH, dtype=torch.float32, device="cuda")
+    OFF = torch.from_numpy(off).cuda()
+    assert L.moses_synth_features_device(SEED_DATA, row0, n_rows, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(SEED_DATA, p_lo, nb * BATCH, Y.data_ptr()) == 0
     torch.cuda.synchronize()
-    nb = shard // BATCH
 
     import ctypes as C
 
     sp = C.c_void_p()
     L.moses_model_stream(dm.h, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
-    gptr = C.POINTER(C.c_float)()
-    L.moses_model_device_ptrs(dm.h, None, C.byref(gptr), None)
-
-    class _CAI:
-        def __init__(self, ptr, n):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
-
-    grads = torch.as_tensor(_CAI(C.cast(gptr, C.c_void_p).value, dm.P), device="cuda")
+    grads = device_gradient_tensor(dm)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     L.moses_set_async(1)
-    row_bytes = ld * 2
 
-    # One CUDA graph per step: device-side batch gather -> gradients [-> update].
-    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, BATCH, LR, MU, int(world == 1)))
+    # One CUDA graph per step: device-side gather of the batch's programs (variable statement counts)
+    # -> pooled gradients [-> update].
+    ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, BATCH,
+                                             rows_pad, LR, MU, int(world == 1)))
 
     def step(b):
         ml._ck(L.moses_train_graph_launch(dm.h, 1))
@@ -292,10 +304,14 @@ def main():
             dist.all_reduce(grads, op=dist.ReduceOp.AVG)
             ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
 
+    # host copies of one batch for the eager profiling pass and the end-to-end leg
+    xb_host = np.ascontiguousarray(X[: int(batch_rows[0])].float().cpu().numpy()[:, : DIMS[0]].astype(np.float64))
+    ob_host = np.ascontiguousarray(off[: BATCH + 1])
+    yb_host = np.ascontiguousarray(Y[:BATCH].cpu().numpy().astype(np.float64))
+
     def step_eager(b):  # profiling pass: same work without the graph (per-kernel-class events)
-        xb = X.data_ptr() + (b % nb) * BATCH * row_bytes
-        yb = Y.data_ptr() + (b % nb) * BATCH * 4
-        ml._ck(L.moses_gradients_device(dm.h, xb, ld, yb, BATCH, None))
+        ml._ck(L.moses_gradients_pooled(dm.h, xb_host.ctypes.data, xb_host.shape[0], DIMS[0], ob_host.ctypes.data,
+                                        BATCH, yb_host.ctypes.data, None))
         if world > 1:
             dist.all_reduce(grads, op=dist.ReduceOp.AVG)
         ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
@@ -334,16 +350,15 @@ def main():
         prof = ml.profile_end()
 
         # ---------------- end to end through the reference-facing C ABI with host buffers
-        x_host = torch.from_numpy(np.ascontiguousarray(
-            np.random.default_rng(rank).random((BATCH, DIMS[0])))).pin_memory()
-        y_host = torch.from_numpy(0.1 + np.random.default_rng(rank + 7).random(BATCH)).pin_memory()
+        x_host = torch.from_numpy(xb_host).pin_memory()
+        y_host = torch.from_numpy(yb_host).pin_memory()
+        o_host = torch.from_numpy(ob_host).pin_memory()
         loss = C.c_double()
         L.moses_set_async(0)
 
         def e2e_step():
-            rc = L.moses_gradients(dm.h, x_host.data_ptr(), y_host.data_ptr(), BATCH, DIMS[0], None, 0.0, C.byref(loss))
-            if rc:
-                raise RuntimeError(L.moses_last_error().decode())
+            ml._ck(L.moses_gradients_pooled(dm.h, x_host.data_ptr(), x_host.shape[0], DIMS[0], o_host.data_ptr(),
+                                            BATCH, y_host.data_ptr(), C.byref(loss)))
             if world > 1:
                 dist.all_reduce(grads, op=dist.ReduceOp.AVG)
             L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
@@ -378,7 +393,7 @@ def main():
         pass
     gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
     gemm_launches = sum(prof[c][1] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
-    flops = gemm_flops_per_step(DIMS, BATCH)
+    flops = gemm_flops_per_step(DIMS, n_rows / nb)  # algorithmic: real statement rows, not the padding
     peak = peaks.get("bf16_tflops_sustained", 1408.7)
     achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     traffic = None
@@ -387,20 +402,22 @@ def main():
     except Exception:
         pass
     step_prof_ms = sum(v[0] for v in prof.values()) / args.profile_steps
-    fwd, wg, dg = train_flops_per_sample(DIMS)
+    fwd, wg, dg = (v * n_rows / (nb * BATCH) for v in train_flops_per_sample(DIMS))
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (keyed SplitMix64 TenSet-shaped features 164-d, labels 0.1+U; random-init model)",
-        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} programs, batch {BATCH}/GPU, "
+        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} TenSet-shaped programs "
+                               f"(segment-sum pooling over statements), batch {BATCH} programs/GPU, "
                                f"momentum SGD lr={LR} mu={MU}", "model": "moses-mlp-4x512", "programs": PROGRAMS,
                    "global_batch": BATCH * world, "seq_len": None, "parallelism": f"dp{world}",
-                   "statements_per_program": 1,
+                   "statements_per_program": f"1 + U{{0..{MAX_STMTS - 1}}} (mean {n_rows / (nb * BATCH):.2f})",
+                   "rows_per_step_padded": rows_pad,
                    "l2": "flushed (256 MiB write) between timed steps, outside the per-step CUDA-event brackets"},
         "e2e": {"value": e2e_value, "unit": "samples/s",
-                "h2d_bytes_per_step": BATCH * DIMS[0] * 8 + BATCH * 8, "d2h_bytes_per_step": 8,
-                "path": "moses_gradients + moses_apply_update (C ABI, pinned host float64 buffers)"},
+                "h2d_bytes_per_step": int(xb_host.size * 8 + BATCH * 8 + (BATCH + 1) * 8), "d2h_bytes_per_step": 8,
+                "path": "moses_gradients_pooled + moses_apply_update (C ABI, pinned host float64 buffers)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "umma_gemm_kernel (tcgen05 bf16, all fwd/dgrad/wgrad launches of a step)",

@@ -104,6 +104,10 @@ MOSES_API int moses_gradients(moses_model_t m, const double* features, const dou
 /* gradients() on device-resident packed rows (x_dev, ldx) and fp32 labels; no adversary. */
 MOSES_API int moses_gradients_device(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
                                      double* loss_out);
+/* gradients with segment-sum pooling (north-star (2)): n_stmt statement rows, `programs` programs with CSR
+ * offsets, one label per program. With all segments of length 1 this is moses_gradients. */
+MOSES_API int moses_gradients_pooled(moses_model_t m, const double* stmt_features, int64_t n_stmt, int32_t D,
+                                     const int64_t* offsets, int64_t programs, const double* labels, double* loss_out);
 MOSES_API int moses_gradients_download(moses_model_t m, double* grads, int64_t count);
 MOSES_API int moses_gradients_upload(moses_model_t m, const double* grads, int64_t count);
 /* objective (model.cpp:246-261) */
@@ -125,6 +129,13 @@ MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_
 MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
                                        int64_t n_batches, int64_t batch, double learning_rate, double momentum,
                                        int32_t with_update);
+/* TenSet-shaped variant: programs of variable statement counts. prog_off_dev: device int64 CSR offsets of
+ * every program's statement rows in x_base (n_batches * batch_programs + 1 entries); rows_pad >= the largest
+ * batch's statement count (GEMM row count captured in the graph; padding rows carry no gradient). */
+MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                              const int64_t* prog_off_dev, int64_t n_batches, int64_t batch_programs,
+                                              int64_t rows_pad, double learning_rate, double momentum,
+                                              int32_t with_update);
 MOSES_API int moses_train_graph_launch(moses_model_t m, int64_t steps);
 MOSES_API int moses_train_graph_kernels(void);
 /* ranking_accuracy (model.cpp:298-312): nb batches, rows [off[b], off[b+1]) of features/labels. */
@@ -202,6 +213,8 @@ MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t 
 MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype,
                                           void* dst, int64_t ld);
 MOSES_API int moses_synth_labels_device(uint64_t seed, int64_t row0, int64_t n, float* dst);
+/* CSR offsets of `programs` programs with 1 + below(max_stmts) statements each (host). */
+MOSES_API int moses_synth_offsets(uint64_t seed, int64_t programs, int32_t max_stmts, int64_t* offsets);
 
 /* ------------------------------------------------------------------ files (model.cpp:344-412, lottery.cpp:267-325) */
 MOSES_API int64_t moses_serialize(const int32_t* dims, int32_t ndims, const double* params, const double* momentum,

@@ -287,6 +287,9 @@ std::vector<R> transpose(const R* A, int rows, int cols) {
   return T;
 }
 
+template <class R>
+void segment_sum(const R* h, int width, const std::int64_t* offsets, std::int64_t programs, R* out);
+
 // ---------------------------------------------------------------- forward (model.cpp:54-62)
 template <class R>
 struct Forward {
@@ -479,6 +482,47 @@ std::vector<R> gradients(const Params<R>& p, const R* x, const R* y, int n, cons
   }
   backprop_from_penultimate(p, f, x, n, std::move(dh), g, threads);
   if (loss_out != nullptr) *loss_out = total_loss;
+  return g;
+}
+
+// North-star extension (parity pinned only by this restatement; S == 1 reduces to gradients()):
+// statement rows -> shared encoder -> per-program segment sum of the last hidden layer -> head.
+template <class R>
+std::vector<R> gradients_pooled(const Params<R>& p, const R* x, int nstmt, const std::int64_t* off, int programs,
+                                const R* y, R* loss_out, int threads = 1) {
+  const int L = p.levels();
+  const int dl = p.dims[L - 1];
+  std::vector<R> g(p.w.size(), R(0));
+  const Forward<R> f = run_forward(p, x, nstmt, threads);
+  const std::vector<R>& hl = f.h.back();
+  std::vector<R> pooled(std::size_t(programs) * dl, R(0));
+  segment_sum(hl.data(), dl, off, programs, pooled.data());
+  const R* wh = p.W(L - 1);
+  const R bh = p.B(L - 1)[0];
+  std::vector<R> s(programs);
+  for (int q = 0; q < programs; ++q) {
+    R acc = R(0);
+    for (int j = 0; j < dl; ++j) acc = std::fma(pooled[std::size_t(q) * dl + j], wh[j], acc);
+    s[q] = acc + bh;
+  }
+  R loss = R(0);
+  std::vector<R> gs(programs);
+  ranking_terms(s.data(), y, programs, loss_out ? &loss : nullptr, gs.data());
+  R* GW = g.data() + level_offset(p.dims, L - 1);
+  for (int j = 0; j < dl; ++j) {
+    R acc = R(0);
+    for (int q = 0; q < programs; ++q) acc = std::fma(gs[q], pooled[std::size_t(q) * dl + j], acc);
+    GW[j] = acc;
+  }
+  R gsum = R(0);
+  for (int q = 0; q < programs; ++q) gsum += gs[q];
+  GW[dl] = gsum;
+  std::vector<R> dh(std::size_t(nstmt) * dl);
+  for (int q = 0; q < programs; ++q)
+    for (std::int64_t i = off[q]; i < off[q + 1]; ++i)
+      for (int j = 0; j < dl; ++j) dh[std::size_t(i) * dl + j] = gs[q] * wh[j];
+  backprop_from_penultimate(p, f, x, nstmt, std::move(dh), g, threads);
+  if (loss_out) *loss_out = loss;
   return g;
 }
 

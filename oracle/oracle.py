@@ -105,6 +105,8 @@ def lib():
             getattr(_lib, f"orc_adam_{s}").argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
                                                       C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double,
                                                       C.c_int]
+        _lib.orc_gradients_pooled_f64.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib.orc_synth_features.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_int, C.c_void_p]
         _lib.orc_synth_labels.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_void_p]
         _lib.orc_synth_offsets.argtypes = [C.c_uint64, C.c_longlong, C.c_int, C.c_void_p]
@@ -207,6 +209,20 @@ def gradients(dims, w, x, y, adv=None, beta=0.0, want_loss=True, threads=1):
         args = (None, rt(0.0), None, 0)
     _check(getattr(lib(), f"orc_gradients_{_sfx(dt)}")(_p(d), len(d), _p(w), _p(x), _p(y), x.shape[0], *args,
                                                       rt(beta), _p(g), _p(loss) if want_loss else None, threads))
+    return g, float(loss[0])
+
+
+def gradients_pooled(dims, w, x, offsets, y, threads=1):
+    """Statement rows x, CSR program offsets, per-program labels y -> (g_flat, loss), fp64."""
+    d = _dims(dims)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    g = np.zeros_like(w)
+    loss = np.zeros(1)
+    _check(lib().orc_gradients_pooled_f64(_p(d), len(d), _p(w), _p(x), x.shape[0], _p(off), len(off) - 1, _p(y),
+                                          _p(g), _p(loss), threads))
     return g, float(loss[0])
 
 

@@ -141,6 +141,17 @@ ORC_RANK(f32, float)
 ORC_GRAD(f64, double)
 ORC_GRAD(f32, float)
 
+ORC int orc_gradients_pooled_f64(const int* dims, int nd, const double* w, const double* x, int nstmt,
+                                 const long long* off, int programs, const double* y, double* g_out, double* loss_out,
+                                 int threads) {
+  return guarded([&] {
+    Params<double> p = make_params<double>(dims, nd, w, nullptr);
+    std::vector<double> g = gradients_pooled(p, x, nstmt, reinterpret_cast<const std::int64_t*>(off), programs, y,
+                                             loss_out, threads);
+    std::memcpy(g_out, g.data(), sizeof(double) * g.size());
+  });
+}
+
 #define ORC_UPD(SUF, R)                                                                             \
   ORC void orc_apply_update_##SUF(R* w, R* mom, const R* g, long long P, double lr, double mu,    \
                                   const std::uint8_t* keep, int use_momentum) {                    \

@@ -197,6 +197,9 @@ struct moses_model {
   // CUDA graph of one device-resident training step (moses_train_graph_*)
   cudaGraphExec_t train_exec = nullptr;
   long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
+  float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
+  long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
+  int* seg_rows = nullptr;         // pooled: program of each statement row (cap)
   // parameters
   float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
   float *m1 = nullptr, *m2 = nullptr;
@@ -242,6 +245,9 @@ struct moses_model {
     for (void* p : dz) dfree(p);
     if (train_exec) cudaGraphExecDestroy(train_exec);
     dfree(dcounter);
+    dfree(gbias);
+    dfree(seg_off);
+    dfree(seg_rows);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
@@ -286,7 +292,8 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
 }
 
 template <typename T>
-void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u) {
+void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u,
+                   const float* gb_override = nullptr) {
   // Two streams: the data-gradient chain (head backward -> dgrad(L-2) -> ... -> dgrad(1)) runs on
   // st; every weight-gradient GEMM (and the head-gradient column reduction) runs on st2 as soon
   // as its dZ is ready. At batch 512 each GEMM fills only 16-40 of the 148 SMs, so the two
@@ -298,7 +305,7 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[0], 0));
   {
     ProfScope ps(P_HEAD, m->st2);
-    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2);
+    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2, gb_override);
   }
   {
     ProfScope ps(P_HEAD, m->st);
@@ -408,13 +415,21 @@ void dispatch_forward(moses_model* m, const void* x0, long long ldx0, long long 
   else forward_rows<float>(m, x0, ldx0, R, u, keep_last);
 }
 
-// gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch.
+// Segment-sum pooling of statement rows into programs (north-star (2); S == 1 is the reference).
+struct Pool {
+  const long long* seg_off = nullptr;  // device, programs+1 CSR offsets over statement rows
+  const int* seg_of_row = nullptr;     // device, program of each statement row (-1 = padding)
+  long long rows = 0;                  // statement rows incl. padding
+};
+
+// gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch;
+// pooled: rows [0, pool->rows) are statements of the n programs.
 void gradients_core(moses_model* m, const void* x0, long long ldx0, const float* y, long long n, moses_adversary* adv,
-                    double beta) {
-  const bool active = adv != nullptr && beta != 0.0 && n > 0;
+                    double beta, const Pool* pool = nullptr) {
+  const bool active = adv != nullptr && beta != 0.0 && n > 0 && pool == nullptr;
   const long long mrep = active ? adv->m : 0;
-  const long long R = mrep + n;
-  if (n == 0) {
+  const long long R = pool ? pool->rows : mrep + n;
+  if (n == 0 || R == 0) {
     MOSES_CUDA(cudaMemsetAsync(m->g, 0, sizeof(float) * m->P, m->st));
     MOSES_CUDA(cudaMemsetAsync(m->dscal, 0, sizeof(double) * 2, m->st));
     m->xi_valid = false;
@@ -423,16 +438,22 @@ void gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
   ProfScope ps(P_RANK, m->st);
-  rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), y, n,
+  rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), pool ? pool->seg_off : nullptr, y, n,
                    {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->scores, m->st);
   FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
+  if (pool) {
+    fo.seg_of_row = pool->seg_of_row;
+    fo.R_rows = R;
+    fo.gb = m->gbias;
+  }
   rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
                 active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
   note_launch(2);
   ps.~ProfScope();
   ps.idx = -1;
-  if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u);
-  else backward_rows<float>(m, x0, ldx0, R, u);
+  const float* gbo = pool ? m->gbias : nullptr;
+  if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, gbo);
+  else backward_rows<float>(m, x0, ldx0, R, u, gbo);
   m->xi_valid = false;
 }
 
@@ -568,6 +589,9 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     select_ws_carve(m->sel_base, seln, &m->sel);
     m->stage_w = std::max<long long>(maxw, 1) + 1;
     m->staging = dalloc<double>(m->cap * m->stage_w);
+    m->gbias = dalloc<float>(4);
+    m->seg_off = dalloc<long long>(m->cap + 1);
+    m->seg_rows = dalloc<int>(m->cap);
     m->adv_ws = dalloc<float>(round_up(m->cap, 64) + round_up(maxw + 1, 64) + 64 + 16 +
                               column_dot_ws_floats(m->cap, maxw) + 64);
     MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -939,6 +963,101 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
     MOSES_CUDA(cudaGraphDestroy(graph));
   });
 }
+MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                              const int64_t* prog_off_dev, int64_t n_batches, int64_t batch_programs,
+                                              int64_t rows_pad, double lr, double mu, int32_t with_update) {
+  return guarded([&] {
+    require_model(m);
+    check_rows(m, rows_pad);
+    if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
+    if (n_batches < 1 || batch_programs < 1) fail(MOSES_ERR_INVALID_ARG, "empty batch plan");
+    if (m->train_exec) {
+      cudaGraphExecDestroy(m->train_exec);
+      m->train_exec = nullptr;
+    }
+    if (!m->dcounter) m->dcounter = dalloc<long long>(1);
+    MOSES_CUDA(cudaMemsetAsync(m->dcounter, 0, sizeof(long long), m->st));
+    const long long row_bytes = ldx * m->esz;
+    const auto* po = reinterpret_cast<const long long*>(prog_off_dev);
+    Pool pool{m->seg_off, m->seg_rows, rows_pad};
+    auto gather = [&] {
+      gather_pooled(x_base, row_bytes, y_base, po, m->dcounter, n_batches, batch_programs, rows_pad, m->act[0],
+                    m->labels, m->seg_off, m->seg_rows, m->st);
+    };
+    gather();
+    gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    cudaGraph_t graph;
+    MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      gather();
+      gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool);
+      if (with_update) sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      advance_counter(m->dcounter, m->st);
+    } catch (...) {
+      cudaStreamEndCapture(m->st, &graph);
+      throw;
+    }
+    MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+    size_t nodes = 0;
+    MOSES_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
+    std::vector<cudaGraphNode_t> nv(nodes);
+    MOSES_CUDA(cudaGraphGetNodes(graph, nv.data(), &nodes));
+    long long kernels = 0;
+    for (auto n : nv) {
+      cudaGraphNodeType t;
+      MOSES_CUDA(cudaGraphNodeGetType(n, &t));
+      kernels += t == cudaGraphNodeTypeKernel;
+    }
+    g_graph_kernels = kernels;
+    MOSES_CUDA(cudaGraphInstantiate(&m->train_exec, graph, 0));
+    MOSES_CUDA(cudaGraphDestroy(graph));
+  });
+}
+
+MOSES_API int moses_gradients_pooled(moses_model_t m, const double* x, int64_t n_stmt, int32_t D, const int64_t* offsets,
+                                     int64_t programs, const double* y, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "statement feature width != model input width");
+    if (programs < 0 || offsets[0] != 0 || offsets[programs] != n_stmt)
+      fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must span the statement rows");
+    for (int64_t p = 0; p < programs; ++p)
+      if (offsets[p + 1] < offsets[p]) fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must be non-decreasing");
+    check_rows(m, n_stmt);
+    std::vector<int> rows(static_cast<size_t>(n_stmt));
+    for (int64_t p = 0; p < programs; ++p)
+      for (int64_t r = offsets[p]; r < offsets[p + 1]; ++r) rows[size_t(r)] = int(p);
+    upload_rows(m, x, n_stmt, 0);
+    upload_f32(m, y, programs, m->labels);
+    MOSES_CUDA(cudaMemcpyAsync(m->seg_off, offsets, sizeof(long long) * (programs + 1), cudaMemcpyHostToDevice, m->st));
+    if (n_stmt) MOSES_CUDA(cudaMemcpyAsync(m->seg_rows, rows.data(), sizeof(int) * n_stmt, cudaMemcpyHostToDevice, m->st));
+    Pool pool{m->seg_off, m->seg_rows, n_stmt};
+    gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool);
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    }
+    MOSES_CUDA(cudaStreamSynchronize(m->st));  // host vectors above must outlive the async copies
+  });
+}
+
+MOSES_API int moses_synth_offsets(uint64_t seed, int64_t programs, int32_t max_stmts, int64_t* offsets) {
+  // statements per program 1 + below(max_stmts) of stream KeyBuilder(seed,"stmts",p)
+  return guarded([&] {
+    if (max_stmts < 1) fail(MOSES_ERR_INVALID_ARG, "max_stmts must be >= 1");
+    offsets[0] = 0;
+    for (int64_t p = 0; p < programs; ++p) {
+      KeyBuilder k;
+      k.add(seed).add("stmts").add(uint64_t(p));
+      Rng r{k.h};
+      const uint64_t n = uint64_t(max_stmts), thr = (0 - n) % n;
+      uint64_t v;
+      do v = r.next(); while (v < thr);
+      offsets[p + 1] = offsets[p] + 1 + int64_t(v % n);
+    }
+  });
+}
+
 MOSES_API int moses_train_graph_launch(moses_model_t m, int64_t steps) {
   return guarded([&] {
     require_model(m);

@@ -127,6 +127,31 @@ __global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long lon
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < batch; i += (long long)gridDim.x * blockDim.x)
     ydst[i] = y_base[b * batch + i];
 }
+// TenSet-shaped batch: programs [b*B, (b+1)*B) of a CSR-packed statement dataset -> statement rows
+// [0, R_b) of dst, batch-relative offsets, program of each row (-1 on padding rows up to rows_pad).
+__global__ void gather_pooled_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
+                                     const long long* __restrict__ prog_off, const long long* __restrict__ counter,
+                                     long long nb, long long B, long long rows_pad, uint8_t* __restrict__ dst,
+                                     float* __restrict__ ydst, long long* __restrict__ seg_off, int* __restrict__ seg_rows) {
+  ptx::pdl_launch_dependents();
+  const long long b = (*counter) % nb;
+  const long long p0 = b * B, r0 = prog_off[p0], Rb = prog_off[p0 + B] - r0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(x_base + r0 * row_bytes);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const long long n16 = Rb * row_bytes / 16;
+  for (long long i = tid; i < n16; i += nthr) d[i] = src[i];
+  for (long long p = tid; p <= B; p += nthr) {
+    const long long lo = prog_off[p0 + p] - r0;
+    seg_off[p] = lo;
+    if (p < B) {
+      ydst[p] = y_base[p0 + p];
+      const long long hi = prog_off[p0 + p + 1] - r0;
+      for (long long r = lo; r < hi; ++r) seg_rows[r] = int(p);
+    }
+  }
+  for (long long r = Rb + tid; r < rows_pad; r += nthr) seg_rows[r] = -1;
+}
 __global__ void advance_counter_kernel(long long* c) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *c += 1;
 }
@@ -151,15 +176,26 @@ constexpr int kRankBlock = 128;
 constexpr int kRankChunk = 32;  // j columns per block: n=512 -> 4 x 16 blocks, n=4096 -> 32 x 128
 // Scores come either from `s` or, fused, from the last forward epilogue's per-N-tile partials
 // (s_r = b + sum_t part[t][r], the same fixed order as head_scores_kernel).
+// With `seg` (CSR program offsets over statement rows) the score of program r is the segment sum of
+// its statements' head dots (segment-sum pooling folded into the head).
 __device__ __forceinline__ float score_of(const float* __restrict__ s, const float* __restrict__ part, int ntiles,
-                                          long long ld, float hb, long long r) {
+                                          long long ld, float hb, const long long* __restrict__ seg, long long r) {
   if (part == nullptr) return s[r];
   float acc = 0.f;
-  for (int t = 0; t < ntiles; ++t) acc += part[t * ld + r];
+  if (seg == nullptr) {
+    for (int t = 0; t < ntiles; ++t) acc += part[t * ld + r];
+  } else {
+    for (long long i = seg[r]; i < seg[r + 1]; ++i) {
+      float a = 0.f;
+      for (int t = 0; t < ntiles; ++t) a += part[t * ld + i];
+      acc += a;
+    }
+  }
   return acc + hb;
 }
 __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __restrict__ s, const float* __restrict__ part,
                                                                 int ntiles, long long ld, const float* __restrict__ hbp,
+                                                                const long long* __restrict__ seg,
                                                                 const float* __restrict__ y, long long n, double* gs_part,
                                                                 double* loss_part, long long* pairs_part,
                                                                 float* __restrict__ s_out) {
@@ -169,12 +205,12 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
   const long long j0 = (long long)blockIdx.y * kRankChunk;
   const int cnt = int(min((long long)kRankChunk, n - j0));
   if (threadIdx.x < cnt) {
-    ss[threadIdx.x] = score_of(s, part, ntiles, ld, hb, j0 + threadIdx.x);
+    ss[threadIdx.x] = score_of(s, part, ntiles, ld, hb, seg, j0 + threadIdx.x);
     sy[threadIdx.x] = y[j0 + threadIdx.x];
   }
   __syncthreads();
   if (i >= n) return;
-  const float si = score_of(s, part, ntiles, ld, hb, i), yi = y[i];
+  const float si = score_of(s, part, ntiles, ld, hb, seg, i), yi = y[i];
   if (s_out != nullptr && blockIdx.y == 0) s_out[i] = si;
   float gs = 0.f, loss = 0.f;
   int pairs = 0;
@@ -230,7 +266,9 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
                                                                   long long roff, const float* part2, int ntiles2,
                                                                   long long ld2, const float* adv_bias, double beta,
                                                                   double* loss_out, long long* pairs_out, float* coefA,
-                                                                  float* coefB, double* ce_out) {
+                                                                  float* coefB, double* ce_out,
+                                                                  const int* __restrict__ seg_of_row, long long R_rows,
+                                                                  float* gb_out) {
   ptx::pdl_launch_dependents();
   using BR = cub::BlockReduce<double, kFinBlock>;
   using BRL = cub::BlockReduce<long long, kFinBlock>;
@@ -255,16 +293,38 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   __syncthreads();
   const long long pairs = sh_pairs;
   const double inv = pairs > 0 ? 1.0 / double(pairs) : 0.0;
-  const long long R = roff + n;
-  for (long long r = threadIdx.x; r < R; r += kFinBlock) {
-    float a = 0.f;
-    if (r >= roff) {
-      double g = 0.0;
-      for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + (r - roff)];
-      a = pairs > 0 ? float(g * inv) : 0.f;
+  const long long R = seg_of_row ? R_rows : roff + n;
+  if (seg_of_row != nullptr) {
+    // pooled: every statement row of program p carries d loss / d s_p (ds_p/dH_i = w_head for i in p);
+    // the head bias enters each program once, so its gradient is sum_p gs_p (written to gb_out).
+    double gbs = 0.0;
+    for (long long q = threadIdx.x; q < n; q += kFinBlock)
+      for (int sp = 0; sp < nsplit; ++sp) gbs += gs_part[sp * n + q];
+    for (long long r = threadIdx.x; r < R; r += kFinBlock) {
+      const int sg = seg_of_row[r];
+      float a = 0.f;
+      if (sg >= 0 && pairs > 0) {
+        double g = 0.0;
+        for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + sg];
+        a = float(g * inv);
+      }
+      coefA[r] = a;
+      coefB[r] = 0.f;
     }
-    coefA[r] = a;
-    coefB[r] = 0.f;
+    __syncthreads();
+    const double gbt = BR(tmp).Sum(gbs);
+    if (threadIdx.x == 0 && gb_out) *gb_out = pairs > 0 ? float(gbt * inv) : 0.f;
+  } else {
+    for (long long r = threadIdx.x; r < R; r += kFinBlock) {
+      float a = 0.f;
+      if (r >= roff) {
+        double g = 0.0;
+        for (int sp = 0; sp < nsplit; ++sp) g += gs_part[sp * n + (r - roff)];
+        a = pairs > 0 ? float(g * inv) : 0.f;
+      }
+      coefA[r] = a;
+      coefB[r] = 0.f;
+    }
   }
   double total = sh_loss;
   if (part2 != nullptr && beta != 0.0 && n > 0) {
@@ -338,8 +398,13 @@ __global__ void column_dot_kernel(const float* __restrict__ coef, const T* __res
     part[(long long)blockIdx.y * (W + 1) + j] = s;
   }
 }
-__global__ void column_sum_kernel(const float* __restrict__ part, int slabs, int W1, float* __restrict__ g) {
+__global__ void column_sum_kernel(const float* __restrict__ part, int slabs, int W1, float* __restrict__ g,
+                                  const float* __restrict__ last_override) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < W1; j += gridDim.x * blockDim.x) {
+    if (last_override != nullptr && j == W1 - 1) {
+      g[j] = *last_override;
+      continue;
+    }
     float s = 0.f;
     for (int q = 0; q < slabs; ++q) s += part[(long long)q * W1 + j];
     g[j] = s;
@@ -938,6 +1003,15 @@ void gather_batch(const void* x_base, long long row_bytes, const float* y_base, 
       static_cast<const uint8_t*>(x_base), row_bytes, y_base, counter, nb, batch, static_cast<uint8_t*>(dst), ydst);
   MOSES_CUDA(cudaGetLastError());
 }
+void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,
+                   const long long* counter, long long nb, long long B, long long rows_pad, void* dst, float* ydst,
+                   long long* seg_off, int* seg_rows, cudaStream_t s) {
+  if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
+  gather_pooled_kernel<<<grid_for(rows_pad * row_bytes / 16, 256), 256, 0, s>>>(
+      static_cast<const uint8_t*>(x_base), row_bytes, y_base, prog_off, counter, nb, B, rows_pad,
+      static_cast<uint8_t*>(dst), ydst, seg_off, seg_rows);
+  MOSES_CUDA(cudaGetLastError());
+}
 void advance_counter(long long* c, cudaStream_t s) {
   advance_counter_kernel<<<1, 32, 0, s>>>(c);
   MOSES_CUDA(cudaGetLastError());
@@ -969,15 +1043,15 @@ int rank_splits(long long n) { return n <= 0 ? 1 : ceil_div(n, kRankChunk); }
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st) {
   if (n <= 0) return;
   dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
-  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, nullptr, 0, 0, nullptr, y, n, ws.gs_part, ws.loss_part,
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, nullptr, 0, 0, nullptr, nullptr, y, n, ws.gs_part, ws.loss_part,
                                                  ws.pairs_part, nullptr);
   MOSES_CUDA(cudaGetLastError());
 }
-void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const float* y, long long n,
-                      const RankWs& ws, float* s_out, cudaStream_t st) {
+void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
+                      long long n, const RankWs& ws, float* s_out, cudaStream_t st) {
   if (n <= 0) return;
   dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
-  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(nullptr, part, ntiles, ld, hb, y, n, ws.gs_part, ws.loss_part,
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(nullptr, part, ntiles, ld, hb, seg, y, n, ws.gs_part, ws.loss_part,
                                                  ws.pairs_part, s_out);
   MOSES_CUDA(cudaGetLastError());
 }
@@ -986,7 +1060,7 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
                    const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st) {
   rank_finalize_kernel<<<1, kFinBlock, 0, st>>>(ws.gs_part, ws.loss_part, ws.pairs_part, ws.nsplit, n, roff, part2,
                                                 ntiles2, ld2, adv_bias, beta, out.loss, out.pairs, out.coefA, out.coefB,
-                                                out.ce);
+                                                out.ce, out.seg_of_row, out.R_rows, out.gb);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -999,14 +1073,15 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
 }
 
 template <typename T>
-void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st) {
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,
+                const float* bias_override) {
   const int slabs = R > 0 ? ceil_div(R, kColSlab) : 1;
   if (R <= 0) {
     MOSES_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (W + 1), st));
     return;
   }
   column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(coef, H, ldh, R, W, ws);
-  column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(ws, slabs, W + 1, g);
+  column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(ws, slabs, W + 1, g, bias_override);
   MOSES_CUDA(cudaGetLastError());
 }
 size_t column_dot_ws_floats(long long R, int W) { return size_t(R > 0 ? ceil_div(R, kColSlab) : 1) * (W + 1); }
@@ -1210,7 +1285,7 @@ void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, l
     const int slabs = ceil_div(R, kColSlab);
     float* part = reinterpret_cast<float*>(dc + 8);
     column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(dz, H, ldh, R, W, part);
-    column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(part, slabs, W + 1, du);
+    column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(part, slabs, W + 1, du, nullptr);
   }
   adv_update_kernel<<<ceil_div(W, 256), 256, 0, st>>>(u, c, du, W, eta, dc);
   MOSES_CUDA(cudaGetLastError());
@@ -1270,7 +1345,8 @@ void synth_labels(unsigned long long seed, long long row0, long long n, float* d
   template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t);                       \
   template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
                                  long long, int, T*, long long, cudaStream_t);                                    \
-  template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t);   \
+  template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t,     \
+                              const float*);                                                                      \
   template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \
                                   float*, float*, float, double*, float*, cudaStream_t);                          \
   template void segment_sum<T>(const T*, long long, int, const long long*, long long, float*, long long,          \

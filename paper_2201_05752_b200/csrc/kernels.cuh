@@ -29,6 +29,9 @@ void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, lo
 void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
                   long long batch, void* dst, float* ydst, cudaStream_t s);
 void advance_counter(long long* c, cudaStream_t s);
+void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,
+                   const long long* counter, long long nb, long long B, long long rows_pad, void* dst, float* ydst,
+                   long long* seg_off, int* seg_rows, cudaStream_t s);
 // out[r] = H[r] . u  (warp per row)
 void row_dot(const float* H, long long ldh, long long R, int W, const float* u, float* out, cudaStream_t s);
 // discriminator_cross_entropy (lottery.cpp:207-218) over z[0,m) source and z[m,m+n) target
@@ -46,8 +49,8 @@ struct RankWs {
 int rank_splits(long long n);
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st);
 // same, scores summed from the forward's per-N-tile head partials (+ head bias); s_out optional
-void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const float* y, long long n,
-                      const RankWs& ws, float* s_out, cudaStream_t st);
+void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
+                      long long n, const RankWs& ws, float* s_out, cudaStream_t st);
 // Reduces the rank partials (fixed order), normalises by the pair count, folds in the
 // adversary's logits when `part2` is given (model.cpp:215-238), and emits per-row
 // backward coefficients coefA (ranking) / coefB (adversary) over all R = roff + n rows.
@@ -57,6 +60,9 @@ struct FinalizeOut {
   float* coefA;       // [R]
   float* coefB;       // [R]
   double* ce;         // [1] discriminator CE (adversary on)
+  const int* seg_of_row = nullptr;  // pooled: program of each statement row (-1 = padding)
+  long long R_rows = 0;             // pooled: statement rows
+  float* gb = nullptr;              // pooled: head-bias gradient
 };
 void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
                    const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st);
@@ -66,7 +72,8 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
                    long long R, int W, T* dz, long long ldz, cudaStream_t st);
 // g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
 template <typename T>
-void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st);
+void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,
+                const float* bias_override = nullptr);
 size_t column_dot_ws_floats(long long R, int W);
 
 // ---- updates (model.cpp:263-296, lottery.cpp:92-120)

@@ -86,6 +86,9 @@ def lib():
         "moses_set_async": (C.c_int, [i32]),
         "moses_train_graph_create": (C.c_int, [vp, vp, i64, vp, i64, i64, dbl, dbl, i32]),
         "moses_train_graph_launch": (C.c_int, [vp, i64]),
+        "moses_train_graph_create_pooled": (C.c_int, [vp, vp, i64, vp, vp, i64, i64, i64, dbl, dbl, i32]),
+        "moses_gradients_pooled": (C.c_int, [vp, vp, i64, i32, vp, i64, vp, vp]),
+        "moses_synth_offsets": (C.c_int, [u64, i64, i32, vp]),
         "moses_train_graph_kernels": (C.c_int, []),
         "moses_profile_begin": (C.c_int, []),
         "moses_profile_end": (C.c_int, [vp, vp, i32]),
@@ -430,6 +433,28 @@ def gradients(model, batch: RankingBatch, adversary: Optional[AdversaryState] = 
         if tmp:
             dm.close()
     return (g, loss.value) if want_loss else g
+
+
+def gradients_pooled(model, stmt_features, offsets, labels, want_loss=False):
+    """Pooled (TenSet-shaped) gradient: statement rows, CSR program offsets, one label per program."""
+    x, y = _f64(stmt_features), _f64(labels)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    dm, tmp = _as_device(model, rows=max(x.shape[0], 1))
+    loss = C.c_double()
+    try:
+        _ck(lib().moses_gradients_pooled(dm.h, _p(x), x.shape[0], x.shape[1], _p(off), len(off) - 1, _p(y),
+                                         C.byref(loss)))
+        g = dm.gradients()
+    finally:
+        if tmp:
+            dm.close()
+    return (g, loss.value) if want_loss else g
+
+
+def synth_offsets(seed, programs, max_stmts=8) -> np.ndarray:
+    out = np.zeros(programs + 1, dtype=np.int64)
+    _ck(lib().moses_synth_offsets(seed, programs, max_stmts, _p(out)))
+    return out
 
 
 def objective(model, batch: RankingBatch, adversary=None, beta=0.0) -> float:

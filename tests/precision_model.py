@@ -144,6 +144,36 @@ def device_gradients(dims, w64, x, y, mode, adv=None, beta=0.0):
     return g, loss
 
 
+def device_gradients_pooled(dims, w64, x, offsets, y, mode):
+    """Pooled (TenSet-shaped) gradient as the device computes it: statement rows, CSR program offsets."""
+    rnd, w, f32_ = _mode(mode, w64)
+    off = np.asarray(offsets, np.int64)
+    P = len(off) - 1
+    s_rows, h_full, acts, ops, blocks = device_forward(dims, w64, x, mode)
+    L = len(dims) - 1
+    wh, bh, offh = blocks[-1]
+    dots = h_full @ wh[:, 0]
+    s = np.array([dots[off[q]:off[q + 1]].sum() for q in range(P)]) + bh[0]
+    coef_p, loss, _ = ranking_coef(f32_(s), np.asarray(y, np.float64))
+    coef_p = f32_(coef_p)
+    seg = np.repeat(np.arange(P), np.diff(off))
+    coefA = coef_p[seg]
+    g = np.zeros(len(w))
+    Hst = acts[-1]
+    g[offh:offh + dims[L - 1]] = coefA @ Hst
+    g[offh + dims[L - 1]] = coef_p.sum()
+    dz = rnd(f32_(np.outer(coefA, wh[:, 0])) * (Hst > 0))
+    for l in range(L - 2, -1, -1):
+        Wop, _ = ops[l]
+        _, _, o = blocks[l]
+        fi, fo = dims[l], dims[l + 1]
+        g[o:o + fi * fo] = (acts[l].T @ dz).reshape(-1)
+        g[o + fi * fo: o + fi * fo + fo] = dz.sum(0)
+        if l > 0:
+            dz = rnd(f32_(dz @ Wop.T) * (acts[l] > 0))
+    return g, loss
+
+
 def nrel(got, ref):
     got, ref = np.asarray(got, float), np.asarray(ref, float)
     return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))

@@ -584,3 +584,71 @@ def test_train_graph_matches_eager_steps(ml):
                                          batch, 0.001, 0.9, None))
     pa, pb = a.download(), b.download()
     assert np.array_equal(pa.params, pb.params) and np.array_equal(pa.momentum, pb.momentum)
+
+
+# ---------------------------------------------------------------- pooled (TenSet-shaped) training
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+@pytest.mark.parametrize("programs,max_stmts", [(12, 4), (512, 8)])
+def test_pooled_gradients(ml, orc, mode, programs, max_stmts):
+    from precision_model import device_gradients_pooled
+
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 8)
+    off = ml.synth_offsets(3, programs, max_stmts)
+    assert np.array_equal(off, orc.synth_offsets(3, programs, max_stmts))
+    x = rows(int(off[-1]), 164, 4)
+    y = labels(programs, 5)
+    dm = ml.DeviceModel(p, ml.PREC_TF32 if mode == "tf32" else ml.PREC_BF16, 4096)
+    g, loss = ml.gradients_pooled(dm, x, off, y, want_loss=True)
+    g_ref, _ = device_gradients_pooled(dims, p.params, x, off, y, mode)
+    ok, why = grad_close(g, g_ref)
+    assert ok, why
+    _, loss64 = orc.gradients_pooled(dims, p.params, x, off, y)
+    assert abs(loss - loss64) <= TOL_TF32 * max(1.0, abs(loss64))
+
+
+def test_pooled_with_unit_segments_equals_unpooled(ml):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 9)
+    x, y = rows(40, 16, 1), labels(40, 2)
+    dm = ml.DeviceModel(p, ml.PREC_BF16, 64)
+    g0 = ml.gradients(dm, ml.RankingBatch(x, y))
+    g1 = ml.gradients_pooled(dm, x, np.arange(41), y)
+    assert np.array_equal(g0[:-1], g1[:-1])  # everything but the head bias (summed in another order)
+    assert g1[-1] == pytest.approx(g0[-1], rel=1e-5, abs=1e-9)
+
+
+def test_pooled_train_graph(ml):
+    """Device-resident TenSet-shaped step (gather of variable-length programs + pooled gradients + update)
+    == the host pooled path, bit for bit."""
+    import torch
+
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 2)
+    L = ml.lib()
+    B, nb = 64, 3
+    off = ml.synth_offsets(7, B * nb, 8)
+    rows_total = int(off[-1])
+    per_batch = [int(off[(b + 1) * B] - off[b * B]) for b in range(nb)]
+    rows_pad = (max(per_batch) + 127) // 128 * 128
+    a = ml.DeviceModel(p, ml.PREC_BF16, rows_pad)
+    bm = ml.DeviceModel(p, ml.PREC_BF16, rows_pad)
+    ld = a.packed_ld
+    X = torch.empty((rows_total, ld), dtype=torch.bfloat16, device="cuda")
+    Y = torch.empty(B * nb, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(1, 0, rows_total, dims[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(1, 0, B * nb, Y.data_ptr()) == 0
+    OFF = torch.from_numpy(off).cuda()
+    torch.cuda.synchronize()
+    ml._ck(L.moses_train_graph_create_pooled(a.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, B, rows_pad,
+                                             0.001, 0.9, 1))
+    ml._ck(L.moses_train_graph_launch(a.h, 4))
+    xs = X.float().cpu().numpy()[:, :dims[0]].astype(np.float64)  # bf16-exact values
+    ys = Y.cpu().numpy().astype(np.float64)
+    for s in range(4):
+        b = s % nb
+        lo, hi = int(off[b * B]), int(off[(b + 1) * B])
+        ml.gradients_pooled(bm, xs[lo:hi], off[b * B:(b + 1) * B + 1] - lo, ys[b * B:(b + 1) * B])
+        ml.apply_update(bm, ml.TrainHyper(learning_rate=0.001, momentum=0.9), None, True)
+    pa, pb = a.download(), bm.download()
+    assert np.array_equal(pa.params, pb.params)

@@ -304,3 +304,25 @@ def test_synthetic_generator_matches_rng(orc):
     off = orc.synth_offsets(1, 100, 8)
     lens = np.diff(off)
     assert lens.min() >= 1 and lens.max() <= 8
+
+
+def test_pooled_gradients_reduce_and_fd(orc):
+    """Segment-sum pooling (north-star extension): S == 1 is exactly gradients(); FD agreement otherwise."""
+    dims = [4, 8, 8, 1]
+    w = orc.init_random(dims, 3)
+    rng = np.random.default_rng(0)
+    x, y = rng.random((7, 4)), 0.1 + rng.random(7)
+    g1, l1 = orc.gradients_pooled(dims, w, x, np.arange(8), y)
+    g2, l2 = orc.gradients(dims, w, x, y)
+    assert np.array_equal(g1, g2) and l1 == l2
+    off = np.array([0, 2, 3, 6, 7])
+    yp = 0.1 + rng.random(4)
+    g, _ = orc.gradients_pooled(dims, w, x, off, yp)
+    h, worst = 1e-6, 0.0
+    for i in range(len(w)):
+        wp, wm = w.copy(), w.copy()
+        wp[i] += h
+        wm[i] -= h
+        fd = (orc.gradients_pooled(dims, wp, x, off, yp)[1] - orc.gradients_pooled(dims, wm, x, off, yp)[1]) / (2 * h)
+        worst = max(worst, abs(fd - g[i]) / max(abs(fd), abs(g[i]), 1e-3))
+    assert worst < 1e-4

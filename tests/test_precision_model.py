@@ -32,3 +32,16 @@ def test_model_with_adversary_matches_oracle(orc):
         g_ref, l_ref = orc.gradients(dims, w, x, y, (u, 0.1, replay), beta)
         g, l = device_gradients(dims, w, x, y, "none", (u, 0.1, replay), beta)
         assert nrel(g, g_ref) < 1e-12 and abs(l - l_ref) < 1e-12
+
+
+def test_pooled_model_matches_oracle(orc):
+    from precision_model import device_gradients_pooled
+
+    dims = [6, 16, 16, 1]
+    w = orc.init_random(dims, 4)
+    off = orc.synth_offsets(2, 9, 4)
+    rng = np.random.default_rng(5)
+    x, y = rng.random((int(off[-1]), 6)), 0.1 + rng.random(9)
+    g_ref, l_ref = orc.gradients_pooled(dims, w, x, off, y)
+    g, l = device_gradients_pooled(dims, w, x, off, y, "none")
+    assert nrel(g, g_ref) < 1e-12 and abs(l - l_ref) < 1e-12
