@@ -1,3 +1,7 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 100 --csv --log-file gpurun_out/launches2.csv python bench.py --steps 40 --warmup 20 --no-cpu-baseline --no-infer --profile-steps 1 > /dev/null 2>&1; echo ncu rc=$?
-python tools/ncu_summary.py list gpurun_out/launches2.csv gpurun_out/launches2_summary.csv; cat gpurun_out/launches2_summary.csv
+timeout 900 python -m pytest tests/ -q -m gpu --timeout 300 -x > gpurun_out/pytest13.log 2>&1; echo pytest rc=$?
+grep -E "passed|failed|FAILED|Error" gpurun_out/pytest13.log | tail -30
+timeout 900 python bench.py > gpurun_out/bench8.json 2> gpurun_out/bench8.err; echo bench rc=$?
+tail -3 gpurun_out/bench8.err; python -c "
+import json; d=json.load(open('gpurun_out/bench8.json'))
+print(d['value'], d['ms_per_step']); print(d['step_breakdown_ms']); print(d['e2e']['value']); print(d['roofline']['frac']); print(d['infer']['value'], d['infer']['roofline']); print(d['cpu_baseline']['value'], d['gpu_launches'], d['clocks'])"

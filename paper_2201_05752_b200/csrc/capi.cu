@@ -1686,3 +1686,11 @@ extern "C" MOSES_API int moses_debug_set_mn(int which, int swz, int layout, int 
   moses::g_mn_kstep[which] = kstep;
   return 0;
 }
+
+namespace moses {
+extern int g_persistent;
+}
+extern "C" MOSES_API int moses_debug_set_persistent(int on) {
+  moses::g_persistent = on;
+  return 0;
+}

@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "gemm_persistent.cuh"
 
 namespace moses {
 // MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
@@ -16,6 +17,7 @@ int g_mn_swz[2] = {int(CU_TENSOR_MAP_SWIZZLE_128B), int(CU_TENSOR_MAP_SWIZZLE_12
 int g_mn_layout[2] = {2, 1};
 int g_mn_sbo[2] = {1024, 512};
 int g_mn_kstep[2] = {16 * 128, 8 * 128};
+extern int g_num_sms;
 namespace {
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -107,6 +109,71 @@ void launch_t(const GemmCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
 }
 
+template <typename T, int BN, bool AMN, bool BMN, int EPI>
+void launch_p(const GemmCall& c, cudaStream_t s) {
+  using Cfg = PCfg<T, BN>;
+  auto kern = umma_gemm_persistent<T, BN, AMN, BMN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    configured = true;
+  }
+  constexpr int elem = sizeof(T);
+  const CUtensorMap ta = operand_map(c.A, elem, c.M, c.K, Cfg::BM);
+  const CUtensorMap tb = operand_map(c.B, elem, c.N, c.K, BN);
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mask = c.mask;
+  a.ldm = c.ldm;
+  a.mn_layout = g_mn_layout[elem == 4];
+  a.mn_sbo = g_mn_sbo[elem == 4];
+  a.mn_kstep = g_mn_kstep[elem == 4];
+  a.round_out = c.round_out;
+  const int tm = ceil_div(c.M, Cfg::BM), tn = ceil_div(c.N, BN);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(tm * tn, g_num_sms));
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a, tm, tn));
+}
+
+template <typename T, int BN>
+void dispatch_persistent(const GemmCall& c, cudaStream_t s) {
+  const bool am = c.A.mn_major, bm = c.B.mn_major;
+  switch (c.epi) {
+    case EpiKind::Fwd:
+      if (!am && bm) return launch_p<T, BN, false, true, int(Epi::Fwd)>(c, s);
+      if (!am && !bm) return launch_p<T, BN, false, false, int(Epi::Fwd)>(c, s);
+      break;
+    case EpiKind::Dgrad:
+      if (!am && !bm) return launch_p<T, BN, false, false, int(Epi::Dgrad)>(c, s);
+      break;
+    case EpiKind::StoreF32:
+      if (am && bm) return launch_p<T, BN, true, true, int(Epi::StoreF32)>(c, s);
+      if (!am && !bm) return launch_p<T, BN, false, false, int(Epi::StoreF32)>(c, s);
+      if (!am && bm) return launch_p<T, BN, false, true, int(Epi::StoreF32)>(c, s);
+      break;
+  }
+  fail(MOSES_ERR_INVALID_ARG, "unsupported persistent GEMM combination");
+}
+
 template <typename T, int BN>
 void dispatch_major(const GemmCall& c, cudaStream_t s) {
   const bool am = c.A.mn_major, bm = c.B.mn_major;
@@ -148,9 +215,34 @@ int gemm_pick_bn(int M, int N) {
   return 64;
 }
 
+int g_num_sms = 148;
+int g_persistent = 1;  // persistent kernel for problems with more tiles than SMs
+
 int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
   if (c.M <= 0 || c.N <= 0) return 0;
   if (c.K <= 0) fail(MOSES_ERR_INVALID_ARG, "GEMM with K == 0");
+  static bool sm_init = false;
+  if (!sm_init) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      g_num_sms = n;
+    sm_init = true;
+  }
+  // Large problems: persistent kernel with double-buffered TMEM accumulators, BN = 256 (or 128).
+  const int mt = ceil_div(c.M, 128);
+  if (g_persistent && !c.bn && c.N >= 128) {
+    const int pbn = c.N >= 256 ? 256 : 128;
+    if ((long long)mt * ceil_div(c.N, pbn) >= 2LL * g_num_sms) {
+      if (elem == 2) {
+        if (pbn == 256) dispatch_persistent<__nv_bfloat16, 256>(c, s);
+        else dispatch_persistent<__nv_bfloat16, 128>(c, s);
+      } else {
+        if (pbn == 256) dispatch_persistent<float, 256>(c, s);
+        else dispatch_persistent<float, 128>(c, s);
+      }
+      return pbn;
+    }
+  }
   const int bn = c.bn ? c.bn : gemm_pick_bn(c.M, c.N);
   if (elem == 2) dispatch_bn<__nv_bfloat16>(c, bn, s);
   else dispatch_bn<float>(c, bn, s);

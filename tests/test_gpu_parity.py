@@ -615,7 +615,7 @@ def test_pooled_with_unit_segments_equals_unpooled(ml):
     g0 = ml.gradients(dm, ml.RankingBatch(x, y))
     g1 = ml.gradients_pooled(dm, x, np.arange(41), y)
     assert np.array_equal(g0[:-1], g1[:-1])  # everything but the head bias (summed in another order)
-    assert g1[-1] == pytest.approx(g0[-1], rel=1e-5, abs=1e-9)
+    assert abs(g1[-1] - g0[-1]) < 1e-6  # sum_p gs_p is 0 up to rounding noise
 
 
 def test_pooled_train_graph(ml):
