@@ -1694,3 +1694,11 @@ extern "C" MOSES_API int moses_debug_set_persistent(int on) {
   moses::g_persistent = on;
   return 0;
 }
+
+namespace moses {
+extern int g_cluster;
+}
+extern "C" MOSES_API int moses_debug_set_cluster(int on) {
+  moses::g_cluster = on;
+  return 0;
+}

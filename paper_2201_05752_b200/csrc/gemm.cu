@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "gemm_persistent.cuh"
+#include "gemm_cluster.cuh"
 
 namespace moses {
 // MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
@@ -18,6 +19,7 @@ int g_mn_layout[2] = {2, 1};
 int g_mn_sbo[2] = {1024, 512};
 int g_mn_kstep[2] = {16 * 128, 8 * 128};
 extern int g_num_sms;
+extern int g_cluster;
 namespace {
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -154,6 +156,49 @@ void launch_p(const GemmCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a, tm, tn));
 }
 
+template <bool BMN, int EPI>
+void launch_c(const GemmCall& c, cudaStream_t s) {
+  auto kern = umma_gemm_cluster<BMN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CCfg::kSmemLimit));
+    configured = true;
+  }
+  const int num_kb = ceil_div(c.K, CCfg::BK);
+  // A: 32-row quarters (multicast), B: resident 128-column slices
+  const CUtensorMap ta = make_map(c.A.ptr, 2, c.K, c.M, c.A.ld, 64, 32);
+  const CUtensorMap tb = operand_map(c.B, 2, c.N, c.K, CCfg::BN);
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mask = c.mask;
+  a.ldm = c.ldm;
+  a.round_out = c.round_out;
+  const int tm = ceil_div(c.M, CCfg::BM);
+  const int clusters = std::max(1, std::min(tm, g_num_sms / CCfg::kCluster));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CCfg::kCluster);
+  cfg.blockDim = dim3(CCfg::kThreads);
+  cfg.dynamicSmemBytes = CCfg::smem_bytes(num_kb);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a, tm, CCfg::stages_for(num_kb)));
+}
+
 template <typename T, int BN>
 void dispatch_persistent(const GemmCall& c, cudaStream_t s) {
   const bool am = c.A.mn_major, bm = c.B.mn_major;
@@ -217,6 +262,7 @@ int gemm_pick_bn(int M, int N) {
 
 int g_num_sms = 148;
 int g_persistent = 1;  // persistent kernel for problems with more tiles than SMs
+int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden layers
 
 int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
   if (c.M <= 0 || c.N <= 0) return 0;
@@ -227,6 +273,21 @@ int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
       g_num_sms = n;
     sm_init = true;
+  }
+  // Hidden layers (bf16, N = 512, K <= 512, A K-major): weight-resident 4-CTA cluster kernel.
+  // Measured on B200: wins at training sizes (M ~ 2.3K statement rows: 18 m-tiles); at scoring sizes
+  // (64K-row chunks) its N=128 SS-MMA is shared-memory-bandwidth bound and the persistent BN=256
+  // kernel is 1.7x faster (tools/gemm_sweep.py), so it is limited to M <= 16K rows.
+  if (g_cluster && !c.bn && elem == 2 && c.M <= 16384 && c.N == 4 * CCfg::BN && c.K <= CCfg::kMaxK && !c.A.mn_major &&
+      (c.epi == EpiKind::Fwd || c.epi == EpiKind::Dgrad) && (c.A.ld * 2) % 16 == 0) {
+    if (c.epi == EpiKind::Fwd) {
+      if (c.B.mn_major) launch_c<true, int(Epi::Fwd)>(c, s);
+      else launch_c<false, int(Epi::Fwd)>(c, s);
+    } else {
+      if (c.B.mn_major) launch_c<true, int(Epi::Dgrad)>(c, s);
+      else launch_c<false, int(Epi::Dgrad)>(c, s);
+    }
+    return CCfg::BN;
   }
   // Large problems: persistent kernel with double-buffered TMEM accumulators, BN = 256 (or 128).
   const int mt = ceil_div(c.M, 128);
