@@ -230,6 +230,103 @@ def bench_infer(ml, L, local, programs, peaks, reps=3):
             "inputs": "device-resident bf16 packed features (3.4 GB > L2)"}
 
 
+def bench_hbm_kernels(ml, L, peaks):
+    """HBM-roofline kernels of the north star on L2-exceeding sizes (> 126 MB working sets):
+    fused lottery step (xi -> partition -> step -> decay), momentum update, segment-sum pooling,
+    candidate top-k. achieved = algorithmic bytes / device time."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
+
+    from paper_2201_05752_b200.distributed import device_gradient_tensor
+
+    hbm = peaks.get("hbm_gbs", 6534.1)
+    out = {}
+
+    def timed(fn, stream, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1000.0
+
+    # ---- parameter-vector kernels on a 268M-scalar model (1 GB per fp32 array)
+    dims = [32768, 8192, 8, 1]
+    P = ml.param_count(dims)
+    dm = ml.DeviceModel(ml.CostModelParams(dims, np.zeros(P)), ml.PREC_BF16, max_rows=128)
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    st = torch.cuda.ExternalStream(sp.value)
+    wptr = C.POINTER(C.c_float)()
+    L.moses_model_device_ptrs(dm.h, C.byref(wptr), None, None)
+
+    class _CAI:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+    w = torch.as_tensor(_CAI(C.cast(wptr, C.c_void_p).value, P), device="cuda")
+    g = device_gradient_tensor(dm)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    w.normal_(0, 0.05, generator=gen)
+    g.normal_(0, 1e-2, generator=gen)
+    g[torch.rand(P, device="cuda", generator=gen) < 0.4] = 0.0  # zero-gradient ties (README.md:106-113)
+    torch.cuda.synchronize()
+    pop = C.c_int64()
+    for mode, value, name in ((2, 0.5, "lottery_step_ratio0.5"), (1, 0.5, "lottery_step_threshold0.5")):
+        t = timed(lambda: ml._ck(L.moses_lottery_step(dm.h, mode, value, 0, 1e-3, 1e-2, None, 0, C.byref(pop))), st)
+        algo = 15.0 * P  # read w,g; write w; mask byte; bf16 operand shadow
+        out[name] = {"params": P, "ms": t * 1e3, "algorithmic_bytes": algo, "achieved_gbs": algo / t / 1e9,
+                     "frac": algo / t / 1e9 / hbm, "bytes_per_param": 15}
+    L.moses_set_async(1)
+    t = timed(lambda: ml._ck(L.moses_apply_update(dm.h, 1e-3, 0.9, None, 0, 1)), st)
+    L.moses_set_async(0)
+    algo = 22.0 * P  # read w,v,g; write w,v; bf16 shadow
+    out["momentum_update"] = {"params": P, "ms": t * 1e3, "algorithmic_bytes": algo, "achieved_gbs": algo / t / 1e9,
+                              "frac": algo / t / 1e9 / hbm, "bytes_per_param": 22}
+    del w, g
+    dm.close()
+    torch.cuda.empty_cache()
+
+    # ---- segment-sum pooling: 4M statement rows x 512 bf16 -> programs x 512 fp32
+    programs = 900_000
+    off = ml.synth_offsets(11, programs, MAX_STMTS)
+    rows = int(off[-1])
+    H = torch.empty((rows, 512), dtype=torch.bfloat16, device="cuda").normal_(generator=gen)
+    OFF = torch.from_numpy(off).cuda()
+    PO = torch.empty((programs, 512), dtype=torch.float32, device="cuda")
+    cur = torch.cuda.current_stream()
+    t = timed(lambda: ml._ck(L.moses_segment_sum_device(H.data_ptr(), ml.DTYPE_BF16, 512, 512, OFF.data_ptr(),
+                                                        programs, PO.data_ptr())), cur)
+    algo = rows * 512 * 2 + programs * 512 * 4 + (programs + 1) * 8
+    out["segment_sum_pooling"] = {"rows": rows, "programs": programs, "ms": t * 1e3, "algorithmic_bytes": algo,
+                                  "achieved_gbs": algo / t / 1e9, "frac": algo / t / 1e9 / hbm}
+    del H, PO
+    torch.cuda.empty_cache()
+
+    # ---- candidate top-k over 100M fp32 scores (k = 1024)
+    n = 100_000_000
+    Sc = torch.empty(n, dtype=torch.float32, device="cuda").normal_(generator=gen)
+    idx = (C.c_int64 * 1024)()
+    ml._ck(L.moses_topk_device(Sc.data_ptr(), n, 1024, idx))
+    t0 = time.perf_counter()
+    for _ in range(3):
+        ml._ck(L.moses_topk_device(Sc.data_ptr(), n, 1024, idx))
+    t = (time.perf_counter() - t0) / 3
+    out["topk_100M"] = {"n": n, "k": 1024, "ms": t * 1e3, "algorithmic_bytes": 4 * n, "achieved_gbs": 4 * n / t / 1e9,
+                        "frac": 4 * n / t / 1e9 / hbm, "note": "wall clock incl. one host sync"}
+    del Sc
+    torch.cuda.empty_cache()
+    out["peak_gbs"] = hbm
+    out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs"
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -239,6 +336,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-infer", action="store_true")
+    ap.add_argument("--no-hbm", action="store_true")
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -431,6 +529,8 @@ def main():
     }
     if not args.no_infer:
         line["infer"] = bench_infer(ml, L, local, args.infer_programs, peaks)
+    if not args.no_hbm:
+        line["hbm_kernels"] = bench_hbm_kernels(ml, L, peaks)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(15.0)
     print(json.dumps(line), flush=True)

@@ -198,6 +198,7 @@ struct moses_model {
   cudaGraphExec_t train_exec = nullptr;
   long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
+  void* lot_ws = nullptr;          // fused lottery-step workspace (lottery.cu)
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
   int* seg_rows = nullptr;         // pooled: program of each statement row (cap)
   // parameters
@@ -246,6 +247,7 @@ struct moses_model {
     if (train_exec) cudaGraphExecDestroy(train_exec);
     dfree(dcounter);
     dfree(gbias);
+    dfree(lot_ws);
     dfree(seg_off);
     dfree(seg_rows);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
@@ -1274,21 +1276,35 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
   return guarded([&] {
     require_model(m);
     const long long keep = partition_validate(m, mode, value, true /* the tuner normalises in threshold mode */);
-    if (mode == MOSES_MODE_RATIO && keep >= m->P) {
-      MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
-    } else {
-      ProfScope ps(P_SELECT, m->st);
-      lottery_select(m->w, m->g, m->P, mode, float(value), keep, m->sel, m->mask, nullptr, false, m->st);
-      note_launch(mode == MOSES_MODE_RATIO ? 8 : 3);
-    }
     // step on kept scalars; decay the rest (reference order: step, then decay validation)
     const double rate = alpha * lambda;
     const bool decay_ok = (rate >= 0.0) && rate < 1.0;
     const bool decay = decay_ok && rate != 0.0;
-    lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
-    note_launch(1);
+    if (mode == MOSES_MODE_RATIO && keep >= m->P) {
+      MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
+      lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
+      note_launch(1);
+    } else {
+      if (!m->lot_ws) MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes()));
+      ProfScope ps(P_SELECT, m->st);
+      lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha), float(1.0 - rate), decay,
+                         m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);
+      note_launch(mode == MOSES_MODE_RATIO ? 7 : 3);
+    }
     m->xi_valid = false;
-    const long long pop = finish_mask(m, mode, keep, mask_out, count);
+    long long pop = std::min(keep, m->P);
+    if (mode == MOSES_MODE_THRESHOLD) {
+      unsigned long long h = 0;
+      MOSES_CUDA(cudaMemcpyAsync(&h, m->dcount, sizeof(h), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      pop = (long long)h;
+    }
+    if (mask_out) {
+      if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "mask count mismatch");
+      MOSES_CUDA(cudaMemcpyAsync(mask_out, m->mask, m->P, cudaMemcpyDeviceToHost, m->st));
+    }
+    if (sync_updates() || mask_out) MOSES_CUDA(cudaStreamSynchronize(m->st));
+    m->mask_valid = true;
     if (popcount) *popcount = pop;
     if (!decay_ok) {
       bool noop;

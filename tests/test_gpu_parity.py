@@ -652,3 +652,24 @@ def test_pooled_train_graph(ml):
         ml.apply_update(bm, ml.TrainHyper(learning_rate=0.001, momentum=0.9), None, True)
     pa, pb = a.download(), bm.download()
     assert np.array_equal(pa.params, pb.params)
+
+
+@pytest.mark.parametrize("rho", [0.3, 0.5, 0.7])
+def test_fused_lottery_step_large_bit_exact(ml, orc, rho):
+    """8.4M scalars (multi-round histogram passes), 40% zero-gradient ties, ratio mode: mask and
+    updated weights bit-identical to xi -> nth_element partition -> step -> decay in fp32."""
+    dims = [4096, 2048, 8, 1]
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(int(rho * 10))
+    w = f32(rng.normal(0, 0.05, P))
+    g = f32(rng.normal(0, 1e-2, P))
+    g[rng.random(P) < 0.4] = 0.0
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    dm.set_gradients(g)
+    mask = ml.lottery_step(dm, ml.RATIO, rho, 0, 0.001, 0.01)
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    ref_mask = orc.partition(orc.xi_scores(w32, g32, False), False, orc.RATIO, rho)
+    assert np.array_equal(mask.transferable, ref_mask)
+    ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+    ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
+    assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
