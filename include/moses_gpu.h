@@ -53,7 +53,9 @@ enum {
   MOSES_ERR_INVALID_ARG = 103
 };
 
-enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1 };            /* GEMM operand precision */
+/* GEMM operand precision. FP32 = 3xTF32 split operands (hi*hi + hi*lo + lo*hi on kind::tf32):
+ * fp32-level accuracy (the <= 1e-5 parity path); host-API inputs only, no training graphs. */
+enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1, MOSES_PREC_FP32 = 2 };
 enum { MOSES_MODE_THRESHOLD = 1, MOSES_MODE_RATIO = 2 };        /* PartitionMode, "MOSK" mode byte */
 enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1 };
 

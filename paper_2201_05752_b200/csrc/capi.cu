@@ -190,6 +190,7 @@ struct moses_model {
   std::vector<long long> off;
   int prec = MOSES_PREC_BF16;
   int esz = 2;
+  bool split = false;  // MOSES_PREC_FP32: 3xTF32 operands, every GEMM operand buffer has a low twin
   long long cap = 0;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;      // weight-gradient side stream
@@ -206,7 +207,7 @@ struct moses_model {
   float *m1 = nullptr, *m2 = nullptr;
   uint8_t* mask = nullptr;
   __nv_bfloat16* wbf = nullptr;  // bf16 operand shadow (BF16 mode)
-  float* wtf = nullptr;          // tf32-rounded operand shadow (TF32 mode)
+  float* wtf = nullptr;          // tf32-rounded operand shadow (TF32 mode; FP32 mode: [hi P | lo P])
   bool xi_valid = false, xi_norm = false, mask_valid = false;
   // activations
   std::vector<void*> act, dz;
@@ -228,7 +229,15 @@ struct moses_model {
   const void* wop(int l) const {
     return esz == 2 ? static_cast<const void*>(wbf + off[l]) : static_cast<const void*>(wtf + off[l]);
   }
-  Shadow shadow() const { return esz == 2 ? Shadow{wbf, 1} : Shadow{wtf, 2}; }
+  // shadow written by the fused update kernels; FP32 mode refreshes the hi/lo pair afterwards
+  Shadow shadow() const { return esz == 2 ? Shadow{wbf, 1} : (split ? Shadow{nullptr, 0} : Shadow{wtf, 2}); }
+  Shadow shadow_full() const { return split ? Shadow{wtf, 3} : shadow(); }
+  const float* wop_lo(int l) const { return split ? wtf + shadow_lo_offset(P) + off[l] : nullptr; }
+  float* act_lo(int l) const { return split ? static_cast<float*>(act[l]) + cap * ld[l] : nullptr; }
+  float* dz_lo(int l) const { return split ? static_cast<float*>(dz[l]) + cap * lddz[l] : nullptr; }
+  void post_update() {  // FP32 mode: hi/lo operand pair of the updated parameters
+    if (split) refresh_shadow(w, P, shadow_full(), st);
+  }
   int width(int l) const { return dims[l]; }
   int W() const { return dims[L - 1]; }
   const float* head_w() const { return w + off[L - 1]; }
@@ -262,13 +271,15 @@ namespace {
 // ---------------------------------------------------------------- forward / backward composition
 template <typename T>
 void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
+  if (m->split && x0 != m->act[0])
+    fail(MOSES_ERR_INVALID_ARG, "FP32 (3xTF32) handles take inputs through the host API only");
   for (int l = 0; l + 1 < m->L; ++l) {
     GemmCall c{};
     c.M = int(R);
     c.N = m->dims[l + 1];
     c.K = m->dims[l];
-    c.A = {l == 0 ? x0 : m->act[l], l == 0 ? ldx0 : m->ld[l], false};
-    c.B = {m->wop(l), m->dims[l + 1], true};
+    c.A = {l == 0 ? x0 : m->act[l], l == 0 ? ldx0 : m->ld[l], false, m->act_lo(l)};
+    c.B = {m->wop(l), m->dims[l + 1], true, m->wop_lo(l)};
     c.epi = EpiKind::Fwd;
     const bool last = l + 2 == m->L;
     c.out = (last && !keep_last) ? nullptr : m->act[l + 1];
@@ -276,6 +287,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     c.bias = m->bias(l);
     c.relu = 1;
     c.round_out = !last;  // the last hidden layer is never a GEMM operand: keep it full fp32
+    if (!last) c.out_lo = m->act_lo(l + 1);
     if (last) {
       c.head_w = m->head_w();
       c.head_u = head_u;
@@ -312,7 +324,7 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   {
     ProfScope ps(P_HEAD, m->st);
     head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
-                     m->lddz[L - 1], m->st);
+                     m->lddz[L - 1], m->st, m->dz_lo(L - 1));
   }
   MOSES_CUDA(cudaEventRecord(ev[1 + (L - 1)], m->st));
   note_launch(2);
@@ -323,8 +335,8 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     wg.M = m->dims[l] + 1;  // + the ones column -> bias gradient row (flat layout: W block then b)
     wg.N = m->dims[l + 1];
     wg.K = int(R);
-    wg.A = {a, lda, true};
-    wg.B = {m->dz[l + 1], m->lddz[l + 1], true};
+    wg.A = {a, lda, true, m->act_lo(l)};
+    wg.B = {m->dz[l + 1], m->lddz[l + 1], true, m->dz_lo(l + 1)};
     wg.epi = EpiKind::StoreF32;
     wg.out = m->g + m->off[l];
     wg.ldo = m->dims[l + 1];
@@ -339,10 +351,11 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       dg.M = int(R);
       dg.N = m->dims[l];
       dg.K = m->dims[l + 1];
-      dg.A = {m->dz[l + 1], m->lddz[l + 1], false};
-      dg.B = {m->wop(l), m->dims[l + 1], false};
+      dg.A = {m->dz[l + 1], m->lddz[l + 1], false, m->dz_lo(l + 1)};
+      dg.B = {m->wop(l), m->dims[l + 1], false, m->wop_lo(l)};
       dg.epi = EpiKind::Dgrad;
       dg.out = m->dz[l];
+      dg.out_lo = m->dz_lo(l);
       dg.ldo = m->lddz[l];
       dg.mask = m->act[l];
       dg.ldm = m->ld[l];
@@ -378,7 +391,8 @@ void upload_rows(moses_model* m, const double* x, long long n, long long row0) {
       pack_rows<__nv_bfloat16>(m->staging, c, D, static_cast<__nv_bfloat16*>(m->act[0]) + (row0 + r) * m->ld[0],
                                m->ld[0], m->st);
     else
-      pack_rows<float>(m->staging, c, D, static_cast<float*>(m->act[0]) + (row0 + r) * m->ld[0], m->ld[0], m->st);
+      pack_rows<float>(m->staging, c, D, static_cast<float*>(m->act[0]) + (row0 + r) * m->ld[0], m->ld[0], m->st,
+                       m->split ? m->act_lo(0) + (row0 + r) * m->ld[0] : nullptr);
     note_launch(1);
     r += c;
   }
@@ -387,7 +401,7 @@ void upload_replay(moses_model* m, const moses_adversary* a) {
   if (m->esz == 2)
     pack_rows_f32<__nv_bfloat16>(a->replay, a->m, a->D, a->D, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0], m->st);
   else
-    pack_rows_f32<float>(a->replay, a->m, a->D, a->D, static_cast<float*>(m->act[0]), m->ld[0], m->st);
+    pack_rows_f32<float>(a->replay, a->m, a->D, a->D, static_cast<float*>(m->act[0]), m->ld[0], m->st, m->act_lo(0));
   note_launch(1);
 }
 void upload_f32(moses_model* m, const double* src, long long n, float* dst) {
@@ -517,7 +531,8 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
   return guarded([&] {
     *out = nullptr;
     check_dims(dims, nd, false);
-    if (precision != MOSES_PREC_BF16 && precision != MOSES_PREC_TF32) fail(MOSES_ERR_INVALID_ARG, "precision");
+    if (precision != MOSES_PREC_BF16 && precision != MOSES_PREC_TF32 && precision != MOSES_PREC_FP32)
+      fail(MOSES_ERR_INVALID_ARG, "precision");
     for (int l = 1; l + 1 < nd; ++l)
       if (dims[l] % 8) fail(MOSES_ERR_INVALID_ARG, "hidden widths must be multiples of 8 (TMA 16-byte rows)");
     if (max_rows < 1) max_rows = 1;
@@ -530,6 +545,8 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     for (int l = 0; l <= m->L; ++l) m->off.push_back(level_off(m->dims, l));
     m->prec = precision;
     m->esz = precision == MOSES_PREC_BF16 ? 2 : 4;
+    m->split = precision == MOSES_PREC_FP32;
+    const int twin = m->split ? 2 : 1;  // FP32 mode: [hi | lo] halves of every GEMM operand buffer
     m->cap = round_up(max_rows, 128);
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st2, cudaStreamNonBlocking));
@@ -542,12 +559,12 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->xi = dalloc<float>(P);
     m->mask = dalloc<uint8_t>(P);
     if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(P);
-    else m->wtf = dalloc<float>(P);
+    else m->wtf = dalloc<float>(twin == 2 ? 2 * shadow_lo_offset(P) : P);
     MOSES_CUDA(cudaMemset(m->w, 0, P * 4));
     MOSES_CUDA(cudaMemset(m->mom, 0, P * 4));
     MOSES_CUDA(cudaMemset(m->g, 0, P * 4));
     if (m->wbf) MOSES_CUDA(cudaMemset(m->wbf, 0, P * 2));
-    if (m->wtf) MOSES_CUDA(cudaMemset(m->wtf, 0, P * 4));
+    if (m->wtf) MOSES_CUDA(cudaMemset(m->wtf, 0, 4 * (twin == 2 ? 2 * shadow_lo_offset(P) : P)));
     const int vec = 16 / m->esz;
     int maxw = 0;
     for (int l = 0; l < m->L; ++l) {
@@ -556,13 +573,13 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
       m->lddz.push_back(round_up(m->dims[l], vec));
       maxw = std::max(maxw, m->dims[l]);
       void* a = nullptr;
-      MOSES_CUDA(cudaMalloc(&a, m->cap * ldl * m->esz));
-      MOSES_CUDA(cudaMemset(a, 0, m->cap * ldl * m->esz));
+      MOSES_CUDA(cudaMalloc(&a, m->cap * ldl * m->esz * twin));
+      MOSES_CUDA(cudaMemset(a, 0, m->cap * ldl * m->esz * twin));
       m->act.push_back(a);
       void* d = nullptr;
       if (l > 0) {
-        MOSES_CUDA(cudaMalloc(&d, m->cap * m->lddz[l] * m->esz));
-        MOSES_CUDA(cudaMemset(d, 0, m->cap * m->lddz[l] * m->esz));
+        MOSES_CUDA(cudaMalloc(&d, m->cap * m->lddz[l] * m->esz * twin));
+        MOSES_CUDA(cudaMemset(d, 0, m->cap * m->lddz[l] * m->esz * twin));
       }
       m->dz.push_back(d);
       // ones column of every activation buffer (never overwritten by the epilogues)
@@ -612,7 +629,7 @@ MOSES_API int moses_model_upload(moses_model_t m, const double* params, const do
     upload_f32(m, params, count, m->w);
     if (momentum) upload_f32(m, momentum, count, m->mom);
     else MOSES_CUDA(cudaMemsetAsync(m->mom, 0, count * 4, m->st));
-    refresh_shadow(m->w, count, m->shadow(), m->st);
+    refresh_shadow(m->w, count, m->shadow_full(), m->st);
     note_launch(1);
     m->xi_valid = false;
     MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -636,7 +653,7 @@ MOSES_API int moses_model_copy(moses_model_t dst, moses_model_t src) {
     MOSES_CUDA(cudaStreamSynchronize(src->st));
     MOSES_CUDA(cudaMemcpyAsync(dst->w, src->w, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
     MOSES_CUDA(cudaMemcpyAsync(dst->mom, src->mom, src->P * 4, cudaMemcpyDeviceToDevice, dst->st));
-    refresh_shadow(dst->w, dst->P, dst->shadow(), dst->st);
+    refresh_shadow(dst->w, dst->P, dst->shadow_full(), dst->st);
     note_launch(1);
     MOSES_CUDA(cudaStreamSynchronize(dst->st));
   });
@@ -873,6 +890,7 @@ MOSES_API int moses_apply_update(moses_model_t m, double lr, double mu, const ui
     {
       ProfScope ps(P_UPDATE, m->st);
       sgd_update(m->w, m->mom, m->g, dm, m->P, float(lr), float(mu), use_momentum != 0, m->shadow(), m->st);
+      m->post_update();
     }
     note_launch(1);
     m->xi_valid = false;
@@ -895,6 +913,7 @@ MOSES_API int moses_adam_update(moses_model_t m, double lr, double b1, double b2
     const float c1 = float(1.0 - std::pow(b1, step)), c2 = float(1.0 - std::pow(b2, step));
     adam_update(m->w, m->m1, m->m2, m->g, dm, m->P, float(lr), float(b1), float(b2), float(eps), c1, c2, m->shadow(),
                 m->st);
+    m->post_update();
     note_launch(1);
     MOSES_CUDA(cudaStreamSynchronize(m->st));
   });
@@ -905,6 +924,7 @@ MOSES_API int moses_train_step(moses_model_t m, const double* x, const double* y
   return guarded([&] {
     gradients_host(m, x, y, n, D, nullptr, 0.0);
     sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+    m->post_update();
     note_launch(1);
     if (loss_out) {
       MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
@@ -920,6 +940,7 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
                                        int64_t n_batches, int64_t batch, double lr, double mu, int32_t with_update) {
   return guarded([&] {
     require_model(m);
+    if (m->split) fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
     check_rows(m, batch);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1) fail(MOSES_ERR_INVALID_ARG, "n_batches must be >= 1");
@@ -970,6 +991,7 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
                                               int64_t rows_pad, double lr, double mu, int32_t with_update) {
   return guarded([&] {
     require_model(m);
+    if (m->split) fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
     check_rows(m, rows_pad);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1 || batch_programs < 1) fail(MOSES_ERR_INVALID_ARG, "empty batch plan");
@@ -1078,6 +1100,7 @@ MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_
     gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
     ProfScope ps(P_UPDATE, m->st);
     sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+    m->post_update();
     note_launch(1);
     if (loss_out) {
       MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
@@ -1242,6 +1265,7 @@ MOSES_API int moses_transferable_step(moses_model_t m, double alpha) {
     require_model(m);
     if (!m->mask_valid) fail(MOSES_ERR_SHAPE_MISMATCH, "mask length != parameter count");
     lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), 1.f, true, false, m->shadow(), m->st);
+    m->post_update();
     note_launch(1);
     m->xi_valid = false;
     MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -1264,6 +1288,7 @@ MOSES_API int moses_variant_decay(moses_model_t m, double alpha, double lambda) 
     const float f = decay_factor(alpha, lambda, &noop);
     if (noop) return;
     lottery_apply(m->w, m->g, m->mask, m->P, 0.f, f, false, true, m->shadow(), m->st);
+    m->post_update();
     note_launch(1);
     m->xi_valid = false;
     MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -1283,12 +1308,14 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
     if (mode == MOSES_MODE_RATIO && keep >= m->P) {
       MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
       lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
+      m->post_update();
       note_launch(1);
     } else {
       if (!m->lot_ws) MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes()));
       ProfScope ps(P_SELECT, m->st);
       lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha), float(1.0 - rate), decay,
                          m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);
+      m->post_update();
       note_launch(mode == MOSES_MODE_RATIO ? 7 : 3);
     }
     m->xi_valid = false;

@@ -34,6 +34,7 @@ struct Operand {
   const void* ptr;
   long long ld;   // row stride in elements of the stored matrix
   bool mn_major;  // true: element (mn, k) at ptr[k*ld + mn]; false: at ptr[mn*ld + k]
+  const void* lo = nullptr;  // 3xTF32: low halves, same layout (nullptr: single operand)
 };
 struct GemmEpilogue;  // fwd decl (gemm.cuh GemmArgs is the device-side form)
 
@@ -56,6 +57,7 @@ struct GemmCall {
   long long ldm = 0;
   int bn = 0;  // 0 = auto
   int round_out = 1;  // fp32 outputs: round to tf32 (operand of the next kind::tf32 GEMM)
+  void* out_lo = nullptr;  // 3xTF32: low halves of the output
 };
 
 // ---------------------------------------------------------------- device-time profiler (capi.cu)

@@ -7,6 +7,7 @@
 #include "gemm.cuh"
 #include "gemm_persistent.cuh"
 #include "gemm_cluster.cuh"
+#include "gemm_split.cuh"
 
 namespace moses {
 // MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
@@ -219,6 +220,60 @@ void dispatch_persistent(const GemmCall& c, cudaStream_t s) {
   fail(MOSES_ERR_INVALID_ARG, "unsupported persistent GEMM combination");
 }
 
+// 3xTF32 (fp32 parity mode): gemm_split.cuh, 128 x 64 tiles
+template <bool AMN, bool BMN, int EPI>
+void launch_s(const GemmCall& c, cudaStream_t s) {
+  constexpr int BN = 64;
+  using Cfg = SCfg<BN>;
+  auto kern = umma_gemm_split<BN, AMN, BMN, EPI>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+  });
+  const CUtensorMap ta = operand_map(c.A, 4, c.M, c.K, Cfg::BM);
+  const CUtensorMap tb = operand_map(c.B, 4, c.N, c.K, BN);
+  const CUtensorMap tal = operand_map({c.A.lo, c.A.ld, c.A.mn_major}, 4, c.M, c.K, Cfg::BM);
+  const CUtensorMap tbl = operand_map({c.B.lo, c.B.ld, c.B.mn_major}, 4, c.N, c.K, BN);
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mask = c.mask;
+  a.ldm = c.ldm;
+  a.mn_layout = g_mn_layout[1];
+  a.mn_sbo = g_mn_sbo[1];
+  a.mn_kstep = g_mn_kstep[1];
+  a.round_out = c.round_out;
+  a.out_lo = c.out_lo;
+  kern<<<dim3(ceil_div(c.M, Cfg::BM), ceil_div(c.N, BN)), 192, Cfg::kSmemBytes, s>>>(ta, tb, tal, tbl, a);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+void dispatch_split(const GemmCall& c, cudaStream_t s) {
+  const bool am = c.A.mn_major, bm = c.B.mn_major;
+  switch (c.epi) {
+    case EpiKind::Fwd:
+      if (!am && bm) return launch_s<false, true, int(Epi::Fwd)>(c, s);
+      break;
+    case EpiKind::Dgrad:
+      if (!am && !bm) return launch_s<false, false, int(Epi::Dgrad)>(c, s);
+      break;
+    case EpiKind::StoreF32:
+      if (am && bm) return launch_s<true, true, int(Epi::StoreF32)>(c, s);
+      break;
+  }
+  fail(MOSES_ERR_INVALID_ARG, "unsupported 3xTF32 GEMM combination");
+}
+
 template <typename T, int BN>
 void dispatch_major(const GemmCall& c, cudaStream_t s) {
   const bool am = c.A.mn_major, bm = c.B.mn_major;
@@ -273,6 +328,11 @@ int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
       g_num_sms = n;
     sm_init = true;
+  }
+  if (c.A.lo != nullptr || c.B.lo != nullptr) {  // 3xTF32: both operands split, non-persistent kernel
+    if (elem != 4 || !c.A.lo || !c.B.lo) fail(MOSES_ERR_INVALID_ARG, "3xTF32 needs fp32 hi/lo operands");
+    dispatch_split(c, s);
+    return 64;
   }
   // Hidden layers (bf16, N = 512, K <= 512, A K-major): weight-resident 4-CTA cluster kernel.
   // Measured on B200: wins at training sizes (M ~ 2.3K statement rows: 18 m-tiles); at scoring sizes

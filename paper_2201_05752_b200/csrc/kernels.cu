@@ -46,26 +46,34 @@ int grid_for(long long n, int block, int per_sm = 8) {
 }
 
 // ---------------------------------------------------------------- data movement
+// 3xTF32 operands (fp32 parity mode): hi = rna_tf32(v) in dst, lo = rna_tf32(v - hi) in lo.
 template <typename T>
-__global__ void pack_rows_kernel(const double* __restrict__ src, long long n, int D, T* __restrict__ dst, long long ld) {
+__device__ __forceinline__ void store_operand(T* dst, float* lo, long long i, float v) {
+  const T h = from_f<T>(v);
+  dst[i] = h;
+  if (lo != nullptr) lo[i] = tf32_rna(v - to_f(h));
+}
+template <typename T>
+__global__ void pack_rows_kernel(const double* __restrict__ src, long long n, int D, T* __restrict__ dst, long long ld,
+                                 float* __restrict__ lo) {
   ptx::pdl_launch_dependents();
   const long long total = n * ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / ld;
     const int c = int(i - r * ld);
     const float v = c < D ? float(src[r * D + c]) : (c == D ? 1.f : 0.f);
-    dst[i] = from_f<T>(v);
+    store_operand(dst, lo, i, v);
   }
 }
 template <typename T>
 __global__ void pack_rows_f32_kernel(const float* __restrict__ src, long long n, int D, long long lds, T* __restrict__ dst,
-                                     long long ld) {
+                                     long long ld, float* __restrict__ lo) {
   const long long total = n * ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / ld;
     const int c = int(i - r * ld);
     const float v = c < D ? src[r * lds + c] : (c == D ? 1.f : 0.f);
-    dst[i] = from_f<T>(v);
+    store_operand(dst, lo, i, v);
   }
 }
 template <typename T>
@@ -363,7 +371,8 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
 template <typename T>
 __global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
                                      const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
-                                     long long ldh, long long R, int W, T* __restrict__ dz, long long ldz) {
+                                     long long ldh, long long R, int W, T* __restrict__ dz, long long ldz,
+                                     float* __restrict__ dz_lo) {
   ptx::pdl_launch_dependents();
   const long long total = R * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -371,7 +380,7 @@ __global__ void head_backward_kernel(const float* __restrict__ coefA, const floa
     const int j = int(i - r * W);
     float v = coefA[r] * wh[j];
     if (u != nullptr) v += coefB[r] * u[j];
-    dz[r * ldz + j] = from_f<T>(to_f(H[r * ldh + j]) > 0.f ? v : 0.f);
+    store_operand(dz, dz_lo, r * ldz + j, to_f(H[r * ldh + j]) > 0.f ? v : 0.f);
   }
 }
 
@@ -692,6 +701,12 @@ __global__ void shadow_kernel2(const float* w, long long n, void* sh) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     store_shadow<2>(sh, i, w[i]);
 }
+// kind 3 (3xTF32): hi at sh[i], lo at sh[shadow_lo_offset(n) + i]
+__global__ void shadow_kernel3(const float* w, long long n, float* sh) {
+  float* lo = sh + shadow_lo_offset(n);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    store_operand(sh, lo, i, w[i]);
+}
 
 __global__ void popcount_kernel(const uint8_t* __restrict__ mask, long long n, unsigned long long* out) {
   using Red = cub::BlockReduce<unsigned long long, kSelBlock>;
@@ -951,15 +966,15 @@ __global__ void synth_labels_kernel(unsigned long long seed, long long row0, lon
 
 // ====================================================================== host wrappers
 template <typename T>
-void pack_rows(const double* src, long long n, int D, T* dst, long long ld, cudaStream_t s) {
+void pack_rows(const double* src, long long n, int D, T* dst, long long ld, cudaStream_t s, float* lo) {
   if (n <= 0) return;
-  pack_rows_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, dst, ld);
+  pack_rows_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, dst, ld, lo);
   MOSES_CUDA(cudaGetLastError());
 }
 template <typename T>
-void pack_rows_f32(const float* src, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s) {
+void pack_rows_f32(const float* src, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s, float* lo) {
   if (n <= 0) return;
-  pack_rows_f32_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, lds, dst, ld);
+  pack_rows_f32_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, lds, dst, ld, lo);
   MOSES_CUDA(cudaGetLastError());
 }
 template <typename T>
@@ -987,7 +1002,8 @@ void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s) {
 void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s) {
   if (n <= 0 || sh.kind == 0) return;
   if (sh.kind == 1) shadow_kernel1<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
-  else shadow_kernel2<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
+  else if (sh.kind == 2) shadow_kernel2<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
+  else shadow_kernel3<<<grid_for(n, 256), 256, 0, s>>>(w, n, static_cast<float*>(sh.ptr));
   MOSES_CUDA(cudaGetLastError());
 }
 void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s) {
@@ -1066,9 +1082,9 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
 
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st) {
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, float* dz_lo) {
   if (R <= 0) return;
-  head_backward_kernel<T><<<grid_for(R * W, 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz, ldz);
+  head_backward_kernel<T><<<grid_for(R * W, 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz, ldz, dz_lo);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -1339,12 +1355,12 @@ void synth_labels(unsigned long long seed, long long row0, long long n, float* d
 }
 
 #define INST(T)                                                                                                   \
-  template void pack_rows<T>(const double*, long long, int, T*, long long, cudaStream_t);                         \
-  template void pack_rows_f32<T>(const float*, long long, int, long long, T*, long long, cudaStream_t);           \
+  template void pack_rows<T>(const double*, long long, int, T*, long long, cudaStream_t, float*);                      \
+  template void pack_rows_f32<T>(const float*, long long, int, long long, T*, long long, cudaStream_t, float*);           \
   template void set_ones_column<T>(T*, long long, int, long long, cudaStream_t);                                  \
   template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t);                       \
   template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
-                                 long long, int, T*, long long, cudaStream_t);                                    \
+                                 long long, int, T*, long long, cudaStream_t, float*);                                    \
   template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t,     \
                               const float*);                                                                      \
   template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \

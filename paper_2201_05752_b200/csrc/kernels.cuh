@@ -5,18 +5,22 @@
 namespace moses {
 
 // Operand shadow of the fp32 master parameters written by every update kernel:
-// kind 0 none, 1 bf16 (kind::f16 operand), 2 tf32-rounded fp32 (kind::tf32 operand).
+// kind 0 none, 1 bf16 (kind::f16 operand), 2 tf32-rounded fp32 (kind::tf32 operand),
+// 3 (refresh_shadow only) 3xTF32 hi/lo pair: hi at ptr[i], lo at ptr[shadow_lo_offset(n) + i].
 struct Shadow {
   void* ptr;
   int kind;
 };
+// low half of a kind-3 shadow starts 128-byte aligned (TMA operands need 16-byte alignment)
+__host__ __device__ constexpr long long shadow_lo_offset(long long n) { return (n + 31) / 32 * 32; }
 void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s);
 
 // ---- data movement
 template <typename T>
-void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s);
+void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s, float* lo = nullptr);
 template <typename T>
-void pack_rows_f32(const float* src_d, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s);
+void pack_rows_f32(const float* src_d, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s,
+                   float* lo = nullptr);
 template <typename T>
 void set_ones_column(T* act, long long rows, int col, long long ld, cudaStream_t s);
 template <typename T>
@@ -69,7 +73,7 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
 // dZ_last[r][j] = (coefA[r]*wh[j] + coefB[r]*u[j]) * [H[r][j] > 0]
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st);
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, float* dz_lo = nullptr);
 // g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
 template <typename T>
 void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,

@@ -34,7 +34,7 @@ ERROR_NAMES = [
 ]
 LIB_ERRORS = {100: "cuda-error", 101: "no-device", 102: "capacity", 103: "invalid-argument"}
 
-PREC_BF16, PREC_TF32 = 0, 1
+PREC_BF16, PREC_TF32, PREC_FP32 = 0, 1, 2  # FP32: 3xTF32 split operands
 THRESHOLD, RATIO = 1, 2
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
