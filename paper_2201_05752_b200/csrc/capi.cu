@@ -269,10 +269,45 @@ namespace moses {
 namespace {
 
 // ---------------------------------------------------------------- forward / backward composition
+// Fused hidden-layer chain (mlp_chain.cuh): bf16, every hidden width 512, input width <= 512.
+bool chain_ok(const moses_model* m) {
+  if (!g_chain || m->esz != 2 || m->L - 1 < 1 || m->L - 1 > 8 || m->dims[0] > 512) return false;
+  for (int l = 1; l < m->L; ++l)
+    if (m->dims[l] != 512) return false;
+  return true;
+}
+
 template <typename T>
 void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
   if (m->split && x0 != m->act[0])
     fail(MOSES_ERR_INVALID_ARG, "FP32 (3xTF32) handles take inputs through the host API only");
+  if (chain_ok(m) && R > 0) {
+    ChainCall cc;
+    cc.fwd = true;
+    cc.M = int(R);
+    cc.n_layers = m->L - 1;
+    cc.in = x0;
+    cc.ld_in = ldx0;
+    for (int l = 0; l + 1 < m->L; ++l) {
+      cc.K[l] = m->dims[l];
+      cc.w[l] = m->wop(l);
+      cc.bias[l] = m->bias(l);
+      cc.out[l] = (l + 2 == m->L && !keep_last) ? nullptr : m->act[l + 1];
+      cc.ldo[l] = m->ld[l + 1];
+    }
+    cc.head_w = m->head_w();
+    cc.head_u = head_u;
+    cc.head_part = m->head_part;
+    cc.head_part2 = head_u ? m->head_part2 : nullptr;
+    cc.head_ld = m->cap;
+    {
+      ProfScope ps(P_GEMM_FWD, m->st);
+      launch_chain(cc, m->st);
+    }
+    note_launch(1);
+    m->last_tiles = 4;
+    return;
+  }
   for (int l = 0; l + 1 < m->L; ++l) {
     GemmCall c{};
     c.M = int(R);
@@ -305,9 +340,14 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
   }
 }
 
+struct SgdFuse {  // momentum-SGD step fused into the grouped weight-gradient epilogue
+  float lr, mu;
+};
+
+// Returns true when `fuse` was applied (every parameter updated) inside the backward pass.
 template <typename T>
-void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u,
-                   const float* gb_override = nullptr) {
+bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u,
+                   const float* gb_override = nullptr, const SgdFuse* fuse = nullptr) {
   // Two streams: the data-gradient chain (head backward -> dgrad(L-2) -> ... -> dgrad(1)) runs on
   // st; every weight-gradient GEMM (and the head-gradient column reduction) runs on st2 as soon
   // as its dZ is ready. At batch 512 each GEMM fills only 16-40 of the 148 SMs, so the two
@@ -328,6 +368,90 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   }
   MOSES_CUDA(cudaEventRecord(ev[1 + (L - 1)], m->st));
   note_launch(2);
+  // dZ chain dz[L-2] .. dz[1] in one clustered kernel when the shape allows (mlp_chain.cuh)
+  const bool chain = sizeof(T) == 2 && chain_ok(m) && L - 2 >= 1;
+  if (chain) {
+    ChainCall cc;
+    cc.fwd = false;
+    cc.M = int(R);
+    cc.n_layers = L - 2;
+    cc.in = m->dz[L - 1];
+    cc.ld_in = m->lddz[L - 1];
+    for (int j = 0; j < L - 2; ++j) {
+      const int lev = L - 2 - j;
+      cc.K[j] = m->dims[lev + 1];
+      cc.w[j] = m->wop(lev);
+      cc.out[j] = m->dz[lev];
+      cc.ldo[j] = m->lddz[lev];
+      cc.mask[j] = m->act[lev];
+      cc.ldm[j] = m->ld[lev];
+    }
+    {
+      ProfScope ps(P_GEMM_DGRAD, m->st);
+      launch_chain(cc, m->st);
+    }
+    note_launch(1);
+    MOSES_CUDA(cudaEventRecord(ev[1 + 1], m->st));  // every dz[l], l <= L-2, is ready
+  }
+  // bf16: all weight-gradient GEMMs in one launch once every dZ exists (gemm_group.cuh)
+  const bool grouped = sizeof(T) == 2 && g_group && L - 1 <= 8;
+  if (grouped) {
+    for (int l = L - 2; l >= 1 && !chain; --l) {
+      GemmCall dg{};
+      dg.M = int(R);
+      dg.N = m->dims[l];
+      dg.K = m->dims[l + 1];
+      dg.A = {m->dz[l + 1], m->lddz[l + 1], false};
+      dg.B = {m->wop(l), m->dims[l + 1], false};
+      dg.epi = EpiKind::Dgrad;
+      dg.out = m->dz[l];
+      dg.ldo = m->lddz[l];
+      dg.mask = m->act[l];
+      dg.ldm = m->ld[l];
+      {
+        ProfScope ps(P_GEMM_DGRAD, m->st);
+        launch_gemm(m->esz, dg, m->st);
+      }
+      note_launch(1);
+    }
+    MOSES_CUDA(cudaEventRecord(ev[1], m->st));
+    MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1], 0));
+    WgradGroupCall wc;
+    wc.n = L - 1;
+    wc.K = int(R);
+    for (int l = 0; l + 1 < L; ++l) {
+      wc.a[l] = l == 0 ? x0 : m->act[l];
+      wc.lda[l] = l == 0 ? ldx0 : m->ld[l];
+      wc.b[l] = m->dz[l + 1];
+      wc.ldb[l] = m->lddz[l + 1];
+      wc.M[l] = m->dims[l] + 1;  // + the ones column -> bias gradient row
+      wc.N[l] = m->dims[l + 1];
+      wc.g[l] = m->g + m->off[l];
+      wc.w[l] = m->w + m->off[l];
+      wc.mom[l] = m->mom + m->off[l];
+      wc.shadow[l] = m->wbf + m->off[l];
+    }
+    if (fuse) {
+      wc.update = true;
+      wc.lr = fuse->lr;
+      wc.mu = fuse->mu;
+    }
+    {
+      ProfScope ps(P_GEMM_WGRAD, m->st2);
+      launch_wgrad_group(wc, m->st2);
+    }
+    note_launch(1);
+    if (fuse) {  // the head block (column_dot, same stream) gets the same update
+      const long long o = m->off[L - 1];
+      ProfScope ps(P_UPDATE, m->st2);
+      sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, m->P - o, fuse->lr, fuse->mu, true,
+                 Shadow{m->wbf + o, 1}, m->st2);
+      note_launch(1);
+    }
+    MOSES_CUDA(cudaEventRecord(ev[L + 1], m->st2));
+    MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 1], 0));
+    return fuse != nullptr;
+  }
   for (int l = L - 2; l >= 0; --l) {
     const void* a = l == 0 ? x0 : m->act[l];
     const long long lda = l == 0 ? ldx0 : m->ld[l];
@@ -340,13 +464,13 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     wg.epi = EpiKind::StoreF32;
     wg.out = m->g + m->off[l];
     wg.ldo = m->dims[l + 1];
-    MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (l + 1)], 0));
+    MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[(chain && l + 1 < L - 1) ? 2 : 1 + (l + 1)], 0));
     {
       ProfScope ps(P_GEMM_WGRAD, m->st2);
       launch_gemm(m->esz, wg, m->st2);
     }
     note_launch(1);
-    if (l > 0) {
+    if (l > 0 && !chain) {
       GemmCall dg{};
       dg.M = int(R);
       dg.N = m->dims[l];
@@ -369,6 +493,7 @@ void backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   }
   MOSES_CUDA(cudaEventRecord(ev[L + 1], m->st2));
   MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 1], 0));
+  return false;
 }
 
 // apply_update is synchronous for host callers (reference value semantics); the device-resident
@@ -440,8 +565,10 @@ struct Pool {
 
 // gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch;
 // pooled: rows [0, pool->rows) are statements of the n programs.
-void gradients_core(moses_model* m, const void* x0, long long ldx0, const float* y, long long n, moses_adversary* adv,
-                    double beta, const Pool* pool = nullptr) {
+// Returns true when `fuse` (momentum SGD) was applied inside the backward pass; the caller runs
+// the separate update otherwise.
+bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float* y, long long n, moses_adversary* adv,
+                    double beta, const Pool* pool = nullptr, const SgdFuse* fuse = nullptr) {
   const bool active = adv != nullptr && beta != 0.0 && n > 0 && pool == nullptr;
   const long long mrep = active ? adv->m : 0;
   const long long R = pool ? pool->rows : mrep + n;
@@ -449,28 +576,29 @@ void gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
     MOSES_CUDA(cudaMemsetAsync(m->g, 0, sizeof(float) * m->P, m->st));
     MOSES_CUDA(cudaMemsetAsync(m->dscal, 0, sizeof(double) * 2, m->st));
     m->xi_valid = false;
-    return;
+    return false;
   }
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
-  ProfScope ps(P_RANK, m->st);
-  rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), pool ? pool->seg_off : nullptr, y, n,
-                   {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->scores, m->st);
-  FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
-  if (pool) {
-    fo.seg_of_row = pool->seg_of_row;
-    fo.R_rows = R;
-    fo.gb = m->gbias;
+  {
+    ProfScope ps(P_RANK, m->st);
+    rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), pool ? pool->seg_off : nullptr, y, n,
+                     {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->scores, m->st);
+    FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
+    if (pool) {
+      fo.seg_of_row = pool->seg_of_row;
+      fo.R_rows = R;
+      fo.gb = m->gbias;
+    }
+    rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
+                  active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
+    note_launch(2);
   }
-  rank_finalize({m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, n, mrep,
-                active ? m->head_part2 : nullptr, m->last_tiles, m->cap, active ? adv->c : nullptr, beta, fo, m->st);
-  note_launch(2);
-  ps.~ProfScope();
-  ps.idx = -1;
   const float* gbo = pool ? m->gbias : nullptr;
-  if (m->esz == 2) backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, gbo);
-  else backward_rows<float>(m, x0, ldx0, R, u, gbo);
+  const bool fused = m->esz == 2 ? backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, gbo, fuse)
+                                 : backward_rows<float>(m, x0, ldx0, R, u, gbo, fuse);
   m->xi_valid = false;
+  return fused;
 }
 
 void check_rows(moses_model* m, long long R) {
@@ -953,8 +1081,11 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
     const long long row_bytes = ldx * m->esz;
     auto body = [&] {
       gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
-      gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
-      if (with_update) sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      const SgdFuse fz{float(lr), float(mu)};
+      const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0, nullptr,
+                                        with_update ? &fz : nullptr);
+      if (with_update && !fused)
+        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
       advance_counter(m->dcounter, m->st);
     };
     {  // eager warm-up without the update (configures kernels, validates shapes; params untouched)
@@ -1015,8 +1146,11 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
     try {
       gather();
-      gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool);
-      if (with_update) sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      const SgdFuse fz{float(lr), float(mu)};
+      const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool,
+                                        with_update ? &fz : nullptr);
+      if (with_update && !fused)
+        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
       advance_counter(m->dcounter, m->st);
     } catch (...) {
       cudaStreamEndCapture(m->st, &graph);
@@ -1097,11 +1231,13 @@ MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_
   return guarded([&] {
     require_model(m);
     check_rows(m, n);
-    gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
-    ProfScope ps(P_UPDATE, m->st);
-    sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-    m->post_update();
-    note_launch(1);
+    const SgdFuse fz{float(lr), float(mu)};
+    if (!gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0, nullptr, &fz)) {
+      ProfScope ps(P_UPDATE, m->st);
+      sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      m->post_update();
+      note_launch(1);
+    }
     if (loss_out) {
       MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
       MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -1719,6 +1855,46 @@ extern "C" MOSES_API int moses_debug_gemm(int elem, int M, int N, int K, const v
   });
 }
 
+// Timing harness for kernel tuning (tools/gemm_latency.py): launches the GEMM `iters` times
+// back to back on a private stream and reports the mean device time per launch.
+extern "C" MOSES_API int moses_debug_gemm_timed(int elem, int M, int N, int K, const void* A, long long lda, int a_mn,
+                                                const void* B, long long ldb, int b_mn, int epi, void* out,
+                                                long long ldo, const float* bias, int relu, int bn, const void* mask,
+                                                long long ldm, int iters, float* ms_out) {
+  return guarded([&] {
+    GemmCall c{};
+    c.M = M;
+    c.N = N;
+    c.K = K;
+    c.A = {A, lda, a_mn != 0};
+    c.B = {B, ldb, b_mn != 0};
+    c.epi = EpiKind(epi);
+    c.out = out;
+    c.ldo = ldo;
+    c.bias = bias;
+    c.relu = relu;
+    c.bn = bn;
+    c.mask = mask;
+    c.ldm = ldm;
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    MOSES_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    MOSES_CUDA(cudaEventCreate(&e0));
+    MOSES_CUDA(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) launch_gemm(elem, c, st);
+    MOSES_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) launch_gemm(elem, c, st);
+    MOSES_CUDA(cudaEventRecord(e1, st));
+    MOSES_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MOSES_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / float(iters);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
 namespace moses {
 extern int g_mn_swz[2], g_mn_layout[2], g_mn_sbo[2], g_mn_kstep[2];
 }
@@ -1740,6 +1916,14 @@ extern "C" MOSES_API int moses_debug_set_persistent(int on) {
 
 namespace moses {
 extern int g_cluster;
+}
+extern "C" MOSES_API int moses_debug_set_group(int on) {
+  moses::g_group = on;
+  return 0;
+}
+extern "C" MOSES_API int moses_debug_set_chain(int on) {
+  moses::g_chain = on;
+  return 0;
 }
 extern "C" MOSES_API int moses_debug_set_cluster(int on) {
   moses::g_cluster = on;

@@ -74,6 +74,49 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// Whole hidden-layer chain of 128-row blocks in one clustered kernel (mlp_chain.cuh; bf16,
+// hidden width 512). fwd: relu(A W + b) per layer with head partials at the last layer
+// (4 partial tiles); !fwd: dZ chain (dz W^T) * [act > 0].
+struct ChainCall {
+  bool fwd = true;
+  int M = 0, n_layers = 0;
+  const void* in = nullptr;  // layer-0 A operand [M][K0] bf16
+  long long ld_in = 0;
+  int K[8] = {};
+  const void* w[8] = {};     // fwd: [K][512]; dgrad: [512][512]
+  const float* bias[8] = {};
+  void* out[8] = {};
+  long long ldo[8] = {};
+  const void* mask[8] = {};
+  long long ldm[8] = {};
+  const float* head_w = nullptr;
+  const float* head_u = nullptr;
+  float* head_part = nullptr;
+  float* head_part2 = nullptr;
+  long long head_ld = 0;
+};
+void launch_chain(const ChainCall& c, cudaStream_t s);
+
+// Every level's weight-gradient GEMM in one launch (gemm_group.cuh; bf16), optionally with the
+// momentum-SGD update of the produced parameters fused into the epilogue.
+struct WgradGroupCall {
+  int n = 0, K = 0;
+  const void* a[8] = {};
+  long long lda[8] = {};
+  const void* b[8] = {};
+  long long ldb[8] = {};
+  int M[8] = {}, N[8] = {};
+  float* g[8] = {};
+  float* w[8] = {};
+  float* mom[8] = {};
+  void* shadow[8] = {};
+  float lr = 0.f, mu = 0.f;
+  bool update = false;
+};
+void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
+extern int g_group;
+extern int g_chain;  // fused chain enabled (moses_debug_set_chain)
+
 // elem = 2 (bf16, kind::f16) or 4 (fp32 operands, kind::tf32). Returns the N tile used.
 int launch_gemm(int elem, const GemmCall& c, cudaStream_t s);
 int gemm_pick_bn(int M, int N);

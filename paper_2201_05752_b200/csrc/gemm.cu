@@ -8,6 +8,8 @@
 #include "gemm_persistent.cuh"
 #include "gemm_cluster.cuh"
 #include "gemm_split.cuh"
+#include "mlp_chain.cuh"
+#include "gemm_group.cuh"
 
 namespace moses {
 // MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
@@ -200,6 +202,88 @@ void launch_c(const GemmCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a, tm, CCfg::stages_for(num_kb)));
 }
 
+template <bool FWD>
+void launch_chain_t(const ChainCall& c, cudaStream_t s) {
+  auto kern = mlp_chain_kernel<FWD>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainCfg::kSmemBytes));
+  });
+  ChainMaps maps;
+  ChainArgs a{};
+  a.M = c.M;
+  a.n_layers = c.n_layers;
+  maps.in = make_map(c.in, 2, c.K[0], c.M, c.ld_in, 64, 128);
+  for (int l = 0; l < c.n_layers; ++l) {
+    a.K[l] = c.K[l];
+    a.bias[l] = c.bias[l];
+    a.out[l] = static_cast<__nv_bfloat16*>(c.out[l]);
+    a.ldo[l] = c.ldo[l];
+    a.mask[l] = static_cast<const __nv_bfloat16*>(c.mask[l]);
+    a.ldm[l] = c.ldm[l];
+    maps.w[l] = FWD ? make_map(c.w[l], 2, ChainCfg::kWidth, c.K[l], ChainCfg::kWidth, 64, 64)
+                    : make_map(c.w[l], 2, ChainCfg::kWidth, ChainCfg::kWidth, ChainCfg::kWidth, 64, 128);
+    if (l + 1 < c.n_layers) maps.out[l] = make_map(c.out[l], 2, ChainCfg::kWidth, c.M, c.ldo[l], 64, 128);
+  }
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ChainCfg::kCluster * ceil_div(c.M, ChainCfg::BM));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = ChainCfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+}
+
+template <bool UPDATE>
+void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
+  auto kern = wgrad_group_kernel<UPDATE>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GroupCfg::kSmemBytes));
+  });
+  GroupMaps maps;
+  GroupArgs a{};
+  a.n = c.n;
+  a.K = c.K;
+  int tiles = 0;
+  for (int l = 0; l < c.n; ++l) {
+    maps.a[l] = make_map(c.a[l], 2, c.M[l], c.K, c.lda[l], 64, 64);
+    maps.b[l] = make_map(c.b[l], 2, c.N[l], c.K, c.ldb[l], 64, 64);
+    a.tile_begin[l] = tiles;
+    a.tiles_n[l] = ceil_div(c.N[l], GroupCfg::BN);
+    a.M[l] = c.M[l];
+    a.N[l] = c.N[l];
+    a.g[l] = c.g[l];
+    a.w[l] = c.w[l];
+    a.mom[l] = c.mom[l];
+    a.shadow[l] = static_cast<__nv_bfloat16*>(c.shadow[l]);
+    tiles += ceil_div(c.M[l], GroupCfg::BM) * a.tiles_n[l];
+  }
+  a.tile_begin[c.n] = tiles;
+  a.lr = c.lr;
+  a.mu = c.mu;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = GroupCfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+}
+
 template <typename T, int BN>
 void dispatch_persistent(const GemmCall& c, cudaStream_t s) {
   const bool am = c.A.mn_major, bm = c.B.mn_major;
@@ -318,6 +402,21 @@ int gemm_pick_bn(int M, int N) {
 int g_num_sms = 148;
 int g_persistent = 1;  // persistent kernel for problems with more tiles than SMs
 int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden layers
+
+int g_chain = 1;
+int g_group = 1;
+void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
+  if (c.K <= 0 || c.n <= 0) return;
+  if (c.n > kGroupMax) fail(MOSES_ERR_INVALID_ARG, "too many levels for the grouped wgrad");
+  if (c.update) launch_group_t<true>(c, s);
+  else launch_group_t<false>(c, s);
+}
+void launch_chain(const ChainCall& c, cudaStream_t s) {
+  if (c.M <= 0) return;
+  if (c.n_layers < 1 || c.n_layers > kChainMaxLayers) fail(MOSES_ERR_INVALID_ARG, "chain depth");
+  if (c.fwd) launch_chain_t<true>(c, s);
+  else launch_chain_t<false>(c, s);
+}
 
 int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
   if (c.M <= 0 || c.N <= 0) return 0;
