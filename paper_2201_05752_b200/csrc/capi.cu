@@ -1917,6 +1917,14 @@ extern "C" MOSES_API int moses_debug_set_persistent(int on) {
 namespace moses {
 extern int g_cluster;
 }
+namespace moses {
+extern unsigned long long* g_chain_trace;
+}
+// device buffer of 4*8*8 u64 that receives chain-kernel phase timestamps (nullptr: off)
+extern "C" MOSES_API int moses_debug_set_chain_trace(void* dev_buf) {
+  moses::g_chain_trace = static_cast<unsigned long long*>(dev_buf);
+  return 0;
+}
 extern "C" MOSES_API int moses_debug_set_group(int on) {
   moses::g_group = on;
   return 0;

@@ -94,6 +94,7 @@ struct ChainCall {
   float* head_part = nullptr;
   float* head_part2 = nullptr;
   long long head_ld = 0;
+  unsigned long long* trace = nullptr;
 };
 void launch_chain(const ChainCall& c, cudaStream_t s);
 

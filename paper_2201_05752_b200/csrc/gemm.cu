@@ -23,6 +23,7 @@ int g_mn_sbo[2] = {1024, 512};
 int g_mn_kstep[2] = {16 * 128, 8 * 128};
 extern int g_num_sms;
 extern int g_cluster;
+extern unsigned long long* g_chain_trace;
 namespace {
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -223,13 +224,14 @@ void launch_chain_t(const ChainCall& c, cudaStream_t s) {
     a.ldm[l] = c.ldm[l];
     maps.w[l] = FWD ? make_map(c.w[l], 2, ChainCfg::kWidth, c.K[l], ChainCfg::kWidth, 64, 64)
                     : make_map(c.w[l], 2, ChainCfg::kWidth, ChainCfg::kWidth, ChainCfg::kWidth, 64, 128);
-    if (l + 1 < c.n_layers) maps.out[l] = make_map(c.out[l], 2, ChainCfg::kWidth, c.M, c.ldo[l], 64, 128);
+    if (c.out[l] != nullptr) maps.out[l] = make_map(c.out[l], 2, ChainCfg::kWidth, c.M, c.ldo[l], 64, 128);
   }
   a.head_w = c.head_w;
   a.head_u = c.head_u;
   a.head_part = c.head_part;
   a.head_part2 = c.head_part2;
   a.head_ld = c.head_ld;
+  a.trace = c.trace ? c.trace : g_chain_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ChainCfg::kCluster * ceil_div(c.M, ChainCfg::BM));
   cfg.blockDim = dim3(192);
@@ -404,6 +406,7 @@ int g_persistent = 1;  // persistent kernel for problems with more tiles than SM
 int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden layers
 
 int g_chain = 1;
+unsigned long long* g_chain_trace = nullptr;
 int g_group = 1;
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
   if (c.K <= 0 || c.n <= 0) return;

@@ -9,10 +9,11 @@
 //   CTA q of the cluster computes output columns [128q, 128q+128) of every layer;
 //   the layer's full 128 x 512 bf16 activation tile (the next layer's A operand, 8 SW128
 //   K-blocks = 128 KB) lives in shared memory of every CTA;
-//   after a layer, CTA q stores its 128 x 128 slice to global (it is needed by the backward
-//   pass anyway), fences it for the async proxy and TMA-MULTICASTS it back from L2 into the
-//   activation tile of all 4 CTAs (2 K-blocks) — the exchange rides the L2->SM fabric instead
-//   of DSMEM's ~20 B/clk ports;
+//   after a layer, CTA q's epilogue writes its 128 x 128 slice straight into its OWN activation
+//   tile (swizzled st.shared; its MMAs of the layer are complete); the producer TMA-stores the
+//   two K-blocks to global (coalesced; the backward pass needs them anyway) and, once the store
+//   has landed, TMA-MULTICASTS them from L2 into the 3 peer tiles. (Pushing the 96 KB per CTA
+//   through DSMEM instead is bound by its ~18 B/clk ports: measured 2.8 us vs 1.3 us per layer.)
 //   weights (16 KB per K-block) stream through a 4-stage TMA ring that prefetches the next
 //   layer while the exchange runs.
 //
@@ -38,7 +39,7 @@ constexpr int kChainMaxLayers = 8;
 struct ChainMaps {
   CUtensorMap in;                        // chain input [M][K0] (x0 or dz_last), box {64, 128}
   CUtensorMap w[kChainMaxLayers];        // FWD: [K][512] box {64, 64}; DGRAD: [512 n][512 k] box {64, 128}
-  CUtensorMap out[kChainMaxLayers];      // outputs [M][512] box {64, 128} (multicast reload)
+  CUtensorMap out[kChainMaxLayers];      // outputs [M][512] box {64, 128}: TMA store + multicast reload
 };
 
 struct ChainArgs {
@@ -55,6 +56,7 @@ struct ChainArgs {
   float* head_part;
   float* head_part2;
   long long head_ld;
+  unsigned long long* trace;  // optional phase timestamps of cluster 0 (tools/chain_trace.py)
 };
 
 struct ChainCfg {
@@ -67,12 +69,46 @@ struct ChainCfg {
 };
 
 namespace chain_detail {
-__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
+// relaxed: the barrier only orders tensor-core reads (signalled through mbarriers) against the
+// peers' later bulk copies; a .release arrive would emit a GPU-scope MEMBAR behind the epilogue's
+// global stores.
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory"); }
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// async bulk copy own smem -> a peer CTA's smem, completing on the peer's mbarrier
+__device__ __forceinline__ void bulk_to_peer(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t mbar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src), "r"(bytes), "r"(mbar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(ptx::smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots: [q][layer][event]; events: 0 mma start, 1 mma issued, 2 acc seen, 3 stores fenced,
+// 4 cluster wait passed (producer), 5 multicast issued, 6 kernel start, 7 kernel end
+#define CHAIN_TRACE(ev, l)                                                                             \
+  do {                                                                                                 \
+    if (args.trace != nullptr && blockIdx.x < 4)                                                       \
+      args.trace[(q * kChainMaxLayers + (l)) * 8 + (ev)] = chain_detail::clk();                        \
+  } while (0)
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 }  // namespace chain_detail
 
@@ -93,7 +129,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
   uint64_t* wempty = wfull + S;
   uint64_t* act_full = wempty + S;
   uint64_t* acc_full = act_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* slice_free = acc_full + 1;  // this CTA's outgoing bulk copies finished reading its slice
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slice_free + 1);
   float* s_bias = reinterpret_cast<float*>(sW + S * C::kWBytes + 256);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
@@ -108,10 +145,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
     }
     ptx::mbar_init(act_full, 1);
     ptx::mbar_init(acc_full, 1);
+    ptx::mbar_init(slice_free, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc<BN>(tmem_slot);
   ptx::pdl_wait();  // every global read below may depend on the previous kernel
+  if (threadIdx.x == 0) CHAIN_TRACE(6, 0);
   if constexpr (FWD) {
     for (int i = threadIdx.x; i < L * BN; i += blockDim.x) {
       const int l = i / BN, j = i - l * BN;
@@ -161,12 +200,33 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
           for (int kb = 0; kb < issued_next; ++kb) load_w(l + 1, kb);
         }
         issued_next = __shfl_sync(0xffffffffu, issued_next, 0);
-        cl_wait();       // every CTA's MMAs of layer l are done: activation tiles are free
-        bar_sync(1, 160);  // this CTA's slice of out[l] is in global memory and fenced
+        bar_sync(1, 160);  // this CTA's slice is in its own activation tile and fenced
         if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(act_full, (C::kWidth / BK) * C::kTile);
-          ptx::tma_load_2d_mc(sAct + (2 * q) * C::kTile, &maps.out[l], act_full, n0, m0, kAll);
-          ptx::tma_load_2d_mc(sAct + (2 * q + 1) * C::kTile, &maps.out[l], act_full, n0 + 64, m0, kAll);
+          CHAIN_TRACE(5, l);
+          tma_store_2d(&maps.out[l], sAct + (2 * q) * C::kTile, n0, m0);
+          tma_store_2d(&maps.out[l], sAct + (2 * q + 1) * C::kTile, n0 + 64, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // slice is in global (L2)
+          ptx::mbar_arrive(slice_free);
+        }
+        __syncwarp();
+        cl_wait();  // every CTA's MMAs of layer l are done: activation tiles are free
+        if (lane == 0) {
+          CHAIN_TRACE(4, l);
+          constexpr uint32_t kSlice = 2 * C::kTile;
+          const uint16_t peers = uint16_t(kAll & ~(1u << q));
+          ptx::mbar_arrive_expect_tx(act_full, (C::kCluster - 1) * kSlice);  // the 3 peer slices
+          ptx::tma_load_2d_mc(sAct + (2 * q) * C::kTile, &maps.out[l], act_full, n0, m0, peers);
+          ptx::tma_load_2d_mc(sAct + (2 * q + 1) * C::kTile, &maps.out[l], act_full, n0 + 64, m0, peers);
+        }
+        __syncwarp();
+      } else if (args.out[l] != nullptr) {  // last layer: coalesced TMA store of the output slice
+        bar_sync(1, 160);
+        if (lane == 0) {
+          tma_store_2d(&maps.out[l], sAct + (2 * q) * C::kTile, n0, m0);
+          tma_store_2d(&maps.out[l], sAct + (2 * q + 1) * C::kTile, n0 + 64, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
         __syncwarp();
       }
@@ -179,6 +239,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       if (lane == 0) {
         ptx::mbar_wait(act_full, uint32_t(l) & 1u);
         ptx::tc_fence_after();
+        CHAIN_TRACE(0, l);
         const int nkb = (args.K[l] + BK - 1) / BK;
         const uint32_t a0 = ptx::smem_u32(sAct), w0 = ptx::smem_u32(sW);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -196,6 +257,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit(acc_full);
+        CHAIN_TRACE(1, l);
       }
       __syncwarp();
       if (l + 1 < L) {
@@ -224,10 +286,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       load_mask(0);
       ptx::mbar_wait(acc_full, uint32_t(l) & 1u);
       ptx::tc_fence_after();
+      if (threadIdx.x == 0) CHAIN_TRACE(2, l);
       if (!last) cl_arrive();
+      const bool store = !last || args.out[l] != nullptr;  // slice goes through the own tile
+      if (store && l >= 1) ptx::mbar_wait(slice_free, uint32_t(l - 1) & 1u);
       float hp = 0.f, hp2 = 0.f;
-      __nv_bfloat16* const out_l = args.out[l];
-      __nv_bfloat16* orow = out_l + (long long)m * args.ldo[l] + n0;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -256,7 +319,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
           for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(mv[j]) > 0.f ? v[j] : 0.f;
           if (c + 1 < BN / 32) load_mask(c + 1);
         }
-        if (row_ok && out_l != nullptr) {
+        if (store) {
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
             uint4 pk;
@@ -268,7 +331,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
             pk.y = *reinterpret_cast<uint32_t*>(&p1);
             pk.z = *reinterpret_cast<uint32_t*>(&p2);
             pk.w = *reinterpret_cast<uint32_t*>(&p3);
-            *reinterpret_cast<uint4*>(orow + c * 32 + j) = pk;
+            // own activation tile (next layer's A operand / TMA-store source): SW128 K-major,
+            // 16-byte chunk (col%64)/8 ^ (row%8)
+            const int col = n0 + c * 32 + j;
+            const int chunk = ((col & 63) >> 3) ^ (row & 7);
+            *reinterpret_cast<uint4*>(sAct + (col >> 6) * C::kTile + row * 128 + chunk * 16) = pk;
           }
         }
       }
@@ -276,13 +343,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
         if (args.head_part != nullptr) args.head_part[(long long)q * args.head_ld + m] = hp;
         if (args.head_part2 != nullptr) args.head_part2[(long long)q * args.head_ld + m] = hp2;
       }
-      if (!last) {
+      if (store) {
         ptx::tc_fence_before();
-        fence_proxy_async_global();  // generic-proxy stores -> the producer's TMA (async proxy) reload
+        fence_proxy_async_smem();  // generic st.shared -> async-proxy readers (TMA store, tensor core)
+        if (threadIdx.x == 0) CHAIN_TRACE(3, l);
         bar_arrive(1, 160);
-        cl_wait();
       }
+      if (!last) cl_wait();
     }
+    if (threadIdx.x == 0) CHAIN_TRACE(7, 0);
     ptx::pdl_launch_dependents();
   }
 

@@ -1,0 +1,54 @@
+"""Phase timeline of the fused chain kernels (cluster 0), from %globaltimer stamps."""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2201_05752_b200 import moseslab as ml
+
+L = ml.lib()
+L.moses_debug_set_chain_trace.argtypes = [C.c_void_p]
+dims = [164, 512, 512, 512, 512, 1]
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 2560
+dm = ml.DeviceModel(ml.init_random(dims, 1, strict=False), ml.PREC_BF16, R)
+ld = dm.packed_ld
+X = torch.zeros((R, ld), dtype=torch.bfloat16, device="cuda")
+X[:, :164] = torch.rand(R, 164, device="cuda").to(torch.bfloat16)
+X[:, 164] = 1
+Y = torch.rand(R, device="cuda") + 0.1
+S = torch.empty(R, device="cuda")
+tr = torch.zeros(4 * 8 * 8, dtype=torch.int64, device="cuda")
+EV = ["mma_start", "mma_issued", "acc_seen", "stores_fenced", "cl_wait_done", "mc_issued", "k_start", "k_end"]
+
+
+def show(title):
+    t = tr.cpu().numpy().reshape(4, 8, 8).astype(np.int64)
+    t0 = t[:, 0, 6][t[:, 0, 6] > 0].min()
+    print(f"--- {title} (us from kernel start of CTA 0..3)")
+    for q in range(4):
+        print(f"  CTA{q} start {(t[q,0,6]-t0)/1e3:.2f} end {(t[q,0,7]-t0)/1e3:.2f}")
+    for l in range(8):
+        if t[0, l, 0] == 0:
+            continue
+        row = []
+        for e in range(6):
+            v = t[0, l, e]
+            row.append(f"{EV[e]} {(v - t0) / 1e3:6.2f}" if v > 0 else f"{EV[e]}   -   ")
+        print(f"  L{l}: " + " | ".join(row))
+
+
+for _ in range(3):
+    ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, R, S.data_ptr()))
+torch.cuda.synchronize()
+tr.zero_()
+L.moses_debug_set_chain_trace(tr.data_ptr())
+ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, R, S.data_ptr()))
+torch.cuda.synchronize()
+show("forward chain")
+tr.zero_()
+ml._ck(L.moses_gradients_device(dm.h, X.data_ptr(), ld, Y.data_ptr(), R, None))
+torch.cuda.synchronize()
+show("dZ chain")
+L.moses_debug_set_chain_trace(None)
