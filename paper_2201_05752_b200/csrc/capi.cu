@@ -202,6 +202,7 @@ struct moses_model {
   void* lot_ws = nullptr;          // fused lottery-step workspace (lottery.cu)
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
   int* seg_rows = nullptr;         // pooled: program of each statement row (cap)
+  unsigned int* rank_ticket = nullptr;  // rank_step last-CTA ticket (self re-arming)
   // parameters
   float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
   float *m1 = nullptr, *m2 = nullptr;
@@ -259,6 +260,7 @@ struct moses_model {
     dfree(lot_ws);
     dfree(seg_off);
     dfree(seg_rows);
+    dfree(rank_ticket);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
@@ -580,7 +582,23 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   }
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
-  {
+  if (!active && g_rank_fused) {
+    if (!m->rank_ticket) {
+      m->rank_ticket = dalloc<unsigned int>(1);
+      MOSES_CUDA(cudaMemsetAsync(m->rank_ticket, 0, sizeof(unsigned int), m->st));
+    }
+  }
+  bool ranked = false;
+  if (!active && g_rank_fused && m->rank_ticket) {
+    ProfScope ps(P_RANK, m->st);
+    FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
+    if (pool) fo.gb = m->gbias;
+    ranked = rank_step(m->head_part, m->last_tiles, m->cap, m->head_b(), pool ? pool->seg_off : nullptr, y, n,
+                       {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->rank_ticket,
+                       m->scores, pool ? pool->seg_of_row : nullptr, R, fo, m->st);
+    if (ranked) note_launch(1);
+  }
+  if (!ranked) {
     ProfScope ps(P_RANK, m->st);
     rank_pairs_fused(m->head_part + mrep, m->last_tiles, m->cap, m->head_b(), pool ? pool->seg_off : nullptr, y, n,
                      {m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n)}, m->scores, m->st);
@@ -1919,6 +1937,14 @@ extern int g_cluster;
 }
 namespace moses {
 extern unsigned long long* g_chain_trace;
+}
+namespace moses { void rank_trace_read(unsigned long long* out); }
+extern "C" MOSES_API int moses_debug_rank_trace(unsigned long long* out16) {
+  return guarded([&] { moses::rank_trace_read(out16); });
+}
+extern "C" MOSES_API int moses_debug_set_rank_fused(int on) {
+  moses::g_rank_fused = on;
+  return 0;
 }
 // device buffer of 4*8*8 u64 that receives chain-kernel phase timestamps (nullptr: off)
 extern "C" MOSES_API int moses_debug_set_chain_trace(void* dev_buf) {

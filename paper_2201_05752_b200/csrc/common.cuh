@@ -116,6 +116,7 @@ struct WgradGroupCall {
 };
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
 extern int g_group;
+extern int g_rank_fused;  // rank_step (one launch) instead of rank_pairs + rank_finalize
 extern int g_chain;  // fused chain enabled (moses_debug_set_chain)
 
 // elem = 2 (bf16, kind::f16) or 4 (fp32 operands, kind::tf32). Returns the N tile used.

@@ -408,6 +408,7 @@ int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden
 int g_chain = 1;
 unsigned long long* g_chain_trace = nullptr;
 int g_group = 1;
+int g_rank_fused = 1;
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
   if (c.K <= 0 || c.n <= 0) return;
   if (c.n > kGroupMax) fail(MOSES_ERR_INVALID_ARG, "too many levels for the grouped wgrad");

@@ -368,6 +368,223 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
   }
 }
 
+// ---------------------------------------------------------------- fused ranking step
+// rank_pairs + rank_finalize in ONE launch (no adversary): one cluster of 16 CTAs x 512 threads.
+// Each CTA scores its n/16 programs (per-row fixed-order tile sums of the forward's head
+// partials, then per-program segment sums — score_of()'s arithmetic), all-gathers the scores
+// through DSMEM, and evaluates the pairs of its n/8 programs with rank_pairs_kernel's (row, 32-column split) float
+// partials, reduced per row in split order (double) — the same per-row values as the two-kernel
+// path. Pair counts, loss and head-bias partials are all-gathered through DSMEM, so every CTA
+// knows 1/pairs and writes the backward coefficients of its programs' statement rows itself;
+// CTA 0 sums the loss / bias partials in CTA order. Deterministic.
+__device__ unsigned long long g_rank_trace[16];
+__device__ __forceinline__ void rank_stamp(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_rank_trace[k] = v;
+  }
+}
+constexpr int kRankCluster = 16;  // non-portable cluster size (B200 supports 16)
+constexpr int kRankThreads = 512;
+constexpr int kRankMaxItems = 4096;  // (rows per CTA) x (32-column splits)
+constexpr int kRankMaxRows = 256;    // programs per CTA
+struct RankRed {
+  long long pairs;
+  double loss, gb;
+};
+__global__ void __launch_bounds__(kRankThreads)
+    rank_cluster_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hbp,
+                        const long long* __restrict__ seg, const float* __restrict__ y, long long n, int nsplit,
+                        int rows_per_cta, float* __restrict__ s_out, long long R, double* loss_out,
+                        long long* pairs_out, float* __restrict__ coefA, float* __restrict__ coefB, float* gb_out) {
+  extern __shared__ float rs_smem[];
+  float* ss = rs_smem;      // [n] scores (all-gathered through DSMEM)
+  float* sy = ss + n;       // [n] labels
+  float* pg = sy + n;       // [items] per-(split, row) partials
+  float* pl = pg + kRankMaxItems;
+  int* pp = reinterpret_cast<int*>(pl + kRankMaxItems);
+  float* srow = reinterpret_cast<float*>(pp + kRankMaxItems);  // pooled: this CTA's statement head dots
+  __shared__ double row_g[kRankMaxRows];
+  __shared__ RankRed red[kRankCluster];  // all-gathered per-CTA totals
+  __shared__ double wl[32], wg[32];
+  __shared__ long long wp[32];
+  __shared__ long long sseg[kRankMaxRows + 1];
+  const int t = threadIdx.x;
+  rank_stamp(0);
+  const uint32_t q = ptx::cluster_ctarank();
+  const float hb = hbp[0];
+  const long long p0 = min(n, (long long)q * rows_per_cta);
+  const long long p1 = min(n, p0 + rows_per_cta);
+  for (long long p = t; p < n; p += blockDim.x) sy[p] = y[p];
+  // scores of THIS CTA's programs (fixed tile order per statement row, then the segment sum)
+  if (seg != nullptr) {
+    for (long long k = t; k <= p1 - p0; k += blockDim.x) sseg[k] = seg[p0 + k];
+    __syncthreads();
+    const long long r0 = sseg[0], r1 = sseg[p1 - p0];
+    for (long long r = r0 + t; r < r1; r += blockDim.x) {
+      float v[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) v[tt] = tt < ntiles ? __ldg(part + tt * ld + r) : 0.f;
+      float a = 0.f;
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt)
+        if (tt < ntiles) a += v[tt];
+      for (int tt = 8; tt < ntiles; ++tt) a += __ldg(part + tt * ld + r);
+      srow[r - r0] = a;
+    }
+    __syncthreads();
+    for (long long p = p0 + t; p < p1; p += blockDim.x) {
+      float acc = 0.f;
+      for (long long i = sseg[p - p0]; i < sseg[p - p0 + 1]; ++i) acc += srow[i - r0];
+      ss[p] = acc + hb;
+    }
+  } else {
+    for (long long p = p0 + t; p < p1; p += blockDim.x) {
+      float a = 0.f;
+      for (int tt = 0; tt < ntiles; ++tt) a += __ldg(part + tt * ld + p);
+      ss[p] = a + hb;
+    }
+  }
+  __syncthreads();
+  rank_stamp(1);
+  // all-gather: every CTA's scores into every peer's ss[] (same offsets)
+  for (long long k = t; k < (p1 - p0) * kRankCluster; k += blockDim.x) {
+    const long long p = p0 + k / kRankCluster;
+    const uint32_t dst = uint32_t(k % kRankCluster);
+    if (dst == q) continue;
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(ptx::smem_u32(ss + p)), "r"(dst));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(ss[p]) : "memory");
+  }
+  ptx::cluster_sync();
+  rank_stamp(2);
+  // pairs of this CTA's programs: item = (split, local row) — a warp shares one split, so the
+  // column reads are shared-memory broadcasts (row-major items put 16 splits 32 floats apart:
+  // 16-way bank conflicts, measured 17 us for this phase)
+  const int items = rows_per_cta * nsplit;
+  for (int it = t; it < items; it += blockDim.x) {
+    const int sp = it / rows_per_cta, lr = it - sp * rows_per_cta;
+    const long long i = p0 + lr;
+    float gs = 0.f, loss = 0.f;
+    int pairs = 0;
+    if (i < n) {
+      const float si = ss[i], yi = sy[i];
+      const long long j0 = (long long)sp * kRankChunk;
+      const int cnt = int(min((long long)kRankChunk, n - j0));
+      // branch-free pair terms: w = +1 (i is the hi row), -1 (lo), 0 (tie). gs accumulates the
+      // same values in the same order as rank_pairs_kernel (+-0 for ties); the softplus uses
+      // log1p(e) = -log(1/(1+e)) on the reciprocal already at hand (MUFU lg2).
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const float yj = sy[j0 + k];
+        const float w = float(yi > yj) - float(yi < yj);
+        const float d = w * (si - ss[j0 + k]);
+        const float e = __expf(-fabsf(d));
+        const float iv = __frcp_rn(1.f + e);
+        const float sig_neg = d >= 0.f ? e * iv : iv;
+        gs = w != 0.f ? gs - w * sig_neg : gs;
+        const bool hi = w > 0.f;
+        loss += hi ? fmaxf(-d, 0.f) - 0.69314718f * __log2f(iv) : 0.f;
+        pairs += hi;
+      }
+    }
+    pg[it] = gs;
+    pl[it] = loss;
+    pp[it] = pairs;
+  }
+  __syncthreads();
+  rank_stamp(3);
+  // per-row reduction in split order; CTA totals (row order)
+  double l_t = 0.0, g_t = 0.0;
+  long long c_t = 0;
+  for (int lr = t; lr < rows_per_cta; lr += blockDim.x) {
+    double g = 0.0, l = 0.0;
+    long long c = 0;
+    if (p0 + lr < n) {
+      for (int k = 0; k < nsplit; ++k) {
+        g += pg[k * rows_per_cta + lr];
+        l += pl[k * rows_per_cta + lr];
+        c += pp[k * rows_per_cta + lr];
+      }
+      if (s_out != nullptr) s_out[p0 + lr] = ss[p0 + lr];
+    }
+    row_g[lr] = g;
+    l_t += l;  // a thread's rows are visited in increasing order; warp/CTA order below is fixed
+    g_t += g;
+    c_t += c;
+  }
+  // fixed-order CTA reduction: lanes (shuffle tree), then warps in order
+  for (int o = 16; o > 0; o >>= 1) {
+    l_t += __shfl_down_sync(0xffffffffu, l_t, o);
+    g_t += __shfl_down_sync(0xffffffffu, g_t, o);
+    c_t += __shfl_down_sync(0xffffffffu, c_t, o);
+  }
+  if ((t & 31) == 0) {
+    wl[t >> 5] = l_t;
+    wg[t >> 5] = g_t;
+    wp[t >> 5] = c_t;
+  }
+  __syncthreads();
+  if (t == 0) {
+    RankRed mine{0, 0.0, 0.0};
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+      mine.loss += wl[w];
+      mine.gb += wg[w];
+      mine.pairs += wp[w];
+    }
+    // all-gather the CTA totals into every CTA's red[q]
+    const uint32_t local = ptx::smem_u32(&red[q]);
+    for (uint32_t dst = 0; dst < kRankCluster; ++dst) {
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(dst));
+      asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(mine.pairs) : "memory");
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra + 8), "d"(mine.loss) : "memory");
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra + 16), "d"(mine.gb) : "memory");
+    }
+  }
+  rank_stamp(4);
+  ptx::cluster_sync();
+  rank_stamp(5);
+  long long P = 0;
+  double L = 0.0, G = 0.0;
+  for (int b = 0; b < kRankCluster; ++b) {  // CTA order
+    P += red[b].pairs;
+    L += red[b].loss;
+    G += red[b].gb;
+  }
+  const double inv = P > 0 ? 1.0 / double(P) : 0.0;
+  if (seg != nullptr) {
+    const long long r0 = sseg[0], r1 = sseg[p1 - p0];
+    for (long long r = r0 + t; r < r1; r += blockDim.x) {
+      int lo = 0, hi = int(p1 - p0) - 1;  // program of row r: last k with sseg[k] <= r
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sseg[mid] <= r) lo = mid;
+        else hi = mid - 1;
+      }
+      coefA[r] = P > 0 ? float(row_g[lo] * inv) : 0.f;
+      coefB[r] = 0.f;
+    }
+    if (q == kRankCluster - 1)
+      for (long long r = seg[n] + t; r < R; r += blockDim.x) {
+        coefA[r] = 0.f;
+        coefB[r] = 0.f;
+      }
+  } else {
+    for (long long r = p0 + t; r < p1; r += blockDim.x) {
+      coefA[r] = P > 0 ? float(row_g[r - p0] * inv) : 0.f;
+      coefB[r] = 0.f;
+    }
+  }
+  rank_stamp(6);
+  if (q == 0 && t == 0) {
+    *loss_out = P > 0 ? L * inv : 0.0;
+    *pairs_out = P;
+    if (gb_out != nullptr) *gb_out = P > 0 ? float(G * inv) : 0.f;
+  }
+}
+
 template <typename T>
 __global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
                                      const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
@@ -1078,6 +1295,46 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
                                                 ntiles2, ld2, adv_bias, beta, out.loss, out.pairs, out.coefA, out.coefB,
                                                 out.ce, out.seg_of_row, out.R_rows, out.gb);
   MOSES_CUDA(cudaGetLastError());
+}
+
+void rank_trace_read(unsigned long long* out) {
+  MOSES_CUDA(cudaMemcpyFromSymbol(out, g_rank_trace, sizeof(unsigned long long) * 16));
+}
+bool rank_step(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
+               long long n, const RankWs& ws, unsigned int* ticket, float* s_out, const int* seg_of_row, long long R,
+               const FinalizeOut& out, cudaStream_t st) {
+  (void)seg_of_row;
+  (void)ws;
+  (void)ticket;
+  const int nsplit = rank_splits(n);
+  if (n <= 0) return false;
+  const int rows_per_cta = ceil_div(n, kRankCluster);
+  if (rows_per_cta * nsplit > kRankMaxItems || rows_per_cta > kRankMaxRows) return false;
+  const size_t smem = size_t(2 * n + 3 * kRankMaxItems + (seg ? R : 0)) * 4;
+  if (smem > 160 * 1024) return false;
+  static bool configured = false;
+  if (!configured) {
+    MOSES_CUDA(cudaFuncSetAttribute(rank_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    MOSES_CUDA(cudaFuncSetAttribute(rank_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kRankCluster);
+  cfg.blockDim = dim3(kRankThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kRankCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const long long Rk = seg ? R : n;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, rank_cluster_kernel, part, ntiles, ld, hb, seg, y, n, nsplit, rows_per_cta, s_out,
+                                Rk, out.loss, out.pairs, out.coefA, out.coefB, out.gb));
+  MOSES_CUDA(cudaGetLastError());
+  return true;
 }
 
 template <typename T>

@@ -70,6 +70,11 @@ struct FinalizeOut {
 };
 void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
                    const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st);
+// rank_pairs_fused + rank_finalize in one launch (no adversary); `ticket` is a zeroed device
+// counter the kernel re-arms. Returns false (nothing launched) when n is out of its range.
+bool rank_step(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
+               long long n, const RankWs& ws, unsigned int* ticket, float* s_out, const int* seg_of_row, long long R,
+               const FinalizeOut& out, cudaStream_t st);
 // dZ_last[r][j] = (coefA[r]*wh[j] + coefB[r]*u[j]) * [H[r][j] > 0]
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,

@@ -135,3 +135,37 @@ def test_fused_train_step_device_bitwise(ml, dims):
     a = run(ml, 1, go)
     b = run(ml, 0, go)
     assert np.array_equal(a.params, b.params) and np.array_equal(a.momentum, b.momentum)
+
+
+@pytest.mark.parametrize("n", [2, 12, 511, 512, 3000])
+@pytest.mark.parametrize("pooled", [False, True])
+def test_rank_step_matches_two_kernel_path(ml, n, pooled):
+    """rank_step (pairs + finalize in one launch, last-CTA reduction) vs rank_pairs + rank_finalize:
+    identical per-row coefficients -> bitwise-equal gradients; the loss uses log1p(e) = -log(1/(1+e))
+    (fast log of the reciprocal) and a different summation order: equal to ~1e-6."""
+    L = ml.lib()
+    L.moses_debug_set_rank_fused.argtypes = [ctypes.c_int]
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 6, strict=False)
+    rng = np.random.default_rng(n)
+    y = 0.1 + np.round(rng.random(n), 2)  # ties included
+    if pooled:
+        off = ml.synth_offsets(2, n, 5)
+        x = rng.random((int(off[-1]), 164))
+    else:
+        x = rng.random((n, 164))
+
+    def go(flag):
+        L.moses_debug_set_rank_fused(flag)
+        try:
+            dm = ml.DeviceModel(p, ml.PREC_BF16, 16384)
+            if pooled:
+                return ml.gradients_pooled(dm, x, off, y, want_loss=True)
+            return ml.gradients(dm, ml.RankingBatch(x, y), want_loss=True)
+        finally:
+            L.moses_debug_set_rank_fused(1)
+
+    g1, l1 = go(1)
+    g0, l0 = go(0)
+    assert np.array_equal(g1, g0)
+    assert abs(l1 - l0) <= 2e-6 * max(1.0, abs(l0))

@@ -11,7 +11,8 @@ import bench as B
 from paper_2201_05752_b200 import moseslab as ml
 
 L = ml.lib()
-for f in ("moses_debug_set_chain", "moses_debug_set_group", "moses_debug_set_cluster"):
+import os
+for f in ("moses_debug_set_chain", "moses_debug_set_group", "moses_debug_set_cluster", "moses_debug_set_rank_fused"):
     getattr(L, f).argtypes = [C.c_int]
 off = ml.synth_offsets(B.SEED_DATA, B.PROGRAMS, B.MAX_STMTS)
 nb = B.PROGRAMS // B.BATCH
@@ -21,9 +22,11 @@ rows_pad = int((np.diff(off[::B.BATCH]).max() + 127) // 128 * 128)
 params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 300
-for chain, group in ((1, 1), (1, 0), (0, 1), (0, 0)):
+CONFIGS = [tuple(int(c) for c in x) for x in os.environ.get("ABL", "111,101,011,001,110").split(",")]
+for chain, group, rankf in CONFIGS:
     L.moses_debug_set_chain(chain)
     L.moses_debug_set_group(group)
+    L.moses_debug_set_rank_fused(rankf)
     dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=rows_pad)
     ld = dm.packed_ld
     X = torch.empty((n_rows, ld), dtype=torch.bfloat16, device="cuda")
@@ -60,6 +63,6 @@ for chain, group in ((1, 1), (1, 0), (0, 1), (0, 0)):
         b.record(st)
         torch.cuda.synchronize()
         res["b2b"] = a.elapsed_time(b) / steps * 1e3
-    print(f"chain={chain} group={group}: flushed mean {res['flush'][0]:.1f} us (median {res['flush'][1]:.1f}); "
+    print(f"chain={chain} group={group} rank_fused={rankf}: flushed mean {res['flush'][0]:.1f} us (median {res['flush'][1]:.1f}); "
           f"warm mean {res['warm'][0]:.1f} us (median {res['warm'][1]:.1f}); back-to-back {res['b2b']:.1f} us", flush=True)
     dm.close()
