@@ -272,6 +272,9 @@ namespace {
 
 // ---------------------------------------------------------------- forward / backward composition
 // Fused hidden-layer chain (mlp_chain.cuh): bf16, every hidden width 512, input width <= 512.
+// The fused chain is a latency design (training batches, ~2.3K statement rows); scoring chunks of
+// 64K rows run layer by layer on the persistent tcgen05 kernels (2x faster there, tools/gemm_sweep.py).
+constexpr long long kChainMaxRows = 16384;
 bool chain_ok(const moses_model* m) {
   if (!g_chain || m->esz != 2 || m->L - 1 < 1 || m->L - 1 > 8 || m->dims[0] > 512) return false;
   for (int l = 1; l < m->L; ++l)
@@ -283,7 +286,7 @@ template <typename T>
 void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
   if (m->split && x0 != m->act[0])
     fail(MOSES_ERR_INVALID_ARG, "FP32 (3xTF32) handles take inputs through the host API only");
-  if (chain_ok(m) && R > 0) {
+  if (chain_ok(m) && R > 0 && R <= kChainMaxRows) {
     ChainCall cc;
     cc.fwd = true;
     cc.M = int(R);
@@ -1957,6 +1960,13 @@ extern "C" MOSES_API int moses_debug_set_group(int on) {
 }
 extern "C" MOSES_API int moses_debug_set_chain(int on) {
   moses::g_chain = on;
+  return 0;
+}
+namespace moses {
+extern int g_fwd;
+}
+extern "C" MOSES_API int moses_debug_set_fwd(int on) {
+  moses::g_fwd = on;
   return 0;
 }
 extern "C" MOSES_API int moses_debug_set_cluster(int on) {

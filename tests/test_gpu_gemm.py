@@ -73,7 +73,7 @@ def test_gemm_exact(ml, elem, shape, majors, bn):
 
 
 @pytest.mark.parametrize("elem", [2, 4])
-@pytest.mark.parametrize("majors,epi", [((0, 1), 0), ((0, 0), 2), ((0, 1), 2)])
+@pytest.mark.parametrize("majors,epi", [((0, 1), 0), ((0, 0), 0), ((0, 0), 2), ((0, 1), 2)])
 def test_persistent_gemm_exact(ml, elem, majors, epi):
     """M large enough for the persistent kernel (>= 2 tiles per SM), incl. a ragged last tile."""
     _case(ml, elem, 65536 + 77, 512, 512 if elem == 2 else 256, *majors, 0, epi)
