@@ -1468,12 +1468,12 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
       m->post_update();
       note_launch(1);
     } else {
-      if (!m->lot_ws) MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes()));
+      if (!m->lot_ws) MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes(m->P)));
       ProfScope ps(P_SELECT, m->st);
-      lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha), float(1.0 - rate), decay,
-                         m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);
+      const int launched = lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha),
+                                              float(1.0 - rate), decay, m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);
       m->post_update();
-      note_launch(mode == MOSES_MODE_RATIO ? 7 : 3);
+      note_launch(launched);
     }
     m->xi_valid = false;
     long long pop = std::min(keep, m->P);

@@ -116,10 +116,10 @@ void partition_from_xi(const float* xi, long long n, int mode, float theta, long
                        uint8_t* mask_out, cudaStream_t st);
 long long popcount_mask(const uint8_t* mask, long long n, unsigned long long* dcount, cudaStream_t st);
 // lottery.cu: fused xi -> partition -> transferable_step -> variant_decay, xi never materialised
-size_t lottery_ws_bytes();
-void lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
-                        float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
-                        cudaStream_t st);
+size_t lottery_ws_bytes(long long n);
+int lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
+                       float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
+                       cudaStream_t st);
 
 // ---- candidate top-k (search.cpp:32-37): (score desc, index asc)
 void topk_select(const float* scores, long long n, long long k, const SelectWs& ws, unsigned* out_key, long long* out_idx,

@@ -10,6 +10,14 @@
 //     pass 4  fused apply: kept = key > T || (key == T && i <= cut);  w -= alpha*g (kept) /
 //             w *= 1 - alpha*lambda (others); operand shadow + mask byte written      31-39 B/param
 // vs the algorithmic 15 B/param (read w, g; write w, bf16 shadow, mask byte).
+// Large vectors (n >= 16M scalars, w + g beyond L2) take the sampled-bracket variant of pass 2:
+//     pass 0  stratified sample (one float4 per 4 KB) -> 15-bit histogram -> bucket bracket
+//             [blo, bhi] that holds the keep-th key with a 6-sigma margin
+//     pass 1  full 15-bit histogram + compaction of every (key, index) whose bucket is in the
+//             bracket (block-aggregated appends)
+//     pass 2  16-bit histogram over the compacted candidates only (a few % of n), when the exact
+//             bucket b1 from pass 1 lies in the bracket; otherwise the (w, g) pass 2 runs as before
+//   so the ratio step reads (w, g) twice instead of three times: ~23 B/param.
 // The passes only count and compare integers, so the mask is bit-identical to nth_element's.
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -32,7 +40,20 @@ struct LotState {
   unsigned max_bits;         // threshold mode: max xi bits
   long long cut;             // last kept index among keys == T (LLONG_MAX: keep all equal keys)
   unsigned long long count;  // threshold mode popcount
+  unsigned blo, bhi;         // sampled bucket bracket (compaction path); blo > bhi: no compaction
+  unsigned long long cand_n; // compacted candidates appended by pass 1
+  unsigned long long cand_cap;
+  int cand_over;             // pass 1 ran out of candidate space
+  int use_cand;              // selection runs over the candidates (set by lot_decide_kernel)
+  unsigned long long need0;  // keep
+  unsigned long long above;  // keys whose bucket lies above the bracket
+  unsigned long long eqc_n;  // candidates with key == T collected for the index cut
+  int cut_done;              // the cut was found over the candidates
 };
+static_assert(sizeof(LotState) <= 256, "LotState must fit its workspace slot");
+
+constexpr long long kCandMinN = 1ll << 24;  // compaction path from 16M scalars (w + g = 128 MB > L2)
+constexpr int kSampleStride = 256;           // float4 groups per sample stratum (one sample per 4 KB)
 
 __device__ __forceinline__ unsigned xi_key(const float* __restrict__ w, const float* __restrict__ g, long long i) {
   return __float_as_uint(fabsf(__fmul_rn(w[i], g[i])));
@@ -55,9 +76,14 @@ __device__ __forceinline__ void hist_add(unsigned* sh, unsigned bin, bool valid)
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ unsigned key_of(float w, float g) { return __float_as_uint(fabsf(__fmul_rn(w, g))); }
 
+struct LotState;
+__device__ __forceinline__ bool use_cand_of(const LotState* st);
+template <bool CHECK>
 __global__ void __launch_bounds__(kPassBlock) lot_hist1_kernel(const float* __restrict__ w, const float* __restrict__ g,
-                                                               long long n, unsigned* __restrict__ hist) {
+                                                               long long n, unsigned* __restrict__ hist,
+                                                               const LotState* st) {
   extern __shared__ unsigned sh[];
+  if (CHECK && use_cand_of(st)) return;  // the compacted candidates carry the selection
   for (int d = threadIdx.x; d < kBins1; d += kPassBlock) sh[d] = 0;
   __syncthreads();
   const long long n4 = n / 4;
@@ -86,11 +112,14 @@ __global__ void __launch_bounds__(kPassBlock) lot_hist1_kernel(const float* __re
 // the block keeps u16 counters and flushes its non-zero bins to the global histogram every
 // 32768 elements (a bin can gain at most 32768 per round: no u16 overflow).
 constexpr int kRound = 32 * kPassBlock;  // multiple of 4 (float4 loads stay aligned)
+__device__ __forceinline__ bool cand_path(const LotState* st);
+template <bool CHECK>
 __global__ void __launch_bounds__(kPassBlock) lot_hist2_kernel(const float* __restrict__ w, const float* __restrict__ g,
                                                                long long n, const LotState* st,
                                                                unsigned* __restrict__ hist) {
   extern __shared__ unsigned short sh16[];
   __shared__ int s_any;
+  if (CHECK && cand_path(st)) return;  // pass 2 already done over the compacted candidates
   const unsigned b1 = st->prefix;
   for (int d = threadIdx.x; d < kBins2; d += kPassBlock) sh16[d] = 0;
   if (threadIdx.x == 0) s_any = 0;
@@ -151,39 +180,329 @@ __global__ void __launch_bounds__(kPassBlock) lot_hist2_kernel(const float* __re
   }
 }
 
+__device__ __forceinline__ unsigned mix32(unsigned x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// Pass 0: one float4 of (w, g) at a hashed position inside every stratum of kSampleStride groups.
+__global__ void __launch_bounds__(kPassBlock) lot_sample_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                                                long long n, unsigned* __restrict__ hist) {
+  extern __shared__ unsigned sh[];
+  for (int d = threadIdx.x; d < kBins1; d += kPassBlock) sh[d] = 0;
+  __syncthreads();
+  const long long strata = n / 4 / kSampleStride;
+  for (long long j0 = blockIdx.x * (long long)kPassBlock; j0 < strata; j0 += (long long)gridDim.x * kPassBlock) {
+    const long long j = j0 + threadIdx.x;
+    const bool ok = j < strata;
+    float4 a = make_float4(0, 0, 0, 0), b = a;
+    if (ok) {
+      const long long q = j * kSampleStride + (mix32(unsigned(j)) % kSampleStride);
+      a = ld4(w + 4 * q);
+      b = ld4(g + 4 * q);
+    }
+    hist_add(sh, key_of(a.x, b.x) >> 16, ok);
+    hist_add(sh, key_of(a.y, b.y) >> 16, ok);
+    hist_add(sh, key_of(a.z, b.z) >> 16, ok);
+    hist_add(sh, key_of(a.w, b.w) >> 16, ok);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kBins1; d += kPassBlock)
+    if (sh[d]) atomicAdd(&hist[d], sh[d]);
+}
+
+// One block: bucket bracket [blo, bhi] around the sample rank of the keep-th key (+- 6 sigma + 32).
+// Sample ranks are converted to integers once; the two owning threads locate their digits like
+// lot_pick_kernel (sum, scan, then one re-read of the owning chunk).
+__global__ void __launch_bounds__(1024) lot_bracket_kernel(LotState* st, unsigned* hist, long long n) {
+  using Scan = cub::BlockScan<unsigned long long, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned s_lo, s_hi;
+  __shared__ unsigned long long s_above_hi, s_upto_lo;
+  constexpr int PER = kBins1 / 1024;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + kBins1 - PER * (threadIdx.x + 1));
+  unsigned long long local = 0;
+#pragma unroll 4
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 v = h4[q];
+    local += (unsigned long long)v.x + v.y + v.z + v.w;
+  }
+  unsigned long long before, total;
+  Scan(tmp).ExclusiveSum(local, before, total);
+  const double frac = double(total) / double(n);
+  const double need_s = double(st->need0) * frac;
+  const double delta = 6.0 * sqrt(fmax(need_s, 1.0)) + 32.0;
+  const long long r_hi = (long long)floor(need_s - delta);  // < 0: bracket open at the top
+  const unsigned long long r_lo = (unsigned long long)ceil(need_s + delta);
+  if (threadIdx.x == 0) {
+    s_lo = 0;
+    s_hi = kBins1 - 1;
+    s_above_hi = 0;
+    s_upto_lo = ~0ull;
+  }
+  __syncthreads();
+  const unsigned* hc = hist + kBins1 - PER * (threadIdx.x + 1);
+  // digit holding sample rank r_hi (0-based): before <= r_hi < before + local
+  if (r_hi >= 0 && before <= (unsigned long long)r_hi && (unsigned long long)r_hi < before + local) {
+    unsigned long long run = before;
+    for (int q = PER - 1; q >= 0; --q) {
+      const unsigned long long v = hc[q];
+      if ((unsigned long long)r_hi < run + v) {
+        s_hi = unsigned(kBins1 - PER * (threadIdx.x + 1) + q);
+        s_above_hi = run;
+        break;
+      }
+      run += v;
+    }
+  }
+  // digit where the cumulative count reaches r_lo: before < r_lo <= before + local
+  if (before < r_lo && r_lo <= before + local) {
+    unsigned long long run = before;
+    for (int q = PER - 1; q >= 0; --q) {
+      const unsigned long long v = hc[q];
+      if (r_lo <= run + v) {
+        s_lo = unsigned(kBins1 - PER * (threadIdx.x + 1) + q);
+        s_upto_lo = run + v;
+        break;
+      }
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned lo = s_lo, hi = s_hi;
+    const bool found = s_upto_lo != ~0ull;  // r_lo <= total
+    const double in = found ? double(s_upto_lo - s_above_hi) : 0.0;  // sampled keys in [lo, hi]
+    const double est = in / fmax(frac, 1e-300) * 1.25 + 4096.0;
+    const bool ok = total > 0 && found && lo > 0 && lo <= hi && est < double(st->cand_cap);
+    st->blo = ok ? lo : 1u;
+    st->bhi = ok ? hi : 0u;
+  }
+  __syncthreads();
+  uint4* z4 = reinterpret_cast<uint4*>(hist);
+  for (int d = threadIdx.x; d < kBins1 / 4; d += 1024) z4[d] = make_uint4(0, 0, 0, 0);
+}
+
+// Pass 1 with compaction: count the keys whose bucket lies above the bracket (register counters)
+// and append every (key, index) whose bucket lies in [blo, bhi] to `cand`. Each warp stages its
+// appends in its own shared-memory slice and flushes them with one global atomic per 128+ entries,
+// so the pass has no block barriers; the next float4 pair is loaded before the current one is
+// processed (two loads in flight per thread).
+constexpr int kWarpStage = 256;  // entries per warp slice (flush at >= 128: one iteration adds <= 128)
+__global__ void __launch_bounds__(kPassBlock) lot_pass1c_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                                                long long n, LotState* st, uint2* __restrict__ cand) {
+  extern __shared__ uint2 sc_all[];
+  using Red = cub::BlockReduce<unsigned long long, kPassBlock>;
+  __shared__ typename Red::TempStorage rtmp;
+  const unsigned blo = st->blo, bhi = st->bhi;
+  if (blo > bhi) return;  // bracket disabled: the (w, g) histogram passes run instead
+  const unsigned lane = threadIdx.x & 31;
+  uint2* sc = sc_all + (threadIdx.x >> 5) * kWarpStage;
+  const unsigned long long cap = st->cand_cap;
+  unsigned cnt = 0;  // warp-uniform
+  unsigned long long above = 0;
+  auto flush = [&]() {  // warp-collective
+    unsigned long long b = 0;
+    if (lane == 0) {
+      b = atomicAdd(&st->cand_n, (unsigned long long)cnt);
+      if (b + cnt > cap) st->cand_over = 1;
+    }
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b + cnt <= cap)
+      for (unsigned i = lane; i < cnt; i += 32) cand[b + i] = sc[i];
+    __syncwarp();
+    cnt = 0;
+  };
+  auto take = [&](unsigned key, long long i, bool ok) {  // warp-collective
+    const unsigned bk = key >> 16;
+    above += (ok && bk > bhi) ? 1u : 0u;
+    const bool in = ok && bk >= blo && bk <= bhi;
+    const unsigned ball = __ballot_sync(0xffffffffu, in);
+    if (in) sc[cnt + __popc(ball & ((1u << lane) - 1u))] = make_uint2(key, unsigned(i));
+    cnt += __popc(ball);
+  };
+  const long long n4 = n / 4;
+  const long long stride = (long long)gridDim.x * kPassBlock;
+  long long q = blockIdx.x * (long long)kPassBlock + threadIdx.x;
+  const long long qend = (n4 + kPassBlock - 1) / kPassBlock * kPassBlock;  // warp-uniform trip count
+  float4 a = make_float4(0, 0, 0, 0), b = a;
+  if (q < n4) {
+    a = ld4(w + 4 * q);
+    b = ld4(g + 4 * q);
+  }
+  for (; q < qend; q += stride) {
+    const bool ok = q < n4;
+    const long long qn = q + stride;
+    float4 an = make_float4(0, 0, 0, 0), bn = an;
+    if (qn < n4) {
+      an = ld4(w + 4 * qn);
+      bn = ld4(g + 4 * qn);
+    }
+    take(key_of(a.x, b.x), 4 * q, ok);
+    take(key_of(a.y, b.y), 4 * q + 1, ok);
+    take(key_of(a.z, b.z), 4 * q + 2, ok);
+    take(key_of(a.w, b.w), 4 * q + 3, ok);
+    if (cnt >= kWarpStage - 128) flush();
+    a = an;
+    b = bn;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // scalar tail (< 4 scalars), warp 0
+    const long long i = 4 * n4 + lane;
+    const bool ok = i < n;
+    take(ok ? xi_key(w, g, i) : 0u, i, ok);
+  }
+  if (cnt) flush();
+  above = Red(rtmp).Sum(above);
+  if (threadIdx.x == 0 && above) atomicAdd(&st->above, above);
+}
+
+// Compaction path usable: no overflow and the keep-th key lies among the candidates.
+__device__ __forceinline__ bool cand_ok(const LotState* st) {
+  return st->blo <= st->bhi && st->cand_over == 0 && st->above < st->need0 && st->need0 - st->above <= st->cand_n;
+}
+
+// one thread: set the selection state for whichever path runs
+__global__ void lot_decide_kernel(LotState* st) {
+  if (cand_ok(st)) {
+    st->gt = st->above;
+    st->need = st->need0 - st->above;
+    st->use_cand = 1;
+  } else {
+    st->use_cand = 0;
+  }
+}
+
+// 15-bit bucket histogram over the compacted candidates (compaction path only).
+__global__ void __launch_bounds__(kPassBlock) lot_hist1_cand_kernel(const uint2* __restrict__ cand, const LotState* st,
+                                                                    unsigned* __restrict__ hist) {
+  extern __shared__ unsigned sh[];
+  if (!st->use_cand) return;
+  for (int d = threadIdx.x; d < kBins1; d += kPassBlock) sh[d] = 0;
+  __syncthreads();
+  const unsigned long long nc = st->cand_n;
+  for (unsigned long long i0 = blockIdx.x * (unsigned long long)kPassBlock; i0 < nc;
+       i0 += gridDim.x * (unsigned long long)kPassBlock) {
+    const unsigned long long i = i0 + threadIdx.x;
+    const bool ok = i < nc;
+    hist_add(sh, ok ? (cand[i].x >> 16) : 0u, ok);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kBins1; d += kPassBlock)
+    if (sh[d]) atomicAdd(&hist[d], sh[d]);
+}
+
+__device__ __forceinline__ bool cand_path(const LotState* st) { return st->use_cand != 0; }
+__device__ __forceinline__ bool use_cand_of(const LotState* st) { return st->use_cand != 0; }
+
+// Pass 2 over the compacted candidates (only when the exact bucket b1 lies in the bracket).
+__global__ void __launch_bounds__(256) lot_hist2c_kernel(const uint2* __restrict__ cand, const LotState* st,
+                                                         unsigned* __restrict__ hist) {
+  if (!cand_path(st)) return;
+  const unsigned b1 = st->prefix;
+  const unsigned long long nc = st->cand_n;
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i - threadIdx.x < nc; i += gridDim.x * 256ull) {
+    const bool ok = i < nc;
+    const unsigned key = ok ? cand[i].x : 0u;
+    const bool in = ok && (key >> kB2) == b1;
+    const unsigned d = key & (kBins2 - 1);
+    const unsigned d0 = __shfl_sync(0xffffffffu, d, 0);
+    if (__all_sync(0xffffffffu, in && d == d0)) {
+      if ((threadIdx.x & 31) == 0) atomicAdd(&hist[d0], 32u);
+    } else if (in) {
+      atomicAdd(&hist[d], 1u);
+    }
+  }
+}
+
 // Single block: choose the digit where the descending cumulative count reaches `need`.
+// Thread t owns the PER consecutive digits BINS-1-t*PER ... BINS-PER-t*PER (descending); the bins
+// are read twice (sum, then locate) instead of being held in registers.
 template <int BINS>
 __global__ void __launch_bounds__(1024) lot_pick_kernel(LotState* st, unsigned* hist, int shift, bool last) {
   using Scan = cub::BlockScan<unsigned long long, 1024>;
   __shared__ typename Scan::TempStorage tmp;
   constexpr int PER = BINS / 1024;
   const unsigned long long need = st->need;  // read before any thread updates the state
-  unsigned long long vals[PER];
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + BINS - PER * (threadIdx.x + 1));  // ascending chunk
   unsigned long long local = 0;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {  // thread t owns digits BINS-1-(t*PER+q): descending order
-    vals[q] = hist[BINS - 1 - (threadIdx.x * PER + q)];
-    local += vals[q];
+#pragma unroll 4
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 v = h4[q];
+    local += (unsigned long long)v.x + v.y + v.z + v.w;
   }
   unsigned long long before;
   Scan(tmp).ExclusiveSum(local, before);
-  unsigned long long run = before;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int d = BINS - 1 - (threadIdx.x * PER + q);
-    if (run < need && run + vals[q] >= need) {  // unique digit d*
-      st->need = need - run;
-      st->gt += run;
-      st->prefix = shift ? unsigned(d) : ((st->prefix << kB2) | unsigned(d));
-      if (last) {
-        st->eq = vals[q];
-        st->cut = 0x7fffffffffffffffll;
+  if (before < need && before + local >= need) {  // the crossing digit is in this thread's chunk
+    const unsigned* hc = hist + BINS - PER * (threadIdx.x + 1);
+    unsigned long long run = before;
+    for (int q = PER - 1; q >= 0; --q) {  // descending digits
+      const unsigned long long v = hc[q];
+      if (run + v >= need) {
+        const int d = BINS - PER * (threadIdx.x + 1) + q;
+        st->need = need - run;
+        st->gt += run;
+        st->prefix = shift ? unsigned(d) : ((st->prefix << kB2) | unsigned(d));
+        if (last) {
+          st->eq = v;
+          st->cut = 0x7fffffffffffffffll;
+        }
+        break;
       }
+      run += v;
     }
-    run += vals[q];
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < BINS; d += 1024) hist[d] = 0;  // ready for the next pass / call
+  uint4* z4 = reinterpret_cast<uint4*>(hist);
+  for (int d = threadIdx.x; d < BINS / 4; d += 1024) z4[d] = make_uint4(0, 0, 0, 0);  // ready for the next pass
+}
+
+// Ties at T straddling the cut, compaction path: every key == T is a candidate, so collect their
+// indices (up to kEqCap) and let one block sort them; the need-th smallest index is the cut.
+constexpr int kEqCap = 4096;
+__global__ void __launch_bounds__(256) lot_eq_cand_kernel(const uint2* __restrict__ cand, LotState* st,
+                                                          unsigned* __restrict__ eq_idx) {
+  if (!st->use_cand || st->need >= st->eq || st->eq > kEqCap) return;
+  const unsigned T = st->prefix;
+  const unsigned long long nc = st->cand_n;
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < nc; i += gridDim.x * 256ull) {
+    const uint2 c = cand[i];
+    if (c.x == T) {
+      const unsigned long long slot = atomicAdd(&st->eqc_n, 1ull);
+      if (slot < kEqCap) eq_idx[slot] = c.y;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) lot_cut_cand_kernel(LotState* st, const unsigned* __restrict__ eq_idx) {
+  __shared__ unsigned sk[kEqCap];
+  if (!st->use_cand || st->need >= st->eq || st->eq > kEqCap || st->eqc_n != st->eq) return;
+  const int m = int(st->eq);
+  for (int i = threadIdx.x; i < kEqCap; i += 1024) sk[i] = i < m ? eq_idx[i] : 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= kEqCap; k <<= 1) {  // bitonic sort, ascending
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < kEqCap; i += 1024) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const unsigned x = sk[i], y = sk[p];
+          if ((x > y) == up) {
+            sk[i] = y;
+            sk[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    st->cut = (long long)sk[st->need - 1];
+    st->cut_done = 1;
+  }
 }
 
 // pass 3 (only when ties at T straddle the cut): per-block counts of key == T over fixed chunks
@@ -193,7 +512,7 @@ __global__ void __launch_bounds__(kPassBlock) lot_eq_count_kernel(const float* _
                                                                   unsigned long long* __restrict__ block_eq) {
   using Red = cub::BlockReduce<unsigned long long, kPassBlock>;
   __shared__ typename Red::TempStorage tmp;
-  if (st->need >= st->eq) return;  // every key equal to T is kept: no index cut needed
+  if (st->need >= st->eq || st->cut_done) return;  // every key equal to T is kept, or cut already found
   const unsigned T = st->prefix;
   const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   unsigned long long c = 0;
@@ -211,7 +530,7 @@ __global__ void __launch_bounds__(kPassBlock) lot_cut_kernel(const float* __rest
   __shared__ long long s_blk;
   __shared__ unsigned long long s_before;
   __shared__ long long s_cut;
-  if (st->need >= st->eq) return;
+  if (st->need >= st->eq || st->cut_done) return;
   const unsigned long long need = st->need;
   if (threadIdx.x == 0) {
     unsigned long long run = 0;
@@ -341,8 +660,18 @@ __global__ void __launch_bounds__(kPassBlock) lot_max_kernel(const float* __rest
   if ((threadIdx.x & 31) == 0 && m) atomicMax(&st->max_bits, m);
 }
 
-__global__ void lot_init_kernel(LotState* st, unsigned long long keep) {
+__global__ void lot_init_kernel(LotState* st, unsigned long long keep, unsigned long long cap) {
   st->need = keep;
+  st->blo = 1;
+  st->bhi = 0;
+  st->cand_n = 0;
+  st->cand_cap = cap;
+  st->cand_over = 0;
+  st->use_cand = 0;
+  st->need0 = keep;
+  st->above = 0;
+  st->eqc_n = 0;
+  st->cut_done = 0;
   st->gt = 0;
   st->eq = 0;
   st->prefix = 0;
@@ -364,27 +693,42 @@ int g_sms() {
 
 }  // namespace
 
-size_t lottery_ws_bytes() {
-  return 256 /*state*/ + size_t(kBins1) * 4 + size_t(kBins2) * 4 + size_t(4096) * 8 + 1024;
+static long long cand_capacity(long long n) { return n >= kCandMinN ? n / 16 + 65536 : 0; }
+
+size_t lottery_ws_bytes(long long n) {
+  return 256 /*state*/ + size_t(kBins1) * 4 * 2 /*hist1, sample hist*/ + size_t(kBins2) * 4 + size_t(4096) * 8 +
+         size_t(kEqCap) * 4 +
+         size_t(cand_capacity(n)) * 8 + 1024;
 }
 
 // Fused Moses step. mode 1 threshold (normalised, strict), 2 ratio (top `keep`, index tie-break).
-void lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
-                        float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
-                        cudaStream_t st) {
+int lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
+                       float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
+                       cudaStream_t st) {
   uint8_t* p = static_cast<uint8_t*>(ws);
   LotState* S = reinterpret_cast<LotState*>(p);
   unsigned* hist1 = reinterpret_cast<unsigned*>(p + 256);
   unsigned* hist2 = hist1 + kBins1;
   unsigned long long* block_eq = reinterpret_cast<unsigned long long*>(hist2 + kBins2);
+  unsigned* hist_s = reinterpret_cast<unsigned*>(block_eq + 4096);
+  unsigned* eq_idx = hist_s + kBins1;
+  uint2* cand = reinterpret_cast<uint2*>(eq_idx + kEqCap);
+  const long long cap = cand_capacity(n);
+  const bool compact = mode != 1 && cap > 0 && n < (1ll << 32);
   const int sms = g_sms();
   static bool configured = false;
   if (!configured) {
-    MOSES_CUDA(cudaFuncSetAttribute(lot_hist1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins1 * 4));
-    MOSES_CUDA(cudaFuncSetAttribute(lot_hist2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins2 * 2));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_hist2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins2 * 2));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_hist2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins2 * 2));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins1 * 4));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_hist1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins1 * 4));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_hist1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins1 * 4));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_hist1_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins1 * 4));
+    MOSES_CUDA(cudaFuncSetAttribute(lot_pass1c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (kPassBlock / 32) * kWarpStage * 8));
     configured = true;
   }
-  lot_init_kernel<<<1, 1, 0, st>>>(S, (unsigned long long)keep);
+  lot_init_kernel<<<1, 1, 0, st>>>(S, (unsigned long long)keep, (unsigned long long)cap);
   const int agrid = std::max<long long>(1, std::min<long long>((n / 4 + 255) / 256, (long long)sms * 16));
   if (mode == 1) {
     lot_max_kernel<<<sms * 2, kPassBlock, 0, st>>>(w, g, n, S);  // 2 x 1024 threads per SM
@@ -392,11 +736,27 @@ void lottery_step_fused(float* w, const float* g, long long n, int mode, float t
     if (sh.kind == 1) LOT_T(1); else if (sh.kind == 2) LOT_T(2); else LOT_T(0);
 #undef LOT_T
   } else {
-    lot_hist1_kernel<<<sms, kPassBlock, kBins1 * 4, st>>>(w, g, n, hist1);
-    lot_pick_kernel<kBins1><<<1, 1024, 0, st>>>(S, hist1, 16, false);
-    lot_hist2_kernel<<<sms, kPassBlock, kBins2 * 2, st>>>(w, g, n, S, hist2);
+    if (compact) {
+      lot_sample_kernel<<<sms, kPassBlock, kBins1 * 4, st>>>(w, g, n, hist_s);
+      lot_bracket_kernel<<<1, 1024, 0, st>>>(S, hist_s, n);
+      lot_pass1c_kernel<<<sms * 2, kPassBlock, (kPassBlock / 32) * kWarpStage * 8, st>>>(w, g, n, S, cand);
+      lot_decide_kernel<<<1, 1, 0, st>>>(S);
+      lot_hist1_kernel<true><<<sms, kPassBlock, kBins1 * 4, st>>>(w, g, n, hist1, S);      // fallback only
+      lot_hist1_cand_kernel<<<sms, kPassBlock, kBins1 * 4, st>>>(cand, S, hist1);          // fast path only
+      lot_pick_kernel<kBins1><<<1, 1024, 0, st>>>(S, hist1, 16, false);
+      lot_hist2c_kernel<<<sms * 8, 256, 0, st>>>(cand, S, hist2);                          // fast path only
+      lot_hist2_kernel<true><<<sms, kPassBlock, kBins2 * 2, st>>>(w, g, n, S, hist2);      // fallback only
+    } else {
+      lot_hist1_kernel<false><<<sms, kPassBlock, kBins1 * 4, st>>>(w, g, n, hist1, S);
+      lot_pick_kernel<kBins1><<<1, 1024, 0, st>>>(S, hist1, 16, false);
+      lot_hist2_kernel<false><<<sms, kPassBlock, kBins2 * 2, st>>>(w, g, n, S, hist2);
+    }
     lot_pick_kernel<kBins2><<<1, 1024, 0, st>>>(S, hist2, 0, true);
-    const int nb = std::min(4096, sms * 4);
+    if (compact) {
+      lot_eq_cand_kernel<<<sms * 4, 256, 0, st>>>(cand, S, eq_idx);
+      lot_cut_cand_kernel<<<1, 1024, 0, st>>>(S, eq_idx);
+    }
+    const int nb = 4096;  // chunks for the general tie cut (block_eq capacity)
     const long long chunk = (n + nb - 1) / nb;
     lot_eq_count_kernel<<<nb, kPassBlock, 0, st>>>(w, g, n, chunk, S, block_eq);
     lot_cut_kernel<<<1, kPassBlock, 0, st>>>(w, g, n, chunk, nb, S, block_eq);
@@ -409,6 +769,7 @@ void lottery_step_fused(float* w, const float* g, long long n, int mode, float t
     MOSES_CUDA(cudaMemcpyAsync(popcount_dev, &S->count, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
   }
   MOSES_CUDA(cudaGetLastError());
+  return mode == 1 ? 3 : (compact ? 16 : 8);  // kernels launched
 }
 
 }  // namespace moses

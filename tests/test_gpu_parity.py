@@ -673,3 +673,38 @@ def test_fused_lottery_step_large_bit_exact(ml, orc, rho):
     ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
     ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
     assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
+
+
+@pytest.mark.parametrize("kind,rho", [("normal", 0.3), ("normal", 0.5), ("normal", 0.01), ("zeros", 0.7),
+                                      ("quantized", 0.37), ("ties", 0.42)])
+def test_fused_lottery_step_compaction_path_bit_exact(ml, orc, kind, rho):
+    """16.8M scalars: the sampled-bracket compaction path of the ratio step (lottery.cu). 'zeros'
+    puts the keep-th key inside the 40% zero-gradient ties (bracket disabled -> exact fallback);
+    'quantized' draws w, g from a few values so the cut falls inside a huge tie group of a non-zero
+    key (general chunked index cut); 'ties' copies the keep-th scalar's (w, g) to 200 random slots
+    so a small tie group straddles the cut (sorted-candidate index cut). Mask and weights bit-exact."""
+    dims = [8192, 2048, 8, 1]
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(int(rho * 100) + len(kind))
+    if kind == "quantized":
+        w = f32(rng.choice([-0.05, -0.02, 0.01, 0.03, 0.07], P))
+        g = f32(rng.choice([-2e-2, -5e-3, 1e-3, 4e-3, 1e-2], P))
+    else:
+        w = f32(rng.normal(0, 0.05, P))
+        g = f32(rng.normal(0, 1e-2, P))
+        g[rng.random(P) < 0.4] = 0.0
+    if kind == "ties":
+        xi = np.abs(w.astype(np.float32) * g.astype(np.float32))
+        keep = orc.ratio_keep(rho, P)
+        r = int(np.argpartition(-xi, keep - 1)[keep - 1])  # the keep-th largest
+        slots = rng.choice(P, 200, replace=False)
+        w[slots], g[slots] = w[r], g[r]
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    dm.set_gradients(g)
+    mask = ml.lottery_step(dm, ml.RATIO, rho, 0, 0.001, 0.01)
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    ref_mask = orc.partition(orc.xi_scores(w32, g32, False), False, orc.RATIO, rho)
+    assert np.array_equal(mask.transferable, ref_mask)
+    ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+    ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
+    assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
