@@ -650,9 +650,23 @@ __global__ void __launch_bounds__(kPassBlock) lot_max_kernel(const float* __rest
                                                              long long n, LotState* st) {
   unsigned m = 0;
   const long long n4 = n / 4;
-  for (long long q = blockIdx.x * (long long)kPassBlock + threadIdx.x; q < n4; q += (long long)gridDim.x * kPassBlock) {
-    const float4 a = ld4(w + 4 * q), b = ld4(g + 4 * q);
+  const long long stride = (long long)gridDim.x * kPassBlock;
+  long long q = blockIdx.x * (long long)kPassBlock + threadIdx.x;
+  float4 a = make_float4(0, 0, 0, 0), b = a;
+  if (q < n4) {
+    a = ld4(w + 4 * q);
+    b = ld4(g + 4 * q);
+  }
+  for (; q < n4; q += stride) {  // next pair loaded before the current one is reduced
+    const long long qn = q + stride;
+    float4 an = make_float4(0, 0, 0, 0), bn = an;
+    if (qn < n4) {
+      an = ld4(w + 4 * qn);
+      bn = ld4(g + 4 * qn);
+    }
     m = max(max(max(m, key_of(a.x, b.x)), key_of(a.y, b.y)), max(key_of(a.z, b.z), key_of(a.w, b.w)));
+    a = an;
+    b = bn;
   }
   if (blockIdx.x == 0)
     for (long long i = 4 * n4 + threadIdx.x; i < n; i += kPassBlock) m = max(m, xi_key(w, g, i));
