@@ -1628,17 +1628,23 @@ MOSES_API int moses_topk_device(const float* scores, int64_t n, int64_t k, int64
     Scratch& sc = scratch();
     std::lock_guard<std::mutex> lk(sc.mu);
     const size_t selb = select_ws_bytes(n, nullptr);
-    Carver cv{static_cast<uint8_t*>(sc.ensure(selb + (kTopkMax * 12) + 8192))};
+    Carver cv{static_cast<uint8_t*>(sc.ensure(selb + (kTopkMax * 12) + topk_fast_ws_bytes(n) + 8192))};
     uint8_t* selbase = cv.take<uint8_t>(selb);
     unsigned* ok = cv.take<unsigned>(n < kTopkMax ? kTopkMax : kTopkMax);
     long long* oi = cv.take<long long>(kTopkMax);
+    void* fast_ws = cv.take<uint8_t>(topk_fast_ws_bytes(n));
     SelectWs ws;
     select_ws_carve(selbase, n, &ws);
     {
       ProfScope ps(P_TOPK, sc.st);
-      topk_select(scores, n, k, ws, ok, oi, sc.st);
+      // one read of the pool when the sampled threshold is conclusive, else the exact radix passes
+      if (topk_fast(scores, n, k, fast_ws, ok, oi, sc.st)) {
+        note_launch(11);
+      } else {
+        topk_select(scores, n, k, ws, ok, oi, sc.st);
+        note_launch(10);
+      }
     }
-    note_launch(10);
     MOSES_CUDA(cudaMemcpyAsync(idx_out, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
     MOSES_CUDA(cudaStreamSynchronize(sc.st));
   });

@@ -1450,6 +1450,12 @@ static void radix_select_passes(const float* a, const float* b, long long n, uns
   MOSES_CUDA(cudaGetLastError());
 }
 
+// exact key of descending rank `need` among ws.keys[0, n) -> SelState::prefix (sel_result_key)
+void select_kth_key(long long n, unsigned long long need, const SelectWs& ws, cudaStream_t st) {
+  radix_select_passes<0>(nullptr, nullptr, n, need, ws, nullptr, st);
+}
+const unsigned* sel_result_key(const SelectWs& ws) { return &reinterpret_cast<const SelState*>(ws.state)->prefix; }
+
 void lottery_select(const float* w, const float* g, long long n, int mode, float theta, long long keep, const SelectWs& ws,
                     uint8_t* mask_out, float* xi_out, bool normalize_xi, cudaStream_t st) {
   int grid;

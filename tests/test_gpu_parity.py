@@ -515,6 +515,29 @@ def test_topk_bit_exact(ml, orc, n, k):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("kind,k", [("normal", 1), ("normal", 12), ("normal", 1024), ("normal", 4096),
+                                    ("ascending", 1024), ("descending", 4096), ("ties", 777), ("equal", 4096),
+                                    ("negative", 100)])
+def test_topk_large_pool_bit_exact(ml, orc, kind, k):
+    """3M-candidate pools: the one-pass sampled top-k (topk.cu) and, where the sample is not
+    conclusive (all-equal scores: the candidate set overflows), the exact radix fallback."""
+    n = 3_000_001
+    rng = np.random.default_rng(k)
+    s = rng.normal(0, 1, n)
+    if kind == "ascending":
+        s = np.sort(s)
+    elif kind == "descending":
+        s = np.sort(s)[::-1].copy()
+    elif kind == "ties":
+        s = np.round(s, 2)
+    elif kind == "equal":
+        s = np.full(n, 0.25)
+    elif kind == "negative":
+        s = -np.abs(s) - 1.0
+    s = f32(s)
+    assert np.array_equal(ml.topk(s, k), orc.topk(s.astype(np.float32), k))
+
+
 def test_topk_negative_and_equal_scores(ml, orc):
     s = np.array([-1.0, -0.5, -0.5, -3.0, 0.0, -0.0, 2.5, -0.5])
     assert np.array_equal(ml.topk(s, 8), orc.topk(s.astype(np.float32), 8))
