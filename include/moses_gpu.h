@@ -209,6 +209,10 @@ MOSES_API int moses_segment_sum_device(const void* h_dev, int32_t dtype, int64_t
 /* Biased MMD^2 with a Gaussian kernel between source and target representations. */
 MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t n, int32_t width, double sigma,
                          double* out);
+/* Same statistic over device-resident fp32 rows (stride ld floats): the cfg3 fine-tune path, where
+   the source/target penultimate activations already live in HBM. tcgen05 kind::tf32 Gram tiles. */
+MOSES_API int moses_mmd2_device(const float* xs, int64_t m, const float* xt, int64_t n, int32_t width, int64_t ld,
+                                double sigma, double* out);
 
 /* ------------------------------------------------------------------ synthetic TenSet-shaped data (bench) */
 /* Rows [row0, row0+n) of the keyed SplitMix64 generator, written in the packed layout. */

@@ -1726,20 +1726,38 @@ MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t 
                          double* out) {
   return guarded([&] {
     if (m <= 0 || n <= 0) fail(MOSES_ERR_INVALID_ARG, "mmd needs non-empty source and target");
+    if (width <= 0) fail(MOSES_ERR_INVALID_ARG, "mmd needs a positive width");
     Scratch& sc = scratch();
     std::lock_guard<std::mutex> lk(sc.mu);
     const long long R = m + n;
-    const long long parts = (long long)ceil_div(m, 64) * ceil_div(m, 64) + ceil_div(n, 64) * ceil_div(n, 64) +
-                            ceil_div(m, 64) * ceil_div(n, 64);
-    Carver cv{static_cast<uint8_t*>(sc.ensure(size_t(R) * width * 12 + size_t(parts + 16) * 8 + 8192))};
+    const size_t wsb = mmd_ws_bytes(m, n, width);
+    Carver cv{static_cast<uint8_t*>(sc.ensure(size_t(R) * width * 12 + wsb + 8192))};
     double* h64 = cv.take<double>(R * width);
     float* H = cv.take<float>(R * width);
-    double* ws = cv.take<double>(parts + 16);
+    void* ws = cv.take<uint8_t>(wsb);
     MOSES_CUDA(cudaMemcpyAsync(h64, xs, 8 * m * width, cudaMemcpyHostToDevice, sc.st));
     MOSES_CUDA(cudaMemcpyAsync(h64 + m * width, xt, 8 * n * width, cudaMemcpyHostToDevice, sc.st));
     f64_to_f32(h64, R * width, H, sc.st);
-    *out = mmd2(H, m, H + m * width, n, width, float(sigma), ws, sc.st);
-    note_launch(7);
+    int launched = 0;
+    *out = mmd2_tc(H, m, H + m * width, n, width, width, float(sigma), ws, sc.st, &launched);
+    note_launch(1 + launched);
+  });
+}
+
+MOSES_API int moses_mmd2_device(const float* xs, int64_t m, const float* xt, int64_t n, int32_t width, int64_t ld,
+                                double sigma, double* out) {
+  return guarded([&] {
+    if (m <= 0 || n <= 0) fail(MOSES_ERR_INVALID_ARG, "mmd needs non-empty source and target");
+    if (width <= 0 || ld < width) fail(MOSES_ERR_INVALID_ARG, "mmd needs 0 < width <= ld");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    void* ws = sc.ensure(mmd_ws_bytes(m, n, width) + 4096);
+    int launched = 0;
+    {
+      ProfScope ps(P_OTHER, sc.st);
+      *out = mmd2_tc(xs, m, xt, n, width, ld, float(sigma), ws, sc.st, &launched);
+    }
+    note_launch(launched);
   });
 }
 

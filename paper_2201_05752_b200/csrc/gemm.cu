@@ -7,6 +7,7 @@
 #include "gemm.cuh"
 #include "gemm_persistent.cuh"
 #include "gemm_fwd.cuh"
+#include "gemm_gram.cuh"
 #include "gemm_cluster.cuh"
 #include "gemm_split.cuh"
 #include "mlp_chain.cuh"
@@ -522,6 +523,101 @@ int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
   if (elem == 2) dispatch_bn<__nv_bfloat16>(c, bn, s);
   else dispatch_bn<float>(c, bn, s);
   return bn;
+}
+
+// ---------------------------------------------------------------- MMD^2 on the tensor cores
+namespace {
+// one warp per row: tf32 (RNA) copy into a 16-B-aligned padded row + squared norm of the rounded row
+__global__ void gram_prep_kernel(const float* __restrict__ X, long long rows, int W, long long ld,
+                                 float* __restrict__ Xp, long long ldp, float* __restrict__ norms) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    float acc = 0.f;
+    for (int j = lane; j < ldp; j += 32) {
+      const float v = j < W ? tf32_round(X[r * ld + j]) : 0.f;
+      Xp[r * ldp + j] = v;
+      acc = fmaf(v, v, acc);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) norms[r] = acc;
+  }
+}
+__global__ void __launch_bounds__(1024) gram_sum_kernel(const double* p, long long n, double* out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) s += p[i];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = sh[threadIdx.x];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = s;
+  }
+}
+long long gram_tiles(long long M, long long N, bool sym) {
+  const long long tm = (M + 127) / 128, tn = (N + 127) / 128;
+  return sym ? tm * (tm + 1) / 2 : tm * tn;
+}
+}  // namespace
+
+size_t mmd_ws_bytes(long long m, long long n, int W) {
+  const long long ldp = (W + 3) / 4 * 4;
+  const long long tiles = std::max(gram_tiles(m, m, true), std::max(gram_tiles(n, n, true), gram_tiles(m, n, false)));
+  return size_t(m + n) * ldp * 4 + size_t(m + n) * 4 + size_t(tiles) * 4 * 8 + 64 + 4 * 256;
+}
+
+// Gram reduction S(X, Y) into *out (device double); X, Y: tf32-rounded rows with stride ldp.
+static void gram_sum(const float* X, long long M, const float* nx, const float* Y, long long N, const float* ny, int W,
+                     long long ldp, float c, bool sym, double* part, double* out, cudaStream_t s) {
+  auto kern = umma_gram_kernel;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GCfg::kSmemBytes));
+  });
+  const CUtensorMap ta = make_map(X, 4, W, M, ldp, 32, 128);
+  const CUtensorMap tb = make_map(Y, 4, W, N, ldp, 32, 128);
+  GramArgs g{};
+  g.M = int(M);
+  g.N = int(N);
+  g.K = W;
+  g.nx = nx;
+  g.ny = ny;
+  g.c = c;
+  g.sym = sym ? 1 : 0;
+  g.part = part;
+  const long long tiles = gram_tiles(M, N, sym);
+  const int grid = int(std::min<long long>(tiles, g_num_sms));
+  kern<<<grid, GCfg::kThreads, GCfg::kSmemBytes, s>>>(ta, tb, g, ceil_div(M, 128), tiles);
+  gram_sum_kernel<<<1, 1024, 0, s>>>(part, tiles * 4, out);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+// Biased MMD^2 (oracle mmd2): S(s,s)/m^2 + S(t,t)/n^2 - 2 S(s,t)/(m n); rows of xs / xt with stride ld.
+double mmd2_tc(const float* xs, long long m, const float* xt, long long n, int W, long long ld, float sigma, void* ws,
+               cudaStream_t s, int* launches) {
+  if (g_num_sms <= 0) g_num_sms = 148;
+  const long long ldp = (W + 3) / 4 * 4;
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  float* Xp = reinterpret_cast<float*>(p);
+  float* norms = Xp + (m + n) * ldp;
+  double* sums = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(norms) + ((m + n) * 4 + 255) / 256 * 256);
+  double* part = sums + 8;
+  gram_prep_kernel<<<int(std::min<long long>((m + 7) / 8, 4096)), 256, 0, s>>>(xs, m, W, ld, Xp, ldp, norms);
+  gram_prep_kernel<<<int(std::min<long long>((n + 7) / 8, 4096)), 256, 0, s>>>(xt, n, W, ld, Xp + m * ldp, ldp,
+                                                                               norms + m);
+  const float c = float(1.4426950408889634 / (2.0 * double(sigma) * double(sigma)));
+  const float* Xs = Xp;
+  const float* Xt = Xp + m * ldp;
+  gram_sum(Xs, m, norms, Xs, m, norms, W, ldp, c, true, part, sums + 0, s);
+  gram_sum(Xt, n, norms + m, Xt, n, norms + m, W, ldp, c, true, part, sums + 1, s);
+  gram_sum(Xs, m, norms, Xt, n, norms + m, W, ldp, c, false, part, sums + 2, s);
+  double h[3];
+  MOSES_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, s));
+  MOSES_CUDA(cudaStreamSynchronize(s));
+  if (launches) *launches = 8;
+  return h[0] / (double(m) * double(m)) + h[1] / (double(n) * double(n)) - 2.0 * h[2] / (double(m) * double(n));
 }
 
 }  // namespace moses

@@ -1085,50 +1085,6 @@ __global__ void segment_sum_scalar_kernel(const float* __restrict__ v, const lon
   }
 }
 
-// ---------------------------------------------------------------- MMD^2 (Gaussian kernel), tiled 64x64 Gram + exp + sum
-constexpr int kGT = 64;
-__global__ void __launch_bounds__(256) gram_exp_kernel(const float* __restrict__ A, long long na, const float* __restrict__ B,
-                                                       long long nb, int W, float inv2s2, double* partial) {
-  __shared__ float sa[kGT][33], sb[kGT][33];
-  using BR = cub::BlockReduce<double, 256>;
-  __shared__ typename BR::TempStorage tmp;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const long long i0 = (long long)blockIdx.x * kGT, j0 = (long long)blockIdx.y * kGT;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < W; k0 += 32) {
-    for (int t = threadIdx.x; t < kGT * 32; t += 256) {
-      const int r = t / 32, k = t % 32;
-      sa[r][k] = (i0 + r < na && k0 + k < W) ? A[(i0 + r) * W + k0 + k] : 0.f;
-      sb[r][k] = (j0 + r < nb && k0 + k < W) ? B[(j0 + r) * W + k0 + k] : 0.f;
-    }
-    __syncthreads();
-    for (int k = 0; k < 32; ++k)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const float d = sa[ty * 4 + a][k] - sb[tx * 4 + b][k];
-          acc[a][b] = fmaf(d, d, acc[a][b]);
-        }
-    __syncthreads();
-  }
-  double s = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (i0 + ty * 4 + a < na && j0 + tx * 4 + b < nb) s += double(expf(-acc[a][b] * inv2s2));
-  s = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) partial[blockIdx.y * (long long)gridDim.x + blockIdx.x] = s;
-}
-__global__ void sum_partials_kernel(const double* p, long long n, double* out) {
-  using BR = cub::BlockReduce<double, 1024>;
-  __shared__ typename BR::TempStorage tmp;
-  double s = 0.0;
-  for (long long i = threadIdx.x; i < n; i += 1024) s += p[i];
-  s = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) *out = s;
-}
 
 // ---------------------------------------------------------------- synthetic data
 __device__ __forceinline__ unsigned long long fnv_u64(unsigned long long h, unsigned long long v) {
@@ -1588,22 +1544,6 @@ void segment_sum_scalar(const float* v, const long long* offsets, long long prog
   MOSES_CUDA(cudaGetLastError());
 }
 
-double mmd2(const float* xs, long long m, const float* xt, long long n, int W, float sigma, double* ws, cudaStream_t st) {
-  const float inv = 1.f / (2.f * sigma * sigma);
-  double sums[3];
-  const float* A[3] = {xs, xt, xs};
-  const float* B[3] = {xs, xt, xt};
-  const long long na[3] = {m, n, m}, nb[3] = {m, n, n};
-  for (int q = 0; q < 3; ++q) {
-    dim3 grid(ceil_div(na[q], kGT), ceil_div(nb[q], kGT));
-    gram_exp_kernel<<<grid, 256, 0, st>>>(A[q], na[q], B[q], nb[q], W, inv, ws + 8);
-    sum_partials_kernel<<<1, 1024, 0, st>>>(ws + 8, (long long)grid.x * grid.y, ws + q);
-  }
-  MOSES_CUDA(cudaGetLastError());
-  MOSES_CUDA(cudaMemcpyAsync(sums, ws, sizeof(sums), cudaMemcpyDeviceToHost, st));
-  MOSES_CUDA(cudaStreamSynchronize(st));
-  return sums[0] / (double(m) * double(m)) + sums[1] / (double(n) * double(n)) - 2.0 * sums[2] / (double(m) * double(n));
-}
 
 template <typename T>
 void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st) {

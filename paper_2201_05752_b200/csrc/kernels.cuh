@@ -147,7 +147,10 @@ void segment_sum(const T* H, long long ldh, int W, const long long* offsets, lon
                  long long ldo, cudaStream_t st);
 void segment_sum_scalar(const float* v, const long long* offsets, long long programs, float bias, float* out,
                         cudaStream_t st);
-double mmd2(const float* xs, long long m, const float* xt, long long n, int W, float sigma, double* ws, cudaStream_t st);
+// tensor-core MMD^2 (gemm_gram.cuh): rows with stride ld; ws of mmd_ws_bytes(m, n, W)
+size_t mmd_ws_bytes(long long m, long long n, int W);
+double mmd2_tc(const float* xs, long long m, const float* xt, long long n, int W, long long ld, float sigma, void* ws,
+               cudaStream_t s, int* launches);
 
 // ---- synthetic TenSet-shaped data (bit-identical to oracle::synth_*)
 template <typename T>

@@ -121,6 +121,7 @@ def lib():
         "moses_segment_sum": (C.c_int, [vp, i64, i32, vp, i64, vp]),
         "moses_segment_sum_device": (C.c_int, [vp, i32, i64, i32, vp, i64, vp]),
         "moses_mmd2": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp]),
+        "moses_mmd2_device": (C.c_int, [vp, i64, vp, i64, i32, i64, dbl, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),

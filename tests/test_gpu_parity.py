@@ -555,10 +555,44 @@ def test_segment_sum_vs_oracle(ml, orc):
     assert nrel(ml.segment_sum(h[:3], empty), orc.segment_sum(h[:3], empty)) < 1e-6
 
 
-def test_mmd_vs_oracle(ml, orc):
-    rng = np.random.default_rng(1)
-    xs, xt = rng.normal(0, 1, (300, 64)), rng.normal(0.3, 1, (120, 64))
-    assert ml.mmd2(xs, xt, 4.0) == pytest.approx(orc.mmd2(xs, xt, 4.0), rel=1e-4, abs=1e-7)
+def gram_sum(a, b, sigma):
+    d = (a * a).sum(1)[:, None] + (b * b).sum(1)[None, :] - 2 * a @ b.T
+    return np.exp(-np.maximum(d, 0) / (2 * sigma * sigma)).sum()
+
+
+@pytest.mark.parametrize("m,n,w,shift", [(300, 120, 64, 0.3), (1000, 257, 512, 0.1), (129, 130, 37, 0.0),
+                                         (2000, 500, 512, 0.0)])
+def test_mmd_vs_oracle(ml, orc, m, n, w, shift):
+    """MMD^2 on tcgen05 kind::tf32 Gram tiles (gemm_gram.cuh) vs fp64: within 1e-3 of the kernel-sum
+    scale S(s,s)/m^2 + S(t,t)/n^2 + 2 S(s,t)/(mn) (the north-star TF32 tolerance; MMD^2 itself can
+    cancel to ~0). Small cases against the C oracle, the large one against its numpy restatement."""
+    rng = np.random.default_rng(m + n + w)
+    xs, xt = rng.normal(0, 1, (m, w)), rng.normal(shift, 1, (n, w))
+    sigma = float(np.sqrt(w))
+    ss, tt, st = gram_sum(xs, xs, sigma), gram_sum(xt, xt, sigma), gram_sum(xs, xt, sigma)
+    scale = ss / m**2 + tt / n**2 + 2 * st / (m * n)
+    ref = orc.mmd2(xs, xt, sigma) if m * n < 400_000 else ss / m**2 + tt / n**2 - 2 * st / (m * n)
+    got = ml.mmd2(xs, xt, sigma)
+    assert abs(got - ref) <= 1e-3 * scale, (got, ref, scale)
+
+
+def test_mmd_device_entry_matches_host_entry(ml):
+    import ctypes as C
+
+    import torch
+
+    rng = np.random.default_rng(4)
+    xs, xt = rng.normal(0, 1, (700, 512)), rng.normal(0.2, 1, (300, 512))
+    ld = 520  # padded row stride
+    X = torch.zeros((1000, ld), dtype=torch.float32)
+    X[:700, :512] = torch.from_numpy(xs)
+    X[700:, :512] = torch.from_numpy(xt)
+    X = X.cuda()
+    out = C.c_double()
+    rc = ml.lib().moses_mmd2_device(C.c_void_p(X.data_ptr()), 700, C.c_void_p(X[700:].data_ptr()), 300, 512, ld,
+                                    8.0, C.byref(out))
+    assert rc == 0, ml.lib().moses_last_error()
+    assert out.value == pytest.approx(ml.mmd2(xs, xt, 8.0), rel=1e-9, abs=1e-12)
 
 
 # ---------------------------------------------------------------- synthetic generator bit-exactness
