@@ -38,20 +38,23 @@ out = torch.empty(R, 520, device=dev).to(bf)
 g = torch.empty(513 * 512, device=dev, dtype=torch.float32)
 bias = torch.randn(512, device=dev)
 EPI_FWD, EPI_DGRAD, EPI_F32 = 0, 1, 2
-for cl, pe in ((1, 1), (0, 1), (0, 0)):
-    L.moses_debug_set_cluster(cl)
-    L.moses_debug_set_persistent(pe)
-    print(f"--- cluster={cl} persistent={pe}  rows={R}")
-    for K in (64, 128, 256, 512):
-        us = t(R, 512, K, act, 520, 0, w, 512, 1, EPI_FWD, out, 520, bias, 1)
-        print(f"fwd  K={K:4d}: {us:7.2f} us  {2 * R * 512 * K / us / 1e6:7.1f} TF/s")
-    us = t(R, 512, 164, x0, 168, 0, w0, 512, 1, EPI_FWD, out, 520, bias, 1)
-    print(f"fwd0 K=164 : {us:7.2f} us")
-    us = t(R, 512, 512, dz, 512, 0, w, 512, 0, EPI_DGRAD, out, 520, None, 0, 0, act, 520)
-    print(f"dgrad      : {us:7.2f} us")
-    for bn in (0, 64, 128, 256):
-        try:
-            us = t(513, 512, R, act, 520, 1, dz, 512, 1, EPI_F32, g, 512, bn=bn)
-            print(f"wgrad bn={bn:3d}: {us:7.2f} us  {2 * R * 512 * 513 / us / 1e6:7.1f} TF/s")
-        except AssertionError as e:
-            print("wgrad bn", bn, e)
+if __name__ != "__main__":
+    pass
+else:
+  for cl, pe in ((1, 1), (0, 1), (0, 0)):
+        L.moses_debug_set_cluster(cl)
+        L.moses_debug_set_persistent(pe)
+        print(f"--- cluster={cl} persistent={pe}  rows={R}")
+        for K in (64, 128, 256, 512):
+            us = t(R, 512, K, act, 520, 0, w, 512, 1, EPI_FWD, out, 520, bias, 1)
+            print(f"fwd  K={K:4d}: {us:7.2f} us  {2 * R * 512 * K / us / 1e6:7.1f} TF/s")
+        us = t(R, 512, 164, x0, 168, 0, w0, 512, 1, EPI_FWD, out, 520, bias, 1)
+        print(f"fwd0 K=164 : {us:7.2f} us")
+        us = t(R, 512, 512, dz, 512, 0, w, 512, 0, EPI_DGRAD, out, 520, None, 0, 0, act, 520)
+        print(f"dgrad      : {us:7.2f} us")
+        for bn in (0, 64, 128, 256):
+            try:
+                us = t(513, 512, R, act, 520, 1, dz, 512, 1, EPI_F32, g, 512, bn=bn)
+                print(f"wgrad bn={bn:3d}: {us:7.2f} us  {2 * R * 512 * 513 / us / 1e6:7.1f} TF/s")
+            except AssertionError as e:
+                print("wgrad bn", bn, e)

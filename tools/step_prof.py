@@ -1,0 +1,52 @@
+"""Kernel timeline (torch profiler / CUPTI) of the bench training step (pooled CUDA graph),
+with and without the 256 MiB L2 flush between steps."""
+import sys
+
+import numpy as np
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, ".")
+import bench as B
+from paper_2201_05752_b200 import moseslab as ml
+
+L = ml.lib()
+off = ml.synth_offsets(B.SEED_DATA, B.PROGRAMS, B.MAX_STMTS)
+nb = B.PROGRAMS // B.BATCH
+off = off[: nb * B.BATCH + 1]
+n_rows = int(off[-1])
+rows_pad = int((np.diff(off[::B.BATCH]).max() + 127) // 128 * 128)
+params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
+dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=rows_pad)
+ld = dm.packed_ld
+X = torch.empty((n_rows, ld), dtype=torch.bfloat16, device="cuda")
+Y = torch.empty(nb * B.BATCH, dtype=torch.float32, device="cuda")
+OFF = torch.from_numpy(off).cuda()
+assert L.moses_synth_features_device(B.SEED_DATA, 0, n_rows, B.DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+assert L.moses_synth_labels_device(B.SEED_DATA, 0, nb * B.BATCH, Y.data_ptr()) == 0
+torch.cuda.synchronize()
+L.moses_set_async(1)
+ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, B.BATCH, rows_pad,
+                                         B.LR, B.MU, 1))
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+for _ in range(20):
+    ml._ck(L.moses_train_graph_launch(dm.h, 1))
+torch.cuda.synchronize()
+for do_flush in (True, False):
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for k in range(4):
+            if do_flush:
+                flush.fill_(float(k))
+            ml._ck(L.moses_train_graph_launch(dm.h, 1))
+        torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    evs.sort(key=lambda e: e.time_range.start)
+    # last step only
+    starts = [i for i, e in enumerate(evs) if "gather_pooled" in e.name]
+    evs = evs[starts[-1]:] if starts else evs
+    t0 = evs[0].time_range.start
+    print(f"--- flush={do_flush}")
+    for e in evs:
+        if "FillFunctor" in e.name:
+            continue
+        print(f"{e.time_range.start - t0:8.1f} {e.time_range.end - t0:8.1f} {e.time_range.elapsed_us():7.1f}  {e.name[:70]}")
