@@ -327,6 +327,99 @@ def bench_hbm_kernels(ml, L, peaks):
     return out
 
 
+def bench_finetune(ml, L, peaks, reps=20):
+    """cfg3: Moses fine-tuning source -> target on the 4x512 model (P = 872,961): one step is the
+    tuner.cpp:251-262 Moses branch through the reference-facing C ABI with host buffers
+    (gradients with the reversed-BCE adversary over 256 replay rows, beta = 0.01 -> discriminator
+    step -> fused lottery step: xi -> ratio 0.5 partition -> transferable step -> variant decay),
+    plus the MMD^2 discrepancy between 50k source and 5k target 512-d representations
+    (device-resident, tensor-core Gram tiles)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
+
+    out = {}
+    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
+    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=1024)
+    rng = np.random.default_rng(3)
+    replay = rng.random((256, DIMS[0]))
+    adv = ml.AdversaryState(replay, DIMS[-2])
+    xt = np.ascontiguousarray(rng.random((BATCH, DIMS[0])))
+    yt = np.ascontiguousarray(0.1 + rng.random(BATCH))
+    loss = C.c_double()
+    dl, cf = C.c_double(), C.c_double()
+    pop = C.c_int64()
+
+    def step():
+        ml._ck(L.moses_gradients(dm.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], adv.h, 0.01, C.byref(loss)))
+        ml._ck(L.moses_adversarial_step(adv.h, dm.h, xt.ctypes.data, BATCH, DIMS[0], 0.01, C.byref(dl), C.byref(cf)))
+        ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    out["moses_step"] = {"ms": dt * 1e3, "samples_per_s": BATCH / dt, "batch": BATCH, "replay": 256,
+                         "params": len(params.params),
+                         "path": "moses_gradients(adv, beta=0.01) + moses_adversarial_step + moses_lottery_step "
+                                 "(ratio 0.5), host float64 buffers, wall clock"}
+    # the lottery step alone at the real parameter count (L2-resident: launch/latency bound)
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    st = torch.cuda.ExternalStream(sp.value)
+    L.moses_set_async(1)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps):
+        ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
+    b.record(st)
+    torch.cuda.synchronize()
+    L.moses_set_async(0)
+    out["lottery_step_real_P"] = {"ms": a.elapsed_time(b) / reps, "params": len(params.params),
+                                  "note": "device time per fused ratio-0.5 step; w, g L2-resident"}
+    del adv
+    dm.close()
+    # MMD^2 over 50k source / 5k target penultimate representations
+    m_s, n_t, w = 50_000, 5_000, DIMS[-2]
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    H = torch.rand((m_s + n_t, w), device="cuda", generator=gen)
+    H[m_s:] += 0.05
+    res = C.c_double()
+    sig = float(np.sqrt(w / 6.0))
+
+    def mmd():
+        ml._ck(L.moses_mmd2_device(C.c_void_p(H.data_ptr()), m_s, C.c_void_p(H[m_s:].data_ptr()), n_t, w, w, sig,
+                                   C.byref(res)))
+
+    mmd()
+    ml.profile_begin()
+    mmd()
+    prof = ml.profile_end()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        mmd()
+    dt = (time.perf_counter() - t0) / 5
+    flops = 2.0 * w * (m_s * (m_s + 1) / 2 + n_t * (n_t + 1) / 2 + m_s * n_t)
+    dev_ms = prof.get("other", (None,))[0]
+    peak = peaks.get("bf16_tflops_sustained", 1408.7) / 2.0
+    ach = flops / (dev_ms / 1e3) / 1e12 if dev_ms else None
+    out["mmd2"] = {"source": m_s, "target": n_t, "width": w, "value": res.value, "ms_wall": dt * 1e3,
+                   "ms_device": dev_ms, "flops_unique_pairs": flops,
+                   "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                "frac": ach / peak if ach else None,
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained / 2 (dense tf32 rate)",
+                                "kernel": "umma_gram_kernel (tcgen05 kind::tf32, exp-sum epilogue)"}}
+    del H
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,6 +430,7 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-infer", action="store_true")
     ap.add_argument("--no-hbm", action="store_true")
+    ap.add_argument("--no-finetune", action="store_true")
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -531,6 +625,8 @@ def main():
         line["infer"] = bench_infer(ml, L, local, args.infer_programs, peaks)
     if not args.no_hbm:
         line["hbm_kernels"] = bench_hbm_kernels(ml, L, peaks)
+    if not args.no_finetune:
+        line["finetune"] = bench_finetune(ml, L, peaks)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(15.0)
     print(json.dumps(line), flush=True)

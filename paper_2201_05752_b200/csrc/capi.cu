@@ -1468,7 +1468,10 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
       m->post_update();
       note_launch(1);
     } else {
-      if (!m->lot_ws) MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes(m->P)));
+      if (!m->lot_ws) {
+        MOSES_CUDA(cudaMalloc(&m->lot_ws, lottery_ws_bytes(m->P)));
+        MOSES_CUDA(cudaMemsetAsync(m->lot_ws, 0, lottery_ws_bytes(m->P), m->st));  // barrier state of the resident step
+      }
       ProfScope ps(P_SELECT, m->st);
       const int launched = lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha),
                                               float(1.0 - rate), decay, m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);

@@ -674,6 +674,231 @@ __global__ void __launch_bounds__(kPassBlock) lot_max_kernel(const float* __rest
   if ((threadIdx.x & 31) == 0 && m) atomicMax(&st->max_bits, m);
 }
 
+// ---------------------------------------------------------------- single-launch resident step
+// For the cost model's own parameter counts (P <= 148 x 512 x 16 ~ 1.2M; the 4x512 model has
+// 872,961) the whole step is ONE cooperative launch: every thread keeps its <= 16 (w, g) pairs in
+// registers, so HBM/L2 see exactly one read of (w, g) and one write of (w, mask, shadow) — the
+// algorithmic 15 B/param — and the selection runs between grid barriers instead of kernel launches:
+//   ratio:      3 radix digits (11/11/10 bits of the xi key; block histograms -> global, every block
+//               re-derives the chosen digit from the global histogram), then the ties at T are
+//               ranked in index order through per-block equal counts, then the fused apply;
+//   threshold:  block max -> global max, then the fused apply (popcount accumulated).
+// Block b owns indices [b*chunk, (b+1)*chunk); thread t holds b*chunk + j*512 + t, j < E.
+constexpr int kResThreads = 512, kResE = 16;
+
+struct ResState {
+  unsigned bar_count, bar_gen;
+  unsigned max_bits;
+  unsigned long long count;
+  unsigned hist1[2048], hist2[2048], hist3[1024];
+  unsigned long long block_eq[1024];
+};
+
+__device__ __forceinline__ void res_grid_sync(ResState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &st->bar_gen;
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0;
+      __threadfence();
+      atomicAdd(&st->bar_gen, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// every block: descending cumulative over `bins` global counts -> the digit where it reaches `need`
+template <int BINS>
+__device__ __forceinline__ void res_pick(const unsigned* hist, unsigned long long need, unsigned* s_digit,
+                                         unsigned long long* s_before) {
+  using Scan = cub::BlockScan<unsigned long long, kResThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int PER = BINS / kResThreads;  // 2 or 1, descending digits per thread
+  unsigned long long v[PER], local = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    v[q] = __ldcg(hist + (BINS - 1 - (threadIdx.x * PER + q)));
+    local += v[q];
+  }
+  unsigned long long before;
+  Scan(tmp).ExclusiveSum(local, before);
+  unsigned long long run = before;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (run < need && run + v[q] >= need) {
+      *s_digit = unsigned(BINS - 1 - (threadIdx.x * PER + q));
+      *s_before = run;
+    }
+    run += v[q];
+  }
+  __syncthreads();
+}
+
+template <int SHADOW, bool THRESH>
+__global__ void __launch_bounds__(kResThreads, 1)
+    lot_resident_kernel(float* __restrict__ w, const float* __restrict__ g, long long n, long long chunk, int E,
+                        unsigned long long keep, float theta, float alpha, float factor, bool decay,
+                        void* __restrict__ shadow, uint8_t* __restrict__ mask, ResState* st,
+                        unsigned long long* popcount_out) {
+  __shared__ unsigned sh[2048];
+  __shared__ unsigned s_digit;
+  __shared__ unsigned long long s_before;
+  using Red = cub::BlockReduce<unsigned long long, kResThreads>;
+  __shared__ typename Red::TempStorage rtmp;
+  const long long base = blockIdx.x * chunk;
+  float wv[kResE], gv[kResE];
+#pragma unroll
+  for (int j = 0; j < kResE; ++j) {
+    const long long i = base + (long long)j * kResThreads + threadIdx.x;
+    const bool ok = j < E && i < n && i < base + chunk;
+    wv[j] = ok ? w[i] : 0.f;
+    gv[j] = ok ? __ldg(g + i) : 0.f;
+  }
+  auto valid = [&](int j) {
+    const long long i = base + (long long)j * kResThreads + threadIdx.x;
+    return j < E && i < n && i < base + chunk;
+  };
+  unsigned T = 0;
+  unsigned long long need_eq = 0, eq_total = 0;  // ratio: keys == T still to keep / present
+  float top = 0.f;
+  if (blockIdx.x == 0) {  // buffers first written after the first barrier
+    for (int d = threadIdx.x; d < 2048; d += kResThreads) st->hist2[d] = 0;
+    for (int d = threadIdx.x; d < 1024; d += kResThreads) st->hist3[d] = 0;
+    if (threadIdx.x == 0) st->count = 0;
+  }
+  if constexpr (THRESH) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < kResE; ++j)
+      if (valid(j)) m = max(m, key_of(wv[j], gv[j]));
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(&st->max_bits, m);
+    res_grid_sync(st);
+    top = __uint_as_float(__ldcg(&st->max_bits));
+  } else {
+    // digit 1: bits [31:21]
+    for (int d = threadIdx.x; d < 2048; d += kResThreads) sh[d] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kResE; ++j)
+      if (valid(j)) atomicAdd(&sh[key_of(wv[j], gv[j]) >> 21], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < 2048; d += kResThreads)
+      if (sh[d]) atomicAdd(&st->hist1[d], sh[d]);
+    res_grid_sync(st);
+    res_pick<2048>(st->hist1, keep, &s_digit, &s_before);
+    const unsigned d1 = s_digit;
+    unsigned long long need = keep - s_before;
+    // digit 2: bits [20:10] among keys with digit 1 == d1
+    for (int d = threadIdx.x; d < 2048; d += kResThreads) sh[d] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kResE; ++j) {
+      const unsigned k = key_of(wv[j], gv[j]);
+      if (valid(j) && (k >> 21) == d1) atomicAdd(&sh[(k >> 10) & 2047u], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 2048; d += kResThreads)
+      if (sh[d]) atomicAdd(&st->hist2[d], sh[d]);
+    res_grid_sync(st);
+    if (blockIdx.x == 0)  // every block has read hist1 (before the barrier): clear it for the next call
+      for (int d = threadIdx.x; d < 2048; d += kResThreads) st->hist1[d] = 0;
+    res_pick<2048>(st->hist2, need, &s_digit, &s_before);
+    const unsigned p2 = (d1 << 11) | s_digit;
+    need -= s_before;
+    // digit 3: bits [9:0] among keys with bits [31:10] == p2
+    for (int d = threadIdx.x; d < 1024; d += kResThreads) sh[d] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kResE; ++j) {
+      const unsigned k = key_of(wv[j], gv[j]);
+      if (valid(j) && (k >> 10) == p2) atomicAdd(&sh[k & 1023u], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 1024; d += kResThreads)
+      if (sh[d]) atomicAdd(&st->hist3[d], sh[d]);
+    res_grid_sync(st);
+    res_pick<1024>(st->hist3, need, &s_digit, &s_before);
+    T = (p2 << 10) | s_digit;
+    need_eq = need - s_before;
+    eq_total = __ldcg(&st->hist3[s_digit]);
+    if (need_eq < eq_total) {  // ties at T straddle the cut: rank them in index order
+      unsigned long long c = 0;
+#pragma unroll
+      for (int j = 0; j < kResE; ++j) c += (valid(j) && key_of(wv[j], gv[j]) == T) ? 1u : 0u;
+      c = Red(rtmp).Sum(c);
+      if (threadIdx.x == 0) st->block_eq[blockIdx.x] = c;
+      res_grid_sync(st);
+    }
+  }
+  // ---- fused apply (the same per-scalar arithmetic as lot_apply_kernel)
+  unsigned long long eq_before = 0;  // keys == T in lower-indexed blocks
+  if (!THRESH && need_eq < eq_total) {
+    unsigned long long c = 0;
+    for (int b = threadIdx.x; b < int(blockIdx.x); b += kResThreads) c += __ldcg(&st->block_eq[b]);
+    eq_before = Red(rtmp).Sum(c);
+    if (threadIdx.x == 0) s_before = eq_before;
+    __syncthreads();
+    eq_before = s_before;
+  }
+  using ScanU = cub::BlockScan<unsigned, kResThreads>;
+  __shared__ typename ScanU::TempStorage stmp;
+  unsigned long long cnt = 0;
+#pragma unroll
+  for (int j = 0; j < kResE; ++j) {
+    const long long i = base + (long long)j * kResThreads + threadIdx.x;
+    const bool ok = valid(j);
+    bool kept = false;
+    const float x = fabsf(__fmul_rn(wv[j], gv[j]));
+    if constexpr (THRESH) {
+      const float xn = top > 0.f ? __fdiv_rn(x, top) : x;
+      kept = ok && xn > theta;
+      cnt += kept;
+    } else {
+      const unsigned key = __float_as_uint(x);
+      const bool eq = ok && key == T;
+      if (need_eq < eq_total) {  // block-ordered rank of this equal key (index order: j, then t)
+        unsigned r, tot;
+        ScanU(stmp).ExclusiveSum(eq ? 1u : 0u, r, tot);
+        kept = ok && (key > T || (eq && eq_before + r < need_eq));
+        eq_before += tot;
+        __syncthreads();
+      } else {
+        kept = ok && key >= T;
+      }
+    }
+    if (ok) {
+      float wi = wv[j];
+      if (kept) wi = __fsub_rn(wi, __fmul_rn(alpha, gv[j]));
+      else if (decay) wi = __fmul_rn(wi, factor);
+      w[i] = wi;
+      mask[i] = kept ? 1 : 0;
+      if constexpr (SHADOW == 1) static_cast<__nv_bfloat16*>(shadow)[i] = __float2bfloat16_rn(wi);
+      if constexpr (SHADOW == 2) {
+        uint32_t tt;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(tt) : "f"(wi));
+        static_cast<float*>(shadow)[i] = __uint_as_float(tt);
+      }
+    }
+  }
+  if constexpr (THRESH) {
+    cnt = Red(rtmp).Sum(cnt);
+    if (threadIdx.x == 0 && cnt) atomicAdd(&st->count, cnt);
+    res_grid_sync(st);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (popcount_out) *popcount_out = st->count;
+      st->max_bits = 0;  // ready for the next call
+    }
+  }
+}
+
+static size_t res_state_bytes() { return (sizeof(ResState) + 255) / 256 * 256; }
+
 __global__ void lot_init_kernel(LotState* st, unsigned long long keep, unsigned long long cap) {
   st->need = keep;
   st->blo = 1;
@@ -710,8 +935,8 @@ int g_sms() {
 static long long cand_capacity(long long n) { return n >= kCandMinN ? n / 16 + 65536 : 0; }
 
 size_t lottery_ws_bytes(long long n) {
-  return 256 /*state*/ + size_t(kBins1) * 4 * 2 /*hist1, sample hist*/ + size_t(kBins2) * 4 + size_t(4096) * 8 +
-         size_t(kEqCap) * 4 +
+  return res_state_bytes() + 256 /*state*/ + size_t(kBins1) * 4 * 2 /*hist1, sample hist*/ + size_t(kBins2) * 4 +
+         size_t(4096) * 8 + size_t(kEqCap) * 4 +
          size_t(cand_capacity(n)) * 8 + 1024;
 }
 
@@ -719,7 +944,8 @@ size_t lottery_ws_bytes(long long n) {
 int lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
                        float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
                        cudaStream_t st) {
-  uint8_t* p = static_cast<uint8_t*>(ws);
+  ResState* R = static_cast<ResState*>(ws);  // zeroed at allocation; every call leaves it reusable
+  uint8_t* p = static_cast<uint8_t*>(ws) + res_state_bytes();
   LotState* S = reinterpret_cast<LotState*>(p);
   unsigned* hist1 = reinterpret_cast<unsigned*>(p + 256);
   unsigned* hist2 = hist1 + kBins1;
@@ -741,6 +967,25 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     MOSES_CUDA(cudaFuncSetAttribute(lot_pass1c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (kPassBlock / 32) * kWarpStage * 8));
     configured = true;
+  }
+  // the cost model's own sizes: one cooperative launch with register-resident (w, g)
+  if (n <= (long long)sms * kResThreads * kResE && n >= 1) {
+    const long long chunk = (n + sms - 1) / sms;
+    const int E = int((chunk + kResThreads - 1) / kResThreads);
+    unsigned long long* pop = popcount_dev;
+    const unsigned long long ukeep = (unsigned long long)keep;
+    void* shp = sh.ptr;
+    int grid = sms;
+    void* args[] = {&w, (void*)&g, &n, (void*)&chunk, (void*)&E, (void*)&ukeep, &theta, &alpha, &factor, &decay, &shp,
+                    &mask, &R, &pop};
+    const void* fn = nullptr;
+    if (mode == 1) fn = sh.kind == 1 ? (const void*)lot_resident_kernel<1, true>
+                      : sh.kind == 2 ? (const void*)lot_resident_kernel<2, true> : (const void*)lot_resident_kernel<0, true>;
+    else fn = sh.kind == 1 ? (const void*)lot_resident_kernel<1, false>
+              : sh.kind == 2 ? (const void*)lot_resident_kernel<2, false> : (const void*)lot_resident_kernel<0, false>;
+    MOSES_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kResThreads), args, 0, st));
+    MOSES_CUDA(cudaGetLastError());
+    return 1;
   }
   lot_init_kernel<<<1, 1, 0, st>>>(S, (unsigned long long)keep, (unsigned long long)cap);
   const int agrid = std::max<long long>(1, std::min<long long>((n / 4 + 255) / 256, (long long)sms * 16));

@@ -765,3 +765,43 @@ def test_fused_lottery_step_compaction_path_bit_exact(ml, orc, kind, rho):
     ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
     ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
     assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
+
+
+@pytest.mark.parametrize("kind", ["normal", "zeros", "quantized", "ties"])
+@pytest.mark.parametrize("mode,value", [(2, 0.01), (2, 0.5), (2, 0.7), (1, 0.5)])
+def test_resident_lottery_step_bit_exact(ml, orc, kind, mode, value):
+    """The single-launch register-resident step (lottery.cu lot_resident_kernel, P <= ~1.2M): three
+    consecutive Moses steps (barrier / histogram state reused across calls, a second model
+    interleaved) — masks and weights bit-identical to xi -> partition -> step -> decay in fp32."""
+    dims = [1024, 1024, 8, 1]
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(int(value * 100) + mode + len(kind))
+    if kind == "quantized":
+        w = f32(rng.choice([-0.05, -0.02, 0.01, 0.03, 0.07], P))
+        g = f32(rng.choice([-2e-2, -5e-3, 1e-3, 4e-3, 1e-2], P))
+    else:
+        w = f32(rng.normal(0, 0.05, P))
+        g = f32(rng.normal(0, 1e-2, P))
+        if kind in ("zeros", "ties"):
+            g[rng.random(P) < 0.4] = 0.0
+    if kind == "ties" and mode == 2:
+        xi = np.abs(w.astype(np.float32) * g.astype(np.float32))
+        keep = orc.ratio_keep(value, P)
+        r = int(np.argpartition(-xi, keep - 1)[keep - 1])
+        slots = rng.choice(P, 300, replace=False)
+        w[slots], g[slots] = w[r], g[r]
+    other = ml.DeviceModel(ml_params([64, 64, 8, 1], f32(rng.normal(0, 1, ml.param_count([64, 64, 8, 1])))),
+                           ml.PREC_BF16, 16)
+    other.set_gradients(f32(rng.normal(0, 1, other.P)))
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    for it in range(3):
+        dm.set_gradients(g32.astype(np.float64))
+        mask = ml.lottery_step(dm, mode, value, it, 0.001, 0.01)
+        ml.lottery_step(other, 2, 0.5, it, 0.001, 0.01)
+        xi = orc.xi_scores(w32, g32, mode == 1)
+        ref_mask = orc.partition(xi, mode == 1, orc.RATIO if mode == 2 else orc.THRESHOLD, value)
+        assert np.array_equal(mask.transferable, ref_mask), it
+        w32, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+        w32 = orc.variant_decay(w32, ref_mask, 0.001, 0.01)
+        assert np.array_equal(dm.download().params, w32.astype(np.float64)), it
