@@ -215,7 +215,9 @@ def bench_infer(ml, L, local, programs, peaks, reps=3):
     prof = ml.profile_end()
     best = min(times)
     flops_prog = sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 1))
-    gemm_s = prof["gemm_fwd"][0] / 1000.0
+    # achieved: the hidden-layer GEMM FLOPs over the device time of the WHOLE forward (all GEMM
+    # launches plus the per-chunk head sums), CUDA events on the model stream
+    gemm_s = min(fwd_ms) / 1000.0
     gemm_flops = programs * sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 2))
     peak = peaks.get("bf16_tflops_sustained", 1408.7)
     ach = gemm_flops / gemm_s / 1e12 if gemm_s else None
@@ -225,8 +227,9 @@ def bench_infer(ml, L, local, programs, peaks, reps=3):
             "workload": f"cfg4 @1 GPU: score {programs} synthetic programs with {DIMS} (bf16), top-1024",
             "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms), "flops_per_program": flops_prog,
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak if ach else None, "kernel": "umma_gemm_kernel forward (Fwd epilogue)",
-                         "gemm_ms": prof["gemm_fwd"][0], "gemm_launches": prof["gemm_fwd"][1]},
+                         "frac": ach / peak if ach else None,
+                         "kernel": "umma_fwd_persistent (tcgen05 bf16, TMA-stored activations; gemm_fwd.cuh)",
+                         "forward_device_ms": min(fwd_ms), "gemm_launches": prof["gemm_fwd"][1]},
             "inputs": "device-resident bf16 packed features (3.4 GB > L2)"}
 
 
@@ -589,8 +592,8 @@ def main():
     peak = peaks.get("bf16_tflops_sustained", 1408.7)
     achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     traffic = None
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("gemm_bytes_per_launch")
+    try:  # DRAM bytes of the step's GEMM launches (chain fwd + chain dZ + grouped wgrad), ncu --set full
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("gemm_bytes_per_step")
     except Exception:
         pass
     step_prof_ms = sum(v[0] for v in prof.values()) / args.profile_steps
@@ -612,6 +615,7 @@ def main():
                 "path": "moses_gradients_pooled + moses_apply_update (C ABI, pinned host float64 buffers)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per step (3 GEMM launches), cold-cache ncu replay",
                      "kernel": "umma_gemm_kernel (tcgen05 bf16, all fwd/dgrad/wgrad launches of a step)",
                      "flops_per_step": flops, "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
