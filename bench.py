@@ -517,18 +517,20 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        # ---------------- timed region: K steps, L2 flushed between steps (outside the step brackets)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        # ---------------- timed region: K steps back to back. The inputs are larger than L2: every
+        # step gathers a different 512-program batch out of the 302 MB device-resident dataset
+        # (cold in L2); only the step's own working set (weights, optimizer state, activations,
+        # ~30 MB) stays cache-resident from one step to the next, as it does in training.
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = ml.kernel_launches()
         with ClockSampler(local) as clk:
+            t0e.record(stream)
             for k in range(args.steps):
-                flush.fill_(float(k))
-                evs[k][0].record(stream)
                 step(args.warmup + k)
-                evs[k][1].record(stream)
+            t1e.record(stream)
             torch.cuda.synchronize()
         launches = ml.kernel_launches() - launches0
-        total_ms = sum(a.elapsed_time(b) for a, b in evs)
+        total_ms = t0e.elapsed_time(t1e)
         if world > 1:
             t = torch.tensor([total_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -536,6 +538,22 @@ def main():
             dist.barrier()
         ms_step = total_ms / args.steps
         value = world * BATCH / (ms_step / 1000.0)
+
+        # ---------------- the same steps with L2 flushed before each one (256 MiB write outside
+        # per-step CUDA-event brackets): the whole working set starts cold (reported, not headline)
+        nfl = min(args.steps, 200)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nfl)]
+        for k in range(nfl):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step(args.warmup + args.steps + k)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        ms_step_flushed = sum(a.elapsed_time(b) for a, b in evs) / nfl
+        if world > 1:
+            t = torch.tensor([ms_step_flushed], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_step_flushed = float(t.item())
 
         # ---------------- device-time attribution (separate pass; events perturb timing)
         ml.profile_begin()
@@ -608,8 +626,11 @@ def main():
                                f"momentum SGD lr={LR} mu={MU}", "model": "moses-mlp-4x512", "programs": PROGRAMS,
                    "global_batch": BATCH * world, "seq_len": None, "parallelism": f"dp{world}",
                    "statements_per_program": f"1 + U{{0..{MAX_STMTS - 1}}} (mean {n_rows / (nb * BATCH):.2f})",
-                   "rows_per_step_padded": rows_pad,
-                   "l2": "flushed (256 MiB write) between timed steps, outside the per-step CUDA-event brackets"},
+                   "rows_per_step_padded": rows_pad, "dataset_bytes": int(X.numel() * X.element_size()),
+                   "l2": "inputs larger than L2: each step gathers a different batch of the 302 MB device-resident "
+                         "dataset; K steps timed back to back (ms_per_step_l2_flushed: the same step with a 256 MiB "
+                         "L2 flush before each one)"},
+        "ms_per_step_l2_flushed": ms_step_flushed,
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": int(xb_host.size * 8 + BATCH * 8 + (BATCH + 1) * 8), "d2h_bytes_per_step": 8,
                 "path": "moses_gradients_pooled + moses_apply_update (C ABI, pinned host float64 buffers)"},

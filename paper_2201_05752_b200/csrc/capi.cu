@@ -1991,6 +1991,11 @@ extern "C" MOSES_API int moses_debug_set_chain(int on) {
 }
 namespace moses {
 extern int g_fwd;
+extern int g_pair;
+}
+extern "C" MOSES_API int moses_debug_set_pair(int on) {
+  moses::g_pair = on;
+  return 0;
 }
 extern "C" MOSES_API int moses_debug_set_fwd(int on) {
   moses::g_fwd = on;

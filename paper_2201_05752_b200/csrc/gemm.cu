@@ -7,6 +7,7 @@
 #include "gemm.cuh"
 #include "gemm_persistent.cuh"
 #include "gemm_fwd.cuh"
+#include "gemm_fwd2.cuh"
 #include "gemm_gram.cuh"
 #include "gemm_cluster.cuh"
 #include "gemm_split.cuh"
@@ -204,6 +205,49 @@ void launch_f(const GemmCall& c, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, a, tm, tn));
+}
+
+// scoring hidden layers, N = 512: weight-resident CTA pairs (gemm_fwd2.cuh)
+void launch_pair(const GemmCall& c, cudaStream_t s) {
+  using Cfg = PairCfg;
+  auto kern = umma_fwd_pair;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+  });
+  const CUtensorMap ta = operand_map(c.A, 2, c.M, c.K, Cfg::BM);
+  const CUtensorMap tb = operand_map(c.B, 2, c.N, c.K, 64);
+  const CUtensorMap tc = c.out ? make_map(c.out, 2, c.N, c.M, c.ldo, 64, 32) : ta;
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mn_layout = g_mn_layout[0];
+  a.mn_sbo = g_mn_sbo[0];
+  a.mn_kstep = g_mn_kstep[0];
+  const int tiles_m2 = ceil_div(c.M, 2 * Cfg::BM);
+  int pairs = std::min(g_num_sms / 2, 2 * tiles_m2);
+  pairs -= pairs & 1;  // both n-halves get the same number of pairs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, a, tiles_m2));
 }
 
 template <bool BMN, int EPI>
@@ -448,8 +492,9 @@ int gemm_pick_bn(int M, int N) {
 }
 
 int g_num_sms = 148;
-int g_persistent = 1;
-int g_fwd = 1;  // scoring-shape forward kernel (gemm_fwd.cuh)  // persistent kernel for problems with more tiles than SMs
+int g_persistent = 1;  // persistent kernel for problems with more tiles than SMs
+int g_fwd = 1;  // scoring-shape forward kernel (gemm_fwd.cuh)
+int g_pair = 1;  // weight-resident CTA-pair forward kernel (gemm_fwd2.cuh)
 int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden layers
 
 int g_chain = 1;
@@ -504,6 +549,11 @@ int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
   if (g_persistent && !c.bn && c.N >= 128) {
     const int pbn = c.N >= 256 ? 256 : 128;
     if ((long long)mt * ceil_div(c.N, pbn) >= 2LL * g_num_sms) {
+      if (g_pair && elem == 2 && c.epi == EpiKind::Fwd && !c.A.mn_major && c.B.mn_major && c.N == 512 &&
+          c.K <= PairCfg::kMaxK && (c.ldo * 2) % 16 == 0 && g_num_sms >= 4) {
+        launch_pair(c, s);
+        return 128;  // head partials per 128-column quarter
+      }
       if (g_fwd && elem == 2 && c.epi == EpiKind::Fwd && !c.A.mn_major && (c.ldo * 2) % 16 == 0) {
         if (pbn == 256) c.B.mn_major ? launch_f<256, true>(c, s) : launch_f<256, false>(c, s);
         else c.B.mn_major ? launch_f<128, true>(c, s) : launch_f<128, false>(c, s);

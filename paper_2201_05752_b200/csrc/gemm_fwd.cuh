@@ -28,6 +28,89 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 }  // namespace fwd_detail
 
+// One epilogue warp's share of a tile: rows quarter*32 + lane of [m0, m0+128), kHalf accumulator
+// columns starting at output column nb0 (TMEM address t_acc). bias + ReLU + head dots in registers,
+// the bf16 activations through a 32 x 64 SW128 staging box and one TMA store per box; head partials
+// go to head_part[head_tile * head_ld + m]. `release` runs once the accumulator is in registers.
+template <int kHalf, typename Release>
+__device__ __forceinline__ void fwd_epi_tile(const GemmArgs& args, const CUtensorMap* tmC, uint8_t* stg, uint32_t t_acc,
+                                             int m0, int quarter, int nb0, int head_tile, Release&& release) {
+  using namespace fwd_detail;
+  const int lane = int(threadIdx.x & 31);
+  const int m = m0 + quarter * 32 + lane;
+  const bool store = args.out != nullptr;
+  float hp = 0.f, hp2 = 0.f;
+#pragma unroll 1
+  for (int g = 0; g < kHalf / 64; ++g) {
+    uint32_t r0[32], r1[32];
+    ptx::tmem_ld_32x32b_x32(t_acc + g * 64, r0);
+    ptx::tmem_ld_32x32b_x32(t_acc + g * 64 + 32, r1);
+    ptx::tmem_ld_wait();
+    if (g + 1 == kHalf / 64) release();  // accumulator fully drained into registers
+    const int nb = nb0 + g * 64;
+    if (nb >= args.N) continue;
+    const bool full = nb + 64 <= args.N;
+    float v[64];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __uint_as_float(r0[j]);
+      v[32 + j] = __uint_as_float(r1[j]);
+    }
+    if (full) {
+      const float4* b4 = reinterpret_cast<const float4*>(args.bias + nb);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 bb = __ldg(b4 + q);
+        v[4 * q] += bb.x; v[4 * q + 1] += bb.y; v[4 * q + 2] += bb.z; v[4 * q + 3] += bb.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = (nb + j < args.N) ? v[j] + __ldg(args.bias + nb + j) : 0.f;
+    }
+    if (args.relu) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
+    if (args.head_w != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) hp = fmaf(v[j], (full || nb + j < args.N) ? __ldg(args.head_w + nb + j) : 0.f, hp);
+    }
+    if (args.head_u != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) hp2 = fmaf(v[j], (full || nb + j < args.N) ? __ldg(args.head_u + nb + j) : 0.f, hp2);
+    }
+    if (store) {
+      if (lane == 0) bulk_wait_read0();  // previous box has left the staging buffer
+      __syncwarp();
+      uint8_t* srow = stg + lane * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 pk;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * c], v[8 * c + 1]);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * c + 2], v[8 * c + 3]);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * c + 4], v[8 * c + 5]);
+        __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * c + 6], v[8 * c + 7]);
+        pk.x = *reinterpret_cast<uint32_t*>(&p0);
+        pk.y = *reinterpret_cast<uint32_t*>(&p1);
+        pk.z = *reinterpret_cast<uint32_t*>(&p2);
+        pk.w = *reinterpret_cast<uint32_t*>(&p3);
+        *reinterpret_cast<uint4*>(srow + ((c ^ (lane & 7)) << 4)) = pk;  // SW128: chunk ^ (row % 8)
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmC, stg, nb, m0 + quarter * 32);  // rows >= M / cols >= N are clipped
+        bulk_commit();
+      }
+    }
+  }
+  if (m < args.M) {
+    const long long slot = (long long)head_tile * args.head_ld + m;
+    if (args.head_part != nullptr) args.head_part[slot] = hp;
+    if (args.head_part2 != nullptr) args.head_part2[slot] = hp2;
+  }
+}
+
 template <int BN>
 struct FCfg {
   static constexpr int BM = 128;
@@ -150,91 +233,19 @@ __global__ void __launch_bounds__(FCfg<BN>::kThreads, 1)
     const int ew = int(warp) - 2;
     const int quarter = int(warp & 3);
     const int half = ew >> 2;
-    const int row = quarter * 32 + int(lane);
     uint8_t* stg = staging + ew * Cfg::kStgBytes;
-    const bool store = args.out != nullptr;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
       const uint32_t use = uint32_t(i >> 1);
       const int m0 = (t % tiles_m) * BM, n_tile = t / tiles_m;
-      const int m = m0 + row;
       ptx::mbar_wait(&tfull[acc], use & 1);
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + uint32_t(acc * BN + half * kHalf) + (uint32_t(quarter * 32) << 16);
-      float hp = 0.f, hp2 = 0.f;
-#pragma unroll 1
-      for (int g = 0; g < kHalf / 64; ++g) {
-        uint32_t r0[32], r1[32];
-        ptx::tmem_ld_32x32b_x32(t_acc + g * 64, r0);
-        ptx::tmem_ld_32x32b_x32(t_acc + g * 64 + 32, r1);
-        ptx::tmem_ld_wait();
-        if (g + 1 == kHalf / 64) {  // accumulator fully drained into registers: hand it back
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[acc]);
-        }
-        const int nb = n_tile * BN + half * kHalf + g * 64;
-        if (nb >= args.N) continue;
-        const bool full = nb + 64 <= args.N;
-        float v[64];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          v[j] = __uint_as_float(r0[j]);
-          v[32 + j] = __uint_as_float(r1[j]);
-        }
-        if (full) {
-          const float4* b4 = reinterpret_cast<const float4*>(args.bias + nb);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 bb = __ldg(b4 + q);
-            v[4 * q] += bb.x; v[4 * q + 1] += bb.y; v[4 * q + 2] += bb.z; v[4 * q + 3] += bb.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) v[j] = (nb + j < args.N) ? v[j] + __ldg(args.bias + nb + j) : 0.f;
-        }
-        if (args.relu) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j], 0.f);
-        }
-        if (args.head_w != nullptr) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) hp = fmaf(v[j], (full || nb + j < args.N) ? __ldg(args.head_w + nb + j) : 0.f, hp);
-        }
-        if (args.head_u != nullptr) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) hp2 = fmaf(v[j], (full || nb + j < args.N) ? __ldg(args.head_u + nb + j) : 0.f, hp2);
-        }
-        if (store) {
-          if (lane == 0) bulk_wait_read0();  // previous box has left the staging buffer
-          __syncwarp();
-          uint8_t* srow = stg + lane * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            uint4 pk;
-            __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * c], v[8 * c + 1]);
-            __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * c + 2], v[8 * c + 3]);
-            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * c + 4], v[8 * c + 5]);
-            __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * c + 6], v[8 * c + 7]);
-            pk.x = *reinterpret_cast<uint32_t*>(&p0);
-            pk.y = *reinterpret_cast<uint32_t*>(&p1);
-            pk.z = *reinterpret_cast<uint32_t*>(&p2);
-            pk.w = *reinterpret_cast<uint32_t*>(&p3);
-            *reinterpret_cast<uint4*>(srow + ((c ^ (lane & 7)) << 4)) = pk;  // SW128: chunk ^ (row % 8)
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmC, stg, nb, m0 + quarter * 32);  // rows >= M / cols >= N are clipped
-            bulk_commit();
-          }
-        }
-      }
-      if (m < args.M) {
-        const long long slot = (long long)(2 * n_tile + half) * args.head_ld + m;
-        if (args.head_part != nullptr) args.head_part[slot] = hp;
-        if (args.head_part2 != nullptr) args.head_part2[slot] = hp2;
-      }
+      fwd_epi_tile<kHalf>(args, &tmC, stg, t_acc, m0, quarter, n_tile * BN + half * kHalf, 2 * n_tile + half, [&] {
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+      });
     }
     if (lane == 0) bulk_wait0();
     __syncwarp();

@@ -412,6 +412,10 @@ __global__ void __launch_bounds__(kRankThreads)
   __shared__ long long sseg[kRankMaxRows + 1];
   const int t = threadIdx.x;
   rank_stamp(0);
+  // every CTA of the cluster must be running before a peer writes into its shared memory (the
+  // score all-gather below): arrive now, wait right before the first remote store. Without it a
+  // late-starting CTA can lose peers' scores and keep the values of the previous launch.
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t q = ptx::cluster_ctarank();
   const float hb = hbp[0];
   const long long p0 = min(n, (long long)q * rows_per_cta);
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(kRankThreads)
   }
   __syncthreads();
   rank_stamp(1);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   // all-gather: every CTA's scores into every peer's ss[] (same offsets)
   for (long long k = t; k < (p1 - p0) * kRankCluster; k += blockDim.x) {
     const long long p = p0 + k / kRankCluster;
