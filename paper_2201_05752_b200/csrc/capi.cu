@@ -709,11 +709,14 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->mask = dalloc<uint8_t>(P);
     if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(P);
     else m->wtf = dalloc<float>(twin == 2 ? 2 * shadow_lo_offset(P) : P);
-    MOSES_CUDA(cudaMemset(m->w, 0, P * 4));
-    MOSES_CUDA(cudaMemset(m->mom, 0, P * 4));
-    MOSES_CUDA(cudaMemset(m->g, 0, P * 4));
-    if (m->wbf) MOSES_CUDA(cudaMemset(m->wbf, 0, P * 2));
-    if (m->wtf) MOSES_CUDA(cudaMemset(m->wtf, 0, 4 * (twin == 2 ? 2 * shadow_lo_offset(P) : P)));
+    // Every initialisation goes through the handle's (non-blocking) stream: a plain cudaMemset runs on
+    // the legacy stream, which does NOT order against m->st, and could land after the first upload or
+    // after the ones-column fill below (an intermittent wrong bias gradient, seen in bitwise tests).
+    MOSES_CUDA(cudaMemsetAsync(m->w, 0, P * 4, m->st));
+    MOSES_CUDA(cudaMemsetAsync(m->mom, 0, P * 4, m->st));
+    MOSES_CUDA(cudaMemsetAsync(m->g, 0, P * 4, m->st));
+    if (m->wbf) MOSES_CUDA(cudaMemsetAsync(m->wbf, 0, P * 2, m->st));
+    if (m->wtf) MOSES_CUDA(cudaMemsetAsync(m->wtf, 0, 4 * (twin == 2 ? 2 * shadow_lo_offset(P) : P), m->st));
     const int vec = 16 / m->esz;
     int maxw = 0;
     for (int l = 0; l < m->L; ++l) {
@@ -723,12 +726,12 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
       maxw = std::max(maxw, m->dims[l]);
       void* a = nullptr;
       MOSES_CUDA(cudaMalloc(&a, m->cap * ldl * m->esz * twin));
-      MOSES_CUDA(cudaMemset(a, 0, m->cap * ldl * m->esz * twin));
+      MOSES_CUDA(cudaMemsetAsync(a, 0, m->cap * ldl * m->esz * twin, m->st));
       m->act.push_back(a);
       void* d = nullptr;
       if (l > 0) {
         MOSES_CUDA(cudaMalloc(&d, m->cap * m->lddz[l] * m->esz * twin));
-        MOSES_CUDA(cudaMemset(d, 0, m->cap * m->lddz[l] * m->esz * twin));
+        MOSES_CUDA(cudaMemsetAsync(d, 0, m->cap * m->lddz[l] * m->esz * twin, m->st));
       }
       m->dz.push_back(d);
       // ones column of every activation buffer (never overwritten by the epilogues)
@@ -1520,6 +1523,8 @@ MOSES_API int moses_adversary_create(const double* replay, int64_t mrows, int32_
     MOSES_CUDA(cudaMemcpy(a->replay, tmp.data(), 4 * tmp.size(), cudaMemcpyHostToDevice));
     MOSES_CUDA(cudaMemset(a->u, 0, 4 * width));
     MOSES_CUDA(cudaMemset(a->c, 0, 4));
+    // the adversary is used on model streams (non-blocking: no implicit order with the legacy stream)
+    MOSES_CUDA(cudaDeviceSynchronize());
     *out = a.release();
   });
 }
@@ -1530,6 +1535,7 @@ MOSES_API int moses_adversary_get(moses_adversary_t a, double* w, int32_t width,
   return guarded([&] {
     if (width != a->W) fail(MOSES_ERR_DIM_MISMATCH, "width mismatch");
     std::vector<float> t(width + 1);
+    MOSES_CUDA(cudaDeviceSynchronize());  // model streams may still be updating the discriminator
     MOSES_CUDA(cudaMemcpy(t.data(), a->u, 4 * width, cudaMemcpyDeviceToHost));
     MOSES_CUDA(cudaMemcpy(t.data() + width, a->c, 4, cudaMemcpyDeviceToHost));
     for (int j = 0; j < width; ++j) w[j] = t[j];
@@ -1542,8 +1548,10 @@ MOSES_API int moses_adversary_set(moses_adversary_t a, const double* w, int32_t 
     std::vector<float> t(width + 1);
     for (int j = 0; j < width; ++j) t[j] = float(w[j]);
     t[width] = float(b);
+    MOSES_CUDA(cudaDeviceSynchronize());  // no model stream may still read the old discriminator
     MOSES_CUDA(cudaMemcpy(a->u, t.data(), 4 * width, cudaMemcpyHostToDevice));
     MOSES_CUDA(cudaMemcpy(a->c, t.data() + width, 4, cudaMemcpyHostToDevice));
+    MOSES_CUDA(cudaDeviceSynchronize());
   });
 }
 
