@@ -434,6 +434,7 @@ def main():
     ap.add_argument("--no-infer", action="store_true")
     ap.add_argument("--no-hbm", action="store_true")
     ap.add_argument("--no-finetune", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -451,9 +452,15 @@ def main():
 
     from paper_2201_05752_b200 import moseslab as ml
 
-    torch.cuda.set_device(local)
+    # --share-gpu: every rank on cuda:0 with the gloo backend — a functional check of the N > 1 path
+    # (sharding, gradient averaging, max-over-ranks timing) on a one-GPU box; never a bench number
+    dev = 0 if args.share_gpu else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = ml.lib()
     if L.moses_device_check() != 0:
         raise SystemExit("moses: " + L.moses_last_error().decode())
@@ -493,10 +500,17 @@ def main():
     ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, BATCH,
                                              rows_pad, LR, MU, int(world == 1)))
 
+    def grad_avg(t):  # NCCL averages in the collective; gloo (--share-gpu check) has no AVG
+        if args.share_gpu:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            t.div_(world)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.AVG)
+
     def step(b):
         ml._ck(L.moses_train_graph_launch(dm.h, 1))
         if world > 1:
-            dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+            grad_avg(grads)
             ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
 
     # host copies of one batch for the eager profiling pass and the end-to-end leg
@@ -508,7 +522,7 @@ def main():
         ml._ck(L.moses_gradients_pooled(dm.h, xb_host.ctypes.data, xb_host.shape[0], DIMS[0], ob_host.ctypes.data,
                                         BATCH, yb_host.ctypes.data, None))
         if world > 1:
-            dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+            grad_avg(grads)
         ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
 
     with torch.cuda.stream(stream):
@@ -523,7 +537,7 @@ def main():
         # ~30 MB) stays cache-resident from one step to the next, as it does in training.
         t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = ml.kernel_launches()
-        with ClockSampler(local) as clk:
+        with ClockSampler(dev) as clk:
             t0e.record(stream)
             for k in range(args.steps):
                 step(args.warmup + k)
@@ -573,7 +587,7 @@ def main():
             ml._ck(L.moses_gradients_pooled(dm.h, x_host.data_ptr(), x_host.shape[0], DIMS[0], o_host.data_ptr(),
                                             BATCH, y_host.data_ptr(), C.byref(loss)))
             if world > 1:
-                dist.all_reduce(grads, op=dist.ReduceOp.AVG)
+                grad_avg(grads)
             L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
 
         for _ in range(3):
