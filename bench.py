@@ -164,73 +164,97 @@ def run_reference(args, rank, world):
     del steps_s
 
 
-def bench_infer(ml, L, local, programs, peaks, reps=3):
-    """cfg4 at one GPU: score a device-resident pool of `programs` synthetic programs with the
-    4x512 model and select the top-1024 (score desc, index asc). programs/s and the forward
-    GEMM roofline; features generated on device (PCIe would otherwise dominate)."""
+def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
+    """cfg4: score a pool of `programs` synthetic programs with the 4x512 model and select the
+    global top-1024 (score desc, index asc). N > 1: the pool is split into contiguous program
+    ranges, one per rank (strong scaling: the pool is fixed); each rank scores and top-k's its shard,
+    the (score, global index) winners are all-gathered and merged (distributed.py) — the only
+    exchange. programs/s = pool / max over ranks of the pass time; the forward GEMM roofline is
+    per GPU. Features are generated on device (PCIe would otherwise dominate)."""
     import ctypes as C
 
+    import numpy as np
+
     import torch
+    import torch.distributed as dist
+
+    from paper_2201_05752_b200.distributed import gather_merge_topk, shard_range
 
     chunk = 65536
+    k = 1024
+    lo, hi = shard_range(programs, rank, world)
+    n_local = hi - lo
     params = ml.init_random(DIMS, SEED_MODEL, strict=False)
     dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=chunk)
     ld = dm.packed_ld
-    X = torch.empty((programs, ld), dtype=torch.bfloat16, device="cuda")
-    S = torch.empty(programs, dtype=torch.float32, device="cuda")
-    assert L.moses_synth_features_device(SEED_DATA + 100, 0, programs, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    X = torch.empty((n_local, ld), dtype=torch.bfloat16, device="cuda")
+    S = torch.empty(n_local, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(SEED_DATA + 100, lo, n_local, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
     torch.cuda.synchronize()
-    idx = (C.c_int64 * 1024)()
+    idx = (C.c_int64 * k)()
     sp = C.c_void_p()
     L.moses_model_stream(dm.h, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
 
-    def run():
-        rc = L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
-        if rc:
-            raise RuntimeError(L.moses_last_error().decode())
+    def one_pass():
+        """forward (device-timed) + local top-k + global merge; returns (seconds, forward ms, winners)"""
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-        rc = L.moses_topk_device(S.data_ptr(), programs, 1024, idx)
-        if rc:
-            raise RuntimeError(L.moses_last_error().decode())
-
-    run()
-    times, fwd_ms = [], []
-    with torch.cuda.stream(stream):
-        for _ in range(reps):
-            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
             a.record(stream)
-            rc = L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
+            ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, n_local, S.data_ptr()))
             b.record(stream)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            L.moses_topk_device(S.data_ptr(), programs, 1024, idx)
-            t_topk = time.perf_counter() - t0
-            times.append(a.elapsed_time(b) / 1000.0 + t_topk)
-            fwd_ms.append(a.elapsed_time(b))
+        torch.cuda.synchronize()
+        kk = min(k, n_local)
+        ml._ck(L.moses_topk_device(S.data_ptr(), n_local, kk, idx))
+        li = np.array(idx[:kk], dtype=np.int64)
+        if world > 1:
+            ls = S[torch.from_numpy(li).cuda()].cpu().numpy()
+            win = gather_merge_topk(ls, li + lo, k)
+        else:
+            win = li
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        return dt, a.elapsed_time(b), win
+
+    one_pass()
+    times, fwd_ms = [], []
+    for _ in range(reps):
+        dt, fm, win = one_pass()
+        times.append(dt)
+        fwd_ms.append(fm)
     ml.profile_begin()
     with torch.cuda.stream(stream):
-        L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, programs, S.data_ptr())
+        L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, n_local, S.data_ptr())
         torch.cuda.synchronize()
     prof = ml.profile_end()
     best = min(times)
     flops_prog = sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 1))
     # achieved: the hidden-layer GEMM FLOPs over the device time of the WHOLE forward (all GEMM
-    # launches plus the per-chunk head sums), CUDA events on the model stream
+    # launches plus the per-chunk head sums), CUDA events on the model stream (this rank)
     gemm_s = min(fwd_ms) / 1000.0
-    gemm_flops = programs * sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 2))
+    gemm_flops = n_local * sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 2))
     peak = peaks.get("bf16_tflops_sustained", 1408.7)
     ach = gemm_flops / gemm_s / 1e12 if gemm_s else None
     del X
     torch.cuda.empty_cache()
     return {"metric": "cost-model programs/sec (infer)", "value": programs / best, "unit": "programs/s",
-            "workload": f"cfg4 @1 GPU: score {programs} synthetic programs with {DIMS} (bf16), top-1024",
+            "workload": f"cfg4: score {programs} synthetic programs with {DIMS} (bf16), global top-{k}, "
+                        f"{world} GPU(s), contiguous program shards",
+            "scaling": "strong", "programs_per_gpu": n_local, "first_winners": [int(v) for v in win[:4]],
             "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms), "flops_per_program": flops_prog,
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak if ach else None,
-                         "kernel": "umma_fwd_persistent (tcgen05 bf16, TMA-stored activations; gemm_fwd.cuh)",
+                         "kernel": "umma_fwd_pair (tcgen05 cta_group::2, weight-resident; gemm_fwd2.cuh)",
                          "forward_device_ms": min(fwd_ms), "gemm_launches": prof["gemm_fwd"][1]},
-            "inputs": "device-resident bf16 packed features (3.4 GB > L2)"}
+            "inputs": "device-resident bf16 packed features (3.4 GB over all GPUs > L2)",
+            "timing": "wall clock per pass (device forward + local top-k + all-gather merge), max over ranks"}
 
 
 def bench_hbm_kernels(ml, L, peaks):
@@ -607,6 +631,15 @@ def main():
             e2e_s = float(t.item())
     e2e_value = world * BATCH * e2e_steps / e2e_s
 
+    infer = None
+    if not args.no_infer:  # every rank: the candidate pool is sharded across the GPUs
+        peaks0 = {}
+        try:
+            peaks0 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        infer = bench_infer(ml, L, args.infer_programs, peaks0, rank, world)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -660,8 +693,8 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if not args.no_infer:
-        line["infer"] = bench_infer(ml, L, local, args.infer_programs, peaks)
+    if infer is not None:
+        line["infer"] = infer
     if not args.no_hbm:
         line["hbm_kernels"] = bench_hbm_kernels(ml, L, peaks)
     if not args.no_finetune:
