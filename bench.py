@@ -447,6 +447,66 @@ def bench_finetune(ml, L, peaks, reps=20):
     return out
 
 
+def bench_search(ml, L, peaks):
+    """the scorer's input path on the device — enumerate a 10.2M-config knob
+    space (6 knobs; space.cpp:168-191 order), encode the 16-d features (space.cpp:140-159) straight
+    into packed bf16 model rows plus FNV-1a hashes (space.cpp:193-197), score with the reference's
+    {16,512,512,1} model and select the top-1024. No host features, no PCIe."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
+
+    knobs = [("tile_x", [1 << i for i in range(16)]), ("tile_y", [1 << i for i in range(16)]),
+             ("unroll", [0, 1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 128, 256, 512]),
+             ("vectorize", [1 << i for i in range(8)]), ("parallel", [1 << i for i in range(13)]),
+             ("split", list(range(1, 25)))]
+    n = int(np.prod([len(d) for _, d in knobs]))
+    task = (2.0, 8.0, 9.0, 5.0)
+    dims = [16, 512, 512, 1]
+    dm = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16, max_rows=65536)
+    ld = dm.packed_ld
+    F = torch.empty((n, ld), dtype=torch.bfloat16, device="cuda")
+    Hh = torch.empty(n, dtype=torch.int64, device="cuda")
+    S = torch.empty(n, dtype=torch.float32, device="cuda")
+    idx = (C.c_int64 * 1024)()
+
+    def encode():
+        ml.encode_configs_device(task, knobs, 0, n, ml.DTYPE_BF16, C.c_void_p(F.data_ptr()), ld, dims[0],
+                                 C.c_void_p(Hh.data_ptr()))
+
+    def score():
+        ml._ck(L.moses_predict_device(dm.h, C.c_void_p(F.data_ptr()), ml.DTYPE_BF16, ld, n, C.c_void_p(S.data_ptr())))
+        torch.cuda.synchronize()
+        ml._ck(L.moses_topk_device(C.c_void_p(S.data_ptr()), n, 1024, idx))
+
+    encode()
+    score()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    encode()
+    b.record()
+    torch.cuda.synchronize()
+    enc_ms = a.elapsed_time(b)
+    t0 = time.perf_counter()
+    encode()
+    score()
+    total = time.perf_counter() - t0
+    wbytes = n * (ld * 2 + 8)
+    hbm = peaks.get("hbm_gbs", 6534.1)
+    out = {"configs": n, "knobs": len(knobs), "model": dims, "encode_ms": enc_ms,
+           "encode_roofline": {"bound": "hbm", "achieved": wbytes / (enc_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                               "frac": wbytes / (enc_ms / 1e3) / 1e9 / hbm,
+                               "algorithmic_bytes": wbytes, "note": "packed bf16 rows + u64 hashes written"},
+           "pipeline_ms": total * 1e3, "configs_per_s": n / total,
+           "pipeline": "encode_configs (device) -> predict (tcgen05) -> top-1024, wall clock"}
+    del F, Hh, S
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -458,6 +518,7 @@ def main():
     ap.add_argument("--no-infer", action="store_true")
     ap.add_argument("--no-hbm", action="store_true")
     ap.add_argument("--no-finetune", action="store_true")
+    ap.add_argument("--no-search", action="store_true")
     ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
     args = ap.parse_args()
@@ -699,6 +760,8 @@ def main():
         line["hbm_kernels"] = bench_hbm_kernels(ml, L, peaks)
     if not args.no_finetune:
         line["finetune"] = bench_finetune(ml, L, peaks)
+    if not args.no_search:
+        line["search"] = bench_search(ml, L, peaks)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(15.0)
     print(json.dumps(line), flush=True)

@@ -36,7 +36,9 @@ extern "C" {
 
 enum {
   MOSES_OK = 0,
+  MOSES_ERR_INVALID_TASK = 1,          /* ErrorCode::InvalidTask */
   MOSES_ERR_INVALID_CONFIG = 2,        /* ErrorCode::InvalidConfig */
+  MOSES_ERR_SPACE_TOO_LARGE = 3,       /* ErrorCode::SpaceTooLarge */
   MOSES_ERR_BAD_DIMS = 5,              /* ErrorCode::BadDims */
   MOSES_ERR_DIM_MISMATCH = 6,          /* ErrorCode::DimMismatch */
   MOSES_ERR_SHAPE_MISMATCH = 7,        /* ErrorCode::ShapeMismatch */
@@ -57,7 +59,7 @@ enum {
  * fp32-level accuracy (the <= 1e-5 parity path); host-API inputs only, no training graphs. */
 enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1, MOSES_PREC_FP32 = 2 };
 enum { MOSES_MODE_THRESHOLD = 1, MOSES_MODE_RATIO = 2 };        /* PartitionMode, "MOSK" mode byte */
-enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1 };
+enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1, MOSES_DTYPE_F64 = 2 };
 
 typedef struct moses_model* moses_model_t;
 typedef struct moses_adversary* moses_adversary_t;
@@ -213,6 +215,19 @@ MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t 
    the source/target penultimate activations already live in HBM. tcgen05 kind::tf32 Gram tiles. */
 MOSES_API int moses_mmd2_device(const float* xs, int64_t m, const float* xt, int64_t n, int32_t width, int64_t ld,
                                 double sigma, double* out);
+
+/* ------------------------------------------------------------------ candidate generation */
+/* Configurations [first, first+n) of a task's knob space in enumerate_configs order (space.cpp:168-191,
+ * last knob fastest), on the device: encode_features rows (space.cpp:140-159; D >= 10 columns, entries
+ * >= 10 zero, 1.0 at column D when ld > D) in dtype (F32 / BF16 / F64) with row stride ld, FNV-1a
+ * config_hash values (space.cpp:193-197) and optionally the knob values (n x n_knobs). task4 =
+ * {work_gflops, bytes_per_unit, ideal_log2_tiles, ideal_log2_unroll} (space.hpp:24-31); roles[i] =
+ * template knob of knob i (0 tile_x, 1 tile_y, 2 unroll, 3 vectorize, 4 parallel, -1 other; knob_view
+ * matches by name, space.cpp:123-138). Any output pointer may be NULL. Default stream. */
+MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                         const int32_t* roles, int32_t n_knobs, uint64_t first, int64_t n,
+                                         int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
+                                         int64_t* values_dev);
 
 /* ------------------------------------------------------------------ synthetic TenSet-shaped data (bench) */
 /* Rows [row0, row0+n) of the keyed SplitMix64 generator, written in the packed layout. */

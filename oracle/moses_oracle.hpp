@@ -750,6 +750,50 @@ inline int synth_stmts(std::uint64_t seed, std::uint64_t prog, int max_stmts) {
   return 1 + int(r.below(std::uint64_t(max_stmts)));
 }
 
+// ---------------------------------------------------------------- knob space (space.cpp)
+// Task descriptors (space.hpp:24-31) and the knob-space helpers the scorer's inputs come from.
+struct TaskDesc {
+  double work_gflops, bytes_per_unit, ideal_log2_tiles, ideal_log2_unroll;
+};
+// roles[i]: which template knob knob i is (knob_view matches by name, space.cpp:123-138):
+// 0 tile_x, 1 tile_y, 2 unroll, 3 vectorize, 4 parallel, -1 none of them.
+// encode_features (space.cpp:140-159): entries 0..9 live, 10..15 zero.
+inline void encode_features(const TaskDesc& t, const std::int64_t* values, const int* roles, int nk, double* f) {
+  std::int64_t kv[5] = {1, 1, 0, 1, 1};  // knob_view fallbacks (space.cpp:132-136)
+  for (int i = 0; i < nk; ++i)
+    if (roles[i] >= 0 && roles[i] < 5) kv[roles[i]] = values[i];
+  const double tx = double(kv[0]), ty = double(kv[1]), un = double(kv[2]);
+  const double footprint = t.bytes_per_unit * tx * ty * std::max<double>(1.0, un);
+  for (int j = 0; j < 16; ++j) f[j] = 0.0;
+  f[0] = std::log2(tx) / 6.0;
+  f[1] = std::log2(ty) / 6.0;
+  f[2] = std::log2(1.0 + un) / 10.0;
+  f[3] = std::log2(double(kv[3])) / 4.0;
+  f[4] = std::log2(double(kv[4])) / 8.0;
+  f[5] = std::log2(tx * ty) / 12.0;
+  f[6] = std::log2(footprint) / 24.0;
+  f[7] = std::clamp(std::log10(t.work_gflops) / 3.0, 0.0, 1.0);
+  f[8] = t.ideal_log2_tiles / 16.0;
+  f[9] = t.ideal_log2_unroll / 10.0;
+}
+// enumerate_configs (space.cpp:168-191): lexicographic, last knob fastest -> config `index`
+inline void decode_config(std::uint64_t index, const std::int64_t* domains, const int* sizes, int nk,
+                          std::int64_t* values) {
+  int off[16];
+  int o = 0;
+  for (int i = 0; i < nk; ++i) { off[i] = o; o += sizes[i]; }
+  for (int i = nk - 1; i >= 0; --i) {
+    values[i] = domains[off[i] + int(index % std::uint64_t(sizes[i]))];
+    index /= std::uint64_t(sizes[i]);
+  }
+}
+// config_hash (space.cpp:193-197): FNV-1a over each value's 8 little-endian bytes
+inline std::uint64_t config_hash(const std::int64_t* values, int nk) {
+  KeyBuilder k;
+  for (int i = 0; i < nk; ++i) k.add(std::uint64_t(values[i]));
+  return k.h;
+}
+
 // ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:267-325)
 inline void put_u32(std::string& o, std::uint32_t v) { for (int i = 0; i < 4; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }
 inline void put_u64(std::string& o, std::uint64_t v) { for (int i = 0; i < 8; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }

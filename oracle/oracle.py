@@ -108,6 +108,8 @@ def lib():
         _lib.orc_gradients_pooled_f64.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                                   C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib.orc_synth_features.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_int, C.c_void_p]
+        _lib.orc_encode_configs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_uint64,
+                                            C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_synth_labels.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_void_p]
         _lib.orc_synth_offsets.argtypes = [C.c_uint64, C.c_longlong, C.c_int, C.c_void_p]
         _lib.orc_serialize.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong]
@@ -387,3 +389,28 @@ def train_step_f64(dims, w, mom, x, y, lr=0.001, mu=0.9, threads=1):
     _check(lib().orc_train_step_f64(_p(d), len(d), _p(w), _p(mom), _p(np.ascontiguousarray(x)),
                                     _p(np.ascontiguousarray(y)), x.shape[0], lr, mu, _p(loss), threads))
     return float(loss[0])
+
+
+# ---------------------------------------------------------------- knob space (space.cpp:28-197)
+TEMPLATE_ROLES = {"tile_x": 0, "tile_y": 1, "unroll": 2, "vectorize": 3, "parallel": 4}
+
+
+def default_knob_template():
+    """space.cpp:28-36 — (name, domain) of the 5 template knobs."""
+    return [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
+            ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
+
+
+def encode_configs(task, knobs, first, n):
+    """encode_features + config_hash over configs [first, first+n) of enumerate_configs' order.
+    task = (work_gflops, bytes_per_unit, ideal_log2_tiles, ideal_log2_unroll); knobs = [(name, domain)].
+    Returns (features n x 16 float64, hashes uint64, values n x nk int64)."""
+    t = np.ascontiguousarray(task, dtype=np.float64)
+    dom = np.ascontiguousarray([v for _, d in knobs for v in d], dtype=np.int64)
+    sizes = np.ascontiguousarray([len(d) for _, d in knobs], dtype=np.int32)
+    roles = np.ascontiguousarray([TEMPLATE_ROLES.get(k, -1) for k, _ in knobs], dtype=np.int32)
+    f = np.zeros((n, 16))
+    h = np.zeros(n, dtype=np.uint64)
+    v = np.zeros((n, len(knobs)), dtype=np.int64)
+    _check(lib().orc_encode_configs(_p(t), _p(dom), _p(sizes), _p(roles), len(knobs), first, n, _p(f), _p(h), _p(v)))
+    return f, h, v

@@ -262,3 +262,21 @@ ORC int orc_train_step_f64(const int* dims, int nd, double* w, double* mom, cons
     std::memcpy(mom, p.mom.data(), sizeof(double) * p.mom.size());
   });
 }
+
+// ---- knob space (space.cpp:140-197): configs [first, first+n) of the lexicographic enumeration
+ORC int orc_encode_configs(const double* task4, const std::int64_t* domains, const int* sizes, const int* roles, int nk,
+                           std::uint64_t first, std::int64_t n, double* feats, std::uint64_t* hashes,
+                           std::int64_t* values_out) {
+  return guarded([&] {
+    if (nk <= 0 || nk > 16) throw std::runtime_error("knob count out of range");
+    const TaskDesc t{task4[0], task4[1], task4[2], task4[3]};
+    std::int64_t v[16];
+    for (std::int64_t i = 0; i < n; ++i) {
+      decode_config(first + std::uint64_t(i), domains, sizes, nk, v);
+      if (feats) encode_features(t, v, roles, nk, feats + i * 16);
+      if (hashes) hashes[i] = config_hash(v, nk);
+      if (values_out)
+        for (int k = 0; k < nk; ++k) values_out[i * nk + k] = v[k];
+    }
+  });
+}

@@ -1772,6 +1772,19 @@ MOSES_API int moses_mmd2_device(const float* xs, int64_t m, const float* xt, int
   });
 }
 
+MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                         const int32_t* roles, int32_t n_knobs, uint64_t first, int64_t n,
+                                         int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
+                                         int64_t* values_dev) {
+  return guarded([&] {
+    if (dtype != MOSES_DTYPE_F32 && dtype != MOSES_DTYPE_BF16 && dtype != MOSES_DTYPE_F64)
+      fail(MOSES_ERR_INVALID_ARG, "unknown dtype");
+    note_launch(encode_configs(task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs, first,
+                               n, dtype, feat_dev, ld, D, reinterpret_cast<unsigned long long*>(hash_dev),
+                               reinterpret_cast<long long*>(values_dev), nullptr));
+  });
+}
+
 MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype, void* dst,
                                           int64_t ld) {
   return guarded([&] {

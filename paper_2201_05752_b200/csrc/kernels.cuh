@@ -157,4 +157,9 @@ template <typename T>
 void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st);
 void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st);
 
+// knob-space candidate generation (space.cu); out_kind 0 f32, 1 bf16, 2 f64
+int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
+                   unsigned long long* hash, long long* values_out, cudaStream_t st);
+
 }  // namespace moses

@@ -1,0 +1,240 @@
+// space.cu — candidate generation on the device: the knob-space helpers
+// of the reference's scorer input path, so a candidate pool never crosses PCIe.
+//
+//   enumerate_configs (space.cpp:168-191): config `index` of the lexicographic enumeration, last
+//     knob fastest = the mixed-radix digits of the index over the knob domain sizes;
+//   encode_features (space.cpp:140-159): the 16-d feature row (10 live entries, 6 zero) in double,
+//     rounded once to the model's operand type and written as a packed model row;
+//   config_hash (space.cpp:193-197): FNV-1a over each value's 8 little-endian bytes — the identity
+//     select_batch dedups on (search.cpp:82-95).
+// One thread per configuration; the task-level entries (f7..f9) are computed on the host exactly
+// like the reference (std::log10 / std::clamp) and passed in.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace moses {
+
+constexpr int kSpaceMaxKnobs = 8;
+constexpr int kSpaceMaxValues = 256;
+
+struct SpaceArgs {
+  double bytes_per_unit;
+  double f7, f8, f9;  // task-level entries
+  int nk;
+  int sizes[kSpaceMaxKnobs], offs[kSpaceMaxKnobs], roles[kSpaceMaxKnobs];
+  long long domains[kSpaceMaxValues];
+  // Table path: f0..f6 are functions of the template knobs' domain indices only, so the host
+  // evaluates them once per value (the reference's own expressions, std::log2 in double) and the
+  // kernel gathers: t[r] = table of role r (f0..f4), t5 over (tile_x, tile_y), t6 over
+  // (tile_x, tile_y, unroll). role_knob[r] = knob index of role r (-1: absent, index 0).
+  const double* tab;  // null: evaluate on the device
+  int tab_off[7], role_knob[5], role_size[5];
+};
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T cvt_out(double v);
+template <>
+__device__ __forceinline__ float cvt_out<float>(double v) { return float(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(double v) { return __float2bfloat16_rn(float(v)); }
+template <>
+__device__ __forceinline__ double cvt_out<double>(double v) { return v; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) encode_configs_kernel(const __grid_constant__ SpaceArgs a,
+                                                             unsigned long long first, long long n, T* __restrict__ feat,
+                                                             long long ld, int D, unsigned long long* __restrict__ hash,
+                                                             long long* __restrict__ values_out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long idx = first + (unsigned long long)i;
+    long long v[kSpaceMaxKnobs];
+    unsigned digit[kSpaceMaxKnobs];
+    if (idx >> 32) {  // mixed-radix digits, last knob fastest
+#pragma unroll
+      for (int k = kSpaceMaxKnobs - 1; k >= 0; --k) {
+        digit[k] = 0;
+        if (k >= a.nk) continue;
+        const unsigned long long s = (unsigned long long)a.sizes[k];
+        digit[k] = unsigned(idx % s);
+        idx /= s;
+      }
+    } else {  // 32-bit division is several times cheaper
+      unsigned i32 = unsigned(idx);
+#pragma unroll
+      for (int k = kSpaceMaxKnobs - 1; k >= 0; --k) {
+        digit[k] = 0;
+        if (k >= a.nk) continue;
+        const unsigned s = unsigned(a.sizes[k]);
+        digit[k] = i32 % s;
+        i32 /= s;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kSpaceMaxKnobs; ++k) v[k] = k < a.nk ? a.domains[a.offs[k] + int(digit[k])] : 0;
+    long long kv[5] = {1, 1, 0, 1, 1};  // knob_view fallbacks (space.cpp:132-136)
+    unsigned seen = 0;                    // find_knob takes the first knob of a name
+    unsigned long long h = 0xcbf29ce484222325ull;
+#pragma unroll
+    for (int k = 0; k < kSpaceMaxKnobs; ++k) {
+      if (k >= a.nk) continue;
+      const int r = a.roles[k];
+      if (r >= 0 && r < 5 && !(seen & (1u << r))) {
+        kv[r] = v[k];
+        seen |= 1u << r;
+      }
+      const unsigned long long u = (unsigned long long)v[k];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        h ^= (u >> (8 * b)) & 0xffull;
+        h *= 0x100000001b3ull;
+      }
+      if (values_out) values_out[i * a.nk + k] = v[k];
+    }
+    if (hash) hash[i] = h;
+    if (feat == nullptr) continue;
+    double f[10];
+    if (a.tab != nullptr) {
+      int ri[5];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        const int k = a.role_knob[r];
+        ri[r] = 0;
+#pragma unroll
+        for (int kk = 0; kk < kSpaceMaxKnobs; ++kk)
+          if (kk == k) ri[r] = int(digit[kk]);
+      }
+#pragma unroll
+      for (int r = 0; r < 5; ++r) f[r] = __ldg(a.tab + a.tab_off[r] + ri[r]);
+      const int txy = ri[0] * a.role_size[1] + ri[1];
+      f[5] = __ldg(a.tab + a.tab_off[5] + txy);
+      f[6] = __ldg(a.tab + a.tab_off[6] + txy * a.role_size[2] + ri[2]);
+    } else {
+      const double tx = double(kv[0]), ty = double(kv[1]), un = double(kv[2]);
+      const double footprint = a.bytes_per_unit * tx * ty * fmax(1.0, un);
+      f[0] = log2(tx) / 6.0;
+      f[1] = log2(ty) / 6.0;
+      f[2] = log2(1.0 + un) / 10.0;
+      f[3] = log2(double(kv[3])) / 4.0;
+      f[4] = log2(double(kv[4])) / 8.0;
+      f[5] = log2(tx * ty) / 12.0;
+      f[6] = log2(footprint) / 24.0;
+    }
+    f[7] = a.f7;
+    f[8] = a.f8;
+    f[9] = a.f9;
+    T* row = feat + i * ld;
+    if constexpr (sizeof(T) == 2) {
+      if (ld % 8 == 0 && ld <= 32 && D + 1 <= ld && ((reinterpret_cast<uintptr_t>(feat) & 15) == 0)) {  // 16-B rows
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += 8) {  // ld <= 32 on this path
+          if (c0 >= ld) break;
+          uint4 pk;
+          T* pe = reinterpret_cast<T*>(&pk);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int j = c0 + q;
+            pe[q] = cvt_out<T>(j < 10 ? f[j < 10 ? j : 0] : (j == D ? 1.0 : 0.0));  // zero beyond D
+          }
+          *reinterpret_cast<uint4*>(row + c0) = pk;
+        }
+        continue;
+      }
+    }
+    for (int j = 0; j < D; ++j) row[j] = cvt_out<T>(j < 10 ? f[j] : 0.0);
+    if (ld > D) row[D] = cvt_out<T>(1.0);  // the packed layout's constant column (gradients' bias row)
+  }
+}
+
+}  // namespace
+
+int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
+                   unsigned long long* hash, long long* values_out, cudaStream_t st) {
+  if (nk <= 0 || nk > kSpaceMaxKnobs) fail(MOSES_ERR_INVALID_ARG, "knob count must lie in [1, 8]");
+  SpaceArgs a{};
+  a.nk = nk;
+  int off = 0;
+  unsigned long long space = 1;
+  for (int k = 0; k < nk; ++k) {
+    if (sizes[k] <= 0) fail(MOSES_ERR_INVALID_TASK, "knob domain must be non-empty");
+    for (int j = 1; j < sizes[k]; ++j)
+      if (domains[off + j - 1] >= domains[off + j]) fail(MOSES_ERR_INVALID_TASK, "knob domain must be strictly increasing");
+    a.sizes[k] = sizes[k];
+    a.offs[k] = off;
+    a.roles[k] = roles[k];
+    off += sizes[k];
+    if (off > kSpaceMaxValues) fail(MOSES_ERR_INVALID_ARG, "knob domains exceed 256 values in total");
+    if (space > ~0ull / (unsigned long long)sizes[k]) fail(MOSES_ERR_SPACE_TOO_LARGE, "knob space overflows 64 bits");
+    space *= (unsigned long long)sizes[k];
+  }
+  if (n < 0 || first > space || (unsigned long long)n > space - first)
+    fail(MOSES_ERR_SHAPE_MISMATCH, "config range exceeds the knob space");
+  std::copy(domains, domains + off, a.domains);
+  a.bytes_per_unit = task4[1];
+  a.f7 = std::clamp(std::log10(task4[0]) / 3.0, 0.0, 1.0);  // space.cpp:154
+  a.f8 = task4[2] / 16.0;
+  a.f9 = task4[3] / 10.0;
+  if (feat != nullptr && (D < 10 || ld < D)) fail(MOSES_ERR_INVALID_ARG, "feature rows need D >= 10 and ld >= D");
+  if (n == 0) return 0;
+  // per-value tables of f0..f6 (host, the reference's expressions in double)
+  std::vector<double> dom_r[5];
+  const long long fallback[5] = {1, 1, 0, 1, 1};  // knob_view fallbacks (space.cpp:132-136)
+  for (int r = 0; r < 5; ++r) {
+    a.role_knob[r] = -1;
+    for (int k = 0; k < nk; ++k)
+      if (roles[k] == r && a.role_knob[r] < 0) a.role_knob[r] = k;
+    if (a.role_knob[r] >= 0)
+      for (int j = 0; j < sizes[a.role_knob[r]]; ++j) dom_r[r].push_back(double(domains[a.offs[a.role_knob[r]] + j]));
+    else
+      dom_r[r].push_back(double(fallback[r]));
+    a.role_size[r] = int(dom_r[r].size());
+  }
+  const size_t n5 = dom_r[0].size() * dom_r[1].size(), n6 = n5 * dom_r[2].size();
+  std::vector<double> tab;
+  if (n6 <= (1u << 20)) {
+    auto put = [&](int slot) { a.tab_off[slot] = int(tab.size()); };
+    const double div[5] = {6.0, 6.0, 10.0, 4.0, 8.0};
+    for (int r = 0; r < 5; ++r) {
+      put(r);
+      for (double x : dom_r[r]) tab.push_back(r == 2 ? std::log2(1.0 + x) / div[r] : std::log2(x) / div[r]);
+    }
+    put(5);
+    for (double tx : dom_r[0])
+      for (double ty : dom_r[1]) tab.push_back(std::log2(tx * ty) / 12.0);
+    put(6);
+    for (double tx : dom_r[0])
+      for (double ty : dom_r[1])
+        for (double un : dom_r[2]) tab.push_back(std::log2(task4[1] * tx * ty * std::max<double>(1.0, un)) / 24.0);
+  }
+  static thread_local double* dtab = nullptr;
+  static thread_local size_t dtab_n = 0;
+  if (!tab.empty()) {
+    if (tab.size() > dtab_n) {
+      if (dtab) cudaFree(dtab);
+      MOSES_CUDA(cudaMalloc(&dtab, tab.size() * sizeof(double)));
+      dtab_n = tab.size();
+    }
+    MOSES_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    a.tab = dtab;
+  }
+  const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
+  if (out_kind == 1)
+    encode_configs_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(a, first, n, static_cast<__nv_bfloat16*>(feat), ld, D,
+                                                              hash, values_out);
+  else if (out_kind == 2)
+    encode_configs_kernel<double><<<grid, 256, 0, st>>>(a, first, n, static_cast<double*>(feat), ld, D, hash, values_out);
+  else
+    encode_configs_kernel<float><<<grid, 256, 0, st>>>(a, first, n, static_cast<float*>(feat), ld, D, hash, values_out);
+  MOSES_CUDA(cudaGetLastError());
+  return 1;
+}
+
+}  // namespace moses

@@ -36,7 +36,7 @@ LIB_ERRORS = {100: "cuda-error", 101: "no-device", 102: "capacity", 103: "invali
 
 PREC_BF16, PREC_TF32, PREC_FP32 = 0, 1, 2  # FP32: 3xTF32 split operands
 THRESHOLD, RATIO = 1, 2
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
 
 
 class MosesError(RuntimeError):
@@ -122,6 +122,7 @@ def lib():
         "moses_segment_sum_device": (C.c_int, [vp, i32, i64, i32, vp, i64, vp]),
         "moses_mmd2": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp]),
         "moses_mmd2_device": (C.c_int, [vp, i64, vp, i64, i32, i64, dbl, vp]),
+        "moses_encode_configs_device": (C.c_int, [vp, vp, vp, vp, i32, C.c_uint64, i64, i32, vp, i64, i32, vp, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),
@@ -698,3 +699,20 @@ def read_mask(path: str) -> ParamMask:
     _ck(lib().moses_read_mask(_p(b), len(b), _p(out), len(out), C.byref(n), C.byref(ph), C.byref(mo),
                               C.byref(val)))
     return ParamMask(out.astype(bool), ph.value, mo.value, val.value)
+
+
+# ---------------------------------------------------------------- candidate generation (space.cpp:140-197)
+TEMPLATE_ROLES = {"tile_x": 0, "tile_y": 1, "unroll": 2, "vectorize": 3, "parallel": 4}
+
+
+def encode_configs_device(task, knobs, first: int, n: int, dtype: int = DTYPE_F32, feat_ptr=None, ld: int = 16,
+                          D: int = 16, hash_ptr=None, values_ptr=None):
+    """Configs [first, first+n) of enumerate_configs' order, on the device: feature rows (encode_features),
+    FNV-1a hashes (config_hash), knob values. task = (work_gflops, bytes_per_unit, ideal_log2_tiles,
+    ideal_log2_unroll); knobs = [(name, sorted domain)]; outputs are device pointers (or None)."""
+    t = np.ascontiguousarray(task, dtype=np.float64)
+    dom = np.ascontiguousarray([v for _, d in knobs for v in d], dtype=np.int64)
+    sizes = np.ascontiguousarray([len(d) for _, d in knobs], dtype=np.int32)
+    roles = np.ascontiguousarray([TEMPLATE_ROLES.get(k, -1) for k, _ in knobs], dtype=np.int32)
+    _ck(lib().moses_encode_configs_device(_p(t), _p(dom), _p(sizes), _p(roles), len(knobs), first, n, dtype,
+                                          feat_ptr, ld, D, hash_ptr, values_ptr))

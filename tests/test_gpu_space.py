@@ -1,0 +1,119 @@
+"""Candidate generation on the device (space.cu) against the oracle's
+restatement of space.cpp:140-197 (itself pinned by the reference's KATs in test_oracle_kat.py):
+enumeration order and knob values and FNV-1a hashes bit-exact, feature rows within fp64 rounding
+(f64 output) and equal after the single rounding to the model's operand type (f32 output)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TASK = (2.0, 8.0, 9.0, 5.0)  # test_space.cpp:19-28
+
+
+@pytest.fixture(scope="module")
+def ml():
+    from paper_2201_05752_b200 import moseslab
+
+    assert moseslab.lib().moses_device_check() == 0, moseslab.lib().moses_last_error()
+    return moseslab
+
+
+def big_space():
+    """6 knobs, 10,223,616 configurations (the 5 template knobs with wider domains + an untemplated one)."""
+    return [("tile_x", [1 << i for i in range(16)]), ("tile_y", [1 << i for i in range(16)]),
+            ("unroll", [0, 1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 128, 256, 512]),
+            ("vectorize", [1 << i for i in range(8)]), ("parallel", [1 << i for i in range(13)]),
+            ("split", list(range(1, 25)))]
+
+
+def run_device(ml, task, knobs, first, n, dtype, D=16, ld=16):
+    import torch
+
+    tdt = {ml.DTYPE_F64: torch.float64, ml.DTYPE_F32: torch.float32, ml.DTYPE_BF16: torch.bfloat16}[dtype]
+    F = torch.full((n, ld), -7.0, dtype=tdt, device="cuda")
+    H = torch.zeros(n, dtype=torch.int64, device="cuda")
+    V = torch.zeros((n, len(knobs)), dtype=torch.int64, device="cuda")
+    ml.encode_configs_device(task, knobs, first, n, dtype, ctypes.c_void_p(F.data_ptr()), ld, D,
+                             ctypes.c_void_p(H.data_ptr()), ctypes.c_void_p(V.data_ptr()))
+    torch.cuda.synchronize()
+    return F.float().cpu().double().numpy() if dtype == ml.DTYPE_BF16 else F.cpu().numpy(), \
+        H.cpu().numpy().view(np.uint64), V.cpu().numpy()
+
+
+def test_default_space_full_enumeration(ml, orc):
+    knobs = orc.default_knob_template()
+    f_ref, h_ref, v_ref = orc.encode_configs(TASK, knobs, 0, 8820)
+    f, h, v = run_device(ml, TASK, knobs, 0, 8820, ml.DTYPE_F64)
+    assert np.array_equal(v, v_ref)
+    assert np.array_equal(h, h_ref)
+    assert np.max(np.abs(f - f_ref)) <= 1e-15
+    f32, _, _ = run_device(ml, TASK, knobs, 0, 8820, ml.DTYPE_F32)
+    assert np.array_equal(f32.astype(np.float32), f_ref.astype(np.float32))
+
+
+def test_reference_vector_and_hash(ml, orc):
+    """test_space.cpp:142-157 / 206-208 through the device path."""
+    knobs = orc.default_knob_template()
+    f, h, v = run_device(ml, TASK, knobs, 0, 8820, ml.DTYPE_F64)
+    i = int(np.nonzero((v == [16, 32, 16, 8, 32]).all(1))[0][0])
+    want = [0.66666666666666663, 0.83333333333333337, 0.40874628412503389, 0.75, 0.625, 0.75,
+            0.66666666666666663, 0.10034333188799373, 0.5625, 0.5]
+    assert np.allclose(f[i, :10], want, rtol=1e-14, atol=0)
+    assert np.all(f[i, 10:] == 0.0)
+    assert int(h[i]) == 0xc27c832e9cdb768d
+
+
+@pytest.mark.parametrize("first,n", [(0, 1), (12345, 4096), (10_223_616 - 5000, 5000), (5_000_000, 100_000)])
+def test_large_space_slices(ml, orc, first, n):
+    knobs = big_space()
+    f_ref, h_ref, v_ref = orc.encode_configs(TASK, knobs, first, n)
+    f, h, v = run_device(ml, TASK, knobs, first, n, ml.DTYPE_F64)
+    assert np.array_equal(v, v_ref) and np.array_equal(h, h_ref)
+    assert np.max(np.abs(f - f_ref)) <= 2e-15
+
+
+def test_packed_model_rows_bf16(ml, orc):
+    """bf16 rows with the packed layout's constant column (ld > D)."""
+    knobs = orc.default_knob_template()
+    f_ref, _, _ = orc.encode_configs(TASK, knobs, 100, 300)
+    f, _, _ = run_device(ml, TASK, knobs, 100, 300, ml.DTYPE_BF16, D=16, ld=24)
+    import torch
+
+    want = torch.from_numpy(f_ref).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(f[:, :16], want)
+    assert np.all(f[:, 16] == 1.0)
+
+
+def test_errors(ml):
+    knobs = [("tile_x", [1, 2]), ("tile_y", [4])]
+    with pytest.raises(ml.MosesError) as e:
+        ml.encode_configs_device(TASK, knobs, 1, 2)  # range beyond the 2-config space
+    assert e.value.code == "shape-mismatch"
+    with pytest.raises(ml.MosesError) as e:
+        ml.encode_configs_device(TASK, [("tile_x", [2, 1])], 0, 1)
+    assert e.value.code == "invalid-task"  # unsorted domain
+
+
+def test_score_whole_space_on_device(ml, orc):
+    """Exhaustive scorer input path without host features: encode 8820 configs on the device ->
+    predict (golden 16-512-512-1 model, TF32) -> scores vs the fp64 oracle on oracle features."""
+    import torch
+
+    knobs = orc.default_knob_template()
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 12345)
+    dm = ml.DeviceModel(p, ml.PREC_TF32, 8832)
+    ld = dm.packed_ld
+    F = torch.zeros((8820, ld), dtype=torch.float32, device="cuda")
+    ml.encode_configs_device(TASK, knobs, 0, 8820, ml.DTYPE_F32, ctypes.c_void_p(F.data_ptr()), ld, 16)
+    S = torch.empty(8820, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ml._ck(ml.lib().moses_predict_device(dm.h, ctypes.c_void_p(F.data_ptr()), ml.DTYPE_F32, ld, 8820,
+                                         ctypes.c_void_p(S.data_ptr())))
+    torch.cuda.synchronize()
+    f_ref, _, _ = orc.encode_configs(TASK, knobs, 0, 8820)
+    ref, _ = orc.forward(dims, p.params, f_ref)
+    got = S.cpu().double().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-3

@@ -326,3 +326,37 @@ def test_pooled_gradients_reduce_and_fd(orc):
         fd = (orc.gradients_pooled(dims, wp, x, off, yp)[1] - orc.gradients_pooled(dims, wm, x, off, yp)[1]) / (2 * h)
         worst = max(worst, abs(fd - g[i]) / max(abs(fd), abs(g[i]), 1e-3))
     assert worst < 1e-4
+
+
+# ---------------------------------------------------------------- knob space (space.cpp:140-197)
+def test_feature_encoding_reference_vector(orc):
+    k = KAT["feature_encoding"]
+    knobs = orc.default_knob_template()
+    f, h, v = orc.encode_configs(k["task"], knobs, 0, KAT["default_space_size"]["value"])
+    i = [j for j in range(len(v)) if list(v[j]) == k["config"]]
+    assert len(i) == 1
+    got = f[i[0]]
+    for a, b in zip(got[:10], k["features"]):
+        assert abs(a - b) <= k["eps"] * max(1.0, abs(b))
+    assert np.all(got[10:] == 0.0)
+    assert int(h[i[0]]) == int(KAT["config_hash_16_32_16_8_32"]["value"], 16)
+
+
+def test_work_term_clamps(orc):
+    k = KAT["work_clamp"]
+    knobs = [(n, [c]) for (n, _), c in zip(orc.default_knob_template(), k["config"])]
+    for g, want in zip((k["low_gflops"], k["high_gflops"]), k["f7"]):
+        f, _, _ = orc.encode_configs((g, 8.0, 9.0, 5.0), knobs, 0, 1)
+        assert f[0, 7] == want
+
+
+def test_enumeration_order_and_completeness(orc):
+    k = KAT["enumeration_order"]
+    knobs = [(n, d) for (n, _), d in zip(orc.default_knob_template(), k["domains"])]
+    _, _, v = orc.encode_configs((2.0, 8.0, 9.0, 5.0), knobs, 0, len(k["configs"]))
+    assert v.tolist() == k["configs"]
+    n = KAT["default_space_size"]["value"]
+    _, h, v = orc.encode_configs((2.0, 8.0, 9.0, 5.0), orc.default_knob_template(), 0, n)
+    assert len({tuple(r) for r in v.tolist()}) == n  # no duplicates
+    assert v.tolist() == sorted(v.tolist())          # lexicographic
+    assert len(set(h.tolist())) == n                 # hashes distinct on the default space
