@@ -496,11 +496,28 @@ def bench_search(ml, L, peaks):
     total = time.perf_counter() - t0
     wbytes = n * (ld * 2 + 8)
     hbm = peaks.get("hbm_gbs", 6534.1)
+    # f3: simulated-hardware labels (oracle.cpp:65-88) for the whole space, and its exhaustive optimum
+    server = {"id": "server", "peak_gflops": 8000.0, "parallel_units": 16.0, "vector_lanes": 8.0,
+              "cache_bytes": 2000000.0, "measure_overhead_ms": 2.0, "noise_std": 0.05, "repeats": 3}
+    lab = torch.empty(n, dtype=torch.float32, device="cuda")
+    ml.measure_configs_device(server, "conv3x3_64", task, knobs, 1, 0, n, label_ptr=C.c_void_p(lab.data_ptr()))
+    a.record()
+    ml.measure_configs_device(server, "conv3x3_64", task, knobs, 1, 0, n, label_ptr=C.c_void_p(lab.data_ptr()))
+    b.record()
+    torch.cuda.synchronize()
+    label_ms = a.elapsed_time(b)
+    t0 = time.perf_counter()
+    best, best_lat = ml.true_best(server, task, knobs)
+    tb_ms = (time.perf_counter() - t0) * 1e3
+    del lab
     out = {"configs": n, "knobs": len(knobs), "model": dims, "encode_ms": enc_ms,
            "encode_roofline": {"bound": "hbm", "achieved": wbytes / (enc_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                "frac": wbytes / (enc_ms / 1e3) / 1e9 / hbm,
                                "algorithmic_bytes": wbytes, "note": "packed bf16 rows + u64 hashes written"},
            "pipeline_ms": total * 1e3, "configs_per_s": n / total,
+           "labels_ms": label_ms, "labels_per_s": n / (label_ms / 1e3),
+           "true_best": {"values": best, "latency_ms": best_lat, "ms": tb_ms,
+                         "note": "exhaustive noise-free optimum over the 10.2M-config space (oracle.cpp:90-105)"},
            "pipeline": "encode_configs (device) -> predict (tcgen05) -> top-1024, wall clock"}
     del F, Hh, S
     torch.cuda.empty_cache()

@@ -229,6 +229,24 @@ MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* do
                                          int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
                                          int64_t* values_dev);
 
+/* ------------------------------------------------------------------ simulated hardware */
+/* device6 = {peak_gflops, parallel_units, vector_lanes, cache_bytes, measure_overhead_ms, noise_std}
+ * (oracle.hpp DeviceSpec). Over configs [first, first+n) of the knob space (enumeration order as in
+ * moses_encode_configs_device): clean_latency_ms (oracle.cpp:58-63) and measure() (oracle.cpp:65-88:
+ * throughput with keyed Gaussian noise, latency, wall cost; label_dev = float throughput, the ranking
+ * label). Any output may be NULL. Default stream. */
+MOSES_API int moses_measure_configs_device(const double* device6, int32_t repeats, const char* device_id,
+                                          const char* task_id, const double* task4, const int64_t* domains,
+                                          const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                                          uint64_t seed, uint64_t first, int64_t n, double* clean_ms_dev,
+                                          double* throughput_dev, double* latency_dev, double* wall_cost_dev,
+                                          float* label_dev);
+/* true_best (oracle.cpp:90-105): exhaustive noise-free optimum on the device; the lexicographically
+ * first configuration on exact ties. best_values (n_knobs) and best_latency are host outputs. */
+MOSES_API int moses_true_best(const double* device6, const double* task4, const int64_t* domains,
+                              const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                              int64_t* best_values, double* best_latency);
+
 /* ------------------------------------------------------------------ synthetic TenSet-shaped data (bench) */
 /* Rows [row0, row0+n) of the keyed SplitMix64 generator, written in the packed layout. */
 MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype,

@@ -794,6 +794,61 @@ inline std::uint64_t config_hash(const std::int64_t* values, int nk) {
   return k.h;
 }
 
+// ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+struct DeviceDesc {
+  double peak_gflops, parallel_units, vector_lanes, cache_bytes, measure_overhead_ms, noise_std;
+  int repeats;
+};
+inline void knob_values(const std::int64_t* values, const int* roles, int nk, std::int64_t kv[5]) {
+  kv[0] = 1; kv[1] = 1; kv[2] = 0; kv[3] = 1; kv[4] = 1;
+  bool seen[5] = {false, false, false, false, false};
+  for (int i = 0; i < nk; ++i)
+    if (roles[i] >= 0 && roles[i] < 5 && !seen[roles[i]]) { kv[roles[i]] = values[i]; seen[roles[i]] = true; }
+}
+// shared_factor (oracle.cpp:33-41)
+inline double shared_factor(const TaskDesc& t, const std::int64_t kv[5]) {
+  const double log_tiles = std::log2(static_cast<double>(kv[0] * kv[1]));
+  const double tile_term = std::exp(-std::pow(log_tiles - t.ideal_log2_tiles, 2.0) / 8.0);
+  const double log_unroll = std::log2(1.0 + static_cast<double>(kv[2]));
+  const double unroll_term = 0.8 + 0.2 * std::exp(-std::pow(log_unroll - t.ideal_log2_unroll, 2.0) / 4.0);
+  return tile_term * unroll_term;
+}
+// device_factor (oracle.cpp:43-56)
+inline double device_factor(const DeviceDesc& d, const TaskDesc& t, const std::int64_t kv[5]) {
+  const double p = static_cast<double>(kv[4]);
+  const double vec = static_cast<double>(kv[3]);
+  const double u = d.parallel_units, l = d.vector_lanes;
+  const double parallel_term = std::min(p / u, u / p);
+  const double vector_term = std::sqrt(std::min(vec / l, l / vec));
+  const double footprint = t.bytes_per_unit * static_cast<double>(kv[0]) * static_cast<double>(kv[1]) *
+                           std::max<double>(1.0, static_cast<double>(kv[2]));
+  const double cache_term = footprint <= d.cache_bytes ? 1.0 : d.cache_bytes / footprint;
+  return parallel_term * vector_term * cache_term;
+}
+// clean_latency_ms (oracle.cpp:58-63)
+inline double clean_latency_ms(const DeviceDesc& d, const TaskDesc& t, const std::int64_t kv[5]) {
+  const double throughput = d.peak_gflops * shared_factor(t, kv) * device_factor(d, t, kv);
+  return t.work_gflops / throughput * 1000.0;
+}
+// measure (oracle.cpp:65-88): noise keyed on (seed, device id, task id, config hash)
+inline void measure(const DeviceDesc& d, const TaskDesc& t, const std::int64_t* values, const int* roles, int nk,
+                    std::uint64_t seed, const char* device_id, const char* task_id, double* throughput,
+                    double* latency, double* wall_cost) {
+  std::int64_t kv[5];
+  knob_values(values, roles, nk, kv);
+  KeyBuilder key;
+  key.add(seed);
+  key.add(std::string_view(device_id));
+  key.add(std::string_view(task_id));
+  key.add(config_hash(values, nk));
+  RngStream rng(key.value());
+  const double eps = rng.gaussian() * d.noise_std;
+  const double noise = std::max(0.05, 1.0 + eps);
+  *throughput = d.peak_gflops * shared_factor(t, kv) * device_factor(d, t, kv) * noise;
+  *latency = t.work_gflops / *throughput * 1000.0;
+  *wall_cost = d.measure_overhead_ms + static_cast<double>(d.repeats) * *latency;
+}
+
 // ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:267-325)
 inline void put_u32(std::string& o, std::uint32_t v) { for (int i = 0; i < 4; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }
 inline void put_u64(std::string& o, std::uint64_t v) { for (int i = 0; i < 8; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }

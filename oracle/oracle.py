@@ -108,6 +108,11 @@ def lib():
         _lib.orc_gradients_pooled_f64.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                                   C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib.orc_synth_features.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_int, C.c_void_p]
+        _lib.orc_measure_configs.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_char_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_longlong,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_true_best.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                       C.c_void_p, C.c_void_p]
         _lib.orc_encode_configs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_uint64,
                                             C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_synth_labels.argtypes = [C.c_uint64, C.c_longlong, C.c_longlong, C.c_void_p]
@@ -414,3 +419,42 @@ def encode_configs(task, knobs, first, n):
     v = np.zeros((n, len(knobs)), dtype=np.int64)
     _check(lib().orc_encode_configs(_p(t), _p(dom), _p(sizes), _p(roles), len(knobs), first, n, _p(f), _p(h), _p(v)))
     return f, h, v
+
+
+# ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+def _dev6(device):
+    return np.ascontiguousarray([device["peak_gflops"], device["parallel_units"], device["vector_lanes"],
+                                 device["cache_bytes"], device["measure_overhead_ms"], device["noise_std"]],
+                                dtype=np.float64)
+
+
+def _task4(task):
+    if isinstance(task, dict):
+        task = (task["work_gflops"], task["bytes_per_unit"], task["ideal_log2_tiles"], task["ideal_log2_unroll"])
+    return np.ascontiguousarray(task, dtype=np.float64)
+
+
+def _space(knobs):
+    dom = np.ascontiguousarray([v for _, d in knobs for v in d], dtype=np.int64)
+    sizes = np.ascontiguousarray([len(d) for _, d in knobs], dtype=np.int32)
+    roles = np.ascontiguousarray([TEMPLATE_ROLES.get(k, -1) for k, _ in knobs], dtype=np.int32)
+    return dom, sizes, roles
+
+
+def measure_configs(device, task_id, task, knobs, seed, first, n):
+    """clean_latency_ms and measure() over configs [first, first+n): (clean, throughput, latency, wall_cost)."""
+    dom, sizes, roles = _space(knobs)
+    out = [np.zeros(n) for _ in range(4)]
+    _check(lib().orc_measure_configs(_p(_dev6(device)), int(device["repeats"]), device["id"].encode(),
+                                     task_id.encode(), _p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs),
+                                     seed, first, n, *(_p(o) for o in out)))
+    return tuple(out)
+
+
+def true_best(device, task, knobs):
+    dom, sizes, roles = _space(knobs)
+    v = np.zeros(len(knobs), dtype=np.int64)
+    lat = np.zeros(1)
+    _check(lib().orc_true_best(_p(_dev6(device)), _p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs),
+                               _p(v), _p(lat)))
+    return v.tolist(), float(lat[0])

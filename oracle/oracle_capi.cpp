@@ -5,6 +5,7 @@
 // Status convention: 0 = ok, otherwise 1 + moseslab::ErrorCode ordinal
 // (errors.hpp:10-36), message retrievable with orc_last_error().
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -278,5 +279,46 @@ ORC int orc_encode_configs(const double* task4, const std::int64_t* domains, con
       if (values_out)
         for (int k = 0; k < nk; ++k) values_out[i * nk + k] = v[k];
     }
+  });
+}
+
+// ---- simulated hardware (oracle.cpp:33-105) over configs [first, first+n) of the enumeration
+ORC int orc_measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                            const double* task4, const std::int64_t* domains, const int* sizes, const int* roles,
+                            int nk, std::uint64_t seed, std::uint64_t first, std::int64_t n, double* clean_ms,
+                            double* throughput, double* latency, double* wall_cost) {
+  return guarded([&] {
+    const DeviceDesc d{dev6[0], dev6[1], dev6[2], dev6[3], dev6[4], dev6[5], repeats};
+    const TaskDesc t{task4[0], task4[1], task4[2], task4[3]};
+    std::int64_t v[16], kv[5];
+    for (std::int64_t i = 0; i < n; ++i) {
+      decode_config(first + std::uint64_t(i), domains, sizes, nk, v);
+      knob_values(v, roles, nk, kv);
+      if (clean_ms) clean_ms[i] = clean_latency_ms(d, t, kv);
+      if (throughput) measure(d, t, v, roles, nk, seed, device_id, task_id, throughput + i, latency + i, wall_cost + i);
+    }
+  });
+}
+
+// true_best (oracle.cpp:90-105): exhaustive noise-free minimum, strict < keeps the lexicographically first
+ORC int orc_true_best(const double* dev6, const double* task4, const std::int64_t* domains, const int* sizes,
+                      const int* roles, int nk, std::int64_t* best_values, double* best_latency) {
+  return guarded([&] {
+    const DeviceDesc d{dev6[0], dev6[1], dev6[2], dev6[3], dev6[4], dev6[5], 1};
+    const TaskDesc t{task4[0], task4[1], task4[2], task4[3]};
+    std::uint64_t space = 1;
+    for (int k = 0; k < nk; ++k) space *= std::uint64_t(sizes[k]);
+    std::int64_t v[16], kv[5];
+    double best = std::numeric_limits<double>::infinity();
+    for (std::uint64_t i = 0; i < space; ++i) {
+      decode_config(i, domains, sizes, nk, v);
+      knob_values(v, roles, nk, kv);
+      const double lat = clean_latency_ms(d, t, kv);
+      if (lat < best) {
+        best = lat;
+        for (int k = 0; k < nk; ++k) best_values[k] = v[k];
+      }
+    }
+    *best_latency = best;
   });
 }

@@ -1785,6 +1785,31 @@ MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* do
   });
 }
 
+MOSES_API int moses_measure_configs_device(const double* device6, int32_t repeats, const char* device_id,
+                                          const char* task_id, const double* task4, const int64_t* domains,
+                                          const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                                          uint64_t seed, uint64_t first, int64_t n, double* clean_ms_dev,
+                                          double* throughput_dev, double* latency_dev, double* wall_cost_dev,
+                                          float* label_dev) {
+  return guarded([&] {
+    note_launch(measure_configs(device6, repeats, device_id, task_id, task4,
+                                reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs, seed, first,
+                                n, clean_ms_dev, throughput_dev, latency_dev, wall_cost_dev, label_dev, nullptr));
+  });
+}
+
+MOSES_API int moses_true_best(const double* device6, const double* task4, const int64_t* domains,
+                              const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                              int64_t* best_values, double* best_latency) {
+  return guarded([&] {
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    sc.ensure(64);
+    note_launch(true_best(device6, task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs,
+                          reinterpret_cast<long long*>(best_values), best_latency, sc.st));
+  });
+}
+
 MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype, void* dst,
                                           int64_t ld) {
   return guarded([&] {

@@ -157,6 +157,13 @@ template <typename T>
 void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st);
 void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st);
 
+// simulated hardware (space.cu): measure() labels and the exhaustive noise-free optimum
+int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
+                    const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,
+                    unsigned long long first, long long n, double* clean_ms, double* thr, double* lat, double* wall,
+                    float* label, cudaStream_t st);
+int true_best(const double* dev6, const double* task4, const long long* domains, const int* sizes, const int* roles,
+              int nk, long long* best_values, double* best_latency, cudaStream_t st);
 // knob-space candidate generation (space.cu); out_kind 0 f32, 1 bf16, 2 f64
 int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
                    unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,

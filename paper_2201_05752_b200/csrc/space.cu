@@ -155,11 +155,10 @@ __global__ void __launch_bounds__(256) encode_configs_kernel(const __grid_consta
 
 }  // namespace
 
-int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
-                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
-                   unsigned long long* hash, long long* values_out, cudaStream_t st) {
+// validate the knob space (space.cpp:41-66, build_space) into `a`; returns the space size
+static unsigned long long fill_space(SpaceArgs& a, const long long* domains, const int* sizes, const int* roles,
+                                     int nk) {
   if (nk <= 0 || nk > kSpaceMaxKnobs) fail(MOSES_ERR_INVALID_ARG, "knob count must lie in [1, 8]");
-  SpaceArgs a{};
   a.nk = nk;
   int off = 0;
   unsigned long long space = 1;
@@ -175,9 +174,17 @@ int encode_configs(const double* task4, const long long* domains, const int* siz
     if (space > ~0ull / (unsigned long long)sizes[k]) fail(MOSES_ERR_SPACE_TOO_LARGE, "knob space overflows 64 bits");
     space *= (unsigned long long)sizes[k];
   }
+  std::copy(domains, domains + off, a.domains);
+  return space;
+}
+
+int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
+                   unsigned long long* hash, long long* values_out, cudaStream_t st) {
+  SpaceArgs a{};
+  const unsigned long long space = fill_space(a, domains, sizes, roles, nk);
   if (n < 0 || first > space || (unsigned long long)n > space - first)
     fail(MOSES_ERR_SHAPE_MISMATCH, "config range exceeds the knob space");
-  std::copy(domains, domains + off, a.domains);
   a.bytes_per_unit = task4[1];
   a.f7 = std::clamp(std::log10(task4[0]) / 3.0, 0.0, 1.0);  // space.cpp:154
   a.f8 = task4[2] / 16.0;
@@ -235,6 +242,232 @@ int encode_configs(const double* task4, const long long* domains, const int* siz
     encode_configs_kernel<float><<<grid, 256, 0, st>>>(a, first, n, static_cast<float*>(feat), ld, D, hash, values_out);
   MOSES_CUDA(cudaGetLastError());
   return 1;
+}
+
+// ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+// The label generator of the synthetic TenSet-style data: the closed-form
+// response model per configuration, keyed Gaussian measurement noise, and the exhaustive
+// noise-free optimum (true_best) as an argmin over (latency, enumeration index) — the
+// lexicographically first configuration on exact ties, like the reference's strict <.
+struct SimArgs {
+  SpaceArgs sp;
+  double peak, units, lanes, cache, overhead, noise_std, work, bytes, ideal_tiles, ideal_unroll;
+  int repeats;
+  unsigned long long key0;  // FNV-1a state after (seed, device id, task id)
+};
+
+namespace {
+
+__device__ __forceinline__ void sim_decode(const SpaceArgs& a, unsigned long long idx, long long kv[5],
+                                           unsigned long long* chash) {
+  long long v[kSpaceMaxKnobs];
+#pragma unroll
+  for (int k = kSpaceMaxKnobs - 1; k >= 0; --k) {
+    v[k] = 0;
+    if (k >= a.nk) continue;
+    const unsigned long long s = (unsigned long long)a.sizes[k];
+    v[k] = a.domains[a.offs[k] + int(idx % s)];
+    idx /= s;
+  }
+  kv[0] = 1; kv[1] = 1; kv[2] = 0; kv[3] = 1; kv[4] = 1;
+  unsigned seen = 0;
+  unsigned long long h = 0xcbf29ce484222325ull;
+#pragma unroll
+  for (int k = 0; k < kSpaceMaxKnobs; ++k) {
+    if (k >= a.nk) continue;
+    const int r = a.roles[k];
+    if (r >= 0 && r < 5 && !(seen & (1u << r))) {
+      kv[r] = v[k];
+      seen |= 1u << r;
+    }
+    const unsigned long long u = (unsigned long long)v[k];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      h ^= (u >> (8 * b)) & 0xffull;
+      h *= 0x100000001b3ull;
+    }
+  }
+  *chash = h;
+}
+
+__device__ __forceinline__ double sim_clean_throughput(const SimArgs& s, const long long kv[5]) {
+  // shared_factor (oracle.cpp:33-41)
+  const double log_tiles = log2(double(kv[0] * kv[1]));
+  const double dt = log_tiles - s.ideal_tiles;
+  const double tile_term = exp(-(dt * dt) / 8.0);  // std::pow(x, 2.0) is correctly rounded: = fl(x * x)
+  const double du = log2(1.0 + double(kv[2])) - s.ideal_unroll;
+  const double unroll_term = 0.8 + 0.2 * exp(-(du * du) / 4.0);
+  // device_factor (oracle.cpp:43-56)
+  const double p = double(kv[4]), vec = double(kv[3]);
+  const double parallel_term = fmin(p / s.units, s.units / p);
+  const double vector_term = sqrt(fmin(vec / s.lanes, s.lanes / vec));
+  const double footprint = s.bytes * double(kv[0]) * double(kv[1]) * fmax(1.0, double(kv[2]));
+  const double cache_term = footprint <= s.cache ? 1.0 : s.cache / footprint;
+  return s.peak * (tile_term * unroll_term) * (parallel_term * vector_term * cache_term);
+}
+
+__device__ __forceinline__ unsigned long long sm64(unsigned long long& st) {
+  st += 0x9e3779b97f4a7c15ull;
+  unsigned long long z = st;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) measure_configs_kernel(const __grid_constant__ SimArgs s,
+                                                              unsigned long long first, long long n,
+                                                              double* __restrict__ clean_ms, double* __restrict__ thr,
+                                                              double* __restrict__ lat, double* __restrict__ wall,
+                                                              float* __restrict__ label) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    long long kv[5];
+    unsigned long long ch;
+    sim_decode(s.sp, first + (unsigned long long)i, kv, &ch);
+    const double clean_thr = sim_clean_throughput(s, kv);
+    if (clean_ms) clean_ms[i] = s.work / clean_thr * 1000.0;  // clean_latency_ms (oracle.cpp:58-63)
+    if (thr == nullptr && lat == nullptr && wall == nullptr && label == nullptr) continue;
+    // measure (oracle.cpp:65-88): RngStream(KeyBuilder(seed, device, task, config_hash)).gaussian()
+    unsigned long long key = s.key0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      key ^= (ch >> (8 * b)) & 0xffull;
+      key *= 0x100000001b3ull;
+    }
+    unsigned long long st = key;
+    const double u1 = double((sm64(st) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = double(sm64(st) >> 11) * 0x1.0p-53;
+    const double g = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+    const double noise = fmax(0.05, 1.0 + g * s.noise_std);
+    const double t = clean_thr * noise;
+    const double l = s.work / t * 1000.0;
+    if (thr) thr[i] = t;
+    if (lat) lat[i] = l;
+    if (wall) wall[i] = s.overhead + double(s.repeats) * l;
+    if (label) label[i] = float(t);
+  }
+}
+
+struct BestItem {
+  double lat;
+  unsigned long long idx;
+};
+__device__ __forceinline__ bool better(const BestItem& a, const BestItem& b) {
+  return a.lat < b.lat || (a.lat == b.lat && a.idx < b.idx);
+}
+
+__global__ void __launch_bounds__(256) true_best_kernel(const __grid_constant__ SimArgs s, unsigned long long space,
+                                                        BestItem* __restrict__ part) {
+  BestItem best{__longlong_as_double(0x7ff0000000000000ll), ~0ull};
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < space; i += gridDim.x * 256ull) {
+    long long kv[5];
+    unsigned long long ch;
+    sim_decode(s.sp, i, kv, &ch);
+    const BestItem c{s.work / sim_clean_throughput(s, kv) * 1000.0, i};
+    if (better(c, best)) best = c;
+  }
+  __shared__ BestItem sh[256];
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o && better(sh[threadIdx.x + o], sh[threadIdx.x])) sh[threadIdx.x] = sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) true_best_final_kernel(BestItem* part, int nparts) {
+  __shared__ BestItem sh[256];
+  BestItem best{__longlong_as_double(0x7ff0000000000000ll), ~0ull};
+  for (int i = threadIdx.x; i < nparts; i += 256)
+    if (better(part[i], best)) best = part[i];
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o && better(sh[threadIdx.x + o], sh[threadIdx.x])) sh[threadIdx.x] = sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[0] = sh[0];
+}
+
+}  // namespace
+
+static SimArgs make_sim(const double* dev6, int repeats, const double* task4, const long long* domains, const int* sizes,
+                        const int* roles, int nk, unsigned long long* space) {
+  SimArgs s{};
+  *space = fill_space(s.sp, domains, sizes, roles, nk);
+  for (int i = 0; i < 4; ++i)
+    if (!(dev6[i] > 0.0) || !std::isfinite(dev6[i])) fail(MOSES_ERR_INVALID_CONFIG, "device parameters must be positive");
+  if (dev6[4] < 0.0 || dev6[5] < 0.0 || repeats < 1) fail(MOSES_ERR_INVALID_CONFIG, "invalid device");  // oracle.cpp:15-31
+  s.peak = dev6[0];
+  s.units = dev6[1];
+  s.lanes = dev6[2];
+  s.cache = dev6[3];
+  s.overhead = dev6[4];
+  s.noise_std = dev6[5];
+  s.repeats = repeats;
+  s.work = task4[0];
+  s.bytes = task4[1];
+  s.ideal_tiles = task4[2];
+  s.ideal_unroll = task4[3];
+  return s;
+}
+
+static void fnv_add_u64(unsigned long long& h, unsigned long long v) {
+  for (int b = 0; b < 8; ++b) {
+    h ^= (v >> (8 * b)) & 0xffull;
+    h *= 0x100000001b3ull;
+  }
+}
+static void fnv_add_str(unsigned long long& h, const char* s) {  // KeyBuilder::add(string): bytes + NUL
+  for (; *s; ++s) {
+    h ^= (unsigned char)*s;
+    h *= 0x100000001b3ull;
+  }
+  h ^= 0;
+  h *= 0x100000001b3ull;
+}
+
+int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
+                    const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,
+                    unsigned long long first, long long n, double* clean_ms, double* thr, double* lat, double* wall,
+                    float* label, cudaStream_t st) {
+  unsigned long long space;
+  SimArgs s = make_sim(dev6, repeats, task4, domains, sizes, roles, nk, &space);
+  if (n < 0 || first > space || (unsigned long long)n > space - first)
+    fail(MOSES_ERR_SHAPE_MISMATCH, "config range exceeds the knob space");
+  unsigned long long h = 0xcbf29ce484222325ull;
+  fnv_add_u64(h, seed);
+  fnv_add_str(h, device_id ? device_id : "");
+  fnv_add_str(h, task_id ? task_id : "");
+  s.key0 = h;
+  if (n == 0) return 0;
+  const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
+  measure_configs_kernel<<<grid, 256, 0, st>>>(s, first, n, clean_ms, thr, lat, wall, label);
+  MOSES_CUDA(cudaGetLastError());
+  return 1;
+}
+
+int true_best(const double* dev6, const double* task4, const long long* domains, const int* sizes, const int* roles,
+              int nk, long long* best_values, double* best_latency, cudaStream_t st) {
+  unsigned long long space;
+  SimArgs s = make_sim(dev6, 1, task4, domains, sizes, roles, nk, &space);
+  if (space > (1ull << 40)) fail(MOSES_ERR_SPACE_TOO_LARGE, "exhaustive search over more than 2^40 configurations");
+  const int grid = int(std::min<unsigned long long>((space + 255) / 256, 148ull * 8));
+  BestItem* part = nullptr;
+  MOSES_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(BestItem) * grid, st));
+  true_best_kernel<<<grid, 256, 0, st>>>(s, space, part);
+  true_best_final_kernel<<<1, 256, 0, st>>>(part, grid);
+  BestItem b;
+  MOSES_CUDA(cudaMemcpyAsync(&b, part, sizeof(b), cudaMemcpyDeviceToHost, st));
+  MOSES_CUDA(cudaFreeAsync(part, st));
+  MOSES_CUDA(cudaStreamSynchronize(st));
+  *best_latency = b.lat;
+  unsigned long long idx = b.idx;
+  for (int k = nk - 1; k >= 0; --k) {
+    best_values[k] = domains[s.sp.offs[k] + int(idx % (unsigned long long)sizes[k])];
+    idx /= (unsigned long long)sizes[k];
+  }
+  return 2;
 }
 
 }  // namespace moses

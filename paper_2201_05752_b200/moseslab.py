@@ -123,6 +123,9 @@ def lib():
         "moses_mmd2": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp]),
         "moses_mmd2_device": (C.c_int, [vp, i64, vp, i64, i32, i64, dbl, vp]),
         "moses_encode_configs_device": (C.c_int, [vp, vp, vp, vp, i32, C.c_uint64, i64, i32, vp, i64, i32, vp, vp]),
+        "moses_measure_configs_device": (C.c_int, [vp, i32, C.c_char_p, C.c_char_p, vp, vp, vp, vp, i32, C.c_uint64,
+                                                   C.c_uint64, i64, vp, vp, vp, vp, vp]),
+        "moses_true_best": (C.c_int, [vp, vp, vp, vp, vp, i32, vp, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),
@@ -716,3 +719,43 @@ def encode_configs_device(task, knobs, first: int, n: int, dtype: int = DTYPE_F3
     roles = np.ascontiguousarray([TEMPLATE_ROLES.get(k, -1) for k, _ in knobs], dtype=np.int32)
     _ck(lib().moses_encode_configs_device(_p(t), _p(dom), _p(sizes), _p(roles), len(knobs), first, n, dtype,
                                           feat_ptr, ld, D, hash_ptr, values_ptr))
+
+
+# ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+def _space_arrays(knobs):
+    dom = np.ascontiguousarray([v for _, d in knobs for v in d], dtype=np.int64)
+    sizes = np.ascontiguousarray([len(d) for _, d in knobs], dtype=np.int32)
+    roles = np.ascontiguousarray([TEMPLATE_ROLES.get(k, -1) for k, _ in knobs], dtype=np.int32)
+    return dom, sizes, roles
+
+
+def _device6(device):
+    return np.ascontiguousarray([device["peak_gflops"], device["parallel_units"], device["vector_lanes"],
+                                 device["cache_bytes"], device["measure_overhead_ms"], device["noise_std"]],
+                                dtype=np.float64)
+
+
+def _task4(task):
+    if isinstance(task, dict):
+        task = (task["work_gflops"], task["bytes_per_unit"], task["ideal_log2_tiles"], task["ideal_log2_unroll"])
+    return np.ascontiguousarray(task, dtype=np.float64)
+
+
+def measure_configs_device(device, task_id, task, knobs, seed, first, n, clean_ptr=None, thr_ptr=None, lat_ptr=None,
+                           wall_ptr=None, label_ptr=None):
+    """clean_latency_ms / measure() over configs [first, first+n) into device buffers (pointers or None)."""
+    dom, sizes, roles = _space_arrays(knobs)
+    _ck(lib().moses_measure_configs_device(_p(_device6(device)), int(device["repeats"]), device["id"].encode(),
+                                           task_id.encode(), _p(_task4(task)), _p(dom), _p(sizes), _p(roles),
+                                           len(knobs), seed, first, n, clean_ptr, thr_ptr, lat_ptr, wall_ptr,
+                                           label_ptr))
+
+
+def true_best(device, task, knobs):
+    """oracle.cpp:90-105 on the device: (values, latency_ms) of the exhaustive noise-free optimum."""
+    dom, sizes, roles = _space_arrays(knobs)
+    v = np.zeros(len(knobs), dtype=np.int64)
+    lat = C.c_double()
+    _ck(lib().moses_true_best(_p(_device6(device)), _p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs),
+                              _p(v), C.byref(lat)))
+    return v.tolist(), lat.value

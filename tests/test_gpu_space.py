@@ -117,3 +117,57 @@ def test_score_whole_space_on_device(ml, orc):
     ref, _ = orc.forward(dims, p.params, f_ref)
     got = S.cpu().double().numpy()
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-3
+
+
+# ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+import json
+import os
+
+SIM = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "simulated_oracle.json")))
+
+
+def test_golden_true_best_on_device(ml, orc):
+    """The 16 frozen optima of proj/tests/golden/true_best_default.json (test_oracle.cpp:313-335):
+    configuration bit-exact, latency within 1e-14 (device exp/log2 vs libm)."""
+    tasks = {t["id"]: t for t in SIM["tasks"]["list"]}
+    knobs = orc.default_knob_template()
+    for e in SIM["true_best"]["entries"]:
+        values, lat = ml.true_best(SIM["devices"][e["device_id"]], tasks[e["task_id"]], knobs)
+        assert values == e["values"], e
+        assert lat == pytest.approx(e["latency_ms"], rel=1e-14), e
+
+
+@pytest.mark.parametrize("first,n", [(0, 8820)])
+def test_measure_matches_oracle(ml, orc, first, n):
+    import torch
+
+    k = SIM["reference_measurement"]
+    knobs = orc.default_knob_template()
+    bufs = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(4)]
+    lab = torch.zeros(n, dtype=torch.float32, device="cuda")
+    ml.measure_configs_device(k["device"], k["task"]["id"], k["task"], knobs, k["seed"], first, n,
+                              *(ctypes.c_void_p(b.data_ptr()) for b in bufs), ctypes.c_void_p(lab.data_ptr()))
+    torch.cuda.synchronize()
+    got = [b.cpu().numpy() for b in bufs]
+    ref = orc.measure_configs(k["device"], k["task"]["id"], k["task"], knobs, k["seed"], first, n)
+    for g, r in zip(got, ref):
+        assert np.max(np.abs(g - r) / np.abs(r)) <= 1e-14
+    assert np.array_equal(lab.cpu().numpy(), got[1].astype(np.float32))
+    # the reference measurement KAT (test_oracle.cpp:142-156) through the device path
+    i = 0
+    for (name, dom), v in zip(knobs, k["config"]):
+        i = i * len(dom) + dom.index(v)
+    assert got[1][i] == pytest.approx(k["throughput_gflops"], rel=k["eps"])
+    assert got[2][i] == pytest.approx(k["latency_ms"], rel=k["eps"])
+
+
+def test_true_best_large_space_matches_oracle(ml, orc):
+    """1.4M-configuration space (wider domains): device argmin == oracle argmin."""
+    knobs = [("tile_x", [1 << i for i in range(12)]), ("tile_y", [1 << i for i in range(12)]),
+             ("unroll", [0, 2, 4, 8, 16, 32, 64, 128, 256, 512]), ("vectorize", [1 << i for i in range(6)]),
+             ("parallel", [1 << i for i in range(10)]), ("split", [1, 2, 3, 4])]
+    dev = SIM["devices"]["embedded"]
+    task = SIM["tasks"]["list"][3]
+    v_ref, l_ref = orc.true_best(dev, task, knobs)
+    v, l = ml.true_best(dev, task, knobs)
+    assert v == v_ref and l == pytest.approx(l_ref, rel=1e-14)

@@ -360,3 +360,36 @@ def test_enumeration_order_and_completeness(orc):
     assert len({tuple(r) for r in v.tolist()}) == n  # no duplicates
     assert v.tolist() == sorted(v.tolist())          # lexicographic
     assert len(set(h.tolist())) == n                 # hashes distinct on the default space
+
+
+# ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
+SIM = json.load(open(os.path.join(HERE, "golden", "simulated_oracle.json")))
+
+
+def _index_of(orc, knobs, values):
+    idx = 0
+    for (name, dom), v in zip(knobs, values):
+        idx = idx * len(dom) + dom.index(v)
+    return idx
+
+
+def test_reference_measurement_values(orc):
+    k = SIM["reference_measurement"]
+    knobs = orc.default_knob_template()
+    i = _index_of(orc, knobs, k["config"])
+    clean, thr, lat, wall = orc.measure_configs(k["device"], k["task"]["id"], k["task"], knobs, k["seed"], i, 1)
+    assert clean[0] == pytest.approx(k["clean_latency_ms"], rel=k["eps"])
+    assert thr[0] == pytest.approx(k["throughput_gflops"], rel=k["eps"])
+    assert lat[0] == pytest.approx(k["latency_ms"], rel=k["eps"])
+    assert wall[0] == pytest.approx(k["device"]["measure_overhead_ms"] + 3 * lat[0], rel=1e-15)
+
+
+def test_golden_true_best_exact(orc):
+    """proj/tests/test_oracle.cpp:313-335 compares these exactly; so does the oracle restatement."""
+    tasks = {t["id"]: t for t in SIM["tasks"]["list"]}
+    knobs = orc.default_knob_template()
+    for e in SIM["true_best"]["entries"]:
+        dev = SIM["devices"][e["device_id"]]
+        values, lat = orc.true_best(dev, tasks[e["task_id"]], knobs)
+        assert values == e["values"], e
+        assert lat == e["latency_ms"], e
