@@ -762,7 +762,7 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per step (3 GEMM launches), cold-cache ncu replay",
-                     "kernel": "umma_gemm_kernel (tcgen05 bf16, all fwd/dgrad/wgrad launches of a step)",
+                     "kernel": "mlp_chain_kernel (fwd), mlp_chain_kernel (dZ), wgrad_group_kernel (tcgen05 bf16): the 3 GEMM launches of a step",
                      "flops_per_step": flops, "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
         "step_breakdown_ms": {k: v[0] / args.profile_steps for k, v in prof.items() if v[1]},
