@@ -560,6 +560,25 @@ __global__ void __launch_bounds__(kPassBlock) lot_cut_kernel(const float* __rest
   if (threadIdx.x == 0) st->cut = s_cut;
 }
 
+// Normalised threshold test without a per-scalar division: for top > 0, fl(x / top) is monotone
+// non-decreasing in x >= 0, so fl(x / top) > theta  <=>  bits(x) >= K, with K the smallest
+// non-negative float bit pattern that passes (31-step binary search, exact __fdiv_rn). top == 0
+// means every xi is 0 and xi_scores does not normalise (lottery.cpp:51-55): test x > theta.
+__device__ __forceinline__ unsigned thresh_key(float top, float theta) {
+  auto pass = [&](unsigned k) {
+    const float x = __uint_as_float(k);
+    return (top > 0.f ? __fdiv_rn(x, top) : x) > theta;
+  };
+  unsigned lo = 0, hi = 0x7f800000u;  // +inf
+  if (!pass(hi)) return 0x7f800001u;  // nothing passes
+  while (lo < hi) {
+    const unsigned mid = lo + (hi - lo) / 2;
+    if (pass(mid)) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 template <int SHADOW, bool THRESH>
 __device__ __forceinline__ void lot_apply_one(long long i, float& wi, float gi, unsigned T, long long cut, float top,
                                               float theta, float alpha, float factor, bool decay, uint8_t& mk,
@@ -567,8 +586,7 @@ __device__ __forceinline__ void lot_apply_one(long long i, float& wi, float gi, 
   const float x = fabsf(__fmul_rn(wi, gi));
   bool kept;
   if constexpr (THRESH) {
-    const float xn = top > 0.f ? __fdiv_rn(x, top) : x;  // xi_scores(normalize) then xi > theta
-    kept = xn > theta;
+    kept = __float_as_uint(x) >= T;  // == (xi / max > theta): T = thresh_key(max, theta)
     cnt += kept;
   } else {
     const unsigned key = __float_as_uint(x);
@@ -607,9 +625,14 @@ __global__ void __launch_bounds__(256) lot_apply_kernel(float* __restrict__ w, c
                                                         uint8_t* __restrict__ mask) {
   using Red = cub::BlockReduce<unsigned long long, 256>;
   __shared__ typename Red::TempStorage tmp;
-  const unsigned T = st->prefix;
+  __shared__ unsigned s_tk;
   const long long cut = st->cut;
   const float top = __uint_as_float(st->max_bits);
+  if constexpr (THRESH) {
+    if (threadIdx.x == 0) s_tk = thresh_key(top, theta);
+    __syncthreads();
+  }
+  const unsigned T = THRESH ? s_tk : st->prefix;
   unsigned long long cnt = 0;
   const long long n4 = n / 4;
   for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n4; q += (long long)gridDim.x * 256) {

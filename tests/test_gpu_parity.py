@@ -805,3 +805,25 @@ def test_resident_lottery_step_bit_exact(ml, orc, kind, mode, value):
         w32, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
         w32 = orc.variant_decay(w32, ref_mask, 0.001, 0.01)
         assert np.array_equal(dm.download().params, w32.astype(np.float64)), it
+
+
+@pytest.mark.parametrize("theta", [0.5, 0.01, 0.999, 0.0])
+def test_threshold_step_large_bit_exact(ml, orc, theta):
+    """Multi-pass threshold step at 4.2M scalars (lot_max -> lot_apply with the division-free
+    normalised test, lottery.cu thresh_key): mask, popcount and weights bit-identical to
+    xi_scores(normalize) -> xi > theta -> step -> decay in fp32."""
+    dims = [2048, 2048, 8, 1]
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(int(theta * 1000) + 3)
+    w = f32(rng.normal(0, 0.05, P))
+    g = f32(rng.normal(0, 1e-2, P))
+    g[rng.random(P) < 0.4] = 0.0
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    dm.set_gradients(g)
+    mask = ml.lottery_step(dm, ml.THRESHOLD, theta, 0, 0.001, 0.01)
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    ref_mask = orc.partition(orc.xi_scores(w32, g32, True), True, orc.THRESHOLD, theta)
+    assert np.array_equal(mask.transferable, ref_mask)
+    ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+    ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
+    assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
