@@ -198,6 +198,21 @@ struct moses_model {
   // CUDA graph of one device-resident training step (moses_train_graph_*)
   cudaGraphExec_t train_exec = nullptr;
   long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
+  // asynchronous host-input pooled step (moses_train_step_pooled_async): two staging slots
+  struct AsyncSlot {
+    double* x = nullptr;           // device float64 statement rows (cap x D)
+    double* y = nullptr;           // device float64 labels (cap)
+    long long* off = nullptr;      // device CSR offsets (cap + 1)
+    long long* dims = nullptr;     // device {n_stmt, programs}
+    long long* dims_host = nullptr;  // pinned source of dims
+    cudaEvent_t ready = nullptr, free = nullptr;
+    bool used = false;
+    cudaGraphExec_t exec = nullptr;
+    long long programs = -1;
+    float lr = 0.f, mu = 0.f;
+  } aslot[2];
+  cudaStream_t st_copy = nullptr;
+  long long async_steps = 0;
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
   void* lot_ws = nullptr;          // fused lottery-step workspace (lottery.cu)
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
@@ -255,6 +270,17 @@ struct moses_model {
     for (void* p : act) dfree(p);
     for (void* p : dz) dfree(p);
     if (train_exec) cudaGraphExecDestroy(train_exec);
+    for (auto& a : aslot) {
+      if (a.exec) cudaGraphExecDestroy(a.exec);
+      dfree(a.x);
+      dfree(a.y);
+      dfree(a.off);
+      dfree(a.dims);
+      if (a.dims_host) cudaFreeHost(a.dims_host);
+      if (a.ready) cudaEventDestroy(a.ready);
+      if (a.free) cudaEventDestroy(a.free);
+    }
+    if (st_copy) cudaStreamDestroy(st_copy);
     dfree(dcounter);
     dfree(gbias);
     dfree(lot_ws);
@@ -1194,6 +1220,94 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     g_graph_kernels = kernels;
     MOSES_CUDA(cudaGraphInstantiate(&m->train_exec, graph, 0));
     MOSES_CUDA(cudaGraphDestroy(graph));
+  });
+}
+
+// tuner.cpp:146-147 (gradients + momentum apply_update) on host float64 statement rows, queued
+// asynchronously: staging slot k % 2 is uploaded on a copy stream (overlapping the previous step's
+// kernels) and consumed by a per-slot CUDA graph (pack -> gradients -> fused update) on the model
+// stream; the loss is copied to loss_out when the step completes.
+MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, int64_t n_stmt, int32_t D,
+                                            const int64_t* offsets, int64_t programs, const double* y, double lr,
+                                            double mu, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    if (m->esz != 2) fail(MOSES_ERR_INVALID_ARG, "the asynchronous pooled step needs a bf16 handle");
+    if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "statement feature width != model input width");
+    if (programs < 1 || offsets[0] != 0 || offsets[programs] != n_stmt)
+      fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must span the statement rows");
+    for (int64_t p = 0; p < programs; ++p)
+      if (offsets[p + 1] < offsets[p]) fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must be non-decreasing");
+    check_rows(m, n_stmt);
+    if (programs > m->cap) fail(MOSES_ERR_CAPACITY, "more programs than the handle capacity");
+    if (!m->st_copy) MOSES_CUDA(cudaStreamCreateWithFlags(&m->st_copy, cudaStreamNonBlocking));
+    auto& a = m->aslot[m->async_steps & 1];
+    if (!a.x) {
+      a.x = dalloc<double>(m->cap * D);
+      a.y = dalloc<double>(m->cap);
+      a.off = dalloc<long long>(m->cap + 1);
+      a.dims = dalloc<long long>(2);
+      MOSES_CUDA(cudaMallocHost(&a.dims_host, 2 * sizeof(long long)));
+      MOSES_CUDA(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
+      MOSES_CUDA(cudaEventCreateWithFlags(&a.free, cudaEventDisableTiming));
+    }
+    // the per-slot graph: pack this slot into act[0] -> pooled gradients -> fused momentum update
+    if (!a.exec || a.programs != programs || a.lr != float(lr) || a.mu != float(mu)) {
+      if (a.exec) {
+        MOSES_CUDA(cudaStreamSynchronize(m->st));
+        cudaGraphExecDestroy(a.exec);
+        a.exec = nullptr;
+      }
+      Pool pool{m->seg_off, m->seg_rows, m->cap};
+      const SgdFuse fz{float(lr), float(mu)};
+      // one eager pass first (lazy workspaces must not be allocated while capturing), on an empty
+      // batch: `programs` programs with no statements -> no pairs, zero gradients, no update
+      MOSES_CUDA(cudaMemsetAsync(a.x, 0, sizeof(double) * m->cap * D, m->st));
+      MOSES_CUDA(cudaMemsetAsync(a.y, 0, sizeof(double) * m->cap, m->st));
+      MOSES_CUDA(cudaMemsetAsync(a.off, 0, sizeof(long long) * (m->cap + 1), m->st));
+      a.dims_host[0] = 0;
+      a.dims_host[1] = programs;
+      MOSES_CUDA(cudaMemcpyAsync(a.dims, a.dims_host, 2 * sizeof(long long), cudaMemcpyHostToDevice, m->st));
+      pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0],
+                                 m->labels, m->seg_off, m->seg_rows, m->st);
+      gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, nullptr);
+      cudaGraph_t graph;
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      try {
+        pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]),
+                                   m->ld[0], m->labels, m->seg_off, m->seg_rows, m->st);
+        if (!gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, &fz))
+          sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+      } catch (...) {
+        cudaStreamEndCapture(m->st, &graph);
+        throw;
+      }
+      MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+      MOSES_CUDA(cudaGraphInstantiate(&a.exec, graph, 0));
+      MOSES_CUDA(cudaGraphDestroy(graph));
+      a.programs = programs;
+      a.lr = float(lr);
+      a.mu = float(mu);
+    }
+    // the slot's previous upload must have left its pinned dims before they are overwritten
+    if (a.used) MOSES_CUDA(cudaEventSynchronize(a.ready));
+    a.dims_host[0] = n_stmt;
+    a.dims_host[1] = programs;
+    if (a.used) MOSES_CUDA(cudaStreamWaitEvent(m->st_copy, a.free, 0));  // its previous step consumed it
+    MOSES_CUDA(cudaMemcpyAsync(a.x, x, sizeof(double) * n_stmt * D, cudaMemcpyHostToDevice, m->st_copy));
+    MOSES_CUDA(cudaMemcpyAsync(a.y, y, sizeof(double) * programs, cudaMemcpyHostToDevice, m->st_copy));
+    MOSES_CUDA(cudaMemcpyAsync(a.off, offsets, sizeof(long long) * (programs + 1), cudaMemcpyHostToDevice,
+                               m->st_copy));
+    MOSES_CUDA(cudaMemcpyAsync(a.dims, a.dims_host, 2 * sizeof(long long), cudaMemcpyHostToDevice, m->st_copy));
+    MOSES_CUDA(cudaEventRecord(a.ready, m->st_copy));
+    MOSES_CUDA(cudaStreamWaitEvent(m->st, a.ready, 0));
+    MOSES_CUDA(cudaGraphLaunch(a.exec, m->st));
+    MOSES_CUDA(cudaEventRecord(a.free, m->st));
+    if (loss_out) MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    a.used = true;
+    ++m->async_steps;
+    note_launch(g_graph_kernels > 0 ? g_graph_kernels : 10);
   });
 }
 

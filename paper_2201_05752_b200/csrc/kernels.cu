@@ -160,6 +160,35 @@ __global__ void gather_pooled_kernel(const uint8_t* __restrict__ x_base, long lo
   }
   for (long long r = Rb + tid; r < rows_pad; r += nthr) seg_rows[r] = -1;
 }
+// Host-input pooled step (moses_train_step_pooled_async): one staging slot of float64 statement
+// rows / labels / CSR offsets -> packed bf16 model rows (+ the constant column), fp32 labels, the
+// batch's segment offsets and row -> program map. Rows [n_stmt, rows_pad) keep their (finite)
+// contents and are masked by seg_rows = -1. *n_stmt_dev / *programs_dev are read on the device so
+// one captured graph serves every batch size up to the capacity.
+template <typename T>
+__global__ void pack_pooled_kernel(const double* __restrict__ xs, const double* __restrict__ ys,
+                                   const long long* __restrict__ offs, const long long* __restrict__ dims_dev, int D,
+                                   long long rows_pad, T* __restrict__ act0, long long ld, float* __restrict__ ydst,
+                                   long long* __restrict__ seg_off, int* __restrict__ seg_rows) {
+  ptx::pdl_launch_dependents();
+  const long long n_stmt = dims_dev[0], programs = dims_dev[1];
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n_stmt * ld; i += nthr) {
+    const long long r = i / ld;
+    const int c = int(i - r * ld);
+    const float v = c < D ? float(xs[r * D + c]) : (c == D ? 1.f : 0.f);
+    act0[i] = from_f<T>(v);
+  }
+  for (long long p = tid; p <= programs; p += nthr) {
+    seg_off[p] = offs[p];
+    if (p < programs) {
+      ydst[p] = float(ys[p]);
+      for (long long r = offs[p]; r < offs[p + 1]; ++r) seg_rows[r] = int(p);
+    }
+  }
+  for (long long r = n_stmt + tid; r < rows_pad; r += nthr) seg_rows[r] = -1;
+}
+
 __global__ void advance_counter_kernel(long long* c) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *c += 1;
 }
@@ -1237,6 +1266,16 @@ void gather_pooled(const void* x_base, long long row_bytes, const float* y_base,
       static_cast<uint8_t*>(dst), ydst, seg_off, seg_rows);
   MOSES_CUDA(cudaGetLastError());
 }
+template <typename T>
+void pack_pooled(const double* xs, const double* ys, const long long* offs, const long long* dims_dev, int D,
+                 long long rows_pad, T* act0, long long ld, float* ydst, long long* seg_off, int* seg_rows,
+                 cudaStream_t s) {
+  pack_pooled_kernel<T><<<grid_for(rows_pad * ld, 256), 256, 0, s>>>(xs, ys, offs, dims_dev, D, rows_pad, act0, ld, ydst,
+                                                                     seg_off, seg_rows);
+  MOSES_CUDA(cudaGetLastError());
+}
+template void pack_pooled<__nv_bfloat16>(const double*, const double*, const long long*, const long long*, int,
+                                         long long, __nv_bfloat16*, long long, float*, long long*, int*, cudaStream_t);
 void advance_counter(long long* c, cudaStream_t s) {
   advance_counter_kernel<<<1, 32, 0, s>>>(c);
   MOSES_CUDA(cudaGetLastError());

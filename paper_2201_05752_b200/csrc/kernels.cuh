@@ -157,6 +157,11 @@ template <typename T>
 void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st);
 void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st);
 
+// host-input pooled training step: staging slot -> packed rows, labels, segments (kernels.cu)
+template <typename T>
+void pack_pooled(const double* xs, const double* ys, const long long* offs, const long long* dims_dev, int D,
+                 long long rows_pad, T* act0, long long ld, float* ydst, long long* seg_off, int* seg_rows,
+                 cudaStream_t s);
 // simulated hardware (space.cu): measure() labels and the exhaustive noise-free optimum
 int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
                     const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,

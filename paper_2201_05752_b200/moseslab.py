@@ -126,6 +126,7 @@ def lib():
         "moses_measure_configs_device": (C.c_int, [vp, i32, C.c_char_p, C.c_char_p, vp, vp, vp, vp, i32, C.c_uint64,
                                                    C.c_uint64, i64, vp, vp, vp, vp, vp]),
         "moses_true_best": (C.c_int, [vp, vp, vp, vp, vp, i32, vp, vp]),
+        "moses_train_step_pooled_async": (C.c_int, [vp, vp, i64, i32, vp, i64, vp, dbl, dbl, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),

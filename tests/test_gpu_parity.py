@@ -827,3 +827,43 @@ def test_threshold_step_large_bit_exact(ml, orc, theta):
     ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
     ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
     assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
+
+
+def test_async_pooled_steps_match_synchronous(ml):
+    """moses_train_step_pooled_async (double-buffered upload + per-slot graph) == gradients_pooled +
+    apply_update(momentum) step by step: parameters bit-identical, per-step losses equal."""
+    import ctypes
+
+    import torch
+
+    dims = [164, 512, 512, 512, 1]
+    p = ml.init_random(dims, 4, strict=False)
+    B = 128
+    batches = []
+    for b in range(3):
+        off = ml.synth_offsets(20 + b, B, 8)
+        x = rows(int(off[-1]), dims[0], 30 + b)
+        y = labels(B, 40 + b)
+        batches.append((np.ascontiguousarray(x), np.ascontiguousarray(off), np.ascontiguousarray(y)))
+    cap = 1024
+    a = ml.DeviceModel(p, ml.PREC_BF16, cap)
+    s = ml.DeviceModel(p, ml.PREC_BF16, cap)
+    hyper = ml.TrainHyper(learning_rate=0.001, momentum=0.9)
+    steps = [0, 1, 2, 0, 1]
+    losses = torch.zeros(len(steps), dtype=torch.float64).pin_memory()
+    keep = []
+    for k, b in enumerate(steps):
+        x, off, y = batches[b]
+        xp, op, yp = (torch.from_numpy(v).pin_memory() for v in (x, off, y))
+        keep.append((xp, op, yp))  # must outlive the queued step
+        ml._ck(ml.lib().moses_train_step_pooled_async(a.h, ctypes.c_void_p(xp.data_ptr()), x.shape[0], dims[0],
+                                                       ctypes.c_void_p(op.data_ptr()), B, ctypes.c_void_p(yp.data_ptr()),
+                                                       0.001, 0.9, ctypes.c_void_p(losses[k:k + 1].data_ptr())))
+    ml._ck(ml.lib().moses_model_synchronize(a.h))
+    ref_losses = []
+    for b in steps:
+        x, off, y = batches[b]
+        ref_losses.append(ml.gradients_pooled(s, x, off, y, want_loss=True)[1])
+        ml.apply_update(s, hyper, None, True)
+    assert np.array_equal(a.download().params, s.download().params)
+    assert np.allclose(losses.numpy(), ref_losses, rtol=0, atol=1e-12)
