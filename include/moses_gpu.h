@@ -178,6 +178,12 @@ MOSES_API int moses_variant_decay(moses_model_t m, double alpha, double lambda);
  * device pass sequence; threshold mode normalises xi like the tuner does. */
 MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, int32_t phase, double alpha,
                                  double lambda, uint8_t* mask_out, int64_t count, int64_t* popcount);
+/* The same fused step with masked Adam on the transferable scalars (the north star's Adam variant;
+ * adam_update arithmetic of moses_adam_update, bias corrections of `step`); variant scalars decay by
+ * 1 - lr * lambda. Moments live on the handle (zero at first use). */
+MOSES_API int moses_lottery_step_adam(moses_model_t m, int32_t mode, double value, int32_t phase, double lr,
+                                      double beta1, double beta2, double eps, int32_t step, double lambda,
+                                      uint8_t* mask_out, int64_t count, int64_t* popcount);
 
 /* ------------------------------------------------------------------ adversary (lottery.hpp:36-42, 64-79) */
 /* make_adversary (lottery.cpp:166-180): zero discriminator over m x D replay rows. */

@@ -1569,10 +1569,9 @@ MOSES_API int moses_variant_decay(moses_model_t m, double alpha, double lambda) 
   });
 }
 
-MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, int32_t phase, double alpha,
-                                 double lambda, uint8_t* mask_out, int64_t count, int64_t* popcount) {
-  (void)phase;
-  return guarded([&] {
+static void lottery_step_impl(moses_model* m, int32_t mode, double value, double alpha, double lambda,
+                              uint8_t* mask_out, int64_t count, int64_t* popcount, const AdamOpt* adam) {
+  {
     require_model(m);
     const long long keep = partition_validate(m, mode, value, true /* the tuner normalises in threshold mode */);
     // step on kept scalars; decay the rest (reference order: step, then decay validation)
@@ -1581,7 +1580,12 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
     const bool decay = decay_ok && rate != 0.0;
     if (mode == MOSES_MODE_RATIO && keep >= m->P) {
       MOSES_CUDA(cudaMemsetAsync(m->mask, 1, m->P, m->st));
-      lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
+      if (adam) {  // every scalar is transferable: masked Adam over all of them, no decay
+        adam_update(m->w, adam->m1, adam->m2, m->g, nullptr, m->P, float(alpha), adam->b1, adam->b2, adam->eps,
+                    adam->c1, adam->c2, m->shadow(), m->st);
+      } else {
+        lottery_apply(m->w, m->g, m->mask, m->P, float(alpha), float(1.0 - rate), true, decay, m->shadow(), m->st);
+      }
       m->post_update();
       note_launch(1);
     } else {
@@ -1591,7 +1595,8 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
       }
       ProfScope ps(P_SELECT, m->st);
       const int launched = lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha),
-                                              float(1.0 - rate), decay, m->shadow(), m->mask, m->lot_ws, m->dcount, m->st);
+                                              float(1.0 - rate), decay, m->shadow(), m->mask, m->lot_ws, m->dcount, m->st,
+                                              adam);
       m->post_update();
       note_launch(launched);
     }
@@ -1614,8 +1619,35 @@ MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, in
       bool noop;
       decay_factor(alpha, lambda, &noop);
     }
+  }
+}
+
+MOSES_API int moses_lottery_step(moses_model_t m, int32_t mode, double value, int32_t phase, double alpha,
+                                 double lambda, uint8_t* mask_out, int64_t count, int64_t* popcount) {
+  (void)phase;
+  return guarded([&] { lottery_step_impl(m, mode, value, alpha, lambda, mask_out, count, popcount, nullptr); });
+}
+
+MOSES_API int moses_lottery_step_adam(moses_model_t m, int32_t mode, double value, int32_t phase, double lr,
+                                      double beta1, double beta2, double eps, int32_t step, double lambda,
+                                      uint8_t* mask_out, int64_t count, int64_t* popcount) {
+  (void)phase;
+  return guarded([&] {
+    require_model(m);
+    if (step < 1) fail(MOSES_ERR_INVALID_ARG, "adam step must be >= 1");
+    if (!m->m1) {
+      m->m1 = dalloc<float>(m->P);
+      m->m2 = dalloc<float>(m->P);
+      MOSES_CUDA(cudaMemsetAsync(m->m1, 0, m->P * 4, m->st));
+      MOSES_CUDA(cudaMemsetAsync(m->m2, 0, m->P * 4, m->st));
+    }
+    const AdamOpt o{m->m1, m->m2, float(beta1), float(beta2), float(eps), float(1.0 - std::pow(beta1, step)),
+                    float(1.0 - std::pow(beta2, step))};
+    lottery_step_impl(m, mode, value, lr, lambda, mask_out, count, popcount, &o);
   });
 }
+
+
 
 // ---------------------------------------------------------------- adversary
 MOSES_API int moses_adversary_create(const double* replay, int64_t mrows, int32_t D, int32_t width, double step,

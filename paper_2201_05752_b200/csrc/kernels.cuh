@@ -117,9 +117,14 @@ void partition_from_xi(const float* xi, long long n, int mode, float theta, long
 long long popcount_mask(const uint8_t* mask, long long n, unsigned long long* dcount, cudaStream_t st);
 // lottery.cu: fused xi -> partition -> transferable_step -> variant_decay, xi never materialised
 size_t lottery_ws_bytes(long long n);
+struct AdamOpt {  // masked Adam on the transferable scalars (null: the reference's plain step)
+  float* m1;
+  float* m2;
+  float b1, b2, eps, c1, c2;
+};
 int lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
                        float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
-                       cudaStream_t st);
+                       cudaStream_t st, const AdamOpt* adam = nullptr);
 
 // ---- candidate top-k (search.cpp:32-37): (score desc, index asc)
 void topk_select(const float* scores, long long n, long long k, const SelectWs& ws, unsigned* out_key, long long* out_idx,

@@ -579,10 +579,28 @@ __device__ __forceinline__ unsigned thresh_key(float top, float theta) {
   return lo;
 }
 
+// Optimizer of the transferable scalars: plain step w -= alpha*g (transferable_step,
+// lottery.cpp:92-97), or masked Adam (the north star's Adam variant; same arithmetic as adam_kernel
+// and the oracle's adam_update, no FMA contraction).
+struct StepOpt {
+  float* m1 = nullptr;  // null: plain step
+  float* m2 = nullptr;
+  float b1 = 0.f, b2 = 0.f, eps = 0.f, c1 = 1.f, c2 = 1.f;
+};
+__device__ __forceinline__ float adam_scalar(float wi, float gi, float& m1, float& m2, float lr, const StepOpt& o) {
+  const float a = __fadd_rn(__fmul_rn(o.b1, m1), __fmul_rn(__fsub_rn(1.f, o.b1), gi));
+  const float b = __fadd_rn(__fmul_rn(o.b2, m2), __fmul_rn(__fsub_rn(1.f, o.b2), __fmul_rn(gi, gi)));
+  m1 = a;
+  m2 = b;
+  const float mh = __fdiv_rn(a, o.c1);
+  const float vh = __fdiv_rn(b, o.c2);
+  return __fsub_rn(wi, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), o.eps)));
+}
+
 template <int SHADOW, bool THRESH>
 __device__ __forceinline__ void lot_apply_one(long long i, float& wi, float gi, unsigned T, long long cut, float top,
                                               float theta, float alpha, float factor, bool decay, uint8_t& mk,
-                                              unsigned long long& cnt) {
+                                              unsigned long long& cnt, const StepOpt& opt, float& m1, float& m2) {
   const float x = fabsf(__fmul_rn(wi, gi));
   bool kept;
   if constexpr (THRESH) {
@@ -592,8 +610,9 @@ __device__ __forceinline__ void lot_apply_one(long long i, float& wi, float gi, 
     const unsigned key = __float_as_uint(x);
     kept = key > T || (key == T && i <= cut);
   }
-  if (kept) wi = __fsub_rn(wi, __fmul_rn(alpha, gi));  // transferable_step (apply_update, no momentum)
-  else if (decay) wi = __fmul_rn(wi, factor);          // variant_decay
+  if (kept) wi = opt.m1 ? adam_scalar(wi, gi, m1, m2, alpha, opt)  // masked Adam
+                        : __fsub_rn(wi, __fmul_rn(alpha, gi));     // transferable_step (apply_update, no momentum)
+  else if (decay) wi = __fmul_rn(wi, factor);                      // variant_decay
   mk = kept ? 1 : 0;
 }
 
@@ -622,7 +641,7 @@ template <int SHADOW, bool THRESH>
 __global__ void __launch_bounds__(256) lot_apply_kernel(float* __restrict__ w, const float* __restrict__ g, long long n,
                                                         LotState* st, float theta, float alpha, float factor,
                                                         bool decay, void* __restrict__ shadow,
-                                                        uint8_t* __restrict__ mask) {
+                                                        uint8_t* __restrict__ mask, const StepOpt opt) {
   using Red = cub::BlockReduce<unsigned long long, 256>;
   __shared__ typename Red::TempStorage tmp;
   __shared__ unsigned s_tk;
@@ -639,11 +658,20 @@ __global__ void __launch_bounds__(256) lot_apply_kernel(float* __restrict__ w, c
     const long long i = 4 * q;
     float4 wv = *reinterpret_cast<const float4*>(w + i);
     const float4 gv = ld4(g + i);
+    float4 a1 = make_float4(0, 0, 0, 0), a2 = a1;
+    if (opt.m1) {
+      a1 = *reinterpret_cast<const float4*>(opt.m1 + i);
+      a2 = *reinterpret_cast<const float4*>(opt.m2 + i);
+    }
     uchar4 mk;
-    lot_apply_one<SHADOW, THRESH>(i, wv.x, gv.x, T, cut, top, theta, alpha, factor, decay, mk.x, cnt);
-    lot_apply_one<SHADOW, THRESH>(i + 1, wv.y, gv.y, T, cut, top, theta, alpha, factor, decay, mk.y, cnt);
-    lot_apply_one<SHADOW, THRESH>(i + 2, wv.z, gv.z, T, cut, top, theta, alpha, factor, decay, mk.z, cnt);
-    lot_apply_one<SHADOW, THRESH>(i + 3, wv.w, gv.w, T, cut, top, theta, alpha, factor, decay, mk.w, cnt);
+    lot_apply_one<SHADOW, THRESH>(i, wv.x, gv.x, T, cut, top, theta, alpha, factor, decay, mk.x, cnt, opt, a1.x, a2.x);
+    lot_apply_one<SHADOW, THRESH>(i + 1, wv.y, gv.y, T, cut, top, theta, alpha, factor, decay, mk.y, cnt, opt, a1.y, a2.y);
+    lot_apply_one<SHADOW, THRESH>(i + 2, wv.z, gv.z, T, cut, top, theta, alpha, factor, decay, mk.z, cnt, opt, a1.z, a2.z);
+    lot_apply_one<SHADOW, THRESH>(i + 3, wv.w, gv.w, T, cut, top, theta, alpha, factor, decay, mk.w, cnt, opt, a1.w, a2.w);
+    if (opt.m1) {
+      *reinterpret_cast<float4*>(opt.m1 + i) = a1;
+      *reinterpret_cast<float4*>(opt.m2 + i) = a2;
+    }
     *reinterpret_cast<float4*>(w + i) = wv;
     *reinterpret_cast<uchar4*>(mask + i) = mk;
     store_shadow4<SHADOW>(shadow, i, wv);
@@ -652,7 +680,12 @@ __global__ void __launch_bounds__(256) lot_apply_kernel(float* __restrict__ w, c
     for (long long i = 4 * n4 + threadIdx.x; i < n; i += 256) {
       float wi = w[i];
       uint8_t mk;
-      lot_apply_one<SHADOW, THRESH>(i, wi, g[i], T, cut, top, theta, alpha, factor, decay, mk, cnt);
+      float a1 = opt.m1 ? opt.m1[i] : 0.f, a2 = opt.m1 ? opt.m2[i] : 0.f;
+      lot_apply_one<SHADOW, THRESH>(i, wi, g[i], T, cut, top, theta, alpha, factor, decay, mk, cnt, opt, a1, a2);
+      if (opt.m1) {
+        opt.m1[i] = a1;
+        opt.m2[i] = a2;
+      }
       w[i] = wi;
       mask[i] = mk;
       if constexpr (SHADOW == 1) static_cast<__nv_bfloat16*>(shadow)[i] = __float2bfloat16_rn(wi);
@@ -767,7 +800,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     lot_resident_kernel(float* __restrict__ w, const float* __restrict__ g, long long n, long long chunk, int E,
                         unsigned long long keep, float theta, float alpha, float factor, bool decay,
                         void* __restrict__ shadow, uint8_t* __restrict__ mask, ResState* st,
-                        unsigned long long* popcount_out) {
+                        unsigned long long* popcount_out, const StepOpt opt) {
   __shared__ unsigned sh[2048];
   __shared__ unsigned s_digit;
   __shared__ unsigned long long s_before;
@@ -897,8 +930,18 @@ __global__ void __launch_bounds__(kResThreads, 1)
     }
     if (ok) {
       float wi = wv[j];
-      if (kept) wi = __fsub_rn(wi, __fmul_rn(alpha, gv[j]));
-      else if (decay) wi = __fmul_rn(wi, factor);
+      if (kept) {
+        if (opt.m1) {  // masked Adam
+          float a1 = opt.m1[i], a2 = opt.m2[i];
+          wi = adam_scalar(wi, gv[j], a1, a2, alpha, opt);
+          opt.m1[i] = a1;
+          opt.m2[i] = a2;
+        } else {
+          wi = __fsub_rn(wi, __fmul_rn(alpha, gv[j]));
+        }
+      } else if (decay) {
+        wi = __fmul_rn(wi, factor);
+      }
       w[i] = wi;
       mask[i] = kept ? 1 : 0;
       if constexpr (SHADOW == 1) static_cast<__nv_bfloat16*>(shadow)[i] = __float2bfloat16_rn(wi);
@@ -966,7 +1009,17 @@ size_t lottery_ws_bytes(long long n) {
 // Fused Moses step. mode 1 threshold (normalised, strict), 2 ratio (top `keep`, index tie-break).
 int lottery_step_fused(float* w, const float* g, long long n, int mode, float theta, long long keep, float alpha,
                        float factor, bool decay, Shadow sh, uint8_t* mask, void* ws, unsigned long long* popcount_dev,
-                       cudaStream_t st) {
+                       cudaStream_t st, const AdamOpt* adam) {
+  StepOpt opt;
+  if (adam) {
+    opt.m1 = adam->m1;
+    opt.m2 = adam->m2;
+    opt.b1 = adam->b1;
+    opt.b2 = adam->b2;
+    opt.eps = adam->eps;
+    opt.c1 = adam->c1;
+    opt.c2 = adam->c2;
+  }
   ResState* R = static_cast<ResState*>(ws);  // zeroed at allocation; every call leaves it reusable
   uint8_t* p = static_cast<uint8_t*>(ws) + res_state_bytes();
   LotState* S = reinterpret_cast<LotState*>(p);
@@ -999,8 +1052,9 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     const unsigned long long ukeep = (unsigned long long)keep;
     void* shp = sh.ptr;
     int grid = sms;
+    StepOpt o = opt;
     void* args[] = {&w, (void*)&g, &n, (void*)&chunk, (void*)&E, (void*)&ukeep, &theta, &alpha, &factor, &decay, &shp,
-                    &mask, &R, &pop};
+                    &mask, &R, &pop, &o};
     const void* fn = nullptr;
     if (mode == 1) fn = sh.kind == 1 ? (const void*)lot_resident_kernel<1, true>
                       : sh.kind == 2 ? (const void*)lot_resident_kernel<2, true> : (const void*)lot_resident_kernel<0, true>;
@@ -1014,7 +1068,7 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
   const int agrid = std::max<long long>(1, std::min<long long>((n / 4 + 255) / 256, (long long)sms * 16));
   if (mode == 1) {
     lot_max_kernel<<<sms * 2, kPassBlock, 0, st>>>(w, g, n, S);  // 2 x 1024 threads per SM
-#define LOT_T(K) lot_apply_kernel<K, true><<<agrid, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask)
+#define LOT_T(K) lot_apply_kernel<K, true><<<agrid, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask, opt)
     if (sh.kind == 1) LOT_T(1); else if (sh.kind == 2) LOT_T(2); else LOT_T(0);
 #undef LOT_T
   } else {
@@ -1042,7 +1096,7 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     const long long chunk = (n + nb - 1) / nb;
     lot_eq_count_kernel<<<nb, kPassBlock, 0, st>>>(w, g, n, chunk, S, block_eq);
     lot_cut_kernel<<<1, kPassBlock, 0, st>>>(w, g, n, chunk, nb, S, block_eq);
-#define LOT_R(K) lot_apply_kernel<K, false><<<agrid, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask)
+#define LOT_R(K) lot_apply_kernel<K, false><<<agrid, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask, opt)
     if (sh.kind == 1) LOT_R(1); else if (sh.kind == 2) LOT_R(2); else LOT_R(0);
 #undef LOT_R
   }

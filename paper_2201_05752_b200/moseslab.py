@@ -127,6 +127,7 @@ def lib():
                                                    C.c_uint64, i64, vp, vp, vp, vp, vp]),
         "moses_true_best": (C.c_int, [vp, vp, vp, vp, vp, i32, vp, vp]),
         "moses_train_step_pooled_async": (C.c_int, [vp, vp, i64, i32, vp, i64, vp, dbl, dbl, vp]),
+        "moses_lottery_step_adam": (C.c_int, [vp, i32, dbl, i32, dbl, dbl, dbl, dbl, i32, dbl, vp, i64, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),
@@ -548,6 +549,16 @@ def variant_decay(model: DeviceModel, mask: Optional[ParamMask], alpha: float, l
         m = np.ascontiguousarray(mask.transferable, dtype=np.uint8)
         _ck(lib().moses_mask_upload(model.h, _p(m), len(m)))
     _ck(lib().moses_variant_decay(model.h, alpha, lam))
+
+
+def lottery_step_adam(model, mode: int, value: float, phase: int, lr: float, b1: float, b2: float, eps: float,
+                      step: int, lam: float) -> "ParamMask":
+    """lottery_step with masked Adam on the transferable scalars (decay 1 - lr*lam on the rest)."""
+    out = np.zeros(model.P, dtype=np.uint8)
+    pop = C.c_int64()
+    _ck(lib().moses_lottery_step_adam(model.h, mode, value, phase, lr, b1, b2, eps, step, lam, _p(out), model.P,
+                                      C.byref(pop)))
+    return ParamMask(out.astype(bool), phase, mode, value)
 
 
 def lottery_step(model: DeviceModel, mode: int, value: float, phase: int, alpha: float, lam: float) -> ParamMask:

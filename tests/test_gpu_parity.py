@@ -867,3 +867,29 @@ def test_async_pooled_steps_match_synchronous(ml):
         ml.apply_update(s, hyper, None, True)
     assert np.array_equal(a.download().params, s.download().params)
     assert np.allclose(losses.numpy(), ref_losses, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("dims", [[164, 512, 512, 512, 512, 1], [2048, 2048, 8, 1]])
+@pytest.mark.parametrize("mode,value", [(2, 0.5), (1, 0.5)])
+def test_lottery_step_adam_bit_exact(ml, orc, dims, mode, value):
+    """Fused Moses step with masked Adam (resident kernel at 873K scalars, multi-pass at 4.2M):
+    two consecutive steps, mask and weights bit-identical to xi -> partition -> adam_update(mask)
+    -> variant_decay(lr, lambda) in fp32."""
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(P % 97 + mode)
+    w = f32(rng.normal(0, 0.05, P))
+    g = f32(rng.normal(0, 1e-2, P))
+    g[rng.random(P) < 0.4] = 0.0
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    m1, m2 = np.zeros(P, np.float32), np.zeros(P, np.float32)
+    lr, b1, b2, eps, lam = 1e-3, 0.9, 0.999, 1e-8, 0.01
+    for step in (1, 2):
+        dm.set_gradients(g32.astype(np.float64))
+        mask = ml.lottery_step_adam(dm, mode, value, step, lr, b1, b2, eps, step, lam)
+        xi = orc.xi_scores(w32, g32, mode == 1)
+        ref_mask = orc.partition(xi, mode == 1, mode, value)
+        assert np.array_equal(mask.transferable, ref_mask)
+        w32, m1, m2 = orc.adam(w32, m1, m2, g32, lr, b1, b2, eps, step, ref_mask)
+        w32 = orc.variant_decay(w32, ref_mask, lr, lam)
+        assert np.array_equal(dm.download().params, w32.astype(np.float64)), step
