@@ -242,6 +242,10 @@ MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* do
                                          const int32_t* roles, int32_t n_knobs, uint64_t first, int64_t n,
                                          int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
                                          int64_t* values_dev);
+/* Host-output variant: float64 feature rows (n x 16) and hashes copied back (either may be NULL). */
+MOSES_API int moses_encode_configs(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                  const int32_t* roles, int32_t n_knobs, uint64_t first, int64_t n,
+                                  double* features_out, uint64_t* hashes_out);
 
 /* ------------------------------------------------------------------ simulated hardware */
 /* device6 = {peak_gflops, parallel_units, vector_lanes, cache_bytes, measure_overhead_ms, noise_std}

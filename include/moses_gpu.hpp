@@ -298,4 +298,77 @@ inline std::vector<int64_t> select_batch(const std::vector<uint64_t>& ordered_ha
   return out;
 }
 
+// ---- space.hpp / oracle.hpp on the device: candidate generation and the simulated hardware
+struct KnobSpec {  // space.hpp:16-20 (the kind only matters to validate_task)
+  std::string name;
+  std::vector<int64_t> domain;
+};
+struct TaskSpec {  // space.hpp:24-31
+  std::string id;
+  double work_gflops = 0.0, bytes_per_unit = 0.0, ideal_log2_tiles = 0.0, ideal_log2_unroll = 0.0;
+  std::vector<KnobSpec> knobs;
+};
+struct DeviceSpec {  // oracle.hpp:12-21
+  std::string id;
+  double peak_gflops = 0.0, parallel_units = 1.0, vector_lanes = 1.0, cache_bytes = 0.0;
+  double measure_overhead_ms = 0.0, noise_std = 0.0;
+  int repeats = 1;
+};
+struct Configuration {
+  std::vector<int64_t> values;
+};
+struct BestConfig {
+  Configuration config;
+  double latency_ms = 0.0;
+};
+inline std::vector<KnobSpec> default_knob_template() {  // space.cpp:28-36
+  return {{"tile_x", {1, 2, 4, 8, 16, 32, 64}}, {"tile_y", {1, 2, 4, 8, 16, 32, 64}}, {"unroll", {0, 16, 64, 512}},
+          {"vectorize", {1, 2, 4, 8, 16}}, {"parallel", {1, 2, 4, 8, 16, 32, 64, 128, 256}}};
+}
+namespace detail {
+struct SpaceArrays {
+  double task4[4];
+  std::vector<int64_t> domains;
+  std::vector<int32_t> sizes, roles;
+  explicit SpaceArrays(const TaskSpec& t)
+      : task4{t.work_gflops, t.bytes_per_unit, t.ideal_log2_tiles, t.ideal_log2_unroll} {
+    const char* names[5] = {"tile_x", "tile_y", "unroll", "vectorize", "parallel"};
+    for (const auto& k : t.knobs) {
+      domains.insert(domains.end(), k.domain.begin(), k.domain.end());
+      sizes.push_back(int32_t(k.domain.size()));
+      int r = -1;
+      for (int i = 0; i < 5; ++i)
+        if (k.name == names[i]) r = i;
+      roles.push_back(r);
+    }
+  }
+};
+inline std::vector<double> device6(const DeviceSpec& d) {
+  return {d.peak_gflops, d.parallel_units, d.vector_lanes, d.cache_bytes, d.measure_overhead_ms, d.noise_std};
+}
+}  // namespace detail
+
+// true_best (oracle.cpp:90-105): exhaustive noise-free optimum, lexicographically first on ties
+inline BestConfig true_best(const DeviceSpec& device, const TaskSpec& task) {
+  const detail::SpaceArrays a(task);
+  BestConfig b;
+  b.config.values.resize(task.knobs.size());
+  const auto d6 = detail::device6(device);
+  check(moses_true_best(d6.data(), a.task4, a.domains.data(), a.sizes.data(), a.roles.data(),
+                        int32_t(task.knobs.size()), b.config.values.data(), &b.latency_ms));
+  return b;
+}
+
+// enumerate_configs + encode_batch + config_hash (space.cpp:140-197) for configs [first, first+n) of the
+// enumeration, computed on the device; host copies (row-major n x 16 features, hashes; either may be null).
+inline void encode_configs(const TaskSpec& task, uint64_t first, int64_t n, Matrix* features,
+                           std::vector<uint64_t>* hashes) {
+  const detail::SpaceArrays a(task);
+  if (features) *features = Matrix(n, 16);
+  if (hashes) hashes->assign(size_t(n), 0);
+  check(moses_encode_configs(a.task4, a.domains.data(), a.sizes.data(), a.roles.data(), int32_t(task.knobs.size()),
+                             first, n, features ? features->data.data() : nullptr,
+                             hashes ? hashes->data() : nullptr));
+}
+
 }  // namespace moseslab_gpu

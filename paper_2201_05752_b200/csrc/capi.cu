@@ -1931,6 +1931,26 @@ MOSES_API int moses_encode_configs_device(const double* task4, const int64_t* do
   });
 }
 
+MOSES_API int moses_encode_configs(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                  const int32_t* roles, int32_t n_knobs, uint64_t first, int64_t n,
+                                  double* features_out, uint64_t* hashes_out) {
+  return guarded([&] {
+    if (n < 0) fail(MOSES_ERR_INVALID_ARG, "negative count");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    Carver cv{static_cast<uint8_t*>(sc.ensure(size_t(n) * (16 * 8 + 8) + 4096))};
+    double* f = cv.take<double>(std::max<int64_t>(n, 1) * 16);
+    unsigned long long* h = cv.take<unsigned long long>(std::max<int64_t>(n, 1));
+    note_launch(encode_configs(task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs, first,
+                               n, MOSES_DTYPE_F64, features_out ? f : nullptr, 16, 16, hashes_out ? h : nullptr,
+                               nullptr, sc.st));
+    if (features_out && n)
+      MOSES_CUDA(cudaMemcpyAsync(features_out, f, sizeof(double) * n * 16, cudaMemcpyDeviceToHost, sc.st));
+    if (hashes_out && n) MOSES_CUDA(cudaMemcpyAsync(hashes_out, h, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+  });
+}
+
 MOSES_API int moses_measure_configs_device(const double* device6, int32_t repeats, const char* device_id,
                                           const char* task_id, const double* task4, const int64_t* domains,
                                           const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,

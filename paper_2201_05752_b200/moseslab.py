@@ -127,6 +127,7 @@ def lib():
                                                    C.c_uint64, i64, vp, vp, vp, vp, vp]),
         "moses_true_best": (C.c_int, [vp, vp, vp, vp, vp, i32, vp, vp]),
         "moses_train_step_pooled_async": (C.c_int, [vp, vp, i64, i32, vp, i64, vp, dbl, dbl, vp]),
+        "moses_encode_configs": (C.c_int, [vp, vp, vp, vp, i32, C.c_uint64, i64, vp, vp]),
         "moses_lottery_step_adam": (C.c_int, [vp, i32, dbl, i32, dbl, dbl, dbl, dbl, i32, dbl, vp, i64, vp]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),

@@ -127,6 +127,25 @@ int main() {
     const auto idx = topk({0.5, 0.9, 0.5, 0.1, 0.9, 0.5}, 4);
     CHECK(idx.size() == 4 && idx[0] == 1 && idx[1] == 4 && idx[2] == 0 && idx[3] == 2);
   }
+  // test_oracle.cpp:313-335: frozen optimum of conv3x3_64 on the shipped server device (true_best_default.json)
+  {
+    TaskSpec t{"conv3x3_64", 2.0, 8.0, 9.0, 6.0, default_knob_template()};
+    DeviceSpec d{"server", 8000.0, 16.0, 8.0, 2000000.0, 2.0, 0.05, 3};
+    const BestConfig b = true_best(d, t);
+    CHECK((b.config.values == std::vector<int64_t>{8, 64, 64, 8, 16}));
+    CHECK(std::abs(b.latency_ms - 0.2500062537535723) < 1e-14 * 0.25);
+  }
+  // test_space.cpp:142-157, 206-208: feature reference vector and config hash of {16,32,16,8,32}
+  {
+    TaskSpec t{"conv3x3_64", 2.0, 8.0, 9.0, 5.0, default_knob_template()};
+    const uint64_t idx = ((((4ull * 7 + 5) * 4 + 1) * 5 + 3) * 9 + 5);  // mixed radix of (16,32,16,8,32)
+    Matrix f;
+    std::vector<uint64_t> h;
+    encode_configs(t, idx, 1, &f, &h);
+    CHECK(std::abs(f(0, 0) - 0.66666666666666663) < 1e-14 && std::abs(f(0, 2) - 0.40874628412503389) < 1e-14);
+    CHECK(std::abs(f(0, 7) - 0.10034333188799373) < 1e-14 && f(0, 12) == 0.0);
+    CHECK(h[0] == 0xc27c832e9cdb768dull);
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
