@@ -1304,7 +1304,18 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
     MOSES_CUDA(cudaStreamWaitEvent(m->st, a.ready, 0));
     MOSES_CUDA(cudaGraphLaunch(a.exec, m->st));
     MOSES_CUDA(cudaEventRecord(a.free, m->st));
-    if (loss_out) MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    if (loss_out) {
+      // pinned (mapped) destination: a one-thread kernel stores the loss over PCIe — an 8-byte D2H
+      // memcpy would queue behind the next batch's upload on the copy engines (~20 us bubble)
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, loss_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+          pa.devicePointer != nullptr) {
+        store_scalar_f64(m->dscal, static_cast<double*>(pa.devicePointer), m->st);
+      } else {
+        cudaGetLastError();
+        MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      }
+    }
     a.used = true;
     ++m->async_steps;
     note_launch(g_graph_kernels > 0 ? g_graph_kernels : 10);

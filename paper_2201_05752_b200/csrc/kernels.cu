@@ -189,6 +189,7 @@ __global__ void pack_pooled_kernel(const double* __restrict__ xs, const double* 
   for (long long r = n_stmt + tid; r < rows_pad; r += nthr) seg_rows[r] = -1;
 }
 
+__global__ void store_scalar_f64_kernel(const double* src, double* dst) { *dst = *src; }
 __global__ void advance_counter_kernel(long long* c) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *c += 1;
 }
@@ -1276,6 +1277,10 @@ void pack_pooled(const double* xs, const double* ys, const long long* offs, cons
 }
 template void pack_pooled<__nv_bfloat16>(const double*, const double*, const long long*, const long long*, int,
                                          long long, __nv_bfloat16*, long long, float*, long long*, int*, cudaStream_t);
+void store_scalar_f64(const double* src, double* dst, cudaStream_t s) {
+  store_scalar_f64_kernel<<<1, 1, 0, s>>>(src, dst);
+  MOSES_CUDA(cudaGetLastError());
+}
 void advance_counter(long long* c, cudaStream_t s) {
   advance_counter_kernel<<<1, 32, 0, s>>>(c);
   MOSES_CUDA(cudaGetLastError());

@@ -162,6 +162,8 @@ template <typename T>
 void synth_features(unsigned long long seed, long long row0, long long n, int D, T* dst, long long ld, cudaStream_t st);
 void synth_labels(unsigned long long seed, long long row0, long long n, float* dst, cudaStream_t st);
 
+// device -> mapped pinned host scalar without a copy engine
+void store_scalar_f64(const double* src, double* dst, cudaStream_t s);
 // host-input pooled training step: staging slot -> packed rows, labels, segments (kernels.cu)
 template <typename T>
 void pack_pooled(const double* xs, const double* ys, const long long* offs, const long long* dims_dev, int D,
