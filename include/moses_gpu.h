@@ -44,10 +44,13 @@ enum {
   MOSES_ERR_SHAPE_MISMATCH = 7,        /* ErrorCode::ShapeMismatch */
   MOSES_ERR_VERSION_MISMATCH = 8,      /* ErrorCode::VersionMismatch */
   MOSES_ERR_CORRUPT_STREAM = 9,        /* ErrorCode::CorruptStream */
+  MOSES_ERR_EMPTY_DATASET = 10,        /* ErrorCode::EmptyDataset */
   MOSES_ERR_INVALID_RATIO = 11,        /* ErrorCode::InvalidRatio */
   MOSES_ERR_UNNORMALIZED_THRESHOLD = 12, /* ErrorCode::UnnormalizedThreshold */
   MOSES_ERR_ADVERSARY_DISABLED = 13,   /* ErrorCode::AdversaryDisabled */
   MOSES_ERR_UNSTABLE_DECAY = 14,       /* ErrorCode::UnstableDecay */
+  MOSES_ERR_PARSE = 22,                /* ErrorCode::ParseError */
+  MOSES_ERR_MISSING_FIELD = 23,        /* ErrorCode::MissingField */
   MOSES_ERR_IO = 24,                   /* ErrorCode::IoError */
   MOSES_ERR_CUDA = 100,
   MOSES_ERR_NO_DEVICE = 101,
@@ -63,6 +66,7 @@ enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1, MOSES_DTYPE_F64 = 2 };
 
 typedef struct moses_model* moses_model_t;
 typedef struct moses_adversary* moses_adversary_t;
+typedef struct moses_records* moses_records_t;
 
 MOSES_API const char* moses_last_error(void);
 MOSES_API const char* moses_version(void);
@@ -264,6 +268,68 @@ MOSES_API int moses_measure_configs_device(const double* device6, int32_t repeat
 MOSES_API int moses_true_best(const double* device6, const double* task4, const int64_t* domains,
                               const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
                               int64_t* best_values, double* best_latency);
+
+/* ------------------------------------------------------------------ training-data pipeline */
+/* generate_dataset (data.cpp:49-65) for ONE task: `samples` configurations drawn by
+ * RngStream(KeyBuilder(seed, "gen", task_id)) through sample_config (space.cpp:94-100), their feature
+ * rows (encode_features, packed layout as moses_encode_configs_device), knob values (samples x
+ * n_knobs), and measure() outputs (oracle.cpp:65-88) — throughput / latency / wall cost in double,
+ * label = float throughput. Any output may be NULL. A store over several tasks is the concatenation
+ * in task order; its seq is the running row index (data.cpp:53-63). Default stream. */
+MOSES_API int moses_generate_dataset_device(const double* device6, int32_t repeats, const char* device_id,
+                                           const char* task_id, const double* task4, const int64_t* domains,
+                                           const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                                           int64_t samples, uint64_t seed, int32_t dtype, void* feat_dev, int64_t ld,
+                                           int32_t D, int64_t* values_dev, double* throughput_dev,
+                                           double* latency_dev, double* wall_cost_dev, float* label_dev);
+/* encode_features over device rows of knob values (n x n_knobs int64): validate_config
+ * (space.cpp:69-81) then the feature row. A value outside its domain fails with
+ * MOSES_ERR_INVALID_CONFIG and *bad_row (host, may be NULL) = the first offending row. */
+MOSES_API int moses_encode_values_device(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                        const int32_t* roles, int32_t n_knobs, const int64_t* values_dev, int64_t n,
+                                        int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
+                                        int64_t* bad_row);
+/* pretrain's per-epoch seed KeyBuilder(seed, "epoch", epoch) (tuner.cpp:136-139). */
+MOSES_API uint64_t moses_epoch_seed(uint64_t seed, uint64_t epoch);
+/* make_ranking_batches (data.cpp:128-164) as a plan of row indices. record_task[i] indexes
+ * task_ids (the ids the shuffle keys hash). Outputs (host, any may be NULL): rows_out (n_records),
+ * batch_off (n_batches + 1 <= n_records / 2 + 1), batch_task (n_batches), n_batches, dropped
+ * singleton chunks. Batch b covers rows_out[batch_off[b] .. batch_off[b+1]). */
+MOSES_API int moses_ranking_plan(const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                int32_t n_task_ids, int32_t batch_size, uint64_t seed, int64_t* rows_out,
+                                int64_t* batch_off, int32_t* batch_task, int64_t* n_batches, int64_t* dropped);
+/* sample_replay_features' row choice (data.cpp:166-183): min(n_records, size) rows, no replacement. */
+MOSES_API int moses_replay_rows(int64_t n_records, int64_t size, uint64_t seed, int64_t* rows_out, int64_t* n_out);
+/* One pretrain epoch over a plan (tuner.cpp:140-155): for each batch in order, gather its rows of the
+ * device-resident packed dataset (x_base rows of stride moses_packed_ld, labels y_base) -> gradients
+ * -> momentum update. Plan arrays are host memory (moses_ranking_plan's output); mean_loss (host,
+ * may be NULL) = mean of the per-batch losses (0 for an empty plan). Full-size batches replay one
+ * CUDA graph (bf16 / tf32 handles). */
+MOSES_API int moses_train_plan_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                     int64_t n_records, const int64_t* rows, const int64_t* batch_off,
+                                     int64_t n_batches, double learning_rate, double momentum, double* mean_loss);
+/* Line-delimited record files (data.cpp:67-126). moses_records_read fails with MOSES_ERR_IO,
+ * MOSES_ERR_PARSE (message names "<path>:line N") or MOSES_ERR_MISSING_FIELD. */
+MOSES_API int moses_records_create(moses_records_t* out);
+MOSES_API int moses_records_read(const char* path, moses_records_t* out);
+MOSES_API void moses_records_destroy(moses_records_t r);
+/* append n records of one task / device, n_values knob values each (values: n x n_values) */
+MOSES_API int moses_records_append(moses_records_t r, const char* task_id, const char* device_id, int64_t n,
+                                  int32_t n_values, const int64_t* values, const double* throughput,
+                                  const double* latency, const double* wall_cost, const uint64_t* seq);
+MOSES_API int moses_records_write(moses_records_t r, const char* path);
+MOSES_API int moses_records_shape(moses_records_t r, int64_t* n_records, int64_t* n_values, int32_t* n_tasks,
+                                 int32_t* n_devices);
+/* interned ids in first-appearance order; NULL when out of range */
+MOSES_API const char* moses_records_task_id(moses_records_t r, int32_t t);
+MOSES_API const char* moses_records_device_id(moses_records_t r, int32_t d);
+/* flat copies into caller buffers (pinned host memory for a following upload); any may be NULL.
+ * value_off: n_records + 1 offsets into values. */
+MOSES_API int moses_records_export(moses_records_t r, int32_t* task_index, int32_t* device_index, int64_t* value_off,
+                                  int64_t* values, double* throughput, double* latency, double* wall_cost,
+                                  uint64_t* seq);
+/* Test hook: force the sequential sampling walk in moses_generate_dataset_device. */
+MOSES_API int moses_debug_force_serial_sampling(int32_t on);
 
 /* ------------------------------------------------------------------ synthetic TenSet-shaped data (bench) */
 /* Rows [row0, row0+n) of the keyed SplitMix64 generator, written in the packed layout. */

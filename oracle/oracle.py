@@ -458,3 +458,117 @@ def true_best(device, task, knobs):
     _check(lib().orc_true_best(_p(_dev6(device)), _p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs),
                                _p(v), _p(lat)))
     return v.tolist(), float(lat[0])
+
+
+# ---------------------------------------------------------------- training-data pipeline (data.cpp, tuner.cpp)
+# Pure-Python restatement (independent of the C++ oracle and of the library): KeyBuilder / RngStream
+# (rng.hpp), make_ranking_batches (data.cpp:128-164), sample_replay_features rows (data.cpp:166-183),
+# generate_dataset (data.cpp:49-65), pretrain's epoch seed and epoch loop (tuner.cpp:130-156).
+_M64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+def key_builder(*parts) -> int:
+    """KeyBuilder: FNV-1a over 8 little-endian bytes per integer, UTF-8 bytes + NUL per string."""
+    h = 0xCBF29CE484222325
+    for p in parts:
+        data = (p.encode() + b"\0") if isinstance(p, str) else int(p & _M64).to_bytes(8, "little")
+        for b in data:
+            h = ((h ^ b) * 0x100000001B3) & _M64
+    return h
+
+
+class RngStream:
+    def __init__(self, key: int):
+        self.s = key & _M64
+
+    def next_u64(self) -> int:
+        self.s = (self.s + _GOLDEN) & _M64
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        return z ^ (z >> 31)
+
+    def below(self, n: int) -> int:
+        t = ((1 << 64) - n) % n
+        while True:
+            r = self.next_u64()
+            if r >= t:
+                return r % n
+
+
+def _shuffle_with(items, rng):  # data.cpp:16-22
+    for i in range(len(items), 1, -1):
+        j = rng.below(i)
+        items[i - 1], items[j] = items[j], items[i - 1]
+
+
+def epoch_seed(seed: int, epoch: int) -> int:  # tuner.cpp:136-139
+    return key_builder(seed, "epoch", epoch)
+
+
+def make_ranking_batches(record_task_ids, batch_size: int, seed: int):
+    """data.cpp:128-164 over the records' task ids: ([(task_id, [row indices])...], dropped_singletons)."""
+    if batch_size < 2:
+        raise OracleError(2, "batch size must be at least 2")
+    order = list(dict.fromkeys(record_task_ids))
+    batches, dropped = [], 0
+    for tid in order:
+        rows = [i for i, t in enumerate(record_task_ids) if t == tid]
+        _shuffle_with(rows, RngStream(key_builder(seed, "shuffle", tid)))
+        for s in range(0, len(rows), batch_size):
+            chunk = rows[s:s + batch_size]
+            if len(chunk) < 2:
+                dropped += 1
+                continue
+            batches.append((tid, chunk))
+    _shuffle_with(batches, RngStream(key_builder(seed, "order")))
+    return batches, dropped
+
+
+def replay_rows(n_records: int, size: int, seed: int):  # data.cpp:166-183
+    if n_records <= 0:
+        raise OracleError(10, "empty record store")
+    if size < 1:
+        raise OracleError(2, "replay size must be positive")
+    rows = list(range(n_records))
+    _shuffle_with(rows, RngStream(key_builder(seed, "replay")))
+    return rows[:min(n_records, size)]
+
+
+def sample_config_indices(seed: int, task_id: str, knobs, samples: int):
+    """generate_dataset's draws for one task (data.cpp:55-61, sample_config space.cpp:94-100) as
+    enumeration indices (last knob fastest)."""
+    rng = RngStream(key_builder(seed, "gen", task_id))
+    out = []
+    for _ in range(samples):
+        idx = 0
+        for _, dom in knobs:
+            idx = idx * len(dom) + rng.below(len(dom))
+        out.append(idx)
+    return out
+
+
+def generate_dataset(device, tasks, knobs, samples_per_task: int, seed: int):
+    """data.cpp:49-65. tasks = [(task_id, task4)]. Returns a list of record dicts (the reference's
+    MeasurementRecord fields) plus a 'features' entry (encode_features)."""
+    recs, seq = [], 0
+    for tid, task in tasks:
+        for idx in sample_config_indices(seed, tid, knobs, samples_per_task):
+            f, _, v = encode_configs(task, knobs, idx, 1)
+            _, thr, lat, wall = measure_configs(device, tid, task, knobs, seed, idx, 1)
+            recs.append({"task_id": tid, "values": [int(x) for x in v[0]], "throughput_gflops": float(thr[0]),
+                         "latency_ms": float(lat[0]), "wall_cost_ms": float(wall[0]), "device_id": device["id"],
+                         "seq": seq, "features": f[0]})
+            seq += 1
+    return recs
+
+
+def pretrain_epoch(dims, w, mom, features, labels, batches, lr, mu=0.9, threads=1):
+    """tuner.cpp:146-151: for each planned batch, gradients + momentum update (float64). Returns
+    (w, mom, mean batch loss)."""
+    losses = [train_step_f64(dims, w, mom, features[rows], labels[rows], lr, mu, threads) for _, rows in batches]
+    acc = 0.0
+    for x in losses:  # loss_sum += loss (tuner.cpp:148-150); Python's sum() would compensate
+        acc += x
+    return w, mom, (acc / len(losses) if losses else 0.0)

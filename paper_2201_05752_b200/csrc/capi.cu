@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "pipeline.cuh"
 
 namespace moses {
 
@@ -213,6 +214,21 @@ struct moses_model {
   } aslot[2];
   cudaStream_t st_copy = nullptr;
   long long async_steps = 0;
+  // epoch over a ranking-batch plan (moses_train_plan_device)
+  struct PlanState {
+    long long* rows = nullptr;     // device row indices
+    long long* off = nullptr;      // device batch offsets
+    long long* counter = nullptr;  // device batch index
+    double* loss_sum = nullptr;    // device running sum of batch losses
+    float* stage = nullptr;        // FP32 handles: gathered fp32 rows before the hi/lo split
+    long long cap_rows = 0, cap_b = 0;
+    cudaGraphExec_t exec = nullptr;
+    const void* x = nullptr;
+    const float* y = nullptr;
+    long long ldx = 0, batch = 0;
+    float lr = 0.f, mu = 0.f;
+    long long graph_kernels = 0;
+  } plan;
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
   void* lot_ws = nullptr;          // fused lottery-step workspace (lottery.cu)
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
@@ -281,6 +297,12 @@ struct moses_model {
       if (a.free) cudaEventDestroy(a.free);
     }
     if (st_copy) cudaStreamDestroy(st_copy);
+    if (plan.exec) cudaGraphExecDestroy(plan.exec);
+    dfree(plan.rows);
+    dfree(plan.off);
+    dfree(plan.counter);
+    dfree(plan.loss_sum);
+    dfree(plan.stage);
     dfree(dcounter);
     dfree(gbias);
     dfree(lot_ws);
@@ -1985,6 +2007,271 @@ MOSES_API int moses_true_best(const double* device6, const double* task4, const 
     note_launch(true_best(device6, task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs,
                           reinterpret_cast<long long*>(best_values), best_latency, sc.st));
   });
+}
+
+// ---------------------------------------------------------------- training-data pipeline
+static int out_kind_of(int32_t dtype) {
+  if (dtype != MOSES_DTYPE_F32 && dtype != MOSES_DTYPE_BF16 && dtype != MOSES_DTYPE_F64)
+    fail(MOSES_ERR_INVALID_ARG, "unknown dtype");
+  return dtype;
+}
+MOSES_API int moses_generate_dataset_device(const double* device6, int32_t repeats, const char* device_id,
+                                           const char* task_id, const double* task4, const int64_t* domains,
+                                           const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs,
+                                           int64_t samples, uint64_t seed, int32_t dtype, void* feat_dev, int64_t ld,
+                                           int32_t D, int64_t* values_dev, double* throughput_dev,
+                                           double* latency_dev, double* wall_cost_dev, float* label_dev) {
+  return guarded([&] {
+    const int ok = out_kind_of(dtype);
+    note_launch(generate_task_dataset(device6, repeats, device_id, task_id, task4,
+                                      reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs, samples,
+                                      seed, ok, feat_dev, ld, D, reinterpret_cast<long long*>(values_dev),
+                                      throughput_dev, latency_dev, wall_cost_dev, label_dev, nullptr, nullptr));
+  });
+}
+MOSES_API int moses_encode_values_device(const double* task4, const int64_t* domains, const int32_t* domain_sizes,
+                                        const int32_t* roles, int32_t n_knobs, const int64_t* values_dev, int64_t n,
+                                        int32_t dtype, void* feat_dev, int64_t ld, int32_t D, uint64_t* hash_dev,
+                                        int64_t* bad_row) {
+  long long bad = -1;
+  const int rc = guarded([&] {
+    const int ok = out_kind_of(dtype);
+    if (feat_dev != nullptr && (D < 10 || ld < D)) fail(MOSES_ERR_INVALID_ARG, "feature rows need D >= 10 and ld >= D");
+    note_launch(encode_values(task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs,
+                              reinterpret_cast<const long long*>(values_dev), n, ok, feat_dev, ld, D,
+                              reinterpret_cast<unsigned long long*>(hash_dev), nullptr, &bad, nullptr));
+  });
+  if (bad_row) *bad_row = bad;
+  return rc;
+}
+MOSES_API uint64_t moses_epoch_seed(uint64_t seed, uint64_t epoch) { return epoch_seed(seed, epoch); }
+MOSES_API int moses_ranking_plan(const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                int32_t n_task_ids, int32_t batch_size, uint64_t seed, int64_t* rows_out,
+                                int64_t* batch_off, int32_t* batch_task, int64_t* n_batches, int64_t* dropped) {
+  return guarded([&] {
+    long long drop = 0;
+    const long long nb = ranking_plan(record_task, n_records, task_ids, n_task_ids, batch_size, seed,
+                                      reinterpret_cast<long long*>(rows_out), reinterpret_cast<long long*>(batch_off),
+                                      batch_task, &drop);
+    if (n_batches) *n_batches = nb;
+    if (dropped) *dropped = drop;
+  });
+}
+MOSES_API int moses_replay_rows(int64_t n_records, int64_t size, uint64_t seed, int64_t* rows_out, int64_t* n_out) {
+  return guarded([&] {
+    const long long k = replay_rows(n_records, size, seed, reinterpret_cast<long long*>(rows_out));
+    if (n_out) *n_out = k;
+  });
+}
+
+MOSES_API int moses_train_plan_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                     int64_t n_records, const int64_t* rows, const int64_t* batch_off,
+                                     int64_t n_batches, double lr, double mu, double* mean_loss) {
+  return guarded([&] {
+    require_model(m);
+    if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
+    if (n_batches < 0) fail(MOSES_ERR_INVALID_ARG, "negative batch count");
+    if (n_batches == 0) {
+      if (mean_loss) *mean_loss = 0.0;  // tuner.cpp:152-154: empty epoch
+      return;
+    }
+    if (rows == nullptr || batch_off == nullptr || x_base == nullptr || y_base == nullptr)
+      fail(MOSES_ERR_INVALID_ARG, "null plan or dataset");
+    if (batch_off[0] != 0) fail(MOSES_ERR_INVALID_ARG, "batch_off[0] must be 0");
+    long long B = 0, nfull = 0;
+    for (int64_t b = 0; b < n_batches; ++b) {
+      const long long len = batch_off[b + 1] - batch_off[b];
+      if (len < 2) fail(MOSES_ERR_INVALID_ARG, "plan batch " + std::to_string(b) + " has fewer than 2 rows");
+      B = std::max(B, len);
+    }
+    check_rows(m, B);
+    for (int64_t b = 0; b < n_batches; ++b) nfull += (batch_off[b + 1] - batch_off[b]) == B;
+    const long long total = batch_off[n_batches];
+    for (long long i = 0; i < total; ++i)
+      if (rows[i] < 0 || rows[i] >= n_records)
+        fail(MOSES_ERR_SHAPE_MISMATCH, "plan row " + std::to_string(rows[i]) + " outside the dataset");
+    auto& ps = m->plan;
+    if (total > ps.cap_rows || n_batches + 1 > ps.cap_b) {
+      if (ps.exec) {
+        cudaGraphExecDestroy(ps.exec);
+        ps.exec = nullptr;
+      }
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      if (total > ps.cap_rows) {
+        dfree(ps.rows);
+        ps.rows = dalloc<long long>(total);
+        ps.cap_rows = total;
+      }
+      if (n_batches + 1 > ps.cap_b) {
+        dfree(ps.off);
+        ps.off = dalloc<long long>(n_batches + 1);
+        ps.cap_b = n_batches + 1;
+      }
+    }
+    if (!ps.counter) ps.counter = dalloc<long long>(1);
+    if (!ps.loss_sum) ps.loss_sum = dalloc<double>(1);
+    MOSES_CUDA(cudaMemcpyAsync(ps.rows, rows, sizeof(long long) * total, cudaMemcpyHostToDevice, m->st));
+    MOSES_CUDA(cudaMemcpyAsync(ps.off, batch_off, sizeof(long long) * (n_batches + 1), cudaMemcpyHostToDevice, m->st));
+    MOSES_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(long long), m->st));
+    MOSES_CUDA(cudaMemsetAsync(ps.loss_sum, 0, sizeof(double), m->st));
+    const long long row_bytes = ldx * m->esz;
+    const SgdFuse fz{float(lr), float(mu)};
+    if (m->split && !ps.stage) ps.stage = dalloc<float>(m->cap * m->ld[0]);
+    auto step = [&](long long n) {
+      if (m->split) {  // 3xTF32 operands: hi/lo split of the gathered fp32 rows
+        gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, n, ps.stage, m->labels, m->st);
+        pack_rows_f32<float>(ps.stage, n, m->dims[0], ldx, static_cast<float*>(m->act[0]), m->ld[0], m->st,
+                             m->act_lo(0));
+        note_launch(1);
+      } else {
+        gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st);
+      }
+      if (!gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, &fz)) {
+        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+        m->post_update();
+        note_launch(1);
+      }
+      accum_f64(m->dscal, ps.loss_sum, m->st);
+      advance_counter(ps.counter, m->st);
+      note_launch(3);
+    };
+    // full-size batches replay one CUDA graph (captured once per dataset / size / hyper-parameters)
+    const bool want_graph = !m->split && nfull >= 4;
+    if (want_graph && !(ps.exec && ps.x == x_base && ps.y == y_base && ps.ldx == ldx && ps.batch == B &&
+                        ps.lr == float(lr) && ps.mu == float(mu))) {
+      if (ps.exec) {
+        cudaGraphExecDestroy(ps.exec);
+        ps.exec = nullptr;
+      }
+      // eager warm-up without the update (configures kernels; parameters untouched)
+      gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, B, m->act[0], m->labels, m->st);
+      gradients_core(m, m->act[0], m->ld[0], m->labels, B, nullptr, 0.0);
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      const long long before = moses_kernel_launches();
+      cudaGraph_t graph;
+      MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      try {
+        step(B);
+      } catch (...) {
+        cudaStreamEndCapture(m->st, &graph);
+        throw;
+      }
+      MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+      ps.graph_kernels = moses_kernel_launches() - before;
+      note_launch(-ps.graph_kernels);  // captured, not launched
+      MOSES_CUDA(cudaGraphInstantiate(&ps.exec, graph, 0));
+      MOSES_CUDA(cudaGraphDestroy(graph));
+      ps.x = x_base;
+      ps.y = y_base;
+      ps.ldx = ldx;
+      ps.batch = B;
+      ps.lr = float(lr);
+      ps.mu = float(mu);
+    }
+    for (int64_t b = 0; b < n_batches; ++b) {
+      const long long len = batch_off[b + 1] - batch_off[b];
+      if (want_graph && len == B) {
+        MOSES_CUDA(cudaGraphLaunch(ps.exec, m->st));
+        note_launch(ps.graph_kernels);
+      } else {
+        step(len);
+      }
+    }
+    if (mean_loss) {
+      double sum = 0.0;
+      MOSES_CUDA(cudaMemcpyAsync(&sum, ps.loss_sum, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      *mean_loss = sum / double(n_batches);
+    }
+  });
+}
+
+struct moses_records : moses::Records {};
+MOSES_API int moses_records_create(moses_records_t* out) {
+  return guarded([&] {
+    if (!out) fail(MOSES_ERR_INVALID_ARG, "null output");
+    *out = new moses_records();
+  });
+}
+MOSES_API int moses_records_read(const char* path, moses_records_t* out) {
+  return guarded([&] {
+    if (!out) fail(MOSES_ERR_INVALID_ARG, "null output");
+    *out = nullptr;
+    std::unique_ptr<Records> r(Records::read(path));
+    auto* h = new moses_records();
+    static_cast<Records&>(*h) = std::move(*r);
+    *out = h;
+  });
+}
+MOSES_API void moses_records_destroy(moses_records_t r) { delete r; }
+MOSES_API int moses_records_append(moses_records_t r, const char* task_id, const char* device_id, int64_t n,
+                                  int32_t n_values, const int64_t* values, const double* thr, const double* lat,
+                                  const double* wall, const uint64_t* seq) {
+  return guarded([&] {
+    if (!r || !task_id || !device_id || n < 0 || n_values < 0 || (n > 0 && (!thr || !lat || !wall || !seq)) ||
+        (n > 0 && n_values > 0 && !values))
+      fail(MOSES_ERR_INVALID_ARG, "invalid record batch");
+    auto intern = [](std::vector<std::string>& tab, std::map<std::string, int>& ix, const std::string& s) {
+      auto it = ix.find(s);
+      if (it != ix.end()) return it->second;
+      tab.push_back(s);
+      ix.emplace(s, int(tab.size()) - 1);
+      return int(tab.size()) - 1;
+    };
+    if (n == 0) return;
+    const int t = intern(r->task_ids, r->task_ix, task_id), d = intern(r->device_ids, r->device_ix, device_id);
+    for (int64_t i = 0; i < n; ++i) {
+      r->task.push_back(t);
+      r->device.push_back(d);
+      r->value_off.push_back(r->value_off.back() + n_values);
+      r->values.insert(r->values.end(), values + i * n_values, values + (i + 1) * n_values);
+      r->throughput.push_back(thr[i]);
+      r->latency.push_back(lat[i]);
+      r->wall_cost.push_back(wall[i]);
+      r->seq.push_back(seq[i]);
+    }
+  });
+}
+MOSES_API int moses_records_write(moses_records_t r, const char* path) {
+  return guarded([&] {
+    if (!r) fail(MOSES_ERR_INVALID_ARG, "null records");
+    r->write(path);
+  });
+}
+MOSES_API int moses_records_shape(moses_records_t r, int64_t* n_records, int64_t* n_values, int32_t* n_tasks,
+                                 int32_t* n_devices) {
+  return guarded([&] {
+    if (!r) fail(MOSES_ERR_INVALID_ARG, "null records");
+    if (n_records) *n_records = r->size();
+    if (n_values) *n_values = (int64_t)r->values.size();
+    if (n_tasks) *n_tasks = int32_t(r->task_ids.size());
+    if (n_devices) *n_devices = int32_t(r->device_ids.size());
+  });
+}
+MOSES_API const char* moses_records_task_id(moses_records_t r, int32_t t) {
+  return (r && t >= 0 && t < int32_t(r->task_ids.size())) ? r->task_ids[t].c_str() : nullptr;
+}
+MOSES_API const char* moses_records_device_id(moses_records_t r, int32_t d) {
+  return (r && d >= 0 && d < int32_t(r->device_ids.size())) ? r->device_ids[d].c_str() : nullptr;
+}
+MOSES_API int moses_records_export(moses_records_t r, int32_t* task_index, int32_t* device_index, int64_t* value_off,
+                                  int64_t* values, double* thr, double* lat, double* wall, uint64_t* seq) {
+  return guarded([&] {
+    if (!r) fail(MOSES_ERR_INVALID_ARG, "null records");
+    const size_t n = size_t(r->size());
+    if (task_index) std::copy(r->task.begin(), r->task.end(), task_index);
+    if (device_index) std::copy(r->device.begin(), r->device.end(), device_index);
+    if (value_off) std::copy(r->value_off.begin(), r->value_off.end(), value_off);
+    if (values) std::copy(r->values.begin(), r->values.end(), values);
+    if (thr) std::copy_n(r->throughput.begin(), n, thr);
+    if (lat) std::copy_n(r->latency.begin(), n, lat);
+    if (wall) std::copy_n(r->wall_cost.begin(), n, wall);
+    if (seq) std::copy_n(r->seq.begin(), n, seq);
+  });
+}
+MOSES_API int moses_debug_force_serial_sampling(int32_t on) {
+  debug_force_serial_sampling(on != 0);
+  return MOSES_OK;
 }
 
 MOSES_API int moses_synth_features_device(uint64_t seed, int64_t row0, int64_t n, int32_t D, int32_t dtype, void* dst,

@@ -135,6 +135,26 @@ __global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long lon
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < batch; i += (long long)gridDim.x * blockDim.x)
     ydst[i] = y_base[b * batch + i];
 }
+// Plan batch b = *counter: rows rows[off[b] + r] (r < n) of a packed dataset -> dst rows [0, n),
+// labels -> ydst. One warp per row, 16-byte lanes.
+__global__ void gather_plan_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
+                                   const long long* __restrict__ rows, const long long* __restrict__ off,
+                                   const long long* __restrict__ counter, long long n, uint8_t* __restrict__ dst,
+                                   float* __restrict__ ydst) {
+  ptx::pdl_launch_dependents();
+  const long long base = off[*counter];
+  const int lane = threadIdx.x & 31;
+  const long long w16 = row_bytes / 16;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long src_row = rows[base + r];
+    const uint4* src = reinterpret_cast<const uint4*>(x_base + src_row * row_bytes);
+    uint4* d = reinterpret_cast<uint4*>(dst + r * row_bytes);
+    for (long long c = lane; c < w16; c += 32) d[c] = src[c];
+    if (lane == 0) ydst[r] = y_base[src_row];
+  }
+}
+__global__ void accum_f64_kernel(const double* __restrict__ src, double* __restrict__ dst) { *dst += *src; }
 // TenSet-shaped batch: programs [b*B, (b+1)*B) of a CSR-packed statement dataset -> statement rows
 // [0, R_b) of dst, batch-relative offsets, program of each row (-1 on padding rows up to rows_pad).
 __global__ void gather_pooled_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
@@ -1256,6 +1276,18 @@ void gather_batch(const void* x_base, long long row_bytes, const float* y_base, 
   if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
   gather_batch_kernel<<<grid_for(batch * row_bytes / 16, 256), 256, 0, s>>>(
       static_cast<const uint8_t*>(x_base), row_bytes, y_base, counter, nb, batch, static_cast<uint8_t*>(dst), ydst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void gather_plan(const void* x_base, long long row_bytes, const float* y_base, const long long* rows, const long long* off,
+                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s) {
+  if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
+  gather_plan_kernel<<<std::max(1, ceil_div(n * 32, 256)), 256, 0, s>>>(static_cast<const uint8_t*>(x_base), row_bytes,
+                                                                         y_base, rows, off, counter, n,
+                                                                         static_cast<uint8_t*>(dst), ydst);
+  MOSES_CUDA(cudaGetLastError());
+}
+void accum_f64(const double* src, double* dst, cudaStream_t s) {
+  accum_f64_kernel<<<1, 1, 0, s>>>(src, dst);
   MOSES_CUDA(cudaGetLastError());
 }
 void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,

@@ -33,6 +33,10 @@ void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, lo
 void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
                   long long batch, void* dst, float* ydst, cudaStream_t s);
 void advance_counter(long long* c, cudaStream_t s);
+// plan batch *counter: rows[off[b] .. off[b] + n) of a packed dataset -> dst, labels -> ydst
+void gather_plan(const void* x_base, long long row_bytes, const float* y_base, const long long* rows, const long long* off,
+                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s);
+void accum_f64(const double* src, double* dst, cudaStream_t s);  // *dst += *src (one thread)
 void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,
                    const long long* counter, long long nb, long long B, long long rows_pad, void* dst, float* ydst,
                    long long* seg_off, int* seg_rows, cudaStream_t s);
@@ -180,5 +184,16 @@ int true_best(const double* dev6, const double* task4, const long long* domains,
 int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
                    unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
                    unsigned long long* hash, long long* values_out, cudaStream_t st);
+// generate_dataset for one task (data.cpp:49-65): keyed sample_config draws, features, measure() labels
+int generate_task_dataset(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                          const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                          long long samples, unsigned long long seed, int out_kind, void* feat, long long ld, int D,
+                          long long* values_out, double* thr, double* lat, double* wall, float* label,
+                          unsigned long long* idx_out, cudaStream_t st);
+void debug_force_serial_sampling(bool on);
+// validate_config + encode_features over device rows of knob values (space.cpp:69-81,140-159)
+int encode_values(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                  const long long* values, long long n, int out_kind, void* feat, long long ld, int D,
+                  unsigned long long* hash, unsigned long long* idx_out, long long* bad_row, cudaStream_t st);
 
 }  // namespace moses

@@ -52,9 +52,10 @@ template <typename T>
 __global__ void __launch_bounds__(256) encode_configs_kernel(const __grid_constant__ SpaceArgs a,
                                                              unsigned long long first, long long n, T* __restrict__ feat,
                                                              long long ld, int D, unsigned long long* __restrict__ hash,
-                                                             long long* __restrict__ values_out) {
+                                                             long long* __restrict__ values_out,
+                                                             const unsigned long long* __restrict__ idx_list) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned long long idx = first + (unsigned long long)i;
+    unsigned long long idx = idx_list ? idx_list[i] : first + (unsigned long long)i;
     long long v[kSpaceMaxKnobs];
     unsigned digit[kSpaceMaxKnobs];
     if (idx >> 32) {  // mixed-radix digits, last knob fastest
@@ -178,12 +179,13 @@ static unsigned long long fill_space(SpaceArgs& a, const long long* domains, con
   return space;
 }
 
-int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
-                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
-                   unsigned long long* hash, long long* values_out, cudaStream_t st) {
+static int encode_impl(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                       unsigned long long first, const unsigned long long* idx_list, long long n, int out_kind,
+                       void* feat, long long ld, int D, unsigned long long* hash, long long* values_out,
+                       cudaStream_t st) {
   SpaceArgs a{};
   const unsigned long long space = fill_space(a, domains, sizes, roles, nk);
-  if (n < 0 || first > space || (unsigned long long)n > space - first)
+  if (n < 0 || (idx_list == nullptr && (first > space || (unsigned long long)n > space - first)))
     fail(MOSES_ERR_SHAPE_MISMATCH, "config range exceeds the knob space");
   a.bytes_per_unit = task4[1];
   a.f7 = std::clamp(std::log10(task4[0]) / 3.0, 0.0, 1.0);  // space.cpp:154
@@ -235,13 +237,20 @@ int encode_configs(const double* task4, const long long* domains, const int* siz
   const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
   if (out_kind == 1)
     encode_configs_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(a, first, n, static_cast<__nv_bfloat16*>(feat), ld, D,
-                                                              hash, values_out);
+                                                              hash, values_out, idx_list);
   else if (out_kind == 2)
-    encode_configs_kernel<double><<<grid, 256, 0, st>>>(a, first, n, static_cast<double*>(feat), ld, D, hash, values_out);
+    encode_configs_kernel<double><<<grid, 256, 0, st>>>(a, first, n, static_cast<double*>(feat), ld, D, hash, values_out,
+                                                       idx_list);
   else
-    encode_configs_kernel<float><<<grid, 256, 0, st>>>(a, first, n, static_cast<float*>(feat), ld, D, hash, values_out);
+    encode_configs_kernel<float><<<grid, 256, 0, st>>>(a, first, n, static_cast<float*>(feat), ld, D, hash, values_out,
+                                                      idx_list);
   MOSES_CUDA(cudaGetLastError());
   return 1;
+}
+int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                   unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
+                   unsigned long long* hash, long long* values_out, cudaStream_t st) {
+  return encode_impl(task4, domains, sizes, roles, nk, first, nullptr, n, out_kind, feat, ld, D, hash, values_out, st);
 }
 
 // ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
@@ -318,11 +327,12 @@ __global__ void __launch_bounds__(256) measure_configs_kernel(const __grid_const
                                                               unsigned long long first, long long n,
                                                               double* __restrict__ clean_ms, double* __restrict__ thr,
                                                               double* __restrict__ lat, double* __restrict__ wall,
-                                                              float* __restrict__ label) {
+                                                              float* __restrict__ label,
+                                                              const unsigned long long* __restrict__ idx_list) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     long long kv[5];
     unsigned long long ch;
-    sim_decode(s.sp, first + (unsigned long long)i, kv, &ch);
+    sim_decode(s.sp, idx_list ? idx_list[i] : first + (unsigned long long)i, kv, &ch);
     const double clean_thr = sim_clean_throughput(s, kv);
     if (clean_ms) clean_ms[i] = s.work / clean_thr * 1000.0;  // clean_latency_ms (oracle.cpp:58-63)
     if (thr == nullptr && lat == nullptr && wall == nullptr && label == nullptr) continue;
@@ -427,13 +437,14 @@ static void fnv_add_str(unsigned long long& h, const char* s) {  // KeyBuilder::
   h *= 0x100000001b3ull;
 }
 
-int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
-                    const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,
-                    unsigned long long first, long long n, double* clean_ms, double* thr, double* lat, double* wall,
-                    float* label, cudaStream_t st) {
+static int measure_impl(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                        const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                        unsigned long long seed, unsigned long long first, const unsigned long long* idx_list,
+                        long long n, double* clean_ms, double* thr, double* lat, double* wall, float* label,
+                        cudaStream_t st) {
   unsigned long long space;
   SimArgs s = make_sim(dev6, repeats, task4, domains, sizes, roles, nk, &space);
-  if (n < 0 || first > space || (unsigned long long)n > space - first)
+  if (n < 0 || (idx_list == nullptr && (first > space || (unsigned long long)n > space - first)))
     fail(MOSES_ERR_SHAPE_MISMATCH, "config range exceeds the knob space");
   unsigned long long h = 0xcbf29ce484222325ull;
   fnv_add_u64(h, seed);
@@ -442,9 +453,16 @@ int measure_configs(const double* dev6, int repeats, const char* device_id, cons
   s.key0 = h;
   if (n == 0) return 0;
   const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
-  measure_configs_kernel<<<grid, 256, 0, st>>>(s, first, n, clean_ms, thr, lat, wall, label);
+  measure_configs_kernel<<<grid, 256, 0, st>>>(s, first, n, clean_ms, thr, lat, wall, label, idx_list);
   MOSES_CUDA(cudaGetLastError());
   return 1;
+}
+int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
+                    const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,
+                    unsigned long long first, long long n, double* clean_ms, double* thr, double* lat, double* wall,
+                    float* label, cudaStream_t st) {
+  return measure_impl(dev6, repeats, device_id, task_id, task4, domains, sizes, roles, nk, seed, first, nullptr, n,
+                      clean_ms, thr, lat, wall, label, st);
 }
 
 int true_best(const double* dev6, const double* task4, const long long* domains, const int* sizes, const int* roles,
@@ -468,6 +486,174 @@ int true_best(const double* dev6, const double* task4, const long long* domains,
     idx /= (unsigned long long)sizes[k];
   }
   return 2;
+}
+
+
+// ---------------------------------------------------------------- dataset generation
+// generate_dataset (data.cpp:49-65), one task: RngStream(KeyBuilder(seed, "gen", task.id)) draws each
+// configuration knob by knob with below(|domain|) (sample_config, space.cpp:94-100), then measure()
+// labels it. Draw k (1-based) of the stream is mix(key + k*gamma), so sample s, knob j is draw
+// s*nk + j + 1 — as long as no below() call rejects. Rejection happens when a draw is < (2^64 - m) % m
+// (< m/2^64, about 1e-17 per draw here): the parallel kernel flags it and the exact sequential
+// walk below replaces its result, so the configurations always equal the reference's.
+struct DrawArgs {
+  int nk;
+  unsigned long long size[kSpaceMaxKnobs], thresh[kSpaceMaxKnobs];
+};
+
+namespace {
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) sample_configs_kernel(const __grid_constant__ DrawArgs d, unsigned long long key,
+                                                             long long n, unsigned long long* __restrict__ idx,
+                                                             int* __restrict__ rejected) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long id = 0;
+    bool rej = false;
+#pragma unroll
+    for (int k = 0; k < kSpaceMaxKnobs; ++k) {
+      if (k >= d.nk) continue;
+      const unsigned long long ctr = (unsigned long long)i * (unsigned long long)d.nk + (unsigned long long)k + 1ull;
+      const unsigned long long r = mix64(key + ctr * 0x9e3779b97f4a7c15ull);
+      rej |= r < d.thresh[k];
+      id = id * d.size[k] + r % d.size[k];
+    }
+    idx[i] = id;
+    if (rej) atomicExch(rejected, 1);
+  }
+}
+
+// the reference's sequential walk, rejection loop included (runs only when the kernel above flagged)
+__global__ void sample_configs_serial_kernel(const __grid_constant__ DrawArgs d, unsigned long long key, long long n,
+                                             unsigned long long* __restrict__ idx) {
+  unsigned long long st = key;
+  for (long long i = 0; i < n; ++i) {
+    unsigned long long id = 0;
+    for (int k = 0; k < d.nk; ++k) {
+      unsigned long long r;
+      do {
+        st += 0x9e3779b97f4a7c15ull;
+        r = mix64(st);
+      } while (r < d.thresh[k]);
+      id = id * d.size[k] + r % d.size[k];
+    }
+    idx[i] = id;
+  }
+}
+
+// Configuration values -> enumeration index; validate_config (space.cpp:69-81): every value must be
+// in its knob's (sorted) domain, else the smallest offending row is reported.
+__global__ void __launch_bounds__(256) values_to_index_kernel(const __grid_constant__ SpaceArgs a,
+                                                              const long long* __restrict__ values, long long n,
+                                                              unsigned long long* __restrict__ idx,
+                                                              unsigned long long* __restrict__ bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long id = 0;
+    bool ok = true;
+    for (int k = 0; k < a.nk; ++k) {
+      const long long v = values[i * a.nk + k];
+      int lo = 0, hi = a.sizes[k];  // first position with domain >= v
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a.domains[a.offs[k] + mid] < v) lo = mid + 1;
+        else hi = mid;
+      }
+      ok &= lo < a.sizes[k] && a.domains[a.offs[k] + lo] == v;
+      id = id * (unsigned long long)a.sizes[k] + (unsigned long long)(lo < a.sizes[k] ? lo : 0);
+    }
+    idx[i] = id;
+    if (!ok) atomicMin(bad, (unsigned long long)i);
+  }
+}
+
+}  // namespace
+
+static bool g_force_serial_sampling = false;
+void debug_force_serial_sampling(bool on) { g_force_serial_sampling = on; }
+
+int generate_task_dataset(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                          const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                          long long samples, unsigned long long seed, int out_kind, void* feat, long long ld, int D,
+                          long long* values_out, double* thr, double* lat, double* wall, float* label,
+                          unsigned long long* idx_out, cudaStream_t st) {
+  if (samples < 1) fail(MOSES_ERR_INVALID_CONFIG, "samples_per_task must be positive");
+  SpaceArgs chk{};
+  fill_space(chk, domains, sizes, roles, nk);  // validate_task / build_space before any draw
+  DrawArgs d{};
+  d.nk = nk;
+  for (int k = 0; k < nk; ++k) {
+    d.size[k] = (unsigned long long)sizes[k];
+    d.thresh[k] = (0ull - d.size[k]) % d.size[k];
+  }
+  unsigned long long key = 0xcbf29ce484222325ull;
+  fnv_add_u64(key, seed);
+  fnv_add_str(key, "gen");
+  fnv_add_str(key, task_id ? task_id : "");
+  unsigned long long* idx = idx_out;
+  int* rej = nullptr;
+  char* ws = nullptr;
+  const size_t idx_bytes = idx_out ? 0 : size_t(samples) * 8;
+  MOSES_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), idx_bytes + 16, st));
+  if (!idx) idx = reinterpret_cast<unsigned long long*>(ws);
+  rej = reinterpret_cast<int*>(ws + idx_bytes);
+  MOSES_CUDA(cudaMemsetAsync(rej, 0, sizeof(int), st));
+  const int grid = int(std::min<long long>((samples + 255) / 256, 148LL * 16));
+  sample_configs_kernel<<<grid, 256, 0, st>>>(d, key, samples, idx, rej);
+  MOSES_CUDA(cudaGetLastError());
+  int launches = 1;
+  int h_rej = 0;
+  MOSES_CUDA(cudaMemcpyAsync(&h_rej, rej, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MOSES_CUDA(cudaStreamSynchronize(st));
+  if (h_rej || g_force_serial_sampling) {
+    sample_configs_serial_kernel<<<1, 1, 0, st>>>(d, key, samples, idx);
+    MOSES_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (feat || values_out)
+    launches += encode_impl(task4, domains, sizes, roles, nk, 0, idx, samples, out_kind, feat, ld, D, nullptr,
+                            values_out, st);
+  if (thr || lat || wall || label)
+    launches += measure_impl(dev6, repeats, device_id, task_id, task4, domains, sizes, roles, nk, seed, 0, idx, samples,
+                             nullptr, thr, lat, wall, label, st);
+  MOSES_CUDA(cudaFreeAsync(ws, st));
+  return launches;
+}
+
+int encode_values(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                  const long long* values, long long n, int out_kind, void* feat, long long ld, int D,
+                  unsigned long long* hash, unsigned long long* idx_out, long long* bad_row, cudaStream_t st) {
+  SpaceArgs a{};
+  fill_space(a, domains, sizes, roles, nk);
+  *bad_row = -1;
+  if (n < 0) fail(MOSES_ERR_SHAPE_MISMATCH, "negative row count");
+  if (n == 0) return 0;
+  char* ws = nullptr;
+  const size_t idx_bytes = idx_out ? 0 : size_t(n) * 8;
+  MOSES_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), idx_bytes + 16, st));
+  unsigned long long* idx = idx_out ? idx_out : reinterpret_cast<unsigned long long*>(ws);
+  auto* bad = reinterpret_cast<unsigned long long*>(ws + idx_bytes);
+  MOSES_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  const int grid = int(std::min<long long>((n + 255) / 256, 148LL * 16));
+  values_to_index_kernel<<<grid, 256, 0, st>>>(a, values, n, idx, bad);
+  MOSES_CUDA(cudaGetLastError());
+  unsigned long long h_bad = 0;
+  MOSES_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, st));
+  MOSES_CUDA(cudaStreamSynchronize(st));
+  int launches = 1;
+  if (h_bad != ~0ull) {
+    *bad_row = (long long)h_bad;
+    MOSES_CUDA(cudaFreeAsync(ws, st));
+    fail(MOSES_ERR_INVALID_CONFIG, "record " + std::to_string(h_bad) + ": value not in its knob's domain");
+  }
+  if (feat || hash)
+    launches += encode_impl(task4, domains, sizes, roles, nk, 0, idx, n, out_kind, feat, ld, D, hash, nullptr, st);
+  MOSES_CUDA(cudaFreeAsync(ws, st));
+  return launches;
 }
 
 }  // namespace moses

@@ -129,6 +129,23 @@ def lib():
         "moses_train_step_pooled_async": (C.c_int, [vp, vp, i64, i32, vp, i64, vp, dbl, dbl, vp]),
         "moses_encode_configs": (C.c_int, [vp, vp, vp, vp, i32, C.c_uint64, i64, vp, vp]),
         "moses_lottery_step_adam": (C.c_int, [vp, i32, dbl, i32, dbl, dbl, dbl, dbl, i32, dbl, vp, i64, vp]),
+        "moses_generate_dataset_device": (C.c_int, [vp, i32, C.c_char_p, C.c_char_p, vp, vp, vp, vp, i32, i64, u64,
+                                                    i32, vp, i64, i32, vp, vp, vp, vp, vp]),
+        "moses_encode_values_device": (C.c_int, [vp, vp, vp, vp, i32, vp, i64, i32, vp, i64, i32, vp, vp]),
+        "moses_epoch_seed": (u64, [u64, u64]),
+        "moses_ranking_plan": (C.c_int, [vp, i64, vp, i32, i32, u64, vp, vp, vp, vp, vp]),
+        "moses_replay_rows": (C.c_int, [i64, i64, u64, vp, vp]),
+        "moses_train_plan_device": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, dbl, dbl, vp]),
+        "moses_records_create": (C.c_int, [vp]),
+        "moses_records_read": (C.c_int, [C.c_char_p, vp]),
+        "moses_records_destroy": (None, [vp]),
+        "moses_records_append": (C.c_int, [vp, C.c_char_p, C.c_char_p, i64, i32, vp, vp, vp, vp, vp]),
+        "moses_records_write": (C.c_int, [vp, C.c_char_p]),
+        "moses_records_shape": (C.c_int, [vp, vp, vp, vp, vp]),
+        "moses_records_task_id": (C.c_char_p, [vp, i32]),
+        "moses_records_device_id": (C.c_char_p, [vp, i32]),
+        "moses_records_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "moses_debug_force_serial_sampling": (C.c_int, [i32]),
         "moses_synth_features_device": (C.c_int, [u64, i64, i64, i32, i32, vp, i64]),
         "moses_synth_labels_device": (C.c_int, [u64, i64, i64, vp]),
         "moses_serialize": (i64, [vp, i32, vp, vp, vp, i64]),
@@ -772,3 +789,153 @@ def true_best(device, task, knobs):
     _ck(lib().moses_true_best(_p(_device6(device)), _p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs),
                               _p(v), C.byref(lat)))
     return v.tolist(), lat.value
+
+
+# ---------------------------------------------------------------- training-data pipeline (data.cpp, tuner.cpp:130-156)
+def generate_dataset_device(device, task_id: str, task, knobs, samples: int, seed: int, dtype: int = DTYPE_F32,
+                            feat_ptr=None, ld: int = 16, D: int = 16, values_ptr=None, thr_ptr=None, lat_ptr=None,
+                            wall_ptr=None, label_ptr=None):
+    """generate_dataset (data.cpp:49-65) for one task into device buffers (pointers or None): keyed
+    sample_config draws, feature rows, knob values (samples x n_knobs int64), measure() outputs."""
+    dom, sizes, roles = _space_arrays(knobs)
+    _ck(lib().moses_generate_dataset_device(_p(_device6(device)), int(device["repeats"]), device["id"].encode(),
+                                            task_id.encode(), _p(_task4(task)), _p(dom), _p(sizes), _p(roles),
+                                            len(knobs), samples, seed, dtype, feat_ptr, ld, D, values_ptr, thr_ptr,
+                                            lat_ptr, wall_ptr, label_ptr))
+
+
+def encode_values_device(task, knobs, values_ptr, n: int, dtype: int = DTYPE_F32, feat_ptr=None, ld: int = 16,
+                         D: int = 16, hash_ptr=None):
+    """validate_config + encode_features (space.cpp:69-81,140-159) over device rows of knob values.
+    Raises MosesError(invalid_config) naming the first bad row."""
+    dom, sizes, roles = _space_arrays(knobs)
+    bad = C.c_int64(-1)
+    _ck(lib().moses_encode_values_device(_p(_task4(task)), _p(dom), _p(sizes), _p(roles), len(knobs), values_ptr, n,
+                                         dtype, feat_ptr, ld, D, hash_ptr, C.byref(bad)))
+
+
+def epoch_seed(seed: int, epoch: int) -> int:
+    """KeyBuilder(seed, "epoch", epoch) (tuner.cpp:136-139)."""
+    return int(lib().moses_epoch_seed(seed, epoch))
+
+
+class RankingPlan:
+    """make_ranking_batches (data.cpp:128-164) as row indices: batch b = rows[off[b]:off[b+1]] of task
+    task_ids[task[b]]."""
+
+    def __init__(self, rows, off, task, task_ids, dropped):
+        self.rows, self.off, self.task, self.task_ids, self.dropped_singletons = rows, off, task, task_ids, dropped
+
+    def __len__(self):
+        return len(self.off) - 1
+
+    def batch(self, b):
+        return self.task_ids[self.task[b]], self.rows[self.off[b]:self.off[b + 1]]
+
+
+def make_ranking_batches(record_task, task_ids, batch_size: int, seed: int) -> RankingPlan:
+    """record_task: per-record index into task_ids (or the task-id strings themselves)."""
+    if len(record_task) and isinstance(record_task[0], str):
+        ids = list(dict.fromkeys(list(task_ids) + list(record_task)))
+        ix = {t: i for i, t in enumerate(ids)}
+        record_task, task_ids = [ix[t] for t in record_task], ids
+    rt = np.ascontiguousarray(record_task, dtype=np.int32)
+    n = len(rt)
+    enc = [t.encode() for t in task_ids]
+    arr = (C.c_char_p * max(1, len(enc)))(*enc)
+    rows = np.zeros(max(n, 1), dtype=np.int64)
+    off = np.zeros(n // 2 + 2, dtype=np.int64)
+    task = np.zeros(n // 2 + 1, dtype=np.int32)
+    nb = C.c_int64()
+    dropped = C.c_int64()
+    _ck(lib().moses_ranking_plan(_p(rt), n, C.cast(arr, C.c_void_p), len(enc), batch_size, seed, _p(rows), _p(off),
+                                 _p(task), C.byref(nb), C.byref(dropped)))
+    k = nb.value
+    return RankingPlan(rows[:off[k]].copy(), off[:k + 1].copy(), task[:k].copy(), list(task_ids), dropped.value)
+
+
+def replay_rows(n_records: int, size: int, seed: int) -> np.ndarray:
+    """sample_replay_features' row choice (data.cpp:166-183)."""
+    out = np.zeros(max(1, min(max(n_records, 0), max(size, 0))), dtype=np.int64)
+    k = C.c_int64()
+    _ck(lib().moses_replay_rows(n_records, size, seed, _p(out), C.byref(k)))
+    return out[:k.value].copy()
+
+
+def train_plan_device(model, x_ptr, ldx: int, y_ptr, n_records: int, plan: RankingPlan, lr: float,
+                      mu: float = 0.9) -> float:
+    """One pretrain epoch (tuner.cpp:140-155) over a device-resident packed dataset; returns the mean
+    batch loss."""
+    rows = np.ascontiguousarray(plan.rows, dtype=np.int64)
+    off = np.ascontiguousarray(plan.off, dtype=np.int64)
+    out = C.c_double()
+    _ck(lib().moses_train_plan_device(model.h, x_ptr, ldx, y_ptr, n_records, _p(rows), _p(off), len(off) - 1, lr, mu,
+                                      C.byref(out)))
+    return out.value
+
+
+class RecordStore:
+    """Line-delimited measurement records (data.cpp:67-126) held by the native reader."""
+
+    def __init__(self, handle=None):
+        self.h = C.c_void_p(handle)
+        if handle is None:
+            _ck(lib().moses_records_create(C.byref(self.h)))
+
+    @classmethod
+    def read(cls, path: str) -> "RecordStore":
+        h = C.c_void_p()
+        _ck(lib().moses_records_read(path.encode(), C.byref(h)))
+        return cls(h.value)
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.moses_records_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def append(self, task_id: str, device_id: str, values, throughput, latency, wall_cost, seq):
+        v = np.ascontiguousarray(values, dtype=np.int64)
+        if v.ndim == 1:
+            v = v.reshape(1, -1)
+        n = v.shape[0]
+        cols = [np.ascontiguousarray(np.broadcast_to(a, (n,)), dtype=t)
+                for a, t in ((throughput, np.float64), (latency, np.float64), (wall_cost, np.float64),
+                             (seq, np.uint64))]
+        _ck(lib().moses_records_append(self.h, task_id.encode(), device_id.encode(), n, v.shape[1], _p(v),
+                                       *(_p(c) for c in cols)))
+
+    def write(self, path: str):
+        _ck(lib().moses_records_write(self.h, path.encode()))
+
+    def shape(self):
+        n, nv, nt, nd = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+        _ck(lib().moses_records_shape(self.h, C.byref(n), C.byref(nv), C.byref(nt), C.byref(nd)))
+        return n.value, nv.value, nt.value, nd.value
+
+    def __len__(self):
+        return self.shape()[0]
+
+    def task_ids(self):
+        return [lib().moses_records_task_id(self.h, t).decode() for t in range(self.shape()[2])]
+
+    def device_ids(self):
+        return [lib().moses_records_device_id(self.h, d).decode() for d in range(self.shape()[3])]
+
+    def export(self, pinned: bool = False):
+        """Flat arrays: task (int32 index into task_ids()), device, value_off, values, throughput,
+        latency, wall_cost, seq. pinned=True returns page-locked torch tensors (ready for a
+        non-blocking upload)."""
+        n, nv, _, _ = self.shape()
+        specs = [("task", n, np.int32), ("device", n, np.int32), ("value_off", n + 1, np.int64),
+                 ("values", nv, np.int64), ("throughput", n, np.float64), ("latency", n, np.float64),
+                 ("wall_cost", n, np.float64), ("seq", n, np.uint64)]
+        if pinned:
+            import torch
+            tmap = {np.int32: torch.int32, np.int64: torch.int64, np.float64: torch.float64, np.uint64: torch.int64}
+            out = {k: torch.empty(max(m, 1), dtype=tmap[t], pin_memory=True) for k, m, t in specs}
+            ptrs = [out[k].data_ptr() for k, _, _ in specs]
+            _ck(lib().moses_records_export(self.h, *ptrs))
+            return {k: out[k][:m] for k, m, _ in specs}
+        out = {k: np.zeros(max(m, 1), dtype=t) for k, m, t in specs}
+        _ck(lib().moses_records_export(self.h, *(_p(out[k]) for k, _, _ in specs)))
+        return {k: out[k][:m] for k, m, _ in specs}
