@@ -524,6 +524,89 @@ def bench_search(ml, L, peaks):
     return out
 
 
+def bench_pretrain(ml, L, peaks, epochs: int = 30, per_task: int = 6000):
+    """the reference's own offline flow — `moseslab gen-dataset --samples 6000`
+    on the 8 default tasks / server device (data.cpp:49-65, cli.cpp:344) then `pretrain` with the
+    default TrainHyper (30 epochs, batch 512, lr 0.001, momentum 0.9; tuner.cpp:130-156) on
+    {16,512,512,1}: dataset generated on the device, per-epoch keyed shuffles / single-task chunking
+    on the host overlapped with the device epochs, batches gathered on the device."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
+
+    sim = json.load(open(os.path.join(ROOT, "tests", "golden", "simulated_oracle.json")))
+    device = sim["devices"]["server"]
+    tasks = [(t["id"], (t["work_gflops"], t["bytes_per_unit"], t["ideal_log2_tiles"], t["ideal_log2_unroll"]))
+             for t in sim["tasks"]["list"]]
+    knobs = [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
+             ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
+    dims = [16, 512, 512, 1]
+    seed = 0
+    dm = ml.DeviceModel(ml.init_random(dims, seed), ml.PREC_BF16, 512)
+    ld = dm.packed_ld
+    n = per_task * len(tasks)
+    X = torch.zeros((n, ld), dtype=torch.bfloat16, device="cuda")
+    Y = torch.zeros(n, dtype=torch.float32, device="cuda")
+
+    def generate():
+        for t, (tid, task) in enumerate(tasks):
+            r0 = t * per_task
+            ml.generate_dataset_device(device, tid, task, knobs, per_task, 1, ml.DTYPE_BF16,
+                                       C.c_void_p(X.data_ptr() + r0 * ld * 2), ld, 16, None, None, None, None,
+                                       C.c_void_p(Y.data_ptr() + r0 * 4))
+
+    generate()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    generate()
+    torch.cuda.synchronize()
+    gen_ms = (time.perf_counter() - t0) * 1e3
+    task_of = [i // per_task for i in range(n)]
+    ids = [tid for tid, _ in tasks]
+    t0 = time.perf_counter()
+    plan = ml.make_ranking_batches(task_of, ids, 512, ml.epoch_seed(seed, 0))
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    ml.pretrain_device(dm, C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids, 512, seed, 1)  # warm
+    dm.upload(ml.init_random(dims, seed))
+    torch.cuda.synchronize()
+    k0 = L.moses_kernel_launches()
+    t0 = time.perf_counter()
+    losses, dropped = ml.pretrain_device(dm, C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids,
+                                         512, seed, epochs, 0.001, 0.9)
+    total = time.perf_counter() - t0
+    launches = L.moses_kernel_launches() - k0
+    # the same loop on the fp64 CPU oracle: a bounded sample of epoch 0's batches
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    threads = os.cpu_count() or 1
+    feats = X[:, :16].float().double().cpu().numpy()
+    labels = Y.double().cpu().numpy()
+    w = orc.init_random(dims, seed)
+    mom = np.zeros_like(w)
+    nb = min(len(plan), 24)
+    t0 = time.perf_counter()
+    for b in range(nb):
+        _, rows = plan.batch(b)
+        orc.train_step_f64(dims, w, mom, feats[rows], labels[rows], 0.001, 0.9, threads)
+    cpu_dt = time.perf_counter() - t0
+    cpu_rows = int(plan.off[nb])
+    del X, Y
+    torch.cuda.empty_cache()
+    return {"workload": f"gen-dataset --samples {per_task} (8 default tasks, server) + pretrain {epochs} epochs, "
+                        f"batch 512, {dims}, bf16",
+            "records": n, "batches_per_epoch": len(plan), "dropped_singletons": dropped,
+            "generate_ms": gen_ms, "plan_ms_host": plan_ms,
+            "pretrain_s": total, "samples_per_s": epochs * n / total, "ms_per_epoch": total / epochs * 1e3,
+            "epoch_mean_loss_first_last": [losses[0], losses[-1]], "gpu_launches": int(launches),
+            "cpu_oracle": {"samples_per_s": cpu_rows / cpu_dt, "cores": threads, "kind": "port",
+                           "sample": f"{nb} batches ({cpu_rows} rows) of epoch 0, fp64"},
+            "path": "moses_generate_dataset_device x8 -> moses_pretrain_device (host plan of epoch e+1 overlapped "
+                    "with device epoch e; full batches replay one CUDA graph), wall clock"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -535,6 +618,7 @@ def main():
     ap.add_argument("--no-infer", action="store_true")
     ap.add_argument("--no-hbm", action="store_true")
     ap.add_argument("--no-finetune", action="store_true")
+    ap.add_argument("--no-pretrain", action="store_true")
     ap.add_argument("--no-search", action="store_true")
     ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
@@ -800,6 +884,8 @@ def main():
         line["finetune"] = bench_finetune(ml, L, peaks)
     if not args.no_search:
         line["search"] = bench_search(ml, L, peaks)
+    if not args.no_pretrain:
+        line["pretrain"] = bench_pretrain(ml, L, peaks)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(15.0)
     print(json.dumps(line), flush=True)

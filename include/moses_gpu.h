@@ -308,6 +308,16 @@ MOSES_API int moses_replay_rows(int64_t n_records, int64_t size, uint64_t seed, 
 MOSES_API int moses_train_plan_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
                                      int64_t n_records, const int64_t* rows, const int64_t* batch_off,
                                      int64_t n_batches, double learning_rate, double momentum, double* mean_loss);
+/* pretrain (tuner.cpp:130-156) over a device-resident packed dataset: for each epoch e,
+ * moses_ranking_plan(seed = moses_epoch_seed(seed, e)) then one momentum step per batch. The model
+ * handle carries the initial parameters (the reference starts from init_random(dims, seed)). The host
+ * computes epoch e+1's plan while the device runs epoch e. epoch_mean_loss (host, `epochs` entries)
+ * and dropped_singletons (epoch 0, as PretrainLog) may be NULL. n_records == 0: MOSES_ERR_EMPTY_DATASET. */
+MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                   const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                   int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs,
+                                   double learning_rate, double momentum, double* epoch_mean_loss,
+                                   int64_t* dropped_singletons);
 /* Line-delimited record files (data.cpp:67-126). moses_records_read fails with MOSES_ERR_IO,
  * MOSES_ERR_PARSE (message names "<path>:line N") or MOSES_ERR_MISSING_FIELD. */
 MOSES_API int moses_records_create(moses_records_t* out);

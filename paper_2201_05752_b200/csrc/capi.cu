@@ -2064,125 +2064,237 @@ MOSES_API int moses_replay_rows(int64_t n_records, int64_t size, uint64_t seed, 
   });
 }
 
+namespace {
+// ---- epochs over ranking-batch plans (moses_train_plan_device, moses_pretrain_device)
+struct PlanShape {
+  long long B = 0, nfull = 0, total = 0;
+};
+PlanShape plan_check(moses_model* m, const long long* rows, const long long* off, long long nb, long long n_records) {
+  PlanShape ps;
+  if (nb < 0) fail(MOSES_ERR_INVALID_ARG, "negative batch count");
+  if (nb == 0) return ps;
+  if (rows == nullptr || off == nullptr) fail(MOSES_ERR_INVALID_ARG, "null plan");
+  if (off[0] != 0) fail(MOSES_ERR_INVALID_ARG, "batch_off[0] must be 0");
+  for (long long b = 0; b < nb; ++b) {
+    const long long len = off[b + 1] - off[b];
+    if (len < 2) fail(MOSES_ERR_INVALID_ARG, "plan batch " + std::to_string(b) + " has fewer than 2 rows");
+    ps.B = std::max(ps.B, len);
+  }
+  check_rows(m, ps.B);
+  for (long long b = 0; b < nb; ++b) ps.nfull += (off[b + 1] - off[b]) == ps.B;
+  ps.total = off[nb];
+  for (long long i = 0; i < ps.total; ++i)
+    if (rows[i] < 0 || rows[i] >= n_records)
+      fail(MOSES_ERR_SHAPE_MISMATCH, "plan row " + std::to_string(rows[i]) + " outside the dataset");
+  return ps;
+}
+void plan_reserve(moses_model* m, long long total, long long nb) {
+  auto& ps = m->plan;
+  if (total > ps.cap_rows || nb + 1 > ps.cap_b) {
+    if (ps.exec) {
+      cudaGraphExecDestroy(ps.exec);
+      ps.exec = nullptr;
+    }
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    if (total > ps.cap_rows) {
+      dfree(ps.rows);
+      ps.rows = dalloc<long long>(total);
+      ps.cap_rows = total;
+    }
+    if (nb + 1 > ps.cap_b) {
+      dfree(ps.off);
+      ps.off = dalloc<long long>(nb + 1);
+      ps.cap_b = nb + 1;
+    }
+  }
+  if (!ps.counter) ps.counter = dalloc<long long>(1);
+  if (!ps.loss_sum) ps.loss_sum = dalloc<double>(1);
+  if (m->split && !ps.stage) ps.stage = dalloc<float>(m->cap * m->ld[0]);
+}
+// one step over plan batch *counter (n rows): gather -> gradients -> momentum update -> loss sum
+void plan_step(moses_model* m, const void* x, long long ldx, const float* y, long long n, float lr, float mu) {
+  auto& ps = m->plan;
+  const long long row_bytes = ldx * m->esz;
+  if (m->split) {  // 3xTF32 operands: hi/lo split of the gathered fp32 rows
+    gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, ps.stage, m->labels, m->st);
+    pack_rows_f32<float>(ps.stage, n, m->dims[0], ldx, static_cast<float*>(m->act[0]), m->ld[0], m->st,
+                         m->act_lo(0));
+    note_launch(1);
+  } else {
+    gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st);
+  }
+  const SgdFuse fz{lr, mu};
+  if (!gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, &fz)) {
+    sgd_update(m->w, m->mom, m->g, nullptr, m->P, lr, mu, true, m->shadow(), m->st);
+    m->post_update();
+    note_launch(1);
+  }
+  accum_f64(m->dscal, ps.loss_sum, m->st);
+  advance_counter(ps.counter, m->st);
+  note_launch(3);
+}
+// full-size batches replay one CUDA graph, captured once per dataset / size / hyper-parameters;
+// needs the plan's rows on the device (the warm-up gathers batch 0's slots)
+bool plan_graph(moses_model* m, const void* x, long long ldx, const float* y, const PlanShape& sh, float lr, float mu) {
+  auto& ps = m->plan;
+  if (m->split || sh.nfull < 4) return false;
+  if (ps.exec && ps.x == x && ps.y == y && ps.ldx == ldx && ps.batch == sh.B && ps.lr == lr && ps.mu == mu) return true;
+  if (ps.exec) {
+    cudaGraphExecDestroy(ps.exec);
+    ps.exec = nullptr;
+  }
+  // eager warm-up without the update (configures kernels; parameters untouched)
+  MOSES_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(long long), m->st));
+  gather_plan(x, ldx * m->esz, y, ps.rows, ps.off, ps.counter, sh.B, m->act[0], m->labels, m->st);
+  gradients_core(m, m->act[0], m->ld[0], m->labels, sh.B, nullptr, 0.0);
+  MOSES_CUDA(cudaStreamSynchronize(m->st));
+  const long long before = moses_kernel_launches();
+  cudaGraph_t graph;
+  MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+  try {
+    plan_step(m, x, ldx, y, sh.B, lr, mu);
+  } catch (...) {
+    cudaStreamEndCapture(m->st, &graph);
+    throw;
+  }
+  MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+  ps.graph_kernels = moses_kernel_launches() - before;
+  note_launch(-ps.graph_kernels);  // captured, not launched
+  MOSES_CUDA(cudaGraphInstantiate(&ps.exec, graph, 0));
+  MOSES_CUDA(cudaGraphDestroy(graph));
+  ps.x = x;
+  ps.y = y;
+  ps.ldx = ldx;
+  ps.batch = sh.B;
+  ps.lr = lr;
+  ps.mu = mu;
+  return true;
+}
+// enqueue one epoch (rows / offsets already on the device); the loss sum is left in ps.loss_sum
+void plan_epoch(moses_model* m, const void* x, long long ldx, const float* y, const long long* off, long long nb,
+                const PlanShape& sh, float lr, float mu, bool graph) {
+  auto& ps = m->plan;
+  MOSES_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(long long), m->st));
+  MOSES_CUDA(cudaMemsetAsync(ps.loss_sum, 0, sizeof(double), m->st));
+  for (long long b = 0; b < nb; ++b) {
+    const long long len = off[b + 1] - off[b];
+    if (graph && len == sh.B) {
+      MOSES_CUDA(cudaGraphLaunch(ps.exec, m->st));
+      note_launch(ps.graph_kernels);
+    } else {
+      plan_step(m, x, ldx, y, len, lr, mu);
+    }
+  }
+}
+}  // namespace
+
 MOSES_API int moses_train_plan_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
                                      int64_t n_records, const int64_t* rows, const int64_t* batch_off,
                                      int64_t n_batches, double lr, double mu, double* mean_loss) {
   return guarded([&] {
     require_model(m);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
-    if (n_batches < 0) fail(MOSES_ERR_INVALID_ARG, "negative batch count");
+    const auto* r = reinterpret_cast<const long long*>(rows);
+    const auto* off = reinterpret_cast<const long long*>(batch_off);
+    const PlanShape sh = plan_check(m, r, off, n_batches, n_records);
     if (n_batches == 0) {
       if (mean_loss) *mean_loss = 0.0;  // tuner.cpp:152-154: empty epoch
       return;
     }
-    if (rows == nullptr || batch_off == nullptr || x_base == nullptr || y_base == nullptr)
-      fail(MOSES_ERR_INVALID_ARG, "null plan or dataset");
-    if (batch_off[0] != 0) fail(MOSES_ERR_INVALID_ARG, "batch_off[0] must be 0");
-    long long B = 0, nfull = 0;
-    for (int64_t b = 0; b < n_batches; ++b) {
-      const long long len = batch_off[b + 1] - batch_off[b];
-      if (len < 2) fail(MOSES_ERR_INVALID_ARG, "plan batch " + std::to_string(b) + " has fewer than 2 rows");
-      B = std::max(B, len);
-    }
-    check_rows(m, B);
-    for (int64_t b = 0; b < n_batches; ++b) nfull += (batch_off[b + 1] - batch_off[b]) == B;
-    const long long total = batch_off[n_batches];
-    for (long long i = 0; i < total; ++i)
-      if (rows[i] < 0 || rows[i] >= n_records)
-        fail(MOSES_ERR_SHAPE_MISMATCH, "plan row " + std::to_string(rows[i]) + " outside the dataset");
+    if (x_base == nullptr || y_base == nullptr) fail(MOSES_ERR_INVALID_ARG, "null dataset");
+    plan_reserve(m, sh.total, n_batches);
     auto& ps = m->plan;
-    if (total > ps.cap_rows || n_batches + 1 > ps.cap_b) {
-      if (ps.exec) {
-        cudaGraphExecDestroy(ps.exec);
-        ps.exec = nullptr;
-      }
-      MOSES_CUDA(cudaStreamSynchronize(m->st));
-      if (total > ps.cap_rows) {
-        dfree(ps.rows);
-        ps.rows = dalloc<long long>(total);
-        ps.cap_rows = total;
-      }
-      if (n_batches + 1 > ps.cap_b) {
-        dfree(ps.off);
-        ps.off = dalloc<long long>(n_batches + 1);
-        ps.cap_b = n_batches + 1;
-      }
-    }
-    if (!ps.counter) ps.counter = dalloc<long long>(1);
-    if (!ps.loss_sum) ps.loss_sum = dalloc<double>(1);
-    MOSES_CUDA(cudaMemcpyAsync(ps.rows, rows, sizeof(long long) * total, cudaMemcpyHostToDevice, m->st));
-    MOSES_CUDA(cudaMemcpyAsync(ps.off, batch_off, sizeof(long long) * (n_batches + 1), cudaMemcpyHostToDevice, m->st));
-    MOSES_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(long long), m->st));
-    MOSES_CUDA(cudaMemsetAsync(ps.loss_sum, 0, sizeof(double), m->st));
-    const long long row_bytes = ldx * m->esz;
-    const SgdFuse fz{float(lr), float(mu)};
-    if (m->split && !ps.stage) ps.stage = dalloc<float>(m->cap * m->ld[0]);
-    auto step = [&](long long n) {
-      if (m->split) {  // 3xTF32 operands: hi/lo split of the gathered fp32 rows
-        gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, n, ps.stage, m->labels, m->st);
-        pack_rows_f32<float>(ps.stage, n, m->dims[0], ldx, static_cast<float*>(m->act[0]), m->ld[0], m->st,
-                             m->act_lo(0));
-        note_launch(1);
-      } else {
-        gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st);
-      }
-      if (!gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, &fz)) {
-        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-        m->post_update();
-        note_launch(1);
-      }
-      accum_f64(m->dscal, ps.loss_sum, m->st);
-      advance_counter(ps.counter, m->st);
-      note_launch(3);
-    };
-    // full-size batches replay one CUDA graph (captured once per dataset / size / hyper-parameters)
-    const bool want_graph = !m->split && nfull >= 4;
-    if (want_graph && !(ps.exec && ps.x == x_base && ps.y == y_base && ps.ldx == ldx && ps.batch == B &&
-                        ps.lr == float(lr) && ps.mu == float(mu))) {
-      if (ps.exec) {
-        cudaGraphExecDestroy(ps.exec);
-        ps.exec = nullptr;
-      }
-      // eager warm-up without the update (configures kernels; parameters untouched)
-      gather_plan(x_base, row_bytes, y_base, ps.rows, ps.off, ps.counter, B, m->act[0], m->labels, m->st);
-      gradients_core(m, m->act[0], m->ld[0], m->labels, B, nullptr, 0.0);
-      MOSES_CUDA(cudaStreamSynchronize(m->st));
-      const long long before = moses_kernel_launches();
-      cudaGraph_t graph;
-      MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
-      try {
-        step(B);
-      } catch (...) {
-        cudaStreamEndCapture(m->st, &graph);
-        throw;
-      }
-      MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
-      ps.graph_kernels = moses_kernel_launches() - before;
-      note_launch(-ps.graph_kernels);  // captured, not launched
-      MOSES_CUDA(cudaGraphInstantiate(&ps.exec, graph, 0));
-      MOSES_CUDA(cudaGraphDestroy(graph));
-      ps.x = x_base;
-      ps.y = y_base;
-      ps.ldx = ldx;
-      ps.batch = B;
-      ps.lr = float(lr);
-      ps.mu = float(mu);
-    }
-    for (int64_t b = 0; b < n_batches; ++b) {
-      const long long len = batch_off[b + 1] - batch_off[b];
-      if (want_graph && len == B) {
-        MOSES_CUDA(cudaGraphLaunch(ps.exec, m->st));
-        note_launch(ps.graph_kernels);
-      } else {
-        step(len);
-      }
-    }
+    MOSES_CUDA(cudaMemcpyAsync(ps.rows, r, sizeof(long long) * sh.total, cudaMemcpyHostToDevice, m->st));
+    MOSES_CUDA(cudaMemcpyAsync(ps.off, off, sizeof(long long) * (n_batches + 1), cudaMemcpyHostToDevice, m->st));
+    const bool graph = plan_graph(m, x_base, ldx, y_base, sh, float(lr), float(mu));
+    plan_epoch(m, x_base, ldx, y_base, off, n_batches, sh, float(lr), float(mu), graph);
     if (mean_loss) {
       double sum = 0.0;
       MOSES_CUDA(cudaMemcpyAsync(&sum, ps.loss_sum, sizeof(double), cudaMemcpyDeviceToHost, m->st));
       MOSES_CUDA(cudaStreamSynchronize(m->st));
       *mean_loss = sum / double(n_batches);
     }
+  });
+}
+
+// pretrain (tuner.cpp:130-156) over a device-resident dataset: per epoch KeyBuilder(seed, "epoch", e)
+// -> make_ranking_batches -> one step per batch. The host computes epoch e+1's plan (into pinned
+// memory) while the device runs epoch e; plan uploads and per-epoch loss sums are stream-ordered,
+// so the only synchronisation is the final read of the per-epoch losses.
+MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                   const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                   int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs, double lr,
+                                   double mu, double* epoch_mean_loss, int64_t* dropped_singletons) {
+  return guarded([&] {
+    require_model(m);
+    if (n_records <= 0) fail(MOSES_ERR_EMPTY_DATASET, "no records to pretrain on");
+    if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
+    if (x_base == nullptr || y_base == nullptr) fail(MOSES_ERR_INVALID_ARG, "null dataset");
+    if (epochs < 0) fail(MOSES_ERR_INVALID_CONFIG, "negative epoch count");
+    if (epochs == 0) return;
+    struct Slot {
+      long long* rows = nullptr;  // pinned
+      long long* off = nullptr;   // pinned
+      long long nb = 0;
+      cudaEvent_t up = nullptr;
+    } slot[2];
+    double* losses = nullptr;
+    auto cleanup = [&] {
+      cudaStreamSynchronize(m->st);
+      for (auto& s : slot) {
+        if (s.rows) cudaFreeHost(s.rows);
+        if (s.off) cudaFreeHost(s.off);
+        if (s.up) cudaEventDestroy(s.up);
+      }
+      dfree(losses);
+    };
+    std::vector<long long> nbs(size_t(epochs), 0);
+    long long drop0 = 0;
+    try {
+      for (auto& s : slot) {
+        MOSES_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s.rows), sizeof(long long) * n_records));
+        MOSES_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s.off), sizeof(long long) * (n_records / 2 + 2)));
+        MOSES_CUDA(cudaEventCreateWithFlags(&s.up, cudaEventDisableTiming));
+      }
+      losses = dalloc<double>(size_t(epochs));
+      auto make_plan = [&](int e) {
+        Slot& s = slot[e & 1];
+        MOSES_CUDA(cudaEventSynchronize(s.up));  // the upload two epochs back has read this slot
+        long long drop = 0;
+        s.nb = ranking_plan(record_task, n_records, task_ids, n_task_ids, batch_size, epoch_seed(seed, uint64_t(e)),
+                            s.rows, s.off, nullptr, &drop);
+        if (e == 0) drop0 = drop;
+      };
+      make_plan(0);
+      plan_reserve(m, n_records, n_records / 2 + 1);
+      auto& ps = m->plan;
+      for (int e = 0; e < epochs; ++e) {
+        Slot& s = slot[e & 1];
+        const PlanShape sh = plan_check(m, s.rows, s.off, s.nb, n_records);
+        nbs[size_t(e)] = s.nb;
+        if (s.nb > 0) {
+          MOSES_CUDA(cudaMemcpyAsync(ps.rows, s.rows, sizeof(long long) * sh.total, cudaMemcpyHostToDevice, m->st));
+          MOSES_CUDA(cudaMemcpyAsync(ps.off, s.off, sizeof(long long) * (s.nb + 1), cudaMemcpyHostToDevice, m->st));
+          MOSES_CUDA(cudaEventRecord(s.up, m->st));
+          const bool graph = plan_graph(m, x_base, ldx, y_base, sh, float(lr), float(mu));
+          plan_epoch(m, x_base, ldx, y_base, s.off, s.nb, sh, float(lr), float(mu), graph);
+          MOSES_CUDA(cudaMemcpyAsync(losses + e, ps.loss_sum, sizeof(double), cudaMemcpyDeviceToDevice, m->st));
+        } else {
+          MOSES_CUDA(cudaMemsetAsync(losses + e, 0, sizeof(double), m->st));
+        }
+        if (e + 1 < epochs) make_plan(e + 1);  // overlaps the epoch just enqueued
+      }
+      std::vector<double> h(static_cast<size_t>(epochs));
+      MOSES_CUDA(cudaMemcpyAsync(h.data(), losses, sizeof(double) * epochs, cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+      if (epoch_mean_loss)
+        for (int e = 0; e < epochs; ++e) epoch_mean_loss[e] = nbs[size_t(e)] ? h[size_t(e)] / double(nbs[size_t(e)]) : 0.0;
+      if (dropped_singletons) *dropped_singletons = drop0;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 

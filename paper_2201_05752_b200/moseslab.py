@@ -136,6 +136,7 @@ def lib():
         "moses_ranking_plan": (C.c_int, [vp, i64, vp, i32, i32, u64, vp, vp, vp, vp, vp]),
         "moses_replay_rows": (C.c_int, [i64, i64, u64, vp, vp]),
         "moses_train_plan_device": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, dbl, dbl, vp]),
+        "moses_pretrain_device": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, i32, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_records_create": (C.c_int, [vp]),
         "moses_records_read": (C.c_int, [C.c_char_p, vp]),
         "moses_records_destroy": (None, [vp]),
@@ -872,6 +873,24 @@ def train_plan_device(model, x_ptr, ldx: int, y_ptr, n_records: int, plan: Ranki
     _ck(lib().moses_train_plan_device(model.h, x_ptr, ldx, y_ptr, n_records, _p(rows), _p(off), len(off) - 1, lr, mu,
                                       C.byref(out)))
     return out.value
+
+
+def pretrain_device(model, x_ptr, ldx: int, y_ptr, record_task, task_ids, batch_size: int = 512, seed: int = 0,
+                    epochs: int = 30, lr: float = 0.001, mu: float = 0.9):
+    """pretrain (tuner.cpp:130-156) on the device: returns (epoch_mean_loss list, dropped_singletons) like
+    PretrainLog. record_task: per-record index into task_ids (or the ids themselves)."""
+    if len(record_task) and isinstance(record_task[0], str):
+        ids = list(dict.fromkeys(list(task_ids) + list(record_task)))
+        ix = {t: i for i, t in enumerate(ids)}
+        record_task, task_ids = [ix[t] for t in record_task], ids
+    rt = np.ascontiguousarray(record_task, dtype=np.int32)
+    enc = [t.encode() for t in task_ids]
+    arr = (C.c_char_p * max(1, len(enc)))(*enc)
+    losses = np.zeros(max(epochs, 1))
+    dropped = C.c_int64()
+    _ck(lib().moses_pretrain_device(model.h, x_ptr, ldx, y_ptr, _p(rt), len(rt), C.cast(arr, C.c_void_p), len(enc),
+                                    batch_size, seed, epochs, lr, mu, _p(losses), C.byref(dropped)))
+    return losses[:epochs].tolist(), dropped.value
 
 
 class RecordStore:

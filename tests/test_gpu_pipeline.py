@@ -208,3 +208,42 @@ def test_train_plan_validation(ml, orc):
     assert e.value.code == "capacity"
     empty = ml.RankingPlan(np.zeros(0, dtype=np.int64), np.array([0]), np.zeros(0), ["a"], 0)
     assert ml.train_plan_device(dm, vp(X), ld, vp(Y), 10, empty, 0.001) == 0.0
+
+
+def test_pretrain_device_equals_plan_epochs(ml, orc):
+    """moses_pretrain_device (plans overlapped with device epochs) == explicit per-epoch plans through
+    moses_train_plan_device, bit for bit, with the same per-epoch losses and PretrainLog drop count."""
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 3)
+    a = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    b = ml.DeviceModel(p, ml.PREC_BF16, 512)
+    X, Y, task_of = _dataset(ml, orc, a, 1025, 2, ml.DTYPE_BF16)  # 1025 = 2 x 512 + a singleton per task
+    ids = [t for t, _ in TASKS]
+    losses, dropped = ml.pretrain_device(a, vp(X), a.packed_ld, vp(Y), task_of, ids, 512, 17, 4, 0.001, 0.9)
+    assert dropped == len(TASKS)
+    for e in range(4):
+        plan = ml.make_ranking_batches(task_of, ids, 512, ml.epoch_seed(17, e))
+        assert ml.train_plan_device(b, vp(X), b.packed_ld, vp(Y), len(task_of), plan, 0.001, 0.9) == losses[e]
+    pa, pb = a.download(), b.download()
+    assert np.array_equal(pa.params, pb.params) and np.array_equal(pa.momentum, pb.momentum)
+    with pytest.raises(ml.MosesError) as e:
+        ml.pretrain_device(a, vp(X), a.packed_ld, vp(Y), [], ids, 512, 17, 1)
+    assert e.value.code == "empty-dataset"
+
+
+def test_pretrain_device_fp32_matches_oracle(ml, orc):
+    """Two epochs of the reference's pretrain loop on an FP32 handle vs the fp64 oracle (tuner.cpp:130-156)."""
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 5)
+    dm = ml.DeviceModel(p, ml.PREC_FP32, 64)
+    X, Y, task_of = _dataset(ml, orc, dm, 50, 6, ml.DTYPE_F32)
+    losses, _ = ml.pretrain_device(dm, vp(X), dm.packed_ld, vp(Y), task_of, [t for t, _ in TASKS], 16, 8, 2,
+                                   0.01, 0.9)
+    feats, labels = X[:, :16].double().cpu().numpy(), Y.double().cpu().numpy()
+    w, mom = p.params.copy(), p.momentum.copy()
+    for e in range(2):
+        batches, _ = orc.make_ranking_batches(task_of, 16, orc.epoch_seed(8, e))
+        w, mom, mean_ref = orc.pretrain_epoch(dims, w, mom, feats, labels, batches, 0.01, 0.9)
+        assert abs(losses[e] - mean_ref) <= 1e-5 * max(1.0, abs(mean_ref))
+    got = dm.download()
+    assert np.max(np.abs(got.params - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))

@@ -12,8 +12,8 @@ timeout 900 python bench.py > gpurun_out/prof/bench.json 2> gpurun_out/prof/benc
 tail -3 gpurun_out/prof/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/prof/bench_ref.json 2> gpurun_out/prof/bench_ref.err; echo ref rc=$?
 N="ncu --clock-control none"
-timeout 600 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -c 400 --csv --log-file gpurun_out/prof/launches_train.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune --no-search --profile-steps 1 > /dev/null 2>&1; echo ncu1 rc=$?
-timeout 900 $N --set full --import-source on -k regex:"mlp_chain|wgrad_group|rank_cluster|head_backward" -s 16 -c 5 -o gpurun_out/prof/train_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune --no-search --profile-steps 1 > /dev/null 2>&1; echo ncu2 rc=$?
+timeout 600 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -c 400 --csv --log-file gpurun_out/prof/launches_train.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune --no-search --no-pretrain --profile-steps 1 > /dev/null 2>&1; echo ncu1 rc=$?
+timeout 900 $N --set full --import-source on -k regex:"mlp_chain|wgrad_group|rank_cluster|head_backward" -s 16 -c 5 -o gpurun_out/prof/train_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune --no-search --no-pretrain --profile-steps 1 > /dev/null 2>&1; echo ncu2 rc=$?
 timeout 600 $N --set full --import-source on -k regex:umma_fwd_pair -s 4 -c 2 -o gpurun_out/prof/score_full python tools/gemm_sweep.py pair > /dev/null 2>&1; echo ncu3 rc=$?
 timeout 600 $N --set full --import-source on -k regex:"lot_pass1c|lot_apply|lot_max" -c 3 -o gpurun_out/prof/lottery_full python tools/lot_prof.py ratio 1 > /dev/null 2>&1; echo ncu4 rc=$?
 timeout 600 $N --set full --import-source on -k regex:"lot_max|lot_apply" -c 2 -o gpurun_out/prof/lottery_thr_full python tools/lot_prof.py threshold 1 > /dev/null 2>&1; echo ncu4b rc=$?
@@ -25,7 +25,7 @@ import sys; sys.path.insert(0,'.'); import numpy as np
 from paper_2201_05752_b200 import moseslab as ml
 dims=[164,512,512,512,512,1]; p=ml.init_random(dims,1,strict=False); dm=ml.DeviceModel(p, ml.PREC_BF16, 16)
 dm.set_gradients(np.random.default_rng(0).normal(0,1e-2,dm.P)); ml.lottery_step(dm, ml.RATIO, 0.5, 0, 1e-3, 1e-2)" > /dev/null 2>&1; echo ncu8 rc=$?
-timeout 600 $N --set full --import-source on -k regex:"encode_configs|measure_configs" -c 2 -o gpurun_out/prof/space_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune > /dev/null 2>&1; echo ncu9 rc=$?
+timeout 600 $N --set full --import-source on -k regex:"encode_configs|measure_configs" -c 2 -o gpurun_out/prof/space_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-infer --no-hbm --no-finetune --no-pretrain > /dev/null 2>&1; echo ncu9 rc=$?
 # summaries on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back limit)
 P=gpurun_out/prof
 python tools/ncu_summary.py list $P/launches_train.csv $P/r_launches_train_summary.csv
