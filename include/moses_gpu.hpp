@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <algorithm>
 #include <string>
 #include <unordered_set>
 #include <utility>
@@ -370,5 +371,91 @@ inline void encode_configs(const TaskSpec& task, uint64_t first, int64_t n, Matr
                              first, n, features ? features->data.data() : nullptr,
                              hashes ? hashes->data() : nullptr));
 }
+
+// ---- data.hpp: record store, ranking-batch plans (row ids), epoch seed
+struct MeasurementRecord {  // oracle.hpp MeasurementRecord
+  std::string task_id;
+  std::vector<int64_t> values;
+  double throughput_gflops = 0.0, latency_ms = 0.0, wall_cost_ms = 0.0;
+  std::string device_id;
+  uint64_t seq = 0;
+};
+struct RecordStore {  // data.hpp:17-19
+  std::vector<MeasurementRecord> records;
+};
+namespace detail {
+struct RecordsHandle {
+  moses_records_t h = nullptr;
+  ~RecordsHandle() { moses_records_destroy(h); }
+};
+}  // namespace detail
+inline RecordStore read_records(const std::string& path) {  // data.cpp:113-126
+  detail::RecordsHandle r;
+  check(moses_records_read(path.c_str(), &r.h));
+  int64_t n = 0, nv = 0;
+  int32_t nt = 0, nd = 0;
+  check(moses_records_shape(r.h, &n, &nv, &nt, &nd));
+  std::vector<int32_t> task(static_cast<size_t>(n)), dev(static_cast<size_t>(n));
+  std::vector<int64_t> off(static_cast<size_t>(n) + 1), vals(static_cast<size_t>(nv));
+  std::vector<double> thr(static_cast<size_t>(n)), lat(static_cast<size_t>(n)), wall(static_cast<size_t>(n));
+  std::vector<uint64_t> seq(static_cast<size_t>(n));
+  check(moses_records_export(r.h, task.data(), dev.data(), off.data(), vals.data(), thr.data(), lat.data(), wall.data(),
+                             seq.data()));
+  RecordStore st;
+  st.records.resize(size_t(n));
+  for (int64_t i = 0; i < n; ++i) {
+    MeasurementRecord& m = st.records[size_t(i)];
+    m.task_id = moses_records_task_id(r.h, task[size_t(i)]);
+    m.device_id = moses_records_device_id(r.h, dev[size_t(i)]);
+    m.values.assign(vals.begin() + off[size_t(i)], vals.begin() + off[size_t(i) + 1]);
+    m.throughput_gflops = thr[size_t(i)];
+    m.latency_ms = lat[size_t(i)];
+    m.wall_cost_ms = wall[size_t(i)];
+    m.seq = seq[size_t(i)];
+  }
+  return st;
+}
+inline void write_records(const RecordStore& store, const std::string& path) {  // data.cpp:106-111
+  detail::RecordsHandle r;
+  check(moses_records_create(&r.h));
+  for (const auto& m : store.records)
+    check(moses_records_append(r.h, m.task_id.c_str(), m.device_id.c_str(), 1, int32_t(m.values.size()),
+                               m.values.data(), &m.throughput_gflops, &m.latency_ms, &m.wall_cost_ms, &m.seq));
+  check(moses_records_write(r.h, path.c_str()));
+}
+inline std::vector<std::string> store_task_ids(const RecordStore& store) {  // data.cpp:26-32
+  std::vector<std::string> ids;
+  for (const auto& r : store.records)
+    if (std::find(ids.begin(), ids.end(), r.task_id) == ids.end()) ids.push_back(r.task_id);
+  return ids;
+}
+struct RowBatch {  // RankingBatch as store row ids (features stay wherever the rows live)
+  std::string task_id;
+  std::vector<int64_t> rows;
+};
+struct BatchPlan {  // data.hpp:39-42
+  std::vector<RowBatch> batches;
+  int64_t dropped_singletons = 0;
+};
+inline BatchPlan make_ranking_batches(const RecordStore& store, int batch_size, uint64_t seed) {  // data.cpp:128-164
+  const std::vector<std::string> ids = store_task_ids(store);
+  std::vector<const char*> cids;
+  for (const auto& t : ids) cids.push_back(t.c_str());
+  std::vector<int32_t> rt;
+  for (const auto& r : store.records)
+    rt.push_back(int32_t(std::find(ids.begin(), ids.end(), r.task_id) - ids.begin()));
+  const int64_t n = int64_t(rt.size());
+  std::vector<int64_t> rows(size_t(n > 0 ? n : 1)), off(size_t(n / 2 + 2));
+  std::vector<int32_t> task(size_t(n / 2 + 1));
+  int64_t nb = 0;
+  BatchPlan plan;
+  check(moses_ranking_plan(rt.data(), n, cids.data(), int32_t(cids.size()), batch_size, seed, rows.data(), off.data(),
+                           task.data(), &nb, &plan.dropped_singletons));
+  for (int64_t b = 0; b < nb; ++b)
+    plan.batches.push_back({ids[size_t(task[size_t(b)])],
+                            std::vector<int64_t>(rows.begin() + off[size_t(b)], rows.begin() + off[size_t(b) + 1])});
+  return plan;
+}
+inline uint64_t epoch_seed(uint64_t seed, uint64_t epoch) { return moses_epoch_seed(seed, epoch); }  // tuner.cpp:136-139
 
 }  // namespace moseslab_gpu

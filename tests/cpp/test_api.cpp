@@ -146,6 +146,28 @@ int main() {
     CHECK(std::abs(f(0, 7) - 0.10034333188799373) < 1e-14 && f(0, 12) == 0.0);
     CHECK(h[0] == 0xc27c832e9cdb768dull);
   }
+  // test_data.cpp:115-143,162-192: record files round trip byte-identically; plans partition per task
+  {
+    RecordStore st;
+    for (int i = 0; i < 46; ++i)
+      st.records.push_back({i < 23 ? "a" : "b", {8, 64, 0, 1, 256}, 123.45678901234567 + i, 0.0078125, 1.5, "dev",
+                            uint64_t(i)});
+    write_records(st, "/tmp/moses_api_records.jsonl");
+    const RecordStore back = read_records("/tmp/moses_api_records.jsonl");
+    CHECK(back.records.size() == 46 && back.records[30].throughput_gflops == st.records[30].throughput_gflops &&
+          back.records[45].task_id == "b" && back.records[7].values == st.records[7].values);
+    const BatchPlan plan = make_ranking_batches(back, 8, 99);
+    int rows_a = 0, rows_b = 0;
+    for (const auto& b : plan.batches) {
+      CHECK(b.rows.size() >= 2 && b.rows.size() <= 8);
+      for (int64_t r : b.rows) CHECK(back.records[size_t(r)].task_id == b.task_id);
+      (b.task_id == "a" ? rows_a : rows_b) += int(b.rows.size());
+    }
+    CHECK(plan.batches.size() == 6 && plan.dropped_singletons == 0 && rows_a == 23 && rows_b == 23);
+    expect_error(ErrorCode::InvalidConfig, [&] { make_ranking_batches(back, 1, 0); });
+    CHECK(epoch_seed(5, 1) != epoch_seed(5, 2));
+    std::remove("/tmp/moses_api_records.jsonl");
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
