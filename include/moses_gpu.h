@@ -338,6 +338,9 @@ MOSES_API const char* moses_records_device_id(moses_records_t r, int32_t d);
 MOSES_API int moses_records_export(moses_records_t r, int32_t* task_index, int32_t* device_index, int64_t* value_off,
                                   int64_t* values, double* throughput, double* latency, double* wall_cost,
                                   uint64_t* seq);
+/* Test hook: force the fused ranking step's grid form (1) instead of the default policy (0:
+ * 16-CTA cluster form when the batch fits it, else the grid form). */
+MOSES_API int moses_debug_set_rank_grid(int32_t on);
 /* Test hook: force the sequential sampling walk in moses_generate_dataset_device. */
 MOSES_API int moses_debug_force_serial_sampling(int32_t on);
 

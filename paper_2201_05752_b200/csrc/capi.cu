@@ -2381,6 +2381,10 @@ MOSES_API int moses_records_export(moses_records_t r, int32_t* task_index, int32
     if (seq) std::copy_n(r->seq.begin(), n, seq);
   });
 }
+MOSES_API int moses_debug_set_rank_grid(int32_t on) {
+  debug_set_rank_grid(on != 0);
+  return MOSES_OK;
+}
 MOSES_API int moses_debug_force_serial_sampling(int32_t on) {
   debug_force_serial_sampling(on != 0);
   return MOSES_OK;

@@ -236,6 +236,12 @@ constexpr int kRankChunk = 32;  // j columns per block: n=512 -> 4 x 16 blocks, 
 // (s_r = b + sum_t part[t][r], the same fixed order as head_scores_kernel).
 // With `seg` (CSR program offsets over statement rows) the score of program r is the segment sum of
 // its statements' head dots (segment-sum pooling folded into the head).
+// 1 / (1 + e) for e in (0, 1]: MUFU reciprocal (<= 1 ulp), no IEEE slow-path branch in the pair loops
+__device__ __forceinline__ float rcp_pair(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float score_of(const float* __restrict__ s, const float* __restrict__ part, int ntiles,
                                           long long ld, float hb, const long long* __restrict__ seg, long long r) {
   if (part == nullptr) return s[r];
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
     const bool hi = yi > yj;
     const float d = hi ? si - ss[q] : ss[q] - si;  // s_hi - s_lo
     const float e = __expf(-fabsf(d));
-    const float inv = __frcp_rn(1.f + e);
+    const float inv = rcp_pair(1.f + e);
     const float sig_neg = d >= 0.f ? e * inv : inv;  // sigma(-d)
     if (hi) {
       gs -= sig_neg;
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(kRankThreads)
         const float w = float(yi > yj) - float(yi < yj);
         const float d = w * (si - ss[j0 + k]);
         const float e = __expf(-fabsf(d));
-        const float iv = __frcp_rn(1.f + e);
+        const float iv = rcp_pair(1.f + e);
         const float sig_neg = d >= 0.f ? e * iv : iv;
         gs = w != 0.f ? gs - w * sig_neg : gs;
         const bool hi = w > 0.f;
@@ -637,6 +643,192 @@ __global__ void __launch_bounds__(kRankThreads)
     *loss_out = P > 0 ? L * inv : 0.0;
     *pairs_out = P;
     if (gb_out != nullptr) *gb_out = P > 0 ? float(G * inv) : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------- fused ranking step, grid form
+// For batches past the cluster form's limits (n > ~1.4K programs). Every CTA of a plain grid (up
+// to one per SM) recomputes all n scores itself (reading the head partials from L2, no
+// all-gather), evaluates the pairs of its rows_per_cta
+// programs with the same (split, row) items and float partials as rank_pairs_kernel, and writes
+// per-row sums (split order, double) to global; the last CTA to finish (self re-arming ticket)
+// reduces the rows in row order and writes loss, pair count, head-bias gradient and every
+// statement row's backward coefficient. Deterministic and independent of the grid size.
+constexpr int kRgThreads = 512;
+__global__ void __launch_bounds__(kRgThreads)
+    rank_grid_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hbp,
+                     const long long* __restrict__ seg, const int* __restrict__ seg_of_row, const float* __restrict__ y,
+                     long long n, int nsplit, int rows_per_cta, float* __restrict__ s_out, long long R,
+                     double* __restrict__ row_g, double* __restrict__ row_l, long long* __restrict__ row_p,
+                     unsigned int* ticket, double* loss_out, long long* pairs_out, float* __restrict__ coefA,
+                     float* __restrict__ coefB, float* gb_out) {
+  extern __shared__ float rg_smem[];
+  const int items = rows_per_cta * nsplit;
+  float* ss = rg_smem;  // [n] scores
+  float* sy = ss + n;   // [n] labels
+  float* pg = sy + n;   // [items] per-(split, row) partials
+  float* pl = pg + items;
+  int* pp = reinterpret_cast<int*>(pl + items);
+  float* srow = reinterpret_cast<float*>(pp + items);  // pooled: statement-row head dots [R]
+  long long* sseg = reinterpret_cast<long long*>(
+      (reinterpret_cast<uintptr_t>(srow + (seg ? R : 0)) + 7) & ~uintptr_t(7));  // pooled: CSR offsets [n+1]
+  double* sg = reinterpret_cast<double*>(sseg + (seg ? n + 1 : 0));           // last CTA: row sums [n]
+  __shared__ bool is_last;
+  __shared__ double wl[kRgThreads / 32], wg[kRgThreads / 32];
+  __shared__ long long wp[kRgThreads / 32];
+  const int t = threadIdx.x;
+  const float hb = hbp[0];
+  for (long long p = t; p < n; p += blockDim.x) sy[p] = y[p];
+  // all scores: fixed tile order per statement row, then the segment sum (score_of()'s arithmetic);
+  // loads are issued 4 rows x 8 tiles at a time (one L2 round trip for ~2K rows)
+  auto row_dot = [&](long long r, long long r1, float* dst) {
+    float v[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        const long long rr = r + (long long)u * blockDim.x;
+        v[u][tt] = (rr < r1 && tt < ntiles) ? __ldg(part + tt * ld + rr) : 0.f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long rr = r + (long long)u * blockDim.x;
+      if (rr >= r1) continue;
+      float a = 0.f;
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt)
+        if (tt < ntiles) a += v[u][tt];
+      for (int tt = 8; tt < ntiles; ++tt) a += __ldg(part + tt * ld + rr);
+      dst[u] = a;
+    }
+  };
+  if (seg != nullptr) {
+    for (long long k = t; k <= n; k += blockDim.x) sseg[k] = seg[k];
+    __syncthreads();
+    const long long r0 = sseg[0], r1 = sseg[n];
+    for (long long r = r0 + t; r < r1; r += 4LL * blockDim.x) {
+      float d[4];
+      row_dot(r, r1, d);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r + (long long)u * blockDim.x < r1) srow[r + (long long)u * blockDim.x - r0] = d[u];
+    }
+    __syncthreads();
+    for (long long p = t; p < n; p += blockDim.x) {
+      float acc = 0.f;
+      const long long e = sseg[p + 1];
+      for (long long i = sseg[p]; i < e; ++i) acc += srow[i - r0];
+      ss[p] = acc + hb;
+    }
+  } else {
+    for (long long p = t; p < n; p += 4LL * blockDim.x) {
+      float d[4];
+      row_dot(p, n, d);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (p + (long long)u * blockDim.x < n) ss[p + (long long)u * blockDim.x] = d[u] + hb;
+    }
+  }
+  __syncthreads();
+  const long long p0 = min(n, (long long)blockIdx.x * rows_per_cta);
+  for (int it = t; it < items; it += blockDim.x) {  // same items / arithmetic as rank_cluster_kernel
+    const int sp = it / rows_per_cta, lr = it - sp * rows_per_cta;
+    const long long i = p0 + lr;
+    float gs = 0.f, loss = 0.f;
+    int pairs = 0;
+    if (i < n) {
+      const float si = ss[i], yi = sy[i];
+      const long long j0 = (long long)sp * kRankChunk;
+      const int cnt = int(min((long long)kRankChunk, n - j0));
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const float yj = sy[j0 + k];
+        const float w = float(yi > yj) - float(yi < yj);
+        const float d = w * (si - ss[j0 + k]);
+        const float e = __expf(-fabsf(d));
+        const float iv = rcp_pair(1.f + e);
+        const float sig_neg = d >= 0.f ? e * iv : iv;
+        gs = w != 0.f ? gs - w * sig_neg : gs;
+        const bool hi = w > 0.f;
+        loss += hi ? fmaxf(-d, 0.f) - 0.69314718f * __log2f(iv) : 0.f;
+        pairs += hi;
+      }
+    }
+    pg[it] = gs;
+    pl[it] = loss;
+    pp[it] = pairs;
+  }
+  __syncthreads();
+  for (int lr = t; lr < rows_per_cta; lr += blockDim.x) {
+    const long long i = p0 + lr;
+    if (i >= n) continue;
+    double g = 0.0, l = 0.0;
+    long long c = 0;
+    for (int k = 0; k < nsplit; ++k) {
+      g += pg[k * rows_per_cta + lr];
+      l += pl[k * rows_per_cta + lr];
+      c += pp[k * rows_per_cta + lr];
+    }
+    row_g[i] = g;
+    row_l[i] = l;
+    row_p[i] = c;
+    if (s_out != nullptr) s_out[i] = ss[i];
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // totals in row order: thread-strided (increasing rows), lane tree, warps in order
+  double l_t = 0.0, g_t = 0.0;
+  long long c_t = 0;
+  for (long long i = t; i < n; i += blockDim.x) {
+    const double gi = __ldcg(row_g + i);
+    sg[i] = gi;
+    l_t += __ldcg(row_l + i);
+    g_t += gi;
+    c_t += __ldcg(row_p + i);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    l_t += __shfl_down_sync(0xffffffffu, l_t, o);
+    g_t += __shfl_down_sync(0xffffffffu, g_t, o);
+    c_t += __shfl_down_sync(0xffffffffu, c_t, o);
+  }
+  if ((t & 31) == 0) {
+    wl[t >> 5] = l_t;
+    wg[t >> 5] = g_t;
+    wp[t >> 5] = c_t;
+  }
+  __syncthreads();
+  double L = 0.0, G = 0.0;
+  long long P = 0;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+    L += wl[w];
+    G += wg[w];
+    P += wp[w];
+  }
+  const double inv = P > 0 ? 1.0 / double(P) : 0.0;
+  if (seg != nullptr) {  // every statement row of program p carries d loss / d s_p; padding rows 0
+    for (long long p = t; p < n; p += blockDim.x) {
+      const float a = P > 0 ? float(sg[p] * inv) : 0.f;
+      for (long long r = sseg[p]; r < sseg[p + 1]; ++r) coefA[r] = a;
+    }
+    for (long long r = t; r < R; r += blockDim.x) {
+      coefB[r] = 0.f;
+      if (r < sseg[0] || r >= sseg[n]) coefA[r] = 0.f;
+    }
+  } else {
+    for (long long r = t; r < n; r += blockDim.x) {
+      coefA[r] = P > 0 ? float(sg[r] * inv) : 0.f;
+      coefB[r] = 0.f;
+    }
+  }
+  if (t == 0) {
+    *loss_out = P > 0 ? L * inv : 0.0;
+    *pairs_out = P;
+    if (gb_out != nullptr) *gb_out = P > 0 ? float(G * inv) : 0.f;
+    *ticket = 0u;  // re-arm for the next launch (stream-ordered)
   }
 }
 
@@ -1368,14 +1560,38 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
 void rank_trace_read(unsigned long long* out) {
   MOSES_CUDA(cudaMemcpyFromSymbol(out, g_rank_trace, sizeof(unsigned long long) * 16));
 }
+// Policy: the 16-CTA cluster form when the batch fits it (at n = 512 it is faster: the grid form's
+// 128 CTAs all read the same head partials, and its last-CTA tail adds ~3 us), else the grid form,
+// else (false) the two-kernel path. The test hook forces the grid form.
+static bool g_rank_grid = false;
+void debug_set_rank_grid(bool on) { g_rank_grid = on; }
 bool rank_step(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
                long long n, const RankWs& ws, unsigned int* ticket, float* s_out, const int* seg_of_row, long long R,
                const FinalizeOut& out, cudaStream_t st) {
-  (void)seg_of_row;
-  (void)ws;
-  (void)ticket;
   const int nsplit = rank_splits(n);
   if (n <= 0) return false;
+  const int cl_rows = ceil_div(n, kRankCluster);
+  const bool cluster_fits = cl_rows * nsplit <= kRankMaxItems && cl_rows <= kRankMaxRows &&
+                            size_t(2 * n + 3 * kRankMaxItems + (seg ? R : 0)) * 4 <= 160 * 1024;
+  if ((g_rank_grid || !cluster_fits) && ticket != nullptr) {
+    const int rows_per_cta = std::max<int>(4, ceil_div(n, 148));
+    const int grid = ceil_div(n, rows_per_cta);
+    const int items = rows_per_cta * nsplit;
+    const size_t smem = size_t(2 * n + 3 * items + (seg ? R : 0)) * 4 + 8 + (seg ? size_t(n + 1) * 8 : 0) + size_t(n) * 8;
+    if (smem <= 200 * 1024) {
+      static bool configured = false;
+      if (!configured) {
+        MOSES_CUDA(cudaFuncSetAttribute(rank_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+      }
+      rank_grid_kernel<<<grid, kRgThreads, smem, st>>>(part, ntiles, ld, hb, seg, seg ? seg_of_row : nullptr, y, n,
+                                                       nsplit, rows_per_cta, s_out, seg ? R : n, ws.gs_part,
+                                                       ws.loss_part, ws.pairs_part, ticket, out.loss, out.pairs,
+                                                       out.coefA, out.coefB, out.gb);
+      MOSES_CUDA(cudaGetLastError());
+      return true;
+    }
+  }
   const int rows_per_cta = ceil_div(n, kRankCluster);
   if (rows_per_cta * nsplit > kRankMaxItems || rows_per_cta > kRankMaxRows) return false;
   const size_t smem = size_t(2 * n + 3 * kRankMaxItems + (seg ? R : 0)) * 4;

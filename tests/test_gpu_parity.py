@@ -162,6 +162,24 @@ def test_gradients_vs_precision_model(ml, orc, dims, n, mode):
     assert abs(loss - loss64) <= TOL_TF32 * max(1.0, abs(loss64))
 
 
+@pytest.mark.parametrize("dims", [[16, 512, 512, 1], [164, 512, 512, 1]])
+@pytest.mark.parametrize("n", [1500, 3000])
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_gradients_large_batch_vs_precision_model(ml, orc, dims, n, mode):
+    """Ranking batches past the 16-CTA cluster form's limits take the grid form of the fused step."""
+    from precision_model import device_gradients
+
+    p = ml.init_random(dims, 22)
+    x, y = rows(n, dims[0], 9), labels(n, 10)
+    g_ref, _ = device_gradients(dims, p.params, x, y, mode)
+    dm = ml.DeviceModel(p, ml.PREC_TF32 if mode == "tf32" else ml.PREC_BF16, 4096)
+    g, loss = ml.gradients(dm, ml.RankingBatch(x, y), want_loss=True)
+    ok, why = grad_close(g, g_ref, q_tol=2e-3)
+    assert ok, why
+    _, loss64 = orc.gradients(dims, p.params, x, y, threads=8)
+    assert abs(loss - loss64) <= TOL_TF32 * max(1.0, abs(loss64))
+
+
 @pytest.mark.parametrize("dims", GRAD_DIMS)
 @pytest.mark.parametrize("prec", [1, 0])
 def test_train_step_updated_weights_vs_oracle(ml, orc, dims, prec):
@@ -893,3 +911,42 @@ def test_lottery_step_adam_bit_exact(ml, orc, dims, mode, value):
         w32, m1, m2 = orc.adam(w32, m1, m2, g32, lr, b1, b2, eps, step, ref_mask)
         w32 = orc.variant_decay(w32, ref_mask, lr, lam)
         assert np.array_equal(dm.download().params, w32.astype(np.float64)), step
+
+
+# ---------------------------------------------------------------- fused ranking step: grid vs cluster form
+@pytest.mark.parametrize("kind,n", [("plain", 2), ("plain", 64), ("plain", 512), ("plain", 1000), ("pooled", 37),
+                                    ("pooled", 512), ("pooled", 900), ("plain", 3000), ("pooled", 2000)])
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+def test_rank_step_grid_matches_cluster(ml, kind, n, prec):
+    """Both forms evaluate the same (split, row) pair items and per-row sums, so every backward
+    coefficient — hence every weight gradient except the head bias — is bitwise equal; loss and
+    head-bias gradient differ only by the order of the final double sums."""
+    dims = [164, 512, 512, 1]
+    p = ml.init_random(dims, 4)
+    dm = ml.DeviceModel(p, ml.PREC_BF16 if prec == "bf16" else ml.PREC_TF32, 16384)
+    rng = np.random.default_rng(n)
+    y = np.round(rng.random(n) * 8) / 8  # ties included
+    L = ml.lib()
+    out = []
+    for grid in (1, 0):
+        L.moses_debug_set_rank_grid(grid)  # 0: default policy (cluster form where it fits)
+        try:
+            if kind == "plain":
+                x = rng.random((n, 164)) if not out else xs
+                xs = x
+                g, loss = ml.gradients(dm, ml.RankingBatch(x, y), want_loss=True)
+            else:
+                off = ml.synth_offsets(7, n, 8)
+                x = rng.random((int(off[-1]), 164)) if not out else xs
+                xs = x
+                g, loss = ml.gradients_pooled(dm, x, off, y, want_loss=True)
+        finally:
+            L.moses_debug_set_rank_grid(0)
+        out.append((g, loss))
+    (g1, l1), (g0, l0) = out
+    hb = dm.P - 1  # head bias: last scalar of the reference order
+    mask = np.ones(dm.P, dtype=bool)
+    mask[hb] = False
+    assert np.array_equal(g1[mask], g0[mask])
+    assert abs(g1[hb] - g0[hb]) <= 1e-6 * max(1e-6, abs(g0[hb]))
+    assert abs(l1 - l0) <= 1e-12 * max(1.0, abs(l0))
