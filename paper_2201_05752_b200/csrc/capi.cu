@@ -234,6 +234,8 @@ struct moses_model {
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
   int* seg_rows = nullptr;         // pooled: program of each statement row (cap)
   unsigned int* rank_ticket = nullptr;  // rank_step last-CTA ticket (self re-arming)
+  long long rank_ws_rows = 0;           // ranking workspace sized for batches of this many rows
+  std::vector<void*> retired;           // outgrown workspaces (captured graphs may still point at them)
   // parameters
   float *w = nullptr, *mom = nullptr, *g = nullptr, *xi = nullptr;
   float *m1 = nullptr, *m2 = nullptr;
@@ -309,6 +311,7 @@ struct moses_model {
     dfree(seg_off);
     dfree(seg_rows);
     dfree(rank_ticket);
+    for (void* p : retired) dfree(p);
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
@@ -616,6 +619,22 @@ struct Pool {
   long long rows = 0;                  // statement rows incl. padding
 };
 
+// Ranking workspace (per-(split, row) partials of the two-kernel path, per-row sums of the grid
+// form): rank_splits(n) * n entries, allocated for min(cap, 4096) rows and grown on the first larger
+// batch. A grown-out buffer is retired, not freed: a CUDA graph captured earlier may reference it.
+constexpr long long kRankWsInitRows = 4096;
+void ensure_rank_ws(moses_model* m, long long n) {
+  if (n <= m->rank_ws_rows) return;
+  const long long ns = rank_splits(n);
+  for (void* p : {(void*)m->rank.gs_part, (void*)m->rank.loss_part, (void*)m->rank.pairs_part})
+    if (p) m->retired.push_back(p);
+  m->rank.gs_part = dalloc<double>(ns * n);
+  m->rank.loss_part = dalloc<double>(ns * n);
+  m->rank.pairs_part = dalloc<long long>(ns * n);
+  m->rank.nsplit = int(ns);
+  m->rank_ws_rows = n;
+}
+
 // gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch;
 // pooled: rows [0, pool->rows) are statements of the n programs.
 // Returns true when `fuse` (momentum SGD) was applied inside the backward pass; the caller runs
@@ -625,6 +644,7 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   const bool active = adv != nullptr && beta != 0.0 && n > 0 && pool == nullptr;
   const long long mrep = active ? adv->m : 0;
   const long long R = pool ? pool->rows : mrep + n;
+  ensure_rank_ws(m, n);  // before any capture-sensitive work (warm-ups reach here with the captured n)
   if (n == 0 || R == 0) {
     MOSES_CUDA(cudaMemsetAsync(m->g, 0, sizeof(float) * m->P, m->st));
     MOSES_CUDA(cudaMemsetAsync(m->dscal, 0, sizeof(double) * 2, m->st));
@@ -794,11 +814,7 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->labels = dalloc<float>(m->cap);
     m->coefA = dalloc<float>(m->cap);
     m->coefB = dalloc<float>(m->cap);
-    const int ns = rank_splits(m->cap);
-    m->rank.nsplit = ns;
-    m->rank.gs_part = dalloc<double>(ns * m->cap);
-    m->rank.loss_part = dalloc<double>(ns * m->cap);
-    m->rank.pairs_part = dalloc<long long>(ns * m->cap);
+    ensure_rank_ws(m.get(), std::min<long long>(m->cap, kRankWsInitRows));
     m->dscal = dalloc<double>(16);
     m->dpairs = dalloc<long long>(4);
     m->dcount = dalloc<unsigned long long>(4);
