@@ -41,7 +41,7 @@ struct GroupCfg {
   static constexpr int BM = 128, BN = 64, BK = 64;
   static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = 6;
+  static constexpr int kStages = 9;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
