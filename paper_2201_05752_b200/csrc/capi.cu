@@ -398,6 +398,10 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
 
 struct SgdFuse {  // momentum-SGD step fused into the grouped weight-gradient epilogue
   float lr, mu;
+  long long* counter = nullptr;      // training graphs: batch index to advance with the step
+  const double* loss_src = nullptr;  // plan epochs: loss to add into loss_acc with the step
+  double* loss_acc = nullptr;
+  mutable bool folded = false;       // set when the grouped wgrad kernel took the bookkeeping
 };
 
 // Returns true when `fuse` was applied (every parameter updated) inside the backward pass.
@@ -470,11 +474,25 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       }
       note_launch(1);
     }
+    if (fuse) {  // the head block (gradient from column_dot on st2) once head_backward has read it
+      MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (L - 1)], 0));
+      const long long o = m->off[L - 1];
+      ProfScope ps(P_UPDATE, m->st2);
+      sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, m->P - o, fuse->lr, fuse->mu, true,
+                 Shadow{m->wbf + o, 1}, m->st2);
+      note_launch(1);
+    }
     MOSES_CUDA(cudaEventRecord(ev[1], m->st));
     MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1], 0));
     WgradGroupCall wc;
     wc.n = L - 1;
     wc.K = int(R);
+    if (fuse) {
+      wc.counter = fuse->counter;
+      wc.loss_src = fuse->loss_src;
+      wc.loss_acc = fuse->loss_acc;
+      fuse->folded = true;
+    }
     for (int l = 0; l + 1 < L; ++l) {
       wc.a[l] = l == 0 ? x0 : m->act[l];
       wc.lda[l] = l == 0 ? ldx0 : m->ld[l];
@@ -497,13 +515,6 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       launch_wgrad_group(wc, m->st2);
     }
     note_launch(1);
-    if (fuse) {  // the head block (column_dot, same stream) gets the same update
-      const long long o = m->off[L - 1];
-      ProfScope ps(P_UPDATE, m->st2);
-      sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, m->P - o, fuse->lr, fuse->mu, true,
-                 Shadow{m->wbf + o, 1}, m->st2);
-      note_launch(1);
-    }
     MOSES_CUDA(cudaEventRecord(ev[L + 1], m->st2));
     MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 1], 0));
     return fuse != nullptr;
@@ -1169,12 +1180,12 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
     const long long row_bytes = ldx * m->esz;
     auto body = [&] {
       gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
-      const SgdFuse fz{float(lr), float(mu)};
+      const SgdFuse fz{float(lr), float(mu), m->dcounter};
       const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0, nullptr,
                                         with_update ? &fz : nullptr);
       if (with_update && !fused)
         sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-      advance_counter(m->dcounter, m->st);
+      if (!fz.folded) advance_counter(m->dcounter, m->st);
     };
     {  // eager warm-up without the update (configures kernels, validates shapes; params untouched)
       gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
@@ -1234,12 +1245,12 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
     try {
       gather();
-      const SgdFuse fz{float(lr), float(mu)};
+      const SgdFuse fz{float(lr), float(mu), m->dcounter};
       const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool,
                                         with_update ? &fz : nullptr);
       if (with_update && !fused)
         sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-      advance_counter(m->dcounter, m->st);
+      if (!fz.folded) advance_counter(m->dcounter, m->st);
     } catch (...) {
       cudaStreamEndCapture(m->st, &graph);
       throw;
@@ -2139,15 +2150,18 @@ void plan_step(moses_model* m, const void* x, long long ldx, const float* y, lon
   } else {
     gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st);
   }
-  const SgdFuse fz{lr, mu};
+  const SgdFuse fz{lr, mu, ps.counter, m->dscal, ps.loss_sum};
   if (!gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, &fz)) {
     sgd_update(m->w, m->mom, m->g, nullptr, m->P, lr, mu, true, m->shadow(), m->st);
     m->post_update();
     note_launch(1);
   }
-  accum_f64(m->dscal, ps.loss_sum, m->st);
-  advance_counter(ps.counter, m->st);
-  note_launch(3);
+  if (!fz.folded) {
+    accum_f64(m->dscal, ps.loss_sum, m->st);
+    advance_counter(ps.counter, m->st);
+    note_launch(2);
+  }
+  note_launch(1);
 }
 // full-size batches replay one CUDA graph, captured once per dataset / size / hyper-parameters;
 // needs the plan's rows on the device (the warm-up gathers batch 0's slots)

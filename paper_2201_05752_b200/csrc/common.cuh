@@ -113,6 +113,9 @@ struct WgradGroupCall {
   void* shadow[8] = {};
   float lr = 0.f, mu = 0.f;
   bool update = false;
+  long long* counter = nullptr;
+  const double* loss_src = nullptr;
+  double* loss_acc = nullptr;
 };
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
 extern int g_group;

@@ -363,6 +363,9 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   a.tile_begin[c.n] = tiles;
   a.lr = c.lr;
   a.mu = c.mu;
+  a.counter = c.counter;
+  a.loss_src = c.loss_src;
+  a.loss_acc = c.loss_acc;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(128);

@@ -35,6 +35,9 @@ struct GroupArgs {
   float* mom[kGroupMax];
   __nv_bfloat16* shadow[kGroupMax];
   float lr, mu;
+  long long* counter;      // optional: step counter advanced once (training graphs' batch index)
+  const double* loss_src;  // optional: *loss_acc += *loss_src once (epoch loss sum)
+  double* loss_acc;
 };
 
 struct GroupCfg {
@@ -84,6 +87,10 @@ __global__ void __launch_bounds__(128, 1)
   }
   if (warp == 2) ptx::tmem_alloc<BN>(tmem_slot);
   ptx::pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 32) {  // step bookkeeping folded into the step's last kernel
+    if (args.counter != nullptr) *args.counter += 1;
+    if (args.loss_acc != nullptr) *args.loss_acc += *args.loss_src;
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
