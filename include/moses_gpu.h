@@ -318,6 +318,17 @@ MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t
                                    int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs,
                                    double learning_rate, double momentum, double* epoch_mean_loss,
                                    int64_t* dropped_singletons);
+/* Job pool over independent pretrain runs sharing one device-resident dataset (the reference's
+ * (strategy, seed) std::thread pool, tuner.cpp:57-69,331-374): job j runs moses_pretrain_device on
+ * models[j] with seeds[j]; `threads` workers (0: MOSES_LAB_THREADS, else the hardware concurrency;
+ * capped at n_jobs) claim jobs in order. Each handle has its own streams, so the jobs' latency-bound
+ * steps overlap on the GPU. epoch_mean_loss: n_jobs x epochs (row per job); dropped_singletons:
+ * n_jobs. Returns the lowest-numbered failing job's status. */
+MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                                 const void* x_base, int64_t ldx, const float* y_base, const int32_t* record_task,
+                                 int64_t n_records, const char* const* task_ids, int32_t n_task_ids,
+                                 int32_t batch_size, int32_t epochs, double learning_rate, double momentum,
+                                 int32_t threads, double* epoch_mean_loss, int64_t* dropped_singletons);
 /* Line-delimited record files (data.cpp:67-126). moses_records_read fails with MOSES_ERR_IO,
  * MOSES_ERR_PARSE (message names "<path>:line N") or MOSES_ERR_MISSING_FIELD. */
 MOSES_API int moses_records_create(moses_records_t* out);

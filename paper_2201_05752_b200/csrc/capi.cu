@@ -13,11 +13,13 @@
 #include <atomic>
 #include <bit>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_set>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -2251,11 +2253,11 @@ MOSES_API int moses_train_plan_device(moses_model_t m, const void* x_base, int64
 // -> make_ranking_batches -> one step per batch. The host computes epoch e+1's plan (into pinned
 // memory) while the device runs epoch e; plan uploads and per-epoch loss sums are stream-ordered,
 // so the only synchronisation is the final read of the per-epoch losses.
-MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
-                                   const int32_t* record_task, int64_t n_records, const char* const* task_ids,
-                                   int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs, double lr,
-                                   double mu, double* epoch_mean_loss, int64_t* dropped_singletons) {
-  return guarded([&] {
+static void pretrain_impl(moses_model* m, const void* x_base, int64_t ldx, const float* y_base,
+                          const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                          int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs, double lr, double mu,
+                          double* epoch_mean_loss, int64_t* dropped_singletons) {
+  {
     require_model(m);
     if (n_records <= 0) fail(MOSES_ERR_EMPTY_DATASET, "no records to pretrain on");
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
@@ -2325,6 +2327,82 @@ MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t
       throw;
     }
     cleanup();
+  }
+}
+
+MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
+                                   const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                   int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs, double lr,
+                                   double mu, double* epoch_mean_loss, int64_t* dropped_singletons) {
+  return guarded([&] {
+    pretrain_impl(m, x_base, ldx, y_base, record_task, n_records, task_ids, n_task_ids, batch_size, seed, epochs, lr,
+                  mu, epoch_mean_loss, dropped_singletons);
+  });
+}
+
+// Job pool over independent pretrain runs (the reference's (strategy, seed) pool, tuner.cpp:57-69,
+// 331-374): jobs are claimed in order by `threads` workers (0: MOSES_LAB_THREADS or the hardware
+// concurrency, capped at the job count); every job owns its model handle and therefore its CUDA
+// streams, so the GPU runs the jobs' small, latency-bound steps concurrently. The first failing
+// job's status is returned; the others still run to completion or to their own error.
+MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                                 const void* x_base, int64_t ldx, const float* y_base, const int32_t* record_task,
+                                 int64_t n_records, const char* const* task_ids, int32_t n_task_ids,
+                                 int32_t batch_size, int32_t epochs, double lr, double mu, int32_t threads,
+                                 double* epoch_mean_loss, int64_t* dropped_singletons) {
+  return guarded([&] {
+    if (n_jobs < 0 || (n_jobs > 0 && (models == nullptr || seeds == nullptr)))
+      fail(MOSES_ERR_INVALID_ARG, "invalid job list");
+    if (n_jobs == 0) return;
+    int width = threads;
+    if (width <= 0) {
+      width = int(std::thread::hardware_concurrency());
+      if (const char* env = std::getenv("MOSES_LAB_THREADS"); env != nullptr && *env != '\0') {
+        char* end = nullptr;
+        const long v = std::strtol(env, &end, 10);
+        if (end == env || *end != '\0' || v < 0)
+          fail(MOSES_ERR_INVALID_CONFIG, std::string("bad MOSES_LAB_THREADS value '") + env + "'");
+        if (v > 0) width = int(v);
+      }
+    }
+    width = std::max(1, std::min(width, n_jobs));
+    std::atomic<int> next{0};
+    std::mutex mu_err;
+    int first_job = -1, first_code = 0;
+    std::string first_msg;
+    auto worker = [&] {
+      for (;;) {
+        const int j = next.fetch_add(1);
+        if (j >= n_jobs) return;
+        try {
+          pretrain_impl(models[j], x_base, ldx, y_base, record_task, n_records, task_ids, n_task_ids, batch_size,
+                        seeds[j], epochs, lr, mu, epoch_mean_loss ? epoch_mean_loss + size_t(j) * epochs : nullptr,
+                        dropped_singletons ? dropped_singletons + j : nullptr);
+        } catch (const Status& e) {
+          std::lock_guard<std::mutex> lk(mu_err);
+          if (first_job < 0 || j < first_job) {
+            first_job = j;
+            first_code = e.code;
+            first_msg = e.what();
+          }
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(mu_err);
+          if (first_job < 0 || j < first_job) {
+            first_job = j;
+            first_code = MOSES_ERR_INVALID_ARG;
+            first_msg = e.what();
+          }
+        }
+      }
+    };
+    if (width == 1) {
+      worker();
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < width; ++t) pool.emplace_back(worker);
+      for (auto& t : pool) t.join();
+    }
+    if (first_job >= 0) fail(first_code, "job " + std::to_string(first_job) + ": " + first_msg);
   });
 }
 

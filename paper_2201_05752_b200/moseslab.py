@@ -137,6 +137,7 @@ def lib():
         "moses_replay_rows": (C.c_int, [i64, i64, u64, vp, vp]),
         "moses_train_plan_device": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, dbl, dbl, vp]),
         "moses_pretrain_device": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, i32, i32, u64, i32, dbl, dbl, vp, vp]),
+        "moses_pretrain_jobs": (C.c_int, [i32, vp, vp, vp, i64, vp, vp, i64, vp, i32, i32, i32, dbl, dbl, i32, vp, vp]),
         "moses_records_create": (C.c_int, [vp]),
         "moses_records_read": (C.c_int, [C.c_char_p, vp]),
         "moses_records_destroy": (None, [vp]),
@@ -891,6 +892,27 @@ def pretrain_device(model, x_ptr, ldx: int, y_ptr, record_task, task_ids, batch_
     _ck(lib().moses_pretrain_device(model.h, x_ptr, ldx, y_ptr, _p(rt), len(rt), C.cast(arr, C.c_void_p), len(enc),
                                     batch_size, seed, epochs, lr, mu, _p(losses), C.byref(dropped)))
     return losses[:epochs].tolist(), dropped.value
+
+
+def pretrain_jobs(models, seeds, x_ptr, ldx: int, y_ptr, record_task, task_ids, batch_size: int = 512,
+                  epochs: int = 30, lr: float = 0.001, mu: float = 0.9, threads: int = 0):
+    """Independent pretrain runs (one per (model, seed)) over one device-resident dataset on a native
+    worker pool (tuner.cpp:331-374). Returns (epoch_mean_loss [jobs x epochs], dropped [jobs])."""
+    if len(record_task) and isinstance(record_task[0], str):
+        ids = list(dict.fromkeys(list(task_ids) + list(record_task)))
+        ix = {t: i for i, t in enumerate(ids)}
+        record_task, task_ids = [ix[t] for t in record_task], ids
+    rt = np.ascontiguousarray(record_task, dtype=np.int32)
+    enc = [t.encode() for t in task_ids]
+    arr = (C.c_char_p * max(1, len(enc)))(*enc)
+    hs = (C.c_void_p * max(1, len(models)))(*[m.h.value if hasattr(m.h, "value") else m.h for m in models])
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    losses = np.zeros((max(len(models), 1), max(epochs, 1)))
+    dropped = np.zeros(max(len(models), 1), dtype=np.int64)
+    _ck(lib().moses_pretrain_jobs(len(models), C.cast(hs, C.c_void_p), _p(sd), x_ptr, ldx, y_ptr, _p(rt), len(rt),
+                                  C.cast(arr, C.c_void_p), len(enc), batch_size, epochs, lr, mu, threads,
+                                  _p(losses), _p(dropped)))
+    return losses[:len(models), :epochs], dropped[:len(models)]
 
 
 class RecordStore:

@@ -247,3 +247,22 @@ def test_pretrain_device_fp32_matches_oracle(ml, orc):
         assert abs(losses[e] - mean_ref) <= 1e-5 * max(1.0, abs(mean_ref))
     got = dm.download()
     assert np.max(np.abs(got.params - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+def test_pretrain_jobs_equal_sequential_runs(ml, orc, threads):
+    """The native job pool (tuner.cpp:331-374 shape): every job's parameters and epoch losses equal
+    its own sequential moses_pretrain_device run, bit for bit, whatever the worker count."""
+    dims = [16, 512, 512, 1]
+    seeds = [11, 12, 13, 14, 15]
+    pool = [ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16, 512) for s in seeds]
+    X, Y, task_of = _dataset(ml, orc, pool[0], 600, 4, ml.DTYPE_BF16)
+    ids = [t for t, _ in TASKS]
+    ld = pool[0].packed_ld
+    losses, dropped = ml.pretrain_jobs(pool, seeds, vp(X), ld, vp(Y), task_of, ids, 128, 3, 0.001, 0.9, threads)
+    for j, s in enumerate(seeds):
+        ref = ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16, 512)
+        l_ref, d_ref = ml.pretrain_device(ref, vp(X), ld, vp(Y), task_of, ids, 128, s, 3, 0.001, 0.9)
+        assert losses[j].tolist() == l_ref and dropped[j] == d_ref
+        a, b = pool[j].download(), ref.download()
+        assert np.array_equal(a.params, b.params) and np.array_equal(a.momentum, b.momentum)
