@@ -318,6 +318,19 @@ MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t
                                    int32_t n_task_ids, int32_t batch_size, uint64_t seed, int32_t epochs,
                                    double learning_rate, double momentum, double* epoch_mean_loss,
                                    int64_t* dropped_singletons);
+/* pretrain(store, tasks, hyper, log) (tuner.cpp:130-156) from host records: record_task[i] indexes
+ * the task tables (task_ids, task4 = n_tasks x {work_gflops, bytes_per_unit, ideal_log2_tiles,
+ * ideal_log2_unroll}; one knob template shared by all tasks, as the default task set); values are
+ * n_records x n_knobs knob values, throughput the measured labels. The store is staged and encoded
+ * on the device (grouped by task; batch composition unchanged), then moses_pretrain_device runs on
+ * the handle, which carries the initial parameters. Invalid values fail with
+ * MOSES_ERR_INVALID_CONFIG naming the record. */
+MOSES_API int moses_pretrain(moses_model_t m, int32_t n_tasks, const char* const* task_ids, const double* task4,
+                            const int64_t* domains, const int32_t* domain_sizes, const int32_t* roles,
+                            int32_t n_knobs, const int32_t* record_task, const int64_t* values,
+                            const double* throughput, int64_t n_records, int32_t batch_size, uint64_t seed,
+                            int32_t epochs, double learning_rate, double momentum, double* epoch_mean_loss,
+                            int64_t* dropped_singletons);
 /* Job pool over independent pretrain runs sharing one device-resident dataset (the reference's
  * (strategy, seed) std::thread pool, tuner.cpp:57-69,331-374): job j runs moses_pretrain_device on
  * models[j] with seeds[j]; `threads` workers (0: MOSES_LAB_THREADS, else the hardware concurrency;

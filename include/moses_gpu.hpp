@@ -458,4 +458,50 @@ inline BatchPlan make_ranking_batches(const RecordStore& store, int batch_size, 
 }
 inline uint64_t epoch_seed(uint64_t seed, uint64_t epoch) { return moses_epoch_seed(seed, epoch); }  // tuner.cpp:136-139
 
+// ---- tuner.hpp: pretrain (tuner.cpp:130-156) on the device
+struct PretrainLog {  // tuner.hpp PretrainLog
+  int64_t dropped_singletons = 0;
+  std::vector<double> epoch_mean_loss;
+};
+// Model {16,512,512,1} from init_random(dims, hyper.seed), hyper.max_epochs epochs of keyed ranking
+// batches; every task shares tasks[0]'s knob template (the default task set). precision: operand
+// precision of the device model (MOSES_PREC_FP32 for fp32-level parity with the fp64 reference).
+inline CostModelParams pretrain(const RecordStore& store, const std::vector<TaskSpec>& tasks, const TrainHyper& hyper,
+                                PretrainLog* log = nullptr, int precision = MOSES_PREC_BF16) {
+  if (store.records.empty()) check(MOSES_ERR_EMPTY_DATASET);
+  if (tasks.empty()) check(MOSES_ERR_INVALID_TASK);
+  const detail::SpaceArrays sp(tasks[0]);
+  std::vector<const char*> ids;
+  std::vector<double> t4;
+  for (const auto& t : tasks) {
+    ids.push_back(t.id.c_str());
+    t4.insert(t4.end(), {t.work_gflops, t.bytes_per_unit, t.ideal_log2_tiles, t.ideal_log2_unroll});
+  }
+  const size_t nk = tasks[0].knobs.size();
+  std::vector<int32_t> rt;
+  std::vector<int64_t> vals;
+  std::vector<double> thr;
+  for (const auto& r : store.records) {
+    int32_t t = -1;
+    for (size_t k = 0; k < tasks.size(); ++k)
+      if (tasks[k].id == r.task_id) t = int32_t(k);
+    if (t < 0 || r.values.size() != nk) check(t < 0 ? MOSES_ERR_INVALID_TASK : MOSES_ERR_INVALID_CONFIG);
+    rt.push_back(t);
+    vals.insert(vals.end(), r.values.begin(), r.values.end());
+    thr.push_back(r.throughput_gflops);
+  }
+  DeviceModel m(init_random({16, 512, 512, 1}, hyper.seed), precision, std::max(hyper.batch_size, 2));
+  std::vector<double> losses(size_t(std::max(hyper.max_epochs, 0)));
+  int64_t dropped = 0;
+  check(moses_pretrain(m.handle(), int32_t(tasks.size()), ids.data(), t4.data(), sp.domains.data(), sp.sizes.data(),
+                       sp.roles.data(), int32_t(nk), rt.data(), vals.data(), thr.data(), int64_t(rt.size()),
+                       hyper.batch_size, hyper.seed, hyper.max_epochs, hyper.learning_rate, hyper.momentum,
+                       losses.data(), &dropped));
+  if (log) {
+    log->dropped_singletons = dropped;
+    log->epoch_mean_loss = losses;
+  }
+  return m.download();
+}
+
 }  // namespace moseslab_gpu

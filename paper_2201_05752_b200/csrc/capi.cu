@@ -2340,6 +2340,90 @@ MOSES_API int moses_pretrain_device(moses_model_t m, const void* x_base, int64_t
   });
 }
 
+// pretrain(store, tasks, hyper) (tuner.cpp:130-156) from host records: the store is staged on the
+// device grouped by task (first-appearance order, store order within a task — the per-task row
+// lists make_ranking_batches shuffles are unchanged, so every batch holds the same records), each
+// task's rows are validated and encoded on the device (encode_features, one shared knob template),
+// labels are the measured throughputs, then the epoch loop runs on the handle.
+MOSES_API int moses_pretrain(moses_model_t m, int32_t n_tasks, const char* const* task_ids, const double* task4,
+                            const int64_t* domains, const int32_t* domain_sizes, const int32_t* roles,
+                            int32_t n_knobs, const int32_t* record_task, const int64_t* values,
+                            const double* throughput, int64_t n_records, int32_t batch_size, uint64_t seed,
+                            int32_t epochs, double lr, double mu, double* epoch_mean_loss,
+                            int64_t* dropped_singletons) {
+  return guarded([&] {
+    require_model(m);
+    if (n_records <= 0) fail(MOSES_ERR_EMPTY_DATASET, "no records to pretrain on");
+    if (m->dims[0] < 10) fail(MOSES_ERR_DIM_MISMATCH, "model input width below the 10 live feature entries");
+    if (n_tasks <= 0 || task_ids == nullptr || task4 == nullptr || record_task == nullptr || values == nullptr ||
+        throughput == nullptr)
+      fail(MOSES_ERR_INVALID_ARG, "null store or task table");
+    // group by task: first-appearance order, store order within a task
+    std::vector<int> order;
+    std::vector<std::vector<long long>> rows(static_cast<size_t>(n_tasks));
+    for (long long i = 0; i < n_records; ++i) {
+      const int t = record_task[i];
+      if (t < 0 || t >= n_tasks) fail(MOSES_ERR_INVALID_TASK, "record " + std::to_string(i) + ": unknown task id");
+      if (rows[t].empty()) order.push_back(t);
+      rows[t].push_back(i);
+    }
+    std::vector<long long> vals_g(size_t(n_records) * n_knobs);
+    std::vector<float> lab_g(static_cast<size_t>(n_records));
+    std::vector<int32_t> task_g(static_cast<size_t>(n_records));
+    std::vector<long long> first(size_t(n_tasks) + 1, 0);
+    long long pos = 0;
+    for (int t : order) {
+      first[t] = pos;
+      for (long long i : rows[t]) {
+        std::copy(values + i * n_knobs, values + (i + 1) * n_knobs, vals_g.begin() + pos * n_knobs);
+        lab_g[size_t(pos)] = float(throughput[i]);
+        task_g[size_t(pos)] = t;
+        ++pos;
+      }
+    }
+    const long long ld = m->ld[0];
+    void* X = nullptr;
+    long long* V = nullptr;
+    float* Y = nullptr;
+    auto release = [&] {
+      cudaStreamSynchronize(m->st);
+      dfree(X);
+      dfree(V);
+      dfree(Y);
+    };
+    try {
+      X = dalloc<uint8_t>(size_t(n_records) * ld * m->esz);
+      V = dalloc<long long>(size_t(n_records) * n_knobs);
+      Y = dalloc<float>(size_t(n_records));
+      MOSES_CUDA(cudaMemcpyAsync(V, vals_g.data(), sizeof(long long) * vals_g.size(), cudaMemcpyHostToDevice, m->st));
+      MOSES_CUDA(cudaMemcpyAsync(Y, lab_g.data(), sizeof(float) * lab_g.size(), cudaMemcpyHostToDevice, m->st));
+      MOSES_CUDA(cudaMemsetAsync(X, 0, size_t(n_records) * ld * m->esz, m->st));
+      const int kind = m->esz == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32;
+      for (int t : order) {
+        long long bad = -1;
+        const long long cnt = (long long)rows[t].size();
+        try {
+          note_launch(encode_values(task4 + 4 * t, reinterpret_cast<const long long*>(domains), domain_sizes, roles,
+                                    n_knobs, V + first[t] * n_knobs, cnt, kind,
+                                    static_cast<uint8_t*>(X) + first[t] * ld * m->esz, ld, m->dims[0], nullptr,
+                                    nullptr, &bad, m->st));
+        } catch (const Status& e) {
+          if (bad >= 0)  // report the caller's record index
+            fail(e.code, "record " + std::to_string(rows[t][size_t(bad)]) + " (task " + task_ids[t] +
+                             "): value not in its knob's domain");
+          throw;
+        }
+      }
+      pretrain_impl(m, X, ld, Y, task_g.data(), n_records, task_ids, n_tasks, batch_size, seed, epochs, lr, mu,
+                    epoch_mean_loss, dropped_singletons);
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+  });
+}
+
 // Job pool over independent pretrain runs (the reference's (strategy, seed) pool, tuner.cpp:57-69,
 // 331-374): jobs are claimed in order by `threads` workers (0: MOSES_LAB_THREADS or the hardware
 // concurrency, capped at the job count); every job owns its model handle and therefore its CUDA

@@ -138,6 +138,7 @@ def lib():
         "moses_train_plan_device": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, dbl, dbl, vp]),
         "moses_pretrain_device": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, i32, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_pretrain_jobs": (C.c_int, [i32, vp, vp, vp, i64, vp, vp, i64, vp, i32, i32, i32, dbl, dbl, i32, vp, vp]),
+        "moses_pretrain": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_records_create": (C.c_int, [vp]),
         "moses_records_read": (C.c_int, [C.c_char_p, vp]),
         "moses_records_destroy": (None, [vp]),
@@ -891,6 +892,26 @@ def pretrain_device(model, x_ptr, ldx: int, y_ptr, record_task, task_ids, batch_
     dropped = C.c_int64()
     _ck(lib().moses_pretrain_device(model.h, x_ptr, ldx, y_ptr, _p(rt), len(rt), C.cast(arr, C.c_void_p), len(enc),
                                     batch_size, seed, epochs, lr, mu, _p(losses), C.byref(dropped)))
+    return losses[:epochs].tolist(), dropped.value
+
+
+def pretrain(model, tasks, knobs, record_task, values, throughput, batch_size: int = 512, seed: int = 0,
+             epochs: int = 30, lr: float = 0.001, mu: float = 0.9):
+    """pretrain (tuner.cpp:130-156) from host records on the device. tasks = [(task_id, task4)];
+    record_task: per-record index into tasks; values: n x n_knobs; throughput: labels.
+    Returns (epoch_mean_loss list, dropped_singletons); the parameters stay on `model`."""
+    dom, sizes, roles = _space_arrays(knobs)
+    enc = [t.encode() for t, _ in tasks]
+    arr = (C.c_char_p * max(1, len(enc)))(*enc)
+    t4 = np.ascontiguousarray([_task4(t) for _, t in tasks], dtype=np.float64)
+    rt = np.ascontiguousarray(record_task, dtype=np.int32)
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    thr = np.ascontiguousarray(throughput, dtype=np.float64)
+    losses = np.zeros(max(epochs, 1))
+    dropped = C.c_int64()
+    _ck(lib().moses_pretrain(model.h, len(tasks), C.cast(arr, C.c_void_p), _p(t4), _p(dom), _p(sizes), _p(roles),
+                             len(knobs), _p(rt), _p(v), _p(thr), len(rt), batch_size, seed, epochs, lr, mu,
+                             _p(losses), C.byref(dropped)))
     return losses[:epochs].tolist(), dropped.value
 
 

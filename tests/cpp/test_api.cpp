@@ -168,6 +168,31 @@ int main() {
     CHECK(epoch_seed(5, 1) != epoch_seed(5, 2));
     std::remove("/tmp/moses_api_records.jsonl");
   }
+  // test_tuner.cpp:320-340 shape: pretrain logs epoch losses and counts dropped singletons; the
+  // loss falls over the epochs on a learnable store
+  {
+    TaskSpec ta{"a", 1.0, 4.0, 6.0, 3.0, default_knob_template()};
+    TaskSpec tb{"b", 1.0, 4.0, 9.0, 3.0, default_knob_template()};
+    RecordStore st;
+    for (int i = 0; i < 131; ++i) {
+      const int64_t tx = int64_t(1) << (i % 7), ty = int64_t(1) << ((i / 7) % 7);
+      st.records.push_back({i % 2 ? "a" : "b", {tx, ty, 16, 4, 16}, double(tx * ty) + 0.5 * (i % 5), 1.0, 1.0, "d",
+                            uint64_t(i)});
+    }
+    TrainHyper h;
+    h.max_epochs = 6;
+    h.batch_size = 16;
+    h.learning_rate = 0.01;
+    PretrainLog log;
+    const CostModelParams p = pretrain(st, {ta, tb}, h, &log);
+    CHECK(p.params.size() == size_t(param_count({16, 512, 512, 1})) && log.epoch_mean_loss.size() == 6);
+    CHECK(log.dropped_singletons == 1);  // "a" has 65 rows: 4 x 16 + 1
+    CHECK(log.epoch_mean_loss.back() < log.epoch_mean_loss.front());
+    RecordStore bad = st;
+    bad.records[3].values[2] = 17;  // not an unroll value
+    expect_error(ErrorCode::InvalidConfig, [&] { pretrain(bad, {ta, tb}, h); });
+    expect_error(ErrorCode::EmptyDataset, [&] { pretrain(RecordStore{}, {ta, tb}, h); });
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -266,3 +266,37 @@ def test_pretrain_jobs_equal_sequential_runs(ml, orc, threads):
         assert losses[j].tolist() == l_ref and dropped[j] == d_ref
         a, b = pool[j].download(), ref.download()
         assert np.array_equal(a.params, b.params) and np.array_equal(a.momentum, b.momentum)
+
+
+def test_pretrain_from_records_matches_oracle(ml, orc):
+    """moses_pretrain (host records -> device staging grouped by task -> encode -> epochs) on an FP32
+    handle vs the fp64 oracle's pretrain over the same records (tuner.cpp:130-156): same batches,
+    epoch losses and parameters within 1e-5."""
+    knobs = orc.default_knob_template()
+    recs = orc.generate_dataset(TOY_DEVICE, TASKS, knobs, 40, 3)
+    order = [2, 0, 1]  # interleave tasks in the store: grouping must not change batch composition
+    recs = [r for k in range(40) for t in order for r in [recs[t * 40 + k]]]
+    ids = [t for t, _ in TASKS]
+    rt = [ids.index(r["task_id"]) for r in recs]
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 6)
+    dm = ml.DeviceModel(p, ml.PREC_FP32, 64)
+    losses, dropped = ml.pretrain(dm, TASKS, knobs, rt, [r["values"] for r in recs],
+                                  [r["throughput_gflops"] for r in recs], 16, 6, 2, 0.01, 0.9)
+    feats = np.stack([r["features"] for r in recs]).astype(np.float32).astype(np.float64)
+    labels = np.array([r["throughput_gflops"] for r in recs], dtype=np.float32).astype(np.float64)
+    w, mom = p.params.copy(), p.momentum.copy()
+    task_of = [r["task_id"] for r in recs]
+    for e in range(2):
+        batches, drop = orc.make_ranking_batches(task_of, 16, orc.epoch_seed(6, e))
+        if e == 0:
+            assert dropped == drop
+        w, mom, mean_ref = orc.pretrain_epoch(dims, w, mom, feats, labels, batches, 0.01, 0.9)
+        assert abs(losses[e] - mean_ref) <= 1e-5 * max(1.0, abs(mean_ref))
+    got = dm.download()
+    assert np.max(np.abs(got.params - w)) <= 1e-5 * max(1.0, np.max(np.abs(w)))
+    bad = [list(r["values"]) for r in recs]
+    bad[7][2] = 17
+    with pytest.raises(ml.MosesError) as e:
+        ml.pretrain(dm, TASKS, knobs, rt, bad, [r["throughput_gflops"] for r in recs], 16, 6, 1)
+    assert e.value.code == "invalid-config" and "record 7" in str(e.value)
