@@ -118,9 +118,10 @@ MOSES_API int moses_gradients_pooled(moses_model_t m, const double* stmt_feature
                                      const int64_t* offsets, int64_t programs, const double* labels, double* loss_out);
 /* tuner.cpp:146-147 (gradients + momentum apply_update) over host float64 statement rows, queued
  * asynchronously (pipelined: the upload of the next batch overlaps this step's kernels). Returns once
- * queued; x / offsets / y must stay valid and unchanged until the step completes, and loss_out (pinned
- * host memory or NULL) is written then — moses_model_synchronize waits for every queued step.
- * bf16 handles; capacity max_rows statement rows per step. */
+ * queued; x / offsets / y must stay valid and unchanged until the step completes. loss_out (host
+ * memory or NULL) receives the step's loss from a per-slot mailbox the step's last kernel writes: by
+ * the second following call on the handle at the latest, or by moses_model_synchronize, which waits
+ * for every queued step. bf16 handles; capacity max_rows statement rows per step. */
 MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* stmt_features, int64_t n_stmt, int32_t D,
                                             const int64_t* offsets, int64_t programs, const double* labels,
                                             double learning_rate, double momentum, double* loss_out);

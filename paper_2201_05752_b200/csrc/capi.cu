@@ -201,7 +201,7 @@ struct moses_model {
   // CUDA graph of one device-resident training step (moses_train_graph_*)
   cudaGraphExec_t train_exec = nullptr;
   long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
-  // asynchronous host-input pooled step (moses_train_step_pooled_async): two staging slots
+  // asynchronous host-input pooled step (moses_train_step_pooled_async): three staging slots
   struct AsyncSlot {
     double* x = nullptr;           // device float64 statement rows (cap x D)
     double* y = nullptr;           // device float64 labels (cap)
@@ -213,7 +213,10 @@ struct moses_model {
     cudaGraphExec_t exec = nullptr;
     long long programs = -1;
     float lr = 0.f, mu = 0.f;
-  } aslot[2];
+    double* box_host = nullptr;    // loss mailbox written by the slot's graph (mapped pinned)
+    double* box_dev = nullptr;
+    double* pending = nullptr;     // caller's loss_out for the slot's step in flight
+  } aslot[3];  // three slots: the host may run two steps ahead of the device
   cudaStream_t st_copy = nullptr;
   long long async_steps = 0;
   // epoch over a ranking-batch plan (moses_train_plan_device)
@@ -297,6 +300,7 @@ struct moses_model {
       dfree(a.off);
       dfree(a.dims);
       if (a.dims_host) cudaFreeHost(a.dims_host);
+      if (a.box_host) cudaFreeHost(a.box_host);
       if (a.ready) cudaEventDestroy(a.ready);
       if (a.free) cudaEventDestroy(a.free);
     }
@@ -403,6 +407,7 @@ struct SgdFuse {  // momentum-SGD step fused into the grouped weight-gradient ep
   long long* counter = nullptr;      // training graphs: batch index to advance with the step
   const double* loss_src = nullptr;  // plan epochs: loss to add into loss_acc with the step
   double* loss_acc = nullptr;
+  double* loss_copy = nullptr;       // async steps: per-slot loss mailbox (mapped pinned memory)
   mutable bool folded = false;       // set when the grouped wgrad kernel took the bookkeeping
 };
 
@@ -493,6 +498,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       wc.counter = fuse->counter;
       wc.loss_src = fuse->loss_src;
       wc.loss_acc = fuse->loss_acc;
+      wc.loss_copy = fuse->loss_copy;
       fuse->folded = true;
     }
     for (int l = 0; l + 1 < L; ++l) {
@@ -892,6 +898,11 @@ MOSES_API int moses_model_synchronize(moses_model_t m) {
   return guarded([&] {
     require_model(m);
     MOSES_CUDA(cudaStreamSynchronize(m->st));
+    for (auto& a : m->aslot)  // asynchronous steps: deliver the losses of the completed steps
+      if (a.pending) {
+        *a.pending = *a.box_host;
+        a.pending = nullptr;
+      }
   });
 }
 
@@ -1292,13 +1303,15 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
     check_rows(m, n_stmt);
     if (programs > m->cap) fail(MOSES_ERR_CAPACITY, "more programs than the handle capacity");
     if (!m->st_copy) MOSES_CUDA(cudaStreamCreateWithFlags(&m->st_copy, cudaStreamNonBlocking));
-    auto& a = m->aslot[m->async_steps & 1];
+    auto& a = m->aslot[m->async_steps % 3];
     if (!a.x) {
       a.x = dalloc<double>(m->cap * D);
       a.y = dalloc<double>(m->cap);
       a.off = dalloc<long long>(m->cap + 1);
       a.dims = dalloc<long long>(2);
       MOSES_CUDA(cudaMallocHost(&a.dims_host, 2 * sizeof(long long)));
+      MOSES_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a.box_host), sizeof(double), cudaHostAllocMapped));
+      MOSES_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.box_dev), a.box_host, 0));
       MOSES_CUDA(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
       MOSES_CUDA(cudaEventCreateWithFlags(&a.free, cudaEventDisableTiming));
     }
@@ -1310,7 +1323,9 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
         a.exec = nullptr;
       }
       Pool pool{m->seg_off, m->seg_rows, m->cap};
-      const SgdFuse fz{float(lr), float(mu)};
+      SgdFuse fz{float(lr), float(mu)};
+      fz.loss_src = m->dscal;
+      fz.loss_copy = a.box_dev;
       // one eager pass first (lazy workspaces must not be allocated while capturing), on an empty
       // batch: `programs` programs with no statements -> no pairs, zero gradients, no update
       MOSES_CUDA(cudaMemsetAsync(a.x, 0, sizeof(double) * m->cap * D, m->st));
@@ -1330,6 +1345,7 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
                                    m->ld[0], m->labels, m->seg_off, m->seg_rows, m->st);
         if (!gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, &fz))
           sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+        if (!fz.folded) store_scalar_f64(m->dscal, a.box_dev, m->st);
       } catch (...) {
         cudaStreamEndCapture(m->st, &graph);
         throw;
@@ -1341,8 +1357,14 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
       a.lr = float(lr);
       a.mu = float(mu);
     }
-    // the slot's previous upload must have left its pinned dims before they are overwritten
+    // the slot's previous upload must have left its pinned dims before they are overwritten, and
+    // its previous step's loss must reach the caller before the mailbox is reused
     if (a.used) MOSES_CUDA(cudaEventSynchronize(a.ready));
+    if (a.used && a.pending) {
+      MOSES_CUDA(cudaEventSynchronize(a.free));
+      *a.pending = *a.box_host;
+      a.pending = nullptr;
+    }
     a.dims_host[0] = n_stmt;
     a.dims_host[1] = programs;
     if (a.used) MOSES_CUDA(cudaStreamWaitEvent(m->st_copy, a.free, 0));  // its previous step consumed it
@@ -1355,18 +1377,7 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
     MOSES_CUDA(cudaStreamWaitEvent(m->st, a.ready, 0));
     MOSES_CUDA(cudaGraphLaunch(a.exec, m->st));
     MOSES_CUDA(cudaEventRecord(a.free, m->st));
-    if (loss_out) {
-      // pinned (mapped) destination: a one-thread kernel stores the loss over PCIe — an 8-byte D2H
-      // memcpy would queue behind the next batch's upload on the copy engines (~20 us bubble)
-      cudaPointerAttributes pa{};
-      if (cudaPointerGetAttributes(&pa, loss_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-          pa.devicePointer != nullptr) {
-        store_scalar_f64(m->dscal, static_cast<double*>(pa.devicePointer), m->st);
-      } else {
-        cudaGetLastError();
-        MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
-      }
-    }
+    a.pending = loss_out;  // copied from the slot's mailbox once its graph has run
     a.used = true;
     ++m->async_steps;
     note_launch(g_graph_kernels > 0 ? g_graph_kernels : 10);

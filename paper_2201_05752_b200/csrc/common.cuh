@@ -116,6 +116,7 @@ struct WgradGroupCall {
   long long* counter = nullptr;
   const double* loss_src = nullptr;
   double* loss_acc = nullptr;
+  double* loss_copy = nullptr;
 };
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
 extern int g_group;

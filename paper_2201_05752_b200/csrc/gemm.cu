@@ -366,6 +366,7 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   a.counter = c.counter;
   a.loss_src = c.loss_src;
   a.loss_acc = c.loss_acc;
+  a.loss_copy = c.loss_copy;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(128);

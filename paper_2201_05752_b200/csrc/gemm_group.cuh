@@ -38,6 +38,7 @@ struct GroupArgs {
   long long* counter;      // optional: step counter advanced once (training graphs' batch index)
   const double* loss_src;  // optional: *loss_acc += *loss_src once (epoch loss sum)
   double* loss_acc;
+  double* loss_copy;       // optional: *loss_copy = *loss_src once (per-step loss mailbox)
 };
 
 struct GroupCfg {
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(128, 1)
   if (blockIdx.x == 0 && threadIdx.x == 32) {  // step bookkeeping folded into the step's last kernel
     if (args.counter != nullptr) *args.counter += 1;
     if (args.loss_acc != nullptr) *args.loss_acc += *args.loss_src;
+    if (args.loss_copy != nullptr) *args.loss_copy = *args.loss_src;
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -847,9 +847,11 @@ def test_threshold_step_large_bit_exact(ml, orc, theta):
     assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
 
 
-def test_async_pooled_steps_match_synchronous(ml):
+@pytest.mark.parametrize("pinned_losses", [True, False])
+def test_async_pooled_steps_match_synchronous(ml, pinned_losses):
     """moses_train_step_pooled_async (double-buffered upload + per-slot graph) == gradients_pooled +
-    apply_update(momentum) step by step: parameters bit-identical, per-step losses equal."""
+    apply_update(momentum) step by step: parameters bit-identical, per-step losses equal (delivered
+    through the slot mailboxes into pinned or pageable host memory)."""
     import ctypes
 
     import torch
@@ -868,7 +870,9 @@ def test_async_pooled_steps_match_synchronous(ml):
     s = ml.DeviceModel(p, ml.PREC_BF16, cap)
     hyper = ml.TrainHyper(learning_rate=0.001, momentum=0.9)
     steps = [0, 1, 2, 0, 1]
-    losses = torch.zeros(len(steps), dtype=torch.float64).pin_memory()
+    losses = torch.full((len(steps),), -1.0, dtype=torch.float64)
+    if pinned_losses:
+        losses = losses.pin_memory()
     keep = []
     for k, b in enumerate(steps):
         x, off, y = batches[b]
