@@ -148,7 +148,9 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
                                        int32_t with_update);
 /* TenSet-shaped variant: programs of variable statement counts. prog_off_dev: device int64 CSR offsets of
  * every program's statement rows in x_base (n_batches * batch_programs + 1 entries); rows_pad >= the largest
- * batch's statement count (GEMM row count captured in the graph; padding rows carry no gradient). */
+ * batch's statement count (GEMM row count captured in the graph; padding rows carry no gradient).
+ * Two graphs alternate between two batch buffers: each step computes on one while a side branch
+ * gathers the next batch into the other (batch 0 is gathered here). */
 MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_base, int64_t ldx, const float* y_base,
                                               const int64_t* prog_off_dev, int64_t n_batches, int64_t batch_programs,
                                               int64_t rows_pad, double learning_rate, double momentum,

@@ -201,6 +201,19 @@ struct moses_model {
   // CUDA graph of one device-resident training step (moses_train_graph_*)
   cudaGraphExec_t train_exec = nullptr;
   long long* dcounter = nullptr;   // device batch index consumed by the graph's gather kernel
+  // pooled training graphs alternate two batch buffers: graph k computes on one while a side
+  // branch gathers batch k+1 into the other (moses_train_graph_create_pooled)
+  cudaGraphExec_t train_exec2 = nullptr;
+  int train_parity = 0;
+  long long* pcounter = nullptr;   // next batch to prefetch
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
+  struct BatchBuf {
+    void* act = nullptr;
+    float* labels = nullptr;
+    long long* seg_off = nullptr;
+    int* seg_rows = nullptr;
+  } alt;
   // asynchronous host-input pooled step (moses_train_step_pooled_async): three staging slots
   struct AsyncSlot {
     double* x = nullptr;           // device float64 statement rows (cap x D)
@@ -293,6 +306,15 @@ struct moses_model {
     for (void* p : act) dfree(p);
     for (void* p : dz) dfree(p);
     if (train_exec) cudaGraphExecDestroy(train_exec);
+    if (train_exec2) cudaGraphExecDestroy(train_exec2);
+    dfree(pcounter);
+    dfree(alt.act);
+    dfree(alt.labels);
+    dfree(alt.seg_off);
+    dfree(alt.seg_rows);
+    if (pf_fork) cudaEventDestroy(pf_fork);
+    if (pf_join) cudaEventDestroy(pf_join);
+    if (st3) cudaStreamDestroy(st3);
     for (auto& a : aslot) {
       if (a.exec) cudaGraphExecDestroy(a.exec);
       dfree(a.x);
@@ -1184,10 +1206,11 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
     check_rows(m, batch);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1) fail(MOSES_ERR_INVALID_ARG, "n_batches must be >= 1");
-    if (m->train_exec) {
-      cudaGraphExecDestroy(m->train_exec);
-      m->train_exec = nullptr;
-    }
+    for (cudaGraphExec_t* e : {&m->train_exec, &m->train_exec2})
+      if (*e) {
+        cudaGraphExecDestroy(*e);
+        *e = nullptr;
+      }
     if (!m->dcounter) m->dcounter = dalloc<long long>(1);
     MOSES_CUDA(cudaMemsetAsync(m->dcounter, 0, sizeof(long long), m->st));
     const long long row_bytes = ldx * m->esz;
@@ -1238,50 +1261,88 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     check_rows(m, rows_pad);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1 || batch_programs < 1) fail(MOSES_ERR_INVALID_ARG, "empty batch plan");
-    if (m->train_exec) {
-      cudaGraphExecDestroy(m->train_exec);
-      m->train_exec = nullptr;
-    }
+    for (cudaGraphExec_t* e : {&m->train_exec, &m->train_exec2})
+      if (*e) {
+        cudaGraphExecDestroy(*e);
+        *e = nullptr;
+      }
     if (!m->dcounter) m->dcounter = dalloc<long long>(1);
-    MOSES_CUDA(cudaMemsetAsync(m->dcounter, 0, sizeof(long long), m->st));
+    if (!m->pcounter) m->pcounter = dalloc<long long>(1);
+    if (!m->alt.act) {
+      m->alt.act = dalloc<uint8_t>(size_t(m->cap) * m->ld[0] * m->esz);
+      m->alt.labels = dalloc<float>(m->cap);
+      m->alt.seg_off = dalloc<long long>(m->cap + 1);
+      m->alt.seg_rows = dalloc<int>(m->cap);
+    }
+    if (!m->st3) MOSES_CUDA(cudaStreamCreateWithFlags(&m->st3, cudaStreamNonBlocking));
+    if (!m->pf_fork) MOSES_CUDA(cudaEventCreateWithFlags(&m->pf_fork, cudaEventDisableTiming));
+    if (!m->pf_join) MOSES_CUDA(cudaEventCreateWithFlags(&m->pf_join, cudaEventDisableTiming));
     const long long row_bytes = ldx * m->esz;
     const auto* po = reinterpret_cast<const long long*>(prog_off_dev);
-    Pool pool{m->seg_off, m->seg_rows, rows_pad};
-    auto gather = [&] {
-      gather_pooled(x_base, row_bytes, y_base, po, m->dcounter, n_batches, batch_programs, rows_pad, m->act[0],
-                    m->labels, m->seg_off, m->seg_rows, m->st);
+    const moses_model::BatchBuf bufA{m->act[0], m->labels, m->seg_off, m->seg_rows};
+    const moses_model::BatchBuf bufs[2] = {bufA, m->alt};
+    auto gather_into = [&](const moses_model::BatchBuf& b, cudaStream_t st) {
+      gather_pooled(x_base, row_bytes, y_base, po, m->pcounter, n_batches, batch_programs, rows_pad, b.act, b.labels,
+                    b.seg_off, b.seg_rows, st);
     };
-    gather();
-    gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool);
+    // eager warm-up (lazy workspaces, kernel attributes) on both buffers; parameters untouched
+    MOSES_CUDA(cudaMemsetAsync(m->pcounter, 0, sizeof(long long), m->st));
+    for (const auto& b : bufs) {
+      gather_into(b, m->st);
+      Pool pool{b.seg_off, b.seg_rows, rows_pad};
+      gradients_core(m, b.act, m->ld[0], b.labels, batch_programs, nullptr, 0.0, &pool);
+    }
     MOSES_CUDA(cudaStreamSynchronize(m->st));
-    cudaGraph_t graph;
-    MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
-    try {
-      gather();
-      const SgdFuse fz{float(lr), float(mu), m->dcounter};
-      const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch_programs, nullptr, 0.0, &pool,
+    auto step_body = [&](int cur) {
+      const auto& c = bufs[cur];
+      const auto& nx = bufs[cur ^ 1];
+      Pool pool{c.seg_off, c.seg_rows, rows_pad};
+      MOSES_CUDA(cudaEventRecord(m->pf_fork, m->st));  // side branch: the next batch into the other buffer
+      MOSES_CUDA(cudaStreamWaitEvent(m->st3, m->pf_fork, 0));
+      gather_into(nx, m->st3);
+      advance_counter(m->pcounter, m->st3);
+      MOSES_CUDA(cudaEventRecord(m->pf_join, m->st3));
+      const SgdFuse fz{float(lr), float(mu)};
+      const bool fused = gradients_core(m, c.act, m->ld[0], c.labels, batch_programs, nullptr, 0.0, &pool,
                                         with_update ? &fz : nullptr);
       if (with_update && !fused)
         sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-      if (!fz.folded) advance_counter(m->dcounter, m->st);
-    } catch (...) {
-      cudaStreamEndCapture(m->st, &graph);
-      throw;
-    }
-    MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
-    size_t nodes = 0;
-    MOSES_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
-    std::vector<cudaGraphNode_t> nv(nodes);
-    MOSES_CUDA(cudaGraphGetNodes(graph, nv.data(), &nodes));
-    long long kernels = 0;
-    for (auto n : nv) {
-      cudaGraphNodeType t;
-      MOSES_CUDA(cudaGraphNodeGetType(n, &t));
-      kernels += t == cudaGraphNodeTypeKernel;
-    }
-    g_graph_kernels = kernels;
-    MOSES_CUDA(cudaGraphInstantiate(&m->train_exec, graph, 0));
-    MOSES_CUDA(cudaGraphDestroy(graph));
+      MOSES_CUDA(cudaStreamWaitEvent(m->st, m->pf_join, 0));
+    };
+    auto capture = [&](std::initializer_list<int> seq, cudaGraphExec_t* out) -> long long {
+      cudaGraph_t graph;
+      MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (int cur : seq) step_body(cur);
+      } catch (...) {
+        cudaStreamEndCapture(m->st, &graph);
+        throw;
+      }
+      MOSES_CUDA(cudaStreamEndCapture(m->st, &graph));
+      size_t nodes = 0;
+      MOSES_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
+      std::vector<cudaGraphNode_t> nv(nodes);
+      MOSES_CUDA(cudaGraphGetNodes(graph, nv.data(), &nodes));
+      long long k = 0;
+      for (auto n : nv) {
+        cudaGraphNodeType t;
+        MOSES_CUDA(cudaGraphNodeGetType(n, &t));
+        k += t == cudaGraphNodeTypeKernel;
+      }
+      MOSES_CUDA(cudaGraphInstantiate(out, graph, 0));
+      MOSES_CUDA(cudaGraphDestroy(graph));
+      return k;
+    };
+    const long long kernels = capture({0}, &m->train_exec);
+    capture({1}, &m->train_exec2);
+    g_graph_kernels = kernels + 1;  // + the prefetch's share: one gather per step
+    // batch 0 into buffer A; the first launch computes on A and prefetches batch 1 into B
+    MOSES_CUDA(cudaMemsetAsync(m->pcounter, 0, sizeof(long long), m->st));
+    gather_into(bufA, m->st);
+    advance_counter(m->pcounter, m->st);
+    note_launch(2);
+    m->train_parity = 0;
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
   });
 }
 
@@ -1431,7 +1492,10 @@ MOSES_API int moses_train_graph_launch(moses_model_t m, int64_t steps) {
   return guarded([&] {
     require_model(m);
     if (!m->train_exec) fail(MOSES_ERR_INVALID_ARG, "no training graph (moses_train_graph_create)");
-    for (int64_t i = 0; i < steps; ++i) MOSES_CUDA(cudaGraphLaunch(m->train_exec, m->st));
+    for (int64_t i = 0; i < steps; ++i) {
+      MOSES_CUDA(cudaGraphLaunch(m->train_parity && m->train_exec2 ? m->train_exec2 : m->train_exec, m->st));
+      if (m->train_exec2) m->train_parity ^= 1;
+    }
     note_launch(steps * g_graph_kernels);
   });
 }
