@@ -273,17 +273,17 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
     const uint32_t t_row = tmem + ((warp * 32u) << 16);
     for (int l = 0; l < L; ++l) {
       const bool last = l + 1 == L;
-      uint4 mk[4];  // DGRAD: relu' source of the first 32-column chunk
-      auto load_mask = [&](int c) {
-        if constexpr (!FWD) {
-          if (row_ok) {
-            const uint4* src = reinterpret_cast<const uint4*>(args.mask[l] + (long long)m * args.ldm[l] + n0 + c * 32);
+      uint4 mk[BN / 32][4];  // DGRAD: relu' source of all four 32-column chunks, loaded before the
+                             // accumulator wait so the L2 latency hides behind the layer's MMAs
+      if constexpr (!FWD) {
+        if (row_ok) {
+          const uint4* src = reinterpret_cast<const uint4*>(args.mask[l] + (long long)m * args.ldm[l] + n0);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) mk[v] = __ldg(src + v);
-          }
+          for (int c = 0; c < BN / 32; ++c)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) mk[c][v] = __ldg(src + c * 4 + v);
         }
-      };
-      load_mask(0);
+      }
       ptx::mbar_wait(acc_full, uint32_t(l) & 1u);
       ptx::tc_fence_after();
       if (threadIdx.x == 0) CHAIN_TRACE(2, l);
@@ -314,10 +314,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
             }
           }
         } else {
-          const __nv_bfloat16* mv = reinterpret_cast<const __nv_bfloat16*>(mk);
+          uint4 cur[4];
+#pragma unroll
+          for (int cc = 0; cc < BN / 32; ++cc)  // static register indexing of the chunk
+            if (cc == c)
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) cur[q4] = mk[cc][q4];
+          const __nv_bfloat16* mv = reinterpret_cast<const __nv_bfloat16*>(cur);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(mv[j]) > 0.f ? v[j] : 0.f;
-          if (c + 1 < BN / 32) load_mask(c + 1);
         }
         if (store) {
 #pragma unroll
