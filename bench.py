@@ -396,6 +396,22 @@ def bench_finetune(ml, L, peaks, reps=20):
                          "params": len(params.params),
                          "path": "moses_gradients(adv, beta=0.01) + moses_adversarial_step + moses_lottery_step "
                                  "(ratio 0.5), host float64 buffers, wall clock"}
+
+    def fused_step():
+        ml._ck(L.moses_moses_step(dm.h, adv.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], 0.01, 2, 0.5, 0, 1e-3,
+                                  1e-2, C.byref(loss), C.byref(dl), C.byref(pop)))
+
+    for _ in range(3):
+        fused_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fused_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    out["moses_step_fused"] = {"ms": dt * 1e3, "samples_per_s": BATCH / dt,
+                               "path": "moses_moses_step: the same three steps in one C-ABI call (the discriminator "
+                                       "step reuses the gradients' forward; one host sync), bit-identical"}
     # the lottery step alone at the real parameter count (L2-resident: launch/latency bound)
     sp = C.c_void_p()
     L.moses_model_stream(dm.h, C.byref(sp))

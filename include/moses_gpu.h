@@ -208,6 +208,14 @@ MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hidden_s
 MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const double* target_features,
                                      int64_t n, int32_t D, double beta, double* discriminator_loss,
                                      double* confusion);
+/* The Moses branch of a tuning step (tuner.cpp:251-262) in one call: moses_gradients(adv, beta) ->
+ * moses_adversarial_step -> moses_lottery_step(mode, value, phase, alpha, lambda), bit-identical to
+ * the three calls, with one host synchronisation; the discriminator step reuses the gradients'
+ * forward pass over the same replay + batch rows. loss_out: the gradients' loss; dloss_out: the
+ * discriminator loss before its step; popcount: transferable scalars. */
+MOSES_API int moses_moses_step(moses_model_t m, moses_adversary_t adv, const double* features, const double* labels,
+                              int64_t n, int32_t D, double beta, int32_t mode, double value, int32_t phase,
+                              double alpha, double lambda, double* loss_out, double* dloss_out, int64_t* popcount);
 /* discriminator_cross_entropy (lottery.cpp:207-218) */
 MOSES_API int moses_discriminator_cross_entropy(const double* zs, int64_t m, const double* zt, int64_t n,
                                                 double* out);

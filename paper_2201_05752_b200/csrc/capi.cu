@@ -1866,6 +1866,44 @@ MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const
   });
 }
 
+// The Moses branch of a tuning step (tuner.cpp:251-262) in one call: gradients with the
+// adversary term -> discriminator step -> lottery step, with one host synchronisation. The
+// discriminator step reuses the forward pass the gradients just ran on the same rows (replay
+// [0, m), batch [m, m+n), discriminator logits in the same epilogue) — moses_adversarial_step
+// would re-upload and recompute exactly these values, since the model has not changed in between.
+MOSES_API int moses_moses_step(moses_model_t m, moses_adversary_t a, const double* x, const double* y, int64_t n,
+                              int32_t D, double beta, int32_t mode, double value, int32_t phase, double alpha,
+                              double lambda, double* loss_out, double* dloss_out, int64_t* popcount) {
+  (void)phase;
+  return guarded([&] {
+    require_model(m);
+    if (!a) fail(MOSES_ERR_ADVERSARY_DISABLED, "null adversary");
+    if (a->m == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "adversary has an empty replay buffer");
+    if (n == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "empty activation batch");
+    if (a->W != m->W()) fail(MOSES_ERR_DIM_MISMATCH, "activation width != discriminator width");
+    gradients_host(m, x, y, n, D, a, beta);
+    if (beta == 0.0) {  // the gradients ran without the adversary rows: forward them for the discriminator
+      upload_replay(m, a);
+      upload_rows(m, x, n, a->m);
+      dispatch_forward(m, m->act[0], m->ld[0], a->m + n, a->u, true);
+      note_launch(1);
+    }
+    if (m->esz == 2)
+      adversary_step<__nv_bfloat16>(m->head_part2, m->last_tiles, m->cap, static_cast<__nv_bfloat16*>(m->act[m->L - 1]),
+                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+    else
+      adversary_step<float>(m->head_part2, m->last_tiles, m->cap, static_cast<float*>(m->act[m->L - 1]),
+                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+    note_launch(2);
+    double sc[3] = {0, 0, 0};
+    MOSES_CUDA(cudaMemcpyAsync(sc, m->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    lottery_step_impl(m, mode, value, alpha, lambda, nullptr, 0, popcount, nullptr);
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+    if (loss_out) *loss_out = sc[0];
+    if (dloss_out) *dloss_out = sc[2];
+  });
+}
+
 MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hs, int64_t ms, const double* ht, int64_t nt,
                                      int32_t width, double beta, double* dloss, double* conf) {
   return guarded([&] {

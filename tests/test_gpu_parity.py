@@ -955,3 +955,41 @@ def test_rank_step_grid_matches_cluster(ml, kind, n, prec):
     assert np.array_equal(g1[mask], g0[mask])
     assert abs(g1[hb] - g0[hb]) <= 1e-6 * max(1e-6, abs(g0[hb]))
     assert abs(l1 - l0) <= 1e-12 * max(1.0, abs(l0))
+
+
+@pytest.mark.parametrize("beta", [0.01, 0.0])
+@pytest.mark.parametrize("mode,value", [(2, 0.5), (1, 0.5)])
+def test_moses_step_fused_equals_three_calls(ml, beta, mode, value):
+    """moses_moses_step == moses_gradients(adv) + moses_adversarial_step + moses_lottery_step, bit for
+    bit: parameters, discriminator weights, losses and popcount over three consecutive steps."""
+    import ctypes as C
+
+    dims = [164, 512, 512, 512, 512, 1]
+    p = ml.init_random(dims, 31, strict=False)
+    rng = np.random.default_rng(5)
+    replay = rng.random((256, dims[0]))
+    L = ml.lib()
+    out = []
+    for fused in (True, False):
+        dm = ml.DeviceModel(p, ml.PREC_BF16, 1024)
+        adv = ml.AdversaryState(replay, dims[-2])
+        rec = []
+        for k in range(3):
+            x = np.ascontiguousarray(np.random.default_rng(100 + k).random((512, dims[0])))
+            y = np.ascontiguousarray(0.1 + np.random.default_rng(200 + k).random(512))
+            loss, dl, cf, pop = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+            if fused:
+                ml._ck(L.moses_moses_step(dm.h, adv.h, x.ctypes.data, y.ctypes.data, 512, dims[0], beta, mode, value, 0,
+                                          1e-3, 1e-2, C.byref(loss), C.byref(dl), C.byref(pop)))
+            else:
+                ml._ck(L.moses_gradients(dm.h, x.ctypes.data, y.ctypes.data, 512, dims[0], adv.h, beta, C.byref(loss)))
+                ml._ck(L.moses_adversarial_step(adv.h, dm.h, x.ctypes.data, 512, dims[0], beta, C.byref(dl),
+                                                C.byref(cf)))
+                ml._ck(L.moses_lottery_step(dm.h, mode, value, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
+            rec.append((loss.value, dl.value, pop.value))
+        out.append((rec, dm.download().params, adv.weight, adv.bias))
+        del adv
+        dm.close()
+    (r1, w1, u1, c1), (r0, w0, u0, c0) = out
+    assert r1 == r0
+    assert np.array_equal(w1, w0) and np.array_equal(u1, u0) and c1 == c0
