@@ -526,6 +526,35 @@ def bench_search(ml, L, peaks):
     best, best_lat = ml.true_best(server, task, knobs)
     tb_ms = (time.perf_counter() - t0) * 1e3
     del lab
+    # evolve (search.cpp:41-71) with the reference SearchParams (128 / 4 generations / 32 survivors x
+    # 4 mutants) on the default knob template, scored by the {16,512,512,1} model on the device
+    dknobs = [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
+              ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
+    em = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16, 1024)
+    ml.evolve(em, task, dknobs, seed=1)
+    t0 = time.perf_counter()
+    for r in range(10):
+        ml.evolve(em, task, dknobs, seed=r)
+    evolve_ms = (time.perf_counter() - t0) / 10 * 1e3
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+
+    wts = orc.init_random(dims, SEED_MODEL)
+    sizes = [len(d) for _, d in dknobs]
+
+    def cpu_scorer(cfgs):
+        rows = []
+        for c in cfgs:
+            i = 0
+            for k, x in enumerate(c):
+                i = i * sizes[k] + dknobs[k][1].index(x)
+            rows.append(orc.encode_configs(task, dknobs, i, 1)[0][0])
+        return list(orc.forward(dims, wts, np.stack(rows))[0])
+
+    t0 = time.perf_counter()
+    orc.evolve(dknobs, cpu_scorer, seed=1)
+    evolve_cpu_ms = (time.perf_counter() - t0) * 1e3
+    em.close()
     out = {"configs": n, "knobs": len(knobs), "model": dims, "encode_ms": enc_ms,
            "encode_roofline": {"bound": "hbm", "achieved": wbytes / (enc_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                "frac": wbytes / (enc_ms / 1e3) / 1e9 / hbm,
@@ -534,7 +563,11 @@ def bench_search(ml, L, peaks):
            "labels_ms": label_ms, "labels_per_s": n / (label_ms / 1e3),
            "true_best": {"values": best, "latency_ms": best_lat, "ms": tb_ms,
                          "note": "exhaustive noise-free optimum over the 10.2M-config space (oracle.cpp:90-105)"},
-           "pipeline": "encode_configs (device) -> predict (tcgen05) -> top-1024, wall clock"}
+           "pipeline": "encode_configs (device) -> predict (tcgen05) -> top-1024, wall clock",
+           "evolve": {"ms": evolve_ms, "cpu_oracle_ms": evolve_cpu_ms,
+                      "params": "population 128, 4 generations, 32 survivors x 4 mutants, eps 0.05 (SearchParams)",
+                      "path": "moses_evolve: device encode from enumeration indices + tcgen05 scoring per "
+                              "generation; host RngStream walk and sort; CPU: fp64 oracle forward, 1 thread"}}
     del F, Hh, S
     torch.cuda.empty_cache()
     return out

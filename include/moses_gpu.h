@@ -39,6 +39,7 @@ enum {
   MOSES_ERR_INVALID_TASK = 1,          /* ErrorCode::InvalidTask */
   MOSES_ERR_INVALID_CONFIG = 2,        /* ErrorCode::InvalidConfig */
   MOSES_ERR_SPACE_TOO_LARGE = 3,       /* ErrorCode::SpaceTooLarge */
+  MOSES_ERR_IMMUTABLE_SPACE = 4,       /* ErrorCode::ImmutableSpace */
   MOSES_ERR_BAD_DIMS = 5,              /* ErrorCode::BadDims */
   MOSES_ERR_DIM_MISMATCH = 6,          /* ErrorCode::DimMismatch */
   MOSES_ERR_SHAPE_MISMATCH = 7,        /* ErrorCode::ShapeMismatch */
@@ -208,6 +209,16 @@ MOSES_API int moses_adversarial_term(moses_adversary_t a, const double* hidden_s
 MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const double* target_features,
                                      int64_t n, int32_t D, double beta, double* discriminator_loss,
                                      double* confusion);
+/* evolve (search.cpp:41-71) with the model scorer on the device: per generation the candidates are
+ * encoded on the device from their enumeration indices and scored there; the GA's RngStream walk
+ * (sample_config / mutate_config, KeyBuilder(seed, "evolve")) and the (score desc, config asc) sort
+ * run on the host. SearchParams: population, generations, mutation_count, survivors, epsilon_random,
+ * seed. Outputs (host): values_out (capacity x n_knobs), scores_out (capacity), n_out = final
+ * population. m == NULL: linear test scorer sum_k lin_w[k] * value_k (double) instead of a model. */
+MOSES_API int moses_evolve(moses_model_t m, const double* lin_w, const double* task4, const int64_t* domains,
+                          const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs, int32_t population,
+                          int32_t generations, int32_t mutation_count, int32_t survivors, double epsilon_random,
+                          uint64_t seed, int64_t* values_out, double* scores_out, int64_t capacity, int64_t* n_out);
 /* The Moses branch of a tuning step (tuner.cpp:251-262) in one call: moses_gradients(adv, beta) ->
  * moses_adversarial_step -> moses_lottery_step(mode, value, phase, alpha, lambda), bit-identical to
  * the three calls, with one host synchronisation; the discriminator step reuses the gradients'

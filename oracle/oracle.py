@@ -496,6 +496,9 @@ class RngStream:
             if r >= t:
                 return r % n
 
+    def uniform01(self) -> float:
+        return (self.next_u64() >> 11) * 2.0 ** -53
+
 
 def _shuffle_with(items, rng):  # data.cpp:16-22
     for i in range(len(items), 1, -1):
@@ -572,3 +575,49 @@ def pretrain_epoch(dims, w, mom, features, labels, batches, lr, mu=0.9, threads=
     for x in losses:  # loss_sum += loss (tuner.cpp:148-150); Python's sum() would compensate
         acc += x
     return w, mom, (acc / len(losses) if losses else 0.0)
+
+
+# ---------------------------------------------------------------- evolve (search.cpp:11-71)
+def evolve(knobs, scorer, population=128, generations=4, mutation_count=4, survivors=32, epsilon_random=0.05,
+           seed=0):
+    """Pure-Python restatement of the GA: scorer(list of value lists) -> list of float scores.
+    Returns [(values, score)] sorted by score desc then values asc (search.cpp:32-37)."""
+    if population < 1 or mutation_count < 1 or survivors < 1:
+        raise OracleError(2, "population, mutation_count and survivors must be positive")
+    if generations < 0:
+        raise OracleError(2, "generations must be non-negative")
+    if survivors > population:
+        raise OracleError(2, "survivors cannot exceed the population")
+    if not (0.0 <= epsilon_random <= 1.0):
+        raise OracleError(2, "epsilon_random must lie in [0,1]")
+    rng = RngStream(key_builder(seed, "evolve"))
+    doms = [list(d) for _, d in knobs]
+
+    def sample():  # space.cpp:94-100
+        return [d[rng.below(len(d))] for d in doms]
+
+    def mutate(cfg):  # space.cpp:102-121
+        mut = [k for k, d in enumerate(doms) if len(d) > 1]
+        if not mut:
+            raise OracleError(4, "every knob domain is a singleton")
+        ki = mut[rng.below(len(mut))]
+        old = doms[ki].index(cfg[ki])
+        pick = rng.below(len(doms[ki]) - 1)
+        if pick >= old:
+            pick += 1
+        out = list(cfg)
+        out[ki] = doms[ki][pick]
+        return out
+
+    def score_all(cfgs):
+        return sorted(zip(cfgs, scorer(cfgs)), key=lambda cs: (-cs[1], cs[0]))
+
+    pop = score_all([sample() for _ in range(population)])
+    for _ in range(generations):
+        keep = min(survivors, len(pop))
+        nxt = [list(pop[s][0]) for s in range(keep)]
+        for s in range(keep):
+            for _ in range(mutation_count):
+                nxt.append(sample() if rng.uniform01() < epsilon_random else mutate(pop[s][0]))
+        pop = score_all(nxt)
+    return pop

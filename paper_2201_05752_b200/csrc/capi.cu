@@ -1866,6 +1866,204 @@ MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const
   });
 }
 
+// evolve (search.cpp:41-71, SearchParams search.hpp:13-20) with the scorer on the device: every
+// generation's configurations are encoded on the device straight into packed model rows (from
+// their enumeration indices) and scored by the model there; the GA's own RngStream walk
+// (sample_config / mutate_config / epsilon draws, space.cpp:94-121) and the sort of <= a few
+// hundred candidates by (score desc, configuration asc) stay on the host — both are sequential
+// by definition. Configurations compare lexicographically by value, which for sorted domains is
+// the order of their mixed-radix enumeration index. m == NULL scores with the linear test scorer
+// sum_k lin_w[k] * value_k (host, double) instead of the model.
+namespace {
+struct EvolveSpace {
+  int nk;
+  std::vector<long long> dom;
+  std::vector<int> size, off;
+  unsigned long long idx_of(const std::vector<int>& dg) const {
+    unsigned long long id = 0;
+    for (int k = 0; k < nk; ++k) id = id * (unsigned long long)size[k] + (unsigned long long)dg[k];
+    return id;
+  }
+  std::vector<int> digits(unsigned long long id) const {
+    std::vector<int> dg(static_cast<size_t>(nk));
+    for (int k = nk - 1; k >= 0; --k) {
+      dg[size_t(k)] = int(id % (unsigned long long)size[k]);
+      id /= (unsigned long long)size[k];
+    }
+    return dg;
+  }
+};
+struct GaRng {  // RngStream (rng.hpp)
+  unsigned long long s;
+  unsigned long long next() {
+    s += 0x9e3779b97f4a7c15ull;
+    unsigned long long z = s;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  unsigned long long below(unsigned long long n) {
+    const unsigned long long t = (0ull - n) % n;
+    for (;;) {
+      const unsigned long long r = next();
+      if (r >= t) return r % n;
+    }
+  }
+  double uniform01() { return double(next() >> 11) * 0x1.0p-53; }
+};
+}  // namespace
+
+MOSES_API int moses_evolve(moses_model_t m, const double* lin_w, const double* task4, const int64_t* domains,
+                          const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs, int32_t population,
+                          int32_t generations, int32_t mutation_count, int32_t survivors, double epsilon_random,
+                          uint64_t seed, int64_t* values_out, double* scores_out, int64_t capacity, int64_t* n_out) {
+  return guarded([&] {
+    // check_params (search.cpp:11-19)
+    if (population < 1 || mutation_count < 1 || survivors < 1)
+      fail(MOSES_ERR_INVALID_CONFIG, "population, mutation_count and survivors must be positive");
+    if (generations < 0) fail(MOSES_ERR_INVALID_CONFIG, "generations must be non-negative");
+    if (survivors > population) fail(MOSES_ERR_INVALID_CONFIG, "survivors cannot exceed the population");
+    if (!(epsilon_random >= 0.0 && epsilon_random <= 1.0))
+      fail(MOSES_ERR_INVALID_CONFIG, "epsilon_random must lie in [0,1]");
+    if (m == nullptr && lin_w == nullptr) fail(MOSES_ERR_INVALID_ARG, "no scorer");
+    if (m != nullptr && m->dims[0] < 10) fail(MOSES_ERR_DIM_MISMATCH, "model input width below the feature width");
+    // build_space / validate_task (space.cpp:41-92)
+    if (n_knobs <= 0 || n_knobs > 8) fail(MOSES_ERR_INVALID_ARG, "knob count must lie in [1, 8]");
+    EvolveSpace sp;
+    sp.nk = n_knobs;
+    int off = 0;
+    unsigned long long space = 1;
+    for (int k = 0; k < n_knobs; ++k) {
+      if (domain_sizes[k] <= 0) fail(MOSES_ERR_INVALID_TASK, "knob domain must be non-empty");
+      for (int j = 1; j < domain_sizes[k]; ++j)
+        if (domains[off + j - 1] >= domains[off + j]) fail(MOSES_ERR_INVALID_TASK, "knob domain must be strictly increasing");
+      if (space > ~0ull / (unsigned long long)domain_sizes[k]) fail(MOSES_ERR_SPACE_TOO_LARGE, "knob space overflows 64 bits");
+      space *= (unsigned long long)domain_sizes[k];
+      sp.size.push_back(domain_sizes[k]);
+      sp.off.push_back(off);
+      off += domain_sizes[k];
+    }
+    sp.dom.assign(domains, domains + off);
+    std::vector<int> mutable_knobs;
+    for (int k = 0; k < n_knobs; ++k)
+      if (sp.size[size_t(k)] > 1) mutable_knobs.push_back(k);
+
+    GaRng rng{0xcbf29ce484222325ull};
+    {  // KeyBuilder(seed, "evolve")
+      auto step = [&](unsigned char b) {
+        rng.s ^= b;
+        rng.s *= 0x100000001b3ull;
+      };
+      for (int i = 0; i < 8; ++i) step((unsigned char)(seed >> (8 * i)));
+      for (const char* c = "evolve"; *c; ++c) step((unsigned char)*c);
+      step(0);
+    }
+    auto sample = [&] {  // sample_config (space.cpp:94-100)
+      std::vector<int> dg(static_cast<size_t>(n_knobs));
+      for (int k = 0; k < n_knobs; ++k) dg[size_t(k)] = int(rng.below((unsigned long long)sp.size[size_t(k)]));
+      return sp.idx_of(dg);
+    };
+    auto mutate = [&](unsigned long long id) {  // mutate_config (space.cpp:102-121)
+      if (mutable_knobs.empty()) fail(MOSES_ERR_IMMUTABLE_SPACE, "every knob domain is a singleton");
+      std::vector<int> dg = sp.digits(id);
+      const int ki = mutable_knobs[size_t(rng.below(mutable_knobs.size()))];
+      const int old_pos = dg[size_t(ki)];
+      int pick = int(rng.below((unsigned long long)(sp.size[size_t(ki)] - 1)));
+      if (pick >= old_pos) ++pick;
+      dg[size_t(ki)] = pick;
+      return sp.idx_of(dg);
+    };
+    // scoring: device encode (from indices) + predict, or the linear test scorer
+    unsigned long long* didx = nullptr;
+    void* feat = nullptr;
+    float* dsc = nullptr;
+    const long long maxn = std::max<long long>(population, (long long)survivors * (1 + mutation_count));
+    cudaStream_t st = m ? m->st : nullptr;
+    auto release = [&] {
+      if (st) cudaStreamSynchronize(st);
+      dfree(didx);
+      dfree(feat);
+      dfree(dsc);
+    };
+    struct Cand {
+      unsigned long long idx;
+      double score;
+    };
+    auto score_all = [&](const std::vector<unsigned long long>& ids) {
+      std::vector<Cand> pop(ids.size());
+      if (m == nullptr) {
+        for (size_t i = 0; i < ids.size(); ++i) {
+          const std::vector<int> dg = sp.digits(ids[i]);
+          double sc = 0.0;
+          for (int k = 0; k < n_knobs; ++k) sc = sc + lin_w[k] * double(sp.dom[size_t(sp.off[size_t(k)] + dg[size_t(k)])]);
+          pop[i] = {ids[i], sc};
+        }
+        return pop;
+      }
+      const long long n = (long long)ids.size();
+      MOSES_CUDA(cudaMemcpyAsync(didx, ids.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, st));
+      note_launch(encode_configs_idx(task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs,
+                                     didx, n, m->esz == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32, feat, m->ld[0],
+                                     m->dims[0], st));
+      for (long long r = 0; r < n;) {
+        const long long c = std::min(n - r, m->cap);
+        dispatch_forward(m, static_cast<uint8_t*>(feat) + r * m->ld[0] * m->esz, m->ld[0], c, nullptr, false);
+        head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, dsc + r, st);
+        note_launch(1);
+        r += c;
+      }
+      std::vector<float> hs(static_cast<size_t>(n));
+      MOSES_CUDA(cudaMemcpyAsync(hs.data(), dsc, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+      MOSES_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < ids.size(); ++i) pop[i] = {ids[i], double(hs[i])};
+      return pop;
+    };
+    auto sort_desc = [](std::vector<Cand>& pop) {  // search.cpp:32-37
+      std::sort(pop.begin(), pop.end(), [](const Cand& a, const Cand& b) {
+        if (a.score != b.score) return a.score > b.score;
+        return a.idx < b.idx;
+      });
+    };
+    std::vector<Cand> pop;
+    try {
+      if (m) {
+        if (m->split) fail(MOSES_ERR_INVALID_ARG, "evolve scores through device rows: bf16 or tf32 handles");
+        didx = dalloc<unsigned long long>(size_t(maxn));
+        feat = dalloc<uint8_t>(size_t(maxn) * m->ld[0] * m->esz);
+        dsc = dalloc<float>(size_t(maxn));
+      }
+      std::vector<unsigned long long> ids;
+      ids.reserve(size_t(population));
+      for (int i = 0; i < population; ++i) ids.push_back(sample());
+      pop = score_all(ids);
+      sort_desc(pop);
+      for (int gen = 0; gen < generations; ++gen) {
+        const size_t keep = std::min<size_t>(size_t(survivors), pop.size());
+        std::vector<unsigned long long> next;
+        next.reserve(keep * size_t(1 + mutation_count));
+        for (size_t s2 = 0; s2 < keep; ++s2) next.push_back(pop[s2].idx);
+        for (size_t s2 = 0; s2 < keep; ++s2)
+          for (int k = 0; k < mutation_count; ++k)
+            next.push_back(rng.uniform01() < epsilon_random ? sample() : mutate(pop[s2].idx));
+        pop = score_all(next);
+        sort_desc(pop);
+      }
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+    if ((long long)pop.size() > capacity) fail(MOSES_ERR_CAPACITY, "output capacity below the final population");
+    for (size_t i = 0; i < pop.size(); ++i) {
+      const std::vector<int> dg = sp.digits(pop[i].idx);
+      for (int k = 0; k < n_knobs; ++k)
+        if (values_out) values_out[i * n_knobs + k] = sp.dom[size_t(sp.off[size_t(k)] + dg[size_t(k)])];
+      if (scores_out) scores_out[i] = pop[i].score;
+    }
+    if (n_out) *n_out = (int64_t)pop.size();
+  });
+}
+
 // The Moses branch of a tuning step (tuner.cpp:251-262) in one call: gradients with the
 // adversary term -> discriminator step -> lottery step, with one host synchronisation. The
 // discriminator step reuses the forward pass the gradients just ran on the same rows (replay

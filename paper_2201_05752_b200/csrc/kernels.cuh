@@ -185,6 +185,10 @@ int true_best(const double* dev6, const double* task4, const long long* domains,
 int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
                    unsigned long long first, long long n, int out_kind, void* feat, long long ld, int D,
                    unsigned long long* hash, long long* values_out, cudaStream_t st);
+// feature rows of configurations given by enumeration index (device list)
+int encode_configs_idx(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                       const unsigned long long* idx_dev, long long n, int out_kind, void* feat, long long ld, int D,
+                       cudaStream_t st);
 // generate_dataset for one task (data.cpp:49-65): keyed sample_config draws, features, measure() labels
 int generate_task_dataset(const double* dev6, int repeats, const char* device_id, const char* task_id,
                           const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,

@@ -252,6 +252,11 @@ int encode_configs(const double* task4, const long long* domains, const int* siz
                    unsigned long long* hash, long long* values_out, cudaStream_t st) {
   return encode_impl(task4, domains, sizes, roles, nk, first, nullptr, n, out_kind, feat, ld, D, hash, values_out, st);
 }
+int encode_configs_idx(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                       const unsigned long long* idx_dev, long long n, int out_kind, void* feat, long long ld, int D,
+                       cudaStream_t st) {
+  return encode_impl(task4, domains, sizes, roles, nk, 0, idx_dev, n, out_kind, feat, ld, D, nullptr, nullptr, st);
+}
 
 // ---------------------------------------------------------------- simulated hardware (oracle.cpp:33-105)
 // The label generator of the synthetic TenSet-style data: the closed-form

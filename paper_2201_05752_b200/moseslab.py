@@ -140,6 +140,7 @@ def lib():
         "moses_pretrain_jobs": (C.c_int, [i32, vp, vp, vp, i64, vp, vp, i64, vp, i32, i32, i32, dbl, dbl, i32, vp, vp]),
         "moses_pretrain": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_moses_step": (C.c_int, [vp, vp, vp, vp, i64, i32, dbl, i32, dbl, i32, dbl, dbl, vp, vp, vp]),
+        "moses_evolve": (C.c_int, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, dbl, u64, vp, vp, i64, vp]),
         "moses_records_create": (C.c_int, [vp]),
         "moses_records_read": (C.c_int, [C.c_char_p, vp]),
         "moses_records_destroy": (None, [vp]),
@@ -894,6 +895,23 @@ def pretrain_device(model, x_ptr, ldx: int, y_ptr, record_task, task_ids, batch_
     _ck(lib().moses_pretrain_device(model.h, x_ptr, ldx, y_ptr, _p(rt), len(rt), C.cast(arr, C.c_void_p), len(enc),
                                     batch_size, seed, epochs, lr, mu, _p(losses), C.byref(dropped)))
     return losses[:epochs].tolist(), dropped.value
+
+
+def evolve(model, task, knobs, population: int = 128, generations: int = 4, mutation_count: int = 4,
+           survivors: int = 32, epsilon_random: float = 0.05, seed: int = 0, lin_w=None):
+    """evolve (search.cpp:41-71) with device encoding + scoring by `model` (or, model=None, the linear
+    test scorer sum_k lin_w[k] * value_k). Returns (values [n x n_knobs], scores [n]) sorted by
+    score desc then configuration asc."""
+    dom, sizes, roles = _space_arrays(knobs)
+    cap = max(population, survivors * (1 + mutation_count))
+    vals = np.zeros((cap, len(knobs)), dtype=np.int64)
+    scores = np.zeros(cap)
+    n = C.c_int64()
+    lw = None if lin_w is None else np.ascontiguousarray(lin_w, dtype=np.float64)
+    _ck(lib().moses_evolve(model.h if model is not None else None, _p(lw), _p(_task4(task)), _p(dom), _p(sizes),
+                           _p(roles), len(knobs), population, generations, mutation_count, survivors, epsilon_random,
+                           seed, _p(vals), _p(scores), cap, C.byref(n)))
+    return vals[:n.value], scores[:n.value]
 
 
 def pretrain(model, tasks, knobs, record_task, values, throughput, batch_size: int = 512, seed: int = 0,
