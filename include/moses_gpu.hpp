@@ -504,4 +504,35 @@ inline CostModelParams pretrain(const RecordStore& store, const std::vector<Task
   return m.download();
 }
 
+// ---- search.hpp: evolve with the model scorer on the device (search.cpp:41-71, 120-127)
+struct SearchParams {  // search.hpp:13-20
+  int population = 128;
+  int generations = 4;
+  int mutation_count = 4;
+  int survivors = 32;
+  double epsilon_random = 0.05;
+  uint64_t seed = 0;
+};
+struct ScoredCandidate {  // search.hpp:22-25
+  Configuration config;
+  double score = 0.0;
+};
+inline std::vector<ScoredCandidate> evolve(DeviceModel& model, const TaskSpec& task, const SearchParams& p) {
+  const detail::SpaceArrays a(task);
+  const size_t nk = task.knobs.size();
+  const int64_t cap = std::max<int64_t>(p.population, int64_t(p.survivors) * (1 + p.mutation_count));
+  std::vector<int64_t> vals(size_t(std::max<int64_t>(cap, 1)) * nk);
+  std::vector<double> sc(size_t(std::max<int64_t>(cap, 1)));
+  int64_t n = 0;
+  check(moses_evolve(model.handle(), nullptr, a.task4, a.domains.data(), a.sizes.data(), a.roles.data(), int32_t(nk),
+                     p.population, p.generations, p.mutation_count, p.survivors, p.epsilon_random, p.seed,
+                     vals.data(), sc.data(), cap, &n));
+  std::vector<ScoredCandidate> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    out[size_t(i)].config.values.assign(vals.begin() + i * int64_t(nk), vals.begin() + (i + 1) * int64_t(nk));
+    out[size_t(i)].score = sc[size_t(i)];
+  }
+  return out;
+}
+
 }  // namespace moseslab_gpu

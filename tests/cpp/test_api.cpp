@@ -193,6 +193,23 @@ int main() {
     expect_error(ErrorCode::InvalidConfig, [&] { pretrain(bad, {ta, tb}, h); });
     expect_error(ErrorCode::EmptyDataset, [&] { pretrain(RecordStore{}, {ta, tb}, h); });
   }
+  // test_search.cpp:82-120: evolve's result is sorted by score then config, of the refilled size
+  {
+    TaskSpec t{"conv3x3_64", 2.0, 8.0, 9.0, 5.0, default_knob_template()};
+    DeviceModel m(init_random({16, 512, 512, 1}, 3), MOSES_PREC_BF16, 1024);
+    SearchParams sp;
+    sp.seed = 4;
+    const auto pop = evolve(m, t, sp);
+    CHECK(pop.size() == 160);
+    bool sorted = true;
+    for (size_t i = 1; i < pop.size(); ++i)
+      sorted = sorted && (pop[i - 1].score > pop[i].score ||
+                          (pop[i - 1].score == pop[i].score && pop[i - 1].config.values <= pop[i].config.values));
+    CHECK(sorted);
+    SearchParams bad = sp;
+    bad.survivors = 500;
+    expect_error(ErrorCode::InvalidConfig, [&] { evolve(m, t, bad); });
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
