@@ -473,13 +473,17 @@ __global__ void __launch_bounds__(kRankThreads)
   // late-starting CTA can lose peers' scores and keep the values of the previous launch.
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t q = ptx::cluster_ctarank();
-  const float hb = hbp[0];
   const long long p0 = min(n, (long long)q * rows_per_cta);
   const long long p1 = min(n, p0 + rows_per_cta);
+  // labels and batch offsets were written before the forward pass: read them while it drains
+  // (programmatic launch); the head partials and bias only after it has completed
   for (long long p = t; p < n; p += blockDim.x) sy[p] = y[p];
+  if (seg != nullptr)
+    for (long long k = t; k <= p1 - p0; k += blockDim.x) sseg[k] = seg[p0 + k];
+  ptx::pdl_wait();
+  const float hb = hbp[0];
   // scores of THIS CTA's programs (fixed tile order per statement row, then the segment sum)
   if (seg != nullptr) {
-    for (long long k = t; k <= p1 - p0; k += blockDim.x) sseg[k] = seg[p0 + k];
     __syncthreads();
     const long long r0 = sseg[0], r1 = sseg[p1 - p0];
     for (long long r = r0 + t; r < r1; r += blockDim.x) {
@@ -1607,13 +1611,15 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
   cfg.blockDim = dim3(kRankThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kRankCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the forward's tail
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   const long long Rk = seg ? R : n;
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, rank_cluster_kernel, part, ntiles, ld, hb, seg, y, n, nsplit, rows_per_cta, s_out,
                                 Rk, out.loss, out.pairs, out.coefA, out.coefB, out.gb));
