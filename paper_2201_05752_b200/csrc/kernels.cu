@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(kRankThreads)
   __shared__ long long sseg[kRankMaxRows + 1];
   const int t = threadIdx.x;
   rank_stamp(0);
+  ptx::pdl_launch_dependents();  // the head backward may be scheduled now; it waits for our completion
   // every CTA of the cluster must be running before a peer writes into its shared memory (the
   // score all-gather below): arrive now, wait right before the first remote store. Without it a
   // late-starting CTA can lose peers' scores and keep the values of the previous launch.
@@ -862,6 +863,7 @@ __global__ void __launch_bounds__(256) head_backward_bf16x8_kernel(const float* 
                                                                    long long R, int W, __nv_bfloat16* __restrict__ dz,
                                                                    long long ldz) {
   ptx::pdl_launch_dependents();
+  ptx::pdl_wait();  // programmatic launch behind the ranking step: coefA is its output
   const int groups = W / 8;
   const long long total = R * groups;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -1634,9 +1636,18 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
   if constexpr (sizeof(T) == 2) {
     if (dz_lo == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
         ((reinterpret_cast<uintptr_t>(H) | reinterpret_cast<uintptr_t>(dz)) & 15) == 0) {
-      head_backward_bf16x8_kernel<<<grid_for(R * (W / 8), 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz,
-                                                                                ldz);
-      MOSES_CUDA(cudaGetLastError());
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid_for(R * (W / 8), 256));
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      MOSES_CUDA(cudaLaunchKernelEx(&cfg, head_backward_bf16x8_kernel, coefA, coefB, wh, u,
+                                    reinterpret_cast<const __nv_bfloat16*>(H), ldh, R, W,
+                                    reinterpret_cast<__nv_bfloat16*>(dz), ldz));
       return;
     }
   }
