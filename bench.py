@@ -867,14 +867,22 @@ def main():
             e2e_step(e2e_steps + (k % 64))
         ml._ck(L.moses_model_synchronize(dm.h))
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for k in range(e2e_steps):
-            e2e_step(k)
-        ml._ck(L.moses_model_synchronize(dm.h))
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
+        # three timed windows of e2e_steps each (median reported; host GC paused inside them)
+        import gc
+
+        e2e_windows = []
+        for _rep in range(3):
+            if world > 1:
+                dist.barrier()
+            gc.disable()
+            t0 = time.perf_counter()
+            for k in range(e2e_steps):
+                e2e_step(k)
+            ml._ck(L.moses_model_synchronize(dm.h))
+            torch.cuda.synchronize()
+            e2e_windows.append(time.perf_counter() - t0)
+            gc.enable()
+        e2e_s = float(np.median(e2e_windows))
         if any(rcs):
             ml._ck(next(r for r in rcs if r))
         assert world > 1 or bool(torch.isfinite(losses[:e2e_steps]).all()) and float(losses[e2e_steps - 1]) > 0.0
@@ -933,6 +941,7 @@ def main():
                          "L2 flush before each one)"},
         "ms_per_step_l2_flushed": ms_step_flushed,
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 8,
+                "windows_samples_per_s": [world * BATCH * e2e_steps / w for w in e2e_windows],
                 "path": ("moses_train_step_pooled_async (C ABI: pinned host float64 rows/offsets/labels uploaded "
                          "every step, upload of step k+1 overlapping step k, per-step loss read back; 4 distinct "
                          "host batches)") if world == 1 else
