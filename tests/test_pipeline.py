@@ -229,3 +229,41 @@ def test_records_number_format(ml, tmp_path, x, want):
     line = open(p).read()
     assert '"throughput_gflops":' + want + "," in line, line
     assert ml.RecordStore.read(p).export()["throughput"][0] == x
+
+
+def test_records_roundtrip_property(ml, tmp_path):
+    """Any record (unicode ids with escapes, any finite double, int64 values, u64 seq) survives
+    write -> read unchanged, and the writer's lines parse as the same JSON object."""
+    hypothesis = pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    path = str(tmp_path / "prop.jsonl")
+    # ids cross the C ABI as NUL-terminated UTF-8: no embedded NUL, no lone surrogates
+    text = st.text(alphabet=st.characters(blacklist_categories=("Cs",), blacklist_characters="\x00"),
+                   min_size=0, max_size=12)
+    dbl = st.floats(allow_nan=False, allow_infinity=False, width=64)
+    rec = st.tuples(text, text, st.lists(st.integers(-2**63, 2**63 - 1), max_size=6), dbl, dbl, dbl,
+                    st.integers(0, 2**64 - 1))
+
+    @settings(max_examples=60, deadline=None)
+    @given(st.lists(rec, min_size=1, max_size=5))
+    def check(records):
+        store = ml.RecordStore()
+        for tid, did, vals, thr, lat, wall, seq in records:
+            store.append(tid, did, [vals] if vals else np.zeros((1, 0), dtype=np.int64), thr, lat, wall, seq)
+        store.write(path)
+        back = ml.RecordStore.read(path).export()
+        ids = ml.RecordStore.read(path)
+        tids, dids = ids.task_ids(), ids.device_ids()
+        lines = open(path, encoding="utf-8").read().split("\n")  # not splitlines(): U+0085 is valid in JSON strings
+        for i, (tid, did, vals, thr, lat, wall, seq) in enumerate(records):
+            assert tids[back["task"][i]] == tid and dids[back["device"][i]] == did
+            assert back["values"][back["value_off"][i]:back["value_off"][i + 1]].tolist() == vals
+            assert back["throughput"][i] == thr and back["latency"][i] == lat and back["wall_cost"][i] == wall
+            assert int(back["seq"][i]) == seq
+            obj = json.loads(lines[i])
+            assert obj["task_id"] == tid and obj["values"] == vals and obj["seq"] == seq
+            assert obj["throughput_gflops"] == thr
+
+    check()
