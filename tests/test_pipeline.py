@@ -267,3 +267,25 @@ def test_records_roundtrip_property(ml, tmp_path):
             assert obj["throughput_gflops"] == thr
 
     check()
+
+
+def test_plan_property_vs_oracle(orc, ml):
+    """Random stores (task interleavings, batch sizes, seeds): the native plan equals the oracle's
+    make_ranking_batches restatement batch for batch."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=80, deadline=None)
+    @given(st.lists(st.integers(0, 4), max_size=120), st.integers(2, 40), st.integers(0, 2**64 - 1))
+    def check(tasks, batch, seed):
+        ids = ["task%d" % t for t in range(5)]
+        rec = [ids[t] for t in tasks]
+        want, dropped = orc.make_ranking_batches(rec, batch, seed)
+        plan = ml.make_ranking_batches(rec, ids, batch, seed)
+        _same_plan(plan, want)
+        assert plan.dropped_singletons == dropped
+        got_rows = sorted(plan.rows.tolist())
+        assert got_rows == sorted(r for _, rows in want for r in rows)
+
+    check()
