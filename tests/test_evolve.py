@@ -72,3 +72,30 @@ def test_evolve_validation(ml, orc):
     assert e.value.code == "immutable-space"
     vals, _ = ml.evolve(None, TASK, single, lin_w=[1.0, 1.0], population=3, survivors=3, generations=0)
     assert vals.tolist() == [[4, 8]] * 3
+
+
+def test_evolve_property_vs_oracle(ml, orc):
+    """Random SearchParams, linear scorers and knob spaces: bit-exact populations and scores."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=40, deadline=None)
+    @given(st.integers(1, 20), st.integers(0, 4), st.integers(1, 4), st.integers(1, 20),
+           st.floats(0.0, 1.0), st.integers(0, 2**64 - 1),
+           st.lists(st.lists(st.integers(-50, 50), min_size=1, max_size=5, unique=True), min_size=1, max_size=4),
+           st.lists(st.floats(-2.0, 2.0, allow_nan=False), min_size=4, max_size=4))
+    def check(pop, gens, mc, surv, eps, seed, doms, w):
+        surv = min(surv, pop)
+        knobs = [("k%d" % i, sorted(d)) for i, d in enumerate(doms)]
+        lw = w[:len(knobs)]
+        if gens > 0 and all(len(d) == 1 for _, d in knobs) and eps < 1.0:
+            return  # mutate_config raises ImmutableSpace on both sides (covered elsewhere)
+        params = dict(population=pop, generations=gens, mutation_count=mc, survivors=surv, epsilon_random=eps,
+                      seed=seed)
+        vals, scores = ml.evolve(None, TASK, knobs, lin_w=lw, **params)
+        want = orc.evolve(knobs, lin_scorer(knobs, lw), **params)
+        assert vals.tolist() == [c for c, _ in want]
+        assert scores.tolist() == [s for _, s in want]
+
+    check()
