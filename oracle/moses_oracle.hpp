@@ -760,8 +760,12 @@ struct TaskDesc {
 // encode_features (space.cpp:140-159): entries 0..9 live, 10..15 zero.
 inline void encode_features(const TaskDesc& t, const std::int64_t* values, const int* roles, int nk, double* f) {
   std::int64_t kv[5] = {1, 1, 0, 1, 1};  // knob_view fallbacks (space.cpp:132-136)
+  bool seen[5] = {false, false, false, false, false};  // find_knob takes the first knob of a name (space.cpp:19-24)
   for (int i = 0; i < nk; ++i)
-    if (roles[i] >= 0 && roles[i] < 5) kv[roles[i]] = values[i];
+    if (roles[i] >= 0 && roles[i] < 5 && !seen[roles[i]]) {
+      kv[roles[i]] = values[i];
+      seen[roles[i]] = true;
+    }
   const double tx = double(kv[0]), ty = double(kv[1]), un = double(kv[2]);
   const double footprint = t.bytes_per_unit * tx * ty * std::max<double>(1.0, un);
   for (int j = 0; j < 16; ++j) f[j] = 0.0;
