@@ -185,7 +185,7 @@ def test_space_property_vs_oracle(ml, orc):
     device = {"id": "dev", "peak_gflops": 5000.0, "parallel_units": 24.0, "vector_lanes": 8.0, "cache_bytes": 3e6,
               "measure_overhead_ms": 1.5, "noise_std": 0.07, "repeats": 2}
 
-    @settings(max_examples=25, deadline=None)
+    @settings(max_examples=12, deadline=None)
     @given(st.lists(st.tuples(st.sampled_from(names),
                               st.lists(st.integers(1, 4096), min_size=1, max_size=9, unique=True)),
                     min_size=1, max_size=6),
