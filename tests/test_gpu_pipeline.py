@@ -300,3 +300,31 @@ def test_pretrain_from_records_matches_oracle(ml, orc):
     with pytest.raises(ml.MosesError) as e:
         ml.pretrain(dm, TASKS, knobs, rt, bad, [r["throughput_gflops"] for r in recs], 16, 6, 1)
     assert e.value.code == "invalid-config" and "record 7" in str(e.value)
+
+
+def test_generate_dataset_property(ml, orc):
+    """Random seeds, task ids (any UTF-8) and sample counts: the device's keyed draws equal the
+    oracle's sample_config walk value for value."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    knobs = orc.default_knob_template()
+    ids = st.text(alphabet=st.characters(blacklist_categories=("Cs",), blacklist_characters="\x00"), max_size=10)
+
+    @settings(max_examples=15, deadline=None)
+    @given(st.integers(0, 2**64 - 1), ids, st.integers(1, 300))
+    def check(seed, tid, n):
+        _, V, *_ = gen_device(ml, tid, TASKS[0][1], knobs, n, seed)
+        idx = orc.sample_config_indices(seed, tid, knobs, n)
+        sizes = [len(d) for _, d in knobs]
+        want = []
+        for x in idx:
+            row = [0] * len(knobs)
+            for k in range(len(knobs) - 1, -1, -1):
+                row[k] = knobs[k][1][x % sizes[k]]
+                x //= sizes[k]
+            want.append(row)
+        assert V.cpu().numpy().tolist() == want
+
+    check()
