@@ -301,6 +301,7 @@ struct Parser {
     }
     v.kind = 'f';
     v.f = std::strtod(tok.c_str(), nullptr);
+    if (!std::isfinite(v.f)) bad("number overflow parsing '" + tok + "'");  // nlohmann rejects it too
     return v;
   }
   Val value(int depth = 0) {

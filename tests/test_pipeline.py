@@ -289,3 +289,31 @@ def test_plan_property_vs_oracle(orc, ml):
         assert got_rows == sorted(r for _, rows in want for r in rows)
 
     check()
+
+
+def test_records_reader_fuzz(ml, tmp_path):
+    """Arbitrary (often malformed) lines never crash the native reader: each file either reads or
+    fails with parse-error / missing-field naming a line."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    path = str(tmp_path / "fuzz.jsonl")
+    good = ('{"task_id":"a","values":[1,2],"throughput_gflops":1.5,"latency_ms":2,"wall_cost_ms":3,'
+            '"device_id":"d","seq":4}')
+    pieces = st.sampled_from(['{', '}', '[', ']', '"', ':', ',', '\\', '\\u12', 'true', 'null', '1e400', '-0',
+                              '"task_id"', '"values"', '"seq"', ' ', '\t', good, good[:-1], good[1:]])
+    line = st.one_of(st.lists(pieces, max_size=12).map("".join), st.text(max_size=40))
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.lists(line, min_size=1, max_size=4))
+    def check(lines):
+        with open(path, "w", encoding="utf-8", errors="surrogatepass") as f:
+            f.write("\n".join(lines) + "\n")
+        try:
+            ml.RecordStore.read(path)
+        except ml.MosesError as e:
+            assert e.code in ("parse-error", "missing-field"), e
+            assert ":line " in str(e)
+
+    check()
