@@ -585,10 +585,10 @@ def bench_pretrain(ml, L, peaks, epochs: int = 30, per_task: int = 6000):
 
     import torch
 
-    sim = json.load(open(os.path.join(ROOT, "tests", "golden", "simulated_oracle.json")))
-    device = sim["devices"]["server"]
+    lab = json.load(open(os.path.join(ROOT, "paper_2201_05752_b200", "configs", "lab.json")))
+    device = lab["devices"]["server"]
     tasks = [(t["id"], (t["work_gflops"], t["bytes_per_unit"], t["ideal_log2_tiles"], t["ideal_log2_unroll"]))
-             for t in sim["tasks"]["list"]]
+             for t in lab["tasks"]]
     knobs = [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
              ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
     dims = [16, 512, 512, 1]

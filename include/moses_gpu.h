@@ -121,7 +121,7 @@ MOSES_API int moses_gradients_pooled(moses_model_t m, const double* stmt_feature
  * asynchronously (pipelined: the upload of the next batch overlaps this step's kernels). Returns once
  * queued; x / offsets / y must stay valid and unchanged until the step completes. loss_out (host
  * memory or NULL) receives the step's loss from a per-slot mailbox the step's last kernel writes: by
- * the second following call on the handle at the latest, or by moses_model_synchronize, which waits
+ * the third following call on the handle at the latest (three staging slots), or by moses_model_synchronize, which waits
  * for every queued step. bf16 handles; capacity max_rows statement rows per step. */
 MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* stmt_features, int64_t n_stmt, int32_t D,
                                             const int64_t* offsets, int64_t programs, const double* labels,
@@ -398,7 +398,7 @@ MOSES_API int moses_synth_labels_device(uint64_t seed, int64_t row0, int64_t n, 
 /* CSR offsets of `programs` programs with 1 + below(max_stmts) statements each (host). */
 MOSES_API int moses_synth_offsets(uint64_t seed, int64_t programs, int32_t max_stmts, int64_t* offsets);
 
-/* ------------------------------------------------------------------ files (model.cpp:344-412, lottery.cpp:267-325) */
+/* ------------------------------------------------------------------ files (model.cpp:344-412, lottery.cpp:182-240) */
 MOSES_API int64_t moses_serialize(const int32_t* dims, int32_t ndims, const double* params, const double* momentum,
                                   uint8_t* out, int64_t cap);
 MOSES_API int moses_deserialize(const uint8_t* bytes, int64_t len, int32_t* dims_out, double* params,

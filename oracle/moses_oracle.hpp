@@ -589,7 +589,7 @@ std::vector<R> xi_scores(const R* w, const R* g, std::int64_t P, bool normalize)
   return xi;
 }
 
-enum class Mode : int { Threshold = 1, Ratio = 2 };  // "MOSK" mode byte (lottery.cpp:280)
+enum class Mode : int { Threshold = 1, Ratio = 2 };  // "MOSK" mode byte (lottery.cpp:195,223-224)
 
 // lottery.cpp:59-90
 template <class R>
@@ -633,7 +633,7 @@ void variant_decay(R* w, std::int64_t P, const std::uint8_t* keep, double alpha,
     if (!keep[i]) w[i] *= factor;
 }
 
-// lottery.cpp:220-249
+// lottery.cpp:135-164
 template <class R>
 R adversarial_term(Adversary<R>& adv, const R* hs, int m, const R* ht, int n, int width) {
   if (adv.m == 0) fail(Err::AdversaryDisabled, "adversary has an empty replay buffer");
@@ -853,7 +853,7 @@ inline void measure(const DeviceDesc& d, const TaskDesc& t, const std::int64_t* 
   *wall_cost = d.measure_overhead_ms + static_cast<double>(d.repeats) * *latency;
 }
 
-// ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:267-325)
+// ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:182-240)
 inline void put_u32(std::string& o, std::uint32_t v) { for (int i = 0; i < 4; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }
 inline void put_u64(std::string& o, std::uint64_t v) { for (int i = 0; i < 8; ++i) o.push_back(char((v >> (8 * i)) & 0xff)); }
 inline void put_f64(std::string& o, double d) { put_u64(o, std::bit_cast<std::uint64_t>(d)); }

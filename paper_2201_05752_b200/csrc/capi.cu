@@ -192,6 +192,7 @@ struct moses_model {
   long long P = 0;
   std::vector<long long> off;
   int prec = MOSES_PREC_BF16;
+  int device = 0;  // CUDA device the handle's streams and buffers live on (current device at create)
   int esz = 2;
   bool split = false;  // MOSES_PREC_FP32: 3xTF32 operands, every GEMM operand buffer has a low twin
   long long cap = 0;
@@ -802,6 +803,7 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->P = level_off(m->dims, m->L);
     for (int l = 0; l <= m->L; ++l) m->off.push_back(level_off(m->dims, l));
     m->prec = precision;
+    MOSES_CUDA(cudaGetDevice(&m->device));
     m->esz = precision == MOSES_PREC_BF16 ? 2 : 4;
     m->split = precision == MOSES_PREC_FP32;
     const int twin = m->split ? 2 : 1;  // FP32 mode: [hi | lo] halves of every GEMM operand buffer
@@ -1791,7 +1793,7 @@ MOSES_API int moses_adversary_create(const double* replay, int64_t mrows, int32_
                                      moses_adversary_t* out) {
   return guarded([&] {
     *out = nullptr;
-    if (mrows == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "replay buffer must be non-empty");  // lottery.cpp:253
+    if (mrows == 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "replay buffer must be non-empty");  // lottery.cpp:168-169
     if (width <= 0) fail(MOSES_ERR_BAD_DIMS, "penultimate width must be positive");
     auto a = std::make_unique<moses_adversary>();
     a->D = D;
@@ -2761,6 +2763,13 @@ MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, c
       }
     }
     width = std::max(1, std::min(width, n_jobs));
+    for (int j = 0; j < n_jobs; ++j) {
+      if (models[j] == nullptr) fail(MOSES_ERR_INVALID_ARG, "null model handle in the job list");
+      for (int i = 0; i < j; ++i)
+        if (models[i] == models[j])
+          fail(MOSES_ERR_INVALID_ARG, "model handle listed twice in the job list (jobs " + std::to_string(i) + ", " +
+                                          std::to_string(j) + "): a handle must not be used concurrently");
+    }
     std::atomic<int> next{0};
     std::mutex mu_err;
     int first_job = -1, first_code = 0;
@@ -2770,6 +2779,8 @@ MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, c
         const int j = next.fetch_add(1);
         if (j >= n_jobs) return;
         try {
+          // new threads start on device 0: every job runs on its handle's device
+          MOSES_CUDA(cudaSetDevice(models[j]->device));
           pretrain_impl(models[j], x_base, ldx, y_base, record_task, n_records, task_ids, n_task_ids, batch_size,
                         seeds[j], epochs, lr, mu, epoch_mean_loss ? epoch_mean_loss + size_t(j) * epochs : nullptr,
                         dropped_singletons ? dropped_singletons + j : nullptr);

@@ -223,14 +223,11 @@ static int encode_impl(const double* task4, const long long* domains, const int*
       for (double ty : dom_r[1])
         for (double un : dom_r[2]) tab.push_back(std::log2(task4[1] * tx * ty * std::max<double>(1.0, un)) / 24.0);
   }
-  static thread_local double* dtab = nullptr;
-  static thread_local size_t dtab_n = 0;
+  // per-call table, stream-ordered on `st`: callers encode on different streams, so a shared buffer
+  // could be overwritten while an earlier encode kernel still reads it
+  double* dtab = nullptr;
   if (!tab.empty()) {
-    if (tab.size() > dtab_n) {
-      if (dtab) cudaFree(dtab);
-      MOSES_CUDA(cudaMalloc(&dtab, tab.size() * sizeof(double)));
-      dtab_n = tab.size();
-    }
+    MOSES_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dtab), tab.size() * sizeof(double), st));
     MOSES_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     a.tab = dtab;
   }
@@ -245,6 +242,7 @@ static int encode_impl(const double* task4, const long long* domains, const int*
     encode_configs_kernel<float><<<grid, 256, 0, st>>>(a, first, n, static_cast<float*>(feat), ld, D, hash, values_out,
                                                       idx_list);
   MOSES_CUDA(cudaGetLastError());
+  if (dtab) MOSES_CUDA(cudaFreeAsync(dtab, st));
   return 1;
 }
 int encode_configs(const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,

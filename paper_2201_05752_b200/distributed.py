@@ -76,12 +76,16 @@ def sharded_score_topk(model, x_dev_shard, ld: int, row0: int, n_local: int, k: 
 
     L = ml.lib()
     scores = torch.empty(n_local, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()  # the shard rows were written on torch's stream
     ml._ck(L.moses_predict_device(model.h, x_dev_shard, dtype, ld, n_local, scores.data_ptr()))
+    # predict only queues work on the handle's stream; top-k reads the scores on another stream
+    ml._ck(L.moses_model_synchronize(model.h))
     kk = min(k, n_local)
     idx = (C.c_int64 * max(kk, 1))()
     ml._ck(L.moses_topk_device(scores.data_ptr(), n_local, kk, idx))
     local_idx = np.frombuffer(idx, dtype=np.int64)[:kk].copy()
-    local_scores = scores.cpu().numpy()[local_idx]
+    # only the k winning scores leave the device
+    local_scores = scores[torch.from_numpy(local_idx).to(scores.device)].cpu().numpy()
     return gather_merge_topk(local_scores, local_idx + row0, k, group)
 
 
@@ -89,7 +93,11 @@ def allreduce_gradients_(grad_tensor, group=None):
     """Average the device gradient buffer across data-parallel ranks (in place)."""
     import torch.distributed as dist
 
-    dist.all_reduce(grad_tensor, op=dist.ReduceOp.AVG, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(grad_tensor, op=dist.ReduceOp.AVG, group=group)
+    else:  # gloo has no AVG
+        dist.all_reduce(grad_tensor, op=dist.ReduceOp.SUM, group=group)
+        grad_tensor.div_(dist.get_world_size(group))
     return grad_tensor
 
 

@@ -23,7 +23,7 @@ import numpy as np
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmoses_gpu.so")
 
-# moseslab::ErrorCode names (errors.hpp:157-186), indexed by ordinal
+# moseslab::ErrorCode names (errors.hpp:10-36), indexed by ordinal
 ERROR_NAMES = [
     "invalid-task", "invalid-config", "space-too-large", "immutable-space", "bad-dims",
     "dim-mismatch", "shape-mismatch", "version-mismatch", "corrupt-stream", "empty-dataset",
@@ -670,7 +670,7 @@ def adam_update(model: DeviceModel, lr, b1=0.9, b2=0.999, eps=1e-8, step=1, mask
     _ck(lib().moses_adam_update(model.h, lr, b1, b2, eps, step, _p(m), 0 if m is None else len(m)))
 
 
-# ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:267-325)
+# ---------------------------------------------------------------- files (model.cpp:344-412, lottery.cpp:182-240)
 def serialize(params: CostModelParams) -> bytes:
     d = _dims(params.dims)
     n = lib().moses_serialize(_p(d), len(d), _p(params.params), _p(params.momentum), None, 0)

@@ -30,11 +30,23 @@ def _worker(rank, world, port, n, k, q):
     lo, hi = shard_range(n, rank, world)
     li = local_topk_host(pool[lo:hi], k)
     merged = gather_merge_topk(pool[lo:hi][li], li + lo, k)
-    # data-parallel gradient average
-    g = torch.full((5,), float(rank + 1))
-    dist.all_reduce(g, op=dist.ReduceOp.AVG) if hasattr(dist.ReduceOp, "AVG") and dist.get_backend() != "gloo" \
-        else (dist.all_reduce(g), g.div_(world))
-    q.put((rank, merged.tolist(), g.tolist()))
+    # data-parallel (throughput mode) gradient average: each rank's oracle gradient of its own batch,
+    # averaged by the library helper
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import oracle as orc
+
+    from paper_2201_05752_b200.distributed import allreduce_gradients_
+
+    dims = [4, 8, 8, 1]
+    w = orc.init_random(dims, 7)
+    xr = np.random.default_rng(10 + rank).random((9, 4))
+    yr = 0.1 + np.random.default_rng(20 + rank).random(9)
+    g_local, _ = orc.gradients(dims, w, xr, yr)
+    g = torch.from_numpy(g_local.copy())
+    allreduce_gradients_(g)
+    q.put((rank, merged.tolist(), g.numpy().tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -57,9 +69,13 @@ def test_sharded_topk_merge_equals_single_device(n, k):
         p.join(timeout=60)
     pool = np.round(np.random.default_rng(123).normal(0, 1, n), 2).astype(np.float32)
     want = orc.topk(pool, k)  # single-device reference order (score desc, index asc)
+    dims = [4, 8, 8, 1]
+    w = orc.init_random(dims, 7)
+    g_mean = np.mean([orc.gradients(dims, w, np.random.default_rng(10 + r).random((9, 4)),
+                                    0.1 + np.random.default_rng(20 + r).random(9))[0] for r in range(2)], axis=0)
     for rank, merged, g in res:
         assert merged == list(want)
-        assert np.allclose(g, 1.5)
+        assert np.allclose(g, g_mean, rtol=0, atol=1e-15)
 
 
 def test_shard_range_covers_everything():

@@ -31,7 +31,7 @@ def store(orc, tasks, per_task, seed):
 
 
 def test_oracle_rng_pins(orc):
-    # SplitMix64(0) first draw (test_rng.cpp:275-287) and KeyBuilder == the C++ oracle's FNV
+    # SplitMix64(0) first draw (test_rng.cpp:14-16) and KeyBuilder == the C++ oracle's FNV
     assert orc.RngStream(0).next_u64() == 0xE220A8397B1DCDAF
     assert orc.key_builder("abc") == orc.fnv_str("abc")
     assert orc.key_builder(7, "gen", "a") != orc.key_builder(7, "gen", "b")
