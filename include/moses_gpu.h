@@ -59,9 +59,18 @@ enum {
   MOSES_ERR_INVALID_ARG = 103
 };
 
-/* GEMM operand precision. FP32 = 3xTF32 split operands (hi*hi + hi*lo + lo*hi on kind::tf32):
- * fp32-level accuracy (the <= 1e-5 parity path); host-API inputs only, no training graphs. */
-enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1, MOSES_PREC_FP32 = 2 };
+/* GEMM operand precision.
+ *   BF16   single bf16 operands (throughput mode; ~5e-3 from the fp64 reference on the cost model).
+ *   TF32   kind::tf32 operands (~5e-4 on predictions, ~2e-3 on gradients).
+ *   FP32   3xTF32 split operands (hi*hi + hi*lo + lo*hi on kind::tf32): fp32-level accuracy (the <= 1e-5
+ *          parity path); host-API inputs (and device fp32 rows), no training graphs.
+ *   BF16X3 split bf16 operands: every operand is hi + lo with hi = rn_bf16(v), lo = rn_bf16(v - hi),
+ *          products A_hi*B_hi + A_hi*B_lo + A_lo*B_hi on the bf16 tensor cores (~1e-5 from the fp64
+ *          reference: inside the north-star 1e-3 tensor-core bound). Fused 512-wide chain kernels only:
+ *          hidden widths 512, input width <= 512. Device-resident input rows are fp32.
+ * Device-resident input rows (moses_*_device, training graphs, plans) are bf16 for BF16 handles and
+ * fp32 otherwise, with the row stride moses_packed_ld. */
+enum { MOSES_PREC_BF16 = 0, MOSES_PREC_TF32 = 1, MOSES_PREC_FP32 = 2, MOSES_PREC_BF16X3 = 3 };
 enum { MOSES_MODE_THRESHOLD = 1, MOSES_MODE_RATIO = 2 };        /* PartitionMode, "MOSK" mode byte */
 enum { MOSES_DTYPE_F32 = 0, MOSES_DTYPE_BF16 = 1, MOSES_DTYPE_F64 = 2 };
 

@@ -194,7 +194,9 @@ struct moses_model {
   int prec = MOSES_PREC_BF16;
   int device = 0;  // CUDA device the handle's streams and buffers live on (current device at create)
   int esz = 2;
-  bool split = false;  // MOSES_PREC_FP32: 3xTF32 operands, every GEMM operand buffer has a low twin
+  // split operands: every GEMM operand buffer has a low twin (hi plane, then lo plane at + cap*ld):
+  // MOSES_PREC_FP32 = 3xTF32 (esz 4), MOSES_PREC_BF16X3 = split bf16 (esz 2, fused chain kernels only)
+  bool split = false;
   long long cap = 0;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;      // weight-gradient side stream
@@ -210,7 +212,7 @@ struct moses_model {
   cudaStream_t st3 = nullptr;
   cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   struct BatchBuf {
-    void* act = nullptr;
+    void* act = nullptr;           // hi plane; split handles: lo plane at + cap * ld[0] elements
     float* labels = nullptr;
     long long* seg_off = nullptr;
     int* seg_rows = nullptr;
@@ -282,12 +284,34 @@ struct moses_model {
   const void* wop(int l) const {
     return esz == 2 ? static_cast<const void*>(wbf + off[l]) : static_cast<const void*>(wtf + off[l]);
   }
-  // shadow written by the fused update kernels; FP32 mode refreshes the hi/lo pair afterwards
-  Shadow shadow() const { return esz == 2 ? Shadow{wbf, 1} : (split ? Shadow{nullptr, 0} : Shadow{wtf, 2}); }
-  Shadow shadow_full() const { return split ? Shadow{wtf, 3} : shadow(); }
-  const float* wop_lo(int l) const { return split ? wtf + shadow_lo_offset(P) + off[l] : nullptr; }
-  float* act_lo(int l) const { return split ? static_cast<float*>(act[l]) + cap * ld[l] : nullptr; }
-  float* dz_lo(int l) const { return split ? static_cast<float*>(dz[l]) + cap * lddz[l] : nullptr; }
+  bool bsplit() const { return split && esz == 2; }  // MOSES_PREC_BF16X3
+  // element type of device-resident input rows (moses_*_device, training graphs, plans): the operand
+  // type, except split-bf16 handles, which take fp32 rows and split them into their hi/lo planes
+  int in_esz() const { return bsplit() ? 4 : esz; }
+  // shadow written by the generic update kernels; split modes refresh the hi/lo pair afterwards
+  // (post_update); the fused training step writes the split-bf16 pair itself
+  Shadow shadow() const { return esz == 2 ? (split ? Shadow{nullptr, 0} : Shadow{wbf, 1}) : (split ? Shadow{nullptr, 0} : Shadow{wtf, 2}); }
+  Shadow shadow_full() const {
+    return split ? (esz == 2 ? Shadow{wbf, 4, shadow_lo_offset(P)} : Shadow{wtf, 3}) : shadow();
+  }
+  const void* wop_lo(int l) const {
+    if (!split) return nullptr;
+    return esz == 2 ? static_cast<const void*>(wbf + shadow_lo_offset(P) + off[l])
+                    : static_cast<const void*>(wtf + shadow_lo_offset(P) + off[l]);
+  }
+  void* act_lo(int l) const { return split ? static_cast<uint8_t*>(act[l]) + cap * ld[l] * esz : nullptr; }
+  void* dz_lo(int l) const { return split ? static_cast<uint8_t*>(dz[l]) + cap * lddz[l] * esz : nullptr; }
+  template <typename T>
+  T* act_lo_t(int l) const { return static_cast<T*>(act_lo(l)); }
+  template <typename T>
+  T* dz_lo_t(int l) const { return static_cast<T*>(dz_lo(l)); }
+  // lo plane of a layer-0 operand buffer (act[0] or the alternate batch buffer)
+  const void* x0_lo(const void* x0) const {
+    if (!split) return nullptr;
+    if (x0 == act[0]) return act_lo(0);
+    if (alt.act != nullptr && x0 == alt.act) return static_cast<const uint8_t*>(alt.act) + cap * ld[0] * esz;
+    fail(MOSES_ERR_INVALID_ARG, "split-operand handles take layer-0 rows from their own packed buffers");
+  }
   void post_update() {  // FP32 mode: hi/lo operand pair of the updated parameters
     if (split) refresh_shadow(w, P, shadow_full(), st);
   }
@@ -364,32 +388,49 @@ bool chain_ok(const moses_model* m) {
 
 template <typename T>
 void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
-  if (m->split && x0 != m->act[0])
-    fail(MOSES_ERR_INVALID_ARG, "FP32 (3xTF32) handles take inputs through the host API only");
-  if (chain_ok(m) && R > 0 && R <= kChainMaxRows) {
-    ChainCall cc;
-    cc.fwd = true;
-    cc.M = int(R);
-    cc.n_layers = m->L - 1;
-    cc.in = x0;
-    cc.ld_in = ldx0;
-    for (int l = 0; l + 1 < m->L; ++l) {
-      cc.K[l] = m->dims[l];
-      cc.w[l] = m->wop(l);
-      cc.bias[l] = m->bias(l);
-      cc.out[l] = (l + 2 == m->L && !keep_last) ? nullptr : m->act[l + 1];
-      cc.ldo[l] = m->ld[l + 1];
+  if (m->split && x0 != m->act[0] && x0 != m->alt.act)
+    fail(MOSES_ERR_INVALID_ARG, "split-operand handles take inputs through their packed buffers");
+  if (m->bsplit() && !chain_ok(m))
+    fail(MOSES_ERR_INVALID_ARG, "split-bf16 handles need hidden widths of 512 and input width <= 512");
+  if (chain_ok(m) && R > 0 && (R <= kChainMaxRows || m->bsplit())) {
+    // split-bf16: the fused chain is its only GEMM path; rows are independent, so any R runs as
+    // row chunks of at most kChainMaxRows
+    const void* x0_lo = m->x0_lo(x0);
+    for (long long r0 = 0; r0 < R; r0 += kChainMaxRows) {
+      const long long Rc = std::min(kChainMaxRows, R - r0);
+      const size_t es = size_t(m->esz);
+      auto at = [&](const void* p, long long ld) -> void* {
+        return p ? const_cast<uint8_t*>(static_cast<const uint8_t*>(p)) + size_t(r0) * size_t(ld) * es : nullptr;
+      };
+      ChainCall cc;
+      cc.fwd = true;
+      cc.M = int(Rc);
+      cc.n_layers = m->L - 1;
+      cc.in = at(x0, ldx0);
+      cc.ld_in = ldx0;
+      cc.split = m->bsplit();
+      cc.in_lo = at(x0_lo, ldx0);
+      for (int l = 0; l + 1 < m->L; ++l) {
+        cc.K[l] = m->dims[l];
+        cc.w[l] = m->wop(l);
+        cc.w_lo[l] = m->wop_lo(l);
+        cc.bias[l] = m->bias(l);
+        const bool keep = !(l + 2 == m->L && !keep_last);
+        cc.out[l] = keep ? at(m->act[l + 1], m->ld[l + 1]) : nullptr;
+        cc.out_lo[l] = keep ? at(m->act_lo(l + 1), m->ld[l + 1]) : nullptr;
+        cc.ldo[l] = m->ld[l + 1];
+      }
+      cc.head_w = m->head_w();
+      cc.head_u = head_u;
+      cc.head_part = m->head_part + r0;
+      cc.head_part2 = head_u ? m->head_part2 + r0 : nullptr;
+      cc.head_ld = m->cap;
+      {
+        ProfScope ps(P_GEMM_FWD, m->st);
+        launch_chain(cc, m->st);
+      }
+      note_launch(1);
     }
-    cc.head_w = m->head_w();
-    cc.head_u = head_u;
-    cc.head_part = m->head_part;
-    cc.head_part2 = head_u ? m->head_part2 : nullptr;
-    cc.head_ld = m->cap;
-    {
-      ProfScope ps(P_GEMM_FWD, m->st);
-      launch_chain(cc, m->st);
-    }
-    note_launch(1);
     m->last_tiles = 4;
     return;
   }
@@ -449,38 +490,52 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[0], 0));
   {
     ProfScope ps(P_HEAD, m->st2);
-    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2, gb_override);
+    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2, gb_override,
+                  m->act_lo_t<T>(L - 1));
   }
   {
     ProfScope ps(P_HEAD, m->st);
     head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
-                     m->lddz[L - 1], m->st, m->dz_lo(L - 1));
+                     m->lddz[L - 1], m->st, m->dz_lo_t<T>(L - 1));
   }
   MOSES_CUDA(cudaEventRecord(ev[1 + (L - 1)], m->st));
   note_launch(2);
-  // dZ chain dz[L-2] .. dz[1] in one clustered kernel when the shape allows (mlp_chain.cuh)
-  const bool chain = sizeof(T) == 2 && chain_ok(m) && L - 2 >= 1;
+  // dZ chain dz[L-2] .. dz[1] in one clustered kernel when the shape allows (mlp_chain.cuh); split-bf16
+  // handles run it in row chunks of at most kChainMaxRows
+  const bool chain = sizeof(T) == 2 && chain_ok(m) && L - 2 >= 1 && (R <= kChainMaxRows || m->bsplit());
+  if (m->bsplit() && !(g_group && L - 1 <= 8))
+    fail(MOSES_ERR_INVALID_ARG, "split-bf16 handles need the grouped weight-gradient kernel");
   if (chain) {
-    ChainCall cc;
-    cc.fwd = false;
-    cc.M = int(R);
-    cc.n_layers = L - 2;
-    cc.in = m->dz[L - 1];
-    cc.ld_in = m->lddz[L - 1];
-    for (int j = 0; j < L - 2; ++j) {
-      const int lev = L - 2 - j;
-      cc.K[j] = m->dims[lev + 1];
-      cc.w[j] = m->wop(lev);
-      cc.out[j] = m->dz[lev];
-      cc.ldo[j] = m->lddz[lev];
-      cc.mask[j] = m->act[lev];
-      cc.ldm[j] = m->ld[lev];
+    for (long long r0 = 0; r0 < R; r0 += kChainMaxRows) {
+      const long long Rc = std::min(kChainMaxRows, R - r0);
+      auto at = [&](const void* p, long long ld) -> void* {
+        return p ? const_cast<uint8_t*>(static_cast<const uint8_t*>(p)) + size_t(r0) * size_t(ld) * sizeof(T) : nullptr;
+      };
+      ChainCall cc;
+      cc.fwd = false;
+      cc.M = int(Rc);
+      cc.n_layers = L - 2;
+      cc.in = at(m->dz[L - 1], m->lddz[L - 1]);
+      cc.ld_in = m->lddz[L - 1];
+      cc.split = m->bsplit();
+      cc.in_lo = at(m->dz_lo(L - 1), m->lddz[L - 1]);
+      for (int j = 0; j < L - 2; ++j) {
+        const int lev = L - 2 - j;
+        cc.K[j] = m->dims[lev + 1];
+        cc.w[j] = m->wop(lev);
+        cc.w_lo[j] = m->wop_lo(lev);
+        cc.out[j] = at(m->dz[lev], m->lddz[lev]);
+        cc.out_lo[j] = at(m->dz_lo(lev), m->lddz[lev]);
+        cc.ldo[j] = m->lddz[lev];
+        cc.mask[j] = at(m->act[lev], m->ld[lev]);
+        cc.ldm[j] = m->ld[lev];
+      }
+      {
+        ProfScope ps(P_GEMM_DGRAD, m->st);
+        launch_chain(cc, m->st);
+      }
+      note_launch(1);
     }
-    {
-      ProfScope ps(P_GEMM_DGRAD, m->st);
-      launch_chain(cc, m->st);
-    }
-    note_launch(1);
     MOSES_CUDA(cudaEventRecord(ev[1 + 1], m->st));  // every dz[l], l <= L-2, is ready
   }
   // bf16: all weight-gradient GEMMs in one launch once every dZ exists (gemm_group.cuh)
@@ -509,7 +564,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       const long long o = m->off[L - 1];
       ProfScope ps(P_UPDATE, m->st2);
       sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, m->P - o, fuse->lr, fuse->mu, true,
-                 Shadow{m->wbf + o, 1}, m->st2);
+                 m->bsplit() ? Shadow{m->wbf + o, 4, shadow_lo_offset(m->P)} : Shadow{m->wbf + o, 1}, m->st2);
       note_launch(1);
     }
     MOSES_CUDA(cudaEventRecord(ev[1], m->st));
@@ -517,6 +572,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     WgradGroupCall wc;
     wc.n = L - 1;
     wc.K = int(R);
+    wc.split = m->bsplit();
     if (fuse) {
       wc.counter = fuse->counter;
       wc.loss_src = fuse->loss_src;
@@ -535,6 +591,11 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       wc.w[l] = m->w + m->off[l];
       wc.mom[l] = m->mom + m->off[l];
       wc.shadow[l] = m->wbf + m->off[l];
+      if (wc.split) {
+        wc.a_lo[l] = l == 0 ? m->x0_lo(x0) : m->act_lo(l);
+        wc.b_lo[l] = m->dz_lo(l + 1);
+        wc.shadow_lo[l] = m->wbf + shadow_lo_offset(m->P) + m->off[l];
+      }
     }
     if (fuse) {
       wc.update = true;
@@ -612,19 +673,22 @@ void upload_rows(moses_model* m, const double* x, long long n, long long row0) {
     MOSES_CUDA(cudaMemcpyAsync(m->staging, x + r * D, sizeof(double) * c * D, cudaMemcpyHostToDevice, m->st));
     if (m->esz == 2)
       pack_rows<__nv_bfloat16>(m->staging, c, D, static_cast<__nv_bfloat16*>(m->act[0]) + (row0 + r) * m->ld[0],
-                               m->ld[0], m->st);
+                               m->ld[0], m->st,
+                               m->split ? m->act_lo_t<__nv_bfloat16>(0) + (row0 + r) * m->ld[0] : nullptr);
     else
       pack_rows<float>(m->staging, c, D, static_cast<float*>(m->act[0]) + (row0 + r) * m->ld[0], m->ld[0], m->st,
-                       m->split ? m->act_lo(0) + (row0 + r) * m->ld[0] : nullptr);
+                       m->split ? m->act_lo_t<float>(0) + (row0 + r) * m->ld[0] : nullptr);
     note_launch(1);
     r += c;
   }
 }
 void upload_replay(moses_model* m, const moses_adversary* a) {
   if (m->esz == 2)
-    pack_rows_f32<__nv_bfloat16>(a->replay, a->m, a->D, a->D, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0], m->st);
+    pack_rows_f32<__nv_bfloat16>(a->replay, a->m, a->D, a->D, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0], m->st,
+                                 m->act_lo_t<__nv_bfloat16>(0));
   else
-    pack_rows_f32<float>(a->replay, a->m, a->D, a->D, static_cast<float*>(m->act[0]), m->ld[0], m->st, m->act_lo(0));
+    pack_rows_f32<float>(a->replay, a->m, a->D, a->D, static_cast<float*>(m->act[0]), m->ld[0], m->st,
+                         m->act_lo_t<float>(0));
   note_launch(1);
 }
 void upload_f32(moses_model* m, const double* src, long long n, float* dst) {
@@ -647,6 +711,26 @@ void download_f32(moses_model* m, const float* src, long long n, double* dst) {
     MOSES_CUDA(cudaStreamSynchronize(m->st));
     r += c;
   }
+}
+
+// Device-resident input rows (x, ldx elements of in_esz() bytes) as the layer-0 operand: split handles
+// convert rows [0, n) into the hi/lo planes of act[0]; every other handle reads them in place.
+const void* stage_device_rows(moses_model* m, const void* x, long long ldx, long long n, long long* ld_out) {
+  if (!m->split) {
+    *ld_out = ldx;
+    return x;
+  }
+  const int D = m->dims[0];
+  if (ldx < D) fail(MOSES_ERR_INVALID_ARG, "row stride below the input width");
+  if (m->esz == 2)
+    pack_rows_f32<__nv_bfloat16>(static_cast<const float*>(x), n, D, ldx, static_cast<__nv_bfloat16*>(m->act[0]),
+                                 m->ld[0], m->st, m->act_lo_t<__nv_bfloat16>(0));
+  else
+    pack_rows_f32<float>(static_cast<const float*>(x), n, D, ldx, static_cast<float*>(m->act[0]), m->ld[0], m->st,
+                         m->act_lo_t<float>(0));
+  note_launch(1);
+  *ld_out = m->ld[0];
+  return m->act[0];
 }
 
 void dispatch_forward(moses_model* m, const void* x0, long long ldx0, long long R, const float* u, bool keep_last) {
@@ -790,8 +874,15 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
   return guarded([&] {
     *out = nullptr;
     check_dims(dims, nd, false);
-    if (precision != MOSES_PREC_BF16 && precision != MOSES_PREC_TF32 && precision != MOSES_PREC_FP32)
+    if (precision != MOSES_PREC_BF16 && precision != MOSES_PREC_TF32 && precision != MOSES_PREC_FP32 &&
+        precision != MOSES_PREC_BF16X3)
       fail(MOSES_ERR_INVALID_ARG, "precision");
+    if (precision == MOSES_PREC_BF16X3) {  // the split-bf16 kernels are the fused 512-wide chains
+      bool ok = dims[0] <= 512 && nd - 2 <= 8;
+      for (int l = 1; l + 1 < nd; ++l) ok = ok && dims[l] == 512;
+      if (!ok) fail(MOSES_ERR_INVALID_ARG, "split-bf16 (BF16X3) handles need hidden widths of 512, input width <= 512 "
+                                           "and at most 8 hidden layers; use TF32 or FP32 for other shapes");
+    }
     for (int l = 1; l + 1 < nd; ++l)
       if (dims[l] % 8) fail(MOSES_ERR_INVALID_ARG, "hidden widths must be multiples of 8 (TMA 16-byte rows)");
     if (max_rows < 1) max_rows = 1;
@@ -804,9 +895,9 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     for (int l = 0; l <= m->L; ++l) m->off.push_back(level_off(m->dims, l));
     m->prec = precision;
     MOSES_CUDA(cudaGetDevice(&m->device));
-    m->esz = precision == MOSES_PREC_BF16 ? 2 : 4;
-    m->split = precision == MOSES_PREC_FP32;
-    const int twin = m->split ? 2 : 1;  // FP32 mode: [hi | lo] halves of every GEMM operand buffer
+    m->esz = (precision == MOSES_PREC_BF16 || precision == MOSES_PREC_BF16X3) ? 2 : 4;
+    m->split = precision == MOSES_PREC_FP32 || precision == MOSES_PREC_BF16X3;
+    const int twin = m->split ? 2 : 1;  // split modes: [hi | lo] halves of every GEMM operand buffer
     m->cap = round_up(max_rows, 128);
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st2, cudaStreamNonBlocking));
@@ -818,16 +909,17 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->g = dalloc<float>(P);
     m->xi = dalloc<float>(P);
     m->mask = dalloc<uint8_t>(P);
-    if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(P);
-    else m->wtf = dalloc<float>(twin == 2 ? 2 * shadow_lo_offset(P) : P);
+    const long long shadow_n = twin == 2 ? 2 * shadow_lo_offset(P) : P;  // split: [hi | lo] at shadow_lo_offset
+    if (m->esz == 2) m->wbf = dalloc<__nv_bfloat16>(shadow_n);
+    else m->wtf = dalloc<float>(shadow_n);
     // Every initialisation goes through the handle's (non-blocking) stream: a plain cudaMemset runs on
     // the legacy stream, which does NOT order against m->st, and could land after the first upload or
     // after the ones-column fill below (an intermittent wrong bias gradient, seen in bitwise tests).
     MOSES_CUDA(cudaMemsetAsync(m->w, 0, P * 4, m->st));
     MOSES_CUDA(cudaMemsetAsync(m->mom, 0, P * 4, m->st));
     MOSES_CUDA(cudaMemsetAsync(m->g, 0, P * 4, m->st));
-    if (m->wbf) MOSES_CUDA(cudaMemsetAsync(m->wbf, 0, P * 2, m->st));
-    if (m->wtf) MOSES_CUDA(cudaMemsetAsync(m->wtf, 0, 4 * (twin == 2 ? 2 * shadow_lo_offset(P) : P), m->st));
+    if (m->wbf) MOSES_CUDA(cudaMemsetAsync(m->wbf, 0, shadow_n * 2, m->st));
+    if (m->wtf) MOSES_CUDA(cudaMemsetAsync(m->wtf, 0, shadow_n * 4, m->st));
     const int vec = 16 / m->esz;
     int maxw = 0;
     for (int l = 0; l < m->L; ++l) {
@@ -943,8 +1035,12 @@ static void predict_impl(moses_model* m, const double* x, long long n, int D, do
     upload_rows(m, x + r * D, c, 0);
     dispatch_forward(m, m->act[0], m->ld[0], c, nullptr, penult);
     if (penult) {
-      if (m->esz == 2) unpack_rows<__nv_bfloat16>(static_cast<__nv_bfloat16*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging, m->st);
-      else unpack_rows<float>(static_cast<float*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging, m->st);
+      if (m->esz == 2)
+        unpack_rows<__nv_bfloat16>(static_cast<__nv_bfloat16*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging,
+                                   m->st, m->act_lo_t<__nv_bfloat16>(m->L - 1));
+      else
+        unpack_rows<float>(static_cast<float*>(m->act[m->L - 1]), c, W, m->ld[m->L - 1], m->staging, m->st,
+                           m->act_lo_t<float>(m->L - 1));
       note_launch(1);
       for (long long q = 0; q < c;) {  // staging holds cap*stage_w doubles >= c*W
         const long long cc = c - q;
@@ -973,11 +1069,13 @@ MOSES_API int moses_predict_device(moses_model_t m, const void* x_dev, int32_t d
                                    float* scores_dev) {
   return guarded([&] {
     require_model(m);
-    if ((dtype == MOSES_DTYPE_BF16) != (m->esz == 2)) fail(MOSES_ERR_INVALID_ARG, "dtype must match the handle precision");
+    if ((dtype == MOSES_DTYPE_BF16) != (m->in_esz() == 2))
+      fail(MOSES_ERR_INVALID_ARG, "dtype must match the handle's input type (bf16 for bf16 handles, else fp32)");
     for (long long r = 0; r < n;) {
       const long long c = std::min(n - r, m->cap);
-      const void* x0 = static_cast<const uint8_t*>(x_dev) + r * ldx * m->esz;
-      dispatch_forward(m, x0, ldx, c, nullptr, false);
+      long long ld0 = 0;
+      const void* x0 = stage_device_rows(m, static_cast<const uint8_t*>(x_dev) + r * ldx * m->in_esz(), ldx, c, &ld0);
+      dispatch_forward(m, x0, ld0, c, nullptr, false);
       head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, scores_dev + r, m->st);
       note_launch(1);
       r += c;
@@ -1077,7 +1175,9 @@ MOSES_API int moses_gradients_device(moses_model_t m, const void* x_dev, int64_t
   return guarded([&] {
     require_model(m);
     check_rows(m, n);
-    gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0);
+    long long ld0 = 0;
+    const void* x0 = stage_device_rows(m, x_dev, ldx, n, &ld0);
+    gradients_core(m, x0, ld0, y_dev, n, nullptr, 0.0);
     if (loss_out) {
       MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
       MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -1204,7 +1304,8 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
                                        int64_t n_batches, int64_t batch, double lr, double mu, int32_t with_update) {
   return guarded([&] {
     require_model(m);
-    if (m->split) fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
+    if (m->split && !m->bsplit())
+      fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
     check_rows(m, batch);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1) fail(MOSES_ERR_INVALID_ARG, "n_batches must be >= 1");
@@ -1215,18 +1316,22 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
       }
     if (!m->dcounter) m->dcounter = dalloc<long long>(1);
     MOSES_CUDA(cudaMemsetAsync(m->dcounter, 0, sizeof(long long), m->st));
-    const long long row_bytes = ldx * m->esz;
+    const long long row_bytes = ldx * m->in_esz();
     auto body = [&] {
-      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
+      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st,
+                   m->act_lo(0));
       const SgdFuse fz{float(lr), float(mu), m->dcounter};
       const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0, nullptr,
                                         with_update ? &fz : nullptr);
-      if (with_update && !fused)
+      if (with_update && !fused) {
         sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+        m->post_update();
+      }
       if (!fz.folded) advance_counter(m->dcounter, m->st);
     };
     {  // eager warm-up without the update (configures kernels, validates shapes; params untouched)
-      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st);
+      gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st,
+                   m->act_lo(0));
       gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
     }
     MOSES_CUDA(cudaStreamSynchronize(m->st));
@@ -1259,7 +1364,8 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
                                               int64_t rows_pad, double lr, double mu, int32_t with_update) {
   return guarded([&] {
     require_model(m);
-    if (m->split) fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
+    if (m->split && !m->bsplit())
+      fail(MOSES_ERR_INVALID_ARG, "training graphs are not available for FP32 (3xTF32) handles");
     check_rows(m, rows_pad);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1 || batch_programs < 1) fail(MOSES_ERR_INVALID_ARG, "empty batch plan");
@@ -1271,7 +1377,8 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     if (!m->dcounter) m->dcounter = dalloc<long long>(1);
     if (!m->pcounter) m->pcounter = dalloc<long long>(1);
     if (!m->alt.act) {
-      m->alt.act = dalloc<uint8_t>(size_t(m->cap) * m->ld[0] * m->esz);
+      m->alt.act = dalloc<uint8_t>(size_t(m->cap) * m->ld[0] * m->esz * (m->split ? 2 : 1));
+      MOSES_CUDA(cudaMemsetAsync(m->alt.act, 0, size_t(m->cap) * m->ld[0] * m->esz * (m->split ? 2 : 1), m->st));
       m->alt.labels = dalloc<float>(m->cap);
       m->alt.seg_off = dalloc<long long>(m->cap + 1);
       m->alt.seg_rows = dalloc<int>(m->cap);
@@ -1279,13 +1386,13 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     if (!m->st3) MOSES_CUDA(cudaStreamCreateWithFlags(&m->st3, cudaStreamNonBlocking));
     if (!m->pf_fork) MOSES_CUDA(cudaEventCreateWithFlags(&m->pf_fork, cudaEventDisableTiming));
     if (!m->pf_join) MOSES_CUDA(cudaEventCreateWithFlags(&m->pf_join, cudaEventDisableTiming));
-    const long long row_bytes = ldx * m->esz;
+    const long long row_bytes = ldx * m->in_esz();
     const auto* po = reinterpret_cast<const long long*>(prog_off_dev);
     const moses_model::BatchBuf bufA{m->act[0], m->labels, m->seg_off, m->seg_rows};
     const moses_model::BatchBuf bufs[2] = {bufA, m->alt};
     auto gather_into = [&](const moses_model::BatchBuf& b, cudaStream_t st) {
       gather_pooled(x_base, row_bytes, y_base, po, m->pcounter, n_batches, batch_programs, rows_pad, b.act, b.labels,
-                    b.seg_off, b.seg_rows, st);
+                    b.seg_off, b.seg_rows, st, const_cast<void*>(m->x0_lo(b.act)));
     };
     // eager warm-up (lazy workspaces, kernel attributes) on both buffers; parameters untouched
     MOSES_CUDA(cudaMemsetAsync(m->pcounter, 0, sizeof(long long), m->st));
@@ -1307,8 +1414,10 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
       const SgdFuse fz{float(lr), float(mu)};
       const bool fused = gradients_core(m, c.act, m->ld[0], c.labels, batch_programs, nullptr, 0.0, &pool,
                                         with_update ? &fz : nullptr);
-      if (with_update && !fused)
+      if (with_update && !fused) {
         sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+        m->post_update();
+      }
       MOSES_CUDA(cudaStreamWaitEvent(m->st, m->pf_join, 0));
     };
     auto capture = [&](std::initializer_list<int> seq, cudaGraphExec_t* out) -> long long {
@@ -1357,7 +1466,7 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
                                             double mu, double* loss_out) {
   return guarded([&] {
     require_model(m);
-    if (m->esz != 2) fail(MOSES_ERR_INVALID_ARG, "the asynchronous pooled step needs a bf16 handle");
+    if (m->esz != 2) fail(MOSES_ERR_INVALID_ARG, "the asynchronous pooled step needs a bf16 or split-bf16 handle");
     if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "statement feature width != model input width");
     if (programs < 1 || offsets[0] != 0 || offsets[programs] != n_stmt)
       fail(MOSES_ERR_SHAPE_MISMATCH, "offsets must span the statement rows");
@@ -1398,16 +1507,18 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
       a.dims_host[1] = programs;
       MOSES_CUDA(cudaMemcpyAsync(a.dims, a.dims_host, 2 * sizeof(long long), cudaMemcpyHostToDevice, m->st));
       pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0],
-                                 m->labels, m->seg_off, m->seg_rows, m->st);
+                                 m->labels, m->seg_off, m->seg_rows, m->st, m->act_lo_t<__nv_bfloat16>(0));
       gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, nullptr);
       cudaGraph_t graph;
       MOSES_CUDA(cudaStreamSynchronize(m->st));
       MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
       try {
         pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]),
-                                   m->ld[0], m->labels, m->seg_off, m->seg_rows, m->st);
-        if (!gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, &fz))
+                                   m->ld[0], m->labels, m->seg_off, m->seg_rows, m->st, m->act_lo_t<__nv_bfloat16>(0));
+        if (!gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, &fz)) {
           sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
+          m->post_update();
+        }
         if (!fz.folded) store_scalar_f64(m->dscal, a.box_dev, m->st);
       } catch (...) {
         cudaStreamEndCapture(m->st, &graph);
@@ -1509,7 +1620,9 @@ MOSES_API int moses_train_step_device(moses_model_t m, const void* x_dev, int64_
     require_model(m);
     check_rows(m, n);
     const SgdFuse fz{float(lr), float(mu)};
-    if (!gradients_core(m, x_dev, ldx, y_dev, n, nullptr, 0.0, nullptr, &fz)) {
+    long long ld0 = 0;
+    const void* x0 = stage_device_rows(m, x_dev, ldx, n, &ld0);
+    if (!gradients_core(m, x0, ld0, y_dev, n, nullptr, 0.0, nullptr, &fz)) {
       ProfScope ps(P_UPDATE, m->st);
       sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
       m->post_update();
@@ -1855,10 +1968,12 @@ MOSES_API int moses_adversarial_step(moses_adversary_t a, moses_model_t m, const
     dispatch_forward(m, m->act[0], m->ld[0], a->m + n, a->u, true);
     if (m->esz == 2)
       adversary_step<__nv_bfloat16>(m->head_part2, m->last_tiles, m->cap, static_cast<__nv_bfloat16*>(m->act[m->L - 1]),
-                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st,
+                                    m->act_lo_t<__nv_bfloat16>(m->L - 1));
     else
       adversary_step<float>(m->head_part2, m->last_tiles, m->cap, static_cast<float*>(m->act[m->L - 1]),
-                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st,
+                            m->act_lo_t<float>(m->L - 1));
     note_launch(3);
     double l = 0;
     MOSES_CUDA(cudaMemcpyAsync(&l, m->dscal + 2, 8, cudaMemcpyDeviceToHost, m->st));
@@ -2090,10 +2205,12 @@ MOSES_API int moses_moses_step(moses_model_t m, moses_adversary_t a, const doubl
     }
     if (m->esz == 2)
       adversary_step<__nv_bfloat16>(m->head_part2, m->last_tiles, m->cap, static_cast<__nv_bfloat16*>(m->act[m->L - 1]),
-                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+                                    m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st,
+                                    m->act_lo_t<__nv_bfloat16>(m->L - 1));
     else
       adversary_step<float>(m->head_part2, m->last_tiles, m->cap, static_cast<float*>(m->act[m->L - 1]),
-                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st);
+                            m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st,
+                            m->act_lo_t<float>(m->L - 1));
     note_launch(2);
     double sc[3] = {0, 0, 0};
     MOSES_CUDA(cudaMemcpyAsync(sc, m->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, m->st));
@@ -2451,19 +2568,19 @@ void plan_reserve(moses_model* m, long long total, long long nb) {
   }
   if (!ps.counter) ps.counter = dalloc<long long>(1);
   if (!ps.loss_sum) ps.loss_sum = dalloc<double>(1);
-  if (m->split && !ps.stage) ps.stage = dalloc<float>(m->cap * m->ld[0]);
+  if (m->split && !m->bsplit() && !ps.stage) ps.stage = dalloc<float>(m->cap * m->ld[0]);
 }
 // one step over plan batch *counter (n rows): gather -> gradients -> momentum update -> loss sum
 void plan_step(moses_model* m, const void* x, long long ldx, const float* y, long long n, float lr, float mu) {
   auto& ps = m->plan;
-  const long long row_bytes = ldx * m->esz;
-  if (m->split) {  // 3xTF32 operands: hi/lo split of the gathered fp32 rows
+  const long long row_bytes = ldx * m->in_esz();
+  if (m->split && !m->bsplit()) {  // 3xTF32 operands: hi/lo split of the gathered fp32 rows
     gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, ps.stage, m->labels, m->st);
     pack_rows_f32<float>(ps.stage, n, m->dims[0], ldx, static_cast<float*>(m->act[0]), m->ld[0], m->st,
-                         m->act_lo(0));
+                         m->act_lo_t<float>(0));
     note_launch(1);
-  } else {
-    gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st);
+  } else {  // split-bf16 handles split the gathered fp32 rows into their hi/lo planes in the gather
+    gather_plan(x, row_bytes, y, ps.rows, ps.off, ps.counter, n, m->act[0], m->labels, m->st, m->act_lo(0));
   }
   const SgdFuse fz{lr, mu, ps.counter, m->dscal, ps.loss_sum};
   if (!gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, &fz)) {
@@ -2482,7 +2599,7 @@ void plan_step(moses_model* m, const void* x, long long ldx, const float* y, lon
 // needs the plan's rows on the device (the warm-up gathers batch 0's slots)
 bool plan_graph(moses_model* m, const void* x, long long ldx, const float* y, const PlanShape& sh, float lr, float mu) {
   auto& ps = m->plan;
-  if (m->split || sh.nfull < 4) return false;
+  if ((m->split && !m->bsplit()) || sh.nfull < 4) return false;
   if (ps.exec && ps.x == x && ps.y == y && ps.ldx == ldx && ps.batch == sh.B && ps.lr == lr && ps.mu == mu) return true;
   if (ps.exec) {
     cudaGraphExecDestroy(ps.exec);
@@ -2490,7 +2607,7 @@ bool plan_graph(moses_model* m, const void* x, long long ldx, const float* y, co
   }
   // eager warm-up without the update (configures kernels; parameters untouched)
   MOSES_CUDA(cudaMemsetAsync(ps.counter, 0, sizeof(long long), m->st));
-  gather_plan(x, ldx * m->esz, y, ps.rows, ps.off, ps.counter, sh.B, m->act[0], m->labels, m->st);
+  gather_plan(x, ldx * m->in_esz(), y, ps.rows, ps.off, ps.counter, sh.B, m->act[0], m->labels, m->st, m->act_lo(0));
   gradients_core(m, m->act[0], m->ld[0], m->labels, sh.B, nullptr, 0.0);
   MOSES_CUDA(cudaStreamSynchronize(m->st));
   const long long before = moses_kernel_launches();
@@ -2705,20 +2822,20 @@ MOSES_API int moses_pretrain(moses_model_t m, int32_t n_tasks, const char* const
       dfree(Y);
     };
     try {
-      X = dalloc<uint8_t>(size_t(n_records) * ld * m->esz);
+      X = dalloc<uint8_t>(size_t(n_records) * ld * m->in_esz());
       V = dalloc<long long>(size_t(n_records) * n_knobs);
       Y = dalloc<float>(size_t(n_records));
       MOSES_CUDA(cudaMemcpyAsync(V, vals_g.data(), sizeof(long long) * vals_g.size(), cudaMemcpyHostToDevice, m->st));
       MOSES_CUDA(cudaMemcpyAsync(Y, lab_g.data(), sizeof(float) * lab_g.size(), cudaMemcpyHostToDevice, m->st));
-      MOSES_CUDA(cudaMemsetAsync(X, 0, size_t(n_records) * ld * m->esz, m->st));
-      const int kind = m->esz == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32;
+      MOSES_CUDA(cudaMemsetAsync(X, 0, size_t(n_records) * ld * m->in_esz(), m->st));
+      const int kind = m->in_esz() == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32;
       for (int t : order) {
         long long bad = -1;
         const long long cnt = (long long)rows[t].size();
         try {
           note_launch(encode_values(task4 + 4 * t, reinterpret_cast<const long long*>(domains), domain_sizes, roles,
                                     n_knobs, V + first[t] * n_knobs, cnt, kind,
-                                    static_cast<uint8_t*>(X) + first[t] * ld * m->esz, ld, m->dims[0], nullptr,
+                                    static_cast<uint8_t*>(X) + first[t] * ld * m->in_esz(), ld, m->dims[0], nullptr,
                                     nullptr, &bad, m->st));
         } catch (const Status& e) {
           if (bad >= 0)  // report the caller's record index

@@ -95,6 +95,11 @@ struct ChainCall {
   float* head_part2 = nullptr;
   long long head_ld = 0;
   unsigned long long* trace = nullptr;
+  // split-bf16 operands (mlp_chain_split.cuh): lo planes of the input, the weights and the outputs
+  bool split = false;
+  const void* in_lo = nullptr;
+  const void* w_lo[8] = {};
+  void* out_lo[8] = {};
 };
 void launch_chain(const ChainCall& c, cudaStream_t s);
 
@@ -111,6 +116,11 @@ struct WgradGroupCall {
   float* w[8] = {};
   float* mom[8] = {};
   void* shadow[8] = {};
+  // split-bf16 operands (MOSES_PREC_BF16X3): lo planes of a / b and the lo half of the shadow
+  bool split = false;
+  const void* a_lo[8] = {};
+  const void* b_lo[8] = {};
+  void* shadow_lo[8] = {};
   float lr = 0.f, mu = 0.f;
   bool update = false;
   long long* counter = nullptr;

@@ -12,6 +12,7 @@
 #include "gemm_cluster.cuh"
 #include "gemm_split.cuh"
 #include "mlp_chain.cuh"
+#include "mlp_chain_split.cuh"
 #include "gemm_group.cuh"
 
 namespace moses {
@@ -335,14 +336,15 @@ void launch_chain_t(const ChainCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
 }
 
-template <bool UPDATE>
+template <bool UPDATE, bool SPLIT>
 void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
-  auto kern = wgrad_group_kernel<UPDATE>;
+  using Cfg = GroupCfgT<SPLIT>;
+  auto kern = wgrad_group_kernel<UPDATE, SPLIT>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GroupCfg::kSmemBytes));
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
   });
-  GroupMaps maps;
+  GroupMapsSplit maps;
   GroupArgs a{};
   a.n = c.n;
   a.K = c.K;
@@ -350,6 +352,13 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   for (int l = 0; l < c.n; ++l) {
     maps.a[l] = make_map(c.a[l], 2, c.M[l], c.K, c.lda[l], 64, 64);
     maps.b[l] = make_map(c.b[l], 2, c.N[l], c.K, c.ldb[l], 64, 64);
+    if constexpr (SPLIT) {
+      if (!c.a_lo[l] || !c.b_lo[l] || (UPDATE && !c.shadow_lo[l]))
+        fail(MOSES_ERR_INVALID_ARG, "split grouped wgrad needs the lo planes");
+      maps.a_lo[l] = make_map(c.a_lo[l], 2, c.M[l], c.K, c.lda[l], 64, 64);
+      maps.b_lo[l] = make_map(c.b_lo[l], 2, c.N[l], c.K, c.ldb[l], 64, 64);
+      a.shadow_lo[l] = static_cast<__nv_bfloat16*>(c.shadow_lo[l]);
+    }
     a.tile_begin[l] = tiles;
     a.tiles_n[l] = ceil_div(c.N[l], GroupCfg::BN);
     a.M[l] = c.M[l];
@@ -370,7 +379,7 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = GroupCfg::kSmemBytes;
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -508,12 +517,72 @@ int g_rank_fused = 1;
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
   if (c.K <= 0 || c.n <= 0) return;
   if (c.n > kGroupMax) fail(MOSES_ERR_INVALID_ARG, "too many levels for the grouped wgrad");
-  if (c.update) launch_group_t<true>(c, s);
-  else launch_group_t<false>(c, s);
+  if (c.split) {
+    if (c.update) launch_group_t<true, true>(c, s);
+    else launch_group_t<false, true>(c, s);
+  } else {
+    if (c.update) launch_group_t<true, false>(c, s);
+    else launch_group_t<false, false>(c, s);
+  }
 }
+template <bool FWD>
+void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
+  auto kern = mlp_chain_split_kernel<FWD>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainSplitCfg::kSmemBytes));
+  });
+  if (c.in_lo == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain needs the input lo plane");
+  ChainSplitMaps maps;
+  ChainArgs a{};
+  a.M = c.M;
+  a.n_layers = c.n_layers;
+  maps.in = make_map(c.in, 2, c.K[0], c.M, c.ld_in, 64, 128);
+  maps.in_lo = make_map(c.in_lo, 2, c.K[0], c.M, c.ld_in, 64, 128);
+  constexpr int W = ChainSplitCfg::kWidth;
+  for (int l = 0; l < c.n_layers; ++l) {
+    a.K[l] = c.K[l];
+    a.bias[l] = c.bias[l];
+    a.out[l] = static_cast<__nv_bfloat16*>(c.out[l]);
+    a.out_lo[l] = static_cast<__nv_bfloat16*>(c.out_lo[l]);
+    a.ldo[l] = c.ldo[l];
+    a.mask[l] = static_cast<const __nv_bfloat16*>(c.mask[l]);
+    a.ldm[l] = c.ldm[l];
+    if (c.w_lo[l] == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain needs the weight lo planes");
+    maps.w[l] = FWD ? make_map(c.w[l], 2, W, c.K[l], W, 64, 64) : make_map(c.w[l], 2, W, W, W, 64, 128);
+    maps.w_lo[l] = FWD ? make_map(c.w_lo[l], 2, W, c.K[l], W, 64, 64) : make_map(c.w_lo[l], 2, W, W, W, 64, 128);
+    if (c.out[l] != nullptr) {
+      if (c.out_lo[l] == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain output without a lo plane");
+      maps.out[l] = make_map(c.out[l], 2, W, c.M, c.ldo[l], 64, 128);
+      maps.out_lo[l] = make_map(c.out_lo[l], 2, W, c.M, c.ldo[l], 64, 128);
+    }
+  }
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ChainSplitCfg::kCluster * ceil_div(c.M, ChainSplitCfg::BM));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = ChainSplitCfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+}
+
 void launch_chain(const ChainCall& c, cudaStream_t s) {
   if (c.M <= 0) return;
   if (c.n_layers < 1 || c.n_layers > kChainMaxLayers) fail(MOSES_ERR_INVALID_ARG, "chain depth");
+  if (c.split) {
+    if (c.fwd) launch_chain_split_t<true>(c, s);
+    else launch_chain_split_t<false>(c, s);
+    return;
+  }
   if (c.fwd) launch_chain_t<true>(c, s);
   else launch_chain_t<false>(c, s);
 }

@@ -23,6 +23,11 @@ struct GroupMaps {
   CUtensorMap a[kGroupMax];  // act_l  [K rows][ld] (MN-major view, M = dims_l + 1 incl. the ones column)
   CUtensorMap b[kGroupMax];  // dZ_l+1 [K rows][ld] (MN-major view)
 };
+// SPLIT (MOSES_PREC_BF16X3): the lo planes of both operands; G = A_hi B_hi + A_hi B_lo + A_lo B_hi
+struct GroupMapsSplit : GroupMaps {
+  CUtensorMap a_lo[kGroupMax];
+  CUtensorMap b_lo[kGroupMax];
+};
 
 struct GroupArgs {
   int n;                       // levels
@@ -34,6 +39,7 @@ struct GroupArgs {
   float* w[kGroupMax];         // UPDATE: parameters / momentum / bf16 shadow of the same block
   float* mom[kGroupMax];
   __nv_bfloat16* shadow[kGroupMax];
+  __nv_bfloat16* shadow_lo[kGroupMax];  // SPLIT: lo half of the operand shadow (hi + lo = w to 2^-18)
   float lr, mu;
   long long* counter;      // optional: step counter advanced once (training graphs' batch index)
   const double* loss_src;  // optional: *loss_acc += *loss_src once (epoch loss sum)
@@ -41,18 +47,20 @@ struct GroupArgs {
   double* loss_copy;       // optional: *loss_copy = *loss_src once (per-step loss mailbox)
 };
 
-struct GroupCfg {
+template <bool SPLIT = false>
+struct GroupCfgT {
   static constexpr int BM = 128, BN = 64, BK = 64;
   static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = 9;
+  static constexpr int kStageBytes = (SPLIT ? 2 : 1) * (kABytes + kBBytes);  // [A_hi B_hi (A_lo B_lo)]
+  static constexpr int kStages = SPLIT ? 4 : 9;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
+using GroupCfg = GroupCfgT<false>;
 
-template <bool UPDATE>
+template <bool UPDATE, bool SPLIT = false>
 __global__ void __launch_bounds__(128, 1)
-    wgrad_group_kernel(const __grid_constant__ GroupMaps maps, const __grid_constant__ GroupArgs args) {
-  using C = GroupCfg;
+    wgrad_group_kernel(const __grid_constant__ GroupMapsSplit maps, const __grid_constant__ GroupArgs args) {
+  using C = GroupCfgT<SPLIT>;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::kStages;
   constexpr uint32_t kIdesc = ptx::umma_idesc(1 /*BF16*/, true, true, BM, BN);
 
@@ -72,6 +80,8 @@ __global__ void __launch_bounds__(128, 1)
   const int M = args.M[lev], N = args.N[lev];
   const CUtensorMap* tmA = &maps.a[lev];
   const CUtensorMap* tmB = &maps.b[lev];
+  const CUtensorMap* tmAl = &maps.a_lo[lev];
+  const CUtensorMap* tmBl = &maps.b_lo[lev];
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const int num_kb = (args.K + BK - 1) / BK;
@@ -79,6 +89,10 @@ __global__ void __launch_bounds__(128, 1)
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(tmA);
     ptx::tma_prefetch_desc(tmB);
+    if constexpr (SPLIT) {
+      ptx::tma_prefetch_desc(tmAl);
+      ptx::tma_prefetch_desc(tmBl);
+    }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
@@ -111,6 +125,13 @@ __global__ void __launch_bounds__(128, 1)
         ptx::tma_load_2d(sa, tmA, &full_bar[stage], m0, k0);
         ptx::tma_load_2d(sa + BK * 128, tmA, &full_bar[stage], m0 + 64, k0);
         ptx::tma_load_2d(sb, tmB, &full_bar[stage], n0, k0);
+        if constexpr (SPLIT) {
+          uint8_t* sal = sb + C::kBBytes;
+          uint8_t* sbl = sal + C::kABytes;
+          ptx::tma_load_2d(sal, tmAl, &full_bar[stage], m0, k0);
+          ptx::tma_load_2d(sal + BK * 128, tmAl, &full_bar[stage], m0 + 64, k0);
+          ptx::tma_load_2d(sbl, tmBl, &full_bar[stage], n0, k0);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -129,6 +150,13 @@ __global__ void __launch_bounds__(128, 1)
           const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, BK * 128, 1024, 2);
           const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, BK * 128, 1024, 2);
           ptx::umma_f16(tmem_base, ad, bd, kIdesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (SPLIT) {
+            const uint32_t sal = sb + C::kBBytes, sbl = sal + C::kABytes;
+            const uint64_t adl = ptx::sw128_desc(sal + kk * 2048, BK * 128, 1024, 2);
+            const uint64_t bdl = ptx::sw128_desc(sbl + kk * 2048, BK * 128, 1024, 2);
+            ptx::umma_f16(tmem_base, ad, bdl, kIdesc, 1u);
+            ptx::umma_f16(tmem_base, adl, bd, kIdesc, 1u);
+          }
         }
         ptx::umma_commit(&empty_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -161,6 +189,7 @@ __global__ void __launch_bounds__(128, 1)
   float* __restrict__ w = args.w[lev];
   float* __restrict__ v = args.mom[lev];
   __nv_bfloat16* __restrict__ sh = args.shadow[lev];
+  __nv_bfloat16* __restrict__ shl = args.shadow_lo[lev];
   auto upd = [&](float gv, float vi0, float wi0, float& vi, float& wi) {
     vi = __fadd_rn(__fmul_rn(args.mu, vi0), gv);
     wi = __fsub_rn(wi0, __fmul_rn(args.lr, vi));
@@ -206,6 +235,14 @@ __global__ void __launch_bounds__(128, 1)
           pk.x = *reinterpret_cast<uint32_t*>(&p0);
           pk.y = *reinterpret_cast<uint32_t*>(&p1);
           *reinterpret_cast<uint2*>(sh + e[u]) = pk;
+          if constexpr (SPLIT) {
+            __nv_bfloat162 l0 = __floats2bfloat162_rn(wo.x - __low2float(p0), wo.y - __high2float(p0));
+            __nv_bfloat162 l1 = __floats2bfloat162_rn(wo.z - __low2float(p1), wo.w - __high2float(p1));
+            uint2 pl;
+            pl.x = *reinterpret_cast<uint32_t*>(&l0);
+            pl.y = *reinterpret_cast<uint32_t*>(&l1);
+            *reinterpret_cast<uint2*>(shl + e[u]) = pl;
+          }
         }
       }
     }
@@ -222,6 +259,7 @@ __global__ void __launch_bounds__(128, 1)
         v[e] = vi;
         w[e] = wi;
         sh[e] = __float2bfloat16_rn(wi);
+        if constexpr (SPLIT) shl[e] = __float2bfloat16_rn(wi - __bfloat162float(sh[e]));
       }
     }
   }

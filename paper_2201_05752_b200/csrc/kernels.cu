@@ -35,9 +35,14 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 // operand shadow of the master parameters: 0 none, 1 bf16, 2 tf32-rounded fp32
 template <int KIND>
-__device__ __forceinline__ void store_shadow(void* sh, long long i, float w) {
+__device__ __forceinline__ void store_shadow(void* sh, long long i, float w, long long lo_off = 0) {
   if constexpr (KIND == 1) static_cast<__nv_bfloat16*>(sh)[i] = __float2bfloat16_rn(w);
   if constexpr (KIND == 2) static_cast<float*>(sh)[i] = tf32_rna(w);
+  if constexpr (KIND == 4) {  // split bf16: hi = rn(w), lo = rn(w - hi)
+    const __nv_bfloat16 h = __float2bfloat16_rn(w);
+    static_cast<__nv_bfloat16*>(sh)[i] = h;
+    static_cast<__nv_bfloat16*>(sh)[i + lo_off] = __float2bfloat16_rn(w - __bfloat162float(h));
+  }
 }
 
 int grid_for(long long n, int block, int per_sm = 8) {
@@ -47,15 +52,21 @@ int grid_for(long long n, int block, int per_sm = 8) {
 
 // ---------------------------------------------------------------- data movement
 // 3xTF32 operands (fp32 parity mode): hi = rna_tf32(v) in dst, lo = rna_tf32(v - hi) in lo.
+// Split operands: lo = the residual rounded to the same operand type (tf32 for 3xTF32, bf16 for
+// split bf16), so hi + lo carries 2x the operand precision.
 template <typename T>
-__device__ __forceinline__ void store_operand(T* dst, float* lo, long long i, float v) {
+__device__ __forceinline__ void store_operand(T* dst, T* lo, long long i, float v) {
   const T h = from_f<T>(v);
   dst[i] = h;
-  if (lo != nullptr) lo[i] = tf32_rna(v - to_f(h));
+  if (lo != nullptr) lo[i] = from_f<T>(v - to_f(h));
+}
+template <typename T>
+__device__ __forceinline__ float load_operand(const T* src, const T* lo, long long i) {
+  return lo != nullptr ? to_f(src[i]) + to_f(lo[i]) : to_f(src[i]);
 }
 template <typename T>
 __global__ void pack_rows_kernel(const double* __restrict__ src, long long n, int D, T* __restrict__ dst, long long ld,
-                                 float* __restrict__ lo) {
+                                 T* __restrict__ lo) {
   ptx::pdl_launch_dependents();
   const long long total = n * ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -67,7 +78,7 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, long long n, in
 }
 template <typename T>
 __global__ void pack_rows_f32_kernel(const float* __restrict__ src, long long n, int D, long long lds, T* __restrict__ dst,
-                                     long long ld, float* __restrict__ lo) {
+                                     long long ld, T* __restrict__ lo) {
   const long long total = n * ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / ld;
@@ -82,12 +93,13 @@ __global__ void set_col_kernel(T* act, long long rows, int col, long long ld) {
     act[r * ld + col] = from_f<T>(1.f);
 }
 template <typename T>
-__global__ void unpack_rows_kernel(const T* __restrict__ src, long long n, int W, long long ld, double* __restrict__ dst) {
+__global__ void unpack_rows_kernel(const T* __restrict__ src, long long n, int W, long long ld, double* __restrict__ dst,
+                                   const T* __restrict__ lo) {
   const long long total = n * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / W;
     const int c = int(i - r * W);
-    dst[i] = double(to_f(src[r * ld + c]));
+    dst[i] = lo != nullptr ? double(to_f(src[r * ld + c])) + double(to_f(lo[r * ld + c])) : double(to_f(src[r * ld + c]));
   }
 }
 __global__ void f32_to_f64_kernel(const float* s, long long n, double* d) {
@@ -122,16 +134,35 @@ __global__ void row_dot_kernel(const float* __restrict__ H, long long ldh, long 
 }
 
 // ---------------------------------------------------------------- device-resident batch gather (graph replay)
+// Every gather moves 16-byte chunks of packed rows. With a lo plane (split-bf16 handles) the dataset
+// rows are fp32 and chunk i (4 values) lands as 4 bf16 hi values at dst[4i..] and 4 bf16 lo values
+// at lo[4i..] (lo = rn(v - hi)).
+__device__ __forceinline__ void put_chunk(uint8_t* __restrict__ dst, uint8_t* __restrict__ lo, long long i, uint4 v) {
+  if (lo == nullptr) {
+    reinterpret_cast<uint4*>(dst)[i] = v;
+    return;
+  }
+  const float f[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(f[0], f[1]), h1 = __floats2bfloat162_rn(f[2], f[3]);
+  const __nv_bfloat162 l0 = __floats2bfloat162_rn(f[0] - __low2float(h0), f[1] - __high2float(h0));
+  const __nv_bfloat162 l1 = __floats2bfloat162_rn(f[2] - __low2float(h1), f[3] - __high2float(h1));
+  uint2 hv, lv;
+  hv.x = *reinterpret_cast<const uint32_t*>(&h0);
+  hv.y = *reinterpret_cast<const uint32_t*>(&h1);
+  lv.x = *reinterpret_cast<const uint32_t*>(&l0);
+  lv.y = *reinterpret_cast<const uint32_t*>(&l1);
+  reinterpret_cast<uint2*>(dst)[i] = hv;
+  reinterpret_cast<uint2*>(lo)[i] = lv;
+}
 __global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
                                     const long long* __restrict__ counter, long long nb, long long batch,
-                                    uint8_t* __restrict__ dst, float* __restrict__ ydst) {
+                                    uint8_t* __restrict__ dst, float* __restrict__ ydst, uint8_t* __restrict__ dlo) {
   ptx::pdl_launch_dependents();
   const long long b = (*counter) % nb;
   const uint4* src = reinterpret_cast<const uint4*>(x_base + b * batch * row_bytes);
-  uint4* d = reinterpret_cast<uint4*>(dst);
   const long long n16 = batch * row_bytes / 16;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
-    d[i] = src[i];
+    put_chunk(dst, dlo, i, src[i]);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < batch; i += (long long)gridDim.x * blockDim.x)
     ydst[i] = y_base[b * batch + i];
 }
@@ -140,7 +171,7 @@ __global__ void gather_batch_kernel(const uint8_t* __restrict__ x_base, long lon
 __global__ void gather_plan_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
                                    const long long* __restrict__ rows, const long long* __restrict__ off,
                                    const long long* __restrict__ counter, long long n, uint8_t* __restrict__ dst,
-                                   float* __restrict__ ydst) {
+                                   float* __restrict__ ydst, uint8_t* __restrict__ dlo) {
   ptx::pdl_launch_dependents();
   const long long base = off[*counter];
   const int lane = threadIdx.x & 31;
@@ -149,8 +180,7 @@ __global__ void gather_plan_kernel(const uint8_t* __restrict__ x_base, long long
        r += ((long long)gridDim.x * blockDim.x) >> 5) {
     const long long src_row = rows[base + r];
     const uint4* src = reinterpret_cast<const uint4*>(x_base + src_row * row_bytes);
-    uint4* d = reinterpret_cast<uint4*>(dst + r * row_bytes);
-    for (long long c = lane; c < w16; c += 32) d[c] = src[c];
+    for (long long c = lane; c < w16; c += 32) put_chunk(dst, dlo, r * w16 + c, src[c]);
     if (lane == 0) ydst[r] = y_base[src_row];
   }
 }
@@ -160,15 +190,15 @@ __global__ void accum_f64_kernel(const double* __restrict__ src, double* __restr
 __global__ void gather_pooled_kernel(const uint8_t* __restrict__ x_base, long long row_bytes, const float* __restrict__ y_base,
                                      const long long* __restrict__ prog_off, const long long* __restrict__ counter,
                                      long long nb, long long B, long long rows_pad, uint8_t* __restrict__ dst,
-                                     float* __restrict__ ydst, long long* __restrict__ seg_off, int* __restrict__ seg_rows) {
+                                     float* __restrict__ ydst, long long* __restrict__ seg_off, int* __restrict__ seg_rows,
+                                     uint8_t* __restrict__ dlo) {
   ptx::pdl_launch_dependents();
   const long long b = (*counter) % nb;
   const long long p0 = b * B, r0 = prog_off[p0], Rb = prog_off[p0 + B] - r0;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
   const uint4* src = reinterpret_cast<const uint4*>(x_base + r0 * row_bytes);
-  uint4* d = reinterpret_cast<uint4*>(dst);
   const long long n16 = Rb * row_bytes / 16;
-  for (long long i = tid; i < n16; i += nthr) d[i] = src[i];
+  for (long long i = tid; i < n16; i += nthr) put_chunk(dst, dlo, i, src[i]);
   for (long long p = tid; p <= B; p += nthr) {
     const long long lo = prog_off[p0 + p] - r0;
     seg_off[p] = lo;
@@ -189,7 +219,7 @@ template <typename T>
 __global__ void pack_pooled_kernel(const double* __restrict__ xs, const double* __restrict__ ys,
                                    const long long* __restrict__ offs, const long long* __restrict__ dims_dev, int D,
                                    long long rows_pad, T* __restrict__ act0, long long ld, float* __restrict__ ydst,
-                                   long long* __restrict__ seg_off, int* __restrict__ seg_rows) {
+                                   long long* __restrict__ seg_off, int* __restrict__ seg_rows, T* __restrict__ lo) {
   ptx::pdl_launch_dependents();
   const long long n_stmt = dims_dev[0], programs = dims_dev[1];
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nthr = (long long)gridDim.x * blockDim.x;
@@ -197,7 +227,7 @@ __global__ void pack_pooled_kernel(const double* __restrict__ xs, const double* 
     const long long r = i / ld;
     const int c = int(i - r * ld);
     const float v = c < D ? float(xs[r * D + c]) : (c == D ? 1.f : 0.f);
-    act0[i] = from_f<T>(v);
+    store_operand(act0, lo, i, v);
   }
   for (long long p = tid; p <= programs; p += nthr) {
     seg_off[p] = offs[p];
@@ -841,7 +871,7 @@ template <typename T>
 __global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
                                      const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
                                      long long ldh, long long R, int W, T* __restrict__ dz, long long ldz,
-                                     float* __restrict__ dz_lo) {
+                                     T* __restrict__ dz_lo) {
   ptx::pdl_launch_dependents();
   const long long total = R * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -890,14 +920,14 @@ __global__ void __launch_bounds__(256) head_backward_bf16x8_kernel(const float* 
 constexpr int kColSlab = 64;
 template <typename T>
 __global__ void column_dot_kernel(const float* __restrict__ coef, const T* __restrict__ H, long long ldh, long long R, int W,
-                                  float* __restrict__ part) {
+                                  float* __restrict__ part, const T* __restrict__ H_lo = nullptr) {
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
   const long long r0 = (long long)blockIdx.y * kColSlab, r1 = min(R, r0 + kColSlab);
   float acc = 0.f;
   if (j < W)
-    for (long long r = r0 + ty; r < r1; r += 8) acc = fmaf(coef[r], to_f(H[r * ldh + j]), acc);
+    for (long long r = r0 + ty; r < r1; r += 8) acc = fmaf(coef[r], load_operand(H, H_lo, r * ldh + j), acc);
   else if (j == W)
     for (long long r = r0 + ty; r < r1; r += 8) acc += coef[r];
   red[ty][tx] = acc;
@@ -925,7 +955,8 @@ __global__ void column_sum_kernel(const float* __restrict__ part, int slabs, int
 // is built with -ffp-contract=off, so v = mu*v + g and w -= lr*v round after every op)
 template <bool MOM, bool MASK, int SHADOW>
 __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
-                           const uint8_t* __restrict__ mask, long long P, float lr, float mu, void* __restrict__ shadow) {
+                           const uint8_t* __restrict__ mask, long long P, float lr, float mu, void* __restrict__ shadow,
+                           long long lo_off) {
   ptx::pdl_launch_dependents();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
     float wi = w[i];
@@ -939,7 +970,7 @@ __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const f
       }
       w[i] = wi;
     }
-    store_shadow<SHADOW>(shadow, i, wi);
+    store_shadow<SHADOW>(shadow, i, wi, lo_off);
   }
 }
 
@@ -1209,6 +1240,12 @@ __global__ void shadow_kernel3(const float* w, long long n, float* sh) {
     store_operand(sh, lo, i, w[i]);
 }
 
+// kind 4 (split bf16): hi at sh[i], lo at sh[i + lo_off]
+__global__ void shadow_kernel4(const float* w, long long n, __nv_bfloat16* sh, long long lo_off) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    store_shadow<4>(sh, i, w[i], lo_off);
+}
+
 __global__ void popcount_kernel(const uint8_t* __restrict__ mask, long long n, unsigned long long* out) {
   using Red = cub::BlockReduce<unsigned long long, kSelBlock>;
   __shared__ typename Red::TempStorage rtmp;
@@ -1423,13 +1460,13 @@ __global__ void synth_labels_kernel(unsigned long long seed, long long row0, lon
 
 // ====================================================================== host wrappers
 template <typename T>
-void pack_rows(const double* src, long long n, int D, T* dst, long long ld, cudaStream_t s, float* lo) {
+void pack_rows(const double* src, long long n, int D, T* dst, long long ld, cudaStream_t s, T* lo) {
   if (n <= 0) return;
   pack_rows_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, dst, ld, lo);
   MOSES_CUDA(cudaGetLastError());
 }
 template <typename T>
-void pack_rows_f32(const float* src, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s, float* lo) {
+void pack_rows_f32(const float* src, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s, T* lo) {
   if (n <= 0) return;
   pack_rows_f32_kernel<T><<<grid_for(n * ld, 256), 256, 0, s>>>(src, n, D, lds, dst, ld, lo);
   MOSES_CUDA(cudaGetLastError());
@@ -1441,9 +1478,9 @@ void set_ones_column(T* act, long long rows, int col, long long ld, cudaStream_t
   MOSES_CUDA(cudaGetLastError());
 }
 template <typename T>
-void unpack_rows(const T* src, long long n, int W, long long ld, double* dst, cudaStream_t s) {
+void unpack_rows(const T* src, long long n, int W, long long ld, double* dst, cudaStream_t s, const T* lo) {
   if (n <= 0) return;
-  unpack_rows_kernel<T><<<grid_for(n * W, 256), 256, 0, s>>>(src, n, W, ld, dst);
+  unpack_rows_kernel<T><<<grid_for(n * W, 256), 256, 0, s>>>(src, n, W, ld, dst, lo);
   MOSES_CUDA(cudaGetLastError());
 }
 void f32_to_f64(const float* src, long long n, double* dst, cudaStream_t s) {
@@ -1460,6 +1497,8 @@ void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s) {
   if (n <= 0 || sh.kind == 0) return;
   if (sh.kind == 1) shadow_kernel1<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
   else if (sh.kind == 2) shadow_kernel2<<<grid_for(n, 256), 256, 0, s>>>(w, n, sh.ptr);
+  else if (sh.kind == 4)
+    shadow_kernel4<<<grid_for(n, 256), 256, 0, s>>>(w, n, static_cast<__nv_bfloat16*>(sh.ptr), sh.lo_off);
   else shadow_kernel3<<<grid_for(n, 256), 256, 0, s>>>(w, n, static_cast<float*>(sh.ptr));
   MOSES_CUDA(cudaGetLastError());
 }
@@ -1470,18 +1509,20 @@ void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t
 }
 
 void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
-                  long long batch, void* dst, float* ydst, cudaStream_t s) {
+                  long long batch, void* dst, float* ydst, cudaStream_t s, void* dst_lo) {
   if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
   gather_batch_kernel<<<grid_for(batch * row_bytes / 16, 256), 256, 0, s>>>(
-      static_cast<const uint8_t*>(x_base), row_bytes, y_base, counter, nb, batch, static_cast<uint8_t*>(dst), ydst);
+      static_cast<const uint8_t*>(x_base), row_bytes, y_base, counter, nb, batch, static_cast<uint8_t*>(dst), ydst,
+      static_cast<uint8_t*>(dst_lo));
   MOSES_CUDA(cudaGetLastError());
 }
 void gather_plan(const void* x_base, long long row_bytes, const float* y_base, const long long* rows, const long long* off,
-                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s) {
+                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s, void* dst_lo) {
   if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
   gather_plan_kernel<<<std::max(1, ceil_div(n * 32, 256)), 256, 0, s>>>(static_cast<const uint8_t*>(x_base), row_bytes,
                                                                          y_base, rows, off, counter, n,
-                                                                         static_cast<uint8_t*>(dst), ydst);
+                                                                         static_cast<uint8_t*>(dst), ydst,
+                                                                         static_cast<uint8_t*>(dst_lo));
   MOSES_CUDA(cudaGetLastError());
 }
 void accum_f64(const double* src, double* dst, cudaStream_t s) {
@@ -1490,23 +1531,24 @@ void accum_f64(const double* src, double* dst, cudaStream_t s) {
 }
 void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,
                    const long long* counter, long long nb, long long B, long long rows_pad, void* dst, float* ydst,
-                   long long* seg_off, int* seg_rows, cudaStream_t s) {
+                   long long* seg_off, int* seg_rows, cudaStream_t s, void* dst_lo) {
   if ((row_bytes % 16) != 0) fail(MOSES_ERR_INVALID_ARG, "packed rows must be 16-byte multiples");
   gather_pooled_kernel<<<grid_for(rows_pad * row_bytes / 16, 256), 256, 0, s>>>(
       static_cast<const uint8_t*>(x_base), row_bytes, y_base, prog_off, counter, nb, B, rows_pad,
-      static_cast<uint8_t*>(dst), ydst, seg_off, seg_rows);
+      static_cast<uint8_t*>(dst), ydst, seg_off, seg_rows, static_cast<uint8_t*>(dst_lo));
   MOSES_CUDA(cudaGetLastError());
 }
 template <typename T>
 void pack_pooled(const double* xs, const double* ys, const long long* offs, const long long* dims_dev, int D,
                  long long rows_pad, T* act0, long long ld, float* ydst, long long* seg_off, int* seg_rows,
-                 cudaStream_t s) {
+                 cudaStream_t s, T* lo) {
   pack_pooled_kernel<T><<<grid_for(rows_pad * ld, 256), 256, 0, s>>>(xs, ys, offs, dims_dev, D, rows_pad, act0, ld, ydst,
-                                                                     seg_off, seg_rows);
+                                                                     seg_off, seg_rows, lo);
   MOSES_CUDA(cudaGetLastError());
 }
 template void pack_pooled<__nv_bfloat16>(const double*, const double*, const long long*, const long long*, int,
-                                         long long, __nv_bfloat16*, long long, float*, long long*, int*, cudaStream_t);
+                                         long long, __nv_bfloat16*, long long, float*, long long*, int*, cudaStream_t,
+                                         __nv_bfloat16*);
 void store_scalar_f64(const double* src, double* dst, cudaStream_t s) {
   store_scalar_f64_kernel<<<1, 1, 0, s>>>(src, dst);
   MOSES_CUDA(cudaGetLastError());
@@ -1631,7 +1673,7 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
 
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st, float* dz_lo) {
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo) {
   if (R <= 0) return;
   if constexpr (sizeof(T) == 2) {
     if (dz_lo == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
@@ -1657,13 +1699,13 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
 
 template <typename T>
 void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,
-                const float* bias_override) {
+                const float* bias_override, const T* H_lo) {
   const int slabs = R > 0 ? ceil_div(R, kColSlab) : 1;
   if (R <= 0) {
     MOSES_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (W + 1), st));
     return;
   }
-  column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(coef, H, ldh, R, W, ws);
+  column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(coef, H, ldh, R, W, ws, H_lo);
   column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(ws, slabs, W + 1, g, bias_override);
   MOSES_CUDA(cudaGetLastError());
 }
@@ -1672,9 +1714,12 @@ size_t column_dot_ws_floats(long long R, int W) { return size_t(R > 0 ? ceil_div
 void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
                 Shadow sh, cudaStream_t st) {
   const int grid = grid_for(P, 256);
-#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr)
-#define SGD_K(M, K) \
-  if (sh.kind == 1) SGD_LAUNCH(M, K, 1); else if (sh.kind == 2) SGD_LAUNCH(M, K, 2); else SGD_LAUNCH(M, K, 0)
+#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr, sh.lo_off)
+#define SGD_K(M, K)                                            \
+  if (sh.kind == 1) SGD_LAUNCH(M, K, 1);                       \
+  else if (sh.kind == 2) SGD_LAUNCH(M, K, 2);                  \
+  else if (sh.kind == 4) SGD_LAUNCH(M, K, 4);                  \
+  else SGD_LAUNCH(M, K, 0)
   const bool k = mask != nullptr;
   if (momentum) {
     if (k) { SGD_K(true, true); } else { SGD_K(true, false); }
@@ -1864,7 +1909,8 @@ void accuracy_counts(const float* s, const float* y, const long long* seg_of_row
 
 template <typename T>
 void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, long long ldh, long long m, long long n,
-                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st) {
+                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st,
+                    const T* H_lo) {
   float* dz = ws;                                   // [m+n]
   float* du = ws + round_up(m + n, 64);             // [W+1]
   double* dc = reinterpret_cast<double*>(du + round_up(W + 1, 64));
@@ -1873,7 +1919,7 @@ void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, l
     const long long R = m + n;
     const int slabs = ceil_div(R, kColSlab);
     float* part = reinterpret_cast<float*>(dc + 8);
-    column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(dz, H, ldh, R, W, part);
+    column_dot_kernel<T><<<dim3(ceil_div(W + 1, 32), slabs), 256, 0, st>>>(dz, H, ldh, R, W, part, H_lo);
     column_sum_kernel<<<ceil_div(W + 1, 256), 256, 0, st>>>(part, slabs, W + 1, du, nullptr);
   }
   adv_update_kernel<<<ceil_div(W, 256), 256, 0, st>>>(u, c, du, W, eta, dc);
@@ -1912,16 +1958,16 @@ void synth_labels(unsigned long long seed, long long row0, long long n, float* d
 }
 
 #define INST(T)                                                                                                   \
-  template void pack_rows<T>(const double*, long long, int, T*, long long, cudaStream_t, float*);                      \
-  template void pack_rows_f32<T>(const float*, long long, int, long long, T*, long long, cudaStream_t, float*);           \
+  template void pack_rows<T>(const double*, long long, int, T*, long long, cudaStream_t, T*);                         \
+  template void pack_rows_f32<T>(const float*, long long, int, long long, T*, long long, cudaStream_t, T*);           \
   template void set_ones_column<T>(T*, long long, int, long long, cudaStream_t);                                  \
-  template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t);                       \
+  template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t, const T*);             \
   template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
-                                 long long, int, T*, long long, cudaStream_t, float*);                                    \
+                                 long long, int, T*, long long, cudaStream_t, T*);                                \
   template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t,     \
-                              const float*);                                                                      \
+                              const float*, const T*);                                                            \
   template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \
-                                  float*, float*, float, double*, float*, cudaStream_t);                          \
+                                  float*, float*, float, double*, float*, cudaStream_t, const T*);                \
   template void segment_sum<T>(const T*, long long, int, const long long*, long long, float*, long long,          \
                                cudaStream_t);                                                                     \
   template void synth_features<T>(unsigned long long, long long, long long, int, T*, long long, cudaStream_t);

@@ -7,9 +7,13 @@ namespace moses {
 // Operand shadow of the fp32 master parameters written by every update kernel:
 // kind 0 none, 1 bf16 (kind::f16 operand), 2 tf32-rounded fp32 (kind::tf32 operand),
 // 3 (refresh_shadow only) 3xTF32 hi/lo pair: hi at ptr[i], lo at ptr[shadow_lo_offset(n) + i].
+// operand shadow written by update kernels: 0 none, 1 bf16, 2 tf32-rounded fp32, 3 tf32 hi/lo pair
+// (lo at ptr + shadow_lo_offset(n), refresh_shadow only), 4 bf16 hi/lo pair (MOSES_PREC_BF16X3: lo at
+// ptr + lo_off elements; sgd_update and refresh_shadow)
 struct Shadow {
   void* ptr;
   int kind;
+  long long lo_off = 0;
 };
 // low half of a kind-3 shadow starts 128-byte aligned (TMA operands need 16-byte alignment)
 __host__ __device__ constexpr long long shadow_lo_offset(long long n) { return (n + 31) / 32 * 32; }
@@ -17,29 +21,30 @@ void refresh_shadow(const float* w, long long n, Shadow sh, cudaStream_t s);
 
 // ---- data movement
 template <typename T>
-void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s, float* lo = nullptr);
+void pack_rows(const double* src_d, long long n, int D, T* dst, long long ld, cudaStream_t s, T* lo = nullptr);
 template <typename T>
 void pack_rows_f32(const float* src_d, long long n, int D, long long lds, T* dst, long long ld, cudaStream_t s,
-                   float* lo = nullptr);
+                   T* lo = nullptr);
 template <typename T>
 void set_ones_column(T* act, long long rows, int col, long long ld, cudaStream_t s);
 template <typename T>
-void unpack_rows(const T* src, long long n, int W, long long ld, double* dst_d, cudaStream_t s);
+void unpack_rows(const T* src, long long n, int W, long long ld, double* dst_d, cudaStream_t s,
+                 const T* lo = nullptr);
 void f32_to_f64(const float* src, long long n, double* dst, cudaStream_t s);
 void f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
 void f32_to_bf16(const float* src, long long n, __nv_bfloat16* dst, cudaStream_t s);
 void strided_f64_to_f32(const double* src, long long rows, int W, float* dst, long long ldd, cudaStream_t s);
 // batch b = (*counter % nb): rows [b*batch, (b+1)*batch) of a packed dataset -> dst, labels -> ydst
 void gather_batch(const void* x_base, long long row_bytes, const float* y_base, const long long* counter, long long nb,
-                  long long batch, void* dst, float* ydst, cudaStream_t s);
+                  long long batch, void* dst, float* ydst, cudaStream_t s, void* dst_lo = nullptr);
 void advance_counter(long long* c, cudaStream_t s);
 // plan batch *counter: rows[off[b] .. off[b] + n) of a packed dataset -> dst, labels -> ydst
 void gather_plan(const void* x_base, long long row_bytes, const float* y_base, const long long* rows, const long long* off,
-                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s);
+                 const long long* counter, long long n, void* dst, float* ydst, cudaStream_t s, void* dst_lo = nullptr);
 void accum_f64(const double* src, double* dst, cudaStream_t s);  // *dst += *src (one thread)
 void gather_pooled(const void* x_base, long long row_bytes, const float* y_base, const long long* prog_off,
                    const long long* counter, long long nb, long long B, long long rows_pad, void* dst, float* ydst,
-                   long long* seg_off, int* seg_rows, cudaStream_t s);
+                   long long* seg_off, int* seg_rows, cudaStream_t s, void* dst_lo = nullptr);
 // out[r] = H[r] . u  (warp per row)
 void row_dot(const float* H, long long ldh, long long R, int W, const float* u, float* out, cudaStream_t s);
 // discriminator_cross_entropy (lottery.cpp:207-218) over z[0,m) source and z[m,m+n) target
@@ -83,11 +88,11 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
 // dZ_last[r][j] = (coefA[r]*wh[j] + coefB[r]*u[j]) * [H[r][j] > 0]
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st, float* dz_lo = nullptr);
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo = nullptr);
 // g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
 template <typename T>
 void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,
-                const float* bias_override = nullptr);
+                const float* bias_override = nullptr, const T* H_lo = nullptr);
 size_t column_dot_ws_floats(long long R, int W);
 
 // ---- updates (model.cpp:263-296, lottery.cpp:92-120)
@@ -149,7 +154,8 @@ void accuracy_counts(const float* s, const float* y, const long long* seg_of_row
 // ---- adversary (lottery.cpp:135-164)
 template <typename T>
 void adversary_step(const float* part2, int ntiles, long long ld2, const T* H, long long ldh, long long m, long long n,
-                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st);
+                    int W, float* u, float* c, float eta, double* loss_out, float* ws, cudaStream_t st,
+                    const T* H_lo = nullptr);
 
 // ---- extensions
 template <typename T>
@@ -173,7 +179,7 @@ void store_scalar_f64(const double* src, double* dst, cudaStream_t s);
 template <typename T>
 void pack_pooled(const double* xs, const double* ys, const long long* offs, const long long* dims_dev, int D,
                  long long rows_pad, T* act0, long long ld, float* ydst, long long* seg_off, int* seg_rows,
-                 cudaStream_t s);
+                 cudaStream_t s, T* lo = nullptr);
 // simulated hardware (space.cu): measure() labels and the exhaustive noise-free optimum
 int measure_configs(const double* dev6, int repeats, const char* device_id, const char* task_id, const double* task4,
                     const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,

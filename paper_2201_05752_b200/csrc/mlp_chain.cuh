@@ -57,6 +57,7 @@ struct ChainArgs {
   float* head_part2;
   long long head_ld;
   unsigned long long* trace;  // optional phase timestamps of cluster 0 (tools/chain_trace.py)
+  __nv_bfloat16* out_lo[kChainMaxLayers];  // split chain: lo planes of the outputs (row stride ldo)
 };
 
 struct ChainCfg {

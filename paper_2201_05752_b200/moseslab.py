@@ -34,9 +34,14 @@ ERROR_NAMES = [
 ]
 LIB_ERRORS = {100: "cuda-error", 101: "no-device", 102: "capacity", 103: "invalid-argument"}
 
-PREC_BF16, PREC_TF32, PREC_FP32 = 0, 1, 2  # FP32: 3xTF32 split operands
+PREC_BF16, PREC_TF32, PREC_FP32, PREC_BF16X3 = 0, 1, 2, 3  # FP32: 3xTF32, BF16X3: split bf16 operands
 THRESHOLD, RATIO = 1, 2
 DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
+
+
+def input_dtype(precision: int) -> int:
+    """Element type of device-resident input rows for a handle of this precision (moses_gpu.h)."""
+    return DTYPE_BF16 if precision == PREC_BF16 else DTYPE_F32
 
 
 class MosesError(RuntimeError):

@@ -88,6 +88,6 @@ def cfg4(precs, n=100_000):
 
 
 if __name__ == "__main__":
-    precs = [("bf16", ml.PREC_BF16), ("tf32", ml.PREC_TF32), ("fp32", ml.PREC_FP32)]
+    precs = [("bf16", ml.PREC_BF16), ("tf32", ml.PREC_TF32), ("fp32", ml.PREC_FP32), ("bf16x3", ml.PREC_BF16X3)]
     cfg2(precs)
     cfg4(precs)
