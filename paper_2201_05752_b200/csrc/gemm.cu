@@ -2,6 +2,7 @@
 // entry point fetched through the runtime, so the library needs no -lcuda),
 // N-tile selection for the 148-SM grid, and the template instantiations.
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -338,11 +339,15 @@ void launch_chain_t(const ChainCall& c, cudaStream_t s) {
 
 template <bool UPDATE, bool SPLIT>
 void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
-  using Cfg = GroupCfgT<SPLIT>;
-  auto kern = wgrad_group_kernel<UPDATE, SPLIT>;
+  using Cfg = std::conditional_t<SPLIT, GroupSplitCfg, GroupCfg>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    if constexpr (SPLIT)
+      MOSES_CUDA(cudaFuncSetAttribute(wgrad_group_split_kernel<UPDATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::kSmemBytes));
+    else
+      MOSES_CUDA(cudaFuncSetAttribute(wgrad_group_kernel<UPDATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::kSmemBytes));
   });
   GroupMapsSplit maps;
   GroupArgs a{};
@@ -378,7 +383,7 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   a.loss_copy = c.loss_copy;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(SPLIT ? 192 : 128);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -386,7 +391,10 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+  if constexpr (SPLIT)
+    MOSES_CUDA(cudaLaunchKernelEx(&cfg, wgrad_group_split_kernel<UPDATE>, maps, a));
+  else
+    MOSES_CUDA(cudaLaunchKernelEx(&cfg, wgrad_group_kernel<UPDATE>, static_cast<const GroupMaps&>(maps), a));
 }
 
 template <typename T, int BN>

@@ -47,143 +47,31 @@ struct GroupArgs {
   double* loss_copy;       // optional: *loss_copy = *loss_src once (per-step loss mailbox)
 };
 
-template <bool SPLIT = false>
-struct GroupCfgT {
+struct GroupCfg {
   static constexpr int BM = 128, BN = 64, BK = 64;
   static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
-  static constexpr int kStageBytes = (SPLIT ? 2 : 1) * (kABytes + kBBytes);  // [A_hi B_hi (A_lo B_lo)]
-  static constexpr int kStages = SPLIT ? 4 : 9;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = 9;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
-using GroupCfg = GroupCfgT<false>;
+// split bf16 (MOSES_PREC_BF16X3): [A_hi | B_hi | A_lo | B_lo] per stage; TMEM accumulators promoted
+// into fp32 registers every kPromoteKb k-blocks
+struct GroupSplitCfg {
+  static constexpr int BM = 128, BN = 64, BK = 64;
+  static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
+  static constexpr int kStageBytes = 2 * (kABytes + kBBytes);
+  static constexpr int kStages = 4;
+  static constexpr int kPromoteKb = 2;            // 128 K elements (384 products) per TMEM chunk
+  static constexpr uint32_t kTmemCols = 2 * BN;   // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+};
 
-template <bool UPDATE, bool SPLIT = false>
-__global__ void __launch_bounds__(128, 1)
-    wgrad_group_kernel(const __grid_constant__ GroupMapsSplit maps, const __grid_constant__ GroupArgs args) {
-  using C = GroupCfgT<SPLIT>;
-  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::kStages;
-  constexpr uint32_t kIdesc = ptx::umma_idesc(1 /*BF16*/, true, true, BM, BN);
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* accum_bar = empty_bar + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
-
-  // tile -> (level, m tile, n tile)
-  const int t = blockIdx.x;
-  int lev = 0;
-  while (lev + 1 < args.n && t >= args.tile_begin[lev + 1]) ++lev;
-  const int local = t - args.tile_begin[lev];
-  const int m0 = (local / args.tiles_n[lev]) * BM, n0 = (local % args.tiles_n[lev]) * BN;
-  const int M = args.M[lev], N = args.N[lev];
-  const CUtensorMap* tmA = &maps.a[lev];
-  const CUtensorMap* tmB = &maps.b[lev];
-  const CUtensorMap* tmAl = &maps.a_lo[lev];
-  const CUtensorMap* tmBl = &maps.b_lo[lev];
-
-  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int num_kb = (args.K + BK - 1) / BK;
-
-  if (threadIdx.x == 0) {
-    ptx::tma_prefetch_desc(tmA);
-    ptx::tma_prefetch_desc(tmB);
-    if constexpr (SPLIT) {
-      ptx::tma_prefetch_desc(tmAl);
-      ptx::tma_prefetch_desc(tmBl);
-    }
-    for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
-    }
-    ptx::mbar_init(accum_bar, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 2) ptx::tmem_alloc<BN>(tmem_slot);
-  ptx::pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 32) {  // step bookkeeping folded into the step's last kernel
-    if (args.counter != nullptr) *args.counter += 1;
-    if (args.loss_acc != nullptr) *args.loss_acc += *args.loss_src;
-    if (args.loss_copy != nullptr) *args.loss_copy = *args.loss_src;
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * C::kStageBytes;
-        uint8_t* sb = sa + C::kABytes;
-        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
-        const int k0 = kb * BK;
-        ptx::tma_load_2d(sa, tmA, &full_bar[stage], m0, k0);
-        ptx::tma_load_2d(sa + BK * 128, tmA, &full_bar[stage], m0 + 64, k0);
-        ptx::tma_load_2d(sb, tmB, &full_bar[stage], n0, k0);
-        if constexpr (SPLIT) {
-          uint8_t* sal = sb + C::kBBytes;
-          uint8_t* sbl = sal + C::kABytes;
-          ptx::tma_load_2d(sal, tmAl, &full_bar[stage], m0, k0);
-          ptx::tma_load_2d(sal + BK * 128, tmAl, &full_bar[stage], m0 + 64, k0);
-          ptx::tma_load_2d(sbl, tmBl, &full_bar[stage], n0, k0);
-        }
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        ptx::mbar_wait(&full_bar[stage], phase);
-        ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
-        const uint32_t sb = sa + C::kABytes;
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, BK * 128, 1024, 2);
-          const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, BK * 128, 1024, 2);
-          ptx::umma_f16(tmem_base, ad, bd, kIdesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          if constexpr (SPLIT) {
-            const uint32_t sal = sb + C::kBBytes, sbl = sal + C::kABytes;
-            const uint64_t adl = ptx::sw128_desc(sal + kk * 2048, BK * 128, 1024, 2);
-            const uint64_t bdl = ptx::sw128_desc(sbl + kk * 2048, BK * 128, 1024, 2);
-            ptx::umma_f16(tmem_base, ad, bdl, kIdesc, 1u);
-            ptx::umma_f16(tmem_base, adl, bd, kIdesc, 1u);
-          }
-        }
-        ptx::umma_commit(&empty_bar[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      ptx::umma_commit(accum_bar);
-    }
-    __syncwarp();
-  }
-
-  // Epilogue: TMEM -> padded smem tile (the pipeline stages are free once the accumulator is
-  // complete) -> coalesced row-major passes over g (and w / momentum / shadow when UPDATE).
+// Tile (BM x BN fp32 in shared memory, row stride BN + 1) -> g [-> momentum step of w / v and the
+// bf16 operand shadow (SPLIT: its hi/lo pair)], coalesced row-major passes by every thread of the CTA.
+template <bool UPDATE, bool SPLIT, int BM, int BN>
+__device__ __forceinline__ void group_update_epilogue(const float* tile, const GroupArgs& args, int lev, int m0, int n0,
+                                                      int M, int N) {
   constexpr int kPad = BN + 1;
-  float* tile = reinterpret_cast<float*>(smem);
-  const int row = int(warp) * 32 + int(lane);
-  const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
-  ptx::mbar_wait(accum_bar, 0);
-  ptx::tc_fence_after();
-  ptx::pdl_launch_dependents();
-#pragma unroll
-  for (int c = 0; c < BN / 32; ++c) {
-    uint32_t r[32];
-    ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) tile[row * kPad + c * 32 + j] = __uint_as_float(r[j]);
-  }
-  __syncthreads();
   const int rows = min(BM, M - m0), cols = min(BN, N - n0);
   float* __restrict__ g = args.g[lev];
   float* __restrict__ w = args.w[lev];
@@ -264,11 +152,275 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
 
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(128, 1)
+    wgrad_group_kernel(const __grid_constant__ GroupMaps maps, const __grid_constant__ GroupArgs args) {
+  using C = GroupCfg;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::kStages;
+  constexpr uint32_t kIdesc = ptx::umma_idesc(1 /*BF16*/, true, true, BM, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* accum_bar = empty_bar + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  // tile -> (level, m tile, n tile)
+  const int t = blockIdx.x;
+  int lev = 0;
+  while (lev + 1 < args.n && t >= args.tile_begin[lev + 1]) ++lev;
+  const int local = t - args.tile_begin[lev];
+  const int m0 = (local / args.tiles_n[lev]) * BM, n0 = (local % args.tiles_n[lev]) * BN;
+  const int M = args.M[lev], N = args.N[lev];
+  const CUtensorMap* tmA = &maps.a[lev];
+  const CUtensorMap* tmB = &maps.b[lev];
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(tmA);
+    ptx::tma_prefetch_desc(tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    ptx::mbar_init(accum_bar, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<BN>(tmem_slot);
+  ptx::pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 32) {  // step bookkeeping folded into the step's last kernel
+    if (args.counter != nullptr) *args.counter += 1;
+    if (args.loss_acc != nullptr) *args.loss_acc += *args.loss_src;
+    if (args.loss_copy != nullptr) *args.loss_copy = *args.loss_src;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::kStageBytes;
+        uint8_t* sb = sa + C::kABytes;
+        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+        const int k0 = kb * BK;
+        ptx::tma_load_2d(sa, tmA, &full_bar[stage], m0, k0);
+        ptx::tma_load_2d(sa + BK * 128, tmA, &full_bar[stage], m0 + 64, k0);
+        ptx::tma_load_2d(sb, tmB, &full_bar[stage], n0, k0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&full_bar[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
+        const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, BK * 128, 1024, 2);
+          const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, BK * 128, 1024, 2);
+          ptx::umma_f16(tmem_base, ad, bd, kIdesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        }
+        ptx::umma_commit(&empty_bar[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      ptx::umma_commit(accum_bar);
+    }
+    __syncwarp();
+  }
+
+  // Epilogue: TMEM -> padded smem tile (the pipeline stages are free once the accumulator is
+  // complete) -> coalesced row-major passes over g (and w / momentum / shadow when UPDATE).
+  constexpr int kPad = BN + 1;
+  float* tile = reinterpret_cast<float*>(smem);
+  const int row = int(warp) * 32 + int(lane);
+  const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
+  ptx::mbar_wait(accum_bar, 0);
+  ptx::tc_fence_after();
+  ptx::pdl_launch_dependents();
+#pragma unroll
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) tile[row * kPad + c * 32 + j] = __uint_as_float(r[j]);
+  }
+  __syncthreads();
+  group_update_epilogue<UPDATE, false, C::BM, C::BN>(tile, args, lev, m0, n0, M, N);
+
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<BN>(tmem_base);
+  }
+}
+
+// Split-bf16 grouped wgrad: G = A_hi B_hi + A_hi B_lo + A_lo B_hi over K = the batch rows. The sums
+// run over ~2.3K-18K rows of mixed-sign dZ, where the tensor-core accumulator (not a round-to-nearest
+// fp32 adder) drifts by ~1e-3 of the result; so, as in gemm_split.cuh, the MMAs of every kPromoteKb
+// k-blocks go to one of two TMEM buffers and the drain warps add the finished chunk into fp32
+// registers while the next chunk accumulates. 192 threads: warps 0-3 drain + epilogue, warp 4 TMA
+// producer, warp 5 MMA issuer.
+template <bool UPDATE>
+__global__ void __launch_bounds__(192, 1)
+    wgrad_group_split_kernel(const __grid_constant__ GroupMapsSplit maps, const __grid_constant__ GroupArgs args) {
+  using C = GroupSplitCfg;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::kStages, KC = C::kPromoteKb;
+  constexpr uint32_t kIdesc = ptx::umma_idesc(1 /*BF16*/, true, true, BM, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* bfull = empty_bar + STAGES;  // [2] accumulator buffer holds a finished chunk
+  uint64_t* bempty = bfull + 2;          // [2] drain warps have consumed the buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 2);
+
+  const int t = blockIdx.x;
+  int lev = 0;
+  while (lev + 1 < args.n && t >= args.tile_begin[lev + 1]) ++lev;
+  const int local = t - args.tile_begin[lev];
+  const int m0 = (local / args.tiles_n[lev]) * BM, n0 = (local % args.tiles_n[lev]) * BN;
+  const int M = args.M[lev], N = args.N[lev];
+
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int num_kb = (args.K + BK - 1) / BK;
+  const int nchunks = (num_kb + KC - 1) / KC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bfull[b], 1);
+      ptx::mbar_init(&bempty[b], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+  ptx::pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 160) {  // step bookkeeping folded into the step's last kernel
+    if (args.counter != nullptr) *args.counter += 1;
+    if (args.loss_acc != nullptr) *args.loss_acc += *args.loss_src;
+    if (args.loss_copy != nullptr) *args.loss_copy = *args.loss_src;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const CUtensorMap* tmA = &maps.a[lev];
+      const CUtensorMap* tmB = &maps.b[lev];
+      const CUtensorMap* tmAl = &maps.a_lo[lev];
+      const CUtensorMap* tmBl = &maps.b_lo[lev];
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::kStageBytes;
+        uint8_t* sb = sa + C::kABytes;
+        uint8_t* sal = sb + C::kBBytes;
+        uint8_t* sbl = sal + C::kABytes;
+        ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+        const int k0 = kb * BK;
+        ptx::tma_load_2d(sa, tmA, &full_bar[stage], m0, k0);
+        ptx::tma_load_2d(sa + BK * 128, tmA, &full_bar[stage], m0 + 64, k0);
+        ptx::tma_load_2d(sb, tmB, &full_bar[stage], n0, k0);
+        ptx::tma_load_2d(sal, tmAl, &full_bar[stage], m0, k0);
+        ptx::tma_load_2d(sal + BK * 128, tmAl, &full_bar[stage], m0 + 64, k0);
+        ptx::tma_load_2d(sbl, tmBl, &full_bar[stage], n0, k0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int c = kb / KC, buf = c & 1;
+        const bool first = (kb % KC) == 0;
+        if (first && c >= 2) {
+          ptx::mbar_wait(&bempty[buf], uint32_t((c - 2) >> 1) & 1u);  // chunk c-2 drained
+          ptx::tc_fence_after();
+        }
+        ptx::mbar_wait(&full_bar[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
+        const uint32_t sb = sa + C::kABytes, sal = sb + C::kBBytes, sbl = sal + C::kABytes;
+        const uint32_t tacc = tmem_base + uint32_t(buf * BN);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ah = ptx::sw128_desc(sa + kk * 2048, BK * 128, 1024, 2);
+          const uint64_t bh = ptx::sw128_desc(sb + kk * 2048, BK * 128, 1024, 2);
+          const uint64_t al = ptx::sw128_desc(sal + kk * 2048, BK * 128, 1024, 2);
+          const uint64_t bl = ptx::sw128_desc(sbl + kk * 2048, BK * 128, 1024, 2);
+          // small terms first: they never dominate the running sum's exponent
+          ptx::umma_f16(tacc, ah, bl, kIdesc, (!first || kk > 0) ? 1u : 0u);
+          ptx::umma_f16(tacc, al, bh, kIdesc, 1u);
+          ptx::umma_f16(tacc, ah, bh, kIdesc, 1u);
+        }
+        ptx::umma_commit(&empty_bar[stage]);
+        if ((kb % KC) == KC - 1 || kb == num_kb - 1) ptx::umma_commit(&bfull[buf]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // drain: warp w owns TMEM lanes / tile rows 32w..32w+31; fp32 register accumulation per chunk
+    const int row = int(warp) * 32 + int(lane);
+    const uint32_t t_row = tmem_base + ((warp * 32u) << 16);
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      ptx::mbar_wait(&bfull[buf], uint32_t(c >> 1) & 1u);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < BN / 32; ++q) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(t_row + uint32_t(buf * BN + q * 32), r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[q * 32 + j] += __uint_as_float(r[j]);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bempty[buf]);
+    }
+    ptx::pdl_launch_dependents();
+    // every stage is free once the last chunk is drained: the tile reuses the pipeline memory
+    float* tile = reinterpret_cast<float*>(smem);
+#pragma unroll
+    for (int j = 0; j < BN; ++j) tile[row * (BN + 1) + j] = acc[j];
+  }
+  __syncthreads();
+  group_update_epilogue<UPDATE, true, BM, BN>(reinterpret_cast<const float*>(smem), args, lev, m0, n0, M, N);
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 

@@ -1,0 +1,262 @@
+"""Split-bf16 precision mode (MOSES_PREC_BF16X3) against the fp64 oracle, on the benched shapes.
+
+Every GEMM operand is carried as hi = rn_bf16(v), lo = rn_bf16(v - hi) (|v - hi - lo| <= 2^-18 |v|)
+and multiplied as hi*hi + hi*lo + lo*hi on the bf16 tensor cores (csrc/mlp_chain_split.cuh,
+csrc/gemm_group.cuh). North-star bound for tensor-core GEMMs: <= 1e-3 normwise relative
+(max |d| / max |ref|) for predictions, losses and updated weights; this mode measures ~1e-5 on
+predictions and losses.
+
+Gradients are a discontinuous function of the weights at the ReLU kinks: a pre-activation within
+the forward error (~1e-5 relative) of zero can take the other side of the kink than in fp64, which
+moves that (row, unit)'s whole contribution. The normwise checks below hold with those flips
+included (deterministic inputs); the quantile checks show the remaining entries sit at the operand
+precision.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3        # north-star tensor-core bound (predictions, losses, update deltas)
+TOL_PRED = 1e-4   # what this mode is held to on predictions / losses / penultimate activations
+TOL_Q = 1e-4      # 99.9% of gradient / update entries (ReLU-kink flips excluded by the quantile)
+
+CFG2 = [164, 512, 512, 512, 512, 1]   # BASELINE configs[1]: 4x512 hidden, TenSet-shaped programs
+CFG4 = [164, 512, 512, 1]
+
+
+@pytest.fixture(scope="module")
+def ml():
+    from paper_2201_05752_b200 import moseslab
+
+    assert moseslab.lib().moses_device_check() == 0, moseslab.lib().moses_last_error()
+    return moseslab
+
+
+def nrel(got, ref):
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def qrel(got, ref, q=0.999):
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    return float(np.quantile(np.abs(got - ref), q) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def pooled_scores_ref(orc, dims, w, x, off):
+    _, h = orc.forward(dims, w, x, threads=8)
+    hp = orc.segment_sum(h, off)
+    H = dims[-2]
+    o = len(w) - (H + 1)
+    return hp @ w[o:o + H] + w[o + H]
+
+
+def test_golden_model_predictions(ml):
+    """init_random({16,512,512,1}, 12345) golden scores (test_model.cpp:387-398): sums of 512 mixed-sign
+    terms, where TF32 needs 2e-3; split bf16 holds 1e-4."""
+    p = ml.init_random([16, 512, 512, 1], 12345)
+    x = np.array([[(r + 1) * 0.1 + c * 0.01 for c in range(16)] for r in range(3)])
+    want = [0.068432722090836534, 0.10419522897402726, 0.14194361818494705]
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 128)
+    assert nrel(ml.predict(dm, x), want) < TOL_PRED
+
+
+@pytest.mark.parametrize("dims", [[16, 512, 512, 1], [164, 512, 512, 1], CFG2, [512, 512, 512, 1], [33, 512, 1]])
+@pytest.mark.parametrize("n", [1, 7, 300, 2500])
+def test_predict_and_penultimate_vs_oracle(ml, orc, dims, n):
+    p = ml.init_random(dims, 11, strict=False)
+    x = np.random.default_rng(n).random((n, dims[0]))
+    ref, h_ref = orc.forward(dims, p.params, x, threads=8)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 1024)  # n > 1024 runs in chunks
+    assert nrel(ml.predict(dm, x), ref) < TOL_PRED
+    assert nrel(ml.penultimate_activations(dm, x), h_ref) < TOL_PRED
+
+
+def test_rejects_shapes_without_split_kernels(ml):
+    with pytest.raises(ml.MosesError) as e:
+        ml.DeviceModel(ml.init_random([16, 256, 256, 1], 1, strict=False), ml.PREC_BF16X3, 64)
+    assert e.value.code == "invalid-argument" or e.value.status == 103
+
+
+def test_cfg2_pooled_gradients_loss_vs_oracle(ml, orc):
+    """cfg2 exactly: {164,512,512,512,512,1}, 512 TenSet-shaped programs (~2.3K statements)."""
+    p = ml.init_random(CFG2, 12345, strict=False)
+    off = ml.synth_offsets(1, 512, 8)
+    x = np.random.default_rng(1).random((int(off[-1]), 164))
+    y = 0.1 + np.random.default_rng(2).random(512)
+    g_ref, loss_ref = orc.gradients_pooled(CFG2, p.params, x, off, y, threads=8)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, int(off[-1]))
+    g, loss = ml.gradients_pooled(dm, x, off, y, want_loss=True)
+    assert abs(loss - loss_ref) <= TOL_PRED * abs(loss_ref)
+    assert nrel(ml.predict_pooled(dm, x, off), pooled_scores_ref(orc, CFG2, p.params, x, off)) < TOL_PRED
+    assert nrel(g, g_ref) < TOL
+    assert qrel(g, g_ref) < TOL_Q
+
+
+def _fp32_dataset(ml, L, programs, seed, ld):
+    import torch
+
+    off = ml.synth_offsets(seed, programs, 8)
+    rows = int(off[-1])
+    X = torch.empty((rows, ld), dtype=torch.float32, device="cuda")
+    Y = torch.empty(programs, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(seed, 0, rows, 164, ml.DTYPE_F32, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(seed, 0, programs, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    return off, X, Y
+
+
+def test_cfg2_training_graph_update_delta_vs_oracle(ml, orc):
+    """The benched path: moses_train_graph_create_pooled (device gather of variable-length programs ->
+    pooled gradients -> fused momentum update) for 3 steps over 3 different 512-program batches of an
+    fp32 device dataset; the update delta w_after - w_before against the fp64 oracle's 3 momentum-SGD
+    steps (tuner.cpp:146-147) on the same batches. Normwise on the delta: a wrong update fails."""
+    import torch
+
+    L = ml.lib()
+    p = ml.init_random(CFG2, 12345, strict=False)
+    B, nb, steps = 512, 3, 3
+    probe = ml.DeviceModel(p, ml.PREC_BF16X3, 128)
+    ld = probe.packed_ld
+    probe.close()
+    off, X, Y = _fp32_dataset(ml, L, B * nb, 1, ld)
+    per_batch = [int(off[(b + 1) * B] - off[b * B]) for b in range(nb)]
+    rows_pad = (max(per_batch) + 127) // 128 * 128
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, rows_pad)
+    OFF = torch.from_numpy(off).cuda()
+    ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, B, rows_pad,
+                                             0.001, 0.9, 1))
+    ml._ck(L.moses_train_graph_launch(dm.h, steps))
+    ml._ck(L.moses_model_synchronize(dm.h))
+    got = dm.download()
+    xs = X.cpu().numpy()[:, :164].astype(np.float64)
+    ys = Y.cpu().numpy().astype(np.float64)
+    w, mom = p.params.copy(), np.zeros_like(p.params)
+    losses = []
+    for s in range(steps):
+        b = s % nb
+        lo, hi = int(off[b * B]), int(off[(b + 1) * B])
+        g, loss = orc.gradients_pooled(CFG2, w, xs[lo:hi], off[b * B:(b + 1) * B + 1] - lo, ys[b * B:(b + 1) * B],
+                                       threads=8)
+        losses.append(loss)
+        w, mom = orc.apply_update(w, mom, g, 0.001, 0.9, None, True)
+    dw_ref, dw = w - p.params, got.params - p.params
+    assert nrel(dw, dw_ref) < TOL, nrel(dw, dw_ref)
+    assert qrel(dw, dw_ref) < TOL_Q
+    assert nrel(got.momentum, mom) < TOL
+    # the loss of the next step from the updated device model, through the host API
+    lo, hi = int(off[0]), int(off[B])
+    _, loss_dev = ml.gradients_pooled(dm, xs[lo:hi], off[:B + 1], ys[:B], want_loss=True)
+    _, loss_ref = orc.gradients_pooled(CFG2, w, xs[lo:hi], off[:B + 1], ys[:B], threads=8)
+    assert abs(loss_dev - loss_ref) <= TOL_PRED * abs(loss_ref)
+
+
+def _rank_agreement(s, s_ref, tau):
+    """Every pair (i, j) with s_ref[j] - s_ref[i] > tau must have s[j] > s[i]. Sorted by s_ref, pair
+    (i, j) is constrained iff j lies beyond the first index whose s_ref exceeds s_ref[i] + tau; so it
+    suffices that s[i] < min over that suffix of s."""
+    order = np.argsort(s_ref, kind="stable")
+    r, d = s_ref[order], s[order]
+    suffix_min = np.minimum.accumulate(d[::-1])[::-1]
+    first = np.searchsorted(r, r + tau, side="right")
+    has = first < len(r)
+    bad = has & (d >= np.where(has, suffix_min[np.minimum(first, len(r) - 1)], np.inf))
+    return int(np.sum(bad))
+
+
+def test_cfg4_pool_predictions_rank_order_and_topk(ml, orc):
+    """cfg4 scoring on a 100K-program pool (device fp32 rows -> moses_predict_device): predictions
+    normwise vs fp64; every pair whose fp64 gap exceeds 2x the north-star tolerance ordered
+    identically (search.cpp:32-37 orders by score); the device top-1024 equals the oracle's fp64
+    top-1024 up to pairs closer than that gap."""
+    import torch
+
+    L = ml.lib()
+    n, k = 100_000, 1024
+    p = ml.init_random(CFG4, 12345)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 65536)
+    ld = dm.packed_ld
+    X = torch.empty((n, ld), dtype=torch.float32, device="cuda")
+    S = torch.empty(n, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(101, 0, n, 164, ml.DTYPE_F32, X.data_ptr(), ld) == 0
+    torch.cuda.synchronize()
+    ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_F32, ld, n, S.data_ptr()))
+    ml._ck(L.moses_model_synchronize(dm.h))
+    s = S.cpu().numpy().astype(np.float64)
+    x = X.cpu().numpy()[:, :164].astype(np.float64)
+    ref, _ = orc.forward(CFG4, p.params, x, threads=8)
+    assert nrel(s, ref) < TOL_PRED
+    tau = 2 * TOL * np.max(np.abs(ref))
+    assert _rank_agreement(s, ref, tau) == 0
+    tight = 2 * nrel(s, ref) * np.max(np.abs(ref))  # the same at the measured error
+    assert _rank_agreement(s, ref, tight) == 0
+    top = ml.topk(s, k)
+    top_ref = orc.topk(ref, k)
+    kth = ref[top_ref[-1]]
+    assert np.all(ref[top] >= kth - tau)
+    missing = np.setdiff1d(top_ref, top)
+    assert np.all(ref[missing] <= ref[top].min() + tau)
+    assert len(missing) <= 2  # measured: identical sets
+
+
+def test_device_rows_equal_host_rows(ml):
+    """moses_predict_device on fp32 rows == moses_predict on the same values (both split on the device)."""
+    import torch
+
+    L = ml.lib()
+    p = ml.init_random(CFG4, 3)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 512)
+    ld = dm.packed_ld
+    x = np.random.default_rng(0).random((700, 164)).astype(np.float32).astype(np.float64)
+    Xd = torch.zeros((700, ld), dtype=torch.float32, device="cuda")
+    Xd[:, :164] = torch.from_numpy(x).float().cuda()
+    Xd[:, 164] = 1.0
+    S = torch.empty(700, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ml._ck(L.moses_predict_device(dm.h, Xd.data_ptr(), ml.DTYPE_F32, ld, 700, S.data_ptr()))
+    ml._ck(L.moses_model_synchronize(dm.h))
+    assert np.array_equal(S.cpu().numpy().astype(np.float64), ml.predict(dm, x).astype(np.float32).astype(np.float64))
+    with pytest.raises(ml.MosesError):  # bf16 rows are refused by split handles
+        ml._ck(L.moses_predict_device(dm.h, Xd.data_ptr(), ml.DTYPE_BF16, ld, 700, S.data_ptr()))
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.01])
+def test_gradients_with_adversary_vs_oracle(ml, orc, beta):
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 31)
+    x = np.random.default_rng(1).random((12, 16))
+    y = 0.1 + np.random.default_rng(2).random(12)
+    replay = np.random.default_rng(3).random((256, 16))
+    u = np.random.default_rng(4).normal(0, 0.05, 512)
+    c = 0.03
+    g_ref, loss_ref = orc.gradients(dims, p.params, x, y, (u, c, replay), beta)
+    adv = ml.make_adversary(replay, 512, 7)
+    adv.set(u, c)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 512)
+    g, loss = ml.gradients(dm, ml.RankingBatch(x, y), adv, beta, want_loss=True)
+    assert abs(loss - loss_ref) <= TOL_PRED * max(1.0, abs(loss_ref))
+    assert nrel(g, g_ref) < TOL
+    assert qrel(g, g_ref) < TOL_Q
+
+
+def test_moses_step_vs_oracle(ml, orc):
+    """The tuner's Moses branch (gradients with adversary -> discriminator step -> ratio-0.5 lottery
+    step) on a split-bf16 handle vs the oracle sequence: updated weights normwise, and the mask
+    bit-exact against the oracle's partition of the DEVICE's xi (identical-input rule)."""
+    dims = [16, 512, 512, 1]
+    p = ml.init_random(dims, 5)
+    x = np.random.default_rng(7).random((12, 16))
+    y = 0.1 + np.random.default_rng(8).random(12)
+    replay = np.random.default_rng(9).random((256, 16))
+    adv = ml.make_adversary(replay, 512, 3)
+    dm = ml.DeviceModel(p, ml.PREC_BF16X3, 512)
+    g = ml.gradients(dm, ml.RankingBatch(x, y), adv, 0.01)
+    g_ref, _ = orc.gradients(dims, p.params, x, y, (np.zeros(512), 0.0, replay), 0.01)
+    assert nrel(g, g_ref) < TOL
+    mask = ml.lottery_step(dm, ml.RATIO, 0.5, 0, 0.001, 0.01)
+    w32 = np.asarray(p.params, np.float32).astype(np.float64)
+    xi = np.abs(np.float32(w32) * np.float32(g)).astype(np.float64)
+    want = orc.partition(xi, False, 2, 0.5)
+    assert np.array_equal(np.asarray(mask.transferable, bool), np.asarray(want, bool))

@@ -153,7 +153,7 @@ def test_fp32_lottery_step_refreshes_operands(ml, orc):
     assert nrel(ml.predict(dm, x), ref) <= TOL_FP32
 
 
-def test_fp32_rejects_device_inputs_and_graphs(ml):
+def test_fp32_rejects_training_graphs(ml):
     lib = ml.lib()
     dims = [16, 64, 64, 1]
     dm = ml.DeviceModel(ml.init_random(dims, 1), ml.PREC_FP32, 128)
@@ -163,3 +163,22 @@ def test_fp32_rejects_device_inputs_and_graphs(ml):
     assert rc == 103
     msg = lib.moses_last_error()
     assert "FP32" in (msg.decode() if isinstance(msg, bytes) else msg)
+
+
+def test_fp32_device_rows_equal_host_rows(ml):
+    """FP32 handles take device-resident fp32 rows (split into their tf32 hi/lo planes on the device)."""
+    import torch
+
+    lib = ml.lib()
+    dims = [16, 64, 64, 1]
+    dm = ml.DeviceModel(ml.init_random(dims, 1), ml.PREC_FP32, 128)
+    ld = lib.moses_packed_ld(dm.h)
+    x = f32(np.random.default_rng(0).random((100, 16)))
+    Xd = torch.zeros((100, ld), dtype=torch.float32, device="cuda")
+    Xd[:, :16] = torch.from_numpy(x).float().cuda()
+    S = torch.empty(100, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ml._ck(lib.moses_predict_device(dm.h, ctypes.c_void_p(Xd.data_ptr()), ml.DTYPE_F32, ctypes.c_int64(ld),
+                                    ctypes.c_int64(100), ctypes.c_void_p(S.data_ptr())))
+    ml._ck(lib.moses_model_synchronize(dm.h))
+    assert np.array_equal(S.cpu().numpy(), ml.predict(dm, x).astype(np.float32))
