@@ -1,25 +1,27 @@
-"""Benchmark of the B200 Moses cost-model hot path (driver contract: one JSON line).
+"""Benchmark of the B200 Moses cost-model hot path (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): source-device pre-training of the cost model
-{164, 512, 512, 512, 512, 1} ("4x512 hidden") on 200k synthetic TenSet-shaped
-programs, batch 512 per GPU, momentum SGD (tuner.cpp:130-156 loop body:
-gradients + apply_update). A step = one batch: forward (tcgen05 GEMMs),
-pairwise ranking loss, backward (dgrad/wgrad GEMMs), momentum update.
-Metric: train samples/s (whole job). N > 1: data parallel, one process per GPU,
-NCCL average of the gradient buffer between gradients and update (weak scaling,
-each rank its own 512-row batch of its own shard).
+Headline workload (BASELINE.json configs[1], cfg2): source-device pre-training of the cost model
+{164, 512, 512, 512, 512, 1} ("4x512 hidden") on 200k synthetic TenSet-shaped programs (1-8
+statements each, segment-sum pooled), batch 512 programs per GPU, momentum SGD — the tuner.cpp:130-156
+loop body (gradients + apply_update). A step = one batch: fused forward chain, pairwise ranking loss,
+fused dZ chain, grouped weight gradients with the momentum update in their epilogue. Precision: split
+bf16 (MOSES_PREC_BF16X3: every operand hi + lo, 3 bf16 tensor-core MMAs per product; ~1e-5 from the
+fp64 reference, tests/test_gpu_bf16x3.py). Metric: train samples/s (whole job). N > 1: data parallel,
+one process per GPU, gradient all-reduce between gradients and update (weak scaling, each rank its own
+512-program batch of its own shard).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
---impl reference times the reference's CPU path (the fp64 C++ oracle restating
-model.cpp; the reference itself cannot be built here) on the
-host cores, rank 0 only.
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks. --impl reference times the reference's CPU path (the fp64 C++ oracle restating model.cpp; the
+reference itself cannot be built here) on the host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -27,6 +29,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 METRIC = "cost-model programs/sec (infer) & train samples/sec, 1–8 B200 vs CPU"
 DIMS = [164, 512, 512, 512, 512, 1]
@@ -35,10 +38,23 @@ BATCH = 512
 SEED_DATA, SEED_MODEL = 1, 12345
 LR, MU = 0.001, 0.9
 MAX_STMTS = 8  # statements per program: 1 + below(8), mean 4.5
+MIN_WINDOW_S = 0.3  # timed K-step windows are repeated until at least this much device time is covered
+E2E_MIN_STEPS = 200
+
+
+def workload_config(world: int) -> dict:
+    """The `config` object of both arms (ours and --impl reference): identical by construction."""
+    return {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} TenSet-shaped programs "
+                        f"(segment-sum pooling over 1-{MAX_STMTS} statements per program), batch {BATCH} "
+                        f"programs per GPU, momentum SGD lr={LR} mu={MU}",
+            "model": "moses-mlp-4x512", "programs": PROGRAMS, "global_batch": BATCH * world,
+            "seq_len": None, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2: every step gathers a different batch of the 605 MB device-resident "
+                  "fp32 dataset"}
 
 
 def train_flops_per_sample(dims):
-    """Algorithmic FLOPs per training sample: forward + weight-grad + data-grad (levels >= 1)."""
+    """Algorithmic FLOPs per training row: forward + weight-grad + data-grad (levels >= 1)."""
     L = len(dims) - 1
     fwd = sum(2 * dims[l] * dims[l + 1] for l in range(L))
     wgrad = sum(2 * dims[l] * dims[l + 1] for l in range(L))
@@ -47,6 +63,7 @@ def train_flops_per_sample(dims):
 
 
 def gemm_flops_per_step(dims, n):
+    """Hidden-layer GEMM FLOPs of one training step over n rows (the head GEMV is not a GEMM)."""
     L = len(dims) - 1
     fwd = sum(2 * n * dims[l] * dims[l + 1] for l in range(L - 1))
     wgrad = sum(2 * n * dims[l] * dims[l + 1] for l in range(L - 1))
@@ -55,69 +72,56 @@ def gemm_flops_per_step(dims, n):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled every 20 ms during the timed region (NVML)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                bits = int(get_reasons(h))
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+                self._stop.wait(0.02)
+        except Exception as e:  # noqa: BLE001 — sampling must never break the bench
+            self.error = repr(e)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self._t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s), "sampler": "NVML every 20 ms over all timed windows"}
 
 
-def cpu_baseline(steps_budget_s: float = 15.0, threads: int | None = None):
-    """Reference CPU path (fp64 oracle, reference formulas) on a bounded sample of the workload."""
+def cpu_baseline(budget_s: float, threads: int):
+    """Reference CPU path (fp64 oracle, reference formulas) on a bounded sample of the cfg2 workload."""
     import numpy as np
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
 
-    threads = threads or os.cpu_count() or 1
     w = orc.init_random(DIMS, SEED_MODEL, strict=False)
     mom = np.zeros_like(w)
     off = orc.synth_offsets(SEED_DATA, BATCH, MAX_STMTS)
@@ -135,7 +139,7 @@ def cpu_baseline(steps_budget_s: float = 15.0, threads: int | None = None):
     while True:
         step()
         n += 1
-        if time.perf_counter() - t0 > steps_budget_s or n >= 2000:
+        if time.perf_counter() - t0 > budget_s or n >= 2000:
             break
     dt = time.perf_counter() - t0
     return {"value": n * BATCH / dt, "unit": "samples/s", "cores": threads, "kind": "port",
@@ -144,39 +148,317 @@ def cpu_baseline(steps_budget_s: float = 15.0, threads: int | None = None):
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (fp64 oracle port), all host threads, rank 0 only."""
     if rank != 0:
         return
-    steps_s = 0.0
-    base = cpu_baseline(steps_budget_s=max(5.0, min(30.0, 0.05 * (args.steps + args.warmup))))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    budget = max(5.0, min(30.0, 0.05 * (args.steps + args.warmup)))
+    base = cpu_baseline(budget, os.cpu_count() or 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / base["value"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (keyed SplitMix64 TenSet-shaped features, labels 0.1+U)",
-        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} TenSet-shaped programs "
-                               f"(segment-sum pooling over statements), batch {BATCH} programs, momentum SGD "
-                               f"lr={LR} mu={MU}",
-                   "programs": PROGRAMS, "global_batch": BATCH, "parallelism": "host threads"},
+        "data": "synthetic (keyed SplitMix64 TenSet-shaped features, labels 0.1+U; random-init model)",
+        "config": workload_config(world),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    del steps_s
 
 
-def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
-    """cfg4: score a pool of `programs` synthetic programs with the 4x512 model and select the
-    global top-1024 (score desc, index asc). N > 1: the pool is split into contiguous program
-    ranges, one per rank (strong scaling: the pool is fixed); each rank scores and top-k's its shard,
-    the (score, global index) winners are all-gathered and merged (distributed.py) — the only
-    exchange. programs/s = pool / max over ranks of the pass time; the forward GEMM roofline is
-    per GPU. Features are generated on device (PCIe would otherwise dominate)."""
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this command under torch.distributed.run with N ranks."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def timed_windows(run_k, K, stream, world, dist):
+    """Device time of K back-to-back steps (CUDA events on the launch stream, barrier + synchronize on
+    both sides, max over ranks), repeated until MIN_WINDOW_S is covered (>= 3 windows)."""
+    import torch
+
+    windows = []
+    while len(windows) < 3 or (sum(windows) < MIN_WINDOW_S * 1e3 and len(windows) < 200):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_k(K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        windows.append(ms)
+    return windows
+
+
+def median(v):
+    s = sorted(v)
+    return s[len(s) // 2] if len(s) % 2 else 0.5 * (s[len(s) // 2 - 1] + s[len(s) // 2])
+
+
+class DataParallel:
+    """Gradient all-reduce of the device gradient buffer between gradients and update (N > 1)."""
+
+    def __init__(self, ml, dm, world, dist):
+        from paper_2201_05752_b200.distributed import device_gradient_tensor
+
+        self.ml, self.dm, self.world, self.dist = ml, dm, world, dist
+        self.grads = device_gradient_tensor(dm) if world > 1 else None
+
+    def step_tail(self, lr, mu):
+        if self.world > 1:
+            self.dist.all_reduce(self.grads, op=self.dist.ReduceOp.AVG)
+            self.ml._ck(self.ml.lib().moses_apply_update(self.dm.h, lr, mu, None, 0, 1))
+
+
+def bench_cfg2(ml, L, args, rank, world, dist, peaks):
+    """The headline: cfg2 training steps on split-bf16 handles, device-resident dataset, graph replay."""
     import ctypes as C
 
     import numpy as np
 
     import torch
-    import torch.distributed as dist
+
+    from paper_2201_05752_b200.distributed import shard_range
+
+    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
+    off_all = ml.synth_offsets(SEED_DATA, PROGRAMS, MAX_STMTS)
+    p_lo, p_hi = shard_range(PROGRAMS, rank, world)
+    nb = (p_hi - p_lo) // BATCH
+    p_hi = p_lo + nb * BATCH
+    off = off_all[p_lo:p_hi + 1] - off_all[p_lo]
+    row0, n_rows = int(off_all[p_lo]), int(off[-1])
+    batch_rows = np.diff(off[::BATCH])
+    rows_pad = int((batch_rows.max() + 127) // 128 * 128)
+    dm = ml.DeviceModel(params, ml.PREC_BF16X3, max_rows=rows_pad)
+    ld = dm.packed_ld
+    X = torch.empty((n_rows, ld), dtype=torch.float32, device="cuda")
+    Y = torch.empty(nb * BATCH, dtype=torch.float32, device="cuda")
+    OFF = torch.from_numpy(off).cuda()
+    assert L.moses_synth_features_device(SEED_DATA, row0, n_rows, DIMS[0], ml.DTYPE_F32, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(SEED_DATA, p_lo, nb * BATCH, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    dp = DataParallel(ml, dm, world, dist)
+    L.moses_set_async(1)
+    # one CUDA graph per step: device gather of the batch's programs -> pooled gradients [-> update]
+    ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, BATCH,
+                                             rows_pad, LR, MU, int(world == 1)))
+
+    def run_k(k):
+        if world == 1:
+            ml._ck(L.moses_train_graph_launch(dm.h, k))
+            return
+        for _ in range(k):
+            ml._ck(L.moses_train_graph_launch(dm.h, 1))
+            dp.step_tail(LR, MU)
+
+    out = {}
+    with torch.cuda.stream(stream):
+        run_k(args.warmup)
+        torch.cuda.synchronize()
+        launches0 = ml.kernel_launches()
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            windows = timed_windows(run_k, args.steps, stream, world, dist)
+        launches = (ml.kernel_launches() - launches0) // len(windows)
+        ms_step = median(windows) / args.steps
+        out["value"] = world * BATCH / (ms_step / 1e3)
+        out["ms_per_step"] = ms_step
+        out["windows_ms"] = windows
+        out["gpu_launches"] = int(launches)
+        out["clocks"] = clk.summary()
+
+        # the same step with a 256 MiB L2 flush before each one (reported, not the headline)
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        nfl = 100
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nfl)]
+        for k in range(nfl):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            run_k(1)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        out["ms_per_step_l2_flushed"] = sum(a.elapsed_time(b) for a, b in evs) / nfl
+        del flush
+
+        # device-time attribution: the same step through the eager C-ABI calls with CUDA events
+        # around every kernel class on its launch stream (a separate pass: events perturb timing)
+        xb = np.ascontiguousarray(X[: int(batch_rows[0]), : DIMS[0]].double().cpu().numpy())
+        ob = np.ascontiguousarray(off[: BATCH + 1])
+        yb = np.ascontiguousarray(Y[:BATCH].double().cpu().numpy())
+        for _ in range(3):
+            ml._ck(L.moses_gradients_pooled(dm.h, xb.ctypes.data, xb.shape[0], DIMS[0], ob.ctypes.data, BATCH,
+                                            yb.ctypes.data, None))
+        ml.profile_begin()
+        for _ in range(args.profile_steps):
+            ml._ck(L.moses_gradients_pooled(dm.h, xb.ctypes.data, xb.shape[0], DIMS[0], ob.ctypes.data, BATCH,
+                                            yb.ctypes.data, None))
+            ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
+        torch.cuda.synchronize()
+        out["prof"] = ml.profile_end()
+        out["rows_per_step"] = n_rows / nb
+        out["rows_pad"] = rows_pad
+
+        # end to end through the reference-facing C ABI with host buffers: every step uploads its
+        # batch's float64 statement rows, CSR offsets and labels from pinned host memory and reads its
+        # loss back. N = 1: moses_train_step_pooled_async (upload of step k+1 overlapping step k);
+        # N > 1: moses_gradients_pooled + all-reduce + moses_apply_update.
+        L.moses_set_async(0)
+        nhb = 4
+        host = []
+        for hb in range(nhb):
+            lo, hi = int(off[hb * BATCH]), int(off[(hb + 1) * BATCH])
+            host.append((torch.from_numpy(np.ascontiguousarray(X[lo:hi, : DIMS[0]].double().cpu().numpy())).pin_memory(),
+                         torch.from_numpy(np.ascontiguousarray(off[hb * BATCH:(hb + 1) * BATCH + 1] - lo)).pin_memory(),
+                         torch.from_numpy(np.ascontiguousarray(Y[hb * BATCH:(hb + 1) * BATCH].double().cpu().numpy()))
+                         .pin_memory()))
+        e2e_steps = max(E2E_MIN_STEPS, args.steps)
+        losses = torch.zeros(e2e_steps + 64, dtype=torch.float64).pin_memory()
+        loss = C.c_double()
+        step_args = [(xh.data_ptr(), xh.shape[0], oh.data_ptr(), yh.data_ptr()) for xh, oh, yh in host]
+        loss_ptrs = [losses[k:k + 1].data_ptr() for k in range(e2e_steps + 64)]
+        async_step = L.moses_train_step_pooled_async
+        rcs = []
+
+        def e2e_step(k):
+            xp, ns, op, yp = step_args[k % nhb]
+            if world == 1:
+                rcs.append(async_step(dm.h, xp, ns, DIMS[0], op, BATCH, yp, LR, MU, loss_ptrs[k]))
+                return
+            ml._ck(L.moses_gradients_pooled(dm.h, xp, ns, DIMS[0], op, BATCH, yp, C.byref(loss)))
+            dp.step_tail(LR, MU)
+
+        for k in range(max(args.warmup, 300)):  # slot graphs captured, copy pipeline in steady state
+            e2e_step(e2e_steps + (k % 64))
+        ml._ck(L.moses_model_synchronize(dm.h))
+        torch.cuda.synchronize()
+        import gc
+
+        e2e_windows = []
+        for _ in range(3):
+            if world > 1:
+                dist.barrier()
+            gc.disable()
+            t0 = time.perf_counter()
+            for k in range(e2e_steps):
+                e2e_step(k)
+            ml._ck(L.moses_model_synchronize(dm.h))
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            gc.enable()
+            if world > 1:
+                t = torch.tensor([dt], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
+            e2e_windows.append(dt)
+        if any(rcs):
+            ml._ck(next(r for r in rcs if r))
+        assert world > 1 or (bool(torch.isfinite(losses[:e2e_steps]).all()) and float(losses[e2e_steps - 1]) > 0)
+        h2d = int(np.mean([sum(t.numel() * t.element_size() for t in hb) for hb in host]))
+        out["e2e"] = {"value": world * BATCH * e2e_steps / median(e2e_windows), "unit": "samples/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "steps_per_window": e2e_steps,
+                      "windows_samples_per_s": [world * BATCH * e2e_steps / w for w in e2e_windows],
+                      "path": ("moses_train_step_pooled_async (C ABI: pinned host float64 rows/offsets/labels "
+                               "uploaded every step, upload of step k+1 overlapping step k, per-step loss read "
+                               "back; 4 distinct host batches)") if world == 1 else
+                              "moses_gradients_pooled + all-reduce + moses_apply_update (C ABI, pinned host buffers)"}
+    out["dataset_bytes"] = int(X.numel() * X.element_size())
+    dm.close()
+    del X, Y
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_cfg5(ml, L, args, rank, world, dist, peaks):
+    """cfg5 shape: TenSet-scale training of {164,512,512,1} on 2M single-statement programs, batch 4096
+    per GPU (throughput-mode data parallel at N > 1), split bf16, graph replay. The GEMM roofline of
+    the step at a batch where the chains are throughput- rather than latency-bound."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2201_05752_b200.distributed import shard_range
+
+    dims, programs, batch = [164, 512, 512, 1], 2_000_000, 4096
+    lo, hi = shard_range(programs, rank, world)
+    nb = (hi - lo) // batch
+    dm = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16X3, max_rows=batch)
+    ld = dm.packed_ld
+    X = torch.empty((nb * batch, ld), dtype=torch.float32, device="cuda")
+    Y = torch.empty(nb * batch, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(SEED_DATA + 5, lo, nb * batch, dims[0], ml.DTYPE_F32, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(SEED_DATA + 5, lo, nb * batch, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    sp = C.c_void_p()
+    L.moses_model_stream(dm.h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    dp = DataParallel(ml, dm, world, dist)
+    L.moses_set_async(1)
+    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, batch, LR, MU, int(world == 1)))
+
+    def run_k(k):
+        if world == 1:
+            ml._ck(L.moses_train_graph_launch(dm.h, k))
+            return
+        for _ in range(k):
+            ml._ck(L.moses_train_graph_launch(dm.h, 1))
+            dp.step_tail(LR, MU)
+
+    with torch.cuda.stream(stream):
+        run_k(5)
+        windows = timed_windows(run_k, 20, stream, world, dist)
+        ms = median(windows) / 20
+        xs = X[:batch]
+        ml.profile_begin()
+        for _ in range(10):
+            ml._ck(L.moses_train_step_device(dm.h, xs.data_ptr(), ld, Y.data_ptr(), batch, LR, MU, None))
+        torch.cuda.synchronize()
+        prof = ml.profile_end()
+    L.moses_set_async(0)
+    gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / 10
+    flops = gemm_flops_per_step(dims, batch)
+    peak = peaks.get("bf16_tflops_sustained", 1395.6)
+    ach = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+    dm.close()
+    del X, Y
+    torch.cuda.empty_cache()
+    return {"workload": f"cfg5: train {dims} on {programs} single-statement programs, batch {batch} per GPU, "
+                        f"split bf16, {world} GPU(s) (throughput-mode DP)",
+            "value": world * batch / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+            "timed_windows": len(windows), "steps_per_window": 20,
+            "scaling": "weak",
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak if ach else None, "mma_per_product": 3,
+                         "tensor_pipe_frac": 3 * ach / peak if ach else None, "flops_per_step": flops,
+                         "gemm_ms_per_step": gemm_ms,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                         "note": "achieved = algorithmic FLOPs / GEMM device time; split bf16 issues 3 bf16 MMAs "
+                                 "per product (tensor_pipe_frac)"},
+            "step_breakdown_ms": {k: v[0] / 10 for k, v in prof.items() if v[1]}}
+
+
+def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
+    """cfg4: score a pool of `programs` synthetic programs with the 4x512 model and select the global
+    top-1024 (score desc, index asc). N > 1: contiguous program ranges per rank (strong scaling); each
+    rank scores and top-k's its shard, the (score, global index) winners are all-gathered and merged
+    (distributed.py) — the only exchange. Features generated on the device."""
+    import ctypes as C
+
+    import numpy as np
+
+    import torch
 
     from paper_2201_05752_b200.distributed import gather_merge_topk, shard_range
 
@@ -184,12 +466,12 @@ def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
     k = 1024
     lo, hi = shard_range(programs, rank, world)
     n_local = hi - lo
-    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
-    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=chunk)
+    dm = ml.DeviceModel(ml.init_random(DIMS, SEED_MODEL, strict=False), precision, max_rows=chunk)
     ld = dm.packed_ld
-    X = torch.empty((n_local, ld), dtype=torch.bfloat16, device="cuda")
+    dt_in = ml.input_dtype(precision)
+    X = torch.empty((n_local, ld), dtype=torch.bfloat16 if dt_in == ml.DTYPE_BF16 else torch.float32, device="cuda")
     S = torch.empty(n_local, dtype=torch.float32, device="cuda")
-    assert L.moses_synth_features_device(SEED_DATA + 100, lo, n_local, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+    assert L.moses_synth_features_device(SEED_DATA + 100, lo, n_local, DIMS[0], dt_in, X.data_ptr(), ld) == 0
     torch.cuda.synchronize()
     idx = (C.c_int64 * k)()
     sp = C.c_void_p()
@@ -197,7 +479,6 @@ def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
     stream = torch.cuda.ExternalStream(sp.value)
 
     def one_pass():
-        """forward (device-timed) + local top-k + global merge; returns (seconds, forward ms, winners)"""
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
@@ -205,17 +486,13 @@ def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
         t0 = time.perf_counter()
         with torch.cuda.stream(stream):
             a.record(stream)
-            ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, n_local, S.data_ptr()))
+            ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), dt_in, ld, n_local, S.data_ptr()))
             b.record(stream)
         torch.cuda.synchronize()
         kk = min(k, n_local)
         ml._ck(L.moses_topk_device(S.data_ptr(), n_local, kk, idx))
         li = np.array(idx[:kk], dtype=np.int64)
-        if world > 1:
-            ls = S[torch.from_numpy(li).cuda()].cpu().numpy()
-            win = gather_merge_topk(ls, li + lo, k)
-        else:
-            win = li
+        win = gather_merge_topk(S[torch.from_numpy(li).cuda()].cpu().numpy(), li + lo, k) if world > 1 else li
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device="cuda", dtype=torch.float64)
@@ -229,457 +506,63 @@ def bench_infer(ml, L, programs, peaks, rank=0, world=1, reps=3):
         dt, fm, win = one_pass()
         times.append(dt)
         fwd_ms.append(fm)
-    ml.profile_begin()
-    with torch.cuda.stream(stream):
-        L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, n_local, S.data_ptr())
-        torch.cuda.synchronize()
-    prof = ml.profile_end()
     best = min(times)
-    flops_prog = sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 1))
-    # achieved: the hidden-layer GEMM FLOPs over the device time of the WHOLE forward (all GEMM
-    # launches plus the per-chunk head sums), CUDA events on the model stream (this rank)
-    gemm_s = min(fwd_ms) / 1000.0
     gemm_flops = n_local * sum(2 * DIMS[l] * DIMS[l + 1] for l in range(len(DIMS) - 2))
-    peak = peaks.get("bf16_tflops_sustained", 1408.7)
-    ach = gemm_flops / gemm_s / 1e12 if gemm_s else None
+    peak = peaks.get("bf16_tflops_sustained", 1395.6)
+    ach = gemm_flops / (min(fwd_ms) / 1e3) / 1e12
+    split = precision == ml.PREC_BF16X3
+    dm.close()
     del X
     torch.cuda.empty_cache()
     return {"metric": "cost-model programs/sec (infer)", "value": programs / best, "unit": "programs/s",
-            "workload": f"cfg4: score {programs} synthetic programs with {DIMS} (bf16), global top-{k}, "
-                        f"{world} GPU(s), contiguous program shards",
+            "precision": "bf16x3 (split bf16, in tolerance)" if split else "bf16 (throughput mode)",
+            "workload": f"cfg4: score {programs} synthetic programs with {DIMS}, global top-{k}, {world} GPU(s), "
+                        f"contiguous program shards",
             "scaling": "strong", "programs_per_gpu": n_local, "first_winners": [int(v) for v in win[:4]],
-            "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms), "flops_per_program": flops_prog,
-            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak if ach else None,
-                         "kernel": "umma_fwd_pair (tcgen05 cta_group::2, weight-resident; gemm_fwd2.cuh)",
-                         "forward_device_ms": min(fwd_ms), "gemm_launches": prof["gemm_fwd"][1]},
-            "inputs": "device-resident bf16 packed features (3.4 GB over all GPUs > L2)",
+            "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "mma_per_product": 3 if split else 1,
+                         "kernel": "mlp_chain_split_kernel (fused split-bf16 chain)" if split else
+                                   "umma_fwd_pair (tcgen05 cta_group::2, weight-resident)",
+                         "forward_device_ms": min(fwd_ms)},
+            "inputs": f"device-resident {'fp32' if dt_in == ml.DTYPE_F32 else 'bf16'} packed features (> L2)",
             "timing": "wall clock per pass (device forward + local top-k + all-gather merge), max over ranks"}
 
 
-def bench_hbm_kernels(ml, L, peaks):
-    """HBM-roofline kernels of the north star on L2-exceeding sizes (> 126 MB working sets):
-    fused lottery step (xi -> partition -> step -> decay), momentum update, segment-sum pooling,
-    candidate top-k. achieved = algorithmic bytes / device time."""
-    import ctypes as C
-
+def bench_cfg1(ml, L):
+    """cfg1: the reference's CPU-runnable case — {164,256,256,1} (2x256 hidden) scoring 4,096 programs,
+    fp32 parity mode (3xTF32, <= 1e-5 of fp64), through moses_predict with host float64 rows."""
     import numpy as np
 
-    import torch
-
-    from paper_2201_05752_b200.distributed import device_gradient_tensor
-
-    hbm = peaks.get("hbm_gbs", 6534.1)
-    out = {}
-
-    def timed(fn, stream, reps=5):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps / 1000.0
-
-    # ---- parameter-vector kernels on a 268M-scalar model (1 GB per fp32 array)
-    dims = [32768, 8192, 8, 1]
-    P = ml.param_count(dims)
-    dm = ml.DeviceModel(ml.CostModelParams(dims, np.zeros(P)), ml.PREC_BF16, max_rows=128)
-    sp = C.c_void_p()
-    L.moses_model_stream(dm.h, C.byref(sp))
-    st = torch.cuda.ExternalStream(sp.value)
-    wptr = C.POINTER(C.c_float)()
-    L.moses_model_device_ptrs(dm.h, C.byref(wptr), None, None)
-
-    class _CAI:
-        def __init__(self, ptr, n):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
-
-    w = torch.as_tensor(_CAI(C.cast(wptr, C.c_void_p).value, P), device="cuda")
-    g = device_gradient_tensor(dm)
-    gen = torch.Generator(device="cuda").manual_seed(0)
-    w.normal_(0, 0.05, generator=gen)
-    g.normal_(0, 1e-2, generator=gen)
-    g[torch.rand(P, device="cuda", generator=gen) < 0.4] = 0.0  # zero-gradient ties (README.md:106-113)
-    torch.cuda.synchronize()
-    pop = C.c_int64()
-    for mode, value, name in ((2, 0.5, "lottery_step_ratio0.5"), (1, 0.5, "lottery_step_threshold0.5")):
-        t = timed(lambda: ml._ck(L.moses_lottery_step(dm.h, mode, value, 0, 1e-3, 1e-2, None, 0, C.byref(pop))), st)
-        algo = 15.0 * P  # read w,g; write w; mask byte; bf16 operand shadow
-        out[name] = {"params": P, "ms": t * 1e3, "algorithmic_bytes": algo, "achieved_gbs": algo / t / 1e9,
-                     "frac": algo / t / 1e9 / hbm, "bytes_per_param": 15}
-    L.moses_set_async(1)
-    t = timed(lambda: ml._ck(L.moses_apply_update(dm.h, 1e-3, 0.9, None, 0, 1)), st)
-    L.moses_set_async(0)
-    algo = 22.0 * P  # read w,v,g; write w,v; bf16 shadow
-    out["momentum_update"] = {"params": P, "ms": t * 1e3, "algorithmic_bytes": algo, "achieved_gbs": algo / t / 1e9,
-                              "frac": algo / t / 1e9 / hbm, "bytes_per_param": 22}
-    del w, g
-    dm.close()
-    torch.cuda.empty_cache()
-
-    # ---- segment-sum pooling: 4M statement rows x 512 bf16 -> programs x 512 fp32
-    programs = 900_000
-    off = ml.synth_offsets(11, programs, MAX_STMTS)
-    rows = int(off[-1])
-    H = torch.empty((rows, 512), dtype=torch.bfloat16, device="cuda").normal_(generator=gen)
-    OFF = torch.from_numpy(off).cuda()
-    PO = torch.empty((programs, 512), dtype=torch.float32, device="cuda")
-    cur = torch.cuda.current_stream()
-    t = timed(lambda: ml._ck(L.moses_segment_sum_device(H.data_ptr(), ml.DTYPE_BF16, 512, 512, OFF.data_ptr(),
-                                                        programs, PO.data_ptr())), cur)
-    algo = rows * 512 * 2 + programs * 512 * 4 + (programs + 1) * 8
-    out["segment_sum_pooling"] = {"rows": rows, "programs": programs, "ms": t * 1e3, "algorithmic_bytes": algo,
-                                  "achieved_gbs": algo / t / 1e9, "frac": algo / t / 1e9 / hbm}
-    del H, PO
-    torch.cuda.empty_cache()
-
-    # ---- candidate top-k over 100M fp32 scores (k = 1024)
-    n = 100_000_000
-    Sc = torch.empty(n, dtype=torch.float32, device="cuda").normal_(generator=gen)
-    idx = (C.c_int64 * 1024)()
-    ml._ck(L.moses_topk_device(Sc.data_ptr(), n, 1024, idx))
-    t0 = time.perf_counter()
-    for _ in range(3):
-        ml._ck(L.moses_topk_device(Sc.data_ptr(), n, 1024, idx))
-    t = (time.perf_counter() - t0) / 3
-    out["topk_100M"] = {"n": n, "k": 1024, "ms": t * 1e3, "algorithmic_bytes": 4 * n, "achieved_gbs": 4 * n / t / 1e9,
-                        "frac": 4 * n / t / 1e9 / hbm, "note": "wall clock incl. one host sync"}
-    del Sc
-    torch.cuda.empty_cache()
-    out["peak_gbs"] = hbm
-    out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs"
-    return out
-
-
-def bench_finetune(ml, L, peaks, reps=20):
-    """cfg3: Moses fine-tuning source -> target on the 4x512 model (P = 872,961): one step is the
-    tuner.cpp:251-262 Moses branch through the reference-facing C ABI with host buffers
-    (gradients with the reversed-BCE adversary over 256 replay rows, beta = 0.01 -> discriminator
-    step -> fused lottery step: xi -> ratio 0.5 partition -> transferable step -> variant decay),
-    plus the MMD^2 discrepancy between 50k source and 5k target 512-d representations
-    (device-resident, tensor-core Gram tiles)."""
-    import ctypes as C
-
-    import numpy as np
-
-    import torch
-
-    out = {}
-    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
-    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=1024)
-    rng = np.random.default_rng(3)
-    replay = rng.random((256, DIMS[0]))
-    adv = ml.AdversaryState(replay, DIMS[-2])
-    xt = np.ascontiguousarray(rng.random((BATCH, DIMS[0])))
-    yt = np.ascontiguousarray(0.1 + rng.random(BATCH))
-    loss = C.c_double()
-    dl, cf = C.c_double(), C.c_double()
-    pop = C.c_int64()
-
-    def step():
-        ml._ck(L.moses_gradients(dm.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], adv.h, 0.01, C.byref(loss)))
-        ml._ck(L.moses_adversarial_step(adv.h, dm.h, xt.ctypes.data, BATCH, DIMS[0], 0.01, C.byref(dl), C.byref(cf)))
-        ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
-
-    for _ in range(3):
-        step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / reps
-    out["moses_step"] = {"ms": dt * 1e3, "samples_per_s": BATCH / dt, "batch": BATCH, "replay": 256,
-                         "params": len(params.params),
-                         "path": "moses_gradients(adv, beta=0.01) + moses_adversarial_step + moses_lottery_step "
-                                 "(ratio 0.5), host float64 buffers, wall clock"}
-
-    def fused_step():
-        ml._ck(L.moses_moses_step(dm.h, adv.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], 0.01, 2, 0.5, 0, 1e-3,
-                                  1e-2, C.byref(loss), C.byref(dl), C.byref(pop)))
-
-    for _ in range(3):
-        fused_step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        fused_step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / reps
-    out["moses_step_fused"] = {"ms": dt * 1e3, "samples_per_s": BATCH / dt,
-                               "path": "moses_moses_step: the same three steps in one C-ABI call (the discriminator "
-                                       "step reuses the gradients' forward; one host sync), bit-identical"}
-    # the lottery step alone at the real parameter count (L2-resident: launch/latency bound)
-    sp = C.c_void_p()
-    L.moses_model_stream(dm.h, C.byref(sp))
-    st = torch.cuda.ExternalStream(sp.value)
-    L.moses_set_async(1)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(reps):
-        ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
-    b.record(st)
-    torch.cuda.synchronize()
-    L.moses_set_async(0)
-    out["lottery_step_real_P"] = {"ms": a.elapsed_time(b) / reps, "params": len(params.params),
-                                  "note": "device time per fused ratio-0.5 step; w, g L2-resident"}
-    del adv
-    dm.close()
-    # MMD^2 over 50k source / 5k target penultimate representations
-    m_s, n_t, w = 50_000, 5_000, DIMS[-2]
-    gen = torch.Generator(device="cuda").manual_seed(5)
-    H = torch.rand((m_s + n_t, w), device="cuda", generator=gen)
-    H[m_s:] += 0.05
-    res = C.c_double()
-    sig = float(np.sqrt(w / 6.0))
-
-    def mmd():
-        ml._ck(L.moses_mmd2_device(C.c_void_p(H.data_ptr()), m_s, C.c_void_p(H[m_s:].data_ptr()), n_t, w, w, sig,
-                                   C.byref(res)))
-
-    mmd()
-    ml.profile_begin()
-    mmd()
-    prof = ml.profile_end()
-    t0 = time.perf_counter()
-    for _ in range(5):
-        mmd()
-    dt = (time.perf_counter() - t0) / 5
-    flops = 2.0 * w * (m_s * (m_s + 1) / 2 + n_t * (n_t + 1) / 2 + m_s * n_t)
-    dev_ms = prof.get("other", (None,))[0]
-    peak = peaks.get("bf16_tflops_sustained", 1408.7) / 2.0
-    ach = flops / (dev_ms / 1e3) / 1e12 if dev_ms else None
-    out["mmd2"] = {"source": m_s, "target": n_t, "width": w, "value": res.value, "ms_wall": dt * 1e3,
-                   "ms_device": dev_ms, "flops_unique_pairs": flops,
-                   "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                                "frac": ach / peak if ach else None,
-                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained / 2 (dense tf32 rate)",
-                                "kernel": "umma_gram_kernel (tcgen05 kind::tf32, exp-sum epilogue)"}}
-    del H
-    torch.cuda.empty_cache()
-    return out
-
-
-def bench_search(ml, L, peaks):
-    """the scorer's input path on the device — enumerate a 10.2M-config knob
-    space (6 knobs; space.cpp:168-191 order), encode the 16-d features (space.cpp:140-159) straight
-    into packed bf16 model rows plus FNV-1a hashes (space.cpp:193-197), score with the reference's
-    {16,512,512,1} model and select the top-1024. No host features, no PCIe."""
-    import ctypes as C
-
-    import numpy as np
-
-    import torch
-
-    knobs = [("tile_x", [1 << i for i in range(16)]), ("tile_y", [1 << i for i in range(16)]),
-             ("unroll", [0, 1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 128, 256, 512]),
-             ("vectorize", [1 << i for i in range(8)]), ("parallel", [1 << i for i in range(13)]),
-             ("split", list(range(1, 25)))]
-    n = int(np.prod([len(d) for _, d in knobs]))
-    task = (2.0, 8.0, 9.0, 5.0)
-    dims = [16, 512, 512, 1]
-    dm = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16, max_rows=65536)
-    ld = dm.packed_ld
-    F = torch.empty((n, ld), dtype=torch.bfloat16, device="cuda")
-    Hh = torch.empty(n, dtype=torch.int64, device="cuda")
-    S = torch.empty(n, dtype=torch.float32, device="cuda")
-    idx = (C.c_int64 * 1024)()
-
-    def encode():
-        ml.encode_configs_device(task, knobs, 0, n, ml.DTYPE_BF16, C.c_void_p(F.data_ptr()), ld, dims[0],
-                                 C.c_void_p(Hh.data_ptr()))
-
-    def score():
-        ml._ck(L.moses_predict_device(dm.h, C.c_void_p(F.data_ptr()), ml.DTYPE_BF16, ld, n, C.c_void_p(S.data_ptr())))
-        torch.cuda.synchronize()
-        ml._ck(L.moses_topk_device(C.c_void_p(S.data_ptr()), n, 1024, idx))
-
-    encode()
-    score()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    encode()
-    b.record()
-    torch.cuda.synchronize()
-    enc_ms = a.elapsed_time(b)
-    t0 = time.perf_counter()
-    encode()
-    score()
-    total = time.perf_counter() - t0
-    wbytes = n * (ld * 2 + 8)
-    hbm = peaks.get("hbm_gbs", 6534.1)
-    # f3: simulated-hardware labels (oracle.cpp:65-88) for the whole space, and its exhaustive optimum
-    server = {"id": "server", "peak_gflops": 8000.0, "parallel_units": 16.0, "vector_lanes": 8.0,
-              "cache_bytes": 2000000.0, "measure_overhead_ms": 2.0, "noise_std": 0.05, "repeats": 3}
-    lab = torch.empty(n, dtype=torch.float32, device="cuda")
-    ml.measure_configs_device(server, "conv3x3_64", task, knobs, 1, 0, n, label_ptr=C.c_void_p(lab.data_ptr()))
-    a.record()
-    ml.measure_configs_device(server, "conv3x3_64", task, knobs, 1, 0, n, label_ptr=C.c_void_p(lab.data_ptr()))
-    b.record()
-    torch.cuda.synchronize()
-    label_ms = a.elapsed_time(b)
-    t0 = time.perf_counter()
-    best, best_lat = ml.true_best(server, task, knobs)
-    tb_ms = (time.perf_counter() - t0) * 1e3
-    del lab
-    # evolve (search.cpp:41-71) with the reference SearchParams (128 / 4 generations / 32 survivors x
-    # 4 mutants) on the default knob template, scored by the {16,512,512,1} model on the device
-    dknobs = [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
-              ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
-    em = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16, 1024)
-    ml.evolve(em, task, dknobs, seed=1)
-    t0 = time.perf_counter()
-    for r in range(10):
-        ml.evolve(em, task, dknobs, seed=r)
-    evolve_ms = (time.perf_counter() - t0) / 10 * 1e3
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
 
-    wts = orc.init_random(dims, SEED_MODEL)
-    sizes = [len(d) for _, d in dknobs]
-
-    def cpu_scorer(cfgs):
-        rows = []
-        for c in cfgs:
-            i = 0
-            for k, x in enumerate(c):
-                i = i * sizes[k] + dknobs[k][1].index(x)
-            rows.append(orc.encode_configs(task, dknobs, i, 1)[0][0])
-        return list(orc.forward(dims, wts, np.stack(rows))[0])
-
+    dims, n = [164, 256, 256, 1], 4096
+    p = ml.init_random(dims, SEED_MODEL, strict=False)
+    x = orc.synth_features(SEED_DATA, 0, n, dims[0])
+    dm = ml.DeviceModel(p, ml.PREC_FP32, n)
+    s = ml.predict(dm, x)
     t0 = time.perf_counter()
-    orc.evolve(dknobs, cpu_scorer, seed=1)
-    evolve_cpu_ms = (time.perf_counter() - t0) * 1e3
-    em.close()
-    out = {"configs": n, "knobs": len(knobs), "model": dims, "encode_ms": enc_ms,
-           "encode_roofline": {"bound": "hbm", "achieved": wbytes / (enc_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                               "frac": wbytes / (enc_ms / 1e3) / 1e9 / hbm,
-                               "algorithmic_bytes": wbytes, "note": "packed bf16 rows + u64 hashes written"},
-           "pipeline_ms": total * 1e3, "configs_per_s": n / total,
-           "labels_ms": label_ms, "labels_per_s": n / (label_ms / 1e3),
-           "true_best": {"values": best, "latency_ms": best_lat, "ms": tb_ms,
-                         "note": "exhaustive noise-free optimum over the 10.2M-config space (oracle.cpp:90-105)"},
-           "pipeline": "encode_configs (device) -> predict (tcgen05) -> top-1024, wall clock",
-           "evolve": {"ms": evolve_ms, "cpu_oracle_ms": evolve_cpu_ms,
-                      "params": "population 128, 4 generations, 32 survivors x 4 mutants, eps 0.05 (SearchParams)",
-                      "path": "moses_evolve: device encode from enumeration indices + tcgen05 scoring per "
-                              "generation; host RngStream walk and sort; CPU: fp64 oracle forward, 1 thread"}}
-    del F, Hh, S
-    torch.cuda.empty_cache()
-    return out
-
-
-def bench_pretrain(ml, L, peaks, epochs: int = 30, per_task: int = 6000):
-    """the reference's own offline flow — `moseslab gen-dataset --samples 6000`
-    on the 8 default tasks / server device (data.cpp:49-65, cli.cpp:344) then `pretrain` with the
-    default TrainHyper (30 epochs, batch 512, lr 0.001, momentum 0.9; tuner.cpp:130-156) on
-    {16,512,512,1}: dataset generated on the device, per-epoch keyed shuffles / single-task chunking
-    on the host overlapped with the device epochs, batches gathered on the device."""
-    import ctypes as C
-
-    import numpy as np
-
-    import torch
-
-    lab = json.load(open(os.path.join(ROOT, "paper_2201_05752_b200", "configs", "lab.json")))
-    device = lab["devices"]["server"]
-    tasks = [(t["id"], (t["work_gflops"], t["bytes_per_unit"], t["ideal_log2_tiles"], t["ideal_log2_unroll"]))
-             for t in lab["tasks"]]
-    knobs = [("tile_x", [1, 2, 4, 8, 16, 32, 64]), ("tile_y", [1, 2, 4, 8, 16, 32, 64]), ("unroll", [0, 16, 64, 512]),
-             ("vectorize", [1, 2, 4, 8, 16]), ("parallel", [1, 2, 4, 8, 16, 32, 64, 128, 256])]
-    dims = [16, 512, 512, 1]
-    seed = 0
-    dm = ml.DeviceModel(ml.init_random(dims, seed), ml.PREC_BF16, 512)
-    ld = dm.packed_ld
-    n = per_task * len(tasks)
-    X = torch.zeros((n, ld), dtype=torch.bfloat16, device="cuda")
-    Y = torch.zeros(n, dtype=torch.float32, device="cuda")
-
-    def generate():
-        for t, (tid, task) in enumerate(tasks):
-            r0 = t * per_task
-            ml.generate_dataset_device(device, tid, task, knobs, per_task, 1, ml.DTYPE_BF16,
-                                       C.c_void_p(X.data_ptr() + r0 * ld * 2), ld, 16, None, None, None, None,
-                                       C.c_void_p(Y.data_ptr() + r0 * 4))
-
-    generate()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    generate()
-    torch.cuda.synchronize()
-    gen_ms = (time.perf_counter() - t0) * 1e3
-    task_of = [i // per_task for i in range(n)]
-    ids = [tid for tid, _ in tasks]
-    t0 = time.perf_counter()
-    plan = ml.make_ranking_batches(task_of, ids, 512, ml.epoch_seed(seed, 0))
-    plan_ms = (time.perf_counter() - t0) * 1e3
-    ml.pretrain_device(dm, C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids, 512, seed, 1)  # warm
-    dm.upload(ml.init_random(dims, seed))
-    torch.cuda.synchronize()
-    k0 = L.moses_kernel_launches()
-    t0 = time.perf_counter()
-    losses, dropped = ml.pretrain_device(dm, C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids,
-                                         512, seed, epochs, 0.001, 0.9)
-    total = time.perf_counter() - t0
-    launches = L.moses_kernel_launches() - k0
-    # SURVEY.md §8(f) f4 shape: a (seed) job grid of independent pretrain runs on the native worker
-    # pool, one handle (and stream set) per job, sharing the device-resident store
-    n_jobs = 8
-    jobs = [ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16, 512) for s in range(n_jobs)]
-    ml.pretrain_jobs(jobs, list(range(n_jobs)), C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids,
-                     512, 1, 0.001, 0.9, n_jobs)  # warm (graph capture per handle)
-    for j, jm in enumerate(jobs):
-        jm.upload(ml.init_random(dims, j))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    job_losses, _ = ml.pretrain_jobs(jobs, list(range(n_jobs)), C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()),
-                                     task_of, ids, 512, epochs, 0.001, 0.9, n_jobs)
-    jobs_s = time.perf_counter() - t0
-    for jm in jobs:
-        jm.close()
-    # the same loop on the fp64 CPU oracle: a bounded sample of epoch 0's batches
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-
-    threads = os.cpu_count() or 1
-    feats = X[:, :16].float().double().cpu().numpy()
-    labels = Y.double().cpu().numpy()
-    w = orc.init_random(dims, seed)
-    mom = np.zeros_like(w)
-    nb = min(len(plan), 24)
-    t0 = time.perf_counter()
-    for b in range(nb):
-        _, rows = plan.batch(b)
-        orc.train_step_f64(dims, w, mom, feats[rows], labels[rows], 0.001, 0.9, threads)
-    cpu_dt = time.perf_counter() - t0
-    cpu_rows = int(plan.off[nb])
-    del X, Y
-    torch.cuda.empty_cache()
-    return {"workload": f"gen-dataset --samples {per_task} (8 default tasks, server) + pretrain {epochs} epochs, "
-                        f"batch 512, {dims}, bf16",
-            "records": n, "batches_per_epoch": len(plan), "dropped_singletons": dropped,
-            "generate_ms": gen_ms, "plan_ms_host": plan_ms,
-            "pretrain_s": total, "samples_per_s": epochs * n / total, "ms_per_epoch": total / epochs * 1e3,
-            "epoch_mean_loss_first_last": [losses[0], losses[-1]], "gpu_launches": int(launches),
-            "job_grid": {"jobs": n_jobs, "workers": n_jobs, "wall_s": jobs_s,
-                         "samples_per_s": n_jobs * epochs * n / jobs_s,
-                         "speedup_vs_sequential": n_jobs * total / jobs_s,
-                         "path": "moses_pretrain_jobs: 8 seeds x 30 epochs, one handle/stream set per job"},
-            "cpu_oracle": {"samples_per_s": cpu_rows / cpu_dt, "cores": threads, "kind": "port",
-                           "sample": f"{nb} batches ({cpu_rows} rows) of epoch 0, fp64"},
-            "path": "moses_generate_dataset_device x8 -> moses_pretrain_device (host plan of epoch e+1 overlapped "
-                    "with device epoch e; full batches replay one CUDA graph), wall clock"}
+    reps = 50
+    for _ in range(reps):
+        s = ml.predict(dm, x)
+    dt = (time.perf_counter() - t0) / reps
+    ref, _ = orc.forward(dims, p.params, x, threads=os.cpu_count() or 1)
+    t1 = time.perf_counter()
+    orc.forward(dims, p.params, x, threads=1)
+    cpu1 = time.perf_counter() - t1
+    err = float(np.max(np.abs(s - ref)) / np.max(np.abs(ref)))
+    dm.close()
+    return {"workload": f"cfg1: score {n} programs with {dims}, fp32 parity mode (3xTF32)", "ms": dt * 1e3,
+            "programs_per_s": n / dt, "normwise_err_vs_fp64": err,
+            "path": "moses_predict (host float64 rows in, scores out; H2D + 2 split GEMMs + head + D2H)",
+            "cpu_oracle_1thread": {"ms": cpu1 * 1e3, "programs_per_s": n / cpu1}}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -688,11 +571,17 @@ def main():
     ap.add_argument("--no-finetune", action="store_true")
     ap.add_argument("--no-pretrain", action="store_true")
     ap.add_argument("--no-search", action="store_true")
-    ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--infer-programs", type=int, default=10_000_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.steps = max(args.steps, 1)
+    if args.headline_only:
+        args.no_infer = args.no_hbm = args.no_finetune = args.no_pretrain = args.no_search = args.no_cfg5 = True
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -700,276 +589,105 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2201_05752_b200 import moseslab as ml
 
-    # --share-gpu: every rank on cuda:0 with the gloo backend — a functional check of the N > 1 path
-    # (sharding, gradient averaging, max-over-ranks timing) on a one-GPU box; never a bench number
-    dev = 0 if args.share_gpu else local
-    torch.cuda.set_device(dev)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    torch.cuda.set_device(local)
     if world > 1:
-        if args.share_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = ml.lib()
     if L.moses_device_check() != 0:
         raise SystemExit("moses: " + L.moses_last_error().decode())
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        tp = json.load(open(os.path.join(ROOT, "profiles", "measured_tf32_peak.json")))
+        peaks["tf32_tflops_sustained"] = tp["tf32_tflops_sustained"]
+        peaks["tf32_source"] = "profiles/measured_tf32_peak.json (tools/measure_tf32_peak.py, this pool's B200)"
+    except Exception:  # noqa: BLE001
+        pass
 
-    # ---------------- model + device-resident TenSet-shaped dataset (this rank's shard of programs)
-    from paper_2201_05752_b200.distributed import device_gradient_tensor, shard_range
-
-    params = ml.init_random(DIMS, SEED_MODEL, strict=False)
-    off_all = ml.synth_offsets(SEED_DATA, PROGRAMS, MAX_STMTS)
-    p_lo, p_hi = shard_range(PROGRAMS, rank, world)
-    nb = (p_hi - p_lo) // BATCH
-    p_hi = p_lo + nb * BATCH
-    off = off_all[p_lo:p_hi + 1] - off_all[p_lo]
-    row0, n_rows = int(off_all[p_lo]), int(off[-1])
-    batch_rows = np.diff(off[::BATCH])
-    rows_pad = int((batch_rows.max() + 127) // 128 * 128)
-    dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=rows_pad)
-    ld = dm.packed_ld
-    X = torch.empty((n_rows, ld), dtype=torch.bfloat16, device="cuda")
-    Y = torch.empty(nb * BATCH, dtype=torch.float32, device="cuda")
-    OFF = torch.from_numpy(off).cuda()
-    assert L.moses_synth_features_device(SEED_DATA, row0, n_rows, DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
-    assert L.moses_synth_labels_device(SEED_DATA, p_lo, nb * BATCH, Y.data_ptr()) == 0
-    torch.cuda.synchronize()
-
-    import ctypes as C
-
-    sp = C.c_void_p()
-    L.moses_model_stream(dm.h, C.byref(sp))
-    stream = torch.cuda.ExternalStream(sp.value)
-    grads = device_gradient_tensor(dm)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
-    L.moses_set_async(1)
-
-    # One CUDA graph per step: device-side gather of the batch's programs (variable statement counts)
-    # -> pooled gradients [-> update].
-    ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, BATCH,
-                                             rows_pad, LR, MU, int(world == 1)))
-
-    def grad_avg(t):  # NCCL averages in the collective; gloo (--share-gpu check) has no AVG
-        if args.share_gpu:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-            t.div_(world)
-        else:
-            dist.all_reduce(t, op=dist.ReduceOp.AVG)
-
-    def step(b):
-        ml._ck(L.moses_train_graph_launch(dm.h, 1))
-        if world > 1:
-            grad_avg(grads)
-            ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
-
-    # host copies of one batch for the eager profiling pass and the end-to-end leg
-    xb_host = np.ascontiguousarray(X[: int(batch_rows[0])].float().cpu().numpy()[:, : DIMS[0]].astype(np.float64))
-    ob_host = np.ascontiguousarray(off[: BATCH + 1])
-    yb_host = np.ascontiguousarray(Y[:BATCH].cpu().numpy().astype(np.float64))
-
-    def step_eager(b):  # profiling pass: same work without the graph (per-kernel-class events)
-        ml._ck(L.moses_gradients_pooled(dm.h, xb_host.ctypes.data, xb_host.shape[0], DIMS[0], ob_host.ctypes.data,
-                                        BATCH, yb_host.ctypes.data, None))
-        if world > 1:
-            grad_avg(grads)
-        ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
-
-    with torch.cuda.stream(stream):
-        for b in range(args.warmup):
-            step(b)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        # ---------------- timed region: K steps back to back. The inputs are larger than L2: every
-        # step gathers a different 512-program batch out of the 302 MB device-resident dataset
-        # (cold in L2); only the step's own working set (weights, optimizer state, activations,
-        # ~30 MB) stays cache-resident from one step to the next, as it does in training.
-        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches0 = ml.kernel_launches()
-        with ClockSampler(dev) as clk:
-            t0e.record(stream)
-            for k in range(args.steps):
-                step(args.warmup + k)
-            t1e.record(stream)
-            torch.cuda.synchronize()
-        launches = ml.kernel_launches() - launches0
-        total_ms = t0e.elapsed_time(t1e)
-        if world > 1:
-            t = torch.tensor([total_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total_ms = float(t.item())
-            dist.barrier()
-        ms_step = total_ms / args.steps
-        value = world * BATCH / (ms_step / 1000.0)
-
-        # ---------------- the same steps with L2 flushed before each one (256 MiB write outside
-        # per-step CUDA-event brackets): the whole working set starts cold (reported, not headline)
-        nfl = min(args.steps, 200)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nfl)]
-        for k in range(nfl):
-            flush.fill_(float(k))
-            evs[k][0].record(stream)
-            step(args.warmup + args.steps + k)
-            evs[k][1].record(stream)
-        torch.cuda.synchronize()
-        ms_step_flushed = sum(a.elapsed_time(b) for a, b in evs) / nfl
-        if world > 1:
-            t = torch.tensor([ms_step_flushed], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_step_flushed = float(t.item())
-
-        # ---------------- device-time attribution (separate pass; events perturb timing)
-        ml.profile_begin()
-        for k in range(args.profile_steps):
-            step_eager(k)
-        torch.cuda.synchronize()
-        prof = ml.profile_end()
-
-        # ---------------- end to end through the reference-facing C ABI with host buffers: every
-        # step uploads its batch's float64 statement rows, CSR offsets and labels from pinned host
-        # memory and reads its loss back. N = 1: moses_train_step_pooled_async (gradients + momentum
-        # update, the next batch's upload overlapping this step's kernels); N > 1: gradients, NCCL
-        # average, update (synchronous C ABI calls).
-        nhb = 4
-        host_batches = []
-        for hb in range(nhb):
-            lo, hi = int(off[hb * BATCH]), int(off[(hb + 1) * BATCH])
-            xb = X[lo:hi].float().cpu().numpy()[:, : DIMS[0]].astype(np.float64)
-            host_batches.append((torch.from_numpy(np.ascontiguousarray(xb)).pin_memory(),
-                                 torch.from_numpy(np.ascontiguousarray(off[hb * BATCH:(hb + 1) * BATCH + 1] - lo)).pin_memory(),
-                                 torch.from_numpy(np.ascontiguousarray(Y[hb * BATCH:(hb + 1) * BATCH].cpu().numpy()
-                                                                       .astype(np.float64))).pin_memory()))
-        e2e_steps = max(10, args.steps // 2)
-        losses = torch.zeros(e2e_steps + 64, dtype=torch.float64).pin_memory()
-        loss = C.c_double()
-        L.moses_set_async(0)
-        # per-step arguments resolved up front: the timed loop is the C-ABI call itself
-        step_args = [(xh.data_ptr(), xh.shape[0], oh.data_ptr(), yh.data_ptr()) for xh, oh, yh in host_batches]
-        loss_ptrs = [losses[k:k + 1].data_ptr() for k in range(e2e_steps + 64)]
-        async_step = L.moses_train_step_pooled_async
-        rcs = []
-
-        def e2e_step(k):
-            xp, ns, op, yp = step_args[k % nhb]
-            if world == 1:
-                rcs.append(async_step(dm.h, xp, ns, DIMS[0], op, BATCH, yp, LR, MU, loss_ptrs[k]))
-                return
-            ml._ck(L.moses_gradients_pooled(dm.h, xp, ns, DIMS[0], op, BATCH, yp, C.byref(loss)))
-            grad_avg(grads)
-            L.moses_apply_update(dm.h, LR, MU, None, 0, 1)
-
-        for k in range(max(args.warmup, 400)):  # slot graphs captured, copy pipeline in steady state (~35 ms)
-            e2e_step(e2e_steps + (k % 64))
-        ml._ck(L.moses_model_synchronize(dm.h))
-        torch.cuda.synchronize()
-        # three timed windows of e2e_steps each (median reported; host GC paused inside them)
-        import gc
-
-        e2e_windows = []
-        for _rep in range(3):
-            if world > 1:
-                dist.barrier()
-            gc.disable()
-            t0 = time.perf_counter()
-            for k in range(e2e_steps):
-                e2e_step(k)
-            ml._ck(L.moses_model_synchronize(dm.h))
-            torch.cuda.synchronize()
-            e2e_windows.append(time.perf_counter() - t0)
-            gc.enable()
-        e2e_s = float(np.median(e2e_windows))
-        if any(rcs):
-            ml._ck(next(r for r in rcs if r))
-        assert world > 1 or bool(torch.isfinite(losses[:e2e_steps]).all()) and float(losses[e2e_steps - 1]) > 0.0
-        if world > 1:
-            t = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        h2d_bytes = int(np.mean([sum(t.numel() * t.element_size() for t in hb) for hb in host_batches]))
-    e2e_value = world * BATCH * e2e_steps / e2e_s
-
-    infer = None
+    head = bench_cfg2(ml, L, args, rank, world, dist, peaks)
+    cfg5 = None if args.no_cfg5 else bench_cfg5(ml, L, args, rank, world, dist, peaks)
+    infer = infer_bf16 = None
     if not args.no_infer:  # every rank: the candidate pool is sharded across the GPUs
-        peaks0 = {}
-        try:
-            peaks0 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        except Exception:
-            pass
-        infer = bench_infer(ml, L, args.infer_programs, peaks0, rank, world)
-
+        infer = bench_infer(ml, L, args.infer_programs, peaks, rank, world, dist, ml.PREC_BF16X3)
+        infer_bf16 = bench_infer(ml, L, args.infer_programs, peaks, rank, world, dist, ml.PREC_BF16)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # ---------------- roofline of the dominant kernel class
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
-    gemm_launches = sum(prof[c][1] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / args.profile_steps
-    flops = gemm_flops_per_step(DIMS, n_rows / nb)  # algorithmic: real statement rows, not the padding
-    peak = peaks.get("bf16_tflops_sustained", 1408.7)
-    achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
+    prof, K = head["prof"], args.profile_steps
+    gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / K
+    gemm_launches = sum(prof[c][1] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / K
+    flops = gemm_flops_per_step(DIMS, head["rows_per_step"])  # real statement rows, not the padding
+    peak = peaks.get("bf16_tflops_sustained", 1395.6)
+    achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = None
-    try:  # DRAM bytes of the step's GEMM launches (chain fwd + chain dZ + grouped wgrad), ncu --set full
+    try:  # DRAM bytes of the step's GEMM launches from one ncu --set full capture
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("gemm_bytes_per_step")
-    except Exception:
+    except Exception:  # noqa: BLE001
         pass
-    step_prof_ms = sum(v[0] for v in prof.values()) / args.profile_steps
-    fwd, wg, dg = (v * n_rows / (nb * BATCH) for v in train_flops_per_sample(DIMS))
+    fwd, wg, dg = (v * head["rows_per_step"] / BATCH for v in train_flops_per_sample(DIMS))
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16",
+        "metric": METRIC, "value": head["value"], "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16x3",
+        "dtype_note": "split bf16: every GEMM operand is hi + lo (bf16 each), products hi*hi + hi*lo + lo*hi on the "
+                      "bf16 tensor cores with fp32 accumulation; ~1e-5 normwise from the fp64 reference "
+                      "(tests/test_gpu_bf16x3.py; north-star bound 1e-3)",
         "data": "synthetic (keyed SplitMix64 TenSet-shaped features 164-d, labels 0.1+U; random-init model)",
-        "config": {"workload": f"cfg2: pretrain {DIMS} (4x512 hidden) on {PROGRAMS} TenSet-shaped programs "
-                               f"(segment-sum pooling over statements), batch {BATCH} programs/GPU, "
-                               f"momentum SGD lr={LR} mu={MU}", "model": "moses-mlp-4x512", "programs": PROGRAMS,
-                   "global_batch": BATCH * world, "seq_len": None, "parallelism": f"dp{world}",
-                   "statements_per_program": f"1 + U{{0..{MAX_STMTS - 1}}} (mean {n_rows / (nb * BATCH):.2f})",
-                   "rows_per_step_padded": rows_pad, "dataset_bytes": int(X.numel() * X.element_size()),
-                   "l2": "inputs larger than L2: each step gathers a different batch of the 302 MB device-resident "
-                         "dataset; K steps timed back to back (ms_per_step_l2_flushed: the same step with a 256 MiB "
-                         "L2 flush before each one)"},
-        "ms_per_step_l2_flushed": ms_step_flushed,
-        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 8,
-                "windows_samples_per_s": [world * BATCH * e2e_steps / w for w in e2e_windows],
-                "path": ("moses_train_step_pooled_async (C ABI: pinned host float64 rows/offsets/labels uploaded "
-                         "every step, upload of step k+1 overlapping step k, per-step loss read back; 4 distinct "
-                         "host batches)") if world == 1 else
-                        "moses_gradients_pooled + NCCL average + moses_apply_update (C ABI, pinned host buffers)"},
+        "config": workload_config(world),
+        "timed_windows": len(head["windows_ms"]), "windows_ms": head["windows_ms"],
+        "ms_per_step_l2_flushed": head["ms_per_step_l2_flushed"],
+        "e2e": head["e2e"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per step (3 GEMM launches), cold-cache ncu replay",
-                     "kernel": "mlp_chain_kernel (fwd), mlp_chain_kernel (dZ), wgrad_group_kernel (tcgen05 bf16): the 3 GEMM launches of a step",
+                     "traffic_unit": "DRAM bytes per step (GEMM launches), cold-cache ncu replay",
+                     "mma_per_product": 3,
+                     "tensor_pipe_frac": 3 * achieved / peak if achieved else None,
+                     "kernel": "mlp_chain_split_kernel (fwd), mlp_chain_split_kernel (dZ), wgrad_group_split_kernel: "
+                               "the 3 GEMM launches of a step",
                      "flops_per_step": flops, "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
+                     "timing": "CUDA events on the launch streams around each GEMM launch, eager profiling pass of "
+                               f"{K} steps beside the timed windows",
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
-        "step_breakdown_ms": {k: v[0] / args.profile_steps for k, v in prof.items() if v[1]},
-        "step_device_ms_profiled": step_prof_ms,
+        "step_breakdown_ms": {k: v[0] / K for k, v in prof.items() if v[1]},
         "algorithmic_flops_per_sample": {"fwd": fwd, "wgrad": wg, "dgrad": dg},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "rows_per_step": head["rows_per_step"], "rows_per_step_padded": head["rows_pad"],
+        "gpu_launches": head["gpu_launches"],
+        "clocks": head["clocks"],
     }
+    if cfg5 is not None:
+        line["cfg5"] = cfg5
     if infer is not None:
         line["infer"] = infer
+        line["infer_bf16_throughput_mode"] = infer_bf16
+    import bench_sections as bs
+
     if not args.no_hbm:
-        line["hbm_kernels"] = bench_hbm_kernels(ml, L, peaks)
+        line["hbm_kernels"] = bs.bench_hbm_kernels(ml, L, peaks)
     if not args.no_finetune:
-        line["finetune"] = bench_finetune(ml, L, peaks)
+        line["finetune"] = bs.bench_finetune(ml, L, peaks)
     if not args.no_search:
-        line["search"] = bench_search(ml, L, peaks)
+        line["search"] = bs.bench_search(ml, L, peaks)
     if not args.no_pretrain:
-        line["pretrain"] = bench_pretrain(ml, L, peaks)
+        line["pretrain"] = bs.bench_pretrain(ml, L, peaks)
+    if world == 1 and not args.headline_only:
+        line["cfg1"] = bench_cfg1(ml, L)
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(15.0)
+        allc = cpu_baseline(10.0, os.cpu_count() or 1)
+        one = cpu_baseline(8.0, 1)
+        line["cpu_baseline"] = allc
+        line["cpu_baseline_1thread"] = one
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
