@@ -407,6 +407,46 @@ MOSES_API int moses_synth_labels_device(uint64_t seed, int64_t row0, int64_t n, 
 /* CSR offsets of `programs` programs with 1 + below(max_stmts) statements each (host). */
 MOSES_API int moses_synth_offsets(uint64_t seed, int64_t programs, int32_t max_stmts, int64_t* offsets);
 
+/* ------------------------------------------------------------------ multi-GPU
+ * NCCL communicators behind the ABI (NCCL is loaded at run time: libnccl.so.2). Either one process per
+ * GPU (rank 0 makes the id with moses_comm_unique_id, the caller distributes its 128 bytes, every rank
+ * calls moses_comm_init_rank on its current device) or one process for n GPUs (moses_comm_init_all:
+ * ncclCommInitAll, comms_out[i] drives devices[i]). */
+typedef struct moses_comm* moses_comm_t;
+MOSES_API int moses_comm_unique_id(uint8_t* id_out, int64_t cap);
+MOSES_API int moses_comm_init_rank(const uint8_t* id, int32_t nranks, int32_t rank, moses_comm_t* out);
+MOSES_API int moses_comm_init_all(int32_t ndev, const int32_t* devices, moses_comm_t* comms_out);
+MOSES_API int moses_comm_destroy(moses_comm_t c);
+MOSES_API int moses_comm_info(moses_comm_t c, int32_t* nranks, int32_t* rank, int32_t* device);
+/* Data-parallel training on a handle (tuner.cpp:134-154's batch loop across ranks). mode 0: none;
+ * 1: throughput mode, every rank steps its own batch and the gradients are averaged (ncclAvg) before the
+ * update; 2: exact batch, the global batch is the rank-ordered concatenation of every rank's rows: local
+ * forward, all-gather of scores + labels, pair terms of the local rows against the whole batch
+ * (model.cpp:71-106, each distinct-label pair counted once), all-reduce of (loss, pairs), local backward,
+ * all-reduce (sum) of the gradients = the gradient of the global batch up to summation order. Mode 2
+ * takes unpooled rows. With a communicator set, moses_train_graph_create[_pooled] capture the
+ * collectives and the update into the step graph. */
+MOSES_API int moses_model_set_comm(moses_model_t m, moses_comm_t c, int32_t mode);
+MOSES_API int moses_dp_allreduce_gradients(moses_model_t m, int32_t average);
+/* one data-parallel step on device rows (packed layout, moses_packed_ld; fp32 labels); loss_out: the
+ * rank's batch loss (mode 1) or the global batch loss (mode 2) */
+MOSES_API int moses_dp_train_step(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                  double learning_rate, double momentum, double* loss_out);
+/* the exact-batch step's phases around its collectives (tests; callers with their own transport):
+ * forward writes the n local scores / labels to s_slot / y_slot (device); rank takes the gathered
+ * n_global scores / labels and this rank's offset p0, writes (loss sum, pair count) partials to
+ * totals_dev[2]; backward takes the summed totals and leaves this rank's gradient share on the handle. */
+MOSES_API int moses_dp_exact_forward(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                     float* s_slot, float* y_slot);
+MOSES_API int moses_dp_exact_rank(moses_model_t m, const float* s_global, const float* y_global, int64_t n_global,
+                                  int64_t p0, double* totals_dev);
+MOSES_API int moses_dp_exact_backward(moses_model_t m, int64_t n_global, const double* totals_dev, double* loss_out);
+/* Sharded candidate scoring (cfg4): top-k of this rank's shard [row0, row0 + n_local) of the pool, winners
+ * all-gathered and merged by (score desc, index asc) (search.cpp:32-37); idx_out[k] (host) is the same on
+ * every rank and equals the single-device top-k of the whole pool. */
+MOSES_API int moses_topk_sharded(moses_comm_t c, const float* scores_dev, int64_t n_local, int64_t row0, int64_t k,
+                                 int64_t* idx_out);
+
 /* ------------------------------------------------------------------ files (model.cpp:344-412, lottery.cpp:182-240) */
 MOSES_API int64_t moses_serialize(const int32_t* dims, int32_t ndims, const double* params, const double* momentum,
                                   uint8_t* out, int64_t cap);

@@ -485,6 +485,35 @@ std::vector<R> gradients(const Params<R>& p, const R* x, const R* y, int n, cons
   return g;
 }
 
+// gradients() (model.cpp:201-244, no adversary) with the score gradient gs supplied by the caller:
+// g.gw[L-1] = gs^T h, g.gb[L-1] = sum(gs), then backprop_from_penultimate. With gs = ranking_terms'
+// this is gradients(); with the rows of one data-parallel rank and gs from the pair terms of those rows
+// against the whole (all-gathered) batch, normalised by the global pair count, it is that rank's
+// share of the global batch gradient (SURVEY.md §8(e) exact mode): the shares sum to gradients().
+template <class R>
+std::vector<R> gradients_from_score_grads(const Params<R>& p, const R* x, int n, const R* gs, int threads = 1) {
+  const int L = p.levels();
+  const int dl = p.dims[L - 1];
+  std::vector<R> g(p.w.size(), R(0));
+  const Forward<R> f = run_forward(p, x, n, threads);
+  const std::vector<R>& hl = f.h.back();
+  R* GW = g.data() + level_offset(p.dims, L - 1);
+  for (int j = 0; j < dl; ++j) {
+    R acc = R(0);
+    for (int r = 0; r < n; ++r) acc = std::fma(gs[r], hl[std::size_t(r) * dl + j], acc);
+    GW[j] = acc;
+  }
+  R gsum = R(0);
+  for (int r = 0; r < n; ++r) gsum += gs[r];
+  GW[dl] = gsum;
+  const R* wh = p.W(L - 1);
+  std::vector<R> dh(std::size_t(n) * dl);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < dl; ++j) dh[std::size_t(r) * dl + j] = gs[r] * wh[j];
+  backprop_from_penultimate(p, f, x, n, std::move(dh), g, threads);
+  return g;
+}
+
 // North-star extension (parity pinned only by this restatement; S == 1 reduces to gradients()):
 // statement rows -> shared encoder -> per-program segment sum of the last hidden layer -> head.
 template <class R>

@@ -233,6 +233,39 @@ def gradients_pooled(dims, w, x, offsets, y, threads=1):
     return g, float(loss[0])
 
 
+def gradients_from_score_grads(dims, w, x, gs, threads=1):
+    """gradients() with a caller-supplied score gradient (model.cpp:201-244 after ranking_terms), fp64."""
+    d = _dims(dims)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    gs = np.ascontiguousarray(gs, dtype=np.float64)
+    g = np.zeros_like(w)
+    _check(lib().orc_gradients_from_score_grads_f64(_p(d), len(d), _p(w), _p(x), x.shape[0], _p(gs), _p(g), threads))
+    return g
+
+
+def pair_terms_rows(s_global, y_global, r0, r1):
+    """Pair terms of rows [r0, r1) against the whole batch (model.cpp:71-106's rule, each distinct-label
+    pair's loss counted at its hi row): (unnormalised gs of those rows, loss sum, pair count)."""
+    s = np.asarray(s_global, dtype=np.float64)
+    y = np.asarray(y_global, dtype=np.float64)
+    gs = np.zeros(r1 - r0)
+    loss, pairs = 0.0, 0
+    for i in range(r0, r1):
+        hi = y[i] > y  # i is the hi row of (i, j)
+        lo = y[i] < y
+        d_hi = s[i] - s[hi]
+        e = np.exp(-np.abs(d_hi))
+        sig = np.where(d_hi >= 0, e / (1 + e), 1 / (1 + e))
+        d_lo = s[lo] - s[i]
+        e2 = np.exp(-np.abs(d_lo))
+        sig2 = np.where(d_lo >= 0, e2 / (1 + e2), 1 / (1 + e2))
+        gs[i - r0] = -sig.sum() + sig2.sum()
+        loss += np.sum(np.where(d_hi >= 0, np.log1p(e), -d_hi + np.log1p(e)))
+        pairs += int(hi.sum())
+    return gs, loss, pairs
+
+
 def objective(dims, w, x, y, adv=None, beta=0.0):
     d = _dims(dims)
     w = np.ascontiguousarray(w)

@@ -142,6 +142,15 @@ ORC_RANK(f32, float)
 ORC_GRAD(f64, double)
 ORC_GRAD(f32, float)
 
+ORC int orc_gradients_from_score_grads_f64(const int* dims, int nd, const double* w, const double* x, int n,
+                                          const double* gs, double* g_out, int threads) {
+  return guarded([&] {
+    Params<double> p = make_params<double>(dims, nd, w, nullptr);
+    std::vector<double> g = gradients_from_score_grads(p, x, n, gs, threads);
+    std::memcpy(g_out, g.data(), sizeof(double) * g.size());
+  });
+}
+
 ORC int orc_gradients_pooled_f64(const int* dims, int nd, const double* w, const double* x, int nstmt,
                                  const long long* off, int programs, const double* y, double* g_out, double* loss_out,
                                  int threads) {

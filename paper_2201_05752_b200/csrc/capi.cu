@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "pipeline.cuh"
@@ -152,9 +153,14 @@ struct Scratch {
     return buf;
   }
 };
+// one scratch context per device (a process may drive several GPUs: moses_comm_init_all)
 Scratch& scratch() {
-  static Scratch s;
-  return s;
+  constexpr int kMaxDev = 64;
+  static Scratch s[kMaxDev];
+  int dev = 0;
+  MOSES_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) fail(MOSES_ERR_NO_DEVICE, "device ordinal out of range");
+  return s[dev];
 }
 
 struct Carver {
@@ -251,6 +257,17 @@ struct moses_model {
     long long graph_kernels = 0;
   } plan;
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
+  // data parallel (moses_model_set_comm): 1 = average the gradients of every rank's own batch
+  // (throughput mode), 2 = exact batch (the global batch is the rank-ordered concatenation of every
+  // rank's rows; scores all-gathered, pair terms of the own rows, gradients summed)
+  moses_comm* comm = nullptr;
+  int comm_mode = 0;
+  float* dp_s = nullptr;           // exact mode: all-gathered scores / labels of the global batch
+  float* dp_y = nullptr;
+  double* dp_tot = nullptr;        // exact mode: (loss sum, pair count) partials -> global
+  long long dp_cap = 0;
+  const void* dp_x0 = nullptr;     // exact mode: the local rows of the step in flight
+  long long dp_ld0 = 0, dp_n = 0;
   void* lot_ws = nullptr;          // fused lottery-step workspace (lottery.cu)
   long long* seg_off = nullptr;    // pooled: device CSR offsets of the current batch (cap+1)
   int* seg_rows = nullptr;         // pooled: program of each statement row (cap)
@@ -360,6 +377,9 @@ struct moses_model {
     dfree(plan.stage);
     dfree(dcounter);
     dfree(gbias);
+    dfree(dp_s);
+    dfree(dp_y);
+    dfree(dp_tot);
     dfree(lot_ws);
     dfree(seg_off);
     dfree(seg_rows);
@@ -819,6 +839,87 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
 void check_rows(moses_model* m, long long R) {
   if (R > m->cap)
     fail(MOSES_ERR_CAPACITY, "rows " + std::to_string(R) + " exceed the handle capacity " + std::to_string(m->cap));
+}
+
+// momentum SGD over every parameter (tuner.cpp:146-147) with the handle's operand shadow kept current
+// (split bf16: the hi/lo pair written by the update kernel itself)
+void update_momentum(moses_model* m, float lr, float mu, cudaStream_t st) {
+  if (m->bsplit()) {
+    sgd_update(m->w, m->mom, m->g, nullptr, m->P, lr, mu, true, m->shadow_full(), st);
+  } else {
+    sgd_update(m->w, m->mom, m->g, nullptr, m->P, lr, mu, true, m->shadow(), st);
+    m->post_update();
+  }
+  note_launch(1);
+}
+
+// ---- data-parallel exact batch: the global batch of n_global = nranks * n
+// rows is the rank-ordered concatenation of every rank's n local rows. Phase 1: local forward, local
+// scores and labels into their slots of the global arrays. (All-gather.) Phase 2: pair terms of the
+// local rows against the whole batch (model.cpp:71-106; each distinct-label pair counted once, at its
+// hi row), (loss sum, pair count) partials. (All-reduce.) Phase 3: coefficients normalised by the
+// global pair count, local backward -> this rank's share of the gradient. (All-reduce: the sum is the
+// gradient of the global batch, up to summation order.) Unpooled rows.
+void dp_reserve(moses_model* m, long long n_global) {
+  if (n_global <= m->dp_cap) return;
+  for (void* p : {(void*)m->dp_s, (void*)m->dp_y})
+    if (p) m->retired.push_back(p);  // captured graphs may still point at them
+  m->dp_s = dalloc<float>(n_global);
+  m->dp_y = dalloc<float>(n_global);
+  if (!m->dp_tot) m->dp_tot = dalloc<double>(2);
+  m->dp_cap = n_global;
+}
+void dp_exact_forward(moses_model* m, const void* x0, long long ld0, const float* y, long long n, float* s_slot,
+                      float* y_slot) {
+  check_rows(m, n);
+  dispatch_forward(m, x0, ld0, n, nullptr, true);
+  head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), n, s_slot, m->st);
+  note_launch(1);
+  if (n > 0 && y_slot != y) MOSES_CUDA(cudaMemcpyAsync(y_slot, y, sizeof(float) * n, cudaMemcpyDeviceToDevice, m->st));
+  m->dp_x0 = x0;
+  m->dp_ld0 = ld0;
+  m->dp_n = n;
+}
+void dp_exact_rank(moses_model* m, const float* s_global, const float* y_global, long long n_global, long long p0,
+                   double* totals_out) {
+  const long long n = m->dp_n;
+  if (p0 < 0 || p0 + n > n_global) fail(MOSES_ERR_SHAPE_MISMATCH, "local rows outside the global batch");
+  const long long need = rank_splits(n_global) * std::max<long long>(n, 1);
+  if (need > rank_splits(m->rank_ws_rows) * m->rank_ws_rows) ensure_rank_ws(m, n_global);
+  const RankWs ws{m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n_global)};
+  ProfScope ps(P_RANK, m->st);
+  rank_pairs_rows(s_global, y_global, n_global, p0, n, ws, m->st);
+  rank_local_totals(ws, n, totals_out, m->st);
+  note_launch(2);
+}
+void dp_exact_backward(moses_model* m, long long n_global, const double* totals_global) {
+  const long long n = m->dp_n;
+  const RankWs ws{m->rank.gs_part, m->rank.loss_part, m->rank.pairs_part, rank_splits(n_global)};
+  {
+    ProfScope ps(P_RANK, m->st);
+    const FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
+    rank_finalize(ws, n, 0, nullptr, 0, 0, nullptr, 0.0, fo, m->st, totals_global);
+    note_launch(1);
+  }
+  if (m->esz == 2) backward_rows<__nv_bfloat16>(m, m->dp_x0, m->dp_ld0, n, nullptr);
+  else backward_rows<float>(m, m->dp_x0, m->dp_ld0, n, nullptr);
+  m->xi_valid = false;
+}
+// one exact-batch step on the handle's communicator (graph-capturable): forward -> all-gather ->
+// pair terms -> all-reduce of (loss, pairs) -> backward -> all-reduce of the gradients [-> update]
+void dp_exact_step(moses_model* m, const void* x0, long long ld0, const float* y, long long n, bool update, float lr,
+                   float mu) {
+  moses_comm* c = m->comm;
+  const long long ng = n * c->nranks, p0 = n * c->rank;
+  dp_reserve(m, ng);
+  dp_exact_forward(m, x0, ld0, y, n, m->dp_s + p0, m->dp_y + p0);
+  comm_allgather_f32(c, m->dp_s + p0, m->dp_s, n, m->st);
+  comm_allgather_f32(c, m->dp_y + p0, m->dp_y, n, m->st);
+  dp_exact_rank(m, m->dp_s, m->dp_y, ng, p0, m->dp_tot);
+  comm_allreduce_f64(c, m->dp_tot, 2, m->st);
+  dp_exact_backward(m, ng, m->dp_tot);
+  comm_allreduce_f32(c, m->g, m->P, false, m->st);
+  if (update) update_momentum(m, lr, mu, m->st);
 }
 
 }  // namespace
@@ -1320,19 +1421,25 @@ MOSES_API int moses_train_graph_create(moses_model_t m, const void* x_base, int6
     auto body = [&] {
       gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st,
                    m->act_lo(0));
+      if (m->comm_mode == 2) {  // data-parallel exact batch: collectives inside the graph
+        dp_exact_step(m, m->act[0], m->ld[0], m->labels, batch, with_update != 0, float(lr), float(mu));
+        advance_counter(m->dcounter, m->st);
+        return;
+      }
       const SgdFuse fz{float(lr), float(mu), m->dcounter};
       const bool fused = gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0, nullptr,
-                                        with_update ? &fz : nullptr);
+                                        (with_update && !m->comm) ? &fz : nullptr);
       if (with_update && !fused) {
-        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-        m->post_update();
+        if (m->comm) comm_allreduce_f32(m->comm, m->g, m->P, true, m->st);  // throughput-mode DP average
+        update_momentum(m, float(lr), float(mu), m->st);
       }
       if (!fz.folded) advance_counter(m->dcounter, m->st);
     };
     {  // eager warm-up without the update (configures kernels, validates shapes; params untouched)
       gather_batch(x_base, row_bytes, y_base, m->dcounter, n_batches, batch, m->act[0], m->labels, m->st,
                    m->act_lo(0));
-      gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
+      if (m->comm_mode == 2) dp_exact_step(m, m->act[0], m->ld[0], m->labels, batch, false, 0.f, 0.f);
+      else gradients_core(m, m->act[0], m->ld[0], m->labels, batch, nullptr, 0.0);
     }
     MOSES_CUDA(cudaStreamSynchronize(m->st));
     cudaGraph_t graph;
@@ -1369,6 +1476,8 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
     check_rows(m, rows_pad);
     if (ldx != m->ld[0]) fail(MOSES_ERR_INVALID_ARG, "dataset row stride must equal moses_packed_ld");
     if (n_batches < 1 || batch_programs < 1) fail(MOSES_ERR_INVALID_ARG, "empty batch plan");
+    if (m->comm_mode == 2)
+      fail(MOSES_ERR_INVALID_ARG, "exact-batch data parallelism takes unpooled rows (moses_train_graph_create)");
     for (cudaGraphExec_t* e : {&m->train_exec, &m->train_exec2})
       if (*e) {
         cudaGraphExecDestroy(*e);
@@ -1413,10 +1522,10 @@ MOSES_API int moses_train_graph_create_pooled(moses_model_t m, const void* x_bas
       MOSES_CUDA(cudaEventRecord(m->pf_join, m->st3));
       const SgdFuse fz{float(lr), float(mu)};
       const bool fused = gradients_core(m, c.act, m->ld[0], c.labels, batch_programs, nullptr, 0.0, &pool,
-                                        with_update ? &fz : nullptr);
+                                        (with_update && !m->comm) ? &fz : nullptr);
       if (with_update && !fused) {
-        sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
-        m->post_update();
+        if (m->comm) comm_allreduce_f32(m->comm, m->g, m->P, true, m->st);  // throughput-mode DP average
+        update_momentum(m, float(lr), float(mu), m->st);
       }
       MOSES_CUDA(cudaStreamWaitEvent(m->st, m->pf_join, 0));
     };
@@ -2296,6 +2405,197 @@ MOSES_API int moses_topk_device(const float* scores, int64_t n, int64_t k, int64
     }
     MOSES_CUDA(cudaMemcpyAsync(idx_out, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
     MOSES_CUDA(cudaStreamSynchronize(sc.st));
+  });
+}
+
+// ====================================================================== NCCL communicators + data parallel
+MOSES_API int moses_comm_unique_id(uint8_t* id_out, int64_t cap) {
+  return guarded([&] {
+    if (id_out == nullptr || cap < int64_t(sizeof(ncclUniqueId))) fail(MOSES_ERR_INVALID_ARG, "id buffer too small");
+    ncclUniqueId id;
+    MOSES_NCCL(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+MOSES_API int moses_comm_init_rank(const uint8_t* id, int32_t nranks, int32_t rank, moses_comm_t* out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (id == nullptr || nranks < 1 || rank < 0 || rank >= nranks) fail(MOSES_ERR_INVALID_ARG, "bad rank / size");
+    auto c = std::make_unique<moses_comm>();
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    MOSES_CUDA(cudaGetDevice(&c->device));
+    MOSES_NCCL(nccl().CommInitRank(&c->comm, nranks, uid, rank));
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c.release();
+  });
+}
+
+MOSES_API int moses_comm_init_all(int32_t ndev, const int32_t* devices, moses_comm_t* out) {
+  return guarded([&] {
+    if (ndev < 1 || devices == nullptr || out == nullptr) fail(MOSES_ERR_INVALID_ARG, "empty device list");
+    std::vector<ncclComm_t> comms(static_cast<size_t>(ndev));
+    MOSES_NCCL(nccl().CommInitAll(comms.data(), ndev, devices));
+    for (int i = 0; i < ndev; ++i) {
+      auto* c = new moses_comm();
+      c->comm = comms[size_t(i)];
+      c->nranks = ndev;
+      c->rank = i;
+      c->device = devices[i];
+      out[i] = c;
+    }
+  });
+}
+
+MOSES_API int moses_comm_destroy(moses_comm_t c) {
+  return guarded([&] {
+    if (c == nullptr) return;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    delete c;
+  });
+}
+
+MOSES_API int moses_comm_info(moses_comm_t c, int32_t* nranks, int32_t* rank, int32_t* device) {
+  return guarded([&] {
+    if (c == nullptr) fail(MOSES_ERR_INVALID_ARG, "null communicator");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+    if (device) *device = c->device;
+  });
+}
+
+MOSES_API int moses_model_set_comm(moses_model_t m, moses_comm_t c, int32_t mode) {
+  return guarded([&] {
+    require_model(m);
+    if (mode < 0 || mode > 2 || (mode != 0 && c == nullptr)) fail(MOSES_ERR_INVALID_ARG, "bad data-parallel mode");
+    if (c != nullptr && c->device != m->device) fail(MOSES_ERR_INVALID_ARG, "communicator and model on different devices");
+    for (cudaGraphExec_t* e : {&m->train_exec, &m->train_exec2})  // graphs captured for the old mode
+      if (*e) {
+        cudaGraphExecDestroy(*e);
+        *e = nullptr;
+      }
+    m->comm = mode == 0 ? nullptr : c;
+    m->comm_mode = mode == 0 ? 0 : mode;
+  });
+}
+
+MOSES_API int moses_dp_allreduce_gradients(moses_model_t m, int32_t average) {
+  return guarded([&] {
+    require_model(m);
+    if (!m->comm) fail(MOSES_ERR_INVALID_ARG, "no communicator (moses_model_set_comm)");
+    comm_allreduce_f32(m->comm, m->g, m->P, average != 0, m->st);
+    if (sync_updates()) MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+MOSES_API int moses_dp_train_step(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                  double lr, double mu, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    if (!m->comm) fail(MOSES_ERR_INVALID_ARG, "no communicator (moses_model_set_comm)");
+    check_rows(m, n);
+    long long ld0 = 0;
+    const void* x0 = stage_device_rows(m, x_dev, ldx, n, &ld0);
+    if (m->comm_mode == 2) {
+      dp_exact_step(m, x0, ld0, y_dev, n, true, float(lr), float(mu));
+    } else {
+      gradients_core(m, x0, ld0, y_dev, n, nullptr, 0.0);
+      comm_allreduce_f32(m->comm, m->g, m->P, true, m->st);
+      update_momentum(m, float(lr), float(mu), m->st);
+    }
+    if (loss_out) {
+      MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    } else if (sync_updates()) {
+      MOSES_CUDA(cudaStreamSynchronize(m->st));
+    }
+  });
+}
+
+MOSES_API int moses_dp_exact_forward(moses_model_t m, const void* x_dev, int64_t ldx, const float* y_dev, int64_t n,
+                                     float* s_slot, float* y_slot) {
+  return guarded([&] {
+    require_model(m);
+    check_rows(m, n);
+    long long ld0 = 0;
+    const void* x0 = stage_device_rows(m, x_dev, ldx, n, &ld0);
+    dp_exact_forward(m, x0, ld0, y_dev, n, s_slot, y_slot);
+  });
+}
+
+MOSES_API int moses_dp_exact_rank(moses_model_t m, const float* s_global, const float* y_global, int64_t n_global,
+                                  int64_t p0, double* totals_dev) {
+  return guarded([&] {
+    require_model(m);
+    dp_exact_rank(m, s_global, y_global, n_global, p0, totals_dev);
+  });
+}
+
+MOSES_API int moses_dp_exact_backward(moses_model_t m, int64_t n_global, const double* totals_dev, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    dp_exact_backward(m, n_global, totals_dev);
+    if (loss_out) MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+// cfg4 across ranks: local top-k of this rank's contiguous shard [row0, row0 + n_local), the k winners'
+// (score, global index) all-gathered over NCCL, merged with the reference comparator (score desc,
+// index asc: search.cpp:32-37) — identical on every rank, equal to the single-device top-k of the pool.
+MOSES_API int moses_topk_sharded(moses_comm_t c, const float* scores_dev, int64_t n_local, int64_t row0, int64_t k,
+                                 int64_t* idx_out) {
+  return guarded([&] {
+    if (c == nullptr) fail(MOSES_ERR_INVALID_ARG, "null communicator");
+    if (k <= 0) return;
+    if (k > kTopkMax) fail(MOSES_ERR_INVALID_ARG, "k must be <= 4096");
+    const long long kk = std::min<long long>(k, std::max<long long>(n_local, 0));
+    MOSES_CUDA(cudaSetDevice(c->device));
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const long long nsel = std::max<long long>(n_local, 1);
+    const size_t selb = select_ws_bytes(nsel, nullptr);
+    const size_t gather_b = size_t(k) * (c->nranks + 1) * (sizeof(float) + sizeof(long long));
+    Carver cv{static_cast<uint8_t*>(sc.ensure(selb + kTopkMax * 12 + topk_fast_ws_bytes(nsel) + gather_b + 16384))};
+    uint8_t* selbase = cv.take<uint8_t>(selb);
+    unsigned* ok = cv.take<unsigned>(kTopkMax);
+    long long* oi = cv.take<long long>(kTopkMax);
+    void* fast_ws = cv.take<uint8_t>(topk_fast_ws_bytes(nsel));
+    float* ws_s = cv.take<float>(size_t(k));
+    long long* ws_i = cv.take<long long>(size_t(k));
+    float* all_s = cv.take<float>(size_t(k) * c->nranks);
+    long long* all_i = cv.take<long long>(size_t(k) * c->nranks);
+    if (kk > 0) {
+      SelectWs ws;
+      select_ws_carve(selbase, n_local, &ws);
+      ProfScope ps(P_TOPK, sc.st);
+      if (topk_fast(scores_dev, n_local, kk, fast_ws, ok, oi, sc.st)) note_launch(11);
+      else {
+        topk_select(scores_dev, n_local, kk, ws, ok, oi, sc.st);
+        note_launch(10);
+      }
+    }
+    topk_winners(scores_dev, oi, kk, k, row0, ws_s, ws_i, sc.st);
+    note_launch(1);
+    MOSES_NCCL(nccl().GroupStart());
+    comm_allgather_bytes(c, ws_s, all_s, k * sizeof(float), sc.st);
+    comm_allgather_bytes(c, ws_i, all_i, k * sizeof(long long), sc.st);
+    MOSES_NCCL(nccl().GroupEnd());
+    std::vector<float> hs(size_t(k) * c->nranks);
+    std::vector<long long> hi(size_t(k) * c->nranks);
+    MOSES_CUDA(cudaMemcpyAsync(hs.data(), all_s, sizeof(float) * hs.size(), cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(hi.data(), all_i, sizeof(long long) * hi.size(), cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+    std::vector<size_t> order;
+    for (size_t i = 0; i < hi.size(); ++i)
+      if (hi[i] >= 0) order.push_back(i);
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+      if (hs[a] != hs[b]) return hs[a] > hs[b];
+      return hi[a] < hi[b];
+    });
+    for (long long i = 0; i < k; ++i) idx_out[i] = i < (long long)order.size() ? hi[order[size_t(i)]] : -1;
   });
 }
 

@@ -292,10 +292,12 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
                                                                 const long long* __restrict__ seg,
                                                                 const float* __restrict__ y, long long n, double* gs_part,
                                                                 double* loss_part, long long* pairs_part,
-                                                                float* __restrict__ s_out) {
+                                                                float* __restrict__ s_out, long long r0, long long nr) {
+  // rows [r0, r0 + nr) of the batch against all n columns (data-parallel exact batches: a rank's
+  // own rows against the all-gathered batch); partials at [split][i - r0]
   __shared__ float ss[kRankChunk], sy[kRankChunk];
   const float hb = part ? hbp[0] : 0.f;
-  const long long i = blockIdx.x * (long long)kRankBlock + threadIdx.x;
+  const long long i = r0 + blockIdx.x * (long long)kRankBlock + threadIdx.x;
   const long long j0 = (long long)blockIdx.y * kRankChunk;
   const int cnt = int(min((long long)kRankChunk, n - j0));
   if (threadIdx.x < cnt) {
@@ -303,9 +305,9 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
     sy[threadIdx.x] = y[j0 + threadIdx.x];
   }
   __syncthreads();
-  if (i >= n) return;
+  if (i >= r0 + nr) return;
   const float si = score_of(s, part, ntiles, ld, hb, seg, i), yi = y[i];
-  if (s_out != nullptr && blockIdx.y == 0) s_out[i] = si;
+  if (s_out != nullptr && blockIdx.y == 0) s_out[i - r0] = si;
   float gs = 0.f, loss = 0.f;
   int pairs = 0;
 #pragma unroll 4
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
       gs += sig_neg;
     }
   }
-  const long long o = (long long)blockIdx.y * n + i;
+  const long long o = (long long)blockIdx.y * nr + (i - r0);
   gs_part[o] = gs;
   loss_part[o] = loss;
   pairs_part[o] = pairs;
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
                                                                   double* loss_out, long long* pairs_out, float* coefA,
                                                                   float* coefB, double* ce_out,
                                                                   const int* __restrict__ seg_of_row, long long R_rows,
-                                                                  float* gb_out) {
+                                                                  float* gb_out, const double* totals) {
   ptx::pdl_launch_dependents();
   using BR = cub::BlockReduce<double, kFinBlock>;
   using BRL = cub::BlockReduce<long long, kFinBlock>;
@@ -377,9 +379,13 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
       p += pairs_part[sp * n + i];
       l += loss_part[sp * n + i];
     }
-  const long long ptot = BRL(tmpl).Sum(p);
+  long long ptot = BRL(tmpl).Sum(p);
   __syncthreads();
-  const double ltot = BR(tmp).Sum(l);
+  double ltot = BR(tmp).Sum(l);
+  if (totals != nullptr) {  // data-parallel exact batch: every rank's partials, all-reduced
+    ltot = totals[0];
+    ptot = (long long)llrint(totals[1]);
+  }
   if (threadIdx.x == 0) {
     sh_pairs = ptot;
     sh_loss = ptot > 0 ? ltot / double(ptot) : 0.0;
@@ -1585,7 +1591,41 @@ void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, c
   if (n <= 0) return;
   dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
   rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, nullptr, 0, 0, nullptr, nullptr, y, n, ws.gs_part, ws.loss_part,
-                                                 ws.pairs_part, nullptr);
+                                                 ws.pairs_part, nullptr, 0, n);
+  MOSES_CUDA(cudaGetLastError());
+}
+void rank_pairs_rows(const float* s, const float* y, long long n, long long r0, long long nr, const RankWs& ws,
+                     cudaStream_t st) {
+  if (nr <= 0 || n <= 0) return;
+  dim3 grid(ceil_div(nr, kRankBlock), ceil_div(n, kRankChunk));
+  rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(s, nullptr, 0, 0, nullptr, nullptr, y, n, ws.gs_part, ws.loss_part,
+                                                 ws.pairs_part, nullptr, r0, nr);
+  MOSES_CUDA(cudaGetLastError());
+}
+// (loss sum, pair count) of the partials of nr rows -> out[0..1] (fixed order, one block)
+__global__ void __launch_bounds__(kFinBlock) rank_totals_kernel(const double* loss_part, const long long* pairs_part,
+                                                                int nsplit, long long nr, double* out) {
+  using BR = cub::BlockReduce<double, kFinBlock>;
+  using BRL = cub::BlockReduce<long long, kFinBlock>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ typename BRL::TempStorage tmpl;
+  long long p = 0;
+  double l = 0.0;
+  for (long long i = threadIdx.x; i < nr; i += kFinBlock)
+    for (int sp = 0; sp < nsplit; ++sp) {
+      p += pairs_part[sp * nr + i];
+      l += loss_part[sp * nr + i];
+    }
+  const long long pt = BRL(tmpl).Sum(p);
+  __syncthreads();
+  const double lt = BR(tmp).Sum(l);
+  if (threadIdx.x == 0) {
+    out[0] = lt;
+    out[1] = double(pt);
+  }
+}
+void rank_local_totals(const RankWs& ws, long long nr, double* out, cudaStream_t st) {
+  rank_totals_kernel<<<1, kFinBlock, 0, st>>>(ws.loss_part, ws.pairs_part, ws.nsplit, nr, out);
   MOSES_CUDA(cudaGetLastError());
 }
 void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
@@ -1593,15 +1633,34 @@ void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* 
   if (n <= 0) return;
   dim3 grid(ceil_div(n, kRankBlock), ceil_div(n, kRankChunk));
   rank_pairs_kernel<<<grid, kRankBlock, 0, st>>>(nullptr, part, ntiles, ld, hb, seg, y, n, ws.gs_part, ws.loss_part,
-                                                 ws.pairs_part, s_out);
+                                                 ws.pairs_part, s_out, 0, n);
   MOSES_CUDA(cudaGetLastError());
 }
 
 void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
-                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st) {
+                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st, const double* totals) {
   rank_finalize_kernel<<<1, kFinBlock, 0, st>>>(ws.gs_part, ws.loss_part, ws.pairs_part, ws.nsplit, n, roff, part2,
                                                 ntiles2, ld2, adv_bias, beta, out.loss, out.pairs, out.coefA, out.coefB,
-                                                out.ce, out.seg_of_row, out.R_rows, out.gb);
+                                                out.ce, out.seg_of_row, out.R_rows, out.gb, totals);
+  MOSES_CUDA(cudaGetLastError());
+}
+
+// sharded top-k: the k local winners (score, global index); slots past k_valid padded (-inf, -1)
+__global__ void topk_winners_kernel(const float* __restrict__ s, const long long* __restrict__ idx, long long k_valid,
+                                    long long k, long long row0, float* __restrict__ out_s, long long* __restrict__ out_i) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < k; i += (long long)gridDim.x * blockDim.x) {
+    if (i < k_valid) {
+      out_s[i] = s[idx[i]];
+      out_i[i] = idx[i] + row0;
+    } else {
+      out_s[i] = -INFINITY;
+      out_i[i] = -1;
+    }
+  }
+}
+void topk_winners(const float* s, const long long* idx, long long k_valid, long long k, long long row0, float* out_s,
+                  long long* out_i, cudaStream_t st) {
+  topk_winners_kernel<<<ceil_div(k, 256), 256, 0, st>>>(s, idx, k_valid, k, row0, out_s, out_i);
   MOSES_CUDA(cudaGetLastError());
 }
 

@@ -79,7 +79,16 @@ struct FinalizeOut {
   float* gb = nullptr;              // pooled: head-bias gradient
 };
 void rank_finalize(const RankWs& ws, long long n, long long roff, const float* part2, int ntiles2, long long ld2,
-                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st);
+                   const float* adv_bias, double beta, const FinalizeOut& out, cudaStream_t st,
+                   const double* totals = nullptr);
+// data-parallel exact batches: rows [r0, r0+nr) against all n columns (partials at [split][i - r0]),
+// and the (loss sum, pair count) of those rows' partials -> out[0..1]
+void rank_pairs_rows(const float* s, const float* y, long long n, long long r0, long long nr, const RankWs& ws,
+                     cudaStream_t st);
+void rank_local_totals(const RankWs& ws, long long nr, double* out, cudaStream_t st);
+// sharded top-k: winners' (score, idx + row0) from device indices; slots [k_valid, k) = (-inf, -1)
+void topk_winners(const float* s, const long long* idx, long long k_valid, long long k, long long row0, float* out_s,
+                  long long* out_i, cudaStream_t st);
 // rank_pairs_fused + rank_finalize in one launch (no adversary); `ticket` is a zeroed device
 // counter the kernel re-arms. Returns false (nothing launched) when n is out of its range.
 bool rank_step(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,

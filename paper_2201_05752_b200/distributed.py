@@ -9,7 +9,10 @@
 * Training (cfg5): data parallel; the flat fp32 gradient buffer of the device
   handle is averaged across ranks between gradients and update.
 
-torch.distributed is the transport (NCCL over NVLink on B200; gloo in the CPU tests).
+The collectives of the data path live in the library (libmoses_gpu.so over NCCL, csrc/comm.cu):
+`Comm` wraps a moses_comm_t, created per rank from an id distributed through torch.distributed
+(`Comm.from_torch`) or for several GPUs of one process (`Comm.init_all`). torch.distributed is only the
+rendezvous here, and the transport of the gloo CPU tests of the host logic.
 """
 from __future__ import annotations
 
@@ -117,3 +120,84 @@ def device_gradient_tensor(model):
             self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
 
     return torch.as_tensor(_CAI(C.cast(g, C.c_void_p).value, model.P), device="cuda")
+
+
+class Comm:
+    """A library NCCL communicator (moses_comm_t)."""
+
+    ID_BYTES = 128
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def from_torch(cls, group=None):
+        """One communicator per rank of a torch.distributed group, on the current CUDA device: rank 0 makes
+        the NCCL id, torch.distributed broadcasts it, every rank calls moses_comm_init_rank."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import moseslab as ml
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        buf = (C.c_uint8 * cls.ID_BYTES)()
+        if rank == 0:
+            ml._ck(ml.lib().moses_comm_unique_id(buf, cls.ID_BYTES))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        idb = (C.c_uint8 * cls.ID_BYTES).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        ml._ck(ml.lib().moses_comm_init_rank(idb, world, rank, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def init_all(cls, devices):
+        """ncclCommInitAll: one communicator per listed device, driven from this process."""
+        import ctypes as C
+
+        from . import moseslab as ml
+
+        n = len(devices)
+        devs = (C.c_int32 * n)(*devices)
+        hs = (C.c_void_p * n)()
+        ml._ck(ml.lib().moses_comm_init_all(n, devs, hs))
+        return [cls(C.c_void_p(hs[i])) for i in range(n)]
+
+    def info(self):
+        import ctypes as C
+
+        from . import moseslab as ml
+
+        n, r, d = C.c_int32(), C.c_int32(), C.c_int32()
+        ml._ck(ml.lib().moses_comm_info(self.h, C.byref(n), C.byref(r), C.byref(d)))
+        return n.value, r.value, d.value
+
+    def close(self):
+        from . import moseslab as ml
+
+        if getattr(self, "h", None):
+            ml.lib().moses_comm_destroy(self.h)
+            self.h = None
+
+
+DP_NONE, DP_AVERAGE, DP_EXACT = 0, 1, 2
+
+
+def set_data_parallel(model, comm, mode):
+    """moses_model_set_comm: DP_AVERAGE (each rank its own batch, averaged gradients) or DP_EXACT (one global
+    batch, the rank-ordered concatenation of the ranks' rows)."""
+    from . import moseslab as ml
+
+    ml._ck(ml.lib().moses_model_set_comm(model.h, comm.h if comm is not None else None, mode))
+
+
+def topk_sharded(comm, scores_dev_ptr, n_local: int, row0: int, k: int) -> np.ndarray:
+    """moses_topk_sharded: the global top-k of a pool sharded by contiguous ranges (same on every rank)."""
+    import ctypes as C
+
+    from . import moseslab as ml
+
+    out = (C.c_int64 * k)()
+    ml._ck(ml.lib().moses_topk_sharded(comm.h, scores_dev_ptr, n_local, row0, k, out))
+    return np.frombuffer(out, dtype=np.int64).copy()

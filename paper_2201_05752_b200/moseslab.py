@@ -164,6 +164,18 @@ def lib():
         "moses_read_mask": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, vp]),
         "moses_model_device_ptrs": (C.c_int, [vp, vp, vp, vp]),
         "moses_model_stream": (C.c_int, [vp, vp]),
+        "moses_comm_unique_id": (C.c_int, [vp, i64]),
+        "moses_comm_init_rank": (C.c_int, [vp, i32, i32, vp]),
+        "moses_comm_init_all": (C.c_int, [i32, vp, vp]),
+        "moses_comm_destroy": (C.c_int, [vp]),
+        "moses_comm_info": (C.c_int, [vp, vp, vp, vp]),
+        "moses_model_set_comm": (C.c_int, [vp, vp, i32]),
+        "moses_dp_allreduce_gradients": (C.c_int, [vp, i32]),
+        "moses_dp_train_step": (C.c_int, [vp, vp, i64, vp, i64, dbl, dbl, vp]),
+        "moses_dp_exact_forward": (C.c_int, [vp, vp, i64, vp, i64, vp, vp]),
+        "moses_dp_exact_rank": (C.c_int, [vp, vp, vp, i64, i64, vp]),
+        "moses_dp_exact_backward": (C.c_int, [vp, i64, vp, vp]),
+        "moses_topk_sharded": (C.c_int, [vp, vp, i64, i64, i64, vp]),
         "moses_debug_gemm": (C.c_int, [C.c_int] * 4 + [vp, C.c_longlong, C.c_int, vp, C.c_longlong, C.c_int, C.c_int,
                                                        vp, C.c_longlong, vp, C.c_int, C.c_int, vp, C.c_longlong]),
     }
