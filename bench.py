@@ -206,19 +206,18 @@ def median(v):
     return s[len(s) // 2] if len(s) % 2 else 0.5 * (s[len(s) // 2 - 1] + s[len(s) // 2])
 
 
-class DataParallel:
-    """Gradient all-reduce of the device gradient buffer between gradients and update (N > 1)."""
+_COMM = None
 
-    def __init__(self, ml, dm, world, dist):
-        from paper_2201_05752_b200.distributed import device_gradient_tensor
 
-        self.ml, self.dm, self.world, self.dist = ml, dm, world, dist
-        self.grads = device_gradient_tensor(dm) if world > 1 else None
+def library_comm(world):
+    """The library's NCCL communicator of this rank (N > 1): every collective of the data path runs inside
+    libmoses_gpu.so (captured into the step graphs); torch.distributed only distributes the NCCL id."""
+    global _COMM
+    if world > 1 and _COMM is None:
+        from paper_2201_05752_b200.distributed import Comm
 
-    def step_tail(self, lr, mu):
-        if self.world > 1:
-            self.dist.all_reduce(self.grads, op=self.dist.ReduceOp.AVG)
-            self.ml._ck(self.ml.lib().moses_apply_update(self.dm.h, lr, mu, None, 0, 1))
+        _COMM = Comm.from_torch()
+    return _COMM
 
 
 def bench_cfg2(ml, L, args, rank, world, dist, peaks):
@@ -251,19 +250,18 @@ def bench_cfg2(ml, L, args, rank, world, dist, peaks):
     sp = C.c_void_p()
     L.moses_model_stream(dm.h, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
-    dp = DataParallel(ml, dm, world, dist)
+    if world > 1:  # throughput-mode DP: NCCL average of the gradients + update inside the step graph
+        from paper_2201_05752_b200.distributed import DP_AVERAGE, set_data_parallel
+
+        set_data_parallel(dm, library_comm(world), DP_AVERAGE)
     L.moses_set_async(1)
-    # one CUDA graph per step: device gather of the batch's programs -> pooled gradients [-> update]
+    # one CUDA graph per step: device gather of the batch's programs -> pooled gradients [-> all-reduce]
+    # -> update
     ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, BATCH,
-                                             rows_pad, LR, MU, int(world == 1)))
+                                             rows_pad, LR, MU, 1))
 
     def run_k(k):
-        if world == 1:
-            ml._ck(L.moses_train_graph_launch(dm.h, k))
-            return
-        for _ in range(k):
-            ml._ck(L.moses_train_graph_launch(dm.h, 1))
-            dp.step_tail(LR, MU)
+        ml._ck(L.moses_train_graph_launch(dm.h, k))
 
     out = {}
     with torch.cuda.stream(stream):
@@ -338,7 +336,8 @@ def bench_cfg2(ml, L, args, rank, world, dist, peaks):
                 rcs.append(async_step(dm.h, xp, ns, DIMS[0], op, BATCH, yp, LR, MU, loss_ptrs[k]))
                 return
             ml._ck(L.moses_gradients_pooled(dm.h, xp, ns, DIMS[0], op, BATCH, yp, C.byref(loss)))
-            dp.step_tail(LR, MU)
+            ml._ck(L.moses_dp_allreduce_gradients(dm.h, 1))
+            ml._ck(L.moses_apply_update(dm.h, LR, MU, None, 0, 1))
 
         for k in range(max(args.warmup, 300)):  # slot graphs captured, copy pipeline in steady state
             e2e_step(e2e_steps + (k % 64))
@@ -373,7 +372,8 @@ def bench_cfg2(ml, L, args, rank, world, dist, peaks):
                       "path": ("moses_train_step_pooled_async (C ABI: pinned host float64 rows/offsets/labels "
                                "uploaded every step, upload of step k+1 overlapping step k, per-step loss read "
                                "back; 4 distinct host batches)") if world == 1 else
-                              "moses_gradients_pooled + all-reduce + moses_apply_update (C ABI, pinned host buffers)"}
+                              "moses_gradients_pooled + moses_dp_allreduce_gradients (NCCL) + moses_apply_update "
+                              "(C ABI, pinned host buffers)"}
     out["dataset_bytes"] = int(X.numel() * X.element_size())
     dm.close()
     del X, Y
@@ -382,16 +382,19 @@ def bench_cfg2(ml, L, args, rank, world, dist, peaks):
 
 
 def bench_cfg5(ml, L, args, rank, world, dist, peaks):
-    """cfg5 shape: TenSet-scale training of {164,512,512,1} on 2M single-statement programs, batch 4096
-    per GPU (throughput-mode data parallel at N > 1), split bf16, graph replay. The GEMM roofline of
-    the step at a batch where the chains are throughput- rather than latency-bound."""
+    """cfg5: TenSet-scale training of {164,512,512,1} on 2M single-statement programs with a GLOBAL batch
+    of 4096 (exact-batch data parallel at N > 1: each rank holds 4096/N rows of every batch, scores are
+    all-gathered so the pair loss couples the whole batch, gradients summed over NCCL inside the step
+    graph), split bf16, graph replay. At N = 1 the GEMM roofline of the step at a batch where the chains
+    are throughput- rather than latency-bound."""
     import ctypes as C
 
     import torch
 
     from paper_2201_05752_b200.distributed import shard_range
 
-    dims, programs, batch = [164, 512, 512, 1], 2_000_000, 4096
+    dims, programs, gbatch = [164, 512, 512, 1], 2_000_000, 4096
+    batch = gbatch // world  # this rank's rows of every global batch
     lo, hi = shard_range(programs, rank, world)
     nb = (hi - lo) // batch
     dm = ml.DeviceModel(ml.init_random(dims, SEED_MODEL), ml.PREC_BF16X3, max_rows=batch)
@@ -404,41 +407,42 @@ def bench_cfg5(ml, L, args, rank, world, dist, peaks):
     sp = C.c_void_p()
     L.moses_model_stream(dm.h, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
-    dp = DataParallel(ml, dm, world, dist)
+    if world > 1:
+        from paper_2201_05752_b200.distributed import DP_EXACT, set_data_parallel
+
+        set_data_parallel(dm, library_comm(world), DP_EXACT)
     L.moses_set_async(1)
-    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, batch, LR, MU, int(world == 1)))
+    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, batch, LR, MU, 1))
 
     def run_k(k):
-        if world == 1:
-            ml._ck(L.moses_train_graph_launch(dm.h, k))
-            return
-        for _ in range(k):
-            ml._ck(L.moses_train_graph_launch(dm.h, 1))
-            dp.step_tail(LR, MU)
+        ml._ck(L.moses_train_graph_launch(dm.h, k))
 
     with torch.cuda.stream(stream):
         run_k(5)
         windows = timed_windows(run_k, 20, stream, world, dist)
         ms = median(windows) / 20
         xs = X[:batch]
+        step_fn = L.moses_dp_train_step if world > 1 else L.moses_train_step_device
         ml.profile_begin()
         for _ in range(10):
-            ml._ck(L.moses_train_step_device(dm.h, xs.data_ptr(), ld, Y.data_ptr(), batch, LR, MU, None))
+            ml._ck(step_fn(dm.h, xs.data_ptr(), ld, Y.data_ptr(), batch, LR, MU, None))
         torch.cuda.synchronize()
         prof = ml.profile_end()
     L.moses_set_async(0)
     gemm_ms = sum(prof[c][0] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / 10
-    flops = gemm_flops_per_step(dims, batch)
+    flops = gemm_flops_per_step(dims, batch)  # this GPU's rows
     peak = peaks.get("bf16_tflops_sustained", 1395.6)
     ach = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
     dm.close()
     del X, Y
     torch.cuda.empty_cache()
-    return {"workload": f"cfg5: train {dims} on {programs} single-statement programs, batch {batch} per GPU, "
-                        f"split bf16, {world} GPU(s) (throughput-mode DP)",
-            "value": world * batch / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+    return {"workload": f"cfg5: train {dims} on {programs} single-statement programs, global batch {gbatch} "
+                        f"({batch} rows per GPU), split bf16, {world} GPU(s)"
+                        + (" (exact-batch DP: score all-gather + gradient all-reduce over NCCL in the step graph)"
+                           if world > 1 else ""),
+            "value": gbatch / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
             "timed_windows": len(windows), "steps_per_window": 20,
-            "scaling": "weak",
+            "scaling": "strong",
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak if ach else None, "mma_per_product": 3,
                          "tensor_pipe_frac": 3 * ach / peak if ach else None, "flops_per_step": flops,
@@ -460,7 +464,7 @@ def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
 
     import torch
 
-    from paper_2201_05752_b200.distributed import gather_merge_topk, shard_range
+    from paper_2201_05752_b200.distributed import shard_range, topk_sharded
 
     chunk = 65536
     k = 1024
@@ -489,10 +493,12 @@ def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
             ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), dt_in, ld, n_local, S.data_ptr()))
             b.record(stream)
         torch.cuda.synchronize()
-        kk = min(k, n_local)
-        ml._ck(L.moses_topk_device(S.data_ptr(), n_local, kk, idx))
-        li = np.array(idx[:kk], dtype=np.int64)
-        win = gather_merge_topk(S[torch.from_numpy(li).cuda()].cpu().numpy(), li + lo, k) if world > 1 else li
+        if world > 1:  # local top-k + NCCL all-gather of the winners + comparator merge (library)
+            win = topk_sharded(library_comm(world), S.data_ptr(), n_local, lo, k)
+        else:
+            kk = min(k, n_local)
+            ml._ck(L.moses_topk_device(S.data_ptr(), n_local, kk, idx))
+            win = np.array(idx[:kk], dtype=np.int64)
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device="cuda", dtype=torch.float64)
@@ -526,7 +532,8 @@ def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
                                    "umma_fwd_pair (tcgen05 cta_group::2, weight-resident)",
                          "forward_device_ms": min(fwd_ms)},
             "inputs": f"device-resident {'fp32' if dt_in == ml.DTYPE_F32 else 'bf16'} packed features (> L2)",
-            "timing": "wall clock per pass (device forward + local top-k + all-gather merge), max over ranks"}
+            "timing": "wall clock per pass (device forward + local top-k + NCCL all-gather merge in the library), "
+                      "max over ranks"}
 
 
 def bench_cfg1(ml, L):

@@ -265,6 +265,16 @@ MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t 
 MOSES_API int moses_mmd2_device(const float* xs, int64_t m, const float* xt, int64_t n, int32_t width, int64_t ld,
                                 double sigma, double* out);
 
+/* MMD^2 as a differentiable domain loss (north-star (4)): gradients() with beta * MMD^2(H_source, H_batch)
+ * of the last hidden layer added to the objective, in the slot the reference's discriminator term uses
+ * (model.cpp:215-238): `source` = ms source-domain rows (D wide; the replay rows), x / y the target batch.
+ * loss_out = rank loss + beta * MMD^2. beta == 0 is gradients() bit for bit. Unpooled rows. */
+MOSES_API int moses_gradients_mmd(moses_model_t m, const double* x, const double* y, int64_t n, int32_t D,
+                                  const double* source, int64_t ms, double beta, double sigma, double* loss_out);
+/* MMD^2 and d MMD^2 / d row for every source / target row (grad_s: m x width, grad_t: n x width, host). */
+MOSES_API int moses_mmd2_grad(const double* xs, int64_t m, const double* xt, int64_t n, int32_t width, double sigma,
+                              double* value, double* grad_s, double* grad_t);
+
 /* ------------------------------------------------------------------ candidate generation */
 /* Configurations [first, first+n) of a task's knob space in enumerate_configs order (space.cpp:168-191,
  * last knob fastest), on the device: encode_features rows (space.cpp:140-159; D >= 10 columns, entries

@@ -740,6 +740,77 @@ R mmd2(const R* xs, int m, const R* xt, int n, int width, R sigma) {
   return ss / (R(m) * R(m)) + tt / (R(n) * R(n)) - R(2) * st / (R(m) * R(n));
 }
 
+// d MMD^2 / d row for the biased estimator above: with alpha = 1/m (source), -1/n (target),
+// MMD^2 = sum_a alpha_a r_a, r_a = sum_b alpha_b k_ab and d/dx_a = -4c alpha_a (x_a r_a - sum_b alpha_b k_ab x_b),
+// c = 1/(2 sigma^2) (k = exp(-c |a-b|^2), dk/da = -2c (a - b) k). Returns MMD^2.
+template <class R>
+R mmd2_grad(const R* xs, int m, const R* xt, int n, int width, R sigma, R* gs, R* gt) {
+  const R c = R(1) / (R(2) * sigma * sigma);
+  const int rows = m + n;
+  auto row = [&](int a) { return a < m ? xs + std::size_t(a) * width : xt + std::size_t(a - m) * width; };
+  auto alpha = [&](int a) { return a < m ? R(1) / R(m) : R(-1) / R(n); };
+  R value = R(0);
+  std::vector<R> o(width);
+  for (int a = 0; a < rows; ++a) {
+    const R* xa = row(a);
+    std::fill(o.begin(), o.end(), R(0));
+    R r = R(0);
+    for (int b = 0; b < rows; ++b) {
+      const R* xb = row(b);
+      R d = R(0);
+      for (int j = 0; j < width; ++j) { const R t = xa[j] - xb[j]; d += t * t; }
+      const R wk = alpha(b) * std::exp(-c * d);
+      r += wk;
+      for (int j = 0; j < width; ++j) o[j] += wk * xb[j];
+    }
+    value += alpha(a) * r;
+    R* g = a < m ? gs + std::size_t(a) * width : gt + std::size_t(a - m) * width;
+    for (int j = 0; j < width; ++j) g[j] = R(-4) * c * alpha(a) * (xa[j] * r - o[j]);
+  }
+  return value;
+}
+
+// gradients() (model.cpp:192-244) with beta * MMD^2(H_source, H_batch) of the last hidden layer as the
+// domain term (north-star (4); the reference's discriminator slot, model.cpp:215-238): the source rows
+// (ms x D) are forwarded, the MMD gradient enters dH of the batch rows (next to gs * w_head) and of the
+// source rows; source rows backprop first, then the batch (model.cpp:235,240).
+template <class R>
+std::vector<R> gradients_mmd(const Params<R>& p, const R* x, const R* y, int n, const R* src, int ms, R beta, R sigma,
+                             R* loss_out, int threads = 1) {
+  if (beta == R(0) || n == 0) return gradients(p, x, y, n, static_cast<const Adversary<R>*>(nullptr), R(0), loss_out,
+                                               threads);
+  const int L = p.levels();
+  const int dl = p.dims[L - 1];
+  std::vector<R> g(p.w.size(), R(0));
+  const Forward<R> f = run_forward(p, x, n, threads);
+  const Forward<R> fs = run_forward(p, src, ms, threads);
+  R rank_loss = R(0);
+  std::vector<R> gs(n);
+  ranking_terms(f.s.data(), y, n, &rank_loss, gs.data());
+  const std::vector<R>& hl = f.h.back();
+  R* GW = g.data() + level_offset(p.dims, L - 1);
+  for (int j = 0; j < dl; ++j) {
+    R acc = R(0);
+    for (int r = 0; r < n; ++r) acc = std::fma(gs[r], hl[std::size_t(r) * dl + j], acc);
+    GW[j] = acc;
+  }
+  R gsum = R(0);
+  for (int r = 0; r < n; ++r) gsum += gs[r];
+  GW[dl] = gsum;
+  std::vector<R> gms(std::size_t(ms) * dl), gmt(std::size_t(n) * dl);
+  const R mmd = mmd2_grad(fs.h.back().data(), ms, hl.data(), n, dl, sigma, gms.data(), gmt.data());
+  const R* wh = p.W(L - 1);
+  std::vector<R> dh(std::size_t(n) * dl);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < dl; ++j) dh[std::size_t(r) * dl + j] = gs[r] * wh[j] + beta * gmt[std::size_t(r) * dl + j];
+  std::vector<R> dhs(std::size_t(ms) * dl);
+  for (std::size_t i = 0; i < dhs.size(); ++i) dhs[i] = beta * gms[i];
+  backprop_from_penultimate(p, fs, src, ms, std::move(dhs), g, threads);
+  backprop_from_penultimate(p, f, x, n, std::move(dh), g, threads);
+  if (loss_out != nullptr) *loss_out = rank_loss + beta * mmd;
+  return g;
+}
+
 // Masked Adam (bias-corrected), same skip rule as apply_update.
 template <class R>
 void adam_update(R* w, R* m1, R* m2, const R* g, std::int64_t P, const std::uint8_t* keep, double lr,

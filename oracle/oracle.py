@@ -55,6 +55,10 @@ def lib():
         build() if not os.path.exists(_SO) else None
         _lib = C.CDLL(_SO)
         _lib.orc_last_error.restype = C.c_char_p
+        vp, ci, cd = C.c_void_p, C.c_int, C.c_double
+        _lib.orc_mmd2_grad_f64.argtypes = [vp, ci, vp, ci, ci, cd, vp, vp, vp]
+        _lib.orc_gradients_mmd_f64.argtypes = [vp, ci, vp, vp, vp, ci, vp, ci, cd, cd, vp, vp, ci]
+        _lib.orc_gradients_from_score_grads_f64.argtypes = [vp, ci, vp, vp, ci, vp, vp, ci]
         for name in ("orc_splitmix_draw", "orc_splitmix_at", "orc_fnv_u64s", "orc_fnv_str", "orc_fnv_u64_str"):
             getattr(_lib, name).restype = C.c_uint64
         _lib.orc_splitmix_draw.argtypes = [C.c_uint64, C.c_int]
@@ -242,6 +246,31 @@ def gradients_from_score_grads(dims, w, x, gs, threads=1):
     g = np.zeros_like(w)
     _check(lib().orc_gradients_from_score_grads_f64(_p(d), len(d), _p(w), _p(x), x.shape[0], _p(gs), _p(g), threads))
     return g
+
+
+def mmd2_grad(xs, xt, sigma):
+    """Biased Gaussian MMD^2 and its gradient w.r.t. every source / target row (fp64)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    xt = np.ascontiguousarray(xt, dtype=np.float64)
+    gs, gt = np.zeros_like(xs), np.zeros_like(xt)
+    v = C.c_double()
+    _check(lib().orc_mmd2_grad_f64(_p(xs), xs.shape[0], _p(xt), xt.shape[0], xs.shape[1], C.c_double(sigma),
+                                   C.byref(v), _p(gs), _p(gt)))
+    return v.value, gs, gt
+
+
+def gradients_mmd(dims, w, x, y, src, beta, sigma, threads=1):
+    """gradients() with beta * MMD^2(H_src, H_batch) as the domain term -> (g_flat, loss), fp64."""
+    d = _dims(dims)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    g = np.zeros_like(w)
+    loss = C.c_double()
+    _check(lib().orc_gradients_mmd_f64(_p(d), len(d), _p(w), _p(x), _p(y), x.shape[0], _p(src), src.shape[0],
+                                       C.c_double(beta), C.c_double(sigma), _p(g), C.byref(loss), threads))
+    return g, loss.value
 
 
 def pair_terms_rows(s_global, y_global, r0, r1):

@@ -142,6 +142,21 @@ ORC_RANK(f32, float)
 ORC_GRAD(f64, double)
 ORC_GRAD(f32, float)
 
+ORC int orc_mmd2_grad_f64(const double* xs, int m, const double* xt, int n, int width, double sigma, double* value,
+                         double* gs, double* gt) {
+  return guarded([&] { *value = mmd2_grad(xs, m, xt, n, width, sigma, gs, gt); });
+}
+
+ORC int orc_gradients_mmd_f64(const int* dims, int nd, const double* w, const double* x, const double* y, int n,
+                             const double* src, int ms, double beta, double sigma, double* g_out, double* loss_out,
+                             int threads) {
+  return guarded([&] {
+    Params<double> p = make_params<double>(dims, nd, w, nullptr);
+    std::vector<double> g = gradients_mmd(p, x, y, n, src, ms, beta, sigma, loss_out, threads);
+    std::memcpy(g_out, g.data(), sizeof(double) * g.size());
+  });
+}
+
 ORC int orc_gradients_from_score_grads_f64(const int* dims, int nd, const double* w, const double* x, int n,
                                           const double* gs, double* g_out, int threads) {
   return guarded([&] {

@@ -257,6 +257,8 @@ struct moses_model {
     long long graph_kernels = 0;
   } plan;
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
+  float* mmd_g = nullptr;          // MMD loss: d MMD^2 / dH of every row (cap x W)
+  double* mmd_v = nullptr;         // MMD loss: per-row value partials (cap)
   // data parallel (moses_model_set_comm): 1 = average the gradients of every rank's own batch
   // (throughput mode), 2 = exact batch (the global batch is the rank-ordered concatenation of every
   // rank's rows; scores all-gathered, pair terms of the own rows, gradients summed)
@@ -377,6 +379,8 @@ struct moses_model {
     dfree(plan.stage);
     dfree(dcounter);
     dfree(gbias);
+    dfree(mmd_g);
+    dfree(mmd_v);
     dfree(dp_s);
     dfree(dp_y);
     dfree(dp_tot);
@@ -498,7 +502,8 @@ struct SgdFuse {  // momentum-SGD step fused into the grouped weight-gradient ep
 // Returns true when `fuse` was applied (every parameter updated) inside the backward pass.
 template <typename T>
 bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* u,
-                   const float* gb_override = nullptr, const SgdFuse* fuse = nullptr) {
+                   const float* gb_override = nullptr, const SgdFuse* fuse = nullptr, const float* extra = nullptr,
+                   float extra_scale = 0.f) {
   // Two streams: the data-gradient chain (head backward -> dgrad(L-2) -> ... -> dgrad(1)) runs on
   // st; every weight-gradient GEMM (and the head-gradient column reduction) runs on st2 as soon
   // as its dZ is ready. At batch 512 each GEMM fills only 16-40 of the 148 SMs, so the two
@@ -516,7 +521,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   {
     ProfScope ps(P_HEAD, m->st);
     head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
-                     m->lddz[L - 1], m->st, m->dz_lo_t<T>(L - 1));
+                     m->lddz[L - 1], m->st, m->dz_lo_t<T>(L - 1), extra, extra_scale);
   }
   MOSES_CUDA(cudaEventRecord(ev[1 + (L - 1)], m->st));
   note_launch(2);
@@ -781,14 +786,29 @@ void ensure_rank_ws(moses_model* m, long long n) {
   m->rank_ws_rows = n;
 }
 
+// MMD^2 domain term (north-star (4)): rows [0, rows) of the step are source rows (the replay rows'
+// slot), beta * MMD^2(H_src, H_batch) joins the loss and its gradient enters dH of every row.
+struct MmdTerm {
+  long long rows = 0;
+  double beta = 0.0;
+  double sigma = 1.0;
+};
+void ensure_mmd_ws(moses_model* m) {
+  if (m->mmd_g) return;
+  m->mmd_g = dalloc<float>(size_t(m->cap) * m->W());
+  m->mmd_v = dalloc<double>(m->cap);
+}
+
 // gradients() core on rows already packed at act[0] (or x0): [0, mrep) replay, [mrep, mrep+n) batch;
 // pooled: rows [0, pool->rows) are statements of the n programs.
 // Returns true when `fuse` (momentum SGD) was applied inside the backward pass; the caller runs
 // the separate update otherwise.
 bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float* y, long long n, moses_adversary* adv,
-                    double beta, const Pool* pool = nullptr, const SgdFuse* fuse = nullptr) {
+                    double beta, const Pool* pool = nullptr, const SgdFuse* fuse = nullptr,
+                    const MmdTerm* mmd = nullptr) {
   const bool active = adv != nullptr && beta != 0.0 && n > 0 && pool == nullptr;
-  const long long mrep = active ? adv->m : 0;
+  const bool mmd_on = mmd != nullptr && mmd->beta != 0.0 && n > 0 && pool == nullptr && !active;
+  const long long mrep = active ? adv->m : (mmd_on ? mmd->rows : 0);
   const long long R = pool ? pool->rows : mrep + n;
   ensure_rank_ws(m, n);  // before any capture-sensitive work (warm-ups reach here with the captured n)
   if (n == 0 || R == 0) {
@@ -799,14 +819,14 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   }
   const float* u = active ? adv->u : nullptr;
   dispatch_forward(m, x0, ldx0, R, u, true);
-  if (!active && g_rank_fused) {
+  if (!active && !mmd_on && g_rank_fused) {
     if (!m->rank_ticket) {
       m->rank_ticket = dalloc<unsigned int>(1);
       MOSES_CUDA(cudaMemsetAsync(m->rank_ticket, 0, sizeof(unsigned int), m->st));
     }
   }
   bool ranked = false;
-  if (!active && g_rank_fused && m->rank_ticket) {
+  if (!active && !mmd_on && g_rank_fused && m->rank_ticket) {
     ProfScope ps(P_RANK, m->st);
     FinalizeOut fo{m->dscal, m->dpairs, m->coefA, m->coefB, m->dscal + 1};
     if (pool) fo.gb = m->gbias;
@@ -830,8 +850,24 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
     note_launch(2);
   }
   const float* gbo = pool ? m->gbias : nullptr;
-  const bool fused = m->esz == 2 ? backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, gbo, fuse)
-                                 : backward_rows<float>(m, x0, ldx0, R, u, gbo, fuse);
+  const float* extra = nullptr;
+  if (mmd_on) {  // beta * MMD^2 between the source rows' and the batch rows' last hidden layer
+    ensure_mmd_ws(m);
+    const int W = m->W();
+    ProfScope ps(P_OTHER, m->st);
+    if (m->esz == 2)
+      mmd_grad<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(m->act[m->L - 1]), m->act_lo_t<__nv_bfloat16>(m->L - 1),
+                              m->ld[m->L - 1], R, mrep, W, float(mmd->sigma), m->mmd_g, m->mmd_v, m->dscal,
+                              mmd->beta, true, m->st);
+    else
+      mmd_grad<float>(static_cast<const float*>(m->act[m->L - 1]), m->act_lo_t<float>(m->L - 1), m->ld[m->L - 1], R,
+                      mrep, W, float(mmd->sigma), m->mmd_g, m->mmd_v, m->dscal, mmd->beta, true, m->st);
+    note_launch(2);
+    extra = m->mmd_g;
+  }
+  const float escale = mmd_on ? float(mmd->beta) : 0.f;
+  const bool fused = m->esz == 2 ? backward_rows<__nv_bfloat16>(m, x0, ldx0, R, u, gbo, fuse, extra, escale)
+                                 : backward_rows<float>(m, x0, ldx0, R, u, gbo, fuse, extra, escale);
   m->xi_valid = false;
   return fused;
 }
@@ -2690,6 +2726,60 @@ MOSES_API int moses_mmd2(const double* xs, int64_t m, const double* xt, int64_t 
     int launched = 0;
     *out = mmd2_tc(H, m, H + m * width, n, width, width, float(sigma), ws, sc.st, &launched);
     note_launch(1 + launched);
+  });
+}
+
+// gradients() with the MMD^2 domain term in the adversary's slot (north-star (4); model.cpp:192-244 with
+// beta * MMD^2(H_source, H_batch) added to the objective): `source` holds ms source-domain rows (the
+// replay rows, D wide), x / y the target batch. loss_out = rank loss + beta * MMD^2. beta == 0 skips the
+// term bit-exactly (gradients()).
+MOSES_API int moses_gradients_mmd(moses_model_t m, const double* x, const double* y, int64_t n, int32_t D,
+                                  const double* source, int64_t ms, double beta, double sigma, double* loss_out) {
+  return guarded([&] {
+    require_model(m);
+    if (D != m->dims[0]) fail(MOSES_ERR_DIM_MISMATCH, "feature width != model input width");
+    if (!(sigma > 0.0)) fail(MOSES_ERR_INVALID_ARG, "sigma must be positive");
+    const bool on = beta != 0.0 && n > 0;
+    if (on && (ms <= 0 || source == nullptr)) fail(MOSES_ERR_ADVERSARY_DISABLED, "MMD needs source rows");
+    const long long mrep = on ? ms : 0;
+    check_rows(m, mrep + n);
+    if (on) upload_rows(m, source, ms, 0);
+    upload_rows(m, x, n, mrep);
+    upload_f32(m, y, n, m->labels);
+    const MmdTerm mt{mrep, beta, sigma};
+    gradients_core(m, m->act[0], m->ld[0], m->labels, n, nullptr, 0.0, nullptr, nullptr, on ? &mt : nullptr);
+    if (loss_out) MOSES_CUDA(cudaMemcpyAsync(loss_out, m->dscal, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    MOSES_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+// MMD^2 and its gradient w.r.t. every source and target row (host float64 rows; device fp32 math).
+MOSES_API int moses_mmd2_grad(const double* xs, int64_t m, const double* xt, int64_t n, int32_t width, double sigma,
+                              double* value, double* grad_s, double* grad_t) {
+  return guarded([&] {
+    if (m <= 0 || n <= 0 || width <= 0) fail(MOSES_ERR_SHAPE_MISMATCH, "empty MMD input");
+    if (!(sigma > 0.0)) fail(MOSES_ERR_INVALID_ARG, "sigma must be positive");
+    Scratch& sc = scratch();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const long long R = m + n;
+    const size_t bytes = sizeof(double) * R * width + sizeof(float) * R * width * 2 + sizeof(double) * (R + 2) + 4096;
+    Carver cv{static_cast<uint8_t*>(sc.ensure(bytes))};
+    double* h64 = cv.take<double>(size_t(R) * width);
+    float* h = cv.take<float>(size_t(R) * width);
+    float* g = cv.take<float>(size_t(R) * width);
+    double* vp = cv.take<double>(size_t(R));
+    double* val = cv.take<double>(2);
+    MOSES_CUDA(cudaMemcpyAsync(h64, xs, sizeof(double) * m * width, cudaMemcpyHostToDevice, sc.st));
+    MOSES_CUDA(cudaMemcpyAsync(h64 + m * width, xt, sizeof(double) * n * width, cudaMemcpyHostToDevice, sc.st));
+    f64_to_f32(h64, R * width, h, sc.st);
+    mmd_grad<float>(h, nullptr, width, R, m, width, float(sigma), g, vp, val, 1.0, false, sc.st);
+    note_launch(3);
+    f32_to_f64(g, R * width, h64, sc.st);
+    MOSES_CUDA(cudaMemcpyAsync(value, val, sizeof(double), cudaMemcpyDeviceToHost, sc.st));
+    if (grad_s) MOSES_CUDA(cudaMemcpyAsync(grad_s, h64, sizeof(double) * m * width, cudaMemcpyDeviceToHost, sc.st));
+    if (grad_t)
+      MOSES_CUDA(cudaMemcpyAsync(grad_t, h64 + m * width, sizeof(double) * n * width, cudaMemcpyDeviceToHost, sc.st));
+    MOSES_CUDA(cudaStreamSynchronize(sc.st));
   });
 }
 

@@ -877,7 +877,7 @@ template <typename T>
 __global__ void head_backward_kernel(const float* __restrict__ coefA, const float* __restrict__ coefB,
                                      const float* __restrict__ wh, const float* __restrict__ u, const T* __restrict__ H,
                                      long long ldh, long long R, int W, T* __restrict__ dz, long long ldz,
-                                     T* __restrict__ dz_lo) {
+                                     T* __restrict__ dz_lo, const float* __restrict__ extra, float extra_scale) {
   ptx::pdl_launch_dependents();
   const long long total = R * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -885,6 +885,7 @@ __global__ void head_backward_kernel(const float* __restrict__ coefA, const floa
     const int j = int(i - r * W);
     float v = coefA[r] * wh[j];
     if (u != nullptr) v += coefB[r] * u[j];
+    if (extra != nullptr) v += extra_scale * extra[i];  // d(beta * MMD^2)/dH (row-major R x W)
     store_operand(dz, dz_lo, r * ldz + j, to_f(H[r * ldh + j]) > 0.f ? v : 0.f);
   }
 }
@@ -1645,6 +1646,99 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
   MOSES_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- MMD^2 as a differentiable loss
+// Biased MMD^2 with k(a,b) = exp(-c |a-b|^2), c = 1/(2 sigma^2), over rows a of X = [S; T] (m source
+// rows, then n target rows) with alpha_a = 1/m (source) or -1/n (target):
+//   MMD^2 = sum_a alpha_a r_a,   r_a = sum_b alpha_b k_ab
+//   dMMD^2/dx_a = -4 c alpha_a (x_a r_a - O_a),   O_a = sum_b alpha_b k_ab x_b
+// One warp per row a (lane holds features lane + 32q), the rows b staged through shared memory in
+// tiles; distances from the differences (no |a|^2 + |b|^2 - 2ab cancellation), fp32 accumulation.
+constexpr int kMmdRowsPerBlock = 8, kMmdTile = 16;
+template <typename T, int Q>
+__global__ void __launch_bounds__(kMmdRowsPerBlock * 32) mmd_grad_kernel(const T* __restrict__ H, const T* __restrict__ H_lo,
+                                                                       long long ld, long long R, long long m, int W,
+                                                                       float c, float* __restrict__ G,
+                                                                       double* __restrict__ vpart) {
+  __shared__ float tile[kMmdTile][Q * 32];
+  __shared__ float alpha[kMmdTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long a = (long long)blockIdx.x * kMmdRowsPerBlock + warp;
+  const float as = 1.f / float(m), at = -1.f / float(R - m);
+  float xa[Q], O[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int f = lane + 32 * q;
+    xa[q] = (a < R && f < W) ? load_operand(H, H_lo, a * ld + f) : 0.f;
+    O[q] = 0.f;
+  }
+  float r = 0.f;
+  for (long long b0 = 0; b0 < R; b0 += kMmdTile) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kMmdTile * Q * 32; e += blockDim.x) {
+      const int bi = e / (Q * 32), f = e - bi * (Q * 32);
+      const long long b = b0 + bi;
+      tile[bi][f] = (b < R && f < W) ? load_operand(H, H_lo, b * ld + f) : 0.f;
+    }
+    if (threadIdx.x < kMmdTile) alpha[threadIdx.x] = (b0 + threadIdx.x < R) ? (b0 + threadIdx.x < m ? as : at) : 0.f;
+    __syncthreads();
+    const int nb = int(min((long long)kMmdTile, R - b0));
+    for (int bi = 0; bi < nb; ++bi) {
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float t = xa[q] - tile[bi][lane + 32 * q];
+        d = fmaf(t, t, d);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const float wk = alpha[bi] * expf(-c * d);
+      r += wk;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) O[q] = fmaf(wk, tile[bi][lane + 32 * q], O[q]);
+    }
+  }
+  if (a >= R) return;
+  const float aa = a < m ? as : at;
+  const float s = -4.f * c * aa;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int f = lane + 32 * q;
+    if (f < W) G[a * W + f] = s * fmaf(xa[q], r, -O[q]);
+  }
+  if (lane == 0) vpart[a] = double(aa) * double(r);
+}
+__global__ void sum_f64_kernel(const double* __restrict__ v, long long n, double scale, double* out, int accumulate) {
+  using BR = cub::BlockReduce<double, 1024>;
+  __shared__ typename BR::TempStorage tmp;
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) acc += v[i];
+  const double t = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) {
+    out[0] = accumulate ? out[0] + scale * t : scale * t;
+  }
+}
+template <typename T>
+void mmd_grad(const T* H, const T* H_lo, long long ld, long long R, long long m, int W, float sigma, float* G,
+              double* vpart, double* value_out, double scale, bool accumulate, cudaStream_t st) {
+  if (m <= 0 || R - m <= 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "MMD needs source and target rows");
+  const float c = 1.f / (2.f * sigma * sigma);
+  const int blocks = ceil_div(R, kMmdRowsPerBlock);
+  if (W <= 128)
+    mmd_grad_kernel<T, 4><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
+  else if (W <= 256)
+    mmd_grad_kernel<T, 8><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
+  else if (W <= 512)
+    mmd_grad_kernel<T, 16><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
+  else
+    fail(MOSES_ERR_INVALID_ARG, "MMD loss supports representation widths <= 512");
+  sum_f64_kernel<<<1, 1024, 0, st>>>(vpart, R, scale, value_out, accumulate ? 1 : 0);
+  MOSES_CUDA(cudaGetLastError());
+}
+template void mmd_grad<float>(const float*, const float*, long long, long long, long long, int, float, float*, double*,
+                              double*, double, bool, cudaStream_t);
+template void mmd_grad<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, long long, long long, long long, int,
+                                      float, float*, double*, double*, double, bool, cudaStream_t);
+
 // sharded top-k: the k local winners (score, global index); slots past k_valid padded (-inf, -1)
 __global__ void topk_winners_kernel(const float* __restrict__ s, const long long* __restrict__ idx, long long k_valid,
                                     long long k, long long row0, float* __restrict__ out_s, long long* __restrict__ out_i) {
@@ -1732,10 +1826,11 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
 
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo) {
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo, const float* extra,
+                   float extra_scale) {
   if (R <= 0) return;
   if constexpr (sizeof(T) == 2) {
-    if (dz_lo == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
+    if (dz_lo == nullptr && extra == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
         ((reinterpret_cast<uintptr_t>(H) | reinterpret_cast<uintptr_t>(dz)) & 15) == 0) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(grid_for(R * (W / 8), 256));
@@ -1752,7 +1847,8 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
       return;
     }
   }
-  head_backward_kernel<T><<<grid_for(R * W, 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz, ldz, dz_lo);
+  head_backward_kernel<T><<<grid_for(R * W, 256), 256, 0, st>>>(coefA, coefB, wh, u, H, ldh, R, W, dz, ldz, dz_lo,
+                                                                 extra, extra_scale);
   MOSES_CUDA(cudaGetLastError());
 }
 
@@ -2022,7 +2118,7 @@ void synth_labels(unsigned long long seed, long long row0, long long n, float* d
   template void set_ones_column<T>(T*, long long, int, long long, cudaStream_t);                                  \
   template void unpack_rows<T>(const T*, long long, int, long long, double*, cudaStream_t, const T*);             \
   template void head_backward<T>(const float*, const float*, const float*, const float*, const T*, long long,     \
-                                 long long, int, T*, long long, cudaStream_t, T*);                                \
+                                 long long, int, T*, long long, cudaStream_t, T*, const float*, float);          \
   template void column_dot<T>(const float*, const T*, long long, long long, int, float*, float*, cudaStream_t,     \
                               const float*, const T*);                                                            \
   template void adversary_step<T>(const float*, int, long long, const T*, long long, long long, long long, int,   \

@@ -86,6 +86,12 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
 void rank_pairs_rows(const float* s, const float* y, long long n, long long r0, long long nr, const RankWs& ws,
                      cudaStream_t st);
 void rank_local_totals(const RankWs& ws, long long nr, double* out, cudaStream_t st);
+// MMD^2 (biased, Gaussian kernel) between rows [0, m) and [m, R) of H (+ H_lo for split operands) and its
+// gradient G (R x W fp32, row-major) w.r.t. every row; value_out[0] = scale * MMD^2 (or += when
+// accumulate). vpart: R doubles of workspace.
+template <typename T>
+void mmd_grad(const T* H, const T* H_lo, long long ld, long long R, long long m, int W, float sigma, float* G,
+              double* vpart, double* value_out, double scale, bool accumulate, cudaStream_t st);
 // sharded top-k: winners' (score, idx + row0) from device indices; slots [k_valid, k) = (-inf, -1)
 void topk_winners(const float* s, const long long* idx, long long k_valid, long long k, long long row0, float* out_s,
                   long long* out_i, cudaStream_t st);
@@ -97,7 +103,8 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
 // dZ_last[r][j] = (coefA[r]*wh[j] + coefB[r]*u[j]) * [H[r][j] > 0]
 template <typename T>
 void head_backward(const float* coefA, const float* coefB, const float* wh, const float* u, const T* H, long long ldh,
-                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo = nullptr);
+                   long long R, int W, T* dz, long long ldz, cudaStream_t st, T* dz_lo = nullptr,
+                   const float* extra = nullptr, float extra_scale = 0.f);
 // g[j] = sum_r coef[r] * H[r][j] (j < W), g[W] = sum_r coef[r]   (deterministic column reduction)
 template <typename T>
 void column_dot(const float* coef, const T* H, long long ldh, long long R, int W, float* g, float* ws, cudaStream_t st,

@@ -127,6 +127,8 @@ def lib():
         "moses_segment_sum_device": (C.c_int, [vp, i32, i64, i32, vp, i64, vp]),
         "moses_mmd2": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp]),
         "moses_mmd2_device": (C.c_int, [vp, i64, vp, i64, i32, i64, dbl, vp]),
+        "moses_gradients_mmd": (C.c_int, [vp, vp, vp, i64, i32, vp, i64, dbl, dbl, vp]),
+        "moses_mmd2_grad": (C.c_int, [vp, i64, vp, i64, i32, dbl, vp, vp, vp]),
         "moses_encode_configs_device": (C.c_int, [vp, vp, vp, vp, i32, C.c_uint64, i64, i32, vp, i64, i32, vp, vp]),
         "moses_measure_configs_device": (C.c_int, [vp, i32, C.c_char_p, C.c_char_p, vp, vp, vp, vp, i32, C.c_uint64,
                                                    C.c_uint64, i64, vp, vp, vp, vp, vp]),
@@ -680,6 +682,32 @@ def mmd2(xs, xt, sigma: float) -> float:
     out = C.c_double()
     _ck(lib().moses_mmd2(_p(xs), xs.shape[0], _p(xt), xt.shape[0], xs.shape[1], sigma, C.byref(out)))
     return out.value
+
+
+def mmd2_grad(xs, xt, sigma: float):
+    """MMD^2 and its gradient w.r.t. every source / target row (moses_mmd2_grad)."""
+    xs, xt = _f64(xs), _f64(xt)
+    val = C.c_double()
+    gs = np.zeros_like(xs)
+    gt = np.zeros_like(xt)
+    _ck(lib().moses_mmd2_grad(_p(xs), xs.shape[0], _p(xt), xt.shape[0], xs.shape[1], sigma, C.byref(val), _p(gs),
+                              _p(gt)))
+    return val.value, gs, gt
+
+
+def gradients_mmd(model, batch: RankingBatch, source_features, beta: float, sigma: float, want_loss=False):
+    """gradients() with beta * MMD^2(H_source, H_batch) as the domain term (moses_gradients_mmd)."""
+    x, y, src = _f64(batch.features), _f64(batch.labels), _f64(source_features)
+    dm, tmp = _as_device(model, rows=x.shape[0] + src.shape[0])
+    loss = C.c_double()
+    try:
+        _ck(lib().moses_gradients_mmd(dm.h, _p(x), _p(y), x.shape[0], x.shape[1], _p(src), src.shape[0], beta, sigma,
+                                      C.byref(loss)))
+        g = dm.gradients()
+    finally:
+        if tmp:
+            dm.close()
+    return (g, loss.value) if want_loss else g
 
 
 def adam_update(model: DeviceModel, lr, b1=0.9, b2=0.999, eps=1e-8, step=1, mask: Optional[ParamMask] = None):

@@ -157,6 +157,26 @@ def bench_finetune(ml, L, peaks, reps=20):
                          "path": "moses_gradients(adv, beta=0.01) + moses_adversarial_step + moses_lottery_step "
                                  "(ratio 0.5), host float64 buffers, wall clock"}
 
+    src = np.ascontiguousarray(rng.random((256, DIMS[0])))
+
+    def mmd_step():  # cfg3 with the MMD^2 domain loss in the discriminator's slot
+        ml._ck(L.moses_gradients_mmd(dm.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], src.ctypes.data, 256, 0.01,
+                                     float(np.sqrt(DIMS[-2] / 6.0)), C.byref(loss)))
+        ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
+
+    for _ in range(3):
+        mmd_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        mmd_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    out["moses_step_mmd"] = {"ms": dt * 1e3, "samples_per_s": BATCH / dt, "source_rows": 256,
+                             "path": "moses_gradients_mmd (beta 0.01: rank loss + beta * MMD^2 of the last hidden "
+                                     "layer, gradient through every row) + moses_lottery_step (ratio 0.5), host "
+                                     "float64 buffers, split-bf16 handle, wall clock"}
+
     def fused_step():
         ml._ck(L.moses_moses_step(dm.h, adv.h, xt.ctypes.data, yt.ctypes.data, BATCH, DIMS[0], 0.01, 2, 0.5, 0, 1e-3,
                                   1e-2, C.byref(loss), C.byref(dl), C.byref(pop)))
