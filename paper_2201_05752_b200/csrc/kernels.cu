@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(256) head_backward_bf16x8_kernel(const float* 
                                                                    const float* __restrict__ u,
                                                                    const __nv_bfloat16* __restrict__ H, long long ldh,
                                                                    long long R, int W, __nv_bfloat16* __restrict__ dz,
-                                                                   long long ldz) {
+                                                                   long long ldz, __nv_bfloat16* __restrict__ dz_lo) {
   ptx::pdl_launch_dependents();
   ptx::pdl_wait();  // programmatic launch behind the ranking step: coefA is its output
   const int groups = W / 8;
@@ -910,15 +910,19 @@ __global__ void __launch_bounds__(256) head_backward_bf16x8_kernel(const float* 
     const float a = coefA[r];
     const float b = u != nullptr ? coefB[r] : 0.f;
     const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
-    uint4 out;
+    uint4 out, outl;
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
+    __nv_bfloat16* ol = reinterpret_cast<__nv_bfloat16*>(&outl);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       float v = a * __ldg(wh + j0 + k);
       if (u != nullptr) v += b * __ldg(u + j0 + k);
-      ob[k] = __float2bfloat16_rn(__bfloat162float(hb[k]) > 0.f ? v : 0.f);
+      v = __bfloat162float(hb[k]) > 0.f ? v : 0.f;
+      ob[k] = __float2bfloat16_rn(v);
+      ol[k] = __float2bfloat16_rn(v - __bfloat162float(ob[k]));  // split bf16: lo = rn(v - hi)
     }
     *reinterpret_cast<uint4*>(dz + r * ldz + j0) = out;
+    if (dz_lo != nullptr) *reinterpret_cast<uint4*>(dz_lo + r * ldz + j0) = outl;
   }
 }
 
@@ -1830,8 +1834,9 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
                    float extra_scale) {
   if (R <= 0) return;
   if constexpr (sizeof(T) == 2) {
-    if (dz_lo == nullptr && extra == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
-        ((reinterpret_cast<uintptr_t>(H) | reinterpret_cast<uintptr_t>(dz)) & 15) == 0) {
+    if (extra == nullptr && W % 8 == 0 && ldh % 8 == 0 && ldz % 8 == 0 &&
+        ((reinterpret_cast<uintptr_t>(H) | reinterpret_cast<uintptr_t>(dz) | reinterpret_cast<uintptr_t>(dz_lo)) & 15) ==
+            0) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(grid_for(R * (W / 8), 256));
       cfg.blockDim = dim3(256);
@@ -1843,7 +1848,8 @@ void head_backward(const float* coefA, const float* coefB, const float* wh, cons
       cfg.numAttrs = 1;
       MOSES_CUDA(cudaLaunchKernelEx(&cfg, head_backward_bf16x8_kernel, coefA, coefB, wh, u,
                                     reinterpret_cast<const __nv_bfloat16*>(H), ldh, R, W,
-                                    reinterpret_cast<__nv_bfloat16*>(dz), ldz));
+                                    reinterpret_cast<__nv_bfloat16*>(dz), ldz,
+                                    reinterpret_cast<__nv_bfloat16*>(dz_lo)));
       return;
     }
   }

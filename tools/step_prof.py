@@ -1,5 +1,6 @@
 """Kernel timeline (torch profiler / CUPTI) of the bench training step (pooled CUDA graph),
 with and without the 256 MiB L2 flush between steps."""
+import os
 import sys
 
 import numpy as np
@@ -17,12 +18,14 @@ off = off[: nb * B.BATCH + 1]
 n_rows = int(off[-1])
 rows_pad = int((np.diff(off[::B.BATCH]).max() + 127) // 128 * 128)
 params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
-dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=rows_pad)
+PREC = getattr(ml, "PREC_" + os.environ.get("PREC", "BF16X3"))
+dm = ml.DeviceModel(params, PREC, max_rows=rows_pad)
 ld = dm.packed_ld
-X = torch.empty((n_rows, ld), dtype=torch.bfloat16, device="cuda")
+DT = ml.input_dtype(PREC)
+X = torch.empty((n_rows, ld), dtype=torch.bfloat16 if DT == ml.DTYPE_BF16 else torch.float32, device="cuda")
 Y = torch.empty(nb * B.BATCH, dtype=torch.float32, device="cuda")
 OFF = torch.from_numpy(off).cuda()
-assert L.moses_synth_features_device(B.SEED_DATA, 0, n_rows, B.DIMS[0], ml.DTYPE_BF16, X.data_ptr(), ld) == 0
+assert L.moses_synth_features_device(B.SEED_DATA, 0, n_rows, B.DIMS[0], DT, X.data_ptr(), ld) == 0
 assert L.moses_synth_labels_device(B.SEED_DATA, 0, nb * B.BATCH, Y.data_ptr()) == 0
 torch.cuda.synchronize()
 L.moses_set_async(1)
@@ -32,7 +35,7 @@ flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 for _ in range(20):
     ml._ck(L.moses_train_graph_launch(dm.h, 1))
 torch.cuda.synchronize()
-for do_flush in (True, False):
+for do_flush in (False,):
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for k in range(4):
             if do_flush:
