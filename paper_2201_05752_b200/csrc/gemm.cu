@@ -355,13 +355,13 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
   a.K = c.K;
   int tiles = 0;
   for (int l = 0; l < c.n; ++l) {
-    maps.a[l] = make_map(c.a[l], 2, c.M[l], c.K, c.lda[l], 64, 64);
-    maps.b[l] = make_map(c.b[l], 2, c.N[l], c.K, c.ldb[l], 64, 64);
+    maps.a[l] = make_map(c.a[l], 2, c.M[l], c.K, c.lda[l], 64, Cfg::BK);
+    maps.b[l] = make_map(c.b[l], 2, c.N[l], c.K, c.ldb[l], 64, Cfg::BK);
     if constexpr (SPLIT) {
       if (!c.a_lo[l] || !c.b_lo[l] || (UPDATE && !c.shadow_lo[l]))
         fail(MOSES_ERR_INVALID_ARG, "split grouped wgrad needs the lo planes");
-      maps.a_lo[l] = make_map(c.a_lo[l], 2, c.M[l], c.K, c.lda[l], 64, 64);
-      maps.b_lo[l] = make_map(c.b_lo[l], 2, c.N[l], c.K, c.ldb[l], 64, 64);
+      maps.a_lo[l] = make_map(c.a_lo[l], 2, c.M[l], c.K, c.lda[l], 64, Cfg::BK);
+      maps.b_lo[l] = make_map(c.b_lo[l], 2, c.N[l], c.K, c.ldb[l], 64, Cfg::BK);
       a.shadow_lo[l] = static_cast<__nv_bfloat16*>(c.shadow_lo[l]);
     }
     a.tile_begin[l] = tiles;
@@ -535,10 +535,11 @@ void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
 }
 template <bool FWD>
 void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
-  auto kern = mlp_chain_split_kernel<FWD>;
+  auto kern = mlp_chain_split_stream_kernel<FWD>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ChainSplitCfg::kSmemBytes));
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ChainSplitStreamCfg::kSmemBytes));
   });
   if (c.in_lo == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain needs the input lo plane");
   ChainSplitMaps maps;
@@ -547,7 +548,7 @@ void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
   a.n_layers = c.n_layers;
   maps.in = make_map(c.in, 2, c.K[0], c.M, c.ld_in, 64, 128);
   maps.in_lo = make_map(c.in_lo, 2, c.K[0], c.M, c.ld_in, 64, 128);
-  constexpr int W = ChainSplitCfg::kWidth;
+  constexpr int W = ChainSplitStreamCfg::kWidth;
   for (int l = 0; l < c.n_layers; ++l) {
     a.K[l] = c.K[l];
     a.bias[l] = c.bias[l];
@@ -570,10 +571,11 @@ void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
   a.head_part = c.head_part;
   a.head_part2 = c.head_part2;
   a.head_ld = c.head_ld;
+  a.trace = c.trace ? c.trace : g_chain_trace;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(ChainSplitCfg::kCluster * ceil_div(c.M, ChainSplitCfg::BM));
+  cfg.gridDim = dim3(ChainSplitStreamCfg::kCluster * ceil_div(c.M, ChainSplitStreamCfg::BM));
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = ChainSplitCfg::kSmemBytes;
+  cfg.dynamicSmemBytes = ChainSplitStreamCfg::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -47,21 +47,24 @@ struct GroupArgs {
   double* loss_copy;       // optional: *loss_copy = *loss_src once (per-step loss mailbox)
 };
 
+// BK = 128 K rows per stage: MN-major boxes of {64, 128} = 16 KB. The per-SM TMA ingest rate grows
+// with the box size (tools/tma_bench.cu, profiles/r2/tma_ingest_bench.json: 8 KB boxes ~22-29 B/clk,
+// 16 KB ~33-52, 32 KB ~66-88), while the ring depth does not matter.
 struct GroupCfg {
-  static constexpr int BM = 128, BN = 64, BK = 64;
-  static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
+  static constexpr int BM = 128, BN = 64, BK = 128;
+  static constexpr int kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = 9;
+  static constexpr int kStages = 4;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 // split bf16 (MOSES_PREC_BF16X3): [A_hi | B_hi | A_lo | B_lo] per stage; TMEM accumulators promoted
 // into fp32 registers every kPromoteKb k-blocks
 struct GroupSplitCfg {
-  static constexpr int BM = 128, BN = 64, BK = 64;
-  static constexpr int kABytes = BM * 128, kBBytes = BN * 128;
+  static constexpr int BM = 128, BN = 64, BK = 128;
+  static constexpr int kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = 2 * (kABytes + kBBytes);
-  static constexpr int kStages = 4;
-  static constexpr int kPromoteKb = 2;            // 128 K elements (384 products) per TMEM chunk
+  static constexpr int kStages = 2;
+  static constexpr int kPromoteKb = 1;            // 128 K elements (384 products) per TMEM chunk
   static constexpr uint32_t kTmemCols = 2 * BN;   // double-buffered accumulator
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };

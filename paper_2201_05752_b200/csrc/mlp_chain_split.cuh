@@ -5,18 +5,12 @@
 // the product). Predictions, losses and gradients then sit ~1e-5 from the fp64 reference instead
 // of the ~5e-3 of single bf16 operands (tools/precision_probe.py), at 3x the MMA work of bf16.
 //
-// Same decomposition as the bf16 chain: a 4-CTA cluster owns a 128-row block for all layers, CTA q
-// computes output columns [128q, 128q+128), the layer's 128 x 512 hi activation tile stays in
-// shared memory (exchanged through a TMA store + L2 multicast) — but the lo tile (another 128 KB)
-// does not fit next to it. It streams from L2 instead, one 64-column K-block per pipeline stage
-// together with that K-block's W_hi and W_lo slices (3 x 16 KB per stage, 2 stages):
-//
-//   stage s: [ W_hi(kb) 16 KB | W_lo(kb) 16 KB | A_lo(kb) 16 KB ]   one mbarrier, 48 KB expected
-//
-// The epilogue writes its lo slice straight to global memory; once all four CTAs' slices are there
-// (fence.proxy.async + a remote arrive on every CTA's `lo_ready` mbarrier, count 4), the producer
-// issues the next layer's A_lo loads. W loads of the next layer's first stages are still prefetched
-// during the exchange (the stage's mbarrier expects all 48 KB, the A_lo part lands later).
+// Decomposition as the bf16 chain: a 4-CTA cluster owns a 128-row block for all layers, CTA q
+// computes output columns [128q, 128q+128). Two operand planes do not fit a resident 128 x 512
+// activation tile next to a weight ring (2 x 128 KB), and a tile is read once per layer anyway, so
+// every operand K-block streams (see the streamed form below). Measured and dropped: a resident hi
+// tile + streamed lo plane (same step time, less in flight); 64-row blocks on all 148 SMs (slower:
+// 2x the weight traffic, M = 64 MMAs, starved side-stream kernels).
 #pragma once
 #include "mlp_chain.cuh"
 
@@ -29,17 +23,6 @@ struct ChainSplitMaps {
   CUtensorMap out[kChainMaxLayers];      // hi outputs: TMA store + multicast reload, box {64, 128}
   CUtensorMap out_lo[kChainMaxLayers];   // lo outputs: the next layer's A_lo stream, box {64, 128}
 };
-
-struct ChainSplitCfg {
-  static constexpr int BM = 128, BN = 128, BK = 64, kWidth = 512, kCluster = 4;
-  static constexpr int kTile = BM * 128;                    // one 64-col K-block of a 128-row bf16 tile
-  static constexpr int kActBytes = (kWidth / BK) * kTile;   // 128 KB hi tile
-  static constexpr int kStages = 2;
-  static constexpr int kWBytes = BN * 128;                  // one K-block of one weight plane (16 KB)
-  static constexpr int kStageBytes = 2 * kWBytes + kTile;   // W_hi | W_lo | A_lo
-  static constexpr int kSmemBytes = kActBytes + kStages * kStageBytes + 1024 + 256;
-};
-static_assert(ChainSplitCfg::kSmemBytes <= 232448, "split chain exceeds the 227 KB shared-memory limit");
 
 namespace chain_detail {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
@@ -56,26 +39,43 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 }  // namespace chain_detail
 
+// ---------------------------------------------------------------------------------------------
+// Streamed form: no resident activation tile. Every operand K-block streams from L2 through a
+// 3-stage ring of [W_hi | W_lo | A_hi | A_lo] (4 x 16 KB), twice the bytes in flight of the
+// resident form (which spends 128 KB of shared memory on a tile each K-block of is read once per
+// layer). The epilogue writes both planes of its 128 x 128 output slice to global memory; the four
+// CTAs of the cluster signal each other through a remote arrive on every CTA's `ready` mbarrier
+// (count 4, one phase per layer), after which the producers stream the next layer's A blocks. The
+// next layer's first weight blocks are prefetched while the epilogue runs.
+struct ChainSplitStreamCfg {
+  static constexpr int BM = 128, BN = 128, BK = 64, kWidth = 512, kCluster = 4;
+  static constexpr int kTile = BM * 128;                    // one 64-col K-block of a 128-row bf16 plane
+  static constexpr int kStages = 3;
+  static constexpr int kWBytes = BN * 128;                  // one K-block of one weight plane (16 KB)
+  static constexpr int kStageBytes = 2 * kWBytes + 2 * kTile;  // W_hi | W_lo | A_hi | A_lo
+  static constexpr int kParamFloats = kChainMaxLayers * BN + 2 * BN;  // bias slices + head_w / head_u slices
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + kParamFloats * 4;
+};
+static_assert(ChainSplitStreamCfg::kSmemBytes <= 232448, "streamed split chain exceeds shared memory");
+
 template <bool FWD>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
-    mlp_chain_split_kernel(const __grid_constant__ ChainSplitMaps maps, const __grid_constant__ ChainArgs args) {
+    mlp_chain_split_stream_kernel(const __grid_constant__ ChainSplitMaps maps, const __grid_constant__ ChainArgs args) {
   using namespace chain_detail;
-  using C = ChainSplitCfg;
+  using C = ChainSplitStreamCfg;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, S = C::kStages;
   constexpr uint32_t kIdesc = ptx::umma_idesc(1 /*BF16*/, false, FWD /*B MN-major*/, BM, BN);
-  constexpr uint16_t kAll = 0xF;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sAct = smem;
-  uint8_t* sRing = smem + C::kActBytes;
+  uint8_t* sRing = smem;
   uint64_t* wfull = reinterpret_cast<uint64_t*>(sRing + S * C::kStageBytes);
   uint64_t* wempty = wfull + S;
-  uint64_t* act_full = wempty + S;
-  uint64_t* acc_full = act_full + 1;
-  uint64_t* slice_free = acc_full + 1;  // this CTA's outgoing TMA store finished reading its slice
-  uint64_t* lo_ready = slice_free + 1;  // all four CTAs' lo slices of the layer are in global memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lo_ready + 1);
+  uint64_t* acc_full = wempty + S;
+  uint64_t* ready = acc_full + 1;  // all four CTAs' output slices of the layer are in global memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + 1);
+  float* s_bias = reinterpret_cast<float*>(sRing + S * C::kStageBytes + 256);  // [layer][BN] (FWD)
+  float* s_head = s_bias + kChainMaxLayers * BN;                                // [2][BN] head_w, head_u
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const uint32_t q = ptx::cluster_ctarank();
@@ -87,16 +87,25 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       ptx::mbar_init(&wfull[s], 1);
       ptx::mbar_init(&wempty[s], 1);
     }
-    ptx::mbar_init(act_full, 1);
     ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(slice_free, 1);
-    ptx::mbar_init(lo_ready, C::kCluster);
+    ptx::mbar_init(ready, C::kCluster);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc<BN>(tmem_slot);
-  ptx::pdl_wait();  // every global read below may depend on the previous kernel
+  ptx::pdl_wait();
+  if (threadIdx.x == 0) CHAIN_TRACE(6, 0);
+  if constexpr (FWD) {  // the slices of every layer's bias and of the head vectors, once
+    for (int i = threadIdx.x; i < L * BN; i += blockDim.x) {
+      const int l = i / BN, j = i - l * BN;
+      s_bias[i] = args.bias[l] ? __ldg(args.bias[l] + n0 + j) : 0.f;
+    }
+    for (int j = threadIdx.x; j < BN; j += blockDim.x) {
+      s_head[j] = args.head_w ? __ldg(args.head_w + n0 + j) : 0.f;
+      s_head[BN + j] = args.head_u ? __ldg(args.head_u + n0 + j) : 0.f;
+    }
+  }
   ptx::tc_fence_before();
-  ptx::cluster_sync();  // barrier inits + TMEM address visible cluster-wide before any multicast / remote arrive
+  ptx::cluster_sync();  // barrier inits visible cluster-wide before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -104,9 +113,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
     // ------------------------------------------------------------ TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    int pend_n = 0;                 // K-blocks of the current layer whose W was issued before its A_lo
+    int pend_n = 0;  // K-blocks of the current layer whose weights were issued before its A blocks
     int pend_stage[S];
-    // W_hi + W_lo of (layer l, K-block kb) into the next stage; the stage also expects its A_lo block
     auto load_w = [&](int l, int kb) -> int {
       ptx::mbar_wait(&wempty[stage], phase ^ 1);
       uint8_t* dst = sRing + stage * C::kStageBytes;
@@ -124,87 +132,53 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       if (++stage == S) { stage = 0; phase ^= 1; }
       return s;
     };
-    auto load_alo = [&](int l, int kb, int s) {
-      const CUtensorMap* src = l == 0 ? &maps.in_lo : &maps.out_lo[l - 1];
-      ptx::tma_load_2d(sRing + s * C::kStageBytes + 2 * C::kWBytes, src, &wfull[s], kb * BK, m0);
+    auto load_a = [&](int l, int kb, int s) {
+      const CUtensorMap* hi = l == 0 ? &maps.in : &maps.out[l - 1];
+      const CUtensorMap* lo = l == 0 ? &maps.in_lo : &maps.out_lo[l - 1];
+      uint8_t* dst = sRing + s * C::kStageBytes + 2 * C::kWBytes;
+      ptx::tma_load_2d(dst, hi, &wfull[s], kb * BK, m0);
+      ptx::tma_load_2d(dst + C::kTile, lo, &wfull[s], kb * BK, m0);
     };
     if (lane == 0) {
       ptx::tma_prefetch_desc(&maps.in);
       ptx::tma_prefetch_desc(&maps.in_lo);
-      const int nkb0 = (args.K[0] + BK - 1) / BK;
-      ptx::mbar_arrive_expect_tx(act_full, nkb0 * C::kTile);
-      for (int kb = int(q); kb < nkb0; kb += C::kCluster)
-        ptx::tma_load_2d_mc(sAct + kb * C::kTile, &maps.in, act_full, kb * BK, m0, kAll);
     }
     for (int l = 0; l < L; ++l) {
       const int nkb = (args.K[l] + BK - 1) / BK;
       if (lane == 0) {
-        if (l > 0) {
-          // every CTA's lo slice of layer l-1 is in global memory: stream the A_lo blocks
-          mbar_wait_cluster(lo_ready, uint32_t(l - 1) & 1u);
+        if (l > 0) {  // every CTA of the cluster has written its slice of layer l-1
+          mbar_wait_cluster(ready, uint32_t(l - 1) & 1u);
           fence_proxy_async_global();
+          CHAIN_TRACE(4, l);
         }
-        for (int i = 0; i < pend_n; ++i) load_alo(l, i, pend_stage[i]);
-        for (int kb = pend_n; kb < nkb; ++kb) load_alo(l, kb, load_w(l, kb));
-      }
-      pend_n = 0;
-      if (l + 1 < L) {
-        __syncwarp();
-        cl_arrive();
-        if (lane == 0) {  // prefetch the next layer's first weight blocks while the exchange runs
+        for (int i = 0; i < pend_n; ++i) load_a(l, i, pend_stage[i]);
+        for (int kb = pend_n; kb < nkb; ++kb) load_a(l, kb, load_w(l, kb));
+        pend_n = 0;
+        if (l + 1 < L) {  // the next layer's first weight blocks, while this layer's MMAs / epilogue run
           const int nn = (args.K[l + 1] + BK - 1) / BK;
           pend_n = nn < S ? nn : S;
           for (int kb = 0; kb < pend_n; ++kb) pend_stage[kb] = load_w(l + 1, kb);
         }
-        pend_n = __shfl_sync(0xffffffffu, pend_n, 0);
-#pragma unroll
-        for (int i = 0; i < S; ++i) pend_stage[i] = __shfl_sync(0xffffffffu, pend_stage[i], 0);
-        bar_sync(1, 160);  // this CTA's hi slice is in its own activation tile and fenced
-        if (lane == 0) {
-          tma_store_2d(&maps.out[l], sAct + (2 * q) * C::kTile, n0, m0);
-          tma_store_2d(&maps.out[l], sAct + (2 * q + 1) * C::kTile, n0 + 64, m0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // slice is in global (L2)
-          ptx::mbar_arrive(slice_free);
-        }
-        __syncwarp();
-        cl_wait();  // every CTA's MMAs of layer l are done: activation tiles are free
-        if (lane == 0) {
-          constexpr uint32_t kSlice = 2 * C::kTile;
-          const uint16_t peers = uint16_t(kAll & ~(1u << q));
-          ptx::mbar_arrive_expect_tx(act_full, (C::kCluster - 1) * kSlice);  // the 3 peer slices
-          ptx::tma_load_2d_mc(sAct + (2 * q) * C::kTile, &maps.out[l], act_full, n0, m0, peers);
-          ptx::tma_load_2d_mc(sAct + (2 * q + 1) * C::kTile, &maps.out[l], act_full, n0 + 64, m0, peers);
-        }
-        __syncwarp();
-      } else if (args.out[l] != nullptr) {  // last layer: coalesced TMA store of the hi output slice
-        bar_sync(1, 160);
-        if (lane == 0) {
-          tma_store_2d(&maps.out[l], sAct + (2 * q) * C::kTile, n0, m0);
-          tma_store_2d(&maps.out[l], sAct + (2 * q + 1) * C::kTile, n0 + 64, m0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        __syncwarp();
       }
     }
+    __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     int stage = 0;
     uint32_t phase = 0;
     for (int l = 0; l < L; ++l) {
       if (lane == 0) {
-        ptx::mbar_wait(act_full, uint32_t(l) & 1u);
-        ptx::tc_fence_after();
         const int nkb = (args.K[l] + BK - 1) / BK;
-        const uint32_t a0 = ptx::smem_u32(sAct), r0 = ptx::smem_u32(sRing);
+        const uint32_t r0 = ptx::smem_u32(sRing);
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(&wfull[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t sb = r0 + stage * C::kStageBytes, sbl = sb + C::kWBytes, sal = sb + 2 * C::kWBytes;
+          if (kb == 0) CHAIN_TRACE(0, l);
+          const uint32_t sb = r0 + stage * C::kStageBytes, sbl = sb + C::kWBytes;
+          const uint32_t sah = sb + 2 * C::kWBytes, sal = sah + C::kTile;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ah = ptx::sw128_desc(a0 + kb * C::kTile + kk * 32, 16, 1024);
+            const uint64_t ah = ptx::sw128_desc(sah + kk * 32, 16, 1024);
             const uint64_t al = ptx::sw128_desc(sal + kk * 32, 16, 1024);
             const uint64_t bh = FWD ? ptx::sw128_desc(sb + kk * 2048, BK * 128, 1024, 2)
                                     : ptx::sw128_desc(sb + kk * 32, 16, 1024);
@@ -218,12 +192,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit(acc_full);
+        CHAIN_TRACE(1, l);
       }
       __syncwarp();
-      if (l + 1 < L) {
-        cl_arrive();
-        cl_wait();
-      }
     }
   } else {
     // ------------------------------------------------------------ epilogue warps 0-3
@@ -245,31 +216,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       }
       ptx::mbar_wait(acc_full, uint32_t(l) & 1u);
       ptx::tc_fence_after();
-      if (!last) cl_arrive();
+      if (threadIdx.x == 0) CHAIN_TRACE(2, l);
       const bool store = !last || args.out[l] != nullptr;
-      if (store && l >= 1) ptx::mbar_wait(slice_free, uint32_t(l - 1) & 1u);
-      __nv_bfloat16* lo_row = (store && row_ok) ? args.out_lo[l] + (long long)m * args.ldo[l] + n0 : nullptr;
+      // the output slice is staged in the A areas of stages 0 (hi) and 1 (lo) — free while the
+      // epilogue runs: this layer's MMAs are complete and the next layer's A loads wait for `ready` —
+      // in the TMA store boxes' SW128 layout, then leaves in four coalesced bulk stores
+      uint8_t* st_hi = sRing + 2 * C::kWBytes;
+      uint8_t* st_lo = sRing + C::kStageBytes + 2 * C::kWBytes;
       float hp = 0.f, hp2 = 0.f;
-#pragma unroll 1
+      uint32_t rr[2][32];  // two 32-column chunks in flight: the TMEM load of c+1 overlaps chunk c
+      ptx::tmem_ld_32x32b_x32(t_row, rr[0]);
+#pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
         ptx::tmem_ld_wait();
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[c & 1][j]);
+        if (c + 1 < BN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rr[(c + 1) & 1]);
         if constexpr (FWD) {
-          const float* bias = args.bias[l] ? args.bias[l] + n0 + c * 32 : nullptr;
+          const float* sb = s_bias + l * BN + c * 32;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + (bias ? __ldg(bias + j) : 0.f), 0.f);
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + sb[j], 0.f);
           if (last) {
             if (args.head_w != nullptr) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) hp = fmaf(v[j], __ldg(args.head_w + n0 + c * 32 + j), hp);
+              for (int j = 0; j < 32; ++j) hp = fmaf(v[j], s_head[c * 32 + j], hp);
             }
             if (args.head_u != nullptr) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], __ldg(args.head_u + n0 + c * 32 + j), hp2);
+              for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], s_head[BN + c * 32 + j], hp2);
             }
           }
         } else {
@@ -297,10 +272,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
               hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
-            const int col = n0 + c * 32 + j;
-            const int chunk = ((col & 63) >> 3) ^ (row & 7);
-            *reinterpret_cast<uint4*>(sAct + (col >> 6) * C::kTile + row * 128 + chunk * 16) = ph;
-            if (lo_row != nullptr) *reinterpret_cast<uint4*>(lo_row + c * 32 + j) = pl;
+            const int col = c * 32 + j;  // within the slice
+            const int off = (col >> 6) * C::kTile + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
+            *reinterpret_cast<uint4*>(st_hi + off) = ph;
+            *reinterpret_cast<uint4*>(st_lo + off) = pl;
           }
         }
       }
@@ -309,29 +284,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
         if (args.head_part2 != nullptr) args.head_part2[(long long)q * args.head_ld + m] = hp2;
       }
       if (store) {
+        // both planes of the slice to global memory (bulk stores complete before the signal), then
+        // one release arrive on every CTA of the cluster: their producers stream the next layer's A
         ptx::tc_fence_before();
-        fence_proxy_async_smem();  // generic st.shared -> async-proxy readers (TMA store, tensor core)
-        bar_arrive(1, 160);
-      }
-      if (!last) {
-        // lo slice -> every CTA's lo_ready: generic global stores made visible to the async proxy
-        // (the peers' TMA loads), then one release arrive per CTA of the cluster
-        fence_proxy_async_global();
+        fence_proxy_async_smem();
         bar_sync(2, 128);
         if (threadIdx.x == 0) {
-          const uint32_t local = ptx::smem_u32(lo_ready);
+          tma_store_2d(&maps.out[l], st_hi, n0, m0);
+          tma_store_2d(&maps.out[l], st_hi + C::kTile, n0 + 64, m0);
+          tma_store_2d(&maps.out_lo[l], st_lo, n0, m0);
+          tma_store_2d(&maps.out_lo[l], st_lo + C::kTile, n0 + 64, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          CHAIN_TRACE(3, l);
+          if (!last) {
+            const uint32_t local = ptx::smem_u32(ready);
 #pragma unroll
-          for (uint32_t p = 0; p < uint32_t(C::kCluster); ++p) mbar_arrive_cluster(mapa(local, p));
+            for (uint32_t p = 0; p < uint32_t(C::kCluster); ++p) mbar_arrive_cluster(mapa(local, p));
+          }
         }
-        cl_wait();
+        bar_sync(2, 128);  // the staging areas are reusable (next layer's epilogue)
       }
     }
+    if (threadIdx.x == 0) CHAIN_TRACE(7, 0);
     ptx::pdl_launch_dependents();
   }
 
   __syncwarp();
   ptx::tc_fence_before();
-  ptx::cluster_sync();  // no CTA leaves while a multicast / remote arrive into it could still be in flight
+  ptx::cluster_sync();  // no CTA leaves while a remote arrive into it could still be in flight
   if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<BN>(tmem);

@@ -1,5 +1,6 @@
 """Phase timeline of the fused chain kernels (cluster 0), from %globaltimer stamps."""
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -12,15 +13,19 @@ L = ml.lib()
 L.moses_debug_set_chain_trace.argtypes = [C.c_void_p]
 dims = [164, 512, 512, 512, 512, 1]
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 2560
-dm = ml.DeviceModel(ml.init_random(dims, 1, strict=False), ml.PREC_BF16, R)
+PREC = getattr(ml, "PREC_" + os.environ.get("PREC", "BF16X3"))
+DT = ml.input_dtype(PREC)
+dm = ml.DeviceModel(ml.init_random(dims, 1, strict=False), PREC, R)
 ld = dm.packed_ld
-X = torch.zeros((R, ld), dtype=torch.bfloat16, device="cuda")
-X[:, :164] = torch.rand(R, 164, device="cuda").to(torch.bfloat16)
+X = torch.zeros((R, ld), dtype=torch.bfloat16 if DT == ml.DTYPE_BF16 else torch.float32, device="cuda")
+X[:, :164] = torch.rand(R, 164, device="cuda").to(X.dtype)
 X[:, 164] = 1
 Y = torch.rand(R, device="cuda") + 0.1
 S = torch.empty(R, device="cuda")
 tr = torch.zeros(4 * 8 * 8, dtype=torch.int64, device="cuda")
 EV = ["mma_start", "mma_issued", "acc_seen", "stores_fenced", "cl_wait_done", "mc_issued", "k_start", "k_end"]
+if os.environ.get("PREC", "BF16X3") == "BF16X3":  # streamed split chain: its own event meanings
+    EV = ["mma_start", "mma_issued", "acc_seen", "slice_written", "ready_seen", "-", "k_start", "k_end"]
 
 
 def show(title):
@@ -40,11 +45,11 @@ def show(title):
 
 
 for _ in range(3):
-    ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, R, S.data_ptr()))
+    ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), DT, ld, R, S.data_ptr()))
 torch.cuda.synchronize()
 tr.zero_()
 L.moses_debug_set_chain_trace(tr.data_ptr())
-ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), ml.DTYPE_BF16, ld, R, S.data_ptr()))
+ml._ck(L.moses_predict_device(dm.h, X.data_ptr(), DT, ld, R, S.data_ptr()))
 torch.cuda.synchronize()
 show("forward chain")
 tr.zero_()
