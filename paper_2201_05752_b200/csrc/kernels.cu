@@ -985,6 +985,82 @@ __global__ void sgd_kernel(float* __restrict__ w, float* __restrict__ v, const f
   }
 }
 
+// Vectorised form of sgd_kernel (same per-element arithmetic): 16-byte lanes for w / v / g, 4-byte mask
+// words, 8-byte bf16 shadow stores; two float4 per thread per iteration in flight. Requires 16-byte
+// aligned w, v, g (4-byte mask, 8-byte shadow); the P % 4 tail runs scalar.
+template <bool MOM, bool MASK, int SHADOW>
+__global__ void __launch_bounds__(256) sgd4_kernel(float* __restrict__ w, float* __restrict__ v,
+                                                   const float* __restrict__ g, const uint8_t* __restrict__ mask,
+                                                   long long P, float lr, float mu, void* __restrict__ shadow,
+                                                   long long lo_off) {
+  ptx::pdl_launch_dependents();
+  const long long n4 = P >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  auto one = [&](float& wi, float& vi, float gi, bool on) {
+    if (!on) return;
+    if (MOM) {
+      vi = __fadd_rn(__fmul_rn(mu, vi), gi);
+      wi = __fsub_rn(wi, __fmul_rn(lr, vi));
+    } else {
+      wi = __fsub_rn(wi, __fmul_rn(lr, gi));
+    }
+  };
+  auto put_shadow4 = [&](long long i4, const float4& x) {
+    if constexpr (SHADOW == 1 || SHADOW == 4) {
+      const __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+      uint2 u;
+      u.x = *reinterpret_cast<const uint32_t*>(&a);
+      u.y = *reinterpret_cast<const uint32_t*>(&b);
+      reinterpret_cast<uint2*>(shadow)[i4] = u;
+      if constexpr (SHADOW == 4) {
+        const __nv_bfloat162 la = __floats2bfloat162_rn(x.x - __low2float(a), x.y - __high2float(a));
+        const __nv_bfloat162 lb = __floats2bfloat162_rn(x.z - __low2float(b), x.w - __high2float(b));
+        uint2 ul;
+        ul.x = *reinterpret_cast<const uint32_t*>(&la);
+        ul.y = *reinterpret_cast<const uint32_t*>(&lb);
+        reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(shadow) + lo_off)[i4] = ul;
+      }
+    }
+    if constexpr (SHADOW == 2)
+      reinterpret_cast<float4*>(shadow)[i4] = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+  };
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < n4; base += 2 * stride) {
+    float4 wv[2], vv[2], gv[2];
+    uchar4 mk[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const long long i4 = base + u * stride;
+      ok[u] = i4 < n4;
+      if (!ok[u]) continue;
+      wv[u] = reinterpret_cast<const float4*>(w)[i4];
+      gv[u] = reinterpret_cast<const float4*>(g)[i4];
+      if (MOM) vv[u] = reinterpret_cast<const float4*>(v)[i4];
+      mk[u] = MASK ? reinterpret_cast<const uchar4*>(mask)[i4] : make_uchar4(1, 1, 1, 1);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      const long long i4 = base + u * stride;
+      float4 x = wv[u], y = MOM ? vv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+      one(x.x, y.x, gv[u].x, mk[u].x != 0);
+      one(x.y, y.y, gv[u].y, mk[u].y != 0);
+      one(x.z, y.z, gv[u].z, mk[u].z != 0);
+      one(x.w, y.w, gv[u].w, mk[u].w != 0);
+      reinterpret_cast<float4*>(w)[i4] = x;
+      if (MOM) reinterpret_cast<float4*>(v)[i4] = y;
+      put_shadow4(i4, x);
+    }
+  }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P; i += stride) {
+    float wi = w[i], vi = MOM ? v[i] : 0.f;
+    one(wi, vi, g[i], !MASK || mask[i]);
+    w[i] = wi;
+    if (MOM) v[i] = vi;
+    store_shadow<SHADOW>(shadow, i, wi, lo_off);
+  }
+}
+
 template <int SHADOW>
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m1, float* __restrict__ m2, const float* __restrict__ g,
                             const uint8_t* __restrict__ mask, long long P, float lr, float b1, float b2, float eps,
@@ -1875,12 +1951,22 @@ size_t column_dot_ws_floats(long long R, int W) { return size_t(R > 0 ? ceil_div
 void sgd_update(float* w, float* v, const float* g, const uint8_t* mask, long long P, float lr, float mu, bool momentum,
                 Shadow sh, cudaStream_t st) {
   const int grid = grid_for(P, 256);
-#define SGD_LAUNCH(M, K, S) sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr, sh.lo_off)
+  // 16-byte lanes when every array allows it (the whole-model buffers do; offset sub-blocks may not)
+  const uintptr_t al16 = reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) |
+                         (momentum ? reinterpret_cast<uintptr_t>(v) : 0);
+  const uintptr_t sh_al = sh.kind == 2 ? 15 : 7;
+  const bool vec = P >= 1024 && (al16 & 15) == 0 && (reinterpret_cast<uintptr_t>(mask) & 3) == 0 &&
+                   (sh.ptr == nullptr || ((reinterpret_cast<uintptr_t>(sh.ptr) & sh_al) == 0 &&
+                                          (sh.kind != 4 || (sh.lo_off & 3) == 0)));
+  const int grid4 = grid_for((P / 4 + 1) / 2, 256, 4);
+#define SGD_LAUNCH(M, K, S)                                                                                   \
+  if (vec) sgd4_kernel<M, K, S><<<grid4, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr, sh.lo_off);           \
+  else sgd_kernel<M, K, S><<<grid, 256, 0, st>>>(w, v, g, mask, P, lr, mu, sh.ptr, sh.lo_off)
 #define SGD_K(M, K)                                            \
-  if (sh.kind == 1) SGD_LAUNCH(M, K, 1);                       \
-  else if (sh.kind == 2) SGD_LAUNCH(M, K, 2);                  \
-  else if (sh.kind == 4) SGD_LAUNCH(M, K, 4);                  \
-  else SGD_LAUNCH(M, K, 0)
+  if (sh.kind == 1) { SGD_LAUNCH(M, K, 1); }                   \
+  else if (sh.kind == 2) { SGD_LAUNCH(M, K, 2); }              \
+  else if (sh.kind == 4) { SGD_LAUNCH(M, K, 4); }              \
+  else { SGD_LAUNCH(M, K, 0); }
   const bool k = mask != nullptr;
   if (momentum) {
     if (k) { SGD_K(true, true); } else { SGD_K(true, false); }
