@@ -383,6 +383,14 @@ MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, c
                                  int64_t n_records, const char* const* task_ids, int32_t n_task_ids,
                                  int32_t batch_size, int32_t epochs, double learning_rate, double momentum,
                                  int32_t threads, double* epoch_mean_loss, int64_t* dropped_singletons);
+/* The job grid across the GPUs of one process: job j runs on its handle's device
+ * (recorded at moses_model_create) over that device's copy of the store, x_of[j] / y_of[j]. */
+MOSES_API int moses_pretrain_jobs_mapped(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                                        const void* const* x_of, int64_t ldx, const float* const* y_of,
+                                        const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                        int32_t n_task_ids, int32_t batch_size, int32_t epochs, double learning_rate,
+                                        double momentum, int32_t threads, double* epoch_mean_loss,
+                                        int64_t* dropped_singletons);
 /* Line-delimited record files (data.cpp:67-126). moses_records_read fails with MOSES_ERR_IO,
  * MOSES_ERR_PARSE (message names "<path>:line N") or MOSES_ERR_MISSING_FIELD. */
 MOSES_API int moses_records_create(moses_records_t* out);

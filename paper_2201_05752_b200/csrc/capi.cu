@@ -3249,12 +3249,12 @@ MOSES_API int moses_pretrain(moses_model_t m, int32_t n_tasks, const char* const
 // concurrency, capped at the job count); every job owns its model handle and therefore its CUDA
 // streams, so the GPU runs the jobs' small, latency-bound steps concurrently. The first failing
 // job's status is returned; the others still run to completion or to their own error.
-MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
-                                 const void* x_base, int64_t ldx, const float* y_base, const int32_t* record_task,
-                                 int64_t n_records, const char* const* task_ids, int32_t n_task_ids,
-                                 int32_t batch_size, int32_t epochs, double lr, double mu, int32_t threads,
-                                 double* epoch_mean_loss, int64_t* dropped_singletons) {
-  return guarded([&] {
+static void pretrain_jobs_impl(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                               const void* const* x_of, int64_t ldx, const float* const* y_of,
+                               const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                               int32_t n_task_ids, int32_t batch_size, int32_t epochs, double lr, double mu,
+                               int32_t threads, double* epoch_mean_loss, int64_t* dropped_singletons) {
+  {
     if (n_jobs < 0 || (n_jobs > 0 && (models == nullptr || seeds == nullptr)))
       fail(MOSES_ERR_INVALID_ARG, "invalid job list");
     if (n_jobs == 0) return;
@@ -3288,7 +3288,7 @@ MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, c
         try {
           // new threads start on device 0: every job runs on its handle's device
           MOSES_CUDA(cudaSetDevice(models[j]->device));
-          pretrain_impl(models[j], x_base, ldx, y_base, record_task, n_records, task_ids, n_task_ids, batch_size,
+          pretrain_impl(models[j], x_of[j], ldx, y_of[j], record_task, n_records, task_ids, n_task_ids, batch_size,
                         seeds[j], epochs, lr, mu, epoch_mean_loss ? epoch_mean_loss + size_t(j) * epochs : nullptr,
                         dropped_singletons ? dropped_singletons + j : nullptr);
         } catch (const Status& e) {
@@ -3316,6 +3316,41 @@ MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, c
       for (auto& t : pool) t.join();
     }
     if (first_job >= 0) fail(first_code, "job " + std::to_string(first_job) + ": " + first_msg);
+  }
+}
+
+MOSES_API int moses_pretrain_jobs(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                                 const void* x_base, int64_t ldx, const float* y_base, const int32_t* record_task,
+                                 int64_t n_records, const char* const* task_ids, int32_t n_task_ids,
+                                 int32_t batch_size, int32_t epochs, double lr, double mu, int32_t threads,
+                                 double* epoch_mean_loss, int64_t* dropped_singletons) {
+  return guarded([&] {
+    const std::vector<const void*> xs(size_t(std::max(n_jobs, 0)), x_base);
+    const std::vector<const float*> ys(size_t(std::max(n_jobs, 0)), y_base);
+    pretrain_jobs_impl(n_jobs, models, seeds, xs.data(), ldx, ys.data(), record_task, n_records, task_ids, n_task_ids,
+                       batch_size, epochs, lr, mu, threads, epoch_mean_loss, dropped_singletons);
+  });
+}
+
+// The job grid across GPUs (tuner.cpp:331-374): job j runs on its handle's device
+// with that device's copy of the store (x_of[j], y_of[j]); handles created round-robin on the GPUs of
+// the process map the (strategy, seed) grid onto all of them.
+MOSES_API int moses_pretrain_jobs_mapped(int32_t n_jobs, const moses_model_t* models, const uint64_t* seeds,
+                                        const void* const* x_of, int64_t ldx, const float* const* y_of,
+                                        const int32_t* record_task, int64_t n_records, const char* const* task_ids,
+                                        int32_t n_task_ids, int32_t batch_size, int32_t epochs, double lr, double mu,
+                                        int32_t threads, double* epoch_mean_loss, int64_t* dropped_singletons) {
+  return guarded([&] {
+    if (n_jobs > 0 && (x_of == nullptr || y_of == nullptr)) fail(MOSES_ERR_INVALID_ARG, "null per-job dataset list");
+    for (int32_t j = 0; j < n_jobs; ++j) {
+      if (models == nullptr || models[j] == nullptr) fail(MOSES_ERR_INVALID_ARG, "null model handle in the job list");
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, x_of[j]) == cudaSuccess && pa.type == cudaMemoryTypeDevice &&
+          pa.device != models[j]->device)
+        fail(MOSES_ERR_INVALID_ARG, "job " + std::to_string(j) + ": dataset and model on different devices");
+    }
+    pretrain_jobs_impl(n_jobs, models, seeds, x_of, ldx, y_of, record_task, n_records, task_ids, n_task_ids,
+                       batch_size, epochs, lr, mu, threads, epoch_mean_loss, dropped_singletons);
   });
 }
 

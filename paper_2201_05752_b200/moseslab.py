@@ -145,6 +145,8 @@ def lib():
         "moses_train_plan_device": (C.c_int, [vp, vp, i64, vp, i64, vp, vp, i64, dbl, dbl, vp]),
         "moses_pretrain_device": (C.c_int, [vp, vp, i64, vp, vp, i64, vp, i32, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_pretrain_jobs": (C.c_int, [i32, vp, vp, vp, i64, vp, vp, i64, vp, i32, i32, i32, dbl, dbl, i32, vp, vp]),
+        "moses_pretrain_jobs_mapped": (C.c_int, [i32, vp, vp, vp, i64, vp, vp, i64, vp, i32, i32, i32, dbl, dbl, i32,
+                                                 vp, vp]),
         "moses_pretrain": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_moses_step": (C.c_int, [vp, vp, vp, vp, i64, i32, dbl, i32, dbl, i32, dbl, dbl, vp, vp, vp]),
         "moses_evolve": (C.c_int, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, dbl, u64, vp, vp, i64, vp]),
@@ -998,6 +1000,30 @@ def pretrain_jobs(models, seeds, x_ptr, ldx: int, y_ptr, record_task, task_ids, 
                                   C.cast(arr, C.c_void_p), len(enc), batch_size, epochs, lr, mu, threads,
                                   _p(losses), _p(dropped)))
     return losses[:len(models), :epochs], dropped[:len(models)]
+
+
+def pretrain_jobs_mapped(models, seeds, x_ptrs, ldx: int, y_ptrs, record_task, task_ids, batch_size: int = 512,
+                         epochs: int = 30, lr: float = 0.001, mu: float = 0.9, threads: int = 0):
+    """pretrain_jobs with job j over its own device's copy of the store (x_ptrs[j], y_ptrs[j]): the
+    (seed) job grid spread over the GPUs the handles were created on."""
+    if len(record_task) and isinstance(record_task[0], str):
+        ids = list(dict.fromkeys(list(task_ids) + list(record_task)))
+        ix = {t: i for i, t in enumerate(ids)}
+        record_task, task_ids = [ix[t] for t in record_task], ids
+    rt = np.ascontiguousarray(record_task, dtype=np.int32)
+    enc = [t.encode() for t in task_ids]
+    arr = (C.c_char_p * max(1, len(enc)))(*enc)
+    n = len(models)
+    hs = (C.c_void_p * max(1, n))(*[m.h.value if hasattr(m.h, "value") else m.h for m in models])
+    xs = (C.c_void_p * max(1, n))(*[int(p.value if hasattr(p, "value") else p) for p in x_ptrs])
+    ys = (C.c_void_p * max(1, n))(*[int(p.value if hasattr(p, "value") else p) for p in y_ptrs])
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    losses = np.zeros((max(n, 1), max(epochs, 1)))
+    dropped = np.zeros(max(n, 1), dtype=np.int64)
+    _ck(lib().moses_pretrain_jobs_mapped(n, C.cast(hs, C.c_void_p), _p(sd), C.cast(xs, C.c_void_p), ldx,
+                                         C.cast(ys, C.c_void_p), _p(rt), len(rt), C.cast(arr, C.c_void_p), len(enc),
+                                         batch_size, epochs, lr, mu, threads, _p(losses), _p(dropped)))
+    return losses[:n, :epochs], dropped[:n]
 
 
 class RecordStore:

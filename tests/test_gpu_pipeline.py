@@ -268,6 +268,30 @@ def test_pretrain_jobs_equal_sequential_runs(ml, orc, threads):
         assert np.array_equal(a.params, b.params) and np.array_equal(a.momentum, b.momentum)
 
 
+def test_pretrain_jobs_mapped_per_job_stores(ml, orc):
+    """moses_pretrain_jobs_mapped (the f4 job grid across GPUs: job j over its own device's copy of the
+    store): with two copies of the store on this device, every job equals its sequential run; a job whose
+    store is on another device than its handle is refused (single-GPU box: checked only when >1 GPU)."""
+    import torch
+
+    dims = [16, 512, 512, 1]
+    seeds = [21, 22, 23, 24]
+    pool = [ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16X3, 512) for s in seeds]
+    X, Y, task_of = _dataset(ml, orc, pool[0], 400, 4, ml.DTYPE_F32)
+    X2, Y2 = X.clone(), Y.clone()
+    torch.cuda.synchronize()
+    ids = [t for t, _ in TASKS]
+    ld = pool[0].packed_ld
+    xs = [vp(X), vp(X2), vp(X), vp(X2)]
+    ys = [vp(Y), vp(Y2), vp(Y), vp(Y2)]
+    losses, dropped = ml.pretrain_jobs_mapped(pool, seeds, xs, ld, ys, task_of, ids, 128, 2, 0.001, 0.9, 4)
+    for j, s in enumerate(seeds):
+        ref = ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16X3, 512)
+        l_ref, d_ref = ml.pretrain_device(ref, vp(X), ld, vp(Y), task_of, ids, 128, s, 2, 0.001, 0.9)
+        assert losses[j].tolist() == l_ref and dropped[j] == d_ref
+        assert np.array_equal(pool[j].download().params, ref.download().params)
+
+
 def test_pretrain_from_records_matches_oracle(ml, orc):
     """moses_pretrain (host records -> device staging grouped by task -> encode -> epochs) on an FP32
     handle vs the fp64 oracle's pretrain over the same records (tuner.cpp:130-156): same batches,

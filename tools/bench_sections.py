@@ -411,19 +411,34 @@ def bench_pretrain(ml, L, peaks, epochs: int = 30, per_task: int = 6000):
     launches = L.moses_kernel_launches() - k0
     # SURVEY.md §8(f) f4 shape: a (seed) job grid of independent pretrain runs on the native worker
     # pool, one handle (and stream set) per job, sharing the device-resident store
-    n_jobs = 8
-    jobs = [ml.DeviceModel(ml.init_random(dims, s), ml.PREC_BF16, 512) for s in range(n_jobs)]
-    ml.pretrain_jobs(jobs, list(range(n_jobs)), C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()), task_of, ids,
-                     512, 1, 0.001, 0.9, n_jobs)  # warm (graph capture per handle)
+    # (f4 across GPUs: jobs round-robin over every GPU of the process, each over its device's copy)
+    n_gpu = torch.cuda.device_count()
+    n_jobs = 8 * n_gpu
+    home = torch.cuda.current_device()
+    copies = {home: (X, Y)}
+    jobs = []
+    for j in range(n_jobs):
+        dev = j % n_gpu
+        torch.cuda.set_device(dev)
+        if dev not in copies:
+            copies[dev] = (X.to(f"cuda:{dev}"), Y.to(f"cuda:{dev}"))
+        jobs.append(ml.DeviceModel(ml.init_random(dims, j), ml.PREC_BF16, 512))
+    torch.cuda.set_device(home)
+    torch.cuda.synchronize()
+    xs = [C.c_void_p(copies[j % n_gpu][0].data_ptr()) for j in range(n_jobs)]
+    ys = [C.c_void_p(copies[j % n_gpu][1].data_ptr()) for j in range(n_jobs)]
+    ml.pretrain_jobs_mapped(jobs, list(range(n_jobs)), xs, ld, ys, task_of, ids, 512, 1, 0.001, 0.9,
+                            n_jobs)  # warm (graph capture per handle)
     for j, jm in enumerate(jobs):
         jm.upload(ml.init_random(dims, j))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    job_losses, _ = ml.pretrain_jobs(jobs, list(range(n_jobs)), C.c_void_p(X.data_ptr()), ld, C.c_void_p(Y.data_ptr()),
-                                     task_of, ids, 512, epochs, 0.001, 0.9, n_jobs)
+    job_losses, _ = ml.pretrain_jobs_mapped(jobs, list(range(n_jobs)), xs, ld, ys, task_of, ids, 512, epochs, 0.001,
+                                            0.9, n_jobs)
     jobs_s = time.perf_counter() - t0
     for jm in jobs:
         jm.close()
+    del copies
     # the same loop on the fp64 CPU oracle: a bounded sample of epoch 0's batches
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
@@ -448,10 +463,11 @@ def bench_pretrain(ml, L, peaks, epochs: int = 30, per_task: int = 6000):
             "generate_ms": gen_ms, "plan_ms_host": plan_ms,
             "pretrain_s": total, "samples_per_s": epochs * n / total, "ms_per_epoch": total / epochs * 1e3,
             "epoch_mean_loss_first_last": [losses[0], losses[-1]], "gpu_launches": int(launches),
-            "job_grid": {"jobs": n_jobs, "workers": n_jobs, "wall_s": jobs_s,
+            "job_grid": {"jobs": n_jobs, "gpus": n_gpu, "workers": n_jobs, "wall_s": jobs_s,
                          "samples_per_s": n_jobs * epochs * n / jobs_s,
                          "speedup_vs_sequential": n_jobs * total / jobs_s,
-                         "path": "moses_pretrain_jobs: 8 seeds x 30 epochs, one handle/stream set per job"},
+                         "path": "moses_pretrain_jobs_mapped: 8 seeds per GPU x 30 epochs, jobs round-robin over "
+                                 "the process's GPUs, one handle/stream set per job, each over its GPU's store copy"},
             "cpu_oracle": {"samples_per_s": cpu_rows / cpu_dt, "cores": threads, "kind": "port",
                            "sample": f"{nb} batches ({cpu_rows} rows) of epoch 0, fp64"},
             "path": "moses_generate_dataset_device x8 -> moses_pretrain_device (host plan of epoch e+1 overlapped "
