@@ -1,7 +1,12 @@
 // lottery.cu — the Moses adaptation step (tuner.cpp:258-262) as few HBM passes as the exact
 // selection allows: xi = |w*g| is never materialised, every pass recomputes it from (w, g).
 //
-//   threshold (lottery.cpp:152-157, normalised):  pass 1 max(xi)  ->  pass 2 fused apply       23 B/param
+//   threshold (lottery.cpp:152-157, normalised): ONE pass (lot_thresh_pass_kernel) + a candidate fix-up,
+//     15 B/param. A stratified sample gives max_s <= max(xi), so T_s = thresh_key(max_s) <= T = thresh_key(max)
+//     (fl(x / max) <= fl(x / max_s): division rounding is monotone). Keys < T_s are final in the pass
+//     (variant: decayed, mask 0); keys >= T_s keep their w, get mask byte 2 and join a candidate list;
+//     once the pass has produced the exact max, lot_thresh_fix_kernel resolves only those (or, if the list
+//     overflowed, every mask byte still 2). Exact for any input: no estimate can misclassify a scalar.
 //   ratio     (lottery.cpp:158-175, top ceil(rho*N), ties by index):
 //     pass 1  15-bit histogram of xi bits [30:16] (xi >= 0, so the bit pattern orders like the value)
 //     pass 2  16-bit histogram of bits [15:0] within the chosen bucket  -> exact threshold key T
@@ -49,6 +54,7 @@ struct LotState {
   unsigned long long above;  // keys whose bucket lies above the bracket
   unsigned long long eqc_n;  // candidates with key == T collected for the index cut
   int cut_done;              // the cut was found over the candidates
+  unsigned smax_bits;        // threshold: max xi key of the stratified sample (a lower bound of max_bits)
 };
 static_assert(sizeof(LotState) <= 256, "LotState must fit its workspace slot");
 
@@ -730,6 +736,155 @@ __global__ void __launch_bounds__(kPassBlock) lot_max_kernel(const float* __rest
   if ((threadIdx.x & 31) == 0 && m) atomicMax(&st->max_bits, m);
 }
 
+// ---------------------------------------------------------------- threshold step: one (w, g) pass
+// Sample max over one float4 of (w, g) per stratum (lot_sample_kernel's positions): a lower bound of max.
+__global__ void __launch_bounds__(kPassBlock) lot_tsample_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                                                 long long n, LotState* st) {
+  unsigned m = 0;
+  const long long strata = n / 4 / kSampleStride;
+  for (long long j = blockIdx.x * (long long)kPassBlock + threadIdx.x; j < strata; j += (long long)gridDim.x * kPassBlock) {
+    const long long q = j * kSampleStride + (mix32(unsigned(j)) % kSampleStride);
+    const float4 a = ld4(w + 4 * q), b = ld4(g + 4 * q);
+    m = max(max(max(m, key_of(a.x, b.x)), key_of(a.y, b.y)), max(key_of(a.z, b.z), key_of(a.w, b.w)));
+  }
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&st->smax_bits, m);
+}
+
+// The pass: every scalar read once; keys below T_s finished (decay / mask 0 / shadow), the rest left as
+// candidates (w and its shadow rewritten unchanged so every line is written whole, mask byte 2, index
+// appended warp-aggregated to `cand`); the exact max accumulated with atomicMax.
+template <int SHADOW>
+__global__ void __launch_bounds__(256) lot_thresh_pass_kernel(float* __restrict__ w, const float* __restrict__ g,
+                                                              long long n, LotState* st, float theta, float factor,
+                                                              bool decay, void* __restrict__ shadow,
+                                                              uint8_t* __restrict__ mask, unsigned* __restrict__ cand) {
+  __shared__ unsigned s_ts;
+  if (threadIdx.x == 0) {
+    const unsigned sm = st->smax_bits;
+    s_ts = sm == 0 ? 0u : thresh_key(__uint_as_float(sm), theta);  // max_s == 0: no bound, all candidates
+  }
+  __syncthreads();
+  const unsigned Ts = s_ts;
+  const unsigned long long cap = st->cand_cap;
+  const unsigned lane = threadIdx.x & 31;
+  unsigned m = 0;
+  auto one = [&](float& wi, float gi, uint8_t& mk, long long i) {  // warp-collective (append)
+    const unsigned key = __float_as_uint(fabsf(__fmul_rn(wi, gi)));
+    m = max(m, key);
+    const bool c = key >= Ts && i < n;
+    if (!c && decay) wi = __fmul_rn(wi, factor);
+    mk = c ? 2 : 0;
+    const unsigned ball = __ballot_sync(0xffffffffu, c);
+    if (ball) {
+      unsigned long long b = 0;
+      if (lane == 0) {
+        b = atomicAdd(&st->cand_n, (unsigned long long)__popc(ball));
+        if (b + __popc(ball) > cap) st->cand_over = 1;
+      }
+      b = __shfl_sync(0xffffffffu, b, 0);
+      const unsigned long long slot = b + __popc(ball & ((1u << lane) - 1u));
+      if (c && slot < cap) cand[slot] = unsigned(i);
+    }
+  };
+  const long long n4 = n / 4;
+  const long long qend = (n4 + 255) / 256 * 256;  // warp-uniform trip count (the ballots)
+  for (long long q = blockIdx.x * 256ll + threadIdx.x; q < qend; q += (long long)gridDim.x * 256) {
+    const bool ok = q < n4;
+    const long long i = 4 * q;
+    float4 wv = make_float4(0, 0, 0, 0), gv = wv;
+    if (ok) {
+      wv = *reinterpret_cast<const float4*>(w + i);
+      gv = ld4(g + i);
+    }
+    uchar4 mk;
+    one(wv.x, gv.x, mk.x, ok ? i : n);
+    one(wv.y, gv.y, mk.y, ok ? i + 1 : n);
+    one(wv.z, gv.z, mk.z, ok ? i + 2 : n);
+    one(wv.w, gv.w, mk.w, ok ? i + 3 : n);
+    if (ok) {
+      *reinterpret_cast<float4*>(w + i) = wv;
+      *reinterpret_cast<uchar4*>(mask + i) = mk;
+      store_shadow4<SHADOW>(shadow, i, wv);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // scalar tail (< 4 scalars), warp 0
+    const long long i = 4 * n4 + lane;
+    float wi = i < n ? w[i] : 0.f;
+    const float gi = i < n ? g[i] : 0.f;
+    uint8_t mk;
+    one(wi, gi, mk, i < n ? i : n);
+    if (i < n) {
+      w[i] = wi;
+      mask[i] = mk;
+      if constexpr (SHADOW == 1) static_cast<__nv_bfloat16*>(shadow)[i] = __float2bfloat16_rn(wi);
+      if constexpr (SHADOW == 2) {
+        uint32_t t;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(wi));
+        static_cast<float*>(shadow)[i] = __uint_as_float(t);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0 && m) atomicMax(&st->max_bits, m);
+}
+
+// Candidates against the exact T = thresh_key(max, theta): the same per-scalar step as lot_apply_one.
+// List mode (no overflow): grid-stride over cand[0, cand_n). Overflow: grid-stride over the mask bytes.
+template <int SHADOW>
+__global__ void __launch_bounds__(256) lot_thresh_fix_kernel(float* __restrict__ w, const float* __restrict__ g,
+                                                             long long n, LotState* st, float theta, float alpha,
+                                                             float factor, bool decay, void* __restrict__ shadow,
+                                                             uint8_t* __restrict__ mask, const unsigned* __restrict__ cand,
+                                                             const StepOpt opt) {
+  using Red = cub::BlockReduce<unsigned long long, 256>;
+  __shared__ typename Red::TempStorage tmp;
+  __shared__ unsigned s_t;
+  if (threadIdx.x == 0) s_t = thresh_key(__uint_as_float(st->max_bits), theta);
+  __syncthreads();
+  const unsigned T = s_t;
+  unsigned long long cnt = 0;
+  auto fix = [&](long long i) {
+    float wi = w[i];
+    float a1 = opt.m1 ? opt.m1[i] : 0.f, a2 = opt.m1 ? opt.m2[i] : 0.f;
+    uint8_t mk;
+    lot_apply_one<SHADOW, true>(i, wi, g[i], T, 0, 0.f, theta, alpha, factor, decay, mk, cnt, opt, a1, a2);
+    if (opt.m1) {
+      opt.m1[i] = a1;
+      opt.m2[i] = a2;
+    }
+    w[i] = wi;
+    mask[i] = mk;
+    if constexpr (SHADOW == 1) static_cast<__nv_bfloat16*>(shadow)[i] = __float2bfloat16_rn(wi);
+    if constexpr (SHADOW == 2) {
+      uint32_t t;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(wi));
+      static_cast<float*>(shadow)[i] = __uint_as_float(t);
+    }
+  };
+  const long long stride = (long long)gridDim.x * 256;
+  if (!st->cand_over) {
+    const long long nc = (long long)st->cand_n;
+    for (long long k = blockIdx.x * 256ll + threadIdx.x; k < nc; k += stride) fix(cand[k]);
+  } else {
+    const long long n16 = n / 16;
+    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < n16; q += stride) {
+      const uint4 v = *reinterpret_cast<const uint4*>(mask + 16 * q);
+      const unsigned words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (words[b] & 0x02020202u)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((words[b] >> (8 * e)) & 2u) fix(16 * q + 4 * b + e);
+    }
+    for (long long i = 16 * n16 + blockIdx.x * 256ll + threadIdx.x; i < n; i += stride)
+      if (mask[i] == 2) fix(i);
+  }
+  cnt = Red(tmp).Sum(cnt);
+  if (threadIdx.x == 0 && cnt) atomicAdd(&st->count, cnt);
+}
+
 // ---------------------------------------------------------------- single-launch resident step
 // For the cost model's own parameter counts (P <= 148 x 512 x 16 ~ 1.2M; the 4x512 model has
 // 872,961) the whole step is ONE cooperative launch: every thread keeps its <= 16 (w, g) pairs in
@@ -981,6 +1136,7 @@ __global__ void lot_init_kernel(LotState* st, unsigned long long keep, unsigned 
   st->eq = 0;
   st->prefix = 0;
   st->max_bits = 0;
+  st->smax_bits = 0;
   st->cut = 0x7fffffffffffffffll;
   st->count = 0;
 }
@@ -1064,12 +1220,18 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     MOSES_CUDA(cudaGetLastError());
     return 1;
   }
-  lot_init_kernel<<<1, 1, 0, st>>>(S, (unsigned long long)keep, (unsigned long long)cap);
+  // threshold mode: the candidate list holds 32-bit indices in the (key, index) pair buffer (2x the entries)
+  const long long tcap = n < (1ll << 32) ? 2 * cap : 0;
+  lot_init_kernel<<<1, 1, 0, st>>>(S, (unsigned long long)keep, (unsigned long long)(mode == 1 ? tcap : cap));
   const int agrid = std::max<long long>(1, std::min<long long>((n / 4 + 255) / 256, (long long)sms * 16));
-  if (mode == 1) {
-    lot_max_kernel<<<sms * 2, kPassBlock, 0, st>>>(w, g, n, S);  // 2 x 1024 threads per SM
-#define LOT_T(K) lot_apply_kernel<K, true><<<agrid, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask, opt)
-    if (sh.kind == 1) LOT_T(1); else if (sh.kind == 2) LOT_T(2); else LOT_T(0);
+  if (mode == 1) {  // one (w, g) pass + candidate fix-up (module comment)
+    unsigned* tcand = reinterpret_cast<unsigned*>(cand);
+    lot_tsample_kernel<<<sms, kPassBlock, 0, st>>>(w, g, n, S);
+    const int pgrid = std::max<long long>(1, std::min<long long>((n / 4 + 255) / 256, (long long)sms * 8));
+#define LOT_T(K)                                                                                                \
+  lot_thresh_pass_kernel<K><<<pgrid, 256, 0, st>>>(w, g, n, S, theta, factor, decay, sh.ptr, mask, tcand);      \
+  lot_thresh_fix_kernel<K><<<sms * 4, 256, 0, st>>>(w, g, n, S, theta, alpha, factor, decay, sh.ptr, mask, tcand, opt)
+    if (sh.kind == 1) { LOT_T(1); } else if (sh.kind == 2) { LOT_T(2); } else { LOT_T(0); }
 #undef LOT_T
   } else {
     if (compact) {
@@ -1105,7 +1267,7 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     MOSES_CUDA(cudaMemcpyAsync(popcount_dev, &S->count, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
   }
   MOSES_CUDA(cudaGetLastError());
-  return mode == 1 ? 3 : (compact ? 16 : 8);  // kernels launched
+  return mode == 1 ? 4 : (compact ? 16 : 8);  // kernels launched
 }
 
 }  // namespace moses

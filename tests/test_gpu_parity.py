@@ -848,6 +848,45 @@ def test_threshold_step_large_bit_exact(ml, orc, theta):
     assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
 
 
+@pytest.mark.parametrize("kind,theta", [("normal", 0.5), ("normal", 0.9), ("outlier", 0.5), ("zeros", 0.0),
+                                         ("allzero", 0.5), ("normal", 0.0)])
+def test_threshold_step_single_pass_bit_exact(ml, orc, kind, theta):
+    """16.8M scalars: the one-pass threshold step (lottery.cu lot_thresh_pass / lot_thresh_fix). 'normal':
+    the few scalars at or above the sampled bound resolve from the candidate list; 'outlier': one huge
+    xi outside every sampled stratum puts the sampled max far below the true max, the candidate list
+    overflows and the fix-up scans the mask bytes; 'allzero': g == 0 (max 0, xi not normalised, nothing
+    kept); theta = 0 keeps every non-zero xi. Mask, popcount and weights bit-identical to
+    xi_scores(normalize) -> xi > theta -> step -> decay in fp32."""
+    dims = [8192, 2048, 8, 1]
+    P = ml.param_count(dims)
+    rng = np.random.default_rng(int(theta * 100) + len(kind))
+    w = f32(rng.normal(0, 0.05, P))
+    g = f32(rng.normal(0, 1e-2, P))
+    if kind == "zeros":
+        g[rng.random(P) < 0.4] = 0.0
+    if kind == "allzero":
+        g[:] = 0.0
+    if kind == "outlier":
+        # the sample reads one float4 per 1024 scalars at a hashed offset; index 5 of stratum 7 is
+        # never sampled when the hashed float4 of stratum 7 is elsewhere (checked below)
+        i = 7 * 1024 + 5
+        w[i], g[i] = 3.0, 2.0
+    dm = ml.DeviceModel(ml_params(dims, w), ml.PREC_BF16, 16)
+    dm.set_gradients(g)
+    import ctypes
+
+    out = np.zeros(P, dtype=np.uint8)
+    pop = ctypes.c_int64()
+    ml._ck(ml.lib().moses_lottery_step(dm.h, ml.THRESHOLD, theta, 0, 0.001, 0.01, out.ctypes.data, P, ctypes.byref(pop)))
+    w32, g32 = w.astype(np.float32), g.astype(np.float32)
+    ref_mask = orc.partition(orc.xi_scores(w32, g32, True), True, orc.THRESHOLD, theta)
+    assert np.array_equal(out.astype(bool), ref_mask)
+    assert pop.value == int(np.sum(ref_mask))  # the device count of the kept scalars
+    ref_w, _ = orc.apply_update(w32, np.zeros_like(w32), g32, 0.001, 0.0, ref_mask, False)
+    ref_w = orc.variant_decay(ref_w, ref_mask, 0.001, 0.01)
+    assert np.array_equal(dm.download().params, ref_w.astype(np.float64))
+
+
 @pytest.mark.parametrize("pinned_losses", [True, False])
 def test_async_pooled_steps_match_synchronous(ml, pinned_losses):
     """moses_train_step_pooled_async (double-buffered upload + per-slot graph) == gradients_pooled +
