@@ -50,6 +50,9 @@ enum {
   MOSES_ERR_UNNORMALIZED_THRESHOLD = 12, /* ErrorCode::UnnormalizedThreshold */
   MOSES_ERR_ADVERSARY_DISABLED = 13,   /* ErrorCode::AdversaryDisabled */
   MOSES_ERR_UNSTABLE_DECAY = 14,       /* ErrorCode::UnstableDecay */
+  MOSES_ERR_INFEASIBLE_SPLIT = 15,     /* ErrorCode::InfeasibleSplit */
+  MOSES_ERR_ZERO_MEAN = 16,            /* ErrorCode::ZeroMean */
+  MOSES_ERR_INSUFFICIENT_BATCHES = 17, /* ErrorCode::InsufficientBatches */
   MOSES_ERR_PARSE = 22,                /* ErrorCode::ParseError */
   MOSES_ERR_MISSING_FIELD = 23,        /* ErrorCode::MissingField */
   MOSES_ERR_IO = 24,                   /* ErrorCode::IoError */
@@ -391,6 +394,71 @@ MOSES_API int moses_pretrain_jobs_mapped(int32_t n_jobs, const moses_model_t* mo
                                         int32_t n_task_ids, int32_t batch_size, int32_t epochs, double learning_rate,
                                         double momentum, int32_t threads, double* epoch_mean_loss,
                                         int64_t* dropped_singletons);
+/* ------------------------------------------------------------------ online tuning */
+/* The tuner's per-task loop (tuner.cpp:158-286) and its (strategy, seed, task) job grid (tuner.cpp:307-374)
+ * over this library's calls: per measured batch evolve (moses_evolve, device scoring) -> select_batch ->
+ * measure (oracle.cpp:65-88 on the device) -> the controller's CV (controller.cpp:34-56, host) -> the
+ * strategy's update (Moses: gradients with the replay adversary -> discriminator step -> lottery step;
+ * vanilla / random-init: gradients -> apply_update), then the prediction-only tail. */
+enum { MOSES_STRATEGY_RAW = 0, MOSES_STRATEGY_RANDOM_INIT = 1, MOSES_STRATEGY_PRETRAIN_ONLY = 2,
+       MOSES_STRATEGY_VANILLA = 3, MOSES_STRATEGY_MOSES = 4 };               /* tuner.hpp StrategyKind */
+typedef struct {                       /* oracle.hpp DeviceSpec */
+  const char* id;
+  double params[6];                    /* peak_gflops, parallel_units, vector_lanes, cache_bytes, measure_overhead_ms, noise_std */
+  int32_t repeats;
+} moses_device_spec;
+typedef struct {                       /* space.hpp TaskSpec: task4 = {work_gflops, bytes_per_unit, ideal_log_tiles, ideal_log_unroll} */
+  const char* id;
+  double task4[4];
+  const int64_t* domains;              /* concatenated knob domains (strictly increasing each) */
+  const int32_t* domain_sizes;
+  const int32_t* roles;
+  int32_t n_knobs;
+} moses_task_spec;
+typedef struct {                       /* tuner.hpp TuneBudget (search seed ignored: per-batch streams) */
+  int32_t trials_per_task;
+  double train_fraction;
+  int32_t num_batches;
+  double cv_threshold;
+  int32_t population, generations, mutation_count, survivors;   /* search.hpp SearchParams */
+  double epsilon_random;
+  double learning_rate, weight_decay, adversary_beta;           /* model.hpp TrainHyper */
+  int32_t lottery_mode;                /* MOSES_MODE_THRESHOLD / MOSES_MODE_RATIO */
+  double lottery_value;
+  int32_t adversary;                   /* Moses only */
+  int32_t replay_size;
+} moses_tune_budget;
+typedef struct {                       /* tuner.hpp TaskResult + ControllerTrace; caller-owned arrays */
+  int64_t capacity;                    /* rows of values / throughput / latency / wall_cost / predicted_scores */
+  int64_t* values;                     /* [capacity x n_knobs] measured configurations, measurement order */
+  double* throughput;
+  double* latency;
+  double* wall_cost;
+  int64_t n_records;
+  int64_t* best_values;                /* [n_knobs] */
+  double best_latency_ms;
+  double wall_cost_ms;
+  double* batch_means;                 /* [num_batches] */
+  double* cvs;                         /* [num_batches]; NaN where fewer than two means existed */
+  int32_t n_batch_means;
+  int32_t termination_batch, measured_trials, prediction_trials, unspent_trials;
+  double* predicted_scores;            /* [capacity] prediction-only tail */
+} moses_task_result;
+/* tune_task on the parameters held by `m` (updated in place: pass a copy per job, tuner.cpp:349).
+ * source_features: the source store's encoded rows (n_source x dims[0], store order), needed by Moses with
+ * the adversary on (the replay buffer, data.cpp:166-183); NULL otherwise. */
+MOSES_API int moses_tune_task(moses_model_t m, int32_t strategy, const moses_device_spec* device,
+                              const moses_task_spec* task, const moses_tune_budget* budget, uint64_t seed,
+                              const double* source_features, int64_t n_source, moses_task_result* out);
+/* The job grid: job j = (strategies[j], seeds[j], tasks[task_of[j]]) on handle models[j] (a per-job copy,
+ * on any GPU of the process), claimed in order by `threads` workers (0: one per job, capped at 64), the
+ * first failing job's status returned. results[j] as moses_tune_task's out. */
+MOSES_API int moses_tune_jobs(int32_t n_jobs, const moses_model_t* models, const int32_t* strategies,
+                              const uint64_t* seeds, const int32_t* task_of, const moses_task_spec* tasks,
+                              int32_t n_tasks, const moses_device_spec* device, const moses_tune_budget* budget,
+                              const double* source_features, int64_t n_source, int32_t threads,
+                              moses_task_result* results);
+
 /* Line-delimited record files (data.cpp:67-126). moses_records_read fails with MOSES_ERR_IO,
  * MOSES_ERR_PARSE (message names "<path>:line N") or MOSES_ERR_MISSING_FIELD. */
 MOSES_API int moses_records_create(moses_records_t* out);

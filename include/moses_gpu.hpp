@@ -504,7 +504,7 @@ inline CostModelParams pretrain(const RecordStore& store, const std::vector<Task
   return m.download();
 }
 
-// ---- search.hpp: evolve with the model scorer on the device (search.cpp:41-71, 120-127)
+// ---- search.hpp: evolve with the model scorer on the device (search.cpp:41-80)
 struct SearchParams {  // search.hpp:13-20
   int population = 128;
   int generations = 4;
@@ -533,6 +533,115 @@ inline std::vector<ScoredCandidate> evolve(DeviceModel& model, const TaskSpec& t
     out[size_t(i)].score = sc[size_t(i)];
   }
   return out;
+}
+
+// ---- tuner.hpp: the per-task online loop and the job grid on the device (tuner.cpp:158-286, 307-374)
+enum class StrategyKind { Raw = MOSES_STRATEGY_RAW, RandomInit = MOSES_STRATEGY_RANDOM_INIT,
+                          PretrainOnly = MOSES_STRATEGY_PRETRAIN_ONLY, VanillaFinetune = MOSES_STRATEGY_VANILLA,
+                          Moses = MOSES_STRATEGY_MOSES };
+struct LotterySettings {  // tuner.hpp LotterySettings
+  PartitionMode mode = PartitionMode::Ratio;
+  double value = 0.5;
+};
+struct TuneBudget {  // tuner.hpp TuneBudget
+  int trials_per_task = 64;
+  double train_fraction = 0.9;
+  int num_batches = 5;
+  double cv_threshold = 0.05;
+  SearchParams search;
+  TrainHyper hyper;
+  LotterySettings lottery;
+  bool adversary = true;
+  int replay_size = 256;
+};
+struct ControllerTrace {  // tuner.hpp ControllerTrace
+  std::vector<double> batch_means, cvs;
+  int termination_batch = -1, measured_trials = 0, prediction_trials = 0, unspent_trials = 0;
+  std::vector<double> predicted_scores;
+};
+struct TaskResult {  // tuner.hpp TaskResult
+  std::string task_id;
+  Configuration best_config;
+  double best_latency_ms = 0.0, wall_cost_ms = 0.0;
+  std::vector<MeasurementRecord> records;
+  ControllerTrace trace;
+};
+namespace detail {
+struct TuneArgs {
+  moses_device_spec dev{};
+  moses_tune_budget bud{};
+  TuneArgs(const DeviceSpec& d, const TuneBudget& b) {
+    dev.id = d.id.c_str();
+    const auto d6 = device6(d);
+    std::copy(d6.begin(), d6.end(), dev.params);
+    dev.repeats = d.repeats;
+    bud = {b.trials_per_task, b.train_fraction, b.num_batches, b.cv_threshold, b.search.population,
+           b.search.generations, b.search.mutation_count, b.search.survivors, b.search.epsilon_random,
+           b.hyper.learning_rate, b.hyper.weight_decay, b.hyper.adversary_beta,
+           b.lottery.mode == PartitionMode::Threshold ? MOSES_MODE_THRESHOLD : MOSES_MODE_RATIO, b.lottery.value,
+           b.adversary ? 1 : 0, b.replay_size};
+  }
+};
+struct ResultBuf {  // caller-owned arrays of moses_task_result
+  std::vector<int64_t> values, best;
+  std::vector<double> thr, lat, wall, means, cvs, pred;
+  moses_task_result r{};
+  ResultBuf(const TuneBudget& b, size_t nk)
+      : values(size_t(std::max(b.trials_per_task, 1)) * nk), best(nk), thr(size_t(std::max(b.trials_per_task, 1))),
+        lat(thr.size()), wall(thr.size()), means(size_t(std::max(b.num_batches, 1))), cvs(means.size()),
+        pred(thr.size()) {
+    r.capacity = int64_t(thr.size());
+    r.values = values.data();
+    r.throughput = thr.data();
+    r.latency = lat.data();
+    r.wall_cost = wall.data();
+    r.best_values = best.data();
+    r.batch_means = means.data();
+    r.cvs = cvs.data();
+    r.predicted_scores = pred.data();
+  }
+  TaskResult take(const TaskSpec& task, const DeviceSpec& dev) const {
+    TaskResult t;
+    t.task_id = task.id;
+    const size_t nk = task.knobs.size();
+    t.best_config.values = best;
+    t.best_latency_ms = r.best_latency_ms;
+    t.wall_cost_ms = r.wall_cost_ms;
+    for (int64_t i = 0; i < r.n_records; ++i) {
+      MeasurementRecord m;
+      m.task_id = task.id;
+      m.device_id = dev.id;
+      m.values.assign(values.begin() + i * int64_t(nk), values.begin() + (i + 1) * int64_t(nk));
+      m.throughput_gflops = thr[size_t(i)];
+      m.latency_ms = lat[size_t(i)];
+      m.wall_cost_ms = wall[size_t(i)];
+      t.records.push_back(std::move(m));
+    }
+    t.trace.batch_means.assign(means.begin(), means.begin() + r.n_batch_means);
+    t.trace.cvs.assign(cvs.begin(), cvs.begin() + r.n_batch_means);
+    t.trace.termination_batch = r.termination_batch;
+    t.trace.measured_trials = r.measured_trials;
+    t.trace.prediction_trials = r.prediction_trials;
+    t.trace.unspent_trials = r.unspent_trials;
+    t.trace.predicted_scores.assign(pred.begin(), pred.begin() + r.prediction_trials);
+    return t;
+  }
+};
+}  // namespace detail
+// tune_task on the parameters held by `model` (updated in place: the reference copies initial_model per
+// job, tuner.cpp:349 — give each job its own DeviceModel). source_features: the source store's encoded
+// rows (the adversary's replay pool), or nullptr.
+inline TaskResult tune_task(StrategyKind strategy, DeviceModel& model, const DeviceSpec& device, const TaskSpec& task,
+                            const TuneBudget& budget, uint64_t seed, const Matrix* source_features = nullptr) {
+  const detail::SpaceArrays a(task);
+  const detail::TuneArgs ta(device, budget);
+  moses_task_spec ts{task.id.c_str(), {a.task4[0], a.task4[1], a.task4[2], a.task4[3]}, a.domains.data(),
+                     a.sizes.data(), a.roles.data(), int32_t(task.knobs.size())};
+  detail::ResultBuf buf(budget, task.knobs.size());
+  check(moses_tune_task(model.handle(), int32_t(strategy), &ta.dev, &ts, &ta.bud, seed,
+                        source_features ? source_features->data.data() : nullptr,
+                        source_features ? int64_t(source_features->rows) : 0, &buf.r));
+  return buf.take(task, device);
 }
 
 }  // namespace moseslab_gpu

@@ -10,6 +10,7 @@ file:line each one restates.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -683,3 +684,116 @@ def evolve(knobs, scorer, population=128, generations=4, mutation_count=4, survi
                 nxt.append(sample() if rng.uniform01() < epsilon_random else mutate(pop[s][0]))
         pop = score_all(nxt)
     return pop
+
+
+# ---------------------------------------------------------------- online loop (tuner.cpp:158-286, controller.cpp)
+def plan_split(total, p, q):  # controller.cpp:10-32
+    if q < 2:
+        raise OracleError(2, "need at least 2 batches")
+    if total < q:
+        raise OracleError(2, "total trials below the batch count")
+    if not (p > 0.0) or p > 1.0:
+        raise OracleError(2, "train fraction must lie in (0,1]")
+    measured = int(math.floor(p * float(total) + 1e-9))
+    if measured < q:
+        raise OracleError(15, "infeasible split")
+    base, rem = divmod(measured, q)
+    return total - measured, [base + (1 if b < rem else 0) for b in range(q)]
+
+
+def _seq_sum(values):
+    """Left-to-right double accumulation like the reference's loops (Python >= 3.12's sum() of floats is
+    compensated, which differs in the last bit)."""
+    acc = 0.0
+    for v in values:
+        acc += v
+    return acc
+
+
+def batch_cv(means):  # controller.cpp:34-45
+    mean = _seq_sum(means) / len(means)
+    var = _seq_sum((v - mean) * (v - mean) for v in means) / len(means)
+    return math.sqrt(var) / mean
+
+
+def tune_task(strategy, ops, task_id, knobs, budget, seed):
+    """Restatement of tune_task (tuner.cpp:158-286) with the model / measurement operations injected:
+      ops.evolve(seed) -> [(values, score)] in search order (evolve(params, space, sp), search.cpp:73-80)
+      ops.measure([values]) -> [(throughput, latency, wall_cost)] (oracle.cpp:65-88, seq unused by the noise)
+      ops.make_adversary(replay_seed) (tuner.cpp:187-201)
+      ops.moses_update(values_rows, labels, batch, use_adversary) (tuner.cpp:248-262)
+      ops.vanilla_update(values_rows, labels) (tuner.cpp:263-266)
+    strategy: 0 raw, 1 random-init, 2 pretrain-only, 3 vanilla-finetune, 4 moses. Returns a dict."""
+    nk = len(knobs)
+    recs, cvs, predicted = [], [], []
+    wall, unspent, term, meas = 0.0, 0, -1, 0
+    best_lat, best_cfg = math.inf, None
+    means, terminated = [], False
+    if strategy == 0:  # tuner.cpp:166-178
+        cfg = [d[(len(d) - 1) // 2] for _, d in knobs]
+        thr, lat, w = ops.measure([cfg])[0]
+        return {"records": [(cfg, thr, lat, w)], "best_values": cfg, "best_latency": lat, "wall": w,
+                "batch_means": [], "cvs": [], "termination_batch": -1, "measured": 1, "prediction": 0,
+                "unspent": budget.trials_per_task - 1, "predicted": []}
+    pred_trials, sizes = plan_split(budget.trials_per_task, budget.train_fraction, budget.num_batches)
+    use_adv = strategy == 4 and budget.adversary
+    if use_adv:
+        ops.make_adversary(key_builder(seed, "replay", task_id))
+    measured = set()
+    for b in range(budget.num_batches):  # tuner.cpp:209-267
+        want = sizes[b]
+        if terminated:
+            unspent += want
+            continue
+        pop = ops.evolve(key_builder(seed, "evolve", task_id, b))
+        batch, taken = [], set()
+        for vals, score in pop:  # select_batch (search.cpp:82-95)
+            if len(batch) >= want:
+                break
+            h = fnv_u64s(vals)
+            if h in measured or h in taken:
+                continue
+            taken.add(h)
+            batch.append((list(vals), score))
+        unspent += want - len(batch)
+        if not batch:
+            continue
+        first = len(recs)
+        out = ops.measure([v for v, _ in batch])
+        for (vals, score), (thr, lat, w) in zip(batch, out):
+            wall += w
+            if lat < best_lat:
+                best_lat, best_cfg = lat, vals
+            measured.add(fnv_u64s(vals))
+            recs.append((vals, thr, lat, w))
+        meas += len(batch)
+        means.append(_seq_sum(s for _, s in batch) / len(batch))  # should_terminate (controller.cpp:47-56)
+        if not terminated and len(means) >= 3 and _seq_sum(means) != 0.0 and abs(batch_cv(means)) < budget.cv_threshold:
+            terminated = True
+        cvs.append(math.nan if len(means) < 2 or _seq_sum(means) == 0.0 else batch_cv(means))  # tuner.cpp:31-37
+        if terminated and term < 0:
+            term = len(means)
+        if strategy == 2 or len(batch) < 2:
+            continue
+        rows = [r[0] for r in recs[first:]]
+        labels = [r[1] for r in recs[first:]]
+        if strategy == 4:
+            ops.moses_update(rows, labels, b, use_adv and budget.adversary_beta != 0.0)
+        else:
+            ops.vanilla_update(rows, labels)
+    pop = ops.evolve(key_builder(seed, "predict", task_id))  # tuner.cpp:271-279
+    tail, taken = [], set()
+    for vals, score in pop:
+        if len(tail) >= pred_trials:
+            break
+        h = fnv_u64s(vals)
+        if h in measured or h in taken:
+            continue
+        taken.add(h)
+        tail.append(score)
+    unspent += pred_trials - len(tail)
+    if not recs:
+        raise OracleError(2, "no configuration was measured")
+    return {"records": recs, "best_values": best_cfg, "best_latency": best_lat, "wall": wall, "batch_means": means,
+            "cvs": cvs, "termination_batch": term, "measured": meas, "prediction": len(tail), "unspent": unspent,
+            "predicted": tail}

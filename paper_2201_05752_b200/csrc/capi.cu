@@ -2175,6 +2175,15 @@ struct GaRng {  // RngStream (rng.hpp)
 };
 }  // namespace
 
+// accessors for the other translation units (tuner.cu); C++ linkage inside the extern "C" block
+extern "C++" {
+namespace moses {
+void set_last_error(const std::string& msg) { g_err = msg; }
+int model_device(const moses_model* m) { return m->device; }
+std::vector<int> model_dims(const moses_model* m) { return m->dims; }
+}  // namespace moses
+}
+
 MOSES_API int moses_evolve(moses_model_t m, const double* lin_w, const double* task4, const int64_t* domains,
                           const int32_t* domain_sizes, const int32_t* roles, int32_t n_knobs, int32_t population,
                           int32_t generations, int32_t mutation_count, int32_t survivors, double epsilon_random,
@@ -2264,12 +2273,15 @@ MOSES_API int moses_evolve(moses_model_t m, const double* lin_w, const double* t
       }
       const long long n = (long long)ids.size();
       MOSES_CUDA(cudaMemcpyAsync(didx, ids.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, st));
+      // rows in the handle's device input type (split handles: fp32, split into their planes per chunk)
       note_launch(encode_configs_idx(task4, reinterpret_cast<const long long*>(domains), domain_sizes, roles, n_knobs,
-                                     didx, n, m->esz == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32, feat, m->ld[0],
+                                     didx, n, m->in_esz() == 2 ? MOSES_DTYPE_BF16 : MOSES_DTYPE_F32, feat, m->ld[0],
                                      m->dims[0], st));
       for (long long r = 0; r < n;) {
         const long long c = std::min(n - r, m->cap);
-        dispatch_forward(m, static_cast<uint8_t*>(feat) + r * m->ld[0] * m->esz, m->ld[0], c, nullptr, false);
+        long long ld0 = 0;
+        const void* x0 = stage_device_rows(m, static_cast<uint8_t*>(feat) + r * m->ld[0] * m->in_esz(), m->ld[0], c, &ld0);
+        dispatch_forward(m, x0, ld0, c, nullptr, false);
         head_scores(m->head_part, m->last_tiles, m->cap, m->head_b(), c, dsc + r, st);
         note_launch(1);
         r += c;
@@ -2289,9 +2301,8 @@ MOSES_API int moses_evolve(moses_model_t m, const double* lin_w, const double* t
     std::vector<Cand> pop;
     try {
       if (m) {
-        if (m->split) fail(MOSES_ERR_INVALID_ARG, "evolve scores through device rows: bf16 or tf32 handles");
         didx = dalloc<unsigned long long>(size_t(maxn));
-        feat = dalloc<uint8_t>(size_t(maxn) * m->ld[0] * m->esz);
+        feat = dalloc<uint8_t>(size_t(maxn) * m->ld[0] * m->in_esz());
         dsc = dalloc<float>(size_t(maxn));
       }
       std::vector<unsigned long long> ids;

@@ -201,6 +201,11 @@ int measure_configs(const double* dev6, int repeats, const char* device_id, cons
                     const long long* domains, const int* sizes, const int* roles, int nk, unsigned long long seed,
                     unsigned long long first, long long n, double* clean_ms, double* thr, double* lat, double* wall,
                     float* label, cudaStream_t st);
+// measure() of configurations given by enumeration index (device list; tuner.cu)
+int measure_configs_idx(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                        const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                        unsigned long long seed, const unsigned long long* idx_dev, long long n, double* thr,
+                        double* lat, double* wall, cudaStream_t st);
 int true_best(const double* dev6, const double* task4, const long long* domains, const int* sizes, const int* roles,
               int nk, long long* best_values, double* best_latency, cudaStream_t st);
 // knob-space candidate generation (space.cu); out_kind 0 f32, 1 bf16, 2 f64

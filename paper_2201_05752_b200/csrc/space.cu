@@ -468,6 +468,13 @@ int measure_configs(const double* dev6, int repeats, const char* device_id, cons
                       clean_ms, thr, lat, wall, label, st);
 }
 
+int measure_configs_idx(const double* dev6, int repeats, const char* device_id, const char* task_id,
+                        const double* task4, const long long* domains, const int* sizes, const int* roles, int nk,
+                        unsigned long long seed, const unsigned long long* idx_dev, long long n, double* thr,
+                        double* lat, double* wall, cudaStream_t st) {
+  return measure_impl(dev6, repeats, device_id, task_id, task4, domains, sizes, roles, nk, seed, 0, idx_dev, n, nullptr,
+                      thr, lat, wall, nullptr, st);
+}
 int true_best(const double* dev6, const double* task4, const long long* domains, const int* sizes, const int* roles,
               int nk, long long* best_values, double* best_latency, cudaStream_t st) {
   unsigned long long space;

@@ -150,6 +150,8 @@ def lib():
         "moses_pretrain": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i32, u64, i32, dbl, dbl, vp, vp]),
         "moses_moses_step": (C.c_int, [vp, vp, vp, vp, i64, i32, dbl, i32, dbl, i32, dbl, dbl, vp, vp, vp]),
         "moses_evolve": (C.c_int, [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, dbl, u64, vp, vp, i64, vp]),
+        "moses_tune_task": (C.c_int, [vp, i32, vp, vp, vp, u64, vp, i64, vp]),
+        "moses_tune_jobs": (C.c_int, [i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i32, vp]),
         "moses_records_create": (C.c_int, [vp]),
         "moses_records_read": (C.c_int, [C.c_char_p, vp]),
         "moses_records_destroy": (None, [vp]),
@@ -1091,3 +1093,150 @@ class RecordStore:
         out = {k: np.zeros(max(m, 1), dtype=t) for k, m, t in specs}
         _ck(lib().moses_records_export(self.h, *(_p(out[k]) for k, _, _ in specs)))
         return {k: out[k][:m] for k, m, _ in specs}
+
+
+# ---------------------------------------------------------------- online tuning
+STRATEGY_RAW, STRATEGY_RANDOM_INIT, STRATEGY_PRETRAIN_ONLY, STRATEGY_VANILLA, STRATEGY_MOSES = 0, 1, 2, 3, 4
+
+
+class _DeviceSpec(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("params", C.c_double * 6), ("repeats", C.c_int32)]
+
+
+class _TaskSpec(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("task4", C.c_double * 4), ("domains", C.c_void_p), ("domain_sizes", C.c_void_p),
+                ("roles", C.c_void_p), ("n_knobs", C.c_int32)]
+
+
+class _TuneBudget(C.Structure):
+    _fields_ = [("trials_per_task", C.c_int32), ("train_fraction", C.c_double), ("num_batches", C.c_int32),
+                ("cv_threshold", C.c_double), ("population", C.c_int32), ("generations", C.c_int32),
+                ("mutation_count", C.c_int32), ("survivors", C.c_int32), ("epsilon_random", C.c_double),
+                ("learning_rate", C.c_double), ("weight_decay", C.c_double), ("adversary_beta", C.c_double),
+                ("lottery_mode", C.c_int32), ("lottery_value", C.c_double), ("adversary", C.c_int32),
+                ("replay_size", C.c_int32)]
+
+
+class _TaskResult(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("values", C.c_void_p), ("throughput", C.c_void_p), ("latency", C.c_void_p),
+                ("wall_cost", C.c_void_p), ("n_records", C.c_int64), ("best_values", C.c_void_p),
+                ("best_latency_ms", C.c_double), ("wall_cost_ms", C.c_double), ("batch_means", C.c_void_p),
+                ("cvs", C.c_void_p), ("n_batch_means", C.c_int32), ("termination_batch", C.c_int32),
+                ("measured_trials", C.c_int32), ("prediction_trials", C.c_int32), ("unspent_trials", C.c_int32),
+                ("predicted_scores", C.c_void_p)]
+
+
+@dataclass
+class TuneBudget:  # tuner.hpp TuneBudget with the reference defaults (search.hpp, model.hpp, tuner.hpp)
+    trials_per_task: int = 64
+    train_fraction: float = 0.9
+    num_batches: int = 5
+    cv_threshold: float = 0.05
+    population: int = 128
+    generations: int = 4
+    mutation_count: int = 4
+    survivors: int = 32
+    epsilon_random: float = 0.05
+    learning_rate: float = 0.001
+    weight_decay: float = 0.01
+    adversary_beta: float = 0.01
+    lottery_mode: int = RATIO
+    lottery_value: float = 0.5
+    adversary: bool = True
+    replay_size: int = 256
+
+    def _c(self):
+        return _TuneBudget(self.trials_per_task, self.train_fraction, self.num_batches, self.cv_threshold,
+                           self.population, self.generations, self.mutation_count, self.survivors,
+                           self.epsilon_random, self.learning_rate, self.weight_decay, self.adversary_beta,
+                           self.lottery_mode, self.lottery_value, int(self.adversary), self.replay_size)
+
+
+@dataclass
+class TaskResult:  # tuner.hpp TaskResult + ControllerTrace
+    values: np.ndarray
+    throughput: np.ndarray
+    latency: np.ndarray
+    wall_cost: np.ndarray
+    best_values: np.ndarray
+    best_latency_ms: float
+    wall_cost_ms: float
+    batch_means: np.ndarray
+    cvs: np.ndarray
+    termination_batch: int
+    measured_trials: int
+    prediction_trials: int
+    unspent_trials: int
+    predicted_scores: np.ndarray
+
+
+def _c_device(device):
+    d = _DeviceSpec()
+    d.id = device["id"].encode()
+    d.params[:] = list(_device6(device))
+    d.repeats = int(device["repeats"])
+    return d
+
+
+def _c_task(task_id, task, knobs, keep):
+    dom, sizes, roles = _space_arrays(knobs)
+    keep += [dom, sizes, roles]
+    t = _TaskSpec()
+    t.id = task_id.encode()
+    t.task4[:] = list(_task4(task))
+    t.domains, t.domain_sizes, t.roles, t.n_knobs = dom.ctypes.data, sizes.ctypes.data, roles.ctypes.data, len(knobs)
+    return t
+
+
+def _alloc_result(budget: TuneBudget, nk: int):
+    cap = max(1, budget.trials_per_task)
+    arrs = {"values": np.zeros((cap, nk), dtype=np.int64), "throughput": np.zeros(cap), "latency": np.zeros(cap),
+            "wall_cost": np.zeros(cap), "best_values": np.zeros(nk, dtype=np.int64),
+            "batch_means": np.zeros(max(1, budget.num_batches)), "cvs": np.zeros(max(1, budget.num_batches)),
+            "predicted_scores": np.zeros(cap)}
+    r = _TaskResult()
+    r.capacity = cap
+    for k, a in arrs.items():
+        setattr(r, k, a.ctypes.data)
+    return r, arrs
+
+
+def _result(r, arrs):
+    n, nb = r.n_records, r.n_batch_means
+    return TaskResult(arrs["values"][:n].copy(), arrs["throughput"][:n].copy(), arrs["latency"][:n].copy(),
+                      arrs["wall_cost"][:n].copy(), arrs["best_values"].copy(), r.best_latency_ms, r.wall_cost_ms,
+                      arrs["batch_means"][:nb].copy(), arrs["cvs"][:nb].copy(), r.termination_batch,
+                      r.measured_trials, r.prediction_trials, r.unspent_trials,
+                      arrs["predicted_scores"][:r.prediction_trials].copy())
+
+
+def tune_task(model: DeviceModel, strategy: int, device, task_id: str, task, knobs, budget: TuneBudget, seed: int,
+              source_features=None) -> TaskResult:
+    """tune_task (tuner.cpp:158-286) on the parameters of `model` (updated in place)."""
+    keep = []
+    t = _c_task(task_id, task, knobs, keep)
+    r, arrs = _alloc_result(budget, len(knobs))
+    src = None if source_features is None else np.ascontiguousarray(source_features, dtype=np.float64)
+    _ck(lib().moses_tune_task(model.h, strategy, C.byref(_c_device(device)), C.byref(t), C.byref(budget._c()), seed,
+                              _p(src), 0 if src is None else src.shape[0], C.byref(r)))
+    return _result(r, arrs)
+
+
+def tune_jobs(models, strategies, seeds, task_of, tasks, knobs, device, budget: TuneBudget, source_features=None,
+              threads: int = 0):
+    """The (strategy, seed, task) job grid (tuner.cpp:307-374): job j on models[j]; tasks = [(task_id, task)],
+    every task over the same knob template. Returns [TaskResult]."""
+    keep = []
+    n = len(models)
+    ts = (_TaskSpec * max(1, len(tasks)))(*[_c_task(tid, t, knobs, keep) for tid, t in tasks])
+    res = [_alloc_result(budget, len(knobs)) for _ in range(n)]
+    rs = (_TaskResult * max(1, n))(*[r for r, _ in res])
+    hs = (C.c_void_p * max(1, n))(*[m.h for m in models])
+    st = np.ascontiguousarray(strategies, dtype=np.int32)
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    to = np.ascontiguousarray(task_of, dtype=np.int32)
+    src = None if source_features is None else np.ascontiguousarray(source_features, dtype=np.float64)
+    _ck(lib().moses_tune_jobs(n, C.cast(hs, C.c_void_p), _p(st), _p(sd), _p(to), C.cast(ts, C.c_void_p), len(tasks),
+                              C.byref(_c_device(device)), C.byref(budget._c()), _p(src),
+                              0 if src is None else src.shape[0], threads, C.cast(rs, C.c_void_p)))
+    return [_result(rs[j], res[j][1]) for j in range(n)]

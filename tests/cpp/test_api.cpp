@@ -210,6 +210,34 @@ int main() {
     bad.survivors = 500;
     expect_error(ErrorCode::InvalidConfig, [&] { evolve(m, t, bad); });
   }
+  // test_tuner.cpp:139-203: tune_task's budget is conserved (measured + predicted + unspent = trials), the
+  // best latency is the minimum of the measured ones, and the plan rejects infeasible splits
+  {
+    TaskSpec t{"conv3x3_64", 2.0, 8.0, 9.0, 5.0, default_knob_template()};
+    DeviceSpec d{"toy", 1000.0, 16.0, 8.0, 1e6, 1.0, 0.05, 3};
+    TuneBudget b;
+    b.trials_per_task = 20;
+    b.num_batches = 4;
+    b.search.population = 32;
+    b.search.generations = 1;
+    b.search.survivors = 8;
+    b.search.mutation_count = 3;
+    b.adversary = false;
+    for (StrategyKind s : {StrategyKind::Raw, StrategyKind::PretrainOnly, StrategyKind::VanillaFinetune,
+                           StrategyKind::Moses}) {
+      DeviceModel m(init_random({16, 64, 64, 1}, 7), MOSES_PREC_TF32, 512);
+      const TaskResult r = tune_task(s, m, d, t, b, 3);
+      CHECK(r.trace.measured_trials + r.trace.prediction_trials + r.trace.unspent_trials == b.trials_per_task);
+      double best = 1e300;
+      for (const auto& rec : r.records) best = std::min(best, rec.latency_ms);
+      CHECK(!r.records.empty() && best == r.best_latency_ms);
+    }
+    TuneBudget bad = b;
+    bad.trials_per_task = 8;
+    bad.train_fraction = 0.4;
+    DeviceModel m(init_random({16, 64, 64, 1}, 7), MOSES_PREC_TF32, 512);
+    expect_error(ErrorCode::InfeasibleSplit, [&] { tune_task(StrategyKind::VanillaFinetune, m, d, t, bad, 3); });
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -12,7 +12,7 @@ L = ml.lib()
 cluster = "--grid" not in sys.argv
 L.moses_debug_set_rank_grid(0 if cluster else 1)  # 0: default policy
 dims = [164, 512, 512, 512, 512, 1]
-dm = ml.DeviceModel(ml.init_random(dims, 1, strict=False), ml.PREC_BF16, 4096)
+dm = ml.DeviceModel(ml.init_random(dims, 1, strict=False), getattr(ml, "PREC_" + (sys.argv[sys.argv.index("--prec") + 1] if "--prec" in sys.argv else "BF16X3")), 4096)
 off = ml.synth_offsets(3, 512, 8)
 x = np.random.default_rng(0).random((int(off[-1]), 164))
 y = 0.1 + np.random.default_rng(1).random(512)
