@@ -416,9 +416,9 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     fail(MOSES_ERR_INVALID_ARG, "split-operand handles take inputs through their packed buffers");
   if (m->bsplit() && !chain_ok(m))
     fail(MOSES_ERR_INVALID_ARG, "split-bf16 handles need hidden widths of 512 and input width <= 512");
-  if (chain_ok(m) && R > 0 && (R <= kChainMaxRows || m->bsplit())) {
-    // split-bf16: the fused chain is its only GEMM path; rows are independent, so any R runs as
-    // row chunks of at most kChainMaxRows
+  if (chain_ok(m) && R > 0 && R <= kChainMaxRows) {
+    // the fused chain: a latency design for training batches; above kChainMaxRows rows (candidate-pool
+    // scoring) the layers run one by one on the throughput kernels (split bf16: umma_fwd_pair_split)
     const void* x0_lo = m->x0_lo(x0);
     for (long long r0 = 0; r0 < R; r0 += kChainMaxRows) {
       const long long Rc = std::min(kChainMaxRows, R - r0);
@@ -463,7 +463,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     c.M = int(R);
     c.N = m->dims[l + 1];
     c.K = m->dims[l];
-    c.A = {l == 0 ? x0 : m->act[l], l == 0 ? ldx0 : m->ld[l], false, m->act_lo(l)};
+    c.A = {l == 0 ? x0 : m->act[l], l == 0 ? ldx0 : m->ld[l], false, l == 0 ? m->x0_lo(x0) : m->act_lo(l)};
     c.B = {m->wop(l), m->dims[l + 1], true, m->wop_lo(l)};
     c.epi = EpiKind::Fwd;
     const bool last = l + 2 == m->L;
@@ -472,7 +472,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     c.bias = m->bias(l);
     c.relu = 1;
     c.round_out = !last;  // the last hidden layer is never a GEMM operand: keep it full fp32
-    if (!last) c.out_lo = m->act_lo(l + 1);
+    if (!last || (m->bsplit() && c.out != nullptr)) c.out_lo = m->act_lo(l + 1);  // split bf16 keeps both planes
     if (last) {
       c.head_w = m->head_w();
       c.head_u = head_u;

@@ -252,6 +252,57 @@ void launch_pair(const GemmCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, a, tiles_m2));
 }
 
+// split-bf16 scoring layers, N % 128 == 0, K <= 512 (gemm_fwd2.cuh umma_fwd_pair_split)
+void launch_pair_split(const GemmCall& c, cudaStream_t s) {
+  using Cfg = PairSplitCfg;
+  auto kern = umma_fwd_pair_split;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+  });
+  if (c.out != nullptr && c.out_lo == nullptr) fail(MOSES_ERR_INVALID_ARG, "split pair layer output without a lo plane");
+  const Operand alo{c.A.lo, c.A.ld, c.A.mn_major}, blo{c.B.lo, c.B.ld, c.B.mn_major};
+  // activations: 32-column K-blocks with 64-byte rows (SWIZZLE_64B), see PairSplitCfg
+  const CUtensorMap ta = make_map(c.A.ptr, 2, c.K, c.M, c.A.ld, Cfg::BKA, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap ta_lo = make_map(alo.ptr, 2, c.K, c.M, c.A.ld, Cfg::BKA, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap tb = operand_map(c.B, 2, c.N, c.K, 64);
+  const CUtensorMap tb_lo = operand_map(blo, 2, c.N, c.K, 64);
+  const CUtensorMap tc = c.out ? make_map(c.out, 2, c.N, c.M, c.ldo, 64, 32) : ta;
+  const CUtensorMap tc_lo = c.out ? make_map(c.out_lo, 2, c.N, c.M, c.ldo, 64, 32) : ta;
+  GemmArgs a{};
+  a.M = c.M;
+  a.N = c.N;
+  a.K = c.K;
+  a.out = c.out;
+  a.ldo = c.ldo;
+  a.bias = c.bias;
+  a.relu = c.relu;
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.mn_layout = g_mn_layout[0];
+  a.mn_sbo = g_mn_sbo[0];
+  a.mn_kstep = g_mn_kstep[0];
+  const int tiles_m2 = ceil_div(c.M, 2 * Cfg::BM);
+  const int groups = c.N / 128;  // pair groups per m tile (4 at N = 512)
+  if (groups != 4) fail(MOSES_ERR_INVALID_ARG, "split pair layer: N = 512");
+  int pairs = std::min(g_num_sms / 2, groups * tiles_m2);
+  pairs -= pairs % groups;  // every column quarter gets the same number of pairs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, ta_lo, tb, tb_lo, tc, tc_lo, a, tiles_m2));
+}
+
 template <bool BMN, int EPI>
 void launch_c(const GemmCall& c, cudaStream_t s) {
   auto kern = umma_gemm_cluster<BMN, EPI>;
@@ -606,6 +657,13 @@ int launch_gemm(int elem, const GemmCall& c, cudaStream_t s) {
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
       g_num_sms = n;
     sm_init = true;
+  }
+  if (elem == 2 && (c.A.lo != nullptr || c.B.lo != nullptr)) {  // split bf16: the weight-resident pair layer
+    if (!c.A.lo || !c.B.lo || c.epi != EpiKind::Fwd || c.A.mn_major || !c.B.mn_major || c.N != 512 ||
+        c.K > PairSplitCfg::kMaxK || (c.ldo * 2) % 16 != 0)
+      fail(MOSES_ERR_INVALID_ARG, "split-bf16 GEMMs: forward layers of width 512 with K <= 512");
+    launch_pair_split(c, s);
+    return 64;  // head partials per 64-column slice
   }
   if (c.A.lo != nullptr || c.B.lo != nullptr) {  // 3xTF32: both operands split, non-persistent kernel
     if (elem != 4 || !c.A.lo || !c.B.lo) fail(MOSES_ERR_INVALID_ARG, "3xTF32 needs fp32 hi/lo operands");

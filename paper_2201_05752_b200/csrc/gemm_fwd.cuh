@@ -32,9 +32,13 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // columns starting at output column nb0 (TMEM address t_acc). bias + ReLU + head dots in registers,
 // the bf16 activations through a 32 x 64 SW128 staging box and one TMA store per box; head partials
 // go to head_part[head_tile * head_ld + m]. `release` runs once the accumulator is in registers.
-template <int kHalf, typename Release>
+// SPLIT (split bf16, gemm_fwd2.cuh umma_fwd_pair_split): the activations leave as a hi / lo pair
+// (hi = rn(v), lo = rn(v - hi)) through the one staging box: hi stored, box drained, lo stored (tmC_lo).
+// (Measured: per-thread direct row stores instead made the layer 1.4x slower than its mainloop.)
+template <int kHalf, bool SPLIT = false, typename Release>
 __device__ __forceinline__ void fwd_epi_tile(const GemmArgs& args, const CUtensorMap* tmC, uint8_t* stg, uint32_t t_acc,
-                                             int m0, int quarter, int nb0, int head_tile, Release&& release) {
+                                             int m0, int quarter, int nb0, int head_tile, Release&& release,
+                                             const CUtensorMap* tmC_lo = nullptr) {
   using namespace fwd_detail;
   const int lane = int(threadIdx.x & 31);
   const int m = m0 + quarter * 32 + lane;
@@ -79,7 +83,32 @@ __device__ __forceinline__ void fwd_epi_tile(const GemmArgs& args, const CUtenso
 #pragma unroll
       for (int j = 0; j < 64; ++j) hp2 = fmaf(v[j], (full || nb + j < args.N) ? __ldg(args.head_u + nb + j) : 0.f, hp2);
     }
-    if (store) {
+    if (store && SPLIT) {
+#pragma unroll
+      for (int plane = 0; plane < 2; ++plane) {  // hi box, then (box drained) lo box
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        uint8_t* srow = stg + lane * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 pk;
+          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x0 = v[8 * c + 2 * e], x1 = v[8 * c + 2 * e + 1];
+            const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+            p2[e] = plane == 0 ? h : __floats2bfloat162_rn(x0 - __low2float(h), x1 - __high2float(h));
+          }
+          *reinterpret_cast<uint4*>(srow + ((c ^ (lane & 7)) << 4)) = pk;  // SW128: chunk ^ (row % 8)
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(plane == 0 ? tmC : tmC_lo, stg, nb, m0 + quarter * 32);  // rows >= M / cols >= N clipped
+          bulk_commit();
+        }
+      }
+    } else if (store) {
       if (lane == 0) bulk_wait_read0();  // previous box has left the staging buffer
       __syncwarp();
       uint8_t* srow = stg + lane * 128;

@@ -260,3 +260,22 @@ def test_moses_step_vs_oracle(ml, orc):
     xi = np.abs(np.float32(w32) * np.float32(g)).astype(np.float64)
     want = orc.partition(xi, False, 2, 0.5)
     assert np.array_equal(np.asarray(mask.transferable, bool), np.asarray(want, bool))
+
+
+@pytest.mark.parametrize("dims", [CFG4, CFG2])
+def test_scoring_pair_layers_equal_the_chain(ml, orc, dims):
+    """Above 16K rows a split-bf16 handle scores layer by layer on the weight-resident CTA pairs
+    (gemm_fwd2.cuh umma_fwd_pair_split) instead of the fused chain: the same products in the same
+    K order, so the hidden activations are bit-identical; the scores differ only in how the head's
+    per-slice partial dots are grouped (64- vs 128-column slices)."""
+    n = 40000
+    p = ml.init_random(dims, 21, strict=False)
+    x = np.random.default_rng(4).random((n, dims[0]))
+    pair = ml.DeviceModel(p, ml.PREC_BF16X3, 65536)   # one 40K-row call: per-layer pair kernels
+    chain = ml.DeviceModel(p, ml.PREC_BF16X3, 16384)  # 16K-row chunks: the fused chain
+    h_pair, h_chain = ml.penultimate_activations(pair, x), ml.penultimate_activations(chain, x)
+    assert np.array_equal(h_pair, h_chain)
+    s_pair, s_chain = ml.predict(pair, x), ml.predict(chain, x)
+    assert nrel(s_pair, s_chain) < 1e-6
+    ref, _ = orc.forward(dims, p.params, x[:5000], threads=8)
+    assert nrel(s_pair[:5000], ref) < TOL_PRED
