@@ -480,8 +480,15 @@ MOSES_API int moses_records_export(moses_records_t r, int32_t* task_index, int32
                                   int64_t* values, double* throughput, double* latency, double* wall_cost,
                                   uint64_t* seq);
 /* Test hook: force the fused ranking step's grid form (1) instead of the default policy (0:
- * 16-CTA cluster form when the batch fits it, else the grid form). */
+ * 16-CTA cluster form when the batch fits it, else the symmetric form, else the grid form). */
 MOSES_API int moses_debug_set_rank_grid(int32_t on);
+/* Test hook: allow (1, default) or disable (0) the ranking step's symmetric form (each pair once). */
+MOSES_API int moses_debug_set_rank_sym(int32_t on);
+/* Test hooks: split-bf16 weight gradients split over the batch rows in clusters (1, default) or one
+ * CTA per tile (0); splits > 0 forces the cluster width. Probe: TMEM promotion interval in 64-row
+ * k-blocks (0 = default) and an optional device buffer of clock64 / globaltimer stamps. */
+MOSES_API int moses_debug_set_wgrad_sk(int on, int splits);
+MOSES_API int moses_debug_wgrad_sk_probe(int kc, void* trace);
 /* Test hook: force the sequential sampling walk in moses_generate_dataset_device. */
 MOSES_API int moses_debug_force_serial_sampling(int32_t on);
 

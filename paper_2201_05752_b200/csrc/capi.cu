@@ -257,6 +257,7 @@ struct moses_model {
     long long graph_kernels = 0;
   } plan;
   float* gbias = nullptr;          // pooled head-bias gradient (device scalar)
+  float* wgsk_ws = nullptr;        // split bf16: L2 workspace of the split-K weight-gradient reduction
   float* mmd_g = nullptr;          // MMD loss: d MMD^2 / dH of every row (cap x W)
   double* mmd_v = nullptr;         // MMD loss: per-row value partials (cap)
   // data parallel (moses_model_set_comm): 1 = average the gradients of every rank's own batch
@@ -345,7 +346,7 @@ struct moses_model {
     for (void* p : {(void*)w, (void*)mom, (void*)g, (void*)xi, (void*)m1, (void*)m2, (void*)mask, (void*)wbf, (void*)wtf,
                     (void*)head_part, (void*)head_part2, (void*)scores, (void*)labels, (void*)coefA, (void*)coefB,
                     (void*)rank.gs_part, (void*)rank.loss_part, (void*)rank.pairs_part, (void*)dscal, (void*)dpairs,
-                    (void*)dcount, sel_base, (void*)staging, (void*)adv_ws})
+                    (void*)dcount, sel_base, (void*)staging, (void*)adv_ws, (void*)wgsk_ws})
       dfree(p);
     for (void* p : act) dfree(p);
     for (void* p : dz) dfree(p);
@@ -598,6 +599,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     wc.n = L - 1;
     wc.K = int(R);
     wc.split = m->bsplit();
+    wc.sk_ws = m->wgsk_ws;
     if (fuse) {
       wc.counter = fuse->counter;
       wc.loss_src = fuse->loss_src;
@@ -821,8 +823,8 @@ bool gradients_core(moses_model* m, const void* x0, long long ldx0, const float*
   dispatch_forward(m, x0, ldx0, R, u, true);
   if (!active && !mmd_on && g_rank_fused) {
     if (!m->rank_ticket) {
-      m->rank_ticket = dalloc<unsigned int>(1);
-      MOSES_CUDA(cudaMemsetAsync(m->rank_ticket, 0, sizeof(unsigned int), m->st));
+      m->rank_ticket = dalloc<unsigned int>(4);  // [grid-form ticket, symmetric form: count, generation, ticket]
+      MOSES_CUDA(cudaMemsetAsync(m->rank_ticket, 0, 4 * sizeof(unsigned int), m->st));
     }
   }
   bool ranked = false;
@@ -1097,6 +1099,7 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->stage_w = std::max<long long>(maxw, 1) + 1;
     m->staging = dalloc<double>(m->cap * m->stage_w);
     m->gbias = dalloc<float>(4);
+    if (m->bsplit()) m->wgsk_ws = dalloc<float>(wgrad_sk_ws_bytes() / sizeof(float));
     m->seg_off = dalloc<long long>(m->cap + 1);
     m->seg_rows = dalloc<int>(m->cap);
     m->adv_ws = dalloc<float>(round_up(m->cap, 64) + round_up(maxw + 1, 64) + 64 + 16 +
@@ -3452,6 +3455,10 @@ MOSES_API int moses_debug_set_rank_grid(int32_t on) {
   debug_set_rank_grid(on != 0);
   return MOSES_OK;
 }
+MOSES_API int moses_debug_set_rank_sym(int32_t on) {
+  debug_set_rank_sym(on != 0);
+  return MOSES_OK;
+}
 MOSES_API int moses_debug_force_serial_sampling(int32_t on) {
   debug_force_serial_sampling(on != 0);
   return MOSES_OK;
@@ -3661,7 +3668,11 @@ extern int g_cluster;
 namespace moses {
 extern unsigned long long* g_chain_trace;
 }
-namespace moses { void rank_trace_read(unsigned long long* out); }
+namespace moses { void rank_trace_read(unsigned long long* out); void rank_cta_trace_read(unsigned long long* out); }
+// rank_sym_kernel per-CTA stamps: 512 x {start, scores, pairs, grid sync, rows} (globaltimer ns)
+extern "C" MOSES_API int moses_debug_rank_cta_trace(unsigned long long* out2560) {
+  return guarded([&] { moses::rank_cta_trace_read(out2560); });
+}
 extern "C" MOSES_API int moses_debug_rank_trace(unsigned long long* out16) {
   return guarded([&] { moses::rank_trace_read(out16); });
 }
@@ -3676,6 +3687,20 @@ extern "C" MOSES_API int moses_debug_set_chain_trace(void* dev_buf) {
 }
 extern "C" MOSES_API int moses_debug_set_group(int on) {
   moses::g_group = on;
+  return 0;
+}
+// split-bf16 weight gradients: 1 = split over K in clusters (gemm_wgrad_sk.cuh), 0 = one CTA per
+// 128 x 64 tile (gemm_group.cuh); splits > 0 forces the cluster width
+extern "C" MOSES_API int moses_debug_set_wgrad_sk(int on, int splits) {
+  moses::g_wgrad_sk = on;
+  moses::g_wgrad_sk_splits = splits;
+  return 0;
+}
+// experiments: TMEM promotion interval (k-blocks of 64 rows; 0 = default) and a device buffer of
+// 131 u64 clock64 stamps of block 0 (nullptr: off)
+extern "C" MOSES_API int moses_debug_wgrad_sk_probe(int kc, void* trace) {
+  moses::g_wgrad_sk_kc = kc;
+  moses::g_wgrad_sk_trace = static_cast<unsigned long long*>(trace);
   return 0;
 }
 extern "C" MOSES_API int moses_debug_set_chain(int on) {

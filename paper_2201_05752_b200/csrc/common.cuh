@@ -127,9 +127,15 @@ struct WgradGroupCall {
   const double* loss_src = nullptr;
   double* loss_acc = nullptr;
   double* loss_copy = nullptr;
+  float* sk_ws = nullptr;  // split-bf16: L2 workspace of the split-K reduction (wgrad_sk_ws_bytes())
 };
+size_t wgrad_sk_ws_bytes();
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
 extern int g_group;
+extern int g_wgrad_sk;
+extern int g_wgrad_sk_splits;
+extern int g_wgrad_sk_kc;
+extern unsigned long long* g_wgrad_sk_trace;
 extern int g_rank_fused;  // rank_step (one launch) instead of rank_pairs + rank_finalize
 extern int g_chain;  // fused chain enabled (moses_debug_set_chain)
 

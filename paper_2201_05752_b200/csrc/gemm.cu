@@ -15,6 +15,7 @@
 #include "mlp_chain.cuh"
 #include "mlp_chain_split.cuh"
 #include "gemm_group.cuh"
+#include "gemm_wgrad_sk.cuh"
 
 namespace moses {
 // MN-major operand encoding (index 0 = bf16, 1 = tf32). 16-bit operands use the plain 128-byte
@@ -448,6 +449,109 @@ void launch_group_t(const WgradGroupCall& c, cudaStream_t s) {
     MOSES_CUDA(cudaLaunchKernelEx(&cfg, wgrad_group_kernel<UPDATE>, static_cast<const GroupMaps&>(maps), a));
 }
 
+// Split-bf16 weight gradients split over the batch rows in clusters of S CTAs (gemm_wgrad_sk.cuh).
+// S is the largest cluster width in 1..8 that still fits every CTA in one wave (the occupancy API's
+// active-cluster count for this kernel) and minimises the 128-row chunks per CTA.
+template <bool UPDATE>
+void launch_wgrad_sk_t(const WgradGroupCall& c, cudaStream_t s) {
+  using C = WgskCfg;
+  auto kern = wgrad_sk_kernel<UPDATE>;
+  static std::once_flag once;
+  static int max_clusters[9] = {};
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    for (int S = 1; S <= 8; ++S) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(S * 16);
+      q.blockDim = dim3(C::kThreads);
+      q.dynamicSmemBytes = C::kSmemBytes;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = unsigned(S);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = 0;
+      }
+      max_clusters[S] = n;
+    }
+  });
+  GroupMapsSplit maps;
+  WgskArgs a{};
+  GroupArgs& ga = a.ga;
+  ga.n = c.n;
+  ga.K = c.K;
+  int tiles = 0;
+  for (int l = 0; l < c.n; ++l) {
+    if (!c.a_lo[l] || !c.b_lo[l] || (c.update && !c.shadow_lo[l]))
+      fail(MOSES_ERR_INVALID_ARG, "split wgrad needs the lo planes");
+    maps.a[l] = make_map(c.a[l], 2, c.M[l], c.K, c.lda[l], 64, C::BK);
+    maps.b[l] = make_map(c.b[l], 2, c.N[l], c.K, c.ldb[l], 64, C::BK);
+    maps.a_lo[l] = make_map(c.a_lo[l], 2, c.M[l], c.K, c.lda[l], 64, C::BK);
+    maps.b_lo[l] = make_map(c.b_lo[l], 2, c.N[l], c.K, c.ldb[l], 64, C::BK);
+    const int dims = c.M[l] - 1;  // the last G row is the bias (ones column of act_l)
+    a.bias_sep[l] = (dims % C::BM) == 0;
+    a.Mg[l] = a.bias_sep[l] ? dims : c.M[l];
+    a.bias_row[l] = dims;
+    {  // bias columns per m-tile: spread over the level's m-tiles when they divide the tile evenly
+      const int mt = ceil_div(a.Mg[l], C::BM);
+      a.bias_w[l] = (C::BN % (2 * mt) == 0) ? C::BN / mt : C::BN;
+    }
+    ga.tile_begin[l] = tiles;
+    ga.tiles_n[l] = ceil_div(c.N[l], C::BN);
+    ga.M[l] = c.M[l];
+    ga.N[l] = c.N[l];
+    ga.g[l] = c.g[l];
+    ga.w[l] = c.w[l];
+    ga.mom[l] = c.mom[l];
+    ga.shadow[l] = static_cast<__nv_bfloat16*>(c.shadow[l]);
+    ga.shadow_lo[l] = static_cast<__nv_bfloat16*>(c.shadow_lo[l]);
+    tiles += ceil_div(a.Mg[l], C::BM) * ga.tiles_n[l];
+  }
+  ga.tile_begin[c.n] = tiles;
+  ga.lr = c.lr;
+  ga.mu = c.mu;
+  ga.counter = c.counter;
+  ga.loss_src = c.loss_src;
+  ga.loss_acc = c.loss_acc;
+  ga.loss_copy = c.loss_copy;
+  a.kc = g_wgrad_sk_kc > 0 ? g_wgrad_sk_kc : C::kChunkKb;
+  a.trace = g_wgrad_sk_trace;
+  const int chunks = ceil_div(c.K, C::BK * a.kc);
+  int S = 1, best = chunks;
+  for (int cand = 2; cand <= 8; ++cand) {
+    if (cand > chunks || (long long)tiles > (long long)max_clusters[cand]) continue;
+    const int per = ceil_div(chunks, cand);
+    if (per < best) {
+      best = per;
+      S = cand;
+    }
+  }
+  if (g_wgrad_sk_splits > 0) S = std::min(g_wgrad_sk_splits, std::max(1, chunks));
+  if (S > 1 && (c.sk_ws == nullptr || (long long)tiles * S > kWgskMaxCtas)) S = 1;
+  a.S = S;
+  a.ws = c.sk_ws;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles * S);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = unsigned(S);
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+}
+
 template <typename T, int BN>
 void dispatch_persistent(const GemmCall& c, cudaStream_t s) {
   const bool am = c.A.mn_major, bm = c.B.mn_major;
@@ -572,11 +676,19 @@ int g_cluster = 1;     // weight-resident cluster kernel for the 512-wide hidden
 int g_chain = 1;
 unsigned long long* g_chain_trace = nullptr;
 int g_group = 1;
+int g_wgrad_sk = 1;          // split-bf16 wgrad split over K in clusters (gemm_wgrad_sk.cuh)
+int g_wgrad_sk_splits = 0;   // > 0: force the cluster width (tests)
+int g_wgrad_sk_kc = 0;       // > 0: k-blocks per TMEM promotion chunk (experiments)
+unsigned long long* g_wgrad_sk_trace = nullptr;
 int g_rank_fused = 1;
+size_t wgrad_sk_ws_bytes() { return size_t(kWgskMaxCtas) * kSlotFloats * sizeof(float); }
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s) {
   if (c.K <= 0 || c.n <= 0) return;
   if (c.n > kGroupMax) fail(MOSES_ERR_INVALID_ARG, "too many levels for the grouped wgrad");
-  if (c.split) {
+  if (c.split && g_wgrad_sk) {
+    if (c.update) launch_wgrad_sk_t<true>(c, s);
+    else launch_wgrad_sk_t<false>(c, s);
+  } else if (c.split) {
     if (c.update) launch_group_t<true, true>(c, s);
     else launch_group_t<false, true>(c, s);
   } else {

@@ -470,6 +470,14 @@ __global__ void __launch_bounds__(kFinBlock) rank_finalize_kernel(const double* 
 // knows 1/pairs and writes the backward coefficients of its programs' statement rows itself;
 // CTA 0 sums the loss / bias partials in CTA order. Deterministic.
 __device__ unsigned long long g_rank_trace[16];
+__device__ unsigned long long g_rank_cta_trace[512 * 5];  // rank_sym_kernel: per-CTA phase stamps
+__device__ __forceinline__ void rank_cta_stamp(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < 512) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_rank_cta_trace[blockIdx.x * 5 + k] = v;
+  }
+}
 __device__ __forceinline__ void rank_stamp(int k) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long v;
@@ -695,33 +703,13 @@ __global__ void __launch_bounds__(kRankThreads)
 // per-row sums (split order, double) to global; the last CTA to finish (self re-arming ticket)
 // reduces the rows in row order and writes loss, pair count, head-bias gradient and every
 // statement row's backward coefficient. Deterministic and independent of the grid size.
-constexpr int kRgThreads = 512;
-__global__ void __launch_bounds__(kRgThreads)
-    rank_grid_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hbp,
-                     const long long* __restrict__ seg, const int* __restrict__ seg_of_row, const float* __restrict__ y,
-                     long long n, int nsplit, int rows_per_cta, float* __restrict__ s_out, long long R,
-                     double* __restrict__ row_g, double* __restrict__ row_l, long long* __restrict__ row_p,
-                     unsigned int* ticket, double* loss_out, long long* pairs_out, float* __restrict__ coefA,
-                     float* __restrict__ coefB, float* gb_out) {
-  extern __shared__ float rg_smem[];
-  const int items = rows_per_cta * nsplit;
-  float* ss = rg_smem;  // [n] scores
-  float* sy = ss + n;   // [n] labels
-  float* pg = sy + n;   // [items] per-(split, row) partials
-  float* pl = pg + items;
-  int* pp = reinterpret_cast<int*>(pl + items);
-  float* srow = reinterpret_cast<float*>(pp + items);  // pooled: statement-row head dots [R]
-  long long* sseg = reinterpret_cast<long long*>(
-      (reinterpret_cast<uintptr_t>(srow + (seg ? R : 0)) + 7) & ~uintptr_t(7));  // pooled: CSR offsets [n+1]
-  double* sg = reinterpret_cast<double*>(sseg + (seg ? n + 1 : 0));           // last CTA: row sums [n]
-  __shared__ bool is_last;
-  __shared__ double wl[kRgThreads / 32], wg[kRgThreads / 32];
-  __shared__ long long wp[kRgThreads / 32];
+// Every score of the batch into shared memory ss[n] (rank_grid_kernel / rank_sym_kernel prologue):
+// fixed tile order per statement row, then the segment sum (score_of()'s arithmetic); loads are
+// issued 4 rows x 8 tiles at a time (one L2 round trip for ~2K rows). Pooled: srow[R] / sseg[n+1].
+__device__ __forceinline__ void rank_all_scores(const float* __restrict__ part, int ntiles, long long ld, float hb,
+                                                const long long* __restrict__ seg, long long n, float* ss, float* srow,
+                                                long long* sseg) {
   const int t = threadIdx.x;
-  const float hb = hbp[0];
-  for (long long p = t; p < n; p += blockDim.x) sy[p] = y[p];
-  // all scores: fixed tile order per statement row, then the segment sum (score_of()'s arithmetic);
-  // loads are issued 4 rows x 8 tiles at a time (one L2 round trip for ~2K rows)
   auto row_dot = [&](long long r, long long r1, float* dst) {
     float v[4][8];
 #pragma unroll
@@ -770,6 +758,34 @@ __global__ void __launch_bounds__(kRgThreads)
         if (p + (long long)u * blockDim.x < n) ss[p + (long long)u * blockDim.x] = d[u] + hb;
     }
   }
+}
+
+constexpr int kRgThreads = 512;
+__global__ void __launch_bounds__(kRgThreads)
+    rank_grid_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hbp,
+                     const long long* __restrict__ seg, const int* __restrict__ seg_of_row, const float* __restrict__ y,
+                     long long n, int nsplit, int rows_per_cta, float* __restrict__ s_out, long long R,
+                     double* __restrict__ row_g, double* __restrict__ row_l, long long* __restrict__ row_p,
+                     unsigned int* ticket, double* loss_out, long long* pairs_out, float* __restrict__ coefA,
+                     float* __restrict__ coefB, float* gb_out) {
+  extern __shared__ float rg_smem[];
+  const int items = rows_per_cta * nsplit;
+  float* ss = rg_smem;  // [n] scores
+  float* sy = ss + n;   // [n] labels
+  float* pg = sy + n;   // [items] per-(split, row) partials
+  float* pl = pg + items;
+  int* pp = reinterpret_cast<int*>(pl + items);
+  float* srow = reinterpret_cast<float*>(pp + items);  // pooled: statement-row head dots [R]
+  long long* sseg = reinterpret_cast<long long*>(
+      (reinterpret_cast<uintptr_t>(srow + (seg ? R : 0)) + 7) & ~uintptr_t(7));  // pooled: CSR offsets [n+1]
+  double* sg = reinterpret_cast<double*>(sseg + (seg ? n + 1 : 0));           // last CTA: row sums [n]
+  __shared__ bool is_last;
+  __shared__ double wl[kRgThreads / 32], wg[kRgThreads / 32];
+  __shared__ long long wp[kRgThreads / 32];
+  const int t = threadIdx.x;
+  const float hb = hbp[0];
+  for (long long p = t; p < n; p += blockDim.x) sy[p] = y[p];
+  rank_all_scores(part, ntiles, ld, hb, seg, n, ss, srow, sseg);
   __syncthreads();
   const long long p0 = min(n, (long long)blockIdx.x * rows_per_cta);
   for (int it = t; it < items; it += blockDim.x) {  // same items / arithmetic as rank_cluster_kernel
@@ -870,6 +886,291 @@ __global__ void __launch_bounds__(kRgThreads)
     *pairs_out = P;
     if (gb_out != nullptr) *gb_out = P > 0 ? float(G * inv) : 0.f;
     *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+  }
+}
+
+// ---------------------------------------------------------------- fused ranking step, symmetric form
+// Large batches (cfg5: n = 4096, 8.4M pairs): every unordered pair is evaluated ONCE (the grid form
+// evaluates it from both rows). The upper triangle of the n x n pair matrix is cut into 32 x 32
+// tiles (bi <= bj), one warp per tile at a time: lane l holds row i = 32 bi + l and at step k meets
+// column j = 32 bj + ((l + k) & 31), so each of the 32 steps covers a rotated diagonal; the row term
+// -w*sigma stays in the lane, the column term +w*sigma is passed by one shuffle to the lane that
+// owns column j. Tile partials (32 row + 32 column floats, loss, pair count) go to global; after a
+// grid barrier (cooperative launch) row block b is reduced by CTA b % grid in a fixed term order
+// (row parts bj = b..nb-1, then column parts bi = 0..b), so coefficients are deterministic and
+// independent of the grid size; the last CTA (ticket) sums loss (tile order) and head-bias
+// gradient (CTA order). Same pair arithmetic as rank_grid_kernel (model.cpp:71-106).
+constexpr int kRsThreads = 1024, kRsWarps = kRsThreads / 32;
+__device__ __forceinline__ long long rs_tile_start(long long b, long long nb) { return b * nb - b * (b - 1) / 2; }
+__device__ __forceinline__ void rs_grid_sync(unsigned* bar) {  // bar[0] arrivals, bar[1] generation
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g0, arrived;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+    if (arrived == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      } while (g == g0);
+    }
+  }
+  __syncthreads();
+}
+// The 32 steps of one pair tile (see rank_sym_kernel). DIAG: only j > i; EDGE: columns past n.
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// The 32 steps of one pair tile (see rank_sym_kernel); sp[j] = (score, label). DIAG: only j > i;
+// EDGE: columns past n. Ties and invalid pairs have w = 0, hence d = 0 and c = 0. The softplus terms
+// log1p(e) of a lane's pairs are taken as one log of their product (32 factors in (1, 2]): 2 MUFU
+// ops per pair (exp, reciprocal) instead of 3.
+template <bool DIAG, bool EDGE>
+__device__ __forceinline__ void rs_tile_steps(const float2* sp, float si, float yi, bool vi, int il, int jb, int n32,
+                                              int lane, float& gr, float& gc, float& ls, float& pcf) {
+  float lp = 1.f;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const int jl = (lane + k) & 31;
+    int j = jb + jl;
+    bool valid = vi;
+    if (EDGE) {
+      valid = valid && j < n32;
+      j = min(j, n32 - 1);
+    }
+    if (DIAG) valid = valid && jl > il;
+    const float2 q = sp[j];
+    float w = float(yi > q.y) - float(yi < q.y);  // +1: i is the hi row, -1: j is, 0: tie
+    if (EDGE || DIAG || !vi) w = valid ? w : 0.f;
+    const float d = w * (si - q.x);               // s_hi - s_lo
+    const float e = ex2_ftz(fabsf(d) * -1.4426950408889634f);
+    const float iv = rcp_pair(1.f + e);
+    const float c = w * ((d >= 0.f ? e : 1.f) * iv);  // w * sigma(-d)
+    gr -= c;
+    gc += __shfl_sync(0xffffffffu, c, (lane - k) & 31);  // the term of the lane meeting column `lane`
+    ls += fmaxf(-d, 0.f);
+    lp *= fmaf(e, fabsf(w), 1.f);
+    pcf += fabsf(w);
+  }
+  ls += 0.69314718055994531f * lg2_ftz(lp);
+}
+__global__ void __launch_bounds__(kRsThreads, 1)
+    rank_sym_kernel(const float* __restrict__ part, int ntiles, long long ld, const float* __restrict__ hbp,
+                    const long long* __restrict__ seg, const float* __restrict__ y, long long n,
+                    float* __restrict__ s_out, long long R, float* __restrict__ rowcol, double* __restrict__ tile_loss,
+                    long long* __restrict__ tile_pairs, double* __restrict__ cta_gb, long long* __restrict__ cta_pairs,
+                    float* __restrict__ scores_g, unsigned* bar, double* loss_out, long long* pairs_out, float* __restrict__ coefA,
+                    float* __restrict__ coefB, float* gb_out) {
+  extern __shared__ float rsym_smem[];
+  float2* sp = reinterpret_cast<float2*>(rsym_smem);  // [n] (score, label)
+  float* ss = rsym_smem;                              // reused after the pairs: CTA partials
+  __shared__ double wsum[kRsWarps][32];
+  __shared__ long long wpairs[kRsWarps];
+  __shared__ double red[kRsWarps];
+  __shared__ long long redp[kRsWarps];
+  __shared__ bool is_last;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const float hb = hbp[0];
+  rank_stamp(8);
+  rank_cta_stamp(0);
+  // ---- every score of the batch, in every CTA (score_of()'s arithmetic: fixed tile order per statement
+  // row, then the segment sum); 4 programs' tile partials in flight per thread
+  for (long long p0 = t; p0 < n; p0 += 4LL * blockDim.x) {
+    float acc[4];
+    if (seg == nullptr) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+          const long long p = p0 + (long long)u * blockDim.x;
+          v[u][tt] = (p < n && tt < ntiles) ? __ldg(part + tt * ld + p) : 0.f;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        float a = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt)
+          if (tt < ntiles) a += v[u][tt];
+        for (int tt = 8; tt < ntiles; ++tt) a += p < n ? __ldg(part + tt * ld + p) : 0.f;
+        acc[u] = a;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        float a = 0.f;
+        if (p < n)
+          for (long long r = seg[p]; r < seg[p + 1]; ++r) {
+            float d = 0.f;
+            for (int tt = 0; tt < ntiles; ++tt) d += __ldg(part + tt * ld + r);
+            a += d;
+          }
+        acc[u] = a;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long p = p0 + (long long)u * blockDim.x;
+      if (p < n) {
+        sp[p] = make_float2(acc[u] + hb, y[p]);
+        if (s_out != nullptr && blockIdx.x == 0) s_out[p] = acc[u] + hb;
+      }
+    }
+  }
+  __syncthreads();
+  rank_stamp(9);
+  rank_cta_stamp(1);
+
+  // ---- pair tiles
+  const long long nb = (n + 31) / 32;
+  const long long T = nb * (nb + 1) / 2;
+  long long my_pairs = 0;
+  // CTA c: tiles [c*T/G, (c+1)*T/G) (balanced per SM), its warps round-robin over them
+  const long long tb0 = (long long)blockIdx.x * T / gridDim.x, tb1 = (long long)(blockIdx.x + 1) * T / gridDim.x;
+  for (long long tile = tb0 + warp; tile < tb1; tile += kRsWarps) {
+    const double q = double(2 * nb + 1);
+    long long bi = (long long)floor((q - sqrt(q * q - 8.0 * double(tile))) * 0.5);
+    bi = max(0LL, min(bi, nb - 1));
+    while (bi > 0 && rs_tile_start(bi, nb) > tile) --bi;
+    while (bi + 1 < nb && rs_tile_start(bi + 1, nb) <= tile) ++bi;
+    const long long bj = bi + (tile - rs_tile_start(bi, nb));
+    const int n32 = int(n), i = int(bi) * 32 + lane, jb = int(bj) * 32;
+    const bool vi = i < n32;
+    const float2 qi = sp[vi ? i : 0];
+    const float si = qi.x, yi = qi.y;
+    float gr = 0.f, gc = 0.f, ls = 0.f, pcf = 0.f;
+    if (bi != bj && jb + 32 <= n32 && bi * 32 + 32 <= n32)
+      rs_tile_steps<false, false>(sp, si, yi, true, lane, jb, n32, lane, gr, gc, ls, pcf);
+    else if (bi != bj) rs_tile_steps<false, true>(sp, si, yi, vi, lane, jb, n32, lane, gr, gc, ls, pcf);
+    else rs_tile_steps<true, true>(sp, si, yi, vi, lane, jb, n32, lane, gr, gc, ls, pcf);
+    const int pc = int(pcf);
+    rowcol[tile * 64 + lane] = gr;
+    rowcol[tile * 64 + 32 + lane] = gc;
+    double l = ls;
+    long long pcl = pc;
+    for (int o = 16; o > 0; o >>= 1) {
+      l += __shfl_down_sync(0xffffffffu, l, o);
+      pcl += __shfl_down_sync(0xffffffffu, pcl, o);
+    }
+    if (lane == 0) {
+      tile_loss[tile] = l;
+      tile_pairs[tile] = pcl;
+      my_pairs += pcl;
+    }
+  }
+  if (lane == 0) wpairs[warp] = my_pairs;
+  __syncthreads();
+  if (t == 0) {
+    long long cp = 0;
+    for (int w = 0; w < kRsWarps; ++w) cp += wpairs[w];
+    cta_pairs[blockIdx.x] = cp;
+  }
+  rank_stamp(10);
+  rank_cta_stamp(2);
+  rs_grid_sync(bar);
+  rank_stamp(11);
+  rank_cta_stamp(3);
+
+  // ---- total pair count (integers: any order), then this CTA's row blocks
+  // every CTA's pair count loaded once per thread in parallel (integers: any order), block-reduced
+  long long pl = 0;
+  for (int b = t; b < int(gridDim.x); b += blockDim.x) pl += __ldcg(cta_pairs + b);
+  for (int o = 16; o > 0; o >>= 1) pl += __shfl_down_sync(0xffffffffu, pl, o);
+  if (lane == 0) redp[warp] = pl;
+  __syncthreads();
+  long long P = 0;
+  for (int w = 0; w < kRsWarps; ++w) P += redp[w];
+  const double inv = P > 0 ? 1.0 / double(P) : 0.0;
+  double gb_local = 0.0;  // sum of this CTA's rows' gs (row-block order, then rows)
+  for (long long b = blockIdx.x; b < nb; b += gridDim.x) {
+    // nb + 1 terms: row parts of tiles (b, bj), bj = b..nb-1, then column parts of (bi, b), bi = 0..b;
+    // warp w takes a contiguous run of them, the runs are added in warp order
+    const long long terms = nb + 1, per = (terms + kRsWarps - 1) / kRsWarps;
+    const long long q0 = warp * per, q1 = min(terms, q0 + per);
+    double acc = 0.0;
+    const long long rows_n = nb - b;
+    for (long long qa = q0; qa < q1; qa += 8) {  // 8 loads in flight, added in term order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long qq = qa + u;
+        v[u] = qq >= q1 ? 0.f
+               : qq < rows_n ? __ldcg(rowcol + (rs_tile_start(b, nb) + qq) * 64 + lane)
+                             : __ldcg(rowcol + (rs_tile_start(qq - rows_n, nb) + (b - (qq - rows_n))) * 64 + 32 + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (qa + u < q1) acc += double(v[u]);
+    }
+    wsum[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double g = 0.0;
+      for (int w = 0; w < kRsWarps; ++w) g += wsum[w][lane];
+      const long long i = b * 32 + lane;
+      if (i < n) {
+        const float a = P > 0 ? float(g * inv) : 0.f;
+        if (seg != nullptr) {
+          for (long long r = seg[i]; r < seg[i + 1]; ++r) {
+            coefA[r] = a;
+            coefB[r] = 0.f;
+          }
+        } else {
+          coefA[i] = a;
+          coefB[i] = 0.f;
+        }
+        gb_local += g;
+      }
+    }
+    __syncthreads();
+  }
+  if (seg != nullptr)  // padding statement rows outside the programs
+    for (long long r = (long long)blockIdx.x * blockDim.x + t; r < R; r += (long long)gridDim.x * blockDim.x)
+      if (r < seg[0] || r >= seg[n]) {
+        coefA[r] = 0.f;
+        coefB[r] = 0.f;
+      }
+  if (warp == 0) {
+    for (int o = 16; o > 0; o >>= 1) gb_local += __shfl_down_sync(0xffffffffu, gb_local, o);
+    if (lane == 0) cta_gb[blockIdx.x] = gb_local;
+  }
+  __threadfence();
+  __syncthreads();
+  rank_stamp(12);
+  rank_cta_stamp(4);
+  if (t == 0) is_last = atomicAdd(bar + 2, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // loss in tile order (thread-strided, lane tree, warps in order); head-bias gradient in CTA order
+  double l_t = 0.0;
+  for (long long k = t; k < T; k += blockDim.x) l_t += __ldcg(tile_loss + k);
+  for (int o = 16; o > 0; o >>= 1) l_t += __shfl_down_sync(0xffffffffu, l_t, o);
+  if (lane == 0) red[warp] = l_t;
+  __syncthreads();
+  double* sgb = reinterpret_cast<double*>(ss);  // scores no longer needed: CTA partials staged in order
+  for (int b = t; b < int(gridDim.x); b += blockDim.x) sgb[b] = __ldcg(cta_gb + b);
+  __syncthreads();
+  if (t == 0) {
+    double L = 0.0, G = 0.0;
+    for (int w = 0; w < kRsWarps; ++w) L += red[w];
+    for (int b = 0; b < int(gridDim.x); ++b) G += sgb[b];
+    *loss_out = P > 0 ? L * inv : 0.0;
+    *pairs_out = P;
+    if (gb_out != nullptr) *gb_out = P > 0 ? float(G * inv) : 0.f;
+    bar[2] = 0u;  // re-arm for the next launch (stream-ordered)
   }
 }
 
@@ -1841,11 +2142,16 @@ void topk_winners(const float* s, const long long* idx, long long k_valid, long 
 void rank_trace_read(unsigned long long* out) {
   MOSES_CUDA(cudaMemcpyFromSymbol(out, g_rank_trace, sizeof(unsigned long long) * 16));
 }
+void rank_cta_trace_read(unsigned long long* out) {
+  MOSES_CUDA(cudaMemcpyFromSymbol(out, g_rank_cta_trace, sizeof(unsigned long long) * 512 * 5));
+}
 // Policy: the 16-CTA cluster form when the batch fits it (at n = 512 it is faster: the grid form's
 // 128 CTAs all read the same head partials, and its last-CTA tail adds ~3 us), else the grid form,
 // else (false) the two-kernel path. The test hook forces the grid form.
 static bool g_rank_grid = false;
+static bool g_rank_sym = true;
 void debug_set_rank_grid(bool on) { g_rank_grid = on; }
+void debug_set_rank_sym(bool on) { g_rank_sym = on; }
 bool rank_step(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
                long long n, const RankWs& ws, unsigned int* ticket, float* s_out, const int* seg_of_row, long long R,
                const FinalizeOut& out, cudaStream_t st) {
@@ -1854,6 +2160,41 @@ bool rank_step(const float* part, int ntiles, long long ld, const float* hb, con
   const int cl_rows = ceil_div(n, kRankCluster);
   const bool cluster_fits = cl_rows * nsplit <= kRankMaxItems && cl_rows <= kRankMaxRows &&
                             size_t(2 * n + 3 * kRankMaxItems + (seg ? R : 0)) * 4 <= 160 * 1024;
+  // symmetric form (each pair once) for batches past the cluster form; the grid form stays reachable
+  // through the test hook (g_rank_grid) and when the symmetric workspace does not fit
+  if (!cluster_fits && !g_rank_grid && g_rank_sym && ticket != nullptr) {
+    const long long nb = ceil_div(n, 32), T = nb * (nb + 1) / 2;
+    const size_t smem = size_t(n) * 8;  // (score, label) pairs
+    const long long ws_entries = (long long)nsplit * n;  // gs_part / loss_part / pairs_part entries
+    static int sms = 0;
+    if (sms == 0) {
+      MOSES_CUDA(cudaFuncSetAttribute(rank_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      int dev = 0;
+      MOSES_CUDA(cudaGetDevice(&dev));
+      MOSES_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int per_sm = 0;  // co-resident CTAs at this batch's shared memory (cooperative launch bound)
+    MOSES_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rank_sym_kernel, kRsThreads, smem));
+    const int sym_grid = sms;  // one 1024-thread CTA per SM
+    if (per_sm >= 1 && smem <= 100 * 1024 && T * 64 <= 2 * ws_entries && T + sym_grid + n <= ws_entries) {
+      float* rowcol = reinterpret_cast<float*>(ws.gs_part);
+      double* tl = ws.loss_part;
+      long long* tp = ws.pairs_part;
+      double* cgb = ws.loss_part + T;
+      long long* cpp = ws.pairs_part + T;
+      float* sg = reinterpret_cast<float*>(ws.loss_part + T + sym_grid);
+      unsigned* bar = ticket + 1;  // [count, generation, final ticket]
+      const long long Rk = seg ? R : n;
+      void* args[] = {(void*)&part, (void*)&ntiles, (void*)&ld, (void*)&hb, (void*)&seg, (void*)&y, (void*)&n,
+                      (void*)&s_out, (void*)&Rk, (void*)&rowcol, (void*)&tl, (void*)&tp, (void*)&cgb, (void*)&cpp,
+                      (void*)&sg, (void*)&bar, (void*)&out.loss, (void*)&out.pairs, (void*)&out.coefA, (void*)&out.coefB,
+                      (void*)&out.gb};
+      MOSES_CUDA(cudaLaunchCooperativeKernel((const void*)rank_sym_kernel, dim3(sym_grid), dim3(kRsThreads), args,
+                                             smem, st));
+      MOSES_CUDA(cudaGetLastError());
+      return true;
+    }
+  }
   if ((g_rank_grid || !cluster_fits) && ticket != nullptr) {
     const int rows_per_cta = std::max<int>(4, ceil_div(n, 148));
     const int grid = ceil_div(n, rows_per_cta);

@@ -157,6 +157,7 @@ def test_rank_step_matches_two_kernel_path(ml, n, pooled):
 
     def go(flag):
         L.moses_debug_set_rank_fused(flag)
+        L.moses_debug_set_rank_sym(0)  # bitwise against the two-kernel path: the grid / cluster forms
         try:
             dm = ml.DeviceModel(p, ml.PREC_BF16, 16384)
             if pooled:
@@ -164,6 +165,7 @@ def test_rank_step_matches_two_kernel_path(ml, n, pooled):
             return ml.gradients(dm, ml.RankingBatch(x, y), want_loss=True)
         finally:
             L.moses_debug_set_rank_fused(1)
+            L.moses_debug_set_rank_sym(1)
 
     g1, l1 = go(1)
     g0, l0 = go(0)

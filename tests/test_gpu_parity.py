@@ -972,6 +972,7 @@ def test_rank_step_grid_matches_cluster(ml, kind, n, prec):
     y = np.round(rng.random(n) * 8) / 8  # ties included
     L = ml.lib()
     out = []
+    L.moses_debug_set_rank_sym(0)  # grid vs cluster here; the symmetric form: tests/test_gpu_rank_sym.py
     for grid in (1, 0):
         L.moses_debug_set_rank_grid(grid)  # 0: default policy (cluster form where it fits)
         try:
@@ -987,6 +988,7 @@ def test_rank_step_grid_matches_cluster(ml, kind, n, prec):
         finally:
             L.moses_debug_set_rank_grid(0)
         out.append((g, loss))
+    L.moses_debug_set_rank_sym(1)
     (g1, l1), (g0, l0) = out
     hb = dm.P - 1  # head bias: last scalar of the reference order
     mask = np.ones(dm.P, dtype=bool)

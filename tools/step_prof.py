@@ -12,25 +12,38 @@ import bench as B
 from paper_2201_05752_b200 import moseslab as ml
 
 L = ml.lib()
-off = ml.synth_offsets(B.SEED_DATA, B.PROGRAMS, B.MAX_STMTS)
-nb = B.PROGRAMS // B.BATCH
-off = off[: nb * B.BATCH + 1]
-n_rows = int(off[-1])
-rows_pad = int((np.diff(off[::B.BATCH]).max() + 127) // 128 * 128)
-params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
 PREC = getattr(ml, "PREC_" + os.environ.get("PREC", "BF16X3"))
-dm = ml.DeviceModel(params, PREC, max_rows=rows_pad)
-ld = dm.packed_ld
+CFG = os.environ.get("CFG", "2")
 DT = ml.input_dtype(PREC)
-X = torch.empty((n_rows, ld), dtype=torch.bfloat16 if DT == ml.DTYPE_BF16 else torch.float32, device="cuda")
-Y = torch.empty(nb * B.BATCH, dtype=torch.float32, device="cuda")
-OFF = torch.from_numpy(off).cuda()
-assert L.moses_synth_features_device(B.SEED_DATA, 0, n_rows, B.DIMS[0], DT, X.data_ptr(), ld) == 0
-assert L.moses_synth_labels_device(B.SEED_DATA, 0, nb * B.BATCH, Y.data_ptr()) == 0
-torch.cuda.synchronize()
-L.moses_set_async(1)
-ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, B.BATCH, rows_pad,
-                                         B.LR, B.MU, 1))
+if CFG == "5":  # cfg5: {164,512,512,1}, 4096 single-statement programs per step (bench_cfg5)
+    dims, batch, nb = [164, 512, 512, 1], 4096, 64
+    dm = ml.DeviceModel(ml.init_random(dims, B.SEED_MODEL), PREC, max_rows=batch)
+    ld = dm.packed_ld
+    X = torch.empty((nb * batch, ld), dtype=torch.bfloat16 if DT == ml.DTYPE_BF16 else torch.float32, device="cuda")
+    Y = torch.empty(nb * batch, dtype=torch.float32, device="cuda")
+    assert L.moses_synth_features_device(B.SEED_DATA + 5, 0, nb * batch, dims[0], DT, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(B.SEED_DATA + 5, 0, nb * batch, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    L.moses_set_async(1)
+    ml._ck(L.moses_train_graph_create(dm.h, X.data_ptr(), ld, Y.data_ptr(), nb, batch, B.LR, B.MU, 1))
+else:
+    off = ml.synth_offsets(B.SEED_DATA, B.PROGRAMS, B.MAX_STMTS)
+    nb = B.PROGRAMS // B.BATCH
+    off = off[: nb * B.BATCH + 1]
+    n_rows = int(off[-1])
+    rows_pad = int((np.diff(off[::B.BATCH]).max() + 127) // 128 * 128)
+    params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
+    dm = ml.DeviceModel(params, PREC, max_rows=rows_pad)
+    ld = dm.packed_ld
+    X = torch.empty((n_rows, ld), dtype=torch.bfloat16 if DT == ml.DTYPE_BF16 else torch.float32, device="cuda")
+    Y = torch.empty(nb * B.BATCH, dtype=torch.float32, device="cuda")
+    OFF = torch.from_numpy(off).cuda()
+    assert L.moses_synth_features_device(B.SEED_DATA, 0, n_rows, B.DIMS[0], DT, X.data_ptr(), ld) == 0
+    assert L.moses_synth_labels_device(B.SEED_DATA, 0, nb * B.BATCH, Y.data_ptr()) == 0
+    torch.cuda.synchronize()
+    L.moses_set_async(1)
+    ml._ck(L.moses_train_graph_create_pooled(dm.h, X.data_ptr(), ld, Y.data_ptr(), OFF.data_ptr(), nb, B.BATCH,
+                                             rows_pad, B.LR, B.MU, 1))
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 for _ in range(20):
     ml._ck(L.moses_train_graph_launch(dm.h, 1))
@@ -45,7 +58,7 @@ for do_flush in (False,):
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     evs.sort(key=lambda e: e.time_range.start)
     # last step only
-    starts = [i for i, e in enumerate(evs) if "gather_pooled" in e.name]
+    starts = [i for i, e in enumerate(evs) if "gather" in e.name]
     evs = evs[starts[-1]:] if starts else evs
     t0 = evs[0].time_range.start
     print(f"--- flush={do_flush}")
