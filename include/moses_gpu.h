@@ -489,6 +489,8 @@ MOSES_API int moses_debug_set_rank_sym(int32_t on);
  * k-blocks (0 = default) and an optional device buffer of clock64 / globaltimer stamps. */
 MOSES_API int moses_debug_set_wgrad_sk(int on, int splits);
 MOSES_API int moses_debug_wgrad_sk_probe(int kc, void* trace);
+/* Test hook: run the last hidden level's split-bf16 weight gradient beside the dZ chain (1, default). */
+MOSES_API int moses_debug_set_wgrad_early(int on);
 /* Test hook: force the sequential sampling walk in moses_generate_dataset_device. */
 MOSES_API int moses_debug_force_serial_sampling(int32_t on);
 

@@ -593,10 +593,53 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
                  m->bsplit() ? Shadow{m->wbf + o, 4, shadow_lo_offset(m->P)} : Shadow{m->wbf + o, 1}, m->st2);
       note_launch(1);
     }
+    // split bf16 beside the dZ chain: the last hidden level's weight gradient needs only the head
+    // backward's dZ, so it runs on the SMs the chain leaves free while the chain computes the others
+    int early = 0;
+    if (chain && m->bsplit() && g_wgrad_sk && g_wgrad_early && L - 2 >= 1) {
+      const int chain_ctas = 4 * int(std::min<long long>(ceil_div(R, 128), ceil_div(kChainMaxRows, 128)));
+      const int free_sms = g_num_sms - chain_ctas;
+      const int lev = L - 2;
+      const int tiles = ceil_div(m->dims[lev], 128) * ceil_div(m->dims[lev + 1], 256);
+      if (free_sms >= 4 * tiles) {
+        WgradGroupCall we;
+        we.n = 1;
+        we.K = int(R);
+        we.split = true;
+        we.sk_ws = m->wgsk_ws;
+        we.max_ctas = free_sms;
+        we.max_split = 4;  // 4-CTA clusters fit the SMs the chain's 4-CTA clusters leave free
+        we.a[0] = m->act[lev];
+        we.lda[0] = m->ld[lev];
+        we.b[0] = m->dz[lev + 1];
+        we.ldb[0] = m->lddz[lev + 1];
+        we.M[0] = m->dims[lev] + 1;
+        we.N[0] = m->dims[lev + 1];
+        we.g[0] = m->g + m->off[lev];
+        we.w[0] = m->w + m->off[lev];
+        we.mom[0] = m->mom + m->off[lev];
+        we.shadow[0] = m->wbf + m->off[lev];
+        we.a_lo[0] = m->act_lo(lev);
+        we.b_lo[0] = m->dz_lo(lev + 1);
+        we.shadow_lo[0] = m->wbf + shadow_lo_offset(m->P) + m->off[lev];
+        if (fuse) {
+          we.update = true;
+          we.lr = fuse->lr;
+          we.mu = fuse->mu;
+        }
+        MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (L - 1)], 0));
+        {
+          ProfScope ps(P_GEMM_WGRAD, m->st2);
+          launch_wgrad_group(we, m->st2);
+        }
+        note_launch(1);
+        early = 1;
+      }
+    }
     MOSES_CUDA(cudaEventRecord(ev[1], m->st));
     MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1], 0));
     WgradGroupCall wc;
-    wc.n = L - 1;
+    wc.n = L - 1 - early;
     wc.K = int(R);
     wc.split = m->bsplit();
     wc.sk_ws = m->wgsk_ws;
@@ -607,7 +650,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       wc.loss_copy = fuse->loss_copy;
       fuse->folded = true;
     }
-    for (int l = 0; l + 1 < L; ++l) {
+    for (int l = 0; l + 1 < L - early; ++l) {
       wc.a[l] = l == 0 ? x0 : m->act[l];
       wc.lda[l] = l == 0 ? ldx0 : m->ld[l];
       wc.b[l] = m->dz[l + 1];
@@ -3698,6 +3741,10 @@ extern "C" MOSES_API int moses_debug_set_wgrad_sk(int on, int splits) {
 }
 // experiments: TMEM promotion interval (k-blocks of 64 rows; 0 = default) and a device buffer of
 // 131 u64 clock64 stamps of block 0 (nullptr: off)
+extern "C" MOSES_API int moses_debug_set_wgrad_early(int on) {
+  moses::g_wgrad_early = on;
+  return 0;
+}
 extern "C" MOSES_API int moses_debug_wgrad_sk_probe(int kc, void* trace) {
   moses::g_wgrad_sk_kc = kc;
   moses::g_wgrad_sk_trace = static_cast<unsigned long long*>(trace);

@@ -128,6 +128,8 @@ struct WgradGroupCall {
   double* loss_acc = nullptr;
   double* loss_copy = nullptr;
   float* sk_ws = nullptr;  // split-bf16: L2 workspace of the split-K reduction (wgrad_sk_ws_bytes())
+  int max_ctas = 0;        // split-bf16: CTA budget of the launch (0: every SM), e.g. beside a running chain
+  int max_split = 8;       // split-bf16: widest cluster (beside a chain only pairs fit the leftover SMs)
 };
 size_t wgrad_sk_ws_bytes();
 void launch_wgrad_group(const WgradGroupCall& c, cudaStream_t s);
@@ -135,6 +137,8 @@ extern int g_group;
 extern int g_wgrad_sk;
 extern int g_wgrad_sk_splits;
 extern int g_wgrad_sk_kc;
+extern int g_wgrad_early;
+extern int g_num_sms;
 extern unsigned long long* g_wgrad_sk_trace;
 extern int g_rank_fused;  // rank_step (one launch) instead of rank_pairs + rank_finalize
 extern int g_chain;  // fused chain enabled (moses_debug_set_chain)

@@ -523,8 +523,9 @@ void launch_wgrad_sk_t(const WgradGroupCall& c, cudaStream_t s) {
   a.trace = g_wgrad_sk_trace;
   const int chunks = ceil_div(c.K, C::BK * a.kc);
   int S = 1, best = chunks;
-  for (int cand = 2; cand <= 8; ++cand) {
-    if (cand > chunks || (long long)tiles > (long long)max_clusters[cand]) continue;
+  const int budget = c.max_ctas > 0 ? std::min(c.max_ctas, kWgskMaxCtas) : kWgskMaxCtas;
+  for (int cand = 2; cand <= std::min(8, c.max_split); ++cand) {
+    if (cand > chunks || (long long)tiles > (long long)max_clusters[cand] || (long long)tiles * cand > budget) continue;
     const int per = ceil_div(chunks, cand);
     if (per < best) {
       best = per;
@@ -678,6 +679,7 @@ unsigned long long* g_chain_trace = nullptr;
 int g_group = 1;
 int g_wgrad_sk = 1;          // split-bf16 wgrad split over K in clusters (gemm_wgrad_sk.cuh)
 int g_wgrad_sk_splits = 0;   // > 0: force the cluster width (tests)
+int g_wgrad_early = 1;       // split bf16: last hidden level's wgrad beside the dZ chain
 int g_wgrad_sk_kc = 0;       // > 0: k-blocks per TMEM promotion chunk (experiments)
 unsigned long long* g_wgrad_sk_trace = nullptr;
 int g_rank_fused = 1;

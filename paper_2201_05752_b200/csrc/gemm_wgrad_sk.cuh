@@ -81,6 +81,20 @@ __device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// shared -> global bulk copy (bulk_group completion); global -> shared bulk copy (mbarrier complete_tx)
+__device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ptx::smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(float* sdst, const float* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx::smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // g[e] = gv; UPDATE: v = mu*v + g; w -= lr*v (no FMA contraction; sgd_kernel arithmetic) and the
@@ -145,7 +159,8 @@ __global__ void __launch_bounds__(WgskCfg::kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* bfull = empty_bar + C::kStages;  // [2] TMEM buffer holds a finished chunk
   uint64_t* bempty = bfull + 2;              // [2] drain warps consumed the buffer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 2);
+  uint64_t* gbar = bempty + 2;               // S > 1: the S slot slices of this CTA's rows have landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 1);
 
   const int S = args.S;
   const int tile = int(blockIdx.x) / S, split = int(blockIdx.x) % S;  // split == %cluster_ctarank
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(WgskCfg::kThreads, 1)
       ptx::mbar_init(&bfull[b], 1);
       ptx::mbar_init(&bempty[b], 8);
     }
+    ptx::mbar_init(gbar, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc<512>(tmem_slot);
@@ -335,37 +351,45 @@ __global__ void __launch_bounds__(WgskCfg::kThreads, 1)
   }
 
   // ---- split reduction. S > 1: every CTA publishes its partial (and bias sums) to its slot of the
-  // L2 workspace with coalesced 16-byte stores (DSMEM moves only ~20 B/clk per SM); after the cluster
-  // barrier CTA `split` sums rows [r0, r1) of the S slots in split order and runs the epilogue.
-  if (S > 1 && threadIdx.x < C::kDrainThreads) {
+  // L2 workspace with bulk copies (TMA engine, one 1 KB row each; LSU stores and DSMEM both move only
+  // ~20-25 B/clk per SM); after the cluster barrier CTA `split` bulk-loads rows [r0, r1) of the S slots
+  // into shared memory, sums them in split order and runs the epilogue.
+  const int r0 = split * BM / S, r1 = (split + 1) * BM / S;
+  float* gbuf = reinterpret_cast<float*>(smem);  // S > 1: [S][r1 - r0][BN], over the published partial
+  const float* slots = args.ws + size_t(tile) * size_t(S) * kSlotFloats;
+  if (S > 1) {
     float* slot = args.ws + size_t(blockIdx.x) * kSlotFloats;
-    constexpr int kIt = BM * BN / 4 / C::kDrainThreads;  // 32 float4 per thread, 8 in flight
-#pragma unroll
-    for (int j0 = 0; j0 < kIt; j0 += 8) {
-      float4 v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int idx = int(threadIdx.x) + (j0 + j) * C::kDrainThreads;
-        v[j] = *reinterpret_cast<const float4*>(part + (idx / (BN / 4)) * C::kPad + (idx % (BN / 4)) * 4);
+    if (threadIdx.x < C::kDrainThreads) {
+      if (bias_here && int(threadIdx.x) < bias_w) slot[BM * BN + threadIdx.x] = btot[threadIdx.x];
+      wgsk::fence_proxy_async_smem();  // the partial's generic smem writes -> the bulk copies' reads
+      wgsk::named_sync(1, C::kDrainThreads);
+      if (lane == 0) {  // warp w: rows [16w, 16w + 16)
+        for (int r = int(warp) * 16; r < int(warp) * 16 + 16; ++r)
+          wgsk::bulk_store(slot + r * BN, part + r * C::kPad, BN * 4);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int idx = int(threadIdx.x) + (j0 + j) * C::kDrainThreads;
-        __stcg(reinterpret_cast<float4*>(slot + idx * 4), v[j]);
-      }
+      __syncwarp();
     }
-    if (bias_here && int(threadIdx.x) < bias_w) slot[BM * BN + threadIdx.x] = btot[threadIdx.x];
   }
   if (args.trace && blockIdx.x == 0 && threadIdx.x == 0) args.trace[127] = clock64();
-  ptx::cluster_sync();  // release / acquire at cluster scope: the slots' global stores are visible
+  ptx::cluster_sync();  // release / acquire at cluster scope: every slot is complete
   if (args.trace && blockIdx.x == 0 && threadIdx.x == 0) args.trace[126] = clock64();
+  if (S > 1) {
+    if (threadIdx.x == 0) {
+      wgsk::fence_proxy_async_global();
+      const uint32_t bytes = uint32_t((r1 - r0) * BN * 4);
+      ptx::mbar_arrive_expect_tx(gbar, bytes * uint32_t(S));
+      for (int p = 0; p < S; ++p)
+        wgsk::bulk_load(gbuf + size_t(p) * (r1 - r0) * BN, slots + size_t(p) * kSlotFloats + size_t(r0) * BN, bytes, gbar);
+    }
+    ptx::mbar_wait(gbar, 0);
+  }
   {
-    const int r0 = split * BM / S, r1 = (split + 1) * BM / S;
     const int Mg = args.Mg[lev];
-    const float* slots = args.ws + size_t(tile) * size_t(S) * kSlotFloats;
     auto src = [&](int p, int r, int c) -> float4 {
       if (S == 1) return *reinterpret_cast<const float4*>(part + r * C::kPad + c);
-      return __ldcg(reinterpret_cast<const float4*>(slots + size_t(p) * kSlotFloats + r * BN + c));
+      return *reinterpret_cast<const float4*>(gbuf + (size_t(p) * (r1 - r0) + (r - r0)) * BN + c);
     };
     const int items = (r1 - r0) * (BN / 4);
     const bool vec = (N % 4) == 0 && ((reinterpret_cast<uintptr_t>(ga.g[lev]) | reinterpret_cast<uintptr_t>(ga.w[lev]) |

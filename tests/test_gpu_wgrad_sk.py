@@ -134,4 +134,22 @@ def test_fused_update_matches_tile_kernel(ml):
         if steps == 1:
             ulp = np.spacing(np.abs(out[0][0]).astype(np.float32)).astype(np.float64)
             dw0 = out[0][0] - p.params
-            assert np.all(np.abs(out[1][0] - out[0][0]) <= ulp + 1e-5 * np.abs(dw0))
+            assert np.all(np.abs(out[1][0] - out[0][0]) <= ulp + 1e-5 * np.max(np.abs(dw0)))
+
+
+@pytest.mark.parametrize("dims,n", [(CFG2, 2560), (CFG5, 4096), ([16, 512, 512, 512, 1], 700)])
+def test_early_last_level_beside_the_chain(ml, dims, n):
+    """The last hidden level's weight gradient launched beside the dZ chain (its own cluster width for
+    the SMs the chain leaves free) equals the single grouped launch up to split-order association."""
+    L = ml.lib()
+    p = ml.init_random(dims, 13, strict=False)
+    x, y = batch(dims, n, 3)
+    L.moses_debug_set_wgrad_early(0)
+    try:
+        g0, l0 = grads(ml, dims, p, x, y, 1)
+    finally:
+        L.moses_debug_set_wgrad_early(1)
+    g1, l1 = grads(ml, dims, p, x, y, 1)
+    g2, _ = grads(ml, dims, p, x, y, 1)
+    assert l0 == l1 and np.array_equal(g1, g2)
+    assert nrel(g1, g0) < 2e-6
