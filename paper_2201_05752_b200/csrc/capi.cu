@@ -456,7 +456,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
       }
       note_launch(1);
     }
-    m->last_tiles = 4;
+    m->last_tiles = m->bsplit() ? 8 : 4;  // split chain: per-64-column head partials
     return;
   }
   for (int l = 0; l + 1 < m->L; ++l) {
@@ -473,6 +473,7 @@ void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, c
     c.bias = m->bias(l);
     c.relu = 1;
     c.round_out = !last;  // the last hidden layer is never a GEMM operand: keep it full fp32
+    c.kperm = l > 0;      // split bf16: the fused chain's K-block order for layers fed by a hidden layer
     if (!last || (m->bsplit() && c.out != nullptr)) c.out_lo = m->act_lo(l + 1);  // split bf16 keeps both planes
     if (last) {
       c.head_w = m->head_w();

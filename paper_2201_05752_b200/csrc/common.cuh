@@ -58,6 +58,7 @@ struct GemmCall {
   int bn = 0;  // 0 = auto
   int round_out = 1;  // fp32 outputs: round to tf32 (operand of the next kind::tf32 GEMM)
   void* out_lo = nullptr;  // 3xTF32: low halves of the output
+  int kperm = 0;  // split-bf16 scoring layer fed by a hidden layer: the chain's K-block order
 };
 
 // ---------------------------------------------------------------- device-time profiler (capi.cu)

@@ -286,6 +286,7 @@ void launch_pair_split(const GemmCall& c, cudaStream_t s) {
   a.mn_layout = g_mn_layout[0];
   a.mn_sbo = g_mn_sbo[0];
   a.mn_kstep = g_mn_kstep[0];
+  a.kperm = c.kperm && c.K == 512;
   const int tiles_m2 = ceil_div(c.M, 2 * Cfg::BM);
   const int groups = c.N / 128;  // pair groups per m tile (4 at N = 512)
   if (groups != 4) fail(MOSES_ERR_INVALID_ARG, "split pair layer: N = 512");
@@ -739,7 +740,7 @@ void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
   a.trace = c.trace ? c.trace : g_chain_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ChainSplitStreamCfg::kCluster * ceil_div(c.M, ChainSplitStreamCfg::BM));
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(ChainSplitStreamCfg::kThreads);
   cfg.dynamicSmemBytes = ChainSplitStreamCfg::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -258,6 +258,11 @@ struct PairSplitCfg {
 };
 static_assert(PairSplitCfg::kSmemBytes <= 232448, "split pair layer exceeds shared memory");
 
+// 32-column activation K-block at position i: the 64-column blocks in chain_kperm order (kperm), each
+// as its two 32-column halves
+__device__ __forceinline__ int pair_kb(bool kperm, int i) {
+  return kperm ? (((i >> 1) & 3) * 2 + ((i >> 1) >> 2)) * 2 + (i & 1) : i;
+}
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThreads, 1)
     umma_fwd_pair_split(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA_lo,
                         const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmB_lo,
@@ -328,7 +333,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
       uint32_t phase = 0;
       for (int i = pair_in_q; i < tiles_m2; i += pairs_per_q) {
         const int m0 = i * 2 * BM + int(rank) * BM;
-        for (int kb = 0; kb < num_kba; ++kb) {
+        for (int i = 0; i < num_kba; ++i) {
+          const int kb = pair_kb(args.kperm != 0, i);
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t lf = mapa(ptx::smem_u32(&full_bar[stage]), 0);
           expect_tx_remote(lf, C::kStageBytes);
@@ -355,7 +361,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
         ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * 2 * C::BNC);
-        for (int kb = 0; kb < num_kba; ++kb) {
+        for (int i = 0; i < num_kba; ++i) {
+          const int kb = pair_kb(args.kperm != 0, i);
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sah = a0 + stage * C::kStageBytes, sal = sah + C::kAPlane;
@@ -369,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
             const int ks = (kb & 1) * (C::BKA / UK) + kk;
             const uint64_t bh = ptx::sw128_desc(sbh + ks * args.mn_kstep, C::BKW * 128, args.mn_sbo, args.mn_layout);
             const uint64_t bl = ptx::sw128_desc(sbl + ks * args.mn_kstep, C::BKW * 128, args.mn_sbo, args.mn_layout);
-            umma_f16_pair(d, ah, bh, kIdesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            umma_f16_pair(d, ah, bh, kIdesc, (i > 0 || kk > 0) ? 1u : 0u);
             umma_f16_pair(d, ah, bl, kIdesc, 1u);
             umma_f16_pair(d, al, bh, kIdesc, 1u);
           }

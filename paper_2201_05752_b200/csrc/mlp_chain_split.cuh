@@ -24,6 +24,12 @@ struct ChainSplitMaps {
   CUtensorMap out_lo[kChainMaxLayers];   // lo outputs: the next layer's A_lo stream, box {64, 128}
 };
 
+// K-block order of a chain layer fed by the previous layer (8 K-blocks of 64 from a 4-CTA cluster):
+// position i -> block (i % 4) * 2 + i / 4, i.e. the first 64-column halves of the four CTAs' slices,
+// then the second halves. umma_fwd_pair_split follows the same order (GemmArgs::kperm), so scoring
+// and the chain stay bit-identical.
+__host__ __device__ __forceinline__ int chain_kperm(bool perm, int i) { return perm ? (i & 3) * 2 + (i >> 2) : i; }
+
 namespace chain_detail {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
@@ -55,11 +61,13 @@ struct ChainSplitStreamCfg {
   static constexpr int kStageBytes = 2 * kWBytes + 2 * kTile;  // W_hi | W_lo | A_hi | A_lo
   static constexpr int kParamFloats = kChainMaxLayers * BN + 2 * BN;  // bias slices + head_w / head_u slices
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + kParamFloats * 4;
+  // warps 0-7 epilogue (warp w: TMEM lanes 32 (w % 4).., columns 64 (w / 4)..), 8 TMA producer, 9 MMA
+  static constexpr int kEpiWarps = 8, kProducerWarp = 8, kMmaWarp = 9, kThreads = 320;
 };
 static_assert(ChainSplitStreamCfg::kSmemBytes <= 232448, "streamed split chain exceeds shared memory");
 
 template <bool FWD>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg::kThreads, 1)
     mlp_chain_split_stream_kernel(const __grid_constant__ ChainSplitMaps maps, const __grid_constant__ ChainArgs args) {
   using namespace chain_detail;
   using C = ChainSplitStreamCfg;
@@ -72,8 +80,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
   uint64_t* wfull = reinterpret_cast<uint64_t*>(sRing + S * C::kStageBytes);
   uint64_t* wempty = wfull + S;
   uint64_t* acc_full = wempty + S;
-  uint64_t* ready = acc_full + 1;  // all four CTAs' output slices of the layer are in global memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + 1);
+  uint64_t* ready = acc_full + 1;  // [2]: half h (columns [64h, 64h+64) of every CTA's slice) is in global memory
+  uint64_t* staged = ready + 2;    // this CTA's half-1 staging (in the ring's A areas) has been read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(staged + 1);
   float* s_bias = reinterpret_cast<float*>(sRing + S * C::kStageBytes + 256);  // [layer][BN] (FWD)
   float* s_head = s_bias + kChainMaxLayers * BN;                                // [2][BN] head_w, head_u
 
@@ -88,7 +97,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       ptx::mbar_init(&wempty[s], 1);
     }
     ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(ready, C::kCluster);
+    ptx::mbar_init(&ready[0], C::kCluster);
+    ptx::mbar_init(&ready[1], C::kCluster);
+    ptx::mbar_init(staged, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc<BN>(tmem_slot);
@@ -109,7 +120,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == C::kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     int stage = 0;
     uint32_t phase = 0;
@@ -146,23 +157,37 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
     for (int l = 0; l < L; ++l) {
       const int nkb = (args.K[l] + BK - 1) / BK;
       if (lane == 0) {
-        if (l > 0) {  // every CTA of the cluster has written its slice of layer l-1
-          mbar_wait_cluster(ready, uint32_t(l - 1) & 1u);
+        // layers fed by the previous one take their K-blocks as chain_kperm orders them: the first
+        // halves of all four slices, then the second halves (each half signalled on its own)
+        const bool perm = l > 0 && nkb == 2 * C::kCluster;
+        if (l > 0) {  // every CTA of the cluster has written half 0 (both halves unless permuted), and
+                      // this CTA's epilogue no longer reads the ring's A areas
+          ptx::mbar_wait(staged, uint32_t(l - 1) & 1u);
+          mbar_wait_cluster(&ready[0], uint32_t(l - 1) & 1u);
+          if (!perm) mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
           fence_proxy_async_global();
           CHAIN_TRACE(4, l);
         }
-        for (int i = 0; i < pend_n; ++i) load_a(l, i, pend_stage[i]);
-        for (int kb = pend_n; kb < nkb; ++kb) load_a(l, kb, load_w(l, kb));
+        for (int i = 0; i < pend_n; ++i) load_a(l, chain_kperm(perm, i), pend_stage[i]);
+        for (int i = pend_n; i < nkb; ++i) {
+          if (perm && i == C::kCluster) {
+            mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
+            fence_proxy_async_global();
+          }
+          const int kb = chain_kperm(perm, i);
+          load_a(l, kb, load_w(l, kb));
+        }
         pend_n = 0;
         if (l + 1 < L) {  // the next layer's first weight blocks, while this layer's MMAs / epilogue run
           const int nn = (args.K[l + 1] + BK - 1) / BK;
+          const bool pn = nn == 2 * C::kCluster;
           pend_n = nn < S ? nn : S;
-          for (int kb = 0; kb < pend_n; ++kb) pend_stage[kb] = load_w(l + 1, kb);
+          for (int i = 0; i < pend_n; ++i) pend_stage[i] = load_w(l + 1, chain_kperm(pn, i));
         }
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     int stage = 0;
     uint32_t phase = 0;
@@ -197,19 +222,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue warps 0-3
-    const int row = int(warp) * 32 + int(lane);
+    // ------------------------------------------------------------ epilogue warps 0-7
+    // warp w: rows 32 (w % 4).. of the block, columns [64h, 64h + 64) of the slice (h = w / 4); the
+    // four warps of half h stage it, and one of them stores and signals it (ready[h])
+    const int h = int(warp) >> 2;
+    const int row = int(warp & 3) * 32 + int(lane);
     const int m = m0 + row;
     const bool row_ok = m < args.M;
-    const uint32_t t_row = tmem + ((warp * 32u) << 16);
+    const uint32_t t_row = tmem + ((uint32_t(warp & 3) * 32u) << 16) + uint32_t(h * 64);
+    const bool issuer = (threadIdx.x & 127) == 0;  // thread 0 of warp 4h
     for (int l = 0; l < L; ++l) {
       const bool last = l + 1 == L;
-      uint4 mk[BN / 32][4];
+      uint4 mk[2][4];
       if constexpr (!FWD) {
         if (row_ok) {
-          const uint4* src = reinterpret_cast<const uint4*>(args.mask[l] + (long long)m * args.ldm[l] + n0);
+          const uint4* src = reinterpret_cast<const uint4*>(args.mask[l] + (long long)m * args.ldm[l] + n0 + h * 64);
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int v = 0; v < 4; ++v) mk[c][v] = __ldg(src + c * 4 + v);
         }
@@ -218,43 +247,37 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
       ptx::tc_fence_after();
       if (threadIdx.x == 0) CHAIN_TRACE(2, l);
       const bool store = !last || args.out[l] != nullptr;
-      // the output slice is staged in the A areas of stages 0 (hi) and 1 (lo) — free while the
-      // epilogue runs: this layer's MMAs are complete and the next layer's A loads wait for `ready` —
-      // in the TMA store boxes' SW128 layout, then leaves in four coalesced bulk stores
-      uint8_t* st_hi = sRing + 2 * C::kWBytes;
-      uint8_t* st_lo = sRing + C::kStageBytes + 2 * C::kWBytes;
+      // the output slice is staged in the A areas of ring stages 0 (hi) and 1 (lo) — free while the
+      // epilogue runs: this layer's MMAs are complete and the next layer's A loads wait for `staged` /
+      // `ready` — in the TMA store boxes' SW128 layout (half h = box h), then leaves in bulk stores
+      uint8_t* st_hi = sRing + 2 * C::kWBytes + h * C::kTile;
+      uint8_t* st_lo = sRing + C::kStageBytes + 2 * C::kWBytes + h * C::kTile;
       float hp = 0.f, hp2 = 0.f;
-      uint32_t rr[2][32];  // two 32-column chunks in flight: the TMEM load of c+1 overlaps chunk c
+      uint32_t rr[2][32];  // both 32-column chunks of the half in flight
       ptx::tmem_ld_32x32b_x32(t_row, rr[0]);
+      ptx::tmem_ld_32x32b_x32(t_row + 32, rr[1]);
+      ptx::tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        ptx::tmem_ld_wait();
+      for (int c = 0; c < 2; ++c) {
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[c & 1][j]);
-        if (c + 1 < BN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rr[(c + 1) & 1]);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[c][j]);
         if constexpr (FWD) {
-          const float* sb = s_bias + l * BN + c * 32;
+          const float* sb = s_bias + l * BN + h * 64 + c * 32;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + sb[j], 0.f);
           if (last) {
             if (args.head_w != nullptr) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) hp = fmaf(v[j], s_head[c * 32 + j], hp);
+              for (int j = 0; j < 32; ++j) hp = fmaf(v[j], s_head[h * 64 + c * 32 + j], hp);
             }
             if (args.head_u != nullptr) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], s_head[BN + c * 32 + j], hp2);
+              for (int j = 0; j < 32; ++j) hp2 = fmaf(v[j], s_head[BN + h * 64 + c * 32 + j], hp2);
             }
           }
         } else {
-          uint4 cur[4];
-#pragma unroll
-          for (int cc = 0; cc < BN / 32; ++cc)
-            if (cc == c)
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) cur[q4] = mk[cc][q4];
-          const __nv_bfloat16* mv = reinterpret_cast<const __nv_bfloat16*>(cur);
+          const __nv_bfloat16* mv = reinterpret_cast<const __nv_bfloat16*>(mk[c]);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(mv[j]) > 0.f ? v[j] : 0.f;
         }
@@ -272,38 +295,38 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
               hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
-            const int col = c * 32 + j;  // within the slice
-            const int off = (col >> 6) * C::kTile + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
+            const int col = c * 32 + j;  // within the half
+            const int off = row * 128 + (((col >> 3) ^ (row & 7)) << 4);
             *reinterpret_cast<uint4*>(st_hi + off) = ph;
             *reinterpret_cast<uint4*>(st_lo + off) = pl;
           }
         }
       }
-      if (FWD && last && row_ok) {
-        if (args.head_part != nullptr) args.head_part[(long long)q * args.head_ld + m] = hp;
-        if (args.head_part2 != nullptr) args.head_part2[(long long)q * args.head_ld + m] = hp2;
+      if (FWD && last && row_ok) {  // per-64-column head partials (8 per row), as the scoring pair layers
+        if (args.head_part != nullptr) args.head_part[(long long)(2 * q + h) * args.head_ld + m] = hp;
+        if (args.head_part2 != nullptr) args.head_part2[(long long)(2 * q + h) * args.head_ld + m] = hp2;
       }
       if (store) {
-        // both planes of the slice to global memory (bulk stores complete before the signal), then
-        // one release arrive on every CTA of the cluster: their producers stream the next layer's A
         ptx::tc_fence_before();
         fence_proxy_async_smem();
-        bar_sync(2, 128);
-        if (threadIdx.x == 0) {
-          tma_store_2d(&maps.out[l], st_hi, n0, m0);
-          tma_store_2d(&maps.out[l], st_hi + C::kTile, n0 + 64, m0);
-          tma_store_2d(&maps.out_lo[l], st_lo, n0, m0);
-          tma_store_2d(&maps.out_lo[l], st_lo + C::kTile, n0 + 64, m0);
+        bar_sync(2 + h, 128);
+        if (issuer) {
+          tma_store_2d(&maps.out[l], st_hi, n0 + 64 * h, m0);
+          tma_store_2d(&maps.out_lo[l], st_lo, n0 + 64 * h, m0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (h == 1) ptx::mbar_arrive(staged);  // half 0's areas are covered by this CTA's ready[0] arrival
           asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          CHAIN_TRACE(3, l);
+          if (h == 1) CHAIN_TRACE(3, l);
           if (!last) {
-            const uint32_t local = ptx::smem_u32(ready);
+            const uint32_t local = ptx::smem_u32(&ready[h]);
 #pragma unroll
             for (uint32_t p = 0; p < uint32_t(C::kCluster); ++p) mbar_arrive_cluster(mapa(local, p));
           }
         }
-        bar_sync(2, 128);  // the staging areas are reusable (next layer's epilogue)
+        bar_sync(2 + h, 128);  // the staging areas are reusable (next layer's epilogue)
+      } else if (h == 1 && issuer) {
+        ptx::mbar_arrive(staged);  // nothing staged: keep the phase count per layer
       }
     }
     if (threadIdx.x == 0) CHAIN_TRACE(7, 0);

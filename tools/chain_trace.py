@@ -42,6 +42,9 @@ def show(title):
             v = t[0, l, e]
             row.append(f"{EV[e]} {(v - t0) / 1e3:6.2f}" if v > 0 else f"{EV[e]}   -   ")
         print(f"  L{l}: " + " | ".join(row))
+        for e in (0, 2, 3, 4):
+            print(f"      {EV[e]:14s} per CTA: " + " ".join(f"{(t[q, l, e] - t0) / 1e3:6.2f}" if t[q, l, e] > 0 else "   -  "
+                                                        for q in range(4)))
 
 
 for _ in range(3):
