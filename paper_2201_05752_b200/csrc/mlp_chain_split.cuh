@@ -61,8 +61,10 @@ struct ChainSplitStreamCfg {
   static constexpr int kStageBytes = 2 * kWBytes + 2 * kTile;  // W_hi | W_lo | A_hi | A_lo
   static constexpr int kParamFloats = kChainMaxLayers * BN + 2 * BN;  // bias slices + head_w / head_u slices
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + kParamFloats * 4;
-  // warps 0-7 epilogue (warp w: TMEM lanes 32 (w % 4).., columns 64 (w / 4)..), 8 TMA producer, 9 MMA
-  static constexpr int kEpiWarps = 8, kProducerWarp = 8, kMmaWarp = 9, kThreads = 320;
+  // warps 0-7 epilogue (warp w: TMEM lanes 32 (w % 4).., columns 64 (w / 4)..), 8 TMA producer of the
+  // weight blocks, 9 MMA, 10 TMA producer of the activation blocks (two issuing warps: ~1.3x the per-SM
+  // TMA ingest of one, profiles/r2/tma_ingest_bench.json)
+  static constexpr int kEpiWarps = 8, kProducerWarp = 8, kMmaWarp = 9, kAProducerWarp = 10, kThreads = 352;
 };
 static_assert(ChainSplitStreamCfg::kSmemBytes <= 232448, "streamed split chain exceeds shared memory");
 
@@ -93,7 +95,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      ptx::mbar_init(&wfull[s], 1);
+      ptx::mbar_init(&wfull[s], 2);  // weight producer + activation producer (each with its bytes)
       ptx::mbar_init(&wempty[s], 1);
     }
     ptx::mbar_init(acc_full, 1);
@@ -121,68 +123,68 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
   const uint32_t tmem = *tmem_slot;
 
   if (warp == C::kProducerWarp) {
-    // ------------------------------------------------------------ TMA producer
-    int stage = 0;
-    uint32_t phase = 0;
-    int pend_n = 0;  // K-blocks of the current layer whose weights were issued before its A blocks
-    int pend_stage[S];
-    auto load_w = [&](int l, int kb) -> int {
-      ptx::mbar_wait(&wempty[stage], phase ^ 1);
-      uint8_t* dst = sRing + stage * C::kStageBytes;
-      ptx::mbar_arrive_expect_tx(&wfull[stage], C::kStageBytes);
-      if constexpr (FWD) {
-        ptx::tma_load_2d(dst, &maps.w[l], &wfull[stage], n0, kb * BK);
-        ptx::tma_load_2d(dst + BK * 128, &maps.w[l], &wfull[stage], n0 + 64, kb * BK);
-        ptx::tma_load_2d(dst + C::kWBytes, &maps.w_lo[l], &wfull[stage], n0, kb * BK);
-        ptx::tma_load_2d(dst + C::kWBytes + BK * 128, &maps.w_lo[l], &wfull[stage], n0 + 64, kb * BK);
-      } else {
-        ptx::tma_load_2d(dst, &maps.w[l], &wfull[stage], kb * BK, n0);
-        ptx::tma_load_2d(dst + C::kWBytes, &maps.w_lo[l], &wfull[stage], kb * BK, n0);
+    // ------------------------------------------------------------ TMA producer: weight blocks
+    // Runs ahead of the activation producer by up to the ring depth (the next layer's first weight
+    // blocks land while this layer's MMAs / epilogue run). Position order per layer: chain_kperm.
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int l = 0; l < L; ++l) {
+        const int nkb = (args.K[l] + BK - 1) / BK;
+        const bool perm = l > 0 && nkb == 2 * C::kCluster;
+        for (int i = 0; i < nkb; ++i) {
+          const int kb = chain_kperm(perm, i);
+          ptx::mbar_wait(&wempty[stage], phase ^ 1);
+          uint8_t* dst = sRing + stage * C::kStageBytes;
+          ptx::mbar_arrive_expect_tx(&wfull[stage], 2 * C::kWBytes);
+          if constexpr (FWD) {
+            ptx::tma_load_2d(dst, &maps.w[l], &wfull[stage], n0, kb * BK);
+            ptx::tma_load_2d(dst + BK * 128, &maps.w[l], &wfull[stage], n0 + 64, kb * BK);
+            ptx::tma_load_2d(dst + C::kWBytes, &maps.w_lo[l], &wfull[stage], n0, kb * BK);
+            ptx::tma_load_2d(dst + C::kWBytes + BK * 128, &maps.w_lo[l], &wfull[stage], n0 + 64, kb * BK);
+          } else {
+            ptx::tma_load_2d(dst, &maps.w[l], &wfull[stage], kb * BK, n0);
+            ptx::tma_load_2d(dst + C::kWBytes, &maps.w_lo[l], &wfull[stage], kb * BK, n0);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
       }
-      const int s = stage;
-      if (++stage == S) { stage = 0; phase ^= 1; }
-      return s;
-    };
-    auto load_a = [&](int l, int kb, int s) {
-      const CUtensorMap* hi = l == 0 ? &maps.in : &maps.out[l - 1];
-      const CUtensorMap* lo = l == 0 ? &maps.in_lo : &maps.out_lo[l - 1];
-      uint8_t* dst = sRing + s * C::kStageBytes + 2 * C::kWBytes;
-      ptx::tma_load_2d(dst, hi, &wfull[s], kb * BK, m0);
-      ptx::tma_load_2d(dst + C::kTile, lo, &wfull[s], kb * BK, m0);
-    };
+    }
+    __syncwarp();
+  } else if (warp == C::kAProducerWarp) {
+    // ------------------------------------------------------------ TMA producer: activation blocks
+    // Layers fed by the previous one wait for the peers' slices: the first 64-column halves of all four
+    // (ready[0]) feed positions 0-3, the second halves (ready[1]) positions 4-7 (chain_kperm); and for
+    // this CTA's own epilogue to have read its staging out of the ring's A areas (staged).
     if (lane == 0) {
       ptx::tma_prefetch_desc(&maps.in);
       ptx::tma_prefetch_desc(&maps.in_lo);
-    }
-    for (int l = 0; l < L; ++l) {
-      const int nkb = (args.K[l] + BK - 1) / BK;
-      if (lane == 0) {
-        // layers fed by the previous one take their K-blocks as chain_kperm orders them: the first
-        // halves of all four slices, then the second halves (each half signalled on its own)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int l = 0; l < L; ++l) {
+        const int nkb = (args.K[l] + BK - 1) / BK;
         const bool perm = l > 0 && nkb == 2 * C::kCluster;
-        if (l > 0) {  // every CTA of the cluster has written half 0 (both halves unless permuted), and
-                      // this CTA's epilogue no longer reads the ring's A areas
+        const CUtensorMap* hi = l == 0 ? &maps.in : &maps.out[l - 1];
+        const CUtensorMap* lo = l == 0 ? &maps.in_lo : &maps.out_lo[l - 1];
+        if (l > 0) {
           ptx::mbar_wait(staged, uint32_t(l - 1) & 1u);
           mbar_wait_cluster(&ready[0], uint32_t(l - 1) & 1u);
           if (!perm) mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
           fence_proxy_async_global();
           CHAIN_TRACE(4, l);
         }
-        for (int i = 0; i < pend_n; ++i) load_a(l, chain_kperm(perm, i), pend_stage[i]);
-        for (int i = pend_n; i < nkb; ++i) {
+        for (int i = 0; i < nkb; ++i) {
           if (perm && i == C::kCluster) {
             mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
             fence_proxy_async_global();
           }
           const int kb = chain_kperm(perm, i);
-          load_a(l, kb, load_w(l, kb));
-        }
-        pend_n = 0;
-        if (l + 1 < L) {  // the next layer's first weight blocks, while this layer's MMAs / epilogue run
-          const int nn = (args.K[l + 1] + BK - 1) / BK;
-          const bool pn = nn == 2 * C::kCluster;
-          pend_n = nn < S ? nn : S;
-          for (int i = 0; i < pend_n; ++i) pend_stage[i] = load_w(l + 1, chain_kperm(pn, i));
+          ptx::mbar_wait(&wempty[stage], phase ^ 1);  // the weight producer claimed the same stage phase
+          uint8_t* dst = sRing + stage * C::kStageBytes + 2 * C::kWBytes;
+          ptx::mbar_arrive_expect_tx(&wfull[stage], 2 * C::kTile);
+          ptx::tma_load_2d(dst, hi, &wfull[stage], kb * BK, m0);
+          ptx::tma_load_2d(dst + C::kTile, lo, &wfull[stage], kb * BK, m0);
+          if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
