@@ -528,12 +528,50 @@ def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
             "ms_per_pass": best * 1000.0, "forward_ms": min(fwd_ms),
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                          "mma_per_product": 3 if split else 1,
-                         "kernel": "mlp_chain_split_kernel (fused split-bf16 chain)" if split else
+                         "kernel": "umma_fwd_pair_split (tcgen05 cta_group::2, split-bf16 weight slices resident, "
+                                   "layer by layer above 16K rows)" if split else
                                    "umma_fwd_pair (tcgen05 cta_group::2, weight-resident)",
                          "forward_device_ms": min(fwd_ms)},
             "inputs": f"device-resident {'fp32' if dt_in == ml.DTYPE_F32 else 'bf16'} packed features (> L2)",
             "timing": "wall clock per pass (device forward + local top-k + NCCL all-gather merge in the library), "
                       "max over ranks"}
+
+
+def roofline_dominant(prof, K, fwd, dg, wg, peak, traffic, flops, gemm_ms, gemm_launches):
+    """Roofline of the step's dominant kernel — the fused forward chain (mlp_chain_split_stream_kernel<FWD>):
+    its algorithmic FLOPs per launch over its average launch duration (CUDA events on its stream); the dZ
+    chain and the split-K weight-gradient launches alongside, each against its own FLOPs."""
+    def ach(f, cat):
+        ms = prof[cat][0] / K
+        return (f / (ms / 1e3) / 1e12 if ms > 0 else None), ms
+
+    a_f, ms_f = ach(fwd, "gemm_fwd")
+    a_d, ms_d = ach(dg, "gemm_dgrad")
+    a_w, ms_w = ach(wg, "gemm_wgrad")
+    kernels = {
+        "fwd_chain": {"kernel": "mlp_chain_split_stream_kernel<FWD>", "flops": fwd, "ms": ms_f, "achieved": a_f},
+        "dz_chain": {"kernel": "mlp_chain_split_stream_kernel<DGRAD>", "flops": dg, "ms": ms_d, "achieved": a_d},
+        "wgrad": {"kernel": "wgrad_sk_kernel (last hidden level beside the dZ chain + the others after it)",
+                  "flops": wg, "ms": ms_w, "achieved": a_w},
+    }
+    for v in kernels.values():
+        v["frac"] = v["achieved"] / peak if v["achieved"] else None
+        v["tensor_pipe_frac"] = 3 * v["achieved"] / peak if v["achieved"] else None
+    return {"bound": "tensor", "achieved": a_f, "peak": peak, "unit": "TFLOP/s",
+            "frac": a_f / peak if a_f else None, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per forward-chain launch, cold-cache ncu replay (profiles/ncu_traffic.json)",
+            "mma_per_product": 3, "tensor_pipe_frac": 3 * a_f / peak if a_f else None,
+            "kernel": "mlp_chain_split_stream_kernel<FWD>: the fused split-bf16 forward chain, the step's "
+                      "longest launch",
+            "kernels": kernels,
+            "all_gemms": {"flops_per_step": flops, "gemm_ms_per_step": gemm_ms,
+                          "gemm_launches_per_step": gemm_launches,
+                          "achieved": flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None,
+                          "note": "sum of GEMM launch durations (the early weight-gradient launch overlaps the dZ "
+                                  "chain, so this undercounts the overlap)"},
+            "timing": f"CUDA events on the launch streams around each GEMM launch, eager profiling pass of {K} steps "
+                      "beside the timed windows",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
 
 
 def bench_cfg1(ml, L):
@@ -636,10 +674,11 @@ def main():
     gemm_launches = sum(prof[c][1] for c in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad")) / K
     flops = gemm_flops_per_step(DIMS, head["rows_per_step"])  # real statement rows, not the padding
     peak = peaks.get("bf16_tflops_sustained", 1395.6)
-    achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = None
-    try:  # DRAM bytes of the step's GEMM launches from one ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("gemm_bytes_per_step")
+    try:  # DRAM bytes per launch of the forward chain from one ncu --set full capture (tools/ncu_train_split.sh)
+        per = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("per_kernel_bytes", {})
+        fw = [v for k, v in per.items() if "chain" in k and ("<true>" in k or "<1>" in k)]
+        traffic = fw[0] if fw else None
     except Exception:  # noqa: BLE001
         pass
     fwd, wg, dg = (v * head["rows_per_step"] / BATCH for v in train_flops_per_sample(DIMS))
@@ -656,17 +695,7 @@ def main():
         "timed_windows": len(head["windows_ms"]), "windows_ms": head["windows_ms"],
         "ms_per_step_l2_flushed": head["ms_per_step_l2_flushed"],
         "e2e": head["e2e"],
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per step (GEMM launches), cold-cache ncu replay",
-                     "mma_per_product": 3,
-                     "tensor_pipe_frac": 3 * achieved / peak if achieved else None,
-                     "kernel": "mlp_chain_split_kernel (fwd), mlp_chain_split_kernel (dZ), wgrad_group_split_kernel: "
-                               "the 3 GEMM launches of a step",
-                     "flops_per_step": flops, "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
-                     "timing": "CUDA events on the launch streams around each GEMM launch, eager profiling pass of "
-                               f"{K} steps beside the timed windows",
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+        "roofline": roofline_dominant(prof, K, fwd, dg, wg, peak, traffic, flops, gemm_ms, gemm_launches),
         "step_breakdown_ms": {k: v[0] / K for k, v in prof.items() if v[1]},
         "algorithmic_flops_per_sample": {"fwd": fwd, "wgrad": wg, "dgrad": dg},
         "rows_per_step": head["rows_per_step"], "rows_per_step_padded": head["rows_pad"],

@@ -79,7 +79,7 @@ def launch_list(src, out):
 
 
 def train_traffic(rep, out):
-    """DRAM bytes per launch of the training step's GEMM kernels (chain fwd, chain dZ, grouped wgrad)
+    """DRAM bytes per launch of the training step's GEMM kernels (chain fwd, chain dZ, split-K / grouped wgrad)
     from one --set full capture -> profiles/ncu_traffic.json (bench.py roofline.traffic)."""
     h, units, data = raw(rep)
     k = h.index("Kernel Name")
@@ -87,7 +87,7 @@ def train_traffic(rep, out):
     per = {}
     for r in data:
         name = r[k].split("(")[0]
-        if not any(s in name for s in ("mlp_chain", "wgrad_group")):
+        if not any(s in name for s in ("mlp_chain", "wgrad_group", "wgrad_sk")):
             continue
         b = float(r[rd].replace(",", "")) * SCALE[units[rd]] + float(r[wr].replace(",", "")) * SCALE[units[wr]]
         per.setdefault(name, []).append(b)
