@@ -272,6 +272,19 @@ __device__ __forceinline__ float rcp_pair(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// exp(-|d|) as one MUFU ex2 of the flush-to-zero kind (no denormal fix-up instructions), for every form
+// of the pair loop alike (the row coefficients stay bit-identical across forms); lg2 for the softplus sums
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ float score_of(const float* __restrict__ s, const float* __restrict__ part, int ntiles,
                                           long long ld, float hb, const long long* __restrict__ seg, long long r) {
   if (part == nullptr) return s[r];
@@ -316,7 +329,7 @@ __global__ void __launch_bounds__(kRankBlock) rank_pairs_kernel(const float* __r
     if (yi == yj) continue;
     const bool hi = yi > yj;
     const float d = hi ? si - ss[q] : ss[q] - si;  // s_hi - s_lo
-    const float e = __expf(-fabsf(d));
+    const float e = ex2_ftz(fabsf(d) * -1.4426950408889634f);
     const float inv = rcp_pair(1.f + e);
     const float sig_neg = d >= 0.f ? e * inv : inv;  // sigma(-d)
     if (hi) {
@@ -576,7 +589,7 @@ __global__ void __launch_bounds__(kRankThreads)
   for (int it = t; it < items; it += blockDim.x) {
     const int sp = it / rows_per_cta, lr = it - sp * rows_per_cta;
     const long long i = p0 + lr;
-    float gs = 0.f, loss = 0.f;
+    float gs = 0.f, loss = 0.f, lp = 1.f;
     int pairs = 0;
     if (i < n) {
       const float si = ss[i], yi = sy[i];
@@ -590,14 +603,16 @@ __global__ void __launch_bounds__(kRankThreads)
         const float yj = sy[j0 + k];
         const float w = float(yi > yj) - float(yi < yj);
         const float d = w * (si - ss[j0 + k]);
-        const float e = __expf(-fabsf(d));
+        const float e = ex2_ftz(fabsf(d) * -1.4426950408889634f);
         const float iv = rcp_pair(1.f + e);
         const float sig_neg = d >= 0.f ? e * iv : iv;
         gs = w != 0.f ? gs - w * sig_neg : gs;
         const bool hi = w > 0.f;
-        loss += hi ? fmaxf(-d, 0.f) - 0.69314718f * __log2f(iv) : 0.f;
+        loss += hi ? fmaxf(-d, 0.f) : 0.f;
+        lp *= hi ? 1.f + e : 1.f;  // softplus terms log1p(e) as one log of their product (<= 2^32)
         pairs += hi;
       }
+      loss += 0.69314718055994531f * lg2_ftz(lp);
     }
     pg[it] = gs;
     pl[it] = loss;
@@ -665,16 +680,14 @@ __global__ void __launch_bounds__(kRankThreads)
   }
   const double inv = P > 0 ? 1.0 / double(P) : 0.0;
   if (seg != nullptr) {
-    const long long r0 = sseg[0], r1 = sseg[p1 - p0];
-    for (long long r = r0 + t; r < r1; r += blockDim.x) {
-      int lo = 0, hi = int(p1 - p0) - 1;  // program of row r: last k with sseg[k] <= r
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sseg[mid] <= r) lo = mid;
-        else hi = mid - 1;
+    // warp per program: its statement rows are contiguous
+    const int wid = t >> 5, ln = t & 31, nw = int(blockDim.x >> 5);
+    for (int k = wid; k < int(p1 - p0); k += nw) {
+      const float a = P > 0 ? float(row_g[k] * inv) : 0.f;
+      for (long long r = sseg[k] + ln; r < sseg[k + 1]; r += 32) {
+        coefA[r] = a;
+        coefB[r] = 0.f;
       }
-      coefA[r] = P > 0 ? float(row_g[lo] * inv) : 0.f;
-      coefB[r] = 0.f;
     }
     if (q == kRankCluster - 1)
       for (long long r = seg[n] + t; r < R; r += blockDim.x) {
@@ -791,7 +804,7 @@ __global__ void __launch_bounds__(kRgThreads)
   for (int it = t; it < items; it += blockDim.x) {  // same items / arithmetic as rank_cluster_kernel
     const int sp = it / rows_per_cta, lr = it - sp * rows_per_cta;
     const long long i = p0 + lr;
-    float gs = 0.f, loss = 0.f;
+    float gs = 0.f, loss = 0.f, lp = 1.f;
     int pairs = 0;
     if (i < n) {
       const float si = ss[i], yi = sy[i];
@@ -802,14 +815,16 @@ __global__ void __launch_bounds__(kRgThreads)
         const float yj = sy[j0 + k];
         const float w = float(yi > yj) - float(yi < yj);
         const float d = w * (si - ss[j0 + k]);
-        const float e = __expf(-fabsf(d));
+        const float e = ex2_ftz(fabsf(d) * -1.4426950408889634f);
         const float iv = rcp_pair(1.f + e);
         const float sig_neg = d >= 0.f ? e * iv : iv;
         gs = w != 0.f ? gs - w * sig_neg : gs;
         const bool hi = w > 0.f;
-        loss += hi ? fmaxf(-d, 0.f) - 0.69314718f * __log2f(iv) : 0.f;
+        loss += hi ? fmaxf(-d, 0.f) : 0.f;
+        lp *= hi ? 1.f + e : 1.f;  // softplus terms log1p(e) as one log of their product (<= 2^32)
         pairs += hi;
       }
+      loss += 0.69314718055994531f * lg2_ftz(lp);
     }
     pg[it] = gs;
     pl[it] = loss;
@@ -921,16 +936,6 @@ __device__ __forceinline__ void rs_grid_sync(unsigned* bar) {  // bar[0] arrival
   __syncthreads();
 }
 // The 32 steps of one pair tile (see rank_sym_kernel). DIAG: only j > i; EDGE: columns past n.
-__device__ __forceinline__ float ex2_ftz(float x) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float lg2_ftz(float x) {
-  float r;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
 // The 32 steps of one pair tile (see rank_sym_kernel); sp[j] = (score, label). DIAG: only j > i;
 // EDGE: columns past n. Ties and invalid pairs have w = 0, hence d = 0 and c = 0. The softplus terms
 // log1p(e) of a lane's pairs are taken as one log of their product (32 factors in (1, 2]): 2 MUFU

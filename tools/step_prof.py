@@ -58,8 +58,24 @@ for do_flush in (False,):
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     evs.sort(key=lambda e: e.time_range.start)
     # last step only
+    # step period: between the ends of the last kernel of consecutive steps (the weight update)
+    ends = sorted(e.time_range.end for e in evs if "wgrad" in e.name)
+    last_ends, prev = [], None
+    for t_end in ends:  # one update per step: the latest wgrad end within each step
+        if prev is not None and t_end - prev > 40:
+            last_ends.append(prev)
+        prev = t_end
+    if prev is not None:
+        last_ends.append(prev)
+    if len(last_ends) >= 2:
+        per = [b - a for a, b in zip(last_ends, last_ends[1:])]
+        print("step period (us):", " ".join(f"{p:.1f}" for p in per))
     starts = [i for i, e in enumerate(evs) if "gather" in e.name]
-    evs = evs[starts[-1]:] if starts else evs
+    # the last step: from the kernel after the previous step's update (the forward may start before the gather)
+    lo = starts[-1] if starts else 0
+    if len(last_ends) >= 2:
+        lo = min(i for i, e in enumerate(evs) if e.time_range.start >= last_ends[-2] - 1)
+    evs = evs[lo:]
     t0 = evs[0].time_range.start
     print(f"--- flush={do_flush}")
     for e in evs:
