@@ -491,6 +491,8 @@ MOSES_API int moses_debug_set_wgrad_sk(int on, int splits);
 MOSES_API int moses_debug_wgrad_sk_probe(int kc, void* trace);
 /* Test hook: run the last hidden level's split-bf16 weight gradient beside the dZ chain (1, default). */
 MOSES_API int moses_debug_set_wgrad_early(int on);
+/* Test hook: split-bf16 fused chain on CTA pairs (1) or single CTAs (0, default); bit-identical results. */
+MOSES_API int moses_debug_set_chain_pair(int on);
 /* Test hook: force the sequential sampling walk in moses_generate_dataset_device. */
 MOSES_API int moses_debug_force_serial_sampling(int32_t on);
 

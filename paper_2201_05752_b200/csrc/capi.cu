@@ -3742,6 +3742,10 @@ extern "C" MOSES_API int moses_debug_set_wgrad_sk(int on, int splits) {
 }
 // experiments: TMEM promotion interval (k-blocks of 64 rows; 0 = default) and a device buffer of
 // 131 u64 clock64 stamps of block 0 (nullptr: off)
+extern "C" MOSES_API int moses_debug_set_chain_pair(int on) {
+  moses::g_chain_pair = on;
+  return 0;
+}
 extern "C" MOSES_API int moses_debug_set_wgrad_early(int on) {
   moses::g_wgrad_early = on;
   return 0;

@@ -139,6 +139,7 @@ extern int g_wgrad_sk;
 extern int g_wgrad_sk_splits;
 extern int g_wgrad_sk_kc;
 extern int g_wgrad_early;
+extern int g_chain_pair;
 extern int g_num_sms;
 extern unsigned long long* g_wgrad_sk_trace;
 extern int g_rank_fused;  // rank_step (one launch) instead of rank_pairs + rank_finalize

@@ -680,6 +680,7 @@ unsigned long long* g_chain_trace = nullptr;
 int g_group = 1;
 int g_wgrad_sk = 1;          // split-bf16 wgrad split over K in clusters (gemm_wgrad_sk.cuh)
 int g_wgrad_sk_splits = 0;   // > 0: force the cluster width (tests)
+int g_chain_pair = 0;        // split chain on CTA pairs (mlp_chain_split_pair_kernel; measured no faster)
 int g_wgrad_early = 1;       // split bf16: last hidden level's wgrad beside the dZ chain
 int g_wgrad_sk_kc = 0;       // > 0: k-blocks per TMEM promotion chunk (experiments)
 unsigned long long* g_wgrad_sk_trace = nullptr;
@@ -751,12 +752,70 @@ void launch_chain_split_t(const ChainCall& c, cudaStream_t s) {
   MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
 }
 
+// split chain on CTA pairs (mlp_chain_split_pair_kernel), 8-CTA clusters of 256 rows
+template <bool FWD>
+void launch_chain_pair_t(const ChainCall& c, cudaStream_t s) {
+  auto kern = mlp_chain_split_pair_kernel<FWD>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    MOSES_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ChainPairCfg::kSmemBytes));
+  });
+  if (c.in_lo == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain needs the input lo plane");
+  ChainSplitMaps maps;
+  ChainArgs a{};
+  a.M = c.M;
+  a.n_layers = c.n_layers;
+  maps.in = make_map(c.in, 2, c.K[0], c.M, c.ld_in, 64, 128);
+  maps.in_lo = make_map(c.in_lo, 2, c.K[0], c.M, c.ld_in, 64, 128);
+  constexpr int W = ChainPairCfg::kWidth;
+  for (int l = 0; l < c.n_layers; ++l) {
+    a.K[l] = c.K[l];
+    a.bias[l] = c.bias[l];
+    a.out[l] = static_cast<__nv_bfloat16*>(c.out[l]);
+    a.out_lo[l] = static_cast<__nv_bfloat16*>(c.out_lo[l]);
+    a.ldo[l] = c.ldo[l];
+    a.mask[l] = static_cast<const __nv_bfloat16*>(c.mask[l]);
+    a.ldm[l] = c.ldm[l];
+    if (c.w_lo[l] == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain needs the weight lo planes");
+    maps.w[l] = FWD ? make_map(c.w[l], 2, W, c.K[l], W, 64, 64) : make_map(c.w[l], 2, W, W, W, 64, 64);
+    maps.w_lo[l] = FWD ? make_map(c.w_lo[l], 2, W, c.K[l], W, 64, 64) : make_map(c.w_lo[l], 2, W, W, W, 64, 64);
+    if (c.out[l] != nullptr) {
+      if (c.out_lo[l] == nullptr) fail(MOSES_ERR_INVALID_ARG, "split chain output without a lo plane");
+      maps.out[l] = make_map(c.out[l], 2, W, c.M, c.ldo[l], 64, 128);
+      maps.out_lo[l] = make_map(c.out_lo[l], 2, W, c.M, c.ldo[l], 64, 128);
+    }
+  }
+  a.head_w = c.head_w;
+  a.head_u = c.head_u;
+  a.head_part = c.head_part;
+  a.head_part2 = c.head_part2;
+  a.head_ld = c.head_ld;
+  a.trace = c.trace ? c.trace : g_chain_trace;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ChainPairCfg::kCluster * ceil_div(c.M, 2 * ChainPairCfg::BM));
+  cfg.blockDim = dim3(ChainPairCfg::kThreads);
+  cfg.dynamicSmemBytes = ChainPairCfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOSES_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+}
+
 void launch_chain(const ChainCall& c, cudaStream_t s) {
   if (c.M <= 0) return;
   if (c.n_layers < 1 || c.n_layers > kChainMaxLayers) fail(MOSES_ERR_INVALID_ARG, "chain depth");
   if (c.split) {
-    if (c.fwd) launch_chain_split_t<true>(c, s);
-    else launch_chain_split_t<false>(c, s);
+    if (g_chain_pair) {
+      if (c.fwd) launch_chain_pair_t<true>(c, s);
+      else launch_chain_pair_t<false>(c, s);
+    } else {
+      if (c.fwd) launch_chain_split_t<true>(c, s);
+      else launch_chain_split_t<false>(c, s);
+    }
     return;
   }
   if (c.fwd) launch_chain_t<true>(c, s);

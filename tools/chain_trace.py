@@ -31,6 +31,9 @@ if os.environ.get("PREC", "BF16X3") == "BF16X3":  # streamed split chain: its ow
 def show(title):
     t = tr.cpu().numpy().reshape(4, 8, 8).astype(np.int64)
     t0 = t[:, 0, 6][t[:, 0, 6] > 0].min()
+    for row, nm in ((5, "W issued"), (6, "A issued"), (4, "MMA start")):
+        if t[0, row, 0] > 0 and t[0, row, 0] - t0 < 10**9:
+            print(f"  layer-1 positions {nm:9s}: " + " ".join(f"{(v - t0) / 1e3:6.2f}" for v in t[0, row]))
     print(f"--- {title} (us from kernel start of CTA 0..3)")
     for q in range(4):
         print(f"  CTA{q} start {(t[q,0,6]-t0)/1e3:.2f} end {(t[q,0,7]-t0)/1e3:.2f}")
