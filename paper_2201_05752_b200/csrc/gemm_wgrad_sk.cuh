@@ -31,14 +31,16 @@
 namespace moses {
 
 struct WgskCfg {
-  static constexpr int BM = 128, BN = 256, BK = 64;
-  static constexpr int kBox = 64 * BK * 2;              // one 64-element MN chunk x BK rows: 8 KB
-  static constexpr int kABytes = BM * BK * 2;           // 16 KB per plane
-  static constexpr int kBBytes = BN * BK * 2;           // 32 KB per plane
+  // BK = 32 rows per stage, 4 stages: the ring is TMA-latency bound (an operand block lands ~2K cycles
+  // after issue), so more, smaller stages in flight beat 2 x 96 KB (1.9-2.0K cycles per 64 rows measured)
+  static constexpr int BM = 128, BN = 256, BK = 32;
+  static constexpr int kBox = 64 * BK * 2;              // one 64-element MN chunk x BK rows: 4 KB
+  static constexpr int kABytes = BM * BK * 2;           // 8 KB per plane
+  static constexpr int kBBytes = BN * BK * 2;           // 16 KB per plane
   static constexpr int kHalfStage = kABytes + kBBytes;  // A and B of one plane: 48 KB
-  static constexpr int kStageBytes = 2 * kHalfStage;    // [A_hi | B_hi | A_lo | B_lo]: 96 KB
-  static constexpr int kStages = 2;
-  static constexpr int kChunkKb = 2;                    // 128 rows per TMEM chunk
+  static constexpr int kStageBytes = 2 * kHalfStage;    // [A_hi | B_hi | A_lo | B_lo]: 48 KB
+  static constexpr int kStages = 4;
+  static constexpr int kChunkKb = 4;                    // 128 rows per TMEM chunk
   static constexpr int kPad = BN + 4;                   // fp32 partial row stride (float4 stores conflict-free)
   static constexpr int kPartBytes = BM * kPad * 4;      // 133,120 B, reuses the stage memory
   static constexpr int kThreads = 352;
