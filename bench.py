@@ -62,6 +62,14 @@ def train_flops_per_sample(dims):
     return fwd, wgrad, dgrad
 
 
+def hidden_flops_per_step(dims, n):
+    """(forward, data-gradient, weight-gradient) FLOPs of the hidden-layer GEMMs of one step over n rows."""
+    L = len(dims) - 1
+    fwd = sum(2 * n * dims[l] * dims[l + 1] for l in range(L - 1))
+    dgrad = sum(2 * n * dims[l] * dims[l + 1] for l in range(1, L - 1))
+    return fwd, dgrad, fwd
+
+
 def gemm_flops_per_step(dims, n):
     """Hidden-layer GEMM FLOPs of one training step over n rows (the head GEMV is not a GEMM)."""
     L = len(dims) - 1
@@ -695,7 +703,8 @@ def main():
         "timed_windows": len(head["windows_ms"]), "windows_ms": head["windows_ms"],
         "ms_per_step_l2_flushed": head["ms_per_step_l2_flushed"],
         "e2e": head["e2e"],
-        "roofline": roofline_dominant(prof, K, fwd, dg, wg, peak, traffic, flops, gemm_ms, gemm_launches),
+        "roofline": roofline_dominant(prof, K, *hidden_flops_per_step(DIMS, head["rows_per_step"]), peak, traffic, flops,
+                                      gemm_ms, gemm_launches),
         "step_breakdown_ms": {k: v[0] / K for k, v in prof.items() if v[1]},
         "algorithmic_flops_per_sample": {"fwd": fwd, "wgrad": wg, "dgrad": dg},
         "rows_per_step": head["rows_per_step"], "rows_per_step_padded": head["rows_pad"],

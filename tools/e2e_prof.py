@@ -1,6 +1,7 @@
 """Timeline of the pipelined host-input training step (bench e2e leg): copies vs kernels."""
 import ctypes as C
 import sys
+import os
 import time
 
 import numpy as np
@@ -14,7 +15,7 @@ from paper_2201_05752_b200 import moseslab as ml
 L = ml.lib()
 off = ml.synth_offsets(B.SEED_DATA, 4 * B.BATCH, B.MAX_STMTS)
 params = ml.init_random(B.DIMS, B.SEED_MODEL, strict=False)
-dm = ml.DeviceModel(params, ml.PREC_BF16, max_rows=2560)
+dm = ml.DeviceModel(params, getattr(ml, "PREC_" + os.environ.get("PREC", "BF16X3")), max_rows=2560)
 batches = []
 rng = np.random.default_rng(0)
 for b in range(4):
