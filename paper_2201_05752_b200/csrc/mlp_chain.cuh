@@ -159,6 +159,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(192, 1)
     }
   }
   ptx::tc_fence_before();
+  __syncthreads();      // CTA-level order of the inits / parameter slices (what compute-sanitizer tracks)
   ptx::cluster_sync();  // barrier inits + TMEM address visible cluster-wide before any multicast
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;

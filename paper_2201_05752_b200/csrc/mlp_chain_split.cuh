@@ -119,6 +119,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
     }
   }
   ptx::tc_fence_before();
+  __syncthreads();      // CTA-level order of the inits / parameter slices (what compute-sanitizer tracks)
   ptx::cluster_sync();  // barrier inits visible cluster-wide before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -445,6 +446,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(ChainPairCfg::kThrea
     }
   }
   ptx::tc_fence_before();
+  __syncthreads();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
