@@ -2037,61 +2037,171 @@ void rank_finalize(const RankWs& ws, long long n, long long roff, const float* p
 // rows, then n target rows) with alpha_a = 1/m (source) or -1/n (target):
 //   MMD^2 = sum_a alpha_a r_a,   r_a = sum_b alpha_b k_ab
 //   dMMD^2/dx_a = -4 c alpha_a (x_a r_a - O_a),   O_a = sum_b alpha_b k_ab x_b
-// One warp per row a (lane holds features lane + 32q), the rows b staged through shared memory in
-// tiles; distances from the differences (no |a|^2 + |b|^2 - 2ab cancellation), fp32 accumulation.
-constexpr int kMmdRowsPerBlock = 8, kMmdTile = 16;
-template <typename T, int Q>
-__global__ void __launch_bounds__(kMmdRowsPerBlock * 32) mmd_grad_kernel(const T* __restrict__ H, const T* __restrict__ H_lo,
-                                                                       long long ld, long long R, long long m, int W,
-                                                                       float c, float* __restrict__ G,
-                                                                       double* __restrict__ vpart) {
-  __shared__ float tile[kMmdTile][Q * 32];
-  __shared__ float alpha[kMmdTile];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long a = (long long)blockIdx.x * kMmdRowsPerBlock + warp;
-  const float as = 1.f / float(m), at = -1.f / float(R - m);
-  float xa[Q], O[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const int f = lane + 32 * q;
-    xa[q] = (a < R && f < W) ? load_operand(H, H_lo, a * ld + f) : 0.f;
-    O[q] = 0.f;
-  }
-  float r = 0.f;
-  for (long long b0 = 0; b0 < R; b0 += kMmdTile) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kMmdTile * Q * 32; e += blockDim.x) {
-      const int bi = e / (Q * 32), f = e - bi * (Q * 32);
-      const long long b = b0 + bi;
-      tile[bi][f] = (b < R && f < W) ? load_operand(H, H_lo, b * ld + f) : 0.f;
-    }
-    if (threadIdx.x < kMmdTile) alpha[threadIdx.x] = (b0 + threadIdx.x < R) ? (b0 + threadIdx.x < m ? as : at) : 0.f;
-    __syncthreads();
-    const int nb = int(min((long long)kMmdTile, R - b0));
-    for (int bi = 0; bi < nb; ++bi) {
-      float d = 0.f;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const float t = xa[q] - tile[bi][lane + 32 * q];
-        d = fmaf(t, t, d);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      const float wk = alpha[bi] * expf(-c * d);
-      r += wk;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) O[q] = fmaf(wk, tile[bi][lane + 32 * q], O[q]);
-    }
-  }
+// Register-tiled passes on the CUDA cores (fp32; the O(R^2 W) work is two GEMM-shaped products,
+// ~0.3 G FMA each at the fine-tune shape R = 768, W = 512):
+//   mmd_prep_kernel  X_a = hi + lo in fp32 and |x_a|^2 (features in order)
+//   mmd_kmat_kernel  K_ab = alpha_b exp(-c max(|x_a|^2 + |x_b|^2 - 2 x_a.x_b, 0)) for a 64 x 64 tile per
+//                    block; the dot products accumulate over the features in the same order as |x_a|^2,
+//                    so d_aa is exactly 0 (an fp32 distance error of ~1e-4 moves k by ~1e-6 relative)
+//   mmd_rows_kernel  r_a = sum_b K_ab (b in order) and the MMD^2 partial alpha_a r_a
+//   mmd_out_kernel   G_a = -4 c alpha_a (x_a r_a - sum_b K_ab x_b) for a 64 x 64 (rows x features) tile
+// Operand tiles are double-buffered through registers. Rows are taken in chunks of kMmdChunk so the K
+// block stays L2-sized. Deterministic.
+constexpr int kMmdT = 64, kMmdF = 32, kMmdChunk = 2048;
+template <typename T>
+__global__ void mmd_prep_kernel(const T* __restrict__ H, const T* __restrict__ H_lo, long long ld, long long R, int W,
+                                float* __restrict__ X, float* __restrict__ nrm) {
+  // a warp per row: lanes write the fp32 row; lane 0 then forms |x|^2 in feature order from it
+  const long long a = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (a >= R) return;
-  const float aa = a < m ? as : at;
-  const float s = -4.f * c * aa;
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const int f = lane + 32 * q;
-    if (f < W) G[a * W + f] = s * fmaf(xa[q], r, -O[q]);
+  for (int f = lane; f < W; f += 32) X[a * W + f] = load_operand(H, H_lo, a * ld + f);
+  __syncwarp();
+  if (lane == 0) {
+    float n = 0.f;
+    for (int f = 0; f < W; ++f) {
+      const float v = X[a * W + f];
+      n = fmaf(v, v, n);
+    }
+    nrm[a] = n;
   }
-  if (lane == 0) vpart[a] = double(aa) * double(r);
+}
+// acc[i][j] += sum_k A(row i, k) B(k, col j) over a 64 x 64 tile, k in chunks of 32, double-buffered
+// through registers. An operand is either row-major with k contiguous (ROWK: X rows, K rows; a thread
+// fetches 4 consecutive k of one row and they are transposed into the [k][row] smem tile) or k-major
+// with the tile's columns contiguous (X rows indexed by k = b). get(row_or_k, col_or_k, ...) -> float4.
+template <bool A_ROWK, bool B_ROWK, typename FA, typename FB>
+__device__ __forceinline__ void mmd_tile_mac(int kdim, FA fa, FB fb, float (&acc)[4][4]) {
+  __shared__ __align__(16) float at[2][kMmdF][kMmdT + 4];
+  __shared__ __align__(16) float bt[2][kMmdF][kMmdT + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float4 ra[2], rb[2];
+  // 512 float4 per 64 x 32 tile: ROWK -> (row e / 8, k 4 (e % 8)); k-major -> (k e / 16, col 4 (e % 16))
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = threadIdx.x + u * 256;
+      ra[u] = A_ROWK ? fa(e >> 3, k0 + (e & 7) * 4) : fa(k0 + (e >> 4), (e & 15) * 4);
+      rb[u] = B_ROWK ? fb(e >> 3, k0 + (e & 7) * 4) : fb(k0 + (e >> 4), (e & 15) * 4);
+    }
+  };
+  auto put = [&](float (*t)[kMmdT + 4], bool rowk, int e, float4 v) {
+    if (rowk) {
+      const int row = e >> 3, k4 = (e & 7) * 4;
+      t[k4 + 0][row] = v.x;
+      t[k4 + 1][row] = v.y;
+      t[k4 + 2][row] = v.z;
+      t[k4 + 3][row] = v.w;
+    } else {
+      *reinterpret_cast<float4*>(&t[e >> 4][(e & 15) * 4]) = v;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = threadIdx.x + u * 256;
+      put(at[buf], A_ROWK, e, ra[u]);
+      put(bt[buf], B_ROWK, e, rb[u]);
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < kdim; k0 += kMmdF) {
+    const bool more = k0 + kMmdF < kdim;
+    if (more) fetch(k0 + kMmdF);
+#pragma unroll 8
+    for (int k = 0; k < kMmdF; ++k) {
+      const float4 va = *reinterpret_cast<const float4*>(&at[buf][k][ty * 4]);
+      const float4 vb = *reinterpret_cast<const float4*>(&bt[buf][k][tx * 4]);
+      const float pa[4] = {va.x, va.y, va.z, va.w}, pb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(pa[i], pb[j], acc[i][j]);
+    }
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+}
+__global__ void __launch_bounds__(256) mmd_kmat_kernel(const float* __restrict__ X, const float* __restrict__ nrm,
+                                                       long long R, long long m, int W, float c, long long a_base,
+                                                       long long na, float* __restrict__ K, long long Rk) {
+  const long long a0 = a_base + (long long)blockIdx.y * kMmdT, b0 = (long long)blockIdx.x * kMmdT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  auto quad = [&](long long row, long long lim, int f) -> float4 {  // X[row][f..f+3], W % 4 == 0
+    return (row < lim && f < W) ? *reinterpret_cast<const float4*>(X + row * W + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  mmd_tile_mac<true, true>(W, [&](int r, int f) { return quad(a0 + r, a_base + na, f); },
+                           [&](int r, int f) { return quad(b0 + r, R, f); }, acc);
+  const float as = 1.f / float(m), at = -1.f / float(R - m);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long a = a0 + ty * 4 + i;
+    if (a >= a_base + na) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long b = b0 + tx * 4 + j;
+      if (b >= R) continue;
+      const float d = fmaxf(fmaf(-2.f, acc[i][j], nrm[a] + nrm[b]), 0.f);
+      K[(a - a_base) * Rk + b] = (b < m ? as : at) * expf(-c * d);
+    }
+  }
+}
+// r_a = sum_b K_ab in b order (a warp per row: lane-strided partial sums, fixed shuffle tree)
+__global__ void mmd_rows_kernel(const float* __restrict__ K, long long R, long long Rk, long long m, long long a_base,
+                                long long na, float* __restrict__ r, double* __restrict__ vpart) {
+  const long long a = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= na) return;
+  float s = 0.f;
+  for (long long b = lane; b < R; b += 32) s += K[a * Rk + b];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const long long ga = a_base + a;
+    r[a] = s;
+    vpart[ga] = double(ga < m ? 1.f / float(m) : -1.f / float(R - m)) * double(s);
+  }
+}
+// G_a,f = -4 c alpha_a (x_a,f r_a - sum_b K_ab x_b,f): rows a x features f tiles of 64 x 64
+__global__ void __launch_bounds__(256) mmd_out_kernel(const float* __restrict__ X, const float* __restrict__ K,
+                                                      const float* __restrict__ r, long long R, long long m, int W,
+                                                      float c, long long a_base, long long na, float* __restrict__ G) {
+  const long long a0 = (long long)blockIdx.y * kMmdT;  // chunk-local row
+  const int f0 = blockIdx.x * kMmdT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  const long long Rk = (R + 3) / 4 * 4;  // K rows are padded to 4 columns (host)
+  mmd_tile_mac<true, false>(
+      int(Rk),
+      [&](int i, int b) {  // K[a0 + i][b..b+3]
+        return (a0 + i < na && b < Rk) ? *reinterpret_cast<const float4*>(K + (a0 + i) * Rk + b)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      },
+      [&](int b, int f) {  // X[b][f0 + f..+3]
+        return (b < R && f0 + f < W) ? *reinterpret_cast<const float4*>(X + (long long)b * W + f0 + f)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      },
+      acc);
+  const float as = 1.f / float(m), at = -1.f / float(R - m);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long al = a0 + ty * 4 + i;
+    if (al >= na) continue;
+    const long long a = a_base + al;
+    const float s = -4.f * c * (a < m ? as : at);
+    const float ra = r[al];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int f = f0 + tx * 4 + j;
+      if (f < W) G[a * W + f] = s * fmaf(X[a * W + f], ra, -acc[i][j]);
+    }
+  }
 }
 __global__ void sum_f64_kernel(const double* __restrict__ v, long long n, double scale, double* out, int accumulate) {
   using BR = cub::BlockReduce<double, 1024>;
@@ -2107,16 +2217,29 @@ template <typename T>
 void mmd_grad(const T* H, const T* H_lo, long long ld, long long R, long long m, int W, float sigma, float* G,
               double* vpart, double* value_out, double scale, bool accumulate, cudaStream_t st) {
   if (m <= 0 || R - m <= 0) fail(MOSES_ERR_ADVERSARY_DISABLED, "MMD needs source and target rows");
+  if (W % 4 != 0) fail(MOSES_ERR_INVALID_ARG, "MMD loss needs a representation width divisible by 4");
   const float c = 1.f / (2.f * sigma * sigma);
-  const int blocks = ceil_div(R, kMmdRowsPerBlock);
-  if (W <= 128)
-    mmd_grad_kernel<T, 4><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
-  else if (W <= 256)
-    mmd_grad_kernel<T, 8><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
-  else if (W <= 512)
-    mmd_grad_kernel<T, 16><<<blocks, kMmdRowsPerBlock * 32, 0, st>>>(H, H_lo, ld, R, m, W, c, G, vpart);
-  else
-    fail(MOSES_ERR_INVALID_ARG, "MMD loss supports representation widths <= 512");
+  const long long chunk = std::min<long long>(R, kMmdChunk);
+  const long long Rk = (R + 3) / 4 * 4;  // K rows padded to 4 columns (float4 loads), pad columns zero
+  float *X = nullptr, *nrm = nullptr, *K = nullptr, *r = nullptr;
+  MOSES_CUDA(cudaMallocAsync(&X, sizeof(float) * size_t(R) * size_t(W), st));
+  MOSES_CUDA(cudaMallocAsync(&nrm, sizeof(float) * size_t(R), st));
+  MOSES_CUDA(cudaMallocAsync(&K, sizeof(float) * size_t(chunk) * size_t(Rk), st));
+  MOSES_CUDA(cudaMallocAsync(&r, sizeof(float) * size_t(chunk), st));
+  if (Rk != R) MOSES_CUDA(cudaMemsetAsync(K, 0, sizeof(float) * size_t(chunk) * size_t(Rk), st));
+  mmd_prep_kernel<T><<<unsigned(ceil_div(R, 8)), 256, 0, st>>>(H, H_lo, ld, R, W, X, nrm);
+  for (long long a0 = 0; a0 < R; a0 += chunk) {
+    const long long na = std::min(chunk, R - a0);
+    const dim3 gk(unsigned(ceil_div(R, kMmdT)), unsigned(ceil_div(na, kMmdT)));
+    mmd_kmat_kernel<<<gk, 256, 0, st>>>(X, nrm, R, m, W, c, a0, na, K, Rk);
+    mmd_rows_kernel<<<unsigned(ceil_div(na, 8)), 256, 0, st>>>(K, R, Rk, m, a0, na, r, vpart);
+    const dim3 go(unsigned(ceil_div(W, kMmdT)), unsigned(ceil_div(na, kMmdT)));
+    mmd_out_kernel<<<go, 256, 0, st>>>(X, K, r, R, m, W, c, a0, na, G);
+  }
+  MOSES_CUDA(cudaFreeAsync(X, st));
+  MOSES_CUDA(cudaFreeAsync(nrm, st));
+  MOSES_CUDA(cudaFreeAsync(K, st));
+  MOSES_CUDA(cudaFreeAsync(r, st));
   sum_f64_kernel<<<1, 1024, 0, st>>>(vpart, R, scale, value_out, accumulate ? 1 : 0);
   MOSES_CUDA(cudaGetLastError());
 }
