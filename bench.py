@@ -375,18 +375,21 @@ def bench_cfg2(ml, L, args, rank, world, dist, peaks):
         assert world > 1 or (bool(torch.isfinite(losses[:e2e_steps]).all()) and float(losses[e2e_steps - 1]) > 0)
         h2d = int(np.mean([sum(t.numel() * t.element_size() for t in hb) for hb in host]))
         # this box's pinned host -> device copy rate for one step's rows (the e2e floor is h2d / rate)
+        # (on a torch-owned stream: the pinned block's use is recorded on it, and the handle's stream
+        # this section runs on is destroyed with the handle)
         xh = host[0][0]
-        dst = torch.empty(xh.numel(), dtype=torch.float64, device="cuda")
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for _ in range(3):
-            dst.copy_(xh.view(-1), non_blocking=True)
-        ev0.record()
-        for _ in range(20):
-            dst.copy_(xh.view(-1), non_blocking=True)
-        ev1.record()
-        torch.cuda.synchronize()
-        h2d_gbs = 20 * xh.numel() * 8 / (ev0.elapsed_time(ev1) / 1e3) / 1e9
-        del dst
+        with torch.cuda.stream(torch.cuda.Stream()):
+            dst = torch.empty(xh.numel(), dtype=torch.float64, device="cuda")
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(3):
+                dst.copy_(xh.view(-1), non_blocking=True)
+            ev0.record()
+            for _ in range(20):
+                dst.copy_(xh.view(-1), non_blocking=True)
+            ev1.record()
+            torch.cuda.synchronize()
+            h2d_gbs = 20 * xh.numel() * 8 / (ev0.elapsed_time(ev1) / 1e3) / 1e9
+            del dst
         out["e2e"] = {"value": world * BATCH * e2e_steps / median(e2e_windows), "unit": "samples/s",
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "steps_per_window": e2e_steps,
                       "h2d_gbs_measured": h2d_gbs,
