@@ -35,6 +35,12 @@ namespace chain_detail {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// one cluster-scope release fence, then relaxed arrivals on several peers' barriers (a .release arrive
+// fences on every call)
+__device__ __forceinline__ void fence_release_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
@@ -325,7 +331,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
           if (!last) {
             const uint32_t local = ptx::smem_u32(&ready[h]);
 #pragma unroll
-            for (uint32_t p = 0; p < uint32_t(C::kCluster); ++p) mbar_arrive_cluster(mapa(local, p));
+            fence_release_cluster();
+            for (uint32_t p = 0; p < uint32_t(C::kCluster); ++p) mbar_arrive_cluster_relaxed(mapa(local, p));
           }
         }
         bar_sync(2 + h, 128);  // the staging areas are reusable (next layer's epilogue)
@@ -648,7 +655,8 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(ChainPairCfg::kThrea
           if (!last) {  // the four CTAs holding the same rows
             const uint32_t local = ptx::smem_u32(&ready[h]);
 #pragma unroll
-            for (uint32_t p = 0; p < 4; ++p) mbar_arrive_cluster(mapa(local, 2 * p + r));
+            fence_release_cluster();
+            for (uint32_t p = 0; p < 4; ++p) mbar_arrive_cluster_relaxed(mapa(local, 2 * p + r));
           }
         }
         bar_sync(2 + h, 128);
