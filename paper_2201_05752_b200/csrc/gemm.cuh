@@ -46,7 +46,7 @@ struct GemmArgs {
   int mn_kstep;         // bytes advanced per MMA K step for MN-major operands
   int round_out;        // fp32 Fwd/Dgrad outputs rounded to tf32 (next GEMM operand)
   void* out_lo;         // 3xTF32 (gemm_split.cuh): low half of the Fwd/Dgrad output
-  int kperm;            // umma_fwd_pair_split: K-blocks in the fused chain's order (chain_kperm)
+  int kperm;            // umma_fwd_pair_split: K-blocks in the fused chain's order (chain_korder)
 };
 
 __device__ __forceinline__ float tf32_round(float x) {

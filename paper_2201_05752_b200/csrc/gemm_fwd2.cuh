@@ -258,10 +258,19 @@ struct PairSplitCfg {
 };
 static_assert(PairSplitCfg::kSmemBytes <= 232448, "split pair layer exceeds shared memory");
 
-// 32-column activation K-block at position i: the 64-column blocks in chain_kperm order (kperm), each
-// as its two 32-column halves
-__device__ __forceinline__ int pair_kb(bool kperm, int i) {
-  return kperm ? (((i >> 1) & 3) * 2 + ((i >> 1) >> 2)) * 2 + (i & 1) : i;
+// K-block order of a fused-chain layer fed by the previous one (8 blocks of 64 from the four CTAs'
+// 128-column slices, two 64-column halves each), for the CTA computing output column group q: its own
+// two blocks first (the chain consumes them straight from its epilogue's staging), then the other
+// CTAs' first halves, then their second halves (each half is signalled on its own).
+__host__ __device__ __forceinline__ int chain_korder(int q, int i) {
+  if (i < 2) return 2 * q + i;
+  const int j = (i - 2) % 3, h = (i - 2) / 3;
+  return 2 * (j + (j >= q ? 1 : 0)) + h;
+}
+// 32-column activation K-block at position i: the 64-column blocks in chain_korder order for column
+// group q (kperm), each as its two 32-column halves
+__device__ __forceinline__ int pair_kb(bool kperm, int q, int i) {
+  return kperm ? chain_korder(q, i >> 1) * 2 + (i & 1) : i;
 }
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThreads, 1)
     umma_fwd_pair_split(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA_lo,
@@ -334,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
       for (int i = pair_in_q; i < tiles_m2; i += pairs_per_q) {
         const int m0 = i * 2 * BM + int(rank) * BM;
         for (int i = 0; i < num_kba; ++i) {
-          const int kb = pair_kb(args.kperm != 0, i);
+          const int kb = pair_kb(args.kperm != 0, nq, i);
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t lf = mapa(ptx::smem_u32(&full_bar[stage]), 0);
           expect_tx_remote(lf, C::kStageBytes);
@@ -362,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + uint32_t(acc * 2 * C::BNC);
         for (int i = 0; i < num_kba; ++i) {
-          const int kb = pair_kb(args.kperm != 0, i);
+          const int kb = pair_kb(args.kperm != 0, nq, i);
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sah = a0 + stage * C::kStageBytes, sal = sah + C::kAPlane;

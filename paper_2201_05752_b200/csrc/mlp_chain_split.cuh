@@ -25,12 +25,6 @@ struct ChainSplitMaps {
   CUtensorMap out_lo[kChainMaxLayers];   // lo outputs: the next layer's A_lo stream, box {64, 128}
 };
 
-// K-block order of a chain layer fed by the previous layer (8 K-blocks of 64 from a 4-CTA cluster):
-// position i -> block (i % 4) * 2 + i / 4, i.e. the first 64-column halves of the four CTAs' slices,
-// then the second halves. umma_fwd_pair_split follows the same order (GemmArgs::kperm), so scoring
-// and the chain stay bit-identical.
-__host__ __device__ __forceinline__ int chain_kperm(bool perm, int i) { return perm ? (i & 3) * 2 + (i >> 2) : i; }
-
 namespace chain_detail {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
@@ -91,7 +85,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
   uint64_t* acc_full = wempty + S;
   uint64_t* ready = acc_full + 1;  // [2]: half h (columns [64h, 64h+64) of every CTA's slice) is in global memory
   uint64_t* staged = ready + 2;    // this CTA's half-1 staging (in the ring's A areas) has been read out
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(staged + 1);
+  uint64_t* own_staged = staged + 1;  // both halves of this CTA's slice are staged (and TMEM is read out)
+  uint64_t* own_done = own_staged + 1;  // the MMAs reading the staged slice as the next layer's A are done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(own_done + 1);
   float* s_bias = reinterpret_cast<float*>(sRing + S * C::kStageBytes + 256);  // [layer][BN] (FWD)
   float* s_head = s_bias + kChainMaxLayers * BN;                                // [2][BN] head_w, head_u
 
@@ -109,6 +105,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
     ptx::mbar_init(&ready[0], C::kCluster);
     ptx::mbar_init(&ready[1], C::kCluster);
     ptx::mbar_init(staged, 1);
+    ptx::mbar_init(own_staged, 2);
+    ptx::mbar_init(own_done, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc<BN>(tmem_slot);
@@ -133,7 +131,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
   if (warp == C::kProducerWarp) {
     // ------------------------------------------------------------ TMA producer: weight blocks
     // Runs ahead of the activation producer by up to the ring depth (the next layer's first weight
-    // blocks land while this layer's MMAs / epilogue run). Position order per layer: chain_kperm.
+    // blocks land while this layer's MMAs / epilogue run). Position order per layer: chain_korder.
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -141,7 +139,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
         const int nkb = (args.K[l] + BK - 1) / BK;
         const bool perm = l > 0 && nkb == 2 * C::kCluster;
         for (int i = 0; i < nkb; ++i) {
-          const int kb = chain_kperm(perm, i);
+          const int kb = perm ? chain_korder(int(q), i) : i;
           ptx::mbar_wait(&wempty[stage], phase ^ 1);
           uint8_t* dst = sRing + stage * C::kStageBytes;
           ptx::mbar_arrive_expect_tx(&wfull[stage], 2 * C::kWBytes);
@@ -161,9 +159,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
     __syncwarp();
   } else if (warp == C::kAProducerWarp) {
     // ------------------------------------------------------------ TMA producer: activation blocks
-    // Layers fed by the previous one wait for the peers' slices: the first 64-column halves of all four
-    // (ready[0]) feed positions 0-3, the second halves (ready[1]) positions 4-7 (chain_kperm); and for
-    // this CTA's own epilogue to have read its staging out of the ring's A areas (staged).
+    // Layers fed by the previous one (chain_korder): positions 0-1 are this CTA's own slice, which the MMA
+    // warp reads straight from the epilogue's staging (the ring stage only brings its weights: a plain
+    // arrive); positions 2-4 are the other CTAs' first halves (ready[0]), 5-7 their second halves
+    // (ready[1]). Before any load into the ring's A areas: the MMAs reading the staging are done
+    // (own_done) and the epilogue's bulk stores have read it out (staged).
     if (lane == 0) {
       ptx::tma_prefetch_desc(&maps.in);
       ptx::tma_prefetch_desc(&maps.in_lo);
@@ -174,24 +174,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
         const bool perm = l > 0 && nkb == 2 * C::kCluster;
         const CUtensorMap* hi = l == 0 ? &maps.in : &maps.out[l - 1];
         const CUtensorMap* lo = l == 0 ? &maps.in_lo : &maps.out_lo[l - 1];
-        if (l > 0) {
+        if (l > 0 && !perm) {
           ptx::mbar_wait(staged, uint32_t(l - 1) & 1u);
           mbar_wait_cluster(&ready[0], uint32_t(l - 1) & 1u);
-          if (!perm) mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
+          mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
           fence_proxy_async_global();
           CHAIN_TRACE(4, l);
         }
         for (int i = 0; i < nkb; ++i) {
-          if (perm && i == C::kCluster) {
-            mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
-            fence_proxy_async_global();
+          const int kb = perm ? chain_korder(int(q), i) : i;
+          ptx::mbar_wait(&wempty[stage], phase ^ 1);
+          if (perm && i < 2) {
+            ptx::mbar_arrive(&wfull[stage]);  // own block: no activation bytes through the ring
+          } else {
+            if (perm && i == 2) {
+              ptx::mbar_wait(own_done, uint32_t(l - 1) & 1u);
+              ptx::mbar_wait(staged, uint32_t(l - 1) & 1u);
+              mbar_wait_cluster(&ready[0], uint32_t(l - 1) & 1u);
+              fence_proxy_async_global();
+              CHAIN_TRACE(4, l);
+            }
+            if (perm && i == 5) {
+              mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
+              fence_proxy_async_global();
+            }
+            uint8_t* dst = sRing + stage * C::kStageBytes + 2 * C::kWBytes;
+            ptx::mbar_arrive_expect_tx(&wfull[stage], 2 * C::kTile);
+            ptx::tma_load_2d(dst, hi, &wfull[stage], kb * BK, m0);
+            ptx::tma_load_2d(dst + C::kTile, lo, &wfull[stage], kb * BK, m0);
           }
-          const int kb = chain_kperm(perm, i);
-          ptx::mbar_wait(&wempty[stage], phase ^ 1);  // the weight producer claimed the same stage phase
-          uint8_t* dst = sRing + stage * C::kStageBytes + 2 * C::kWBytes;
-          ptx::mbar_arrive_expect_tx(&wfull[stage], 2 * C::kTile);
-          ptx::tma_load_2d(dst, hi, &wfull[stage], kb * BK, m0);
-          ptx::tma_load_2d(dst + C::kTile, lo, &wfull[stage], kb * BK, m0);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -204,13 +215,20 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
     for (int l = 0; l < L; ++l) {
       if (lane == 0) {
         const int nkb = (args.K[l] + BK - 1) / BK;
+        const bool perm = l > 0 && nkb == 2 * C::kCluster;
         const uint32_t r0 = ptx::smem_u32(sRing);
         for (int kb = 0; kb < nkb; ++kb) {
+          if (perm && kb == 0) {  // this CTA's slice of the previous layer is staged: its blocks first
+            ptx::mbar_wait(own_staged, uint32_t(l - 1) & 1u);
+            ptx::tc_fence_after();
+          }
           ptx::mbar_wait(&wfull[stage], phase);
           ptx::tc_fence_after();
           if (kb == 0) CHAIN_TRACE(0, l);
           const uint32_t sb = r0 + stage * C::kStageBytes, sbl = sb + C::kWBytes;
-          const uint32_t sah = sb + 2 * C::kWBytes, sal = sah + C::kTile;
+          // own blocks (positions 0-1): half kb of the staged slice, hi in stage 0's A areas, lo in stage 1's
+          const uint32_t sah = (perm && kb < 2) ? r0 + 2 * C::kWBytes + kb * C::kTile : sb + 2 * C::kWBytes;
+          const uint32_t sal = (perm && kb < 2) ? r0 + C::kStageBytes + 2 * C::kWBytes + kb * C::kTile : sah + C::kTile;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ah = ptx::sw128_desc(sah + kk * 32, 16, 1024);
@@ -224,6 +242,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
             ptx::umma_f16(tmem, al, bh, kIdesc, 1u);
           }
           ptx::umma_commit(&wempty[stage]);
+          if (perm && kb == 1) ptx::umma_commit(own_done);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit(acc_full);
@@ -321,6 +340,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(ChainSplitStreamCfg:
         fence_proxy_async_smem();
         bar_sync(2 + h, 128);
         if (issuer) {
+          if (!last) ptx::mbar_arrive(own_staged);  // the next layer's MMAs may read this half (and TMEM is free)
           tma_store_2d(&maps.out[l], st_hi, n0 + 64 * h, m0);
           tma_store_2d(&maps.out_lo[l], st_lo, n0 + 64 * h, m0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -467,7 +487,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(ChainPairCfg::kThrea
         const int nkb = (args.K[l] + BK - 1) / BK;
         const bool perm = l > 0 && nkb == 8;
         for (int i = 0; i < nkb; ++i) {
-          const int kb = chain_kperm(perm, i);
+          const int kb = perm ? chain_korder(int(q), i) : i;
           ptx::mbar_wait(&wempty[stage], phase ^ 1);
           if (l == 1 && i < 8 && args.trace != nullptr && blockIdx.x == 0)
             args.trace[(0 * kChainMaxLayers + 5) * 8 + i] = chain_detail::clk();
@@ -501,16 +521,12 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(ChainPairCfg::kThrea
         if (l > 0) {
           ptx::mbar_wait(staged, uint32_t(l - 1) & 1u);
           mbar_wait_cluster(&ready[0], uint32_t(l - 1) & 1u);
-          if (!perm) mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
+          mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);  // own blocks come first, from global here
           fence_proxy_async_global();
           if (r == 0) CHAIN_TRACE_P(4, l);
         }
         for (int i = 0; i < nkb; ++i) {
-          if (perm && i == 4) {
-            mbar_wait_cluster(&ready[1], uint32_t(l - 1) & 1u);
-            fence_proxy_async_global();
-          }
-          const int kb = chain_kperm(perm, i);
+          const int kb = perm ? chain_korder(int(q), i) : i;
           ptx::mbar_wait(&wempty[stage], phase ^ 1);
           if (l == 1 && i < 8 && args.trace != nullptr && blockIdx.x == 0)
             args.trace[(0 * kChainMaxLayers + 6) * 8 + i] = chain_detail::clk();
