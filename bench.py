@@ -629,6 +629,40 @@ def bench_cfg1(ml, L):
             "cpu_oracle_1thread": {"ms": cpu1 * 1e3, "programs_per_s": n / cpu1}}
 
 
+_FULL_AFFINITY = set()
+
+
+def restore_affinity():
+    """All host cores again (the CPU baselines time the reference path on every core)."""
+    if _FULL_AFFINITY:
+        os.sched_setaffinity(0, _FULL_AFFINITY)
+
+
+def gpu_local_affinity(local):
+    """Run this rank on the CPUs of its GPU's NUMA node (as numactl --cpunodebind would), so the pinned
+    host buffers of the end-to-end leg are allocated node-local to the GPU's PCIe root; a far node
+    halves the H2D rate of the float64 rows on some boxes. No-op when the topology is unavailable."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        bus = pynvml.nvmlDeviceGetPciInfo(h).busId
+        bus = (bus.decode() if isinstance(bus, bytes) else bus).lower()
+        dom, rest = bus.split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/local_cpulist"
+        cpus = set()
+        for part in open(path).read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            _FULL_AFFINITY.update(os.sched_getaffinity(0))
+            os.sched_setaffinity(0, cpus)
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -659,6 +693,7 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    gpu_local_affinity(local)
 
     import torch
     import torch.distributed as dist
@@ -685,6 +720,7 @@ def main():
         pass
 
     head = bench_cfg2(ml, L, args, rank, world, dist, peaks)
+    restore_affinity()  # the node-local binding only matters for the e2e leg's pinned buffers
     cfg5 = None if args.no_cfg5 else bench_cfg5(ml, L, args, rank, world, dist, peaks)
     infer = infer_bf16 = None
     if not args.no_infer:  # every rank: the candidate pool is sharded across the GPUs
@@ -747,6 +783,7 @@ def main():
     if world == 1 and not args.headline_only:
         line["cfg1"] = bench_cfg1(ml, L)
     if not args.no_cpu_baseline and world == 1:
+        restore_affinity()
         allc = cpu_baseline(10.0, os.cpu_count() or 1)
         one = cpu_baseline(8.0, 1)
         line["cpu_baseline"] = allc
