@@ -216,6 +216,7 @@ struct moses_model {
   int train_parity = 0;
   long long* pcounter = nullptr;   // next batch to prefetch
   cudaStream_t st3 = nullptr;
+  cudaStream_t st4 = nullptr;      // head gradient / head-block update beside the early weight gradient
   cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   struct BatchBuf {
     void* act = nullptr;           // hi plane; split handles: lo plane at + cap * ld[0] elements
@@ -360,6 +361,7 @@ struct moses_model {
     if (pf_fork) cudaEventDestroy(pf_fork);
     if (pf_join) cudaEventDestroy(pf_join);
     if (st3) cudaStreamDestroy(st3);
+    if (st4) cudaStreamDestroy(st4);
     for (auto& a : aslot) {
       if (a.exec) cudaGraphExecDestroy(a.exec);
       dfree(a.x);
@@ -515,11 +517,24 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
   cudaEvent_t* ev = m->evs.data();  // ev[0] fork, ev[1 + l] "dz[l] ready", ev[L + 1] join
   MOSES_CUDA(cudaEventRecord(ev[0], m->st));
   MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[0], 0));
-  {
-    ProfScope ps(P_HEAD, m->st2);
-    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, m->st2, gb_override,
-                  m->act_lo_t<T>(L - 1));
+  // split bf16 beside the dZ chain: the last hidden level's weight gradient needs only the head
+  // backward's dZ, so it runs on the SMs the chain leaves free while the chain computes the others;
+  // it goes first on the side stream (the head-gradient reduction and head-block update follow it)
+  const bool chain_path = sizeof(T) == 2 && chain_ok(m) && L - 2 >= 1 && (R <= kChainMaxRows || m->bsplit());
+  int free_sms = 0;
+  bool early_ok = false;
+  if (chain_path && m->bsplit() && g_group && L - 1 <= 8 && g_wgrad_sk && g_wgrad_early) {
+    const int chain_ctas = 4 * int(std::min<long long>(ceil_div(R, 128), ceil_div(kChainMaxRows, 128)));
+    free_sms = g_num_sms - chain_ctas;
+    const int tiles = ceil_div(m->dims[L - 2], 128) * ceil_div(m->dims[L - 1], 256);
+    early_ok = free_sms >= 4 * tiles;
   }
+  auto head_grad = [&](cudaStream_t hs) {
+    ProfScope ps(P_HEAD, hs);
+    column_dot<T>(m->coefA, hl, m->ld[L - 1], R, W, m->g + m->off[L - 1], m->adv_ws, hs, gb_override,
+                  m->act_lo_t<T>(L - 1));
+  };
+  if (!early_ok) head_grad(m->st2);
   {
     ProfScope ps(P_HEAD, m->st);
     head_backward<T>(m->coefA, m->coefB, m->head_w(), u, hl, m->ld[L - 1], R, W, static_cast<T*>(m->dz[L - 1]),
@@ -586,23 +601,20 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       }
       note_launch(1);
     }
-    if (fuse) {  // the head block (gradient from column_dot on st2) once head_backward has read it
-      MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (L - 1)], 0));
+    auto head_update = [&](cudaStream_t hs) {  // the head block (gradient from column_dot) once head_backward read it
+      if (!fuse) return;
+      MOSES_CUDA(cudaStreamWaitEvent(hs, ev[1 + (L - 1)], 0));
       const long long o = m->off[L - 1];
-      ProfScope ps(P_UPDATE, m->st2);
+      ProfScope ps(P_UPDATE, hs);
       sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, m->P - o, fuse->lr, fuse->mu, true,
-                 m->bsplit() ? Shadow{m->wbf + o, 4, shadow_lo_offset(m->P)} : Shadow{m->wbf + o, 1}, m->st2);
+                 m->bsplit() ? Shadow{m->wbf + o, 4, shadow_lo_offset(m->P)} : Shadow{m->wbf + o, 1}, hs);
       note_launch(1);
-    }
-    // split bf16 beside the dZ chain: the last hidden level's weight gradient needs only the head
-    // backward's dZ, so it runs on the SMs the chain leaves free while the chain computes the others
+    };
+    if (!early_ok) head_update(m->st2);
     int early = 0;
-    if (chain && m->bsplit() && g_wgrad_sk && g_wgrad_early && L - 2 >= 1) {
-      const int chain_ctas = 4 * int(std::min<long long>(ceil_div(R, 128), ceil_div(kChainMaxRows, 128)));
-      const int free_sms = g_num_sms - chain_ctas;
+    if (early_ok) {
       const int lev = L - 2;
-      const int tiles = ceil_div(m->dims[lev], 128) * ceil_div(m->dims[lev + 1], 256);
-      if (free_sms >= 4 * tiles) {
+      {
         WgradGroupCall we;
         we.n = 1;
         we.K = int(R);
@@ -636,6 +648,13 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
         note_launch(1);
         early = 1;
       }
+      // the head gradient and head-block update on a fourth stream (joined before the step ends), so
+      // neither the early nor the remaining weight-gradient launch queues behind them
+      if (!m->st4) MOSES_CUDA(cudaStreamCreateWithFlags(&m->st4, cudaStreamNonBlocking));
+      MOSES_CUDA(cudaStreamWaitEvent(m->st4, ev[0], 0));
+      head_grad(m->st4);
+      head_update(m->st4);
+      MOSES_CUDA(cudaEventRecord(ev[L + 2], m->st4));
     }
     MOSES_CUDA(cudaEventRecord(ev[1], m->st));
     MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1], 0));
@@ -680,6 +699,7 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
     note_launch(1);
     MOSES_CUDA(cudaEventRecord(ev[L + 1], m->st2));
     MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 1], 0));
+    if (early) MOSES_CUDA(cudaStreamWaitEvent(m->st, ev[L + 2], 0));
     return fuse != nullptr;
   }
   for (int l = L - 2; l >= 0; --l) {
