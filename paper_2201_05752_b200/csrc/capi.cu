@@ -1102,6 +1102,7 @@ MOSES_API int moses_model_create(const int32_t* dims, int32_t nd, int32_t precis
     m->split = precision == MOSES_PREC_FP32 || precision == MOSES_PREC_BF16X3;
     const int twin = m->split ? 2 : 1;  // split modes: [hi | lo] halves of every GEMM operand buffer
     m->cap = round_up(max_rows, 128);
+    keep_async_pool();  // per-call stream-ordered workspaces (encode, MMD, tune loop) stay mapped
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     MOSES_CUDA(cudaStreamCreateWithFlags(&m->st2, cudaStreamNonBlocking));
     m->evs.resize(m->L + 4);

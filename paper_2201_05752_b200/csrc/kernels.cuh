@@ -60,8 +60,9 @@ struct RankWs {
   int nsplit;
 };
 int rank_splits(long long n);
-void debug_set_rank_grid(bool on);
-void debug_set_rank_sym(bool on);  // rank_step: symmetric form for batches past the cluster form (default on)  // rank_step: grid form (default) or the 16-CTA cluster form
+void debug_set_rank_grid(bool on);  // rank_step: force the grid form
+void debug_set_rank_sym(bool on);   // rank_step: symmetric form for batches past the cluster form (default on)
+void keep_async_pool();             // the default memory pool keeps its memory across synchronisations
 void rank_pairs(const float* s, const float* y, long long n, const RankWs& ws, cudaStream_t st);
 // same, scores summed from the forward's per-N-tile head partials (+ head bias); s_out optional
 void rank_pairs_fused(const float* part, int ntiles, long long ld, const float* hb, const long long* seg, const float* y,
