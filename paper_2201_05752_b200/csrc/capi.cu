@@ -217,6 +217,7 @@ struct moses_model {
   long long* pcounter = nullptr;   // next batch to prefetch
   cudaStream_t st3 = nullptr;
   cudaStream_t st4 = nullptr;      // head gradient / head-block update beside the early weight gradient
+  double* host_sc = nullptr;       // pinned: per-call scalars read back without a blocking pageable copy
   cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   struct BatchBuf {
     void* act = nullptr;           // hi plane; split handles: lo plane at + cap * ld[0] elements
@@ -362,6 +363,7 @@ struct moses_model {
     if (pf_join) cudaEventDestroy(pf_join);
     if (st3) cudaStreamDestroy(st3);
     if (st4) cudaStreamDestroy(st4);
+    if (host_sc) cudaFreeHost(host_sc);
     for (auto& a : aslot) {
       if (a.exec) cudaGraphExecDestroy(a.exec);
       dfree(a.x);
@@ -2436,7 +2438,10 @@ MOSES_API int moses_moses_step(moses_model_t m, moses_adversary_t a, const doubl
                             m->ld[m->L - 1], a->m, n, m->W(), a->u, a->c, a->eta, m->dscal + 2, m->adv_ws, m->st,
                             m->act_lo_t<float>(m->L - 1));
     note_launch(2);
-    double sc[3] = {0, 0, 0};
+    // the scalars land in pinned memory asynchronously (a pageable copy would block the host before the
+    // lottery step is even launched); one synchronisation at the end
+    if (!m->host_sc) MOSES_CUDA(cudaMallocHost(&m->host_sc, 4 * sizeof(double)));
+    double* sc = m->host_sc;
     MOSES_CUDA(cudaMemcpyAsync(sc, m->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, m->st));
     lottery_step_impl(m, mode, value, alpha, lambda, nullptr, 0, popcount, nullptr);
     MOSES_CUDA(cudaStreamSynchronize(m->st));

@@ -36,7 +36,12 @@ def mmd():
     ml._ck(L.moses_lottery_step(dm.h, 2, 0.5, 0, 1e-3, 1e-2, None, 0, C.byref(pop)))
 
 
-for name, fn in (("moses (adversary)", moses), ("mmd", mmd)):
+def fused():
+    ml._ck(L.moses_moses_step(dm.h, adv.h, xt.ctypes.data, yt.ctypes.data, 512, DIMS[0], 0.01, 2, 0.5, 0, 1e-3, 1e-2,
+                              C.byref(loss), C.byref(dl), C.byref(pop)))
+
+
+for name, fn in (("moses (adversary)", moses), ("mmd", mmd), ("moses_moses_step (fused)", fused)):
     for _ in range(5):
         fn()
     torch.cuda.synchronize()
