@@ -240,6 +240,12 @@ struct moses_model {
     double* box_host = nullptr;    // loss mailbox written by the slot's graph (mapped pinned)
     double* box_dev = nullptr;
     double* pending = nullptr;     // caller's loss_out for the slot's step in flight
+    // the slot's packed batch (layer-0 rows [hi | lo], labels, CSR offsets, row -> program): packed on
+    // the copy stream right after the upload, while the previous step still computes
+    void* act = nullptr;
+    float* labels = nullptr;
+    long long* seg_off = nullptr;
+    int* seg_rows = nullptr;
   } aslot[3];  // three slots: the host may run two steps ahead of the device
   cudaStream_t st_copy = nullptr;
   long long async_steps = 0;
@@ -332,6 +338,8 @@ struct moses_model {
     if (!split) return nullptr;
     if (x0 == act[0]) return act_lo(0);
     if (alt.act != nullptr && x0 == alt.act) return static_cast<const uint8_t*>(alt.act) + cap * ld[0] * esz;
+    for (const auto& a : aslot)
+      if (a.act != nullptr && x0 == a.act) return static_cast<const uint8_t*>(a.act) + cap * ld[0] * esz;
     fail(MOSES_ERR_INVALID_ARG, "split-operand handles take layer-0 rows from their own packed buffers");
   }
   void post_update() {  // FP32 mode: hi/lo operand pair of the updated parameters
@@ -370,6 +378,10 @@ struct moses_model {
       dfree(a.y);
       dfree(a.off);
       dfree(a.dims);
+      dfree(a.act);
+      dfree(a.labels);
+      dfree(a.seg_off);
+      dfree(a.seg_rows);
       if (a.dims_host) cudaFreeHost(a.dims_host);
       if (a.box_host) cudaFreeHost(a.box_host);
       if (a.ready) cudaEventDestroy(a.ready);
@@ -417,7 +429,8 @@ bool chain_ok(const moses_model* m) {
 
 template <typename T>
 void forward_rows(moses_model* m, const void* x0, long long ldx0, long long R, const float* head_u, bool keep_last) {
-  if (m->split && x0 != m->act[0] && x0 != m->alt.act)
+  if (m->split && x0 != m->act[0] && x0 != m->alt.act && x0 != m->aslot[0].act && x0 != m->aslot[1].act &&
+      x0 != m->aslot[2].act)
     fail(MOSES_ERR_INVALID_ARG, "split-operand handles take inputs through their packed buffers");
   if (m->bsplit() && !chain_ok(m))
     fail(MOSES_ERR_INVALID_ARG, "split-bf16 handles need hidden widths of 512 and input width <= 512");
@@ -1701,15 +1714,31 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
       MOSES_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.box_dev), a.box_host, 0));
       MOSES_CUDA(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
       MOSES_CUDA(cudaEventCreateWithFlags(&a.free, cudaEventDisableTiming));
+      const size_t act_bytes = size_t(m->cap) * size_t(m->ld[0]) * size_t(m->esz) * (m->split ? 2 : 1);
+      MOSES_CUDA(cudaMalloc(&a.act, act_bytes));
+      MOSES_CUDA(cudaMemsetAsync(a.act, 0, act_bytes, m->st));
+      a.labels = dalloc<float>(m->cap);
+      a.seg_off = dalloc<long long>(m->cap + 1);
+      a.seg_rows = dalloc<int>(m->cap);
+      MOSES_CUDA(cudaMemsetAsync(a.labels, 0, sizeof(float) * m->cap, m->st));
+      MOSES_CUDA(cudaMemsetAsync(a.seg_off, 0, sizeof(long long) * (m->cap + 1), m->st));
+      MOSES_CUDA(cudaMemsetAsync(a.seg_rows, 0xff, sizeof(int) * m->cap, m->st));
     }
-    // the per-slot graph: pack this slot into act[0] -> pooled gradients -> fused momentum update
+    auto* act_s = static_cast<__nv_bfloat16*>(a.act);
+    __nv_bfloat16* act_s_lo = m->split ? act_s + m->cap * m->ld[0] : nullptr;
+    auto pack_slot = [&](cudaStream_t ps) {
+      pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, act_s, m->ld[0], a.labels, a.seg_off, a.seg_rows,
+                                 ps, act_s_lo);
+    };
+    // the per-slot graph: pooled gradients of the slot's packed batch -> fused momentum update (the
+    // slot is packed on the copy stream right after its upload, outside the graph)
     if (!a.exec || a.programs != programs || a.lr != float(lr) || a.mu != float(mu)) {
       if (a.exec) {
         MOSES_CUDA(cudaStreamSynchronize(m->st));
         cudaGraphExecDestroy(a.exec);
         a.exec = nullptr;
       }
-      Pool pool{m->seg_off, m->seg_rows, m->cap};
+      Pool pool{a.seg_off, a.seg_rows, m->cap};
       SgdFuse fz{float(lr), float(mu)};
       fz.loss_src = m->dscal;
       fz.loss_copy = a.box_dev;
@@ -1721,16 +1750,13 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
       a.dims_host[0] = 0;
       a.dims_host[1] = programs;
       MOSES_CUDA(cudaMemcpyAsync(a.dims, a.dims_host, 2 * sizeof(long long), cudaMemcpyHostToDevice, m->st));
-      pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]), m->ld[0],
-                                 m->labels, m->seg_off, m->seg_rows, m->st, m->act_lo_t<__nv_bfloat16>(0));
-      gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, nullptr);
+      pack_slot(m->st);
+      gradients_core(m, a.act, m->ld[0], a.labels, programs, nullptr, 0.0, &pool, nullptr);
       cudaGraph_t graph;
       MOSES_CUDA(cudaStreamSynchronize(m->st));
       MOSES_CUDA(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
       try {
-        pack_pooled<__nv_bfloat16>(a.x, a.y, a.off, a.dims, D, m->cap, static_cast<__nv_bfloat16*>(m->act[0]),
-                                   m->ld[0], m->labels, m->seg_off, m->seg_rows, m->st, m->act_lo_t<__nv_bfloat16>(0));
-        if (!gradients_core(m, m->act[0], m->ld[0], m->labels, programs, nullptr, 0.0, &pool, &fz)) {
+        if (!gradients_core(m, a.act, m->ld[0], a.labels, programs, nullptr, 0.0, &pool, &fz)) {
           sgd_update(m->w, m->mom, m->g, nullptr, m->P, float(lr), float(mu), true, m->shadow(), m->st);
           m->post_update();
         }
@@ -1762,6 +1788,7 @@ MOSES_API int moses_train_step_pooled_async(moses_model_t m, const double* x, in
     MOSES_CUDA(cudaMemcpyAsync(a.off, offsets, sizeof(long long) * (programs + 1), cudaMemcpyHostToDevice,
                                m->st_copy));
     MOSES_CUDA(cudaMemcpyAsync(a.dims, a.dims_host, 2 * sizeof(long long), cudaMemcpyHostToDevice, m->st_copy));
+    pack_slot(m->st_copy);  // overlaps the previous step
     MOSES_CUDA(cudaEventRecord(a.ready, m->st_copy));
     MOSES_CUDA(cudaStreamWaitEvent(m->st, a.ready, 0));
     MOSES_CUDA(cudaGraphLaunch(a.exec, m->st));
