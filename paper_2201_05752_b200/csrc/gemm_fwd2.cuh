@@ -249,8 +249,11 @@ struct PairSplitCfg {
   static constexpr int kWBytes = 2 * kWPlane;
   static constexpr int kAPlane = BM * BKA * 2;             // one 128 x 32 activation block: 8 KB
   static constexpr int kStageBytes = 2 * kAPlane;          // hi | lo
-  static constexpr int kStages = 4;
-  static constexpr int kEpiWarps = 8;
+  // The activation ring is TMA-latency bound (an 8 KB x 2 block lands ~2-3K cycles after issue against 384
+  // MMA cycles per block): 4 epilogue warps (each draining both 64-column halves of its lane quarter,
+  // well inside a tile's MMA time) leave shared memory for a fifth stage.
+  static constexpr int kStages = 5;
+  static constexpr int kEpiWarps = 4;
   static constexpr int kStgBytes = 32 * 128;
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   static constexpr uint32_t kTmemCols = 256;  // two 128-column accumulators
@@ -397,10 +400,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ epilogue warps 2..9 (both CTAs)
+    // ------------------------------------------------------------ epilogue warps 2..5 (both CTAs)
+    // warp w: TMEM lane quarter w % 4, both 64-column halves of the accumulator in turn
     const int ew = int(warp) - 2;
     const int quarter = int(warp & 3);
-    const int half = ew >> 2;
     uint8_t* stg = staging + ew * C::kStgBytes;
     const uint32_t lt[2] = {mapa(ptx::smem_u32(&tempty[0]), 0), mapa(ptx::smem_u32(&tempty[1]), 0)};
     int it = 0;
@@ -410,14 +413,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairSplitCfg::kThrea
       const int m0 = i * 2 * BM + int(rank) * BM;
       ptx::mbar_wait(&tfull[acc], use & 1);
       ptx::tc_fence_after();
-      const uint32_t t_acc = tmem_base + uint32_t(acc * 2 * C::BNC + half * C::BNC) + (uint32_t(quarter * 32) << 16);
-      fwd_epi_tile<C::BNC, true>(args, &tmC, stg, t_acc, m0, quarter, nq * 128 + half * C::BNC, 2 * nq + half,
-                                 [&] {
-                                   ptx::tc_fence_before();
-                                   __syncwarp();
-                                   if (lane == 0) arrive_remote(lt[acc]);
-                                 },
-                                 &tmC_lo);
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const uint32_t t_acc =
+            tmem_base + uint32_t(acc * 2 * C::BNC + half * C::BNC) + (uint32_t(quarter * 32) << 16);
+        fwd_epi_tile<C::BNC, true>(args, &tmC, stg, t_acc, m0, quarter, nq * 128 + half * C::BNC, 2 * nq + half,
+                                   [&] {
+                                     if (half == 1) {  // the whole accumulator is in registers / staged
+                                       ptx::tc_fence_before();
+                                       __syncwarp();
+                                       if (lane == 0) arrive_remote(lt[acc]);
+                                     }
+                                   },
+                                   &tmC_lo);
+      }
     }
     if (lane == 0) fwd_detail::bulk_wait0();
     __syncwarp();
