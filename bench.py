@@ -492,7 +492,7 @@ def bench_infer(ml, L, programs, peaks, rank, world, dist, precision, reps=3):
 
     from paper_2201_05752_b200.distributed import shard_range, topk_sharded
 
-    chunk = 65536
+    chunk = 131072  # rows per predict call (tools/score_chunk_probe.py: larger chunks amortise the per-layer launch tails)
     k = 1024
     lo, hi = shard_range(programs, rank, world)
     n_local = hi - lo
