@@ -650,16 +650,14 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
         we.a_lo[0] = m->act_lo(lev);
         we.b_lo[0] = m->dz_lo(lev + 1);
         we.shadow_lo[0] = m->wbf + shadow_lo_offset(m->P) + m->off[lev];
-        if (fuse) {
-          we.update = true;
-          we.lr = fuse->lr;
-          we.mu = fuse->mu;
-        }
+        // gradient only: the dZ chain's first layer reads this level's weights (their operand shadow)
+        // while the launch runs, so the level's update waits for the chain (below, on the fourth stream)
         MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1 + (L - 1)], 0));
         {
           ProfScope ps(P_GEMM_WGRAD, m->st2);
           launch_wgrad_group(we, m->st2);
         }
+        MOSES_CUDA(cudaEventRecord(ev[L + 3], m->st2));  // the early level's gradient exists
         note_launch(1);
         early = 1;
       }
@@ -669,9 +667,21 @@ bool backward_rows(moses_model* m, const void* x0, long long ldx0, long long R, 
       MOSES_CUDA(cudaStreamWaitEvent(m->st4, ev[0], 0));
       head_grad(m->st4);
       head_update(m->st4);
-      MOSES_CUDA(cudaEventRecord(ev[L + 2], m->st4));
     }
     MOSES_CUDA(cudaEventRecord(ev[1], m->st));
+    if (early) {
+      if (fuse) {  // the early level's update once the chain has read its weights (and its gradient exists)
+        const int lev = L - 2;
+        const long long o = m->off[lev], cnt = m->off[lev + 1] - o;
+        MOSES_CUDA(cudaStreamWaitEvent(m->st4, ev[1], 0));
+        MOSES_CUDA(cudaStreamWaitEvent(m->st4, ev[L + 3], 0));
+        ProfScope ps(P_UPDATE, m->st4);
+        sgd_update(m->w + o, m->mom + o, m->g + o, nullptr, cnt, fuse->lr, fuse->mu, true,
+                   Shadow{m->wbf + o, 4, shadow_lo_offset(m->P)}, m->st4);
+        note_launch(1);
+      }
+      MOSES_CUDA(cudaEventRecord(ev[L + 2], m->st4));
+    }
     MOSES_CUDA(cudaStreamWaitEvent(m->st2, ev[1], 0));
     WgradGroupCall wc;
     wc.n = L - 1 - early;

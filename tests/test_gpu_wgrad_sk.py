@@ -153,3 +153,36 @@ def test_early_last_level_beside_the_chain(ml, dims, n):
     g2, _ = grads(ml, dims, p, x, y, 1)
     assert l0 == l1 and np.array_equal(g1, g2)
     assert nrel(g1, g0) < 2e-6
+
+
+@pytest.mark.parametrize("n", [300, 512, 2560])
+def test_fused_update_with_early_level_equals_single_launch(ml, n):
+    """moses_train_step with the last level's weight gradient beside the dZ chain: that launch computes the
+    gradient only and the level's update runs after the chain has read its weights (the chain's first layer
+    uses them), so weights, momentum and the split operand shadow (via the next step) are bit-identical to
+    the single grouped launch at the same cluster width — over small batches too, where the early launch
+    would otherwise finish inside the chain's first layer."""
+    L = ml.lib()
+    dims = CFG2
+    p = ml.init_random(dims, 21, strict=False)
+    out = {}
+    for early in (1, 0):
+        L.moses_debug_set_wgrad_early(early)
+        L.moses_debug_set_wgrad_sk(1, 2)
+        try:
+            dm = ml.DeviceModel(p, ml.PREC_BF16X3, max(128, n))
+            for s in range(2):
+                x, y = batch(dims, n, 300 + s)
+                loss = C.c_double()
+                ml._ck(L.moses_train_step(dm.h, ml._p(np.ascontiguousarray(x)), ml._p(np.ascontiguousarray(y)), n,
+                                          dims[0], C.c_double(0.001), C.c_double(0.9), C.byref(loss)))
+            w = np.zeros(dm.P)
+            v = np.zeros(dm.P)
+            ml._ck(L.moses_model_download(dm.h, ml._p(w), ml._p(v), dm.P))
+            out[early] = (w, v, loss.value)
+            dm.close()
+        finally:
+            L.moses_debug_set_wgrad_early(1)
+            L.moses_debug_set_wgrad_sk(1, 0)
+    assert np.array_equal(out[1][0], out[0][0]) and np.array_equal(out[1][1], out[0][1])
+    assert out[1][2] == out[0][2]
