@@ -141,6 +141,15 @@ struct Scratch {
   cudaStream_t st = nullptr;
   void* buf = nullptr;
   size_t cap = 0;
+  long long* host = nullptr;      // pinned, mapped: the top-k result (conclusive flag + indices)
+  long long* host_dev = nullptr;  // its device address (the kernel writes it directly)
+  long long* pinned() {
+    if (!host) {
+      MOSES_CUDA(cudaHostAlloc(&host, sizeof(long long) * (kTopkMax + 1), cudaHostAllocPortable | cudaHostAllocMapped));
+      MOSES_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_dev), host, 0));
+    }
+    return host;
+  }
   void* ensure(size_t bytes) {
     if (!st) MOSES_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     if (bytes > cap) {
@@ -2545,23 +2554,31 @@ MOSES_API int moses_topk_device(const float* scores, int64_t n, int64_t k, int64
     const size_t selb = select_ws_bytes(n, nullptr);
     Carver cv{static_cast<uint8_t*>(sc.ensure(selb + (kTopkMax * 12) + topk_fast_ws_bytes(n) + 8192))};
     uint8_t* selbase = cv.take<uint8_t>(selb);
-    unsigned* ok = cv.take<unsigned>(n < kTopkMax ? kTopkMax : kTopkMax);
+    unsigned* ok = cv.take<unsigned>(kTopkMax);
     long long* oi = cv.take<long long>(kTopkMax);
     void* fast_ws = cv.take<uint8_t>(topk_fast_ws_bytes(n));
     SelectWs ws;
     select_ws_carve(selbase, n, &ws);
+    long long* hb = sc.pinned();  // [0] = not-conclusive flag (first 4 bytes), [1, k] = indices
+    bool done = false;
     {
       ProfScope ps(P_TOPK, sc.st);
-      // one read of the pool when the sampled threshold is conclusive, else the exact radix passes
-      if (topk_fast(scores, n, k, fast_ws, ok, oi, sc.st)) {
-        note_launch(11);
-      } else {
+      // one launch (one read of the pool) when the sampled threshold is conclusive: it writes its flag
+      // and the indices straight into pinned host memory (no copy behind it); else the exact radix passes
+      if (topk_fast_launch(scores, n, k, fast_ws, ok, sc.host_dev + 1, reinterpret_cast<unsigned*>(sc.host_dev),
+                           sc.st)) {
+        note_launch(1);
+        MOSES_CUDA(cudaStreamSynchronize(sc.st));
+        done = *reinterpret_cast<const volatile unsigned*>(hb) == 0;
+      }
+      if (!done) {
         topk_select(scores, n, k, ws, ok, oi, sc.st);
         note_launch(10);
+        MOSES_CUDA(cudaMemcpyAsync(hb + 1, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
+        MOSES_CUDA(cudaStreamSynchronize(sc.st));
       }
     }
-    MOSES_CUDA(cudaMemcpyAsync(idx_out, oi, sizeof(long long) * k, cudaMemcpyDeviceToHost, sc.st));
-    MOSES_CUDA(cudaStreamSynchronize(sc.st));
+    std::memcpy(idx_out, hb + 1, sizeof(long long) * k);
   });
 }
 
@@ -2728,7 +2745,7 @@ MOSES_API int moses_topk_sharded(moses_comm_t c, const float* scores_dev, int64_
       SelectWs ws;
       select_ws_carve(selbase, n_local, &ws);
       ProfScope ps(P_TOPK, sc.st);
-      if (topk_fast(scores_dev, n_local, kk, fast_ws, ok, oi, sc.st)) note_launch(11);
+      if (topk_fast(scores_dev, n_local, kk, fast_ws, ok, oi, sc.st)) note_launch(1);
       else {
         topk_select(scores_dev, n_local, kk, ws, ok, oi, sc.st);
         note_launch(10);
@@ -3779,6 +3796,9 @@ namespace moses { void rank_trace_read(unsigned long long* out); void rank_cta_t
 // rank_sym_kernel per-CTA stamps: 512 x {start, scores, pairs, grid sync, rows} (globaltimer ns)
 extern "C" MOSES_API int moses_debug_rank_cta_trace(unsigned long long* out2560) {
   return guarded([&] { moses::rank_cta_trace_read(out2560); });
+}
+extern "C" MOSES_API int moses_debug_topk_trace(unsigned long long* out16) {
+  return guarded([&] { moses::topk_trace_read(out16); });
 }
 extern "C" MOSES_API int moses_debug_rank_trace(unsigned long long* out16) {
   return guarded([&] { moses::rank_trace_read(out16); });

@@ -158,8 +158,12 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
 void topk_select(const float* scores, long long n, long long k, const SelectWs& ws, unsigned* out_key, long long* out_idx,
                  cudaStream_t st);
 constexpr long long kTopkMax = 4096;
-// one-pass sampled top-k (topk.cu); false = not applicable / not conclusive (run topk_select)
+// one-launch sampled top-k (topk.cu); false = not applicable / not conclusive (run topk_select)
 size_t topk_fast_ws_bytes(long long n);
+// launch only (false = not applicable); *fail_out (device) = 1 when not conclusive, else 0 and the result out
+void topk_trace_read(unsigned long long* out16);  // debug: the one-launch kernel's phase stamps
+bool topk_fast_launch(const float* scores, long long n, long long k, void* ws, unsigned* out_key, long long* out_idx,
+                      unsigned* fail_out, cudaStream_t st);
 void select_kth_key(long long n, unsigned long long need, const SelectWs& ws, cudaStream_t st);
 const unsigned* sel_result_key(const SelectWs& ws);
 bool topk_fast(const float* scores, long long n, long long k, void* ws, unsigned* out_key, long long* out_idx,

@@ -5,6 +5,7 @@ relative (max |d| / max |ref|); masks, top-k indices, popcounts, accuracy counts
 bit-exact on identical inputs in identical precision (fp32 on both sides).
 bf16 mode is the throughput mode: its error is measured and bounded looser.
 """
+import ctypes as C
 import math
 
 import numpy as np
@@ -554,6 +555,20 @@ def test_topk_large_pool_bit_exact(ml, orc, kind, k):
         s = -np.abs(s) - 1.0
     s = f32(s)
     assert np.array_equal(ml.topk(s, k), orc.topk(s.astype(np.float32), k))
+
+
+@pytest.mark.parametrize("n,k", [(20_000_003, 1024), ((1 << 20) + 1, 1), (8_388_611, 4096)])
+def test_topk_one_launch_pools(ml, orc, n, k):
+    """Pools sized like the scoring workload (ragged tails: n mod 4 = 3 / 1 / 3) through the one-launch
+    sampled top-k: the result equals the oracle order, ties in the candidate set included."""
+    rng = np.random.default_rng(n)
+    s = f32(np.round(rng.normal(0, 1, n), 4))
+    L = ml.lib()
+    L.moses_kernel_launches.restype = C.c_int64
+    l0 = L.moses_kernel_launches()
+    got = ml.topk(s, k)
+    assert L.moses_kernel_launches() - l0 == 2  # f64 -> f32 conversion + the one top-k launch (conclusive)
+    assert np.array_equal(got, orc.topk(s.astype(np.float32), k))
 
 
 def test_topk_negative_and_equal_scores(ml, orc):

@@ -30,3 +30,9 @@ evs.sort(key=lambda e: e.time_range.start)
 t0 = evs[0].time_range.start
 for e in evs:
     print(f"{e.time_range.start - t0:10.1f} {e.time_range.elapsed_us():9.1f}  {e.name[:80]}")
+tr = (C.c_uint64 * 16)()
+ml._ck(L.moses_debug_topk_trace(tr))
+names = ["sample+hist", "level 1", "level 2", "pass", "barrier", "final"]
+print("phases (us):", ", ".join(f"{names[i]} {(tr[i + 1] - tr[i]) / 1e3:.1f}" for i in range(6)),
+      f"(sample loop {(tr[7] - tr[0]) / 1e3:.1f}); candidates {tr[8]}; pass end over CTAs "
+      f"{(tr[9] - tr[3]) / 1e3:.1f}-{(tr[10] - tr[3]) / 1e3:.1f} us after its start")
