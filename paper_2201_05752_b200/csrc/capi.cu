@@ -2107,19 +2107,20 @@ static void lottery_step_impl(moses_model* m, int32_t mode, double value, double
         MOSES_CUDA(cudaMemsetAsync(m->lot_ws, 0, lottery_ws_bytes(m->P), m->st));  // barrier state of the resident step
       }
       ProfScope ps(P_SELECT, m->st);
+      // the step writes every operand shadow itself (split pairs included)
       const int launched = lottery_step_fused(m->w, m->g, m->P, mode, float(value), keep, float(alpha),
-                                              float(1.0 - rate), decay, m->shadow(), m->mask, m->lot_ws, m->dcount, m->st,
-                                              adam);
-      m->post_update();
+                                              float(1.0 - rate), decay, m->shadow_full(), m->mask, m->lot_ws, m->dcount,
+                                              m->st, adam);
       note_launch(launched);
     }
     m->xi_valid = false;
     long long pop = std::min(keep, m->P);
-    if (mode == MOSES_MODE_THRESHOLD) {
-      unsigned long long h = 0;
-      MOSES_CUDA(cudaMemcpyAsync(&h, m->dcount, sizeof(h), cudaMemcpyDeviceToHost, m->st));
+    if (mode == MOSES_MODE_THRESHOLD) {  // the counted kept scalars, through the pinned scalar slot
+      if (!m->host_sc) MOSES_CUDA(cudaMallocHost(&m->host_sc, 4 * sizeof(double)));
+      unsigned long long* h = reinterpret_cast<unsigned long long*>(m->host_sc + 3);
+      MOSES_CUDA(cudaMemcpyAsync(h, m->dcount, sizeof(*h), cudaMemcpyDeviceToHost, m->st));
       MOSES_CUDA(cudaStreamSynchronize(m->st));
-      pop = (long long)h;
+      pop = (long long)*h;
     }
     if (mask_out) {
       if (count != m->P) fail(MOSES_ERR_SHAPE_MISMATCH, "mask count mismatch");
@@ -3796,6 +3797,9 @@ namespace moses { void rank_trace_read(unsigned long long* out); void rank_cta_t
 // rank_sym_kernel per-CTA stamps: 512 x {start, scores, pairs, grid sync, rows} (globaltimer ns)
 extern "C" MOSES_API int moses_debug_rank_cta_trace(unsigned long long* out2560) {
   return guarded([&] { moses::rank_cta_trace_read(out2560); });
+}
+extern "C" MOSES_API int moses_debug_lottery_trace(unsigned long long* out8) {
+  return guarded([&] { moses::lottery_res_trace_read(out8); });
 }
 extern "C" MOSES_API int moses_debug_topk_trace(unsigned long long* out16) {
   return guarded([&] { moses::topk_trace_read(out16); });

@@ -161,6 +161,7 @@ constexpr long long kTopkMax = 4096;
 // one-launch sampled top-k (topk.cu); false = not applicable / not conclusive (run topk_select)
 size_t topk_fast_ws_bytes(long long n);
 // launch only (false = not applicable); *fail_out (device) = 1 when not conclusive, else 0 and the result out
+void lottery_res_trace_read(unsigned long long* out8);  // debug: the resident step's phase stamps
 void topk_trace_read(unsigned long long* out16);  // debug: the one-launch kernel's phase stamps
 bool topk_fast_launch(const float* scores, long long n, long long k, void* ws, unsigned* out_key, long long* out_idx,
                       unsigned* fail_out, cudaStream_t st);

@@ -905,20 +905,31 @@ struct ResState {
   unsigned long long block_eq[1024];
 };
 
+__device__ unsigned long long g_res_trace[8];  // CTA 0's phase stamps (globaltimer), debug read-out
+__device__ __forceinline__ void res_stamp(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_res_trace[k] = v;
+  }
+}
+
+// acquire/release grid barrier (no full fences, no back-off sleep: the whole grid is resident)
 __device__ __forceinline__ void res_grid_sync(ResState* st) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = &st->bar_gen;
-    const unsigned g0 = *gen;
-    __threadfence();
-    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
-      st->bar_count = 0;
-      __threadfence();
-      atomicAdd(&st->bar_gen, 1u);
+    unsigned g0, arrived;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(&st->bar_gen) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(&st->bar_count) : "memory");
+    if (arrived == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&st->bar_count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&st->bar_gen) : "memory");
     } else {
-      while (*gen == g0) __nanosleep(32);
+      unsigned gg;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gg) : "l"(&st->bar_gen) : "memory");
+      } while (gg == g0);
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -954,13 +965,14 @@ template <int SHADOW, bool THRESH>
 __global__ void __launch_bounds__(kResThreads, 1)
     lot_resident_kernel(float* __restrict__ w, const float* __restrict__ g, long long n, long long chunk, int E,
                         unsigned long long keep, float theta, float alpha, float factor, bool decay,
-                        void* __restrict__ shadow, uint8_t* __restrict__ mask, ResState* st,
+                        void* __restrict__ shadow, long long lo_off, uint8_t* __restrict__ mask, ResState* st,
                         unsigned long long* popcount_out, const StepOpt opt) {
   __shared__ unsigned sh[2048];
   __shared__ unsigned s_digit;
   __shared__ unsigned long long s_before;
   using Red = cub::BlockReduce<unsigned long long, kResThreads>;
   __shared__ typename Red::TempStorage rtmp;
+  res_stamp(0);
   const long long base = blockIdx.x * chunk;
   float wv[kResE], gv[kResE];
 #pragma unroll
@@ -1002,6 +1014,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     for (int d = threadIdx.x; d < 2048; d += kResThreads)
       if (sh[d]) atomicAdd(&st->hist1[d], sh[d]);
     res_grid_sync(st);
+    res_stamp(1);
     res_pick<2048>(st->hist1, keep, &s_digit, &s_before);
     const unsigned d1 = s_digit;
     unsigned long long need = keep - s_before;
@@ -1017,6 +1030,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     for (int d = threadIdx.x; d < 2048; d += kResThreads)
       if (sh[d]) atomicAdd(&st->hist2[d], sh[d]);
     res_grid_sync(st);
+    res_stamp(2);
     if (blockIdx.x == 0)  // every block has read hist1 (before the barrier): clear it for the next call
       for (int d = threadIdx.x; d < 2048; d += kResThreads) st->hist1[d] = 0;
     res_pick<2048>(st->hist2, need, &s_digit, &s_before);
@@ -1034,6 +1048,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     for (int d = threadIdx.x; d < 1024; d += kResThreads)
       if (sh[d]) atomicAdd(&st->hist3[d], sh[d]);
     res_grid_sync(st);
+    res_stamp(3);
     res_pick<1024>(st->hist3, need, &s_digit, &s_before);
     T = (p2 << 10) | s_digit;
     need_eq = need - s_before;
@@ -1047,6 +1062,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
       res_grid_sync(st);
     }
   }
+  res_stamp(4);
   // ---- fused apply (the same per-scalar arithmetic as lot_apply_kernel)
   unsigned long long eq_before = 0;  // keys == T in lower-indexed blocks
   if (!THRESH && need_eq < eq_total) {
@@ -1105,8 +1121,21 @@ __global__ void __launch_bounds__(kResThreads, 1)
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(tt) : "f"(wi));
         static_cast<float*>(shadow)[i] = __uint_as_float(tt);
       }
+      if constexpr (SHADOW == 3) {  // 3xTF32 pair (kernels.cu store_operand<float>)
+        uint32_t hh, ll;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hh) : "f"(wi));
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(ll) : "f"(wi - __uint_as_float(hh)));
+        static_cast<float*>(shadow)[i] = __uint_as_float(hh);
+        static_cast<float*>(shadow)[i + lo_off] = __uint_as_float(ll);
+      }
+      if constexpr (SHADOW == 4) {  // split bf16 pair (kernels.cu store_shadow<4>)
+        const __nv_bfloat16 hb = __float2bfloat16_rn(wi);
+        static_cast<__nv_bfloat16*>(shadow)[i] = hb;
+        static_cast<__nv_bfloat16*>(shadow)[i + lo_off] = __float2bfloat16_rn(wi - __bfloat162float(hb));
+      }
     }
   }
+  res_stamp(5);
   if constexpr (THRESH) {
     cnt = Red(rtmp).Sum(cnt);
     if (threadIdx.x == 0 && cnt) atomicAdd(&st->count, cnt);
@@ -1207,15 +1236,18 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     unsigned long long* pop = popcount_dev;
     const unsigned long long ukeep = (unsigned long long)keep;
     void* shp = sh.ptr;
+    long long lo_off = sh.kind == 3 ? shadow_lo_offset(n) : sh.lo_off;
     int grid = sms;
     StepOpt o = opt;
-    void* args[] = {&w, (void*)&g, &n, (void*)&chunk, (void*)&E, (void*)&ukeep, &theta, &alpha, &factor, &decay, &shp,
-                    &mask, &R, &pop, &o};
-    const void* fn = nullptr;
-    if (mode == 1) fn = sh.kind == 1 ? (const void*)lot_resident_kernel<1, true>
-                      : sh.kind == 2 ? (const void*)lot_resident_kernel<2, true> : (const void*)lot_resident_kernel<0, true>;
-    else fn = sh.kind == 1 ? (const void*)lot_resident_kernel<1, false>
-              : sh.kind == 2 ? (const void*)lot_resident_kernel<2, false> : (const void*)lot_resident_kernel<0, false>;
+    void* args[] = {&w,   (void*)&g, &n,    (void*)&chunk, (void*)&E, (void*)&ukeep, &theta, &alpha, &factor,
+                    &decay, &shp,    &lo_off, &mask,        &R,        &pop,          &o};
+    const void* fns[2][5] = {{(const void*)lot_resident_kernel<0, false>, (const void*)lot_resident_kernel<1, false>,
+                              (const void*)lot_resident_kernel<2, false>, (const void*)lot_resident_kernel<3, false>,
+                              (const void*)lot_resident_kernel<4, false>},
+                             {(const void*)lot_resident_kernel<0, true>, (const void*)lot_resident_kernel<1, true>,
+                              (const void*)lot_resident_kernel<2, true>, (const void*)lot_resident_kernel<3, true>,
+                              (const void*)lot_resident_kernel<4, true>}};
+    const void* fn = fns[mode == 1 ? 1 : 0][sh.kind >= 0 && sh.kind <= 4 ? sh.kind : 0];
     MOSES_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kResThreads), args, 0, st));
     MOSES_CUDA(cudaGetLastError());
     return 1;
@@ -1267,7 +1299,12 @@ int lottery_step_fused(float* w, const float* g, long long n, int mode, float th
     MOSES_CUDA(cudaMemcpyAsync(popcount_dev, &S->count, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
   }
   MOSES_CUDA(cudaGetLastError());
-  return mode == 1 ? 4 : (compact ? 16 : 8);  // kernels launched
+  if (sh.kind >= 3) refresh_shadow(w, n, sh, st);  // split operand pairs: not written by the pass kernels
+  return (mode == 1 ? 4 : (compact ? 16 : 8)) + (sh.kind >= 3 ? 1 : 0);  // kernels launched
+}
+
+void lottery_res_trace_read(unsigned long long* out8) {
+  MOSES_CUDA(cudaMemcpyFromSymbol(out8, g_res_trace, sizeof(unsigned long long) * 8));
 }
 
 }  // namespace moses
