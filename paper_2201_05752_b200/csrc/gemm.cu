@@ -2,6 +2,7 @@
 // entry point fetched through the runtime, so the library needs no -lcuda),
 // N-tile selection for the 148-SM grid, and the template instantiations.
 #include <mutex>
+#include <unordered_map>
 #include <type_traits>
 
 #include "common.cuh"
@@ -52,8 +53,41 @@ EncodeTiledFn encode_fn() {
 
 // 2-D tiled map over a row-major matrix: `inner` contiguous elements per row,
 // `outer` rows, row stride `ld` elements; box = box_inner x box_outer, 128-B swizzle.
+// Encoded maps are memoised per host thread: a map is a pure function of its arguments, and an eager
+// call (gradients, the Moses step, predict) encodes tens of them on the host before its first launch.
+struct MapKey {
+  const void* base;
+  long long inner, outer, ld;
+  int elem, box_inner, box_outer, swz;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld && elem == o.elem &&
+           box_inner == o.box_inner && box_outer == o.box_outer && swz == o.swz;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.base) * 0x9e3779b97f4a7c15ull;
+    for (long long v : {k.inner, k.outer, k.ld, (long long)k.elem, (long long)k.box_inner, (long long)k.box_outer,
+                        (long long)k.swz})
+      h = (h ^ uint64_t(v)) * 0x100000001b3ull;
+    return size_t(h ^ (h >> 29));
+  }
+};
+CUtensorMap encode_map(const void* base, int elem, long long inner, long long outer, long long ld, int box_inner,
+                       int box_outer, CUtensorMapSwizzle swz);
 CUtensorMap make_map(const void* base, int elem, long long inner, long long outer, long long ld, int box_inner,
                      int box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{base, inner, outer, ld, elem, box_inner, box_outer, int(swz)};
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() >= 4096) cache.clear();  // bounded: callers passing ever-new buffers
+  const CUtensorMap m = encode_map(base, elem, inner, outer, ld, box_inner, box_outer, swz);
+  cache.emplace(key, m);
+  return m;
+}
+CUtensorMap encode_map(const void* base, int elem, long long inner, long long outer, long long ld, int box_inner,
+                       int box_outer, CUtensorMapSwizzle swz) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
   const cuuint64_t strides[1] = {cuuint64_t(ld) * elem};
