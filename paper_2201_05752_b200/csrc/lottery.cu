@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kPassBlock) lot_pass1c_kernel(const float* __r
   unsigned cnt = 0;  // warp-uniform
   unsigned long long above = 0;
   auto flush = [&]() {  // warp-collective
+    __syncwarp();  // the lanes' staging writes before the copy-out reads them
     unsigned long long b = 0;
     if (lane == 0) {
       b = atomicAdd(&st->cand_n, (unsigned long long)cnt);

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     uint2* sc = stage_all + warp * kTkWarpStage;
     unsigned cnt = 0;  // warp-uniform
     auto flush = [&]() {
+      __syncwarp();  // the lanes' staging writes before the copy-out reads them
       unsigned long long b = 0;
       if (lane == 0) b = atomicAdd(&st->cand_n, (unsigned long long)cnt);
       b = __shfl_sync(0xffffffffu, b, 0);

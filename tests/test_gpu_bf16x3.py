@@ -279,3 +279,25 @@ def test_scoring_pair_layers_equal_the_chain(ml, orc, dims):
     assert nrel(s_pair, s_chain) < 1e-6
     ref, _ = orc.forward(dims, p.params, x[:5000], threads=8)
     assert nrel(s_pair[:5000], ref) < TOL_PRED
+
+
+@pytest.mark.parametrize("prec", ["BF16X3", "FP32"])
+@pytest.mark.parametrize("dims", [[164, 512, 512, 1], [512] + [512] * 6 + [1]])
+@pytest.mark.parametrize("mode,value", [(2, 0.5), (1, 0.5)])
+def test_lottery_step_keeps_split_operands_current(prec, dims, mode, value):
+    """The lottery step writes the split operand pairs of the updated weights itself (inside the
+    resident single launch at P = 263K; after the multi-pass step at P = 1.58M): predictions through
+    the stepped handle equal those of a fresh handle built from its downloaded weights, bit for bit."""
+    from paper_2201_05752_b200 import moseslab as ml
+
+    rng = np.random.default_rng(len(dims) + mode)
+    p = ml.init_random(dims, 4, strict=False)
+    dm = ml.DeviceModel(p, getattr(ml, "PREC_" + prec), 256)
+    dm.set_gradients(rng.normal(0, 1e-2, dm.P))
+    ml.lottery_step(dm, mode, value, 0, 1e-3, 1e-2)
+    x = rng.random((200, dims[0]))
+    fresh = ml.DeviceModel(dm.download(), getattr(ml, "PREC_" + prec), 256)
+    assert not np.array_equal(fresh.download().params, p.params)
+    assert np.array_equal(ml.predict(dm, x), ml.predict(fresh, x))
+    dm.close()
+    fresh.close()
