@@ -5,8 +5,8 @@
 //   sample  one full 128-byte line (32 scores) at a hashed position in every 2048-score stratum
 //           (1/64 of the pool, 1/64 of its bytes) -> order-preserving keys, kept, and a histogram of
 //           their top 11 bits
-//   tau     the exact key of sample rank r = k/64 + 4 sqrt(k/64) + 16 from the top: two more
-//           digit histograms (bits 10-20, 0-9) over the sampled keys of the chosen prefix; every key
+//   tau     the key of sample rank r = k/64 + 4 sqrt(k/64) + 16 from the top, to as many further
+//           digit levels (11, 10 bits) over the sampled keys of the chosen prefix as needed; every key
 //           >= tau is a candidate (expected ~64 r of them, >= k with overwhelming probability)
 //   pass    ONE read of the pool (4 float4 loads in flight per thread): keys >= tau appended as
 //           (key, index) through per-warp staging
@@ -34,23 +34,27 @@ constexpr int kTkCap = 16384;
 constexpr int kTkThreads = 1024;
 constexpr int kTkWarps = kTkThreads / 32;
 constexpr int kTkWarpStage = 128;
-constexpr int kTkBins = 2048;
+constexpr int kTkBits0 = 11, kTkBits1 = 11, kTkBits2 = 10;  // digit levels over the 32-bit key
+constexpr int kTkBins0 = 1 << kTkBits0, kTkBins1 = 1 << kTkBits1, kTkBins2 = 1 << kTkBits2;
+constexpr int kTkHist = kTkBins0 + kTkBins1 + kTkBins2;
 constexpr int kTkDynSmem = kTkCap * 8;  // >= the pass staging (kTkWarps * kTkWarpStage * 8)
 static_assert(kTkDynSmem >= kTkWarps * kTkWarpStage * 8, "staging");
 // a digit level is enough once at most this many sampled keys lie at or above its bucket's lower bound
-// (~64x as many candidates expected: ~8K of the 16K candidate capacity)
+// (~64x as many candidates expected: ~8K of the 16K candidate capacity). A 13-bit level 0 (1/16-octave
+// buckets) usually settled a normal pool's top-1024 threshold alone, but with ~50 % more candidates the
+// exact-rank phase cost more than the skipped digit level (101 vs 98 us per call): 11 bits.
 constexpr unsigned kTkLoose = 128;
 
 // Persistent per device, zero between launches: allocated zeroed once, and every launch restores it (the
 // grid barrier's arrival count returns to 0 at each barrier, the histograms are cleared once their last
-// reader has passed the barrier after the pass, the candidate count by the last CTA to have read it), so
-// a call is one launch with no memset in front of it.
+// reader has passed the barrier after the pass, and launches alternate between two candidate counters,
+// each cleared during the other's launch), so a call is one launch with no memset in front of it.
 struct TkState {
   unsigned bar[2];  // grid barrier: arrivals, generation
-  unsigned done;    // CTAs that have read cand_n
+  unsigned parity;  // which candidate counter this launch uses (the other is cleared for the next)
   unsigned pad;
-  unsigned long long cand_n;
-  unsigned hist[3][kTkBins];
+  unsigned long long cand_n[2];
+  unsigned hist[kTkHist];  // level 0 | level 1 | level 2
 };
 
 __device__ __forceinline__ unsigned tk_key(float f) {  // larger float -> larger key (kernels.cu float_key_desc)
@@ -101,16 +105,17 @@ __device__ __forceinline__ void tk_hist_add(unsigned* h, bool in, unsigned d) {
   if (in) atomicAdd(h + d, 1u);
 }
 
-// the digit holding descending rank `need` (1-based) of a global histogram of nb <= 2 * kTkThreads bins:
+// the digit holding descending rank `need` (1-based) of a global histogram of NB bins:
 // out[0] = digit, out[1] = its rank within the digit, out[2] = keys at or above the digit's lower bound
 template <int NB>
 __device__ __forceinline__ void tk_pick(const unsigned* gh, unsigned need, unsigned* out, void* scan_tmp) {
   using Scan = cub::BlockScan<unsigned, kTkThreads>;
-  constexpr int PER = NB / kTkThreads;
+  constexpr int PER = NB >= kTkThreads ? NB / kTkThreads : 1;
   unsigned c[PER], tot = 0;
 #pragma unroll
   for (int u = 0; u < PER; ++u) {  // bins in descending digit order
-    c[u] = __ldcg(gh + (NB - 1 - (int(threadIdx.x) * PER + u)));
+    const int b = int(threadIdx.x) * PER + u;
+    c[u] = b < NB ? __ldcg(gh + (NB - 1 - b)) : 0u;
     tot += c[u];
   }
   unsigned excl;
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     tk_fused_kernel(const float* __restrict__ s, long long n, long long k, unsigned r, TkState* st,
                     unsigned* __restrict__ keys, uint2* __restrict__ cand, unsigned* __restrict__ out_key,
                     long long* __restrict__ out_idx, unsigned* __restrict__ fail_out) {
-  __shared__ unsigned h[kTkBins];
+  __shared__ unsigned h[kTkBins0];
   extern __shared__ __align__(16) uint2 dyn[];  // pass: per-warp staging; final: the candidates
   uint2* stage_all = dyn;
   __shared__ unsigned part[kTkWarps * 32];  // final: partial ranks
@@ -146,8 +151,10 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     g_tk_trace[9] = ~0ull;
     g_tk_trace[10] = 0;
   }
-  // ---- sample + histogram of the top 11 key bits
-  for (int i = t; i < kTkBins; i += kTkThreads) h[i] = 0;
+  const unsigned par = __ldcg(&st->parity);
+  unsigned long long* cand_n = &st->cand_n[par];
+  // ---- sample + histogram of the top kTkBits0 key bits
+  for (int i = t; i < kTkBins0; i += kTkThreads) h[i] = 0;
   __syncthreads();
   {  // SU strata per warp in flight (each line is one dependent HBM round trip otherwise)
     constexpr int SU = 8;
@@ -167,33 +174,35 @@ __global__ void __launch_bounds__(kTkThreads, 1)
         const bool ok = j < strata;
         const unsigned key = tk_key(v[u]);
         if (ok) keys[j * kTkLine + lane] = key;
-        tk_hist_add(h, ok, key >> 21);
+        tk_hist_add(h, ok, key >> (32 - kTkBits0));
       }
     }
   }
   tk_stamp(7);
   __syncthreads();
-  for (int i = t; i < kTkBins; i += kTkThreads)
-    if (h[i]) atomicAdd(&st->hist[0][i], h[i]);
+  for (int i = t; i < kTkBins0; i += kTkThreads)
+    if (h[i]) atomicAdd(&st->hist[i], h[i]);
   tk_grid_sync(st->bar);
   tk_stamp(1);
 
   // ---- tau: the sample key of rank r to as many digit levels (11, 11, 10 bits) as the candidate count
   // needs — the lower bound of the bucket holding it once few enough sampled keys lie at or above that
   // bound (a lower tau only adds candidates), the exact key after all three levels
-  tk_pick<kTkBins>(st->hist[0], r, sel, scan_tmp);
+  tk_pick<kTkBins0>(st->hist, r, sel, scan_tmp);
   unsigned prefix = sel[0], need = sel[1], ge = sel[2];
-  int bits = 11;
+  int bits = kTkBits0;
   const long long gt = (long long)gridDim.x * kTkThreads;
   const long long q4 = ns / 4;
   constexpr int LU = 4;  // sampled-key loads in flight per thread
   const long long qend = (q4 + gt * LU - 1) / (gt * LU) * (gt * LU);
   int lev = 1;
   for (; lev <= 2 && ge > kTkLoose; ++lev) {
-    const int shift = lev == 1 ? 21 : 10;  // prefix bits are key >> shift
-    const unsigned dmask = lev == 1 ? 2047u : 1023u;
-    const int dshift = lev == 1 ? 10 : 0;
-    for (int i = t; i < kTkBins; i += kTkThreads) h[i] = 0;
+    const int shift = 32 - bits;  // prefix bits are key >> shift
+    const int dbits = lev == 1 ? kTkBits1 : kTkBits2;
+    const unsigned dmask = (1u << dbits) - 1u;
+    const int dshift = shift - dbits;
+    unsigned* gh = st->hist + (lev == 1 ? kTkBins0 : kTkBins0 + kTkBins1);
+    for (int i = t; i <= int(dmask); i += kTkThreads) h[i] = 0;
     __syncthreads();
     for (long long q0 = blockIdx.x * (long long)kTkThreads + t; q0 < qend; q0 += gt * LU) {
       uint4 v[LU];
@@ -213,15 +222,15 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     }
     __syncthreads();
     for (int i = t; i <= int(dmask); i += kTkThreads)
-      if (h[i]) atomicAdd(&st->hist[lev][i], h[i]);
+      if (h[i]) atomicAdd(gh + i, h[i]);
     tk_grid_sync(st->bar);
     tk_stamp(1 + lev);
-    if (lev == 1) tk_pick<kTkBins>(st->hist[1], need, sel, scan_tmp);
-    else tk_pick<kTkThreads>(st->hist[2], need, sel, scan_tmp);
-    prefix = (prefix << (lev == 1 ? 11 : 10)) | sel[0];
+    if (lev == 1) tk_pick<kTkBins1>(gh, need, sel, scan_tmp);
+    else tk_pick<kTkBins2>(gh, need, sel, scan_tmp);
+    prefix = (prefix << dbits) | sel[0];
     ge = (r - need) + sel[2];  // keys above the previous bucket + those at or above this one's bound in it
     need = sel[1];
-    bits += lev == 1 ? 11 : 10;
+    bits += dbits;
   }
   for (; lev <= 2; ++lev) tk_stamp(1 + lev);
   const unsigned tau = bits == 32 ? prefix : prefix << (32 - bits);
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     auto flush = [&]() {
       __syncwarp();  // the lanes' staging writes before the copy-out reads them
       unsigned long long b = 0;
-      if (lane == 0) b = atomicAdd(&st->cand_n, (unsigned long long)cnt);
+      if (lane == 0) b = atomicAdd(cand_n, (unsigned long long)cnt);
       b = __shfl_sync(0xffffffffu, b, 0);
       if (b + cnt <= kTkCap)
         for (unsigned i = lane; i < cnt; i += 32) cand[b + i] = sc[i];
@@ -293,18 +302,14 @@ __global__ void __launch_bounds__(kTkThreads, 1)
   tk_grid_sync(st->bar);
   tk_stamp(5);
   // every CTA is past its last histogram read: clear them for the next launch
-  for (int i = blockIdx.x * kTkThreads + t; i < 3 * kTkBins; i += gridDim.x * kTkThreads) (&st->hist[0][0])[i] = 0;
+  for (int i = blockIdx.x * kTkThreads + t; i < kTkHist; i += gridDim.x * kTkThreads) st->hist[i] = 0;
+  if (blockIdx.x == 0 && t == 0) {  // every CTA read `parity` at its start: the next launch uses the other
+    st->cand_n[par ^ 1u] = 0;       // counter (unused by this one), so this one's needs no clearing barrier
+    st->parity = par ^ 1u;
+  }
 
   // ---- exact ranks of the candidates; the first k out
-  if (t == 0) {
-    sel[0] = unsigned(min(__ldcg(&st->cand_n), (unsigned long long)kTkCap + 1));
-    unsigned prev;  // the last CTA to have read the count clears it
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&st->done) : "memory");
-    if (prev == gridDim.x - 1) {
-      st->cand_n = 0;
-      st->done = 0;
-    }
-  }
+  if (t == 0) sel[0] = unsigned(min(__ldcg(cand_n), (unsigned long long)kTkCap + 1));
   __syncthreads();
   const unsigned c = sel[0];
   if (blockIdx.x == 0 && t == 0) g_tk_trace[8] = c;
