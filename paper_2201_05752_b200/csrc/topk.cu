@@ -4,15 +4,15 @@
 // ONE cooperative kernel, phases separated by grid barriers:
 //   sample  one full 128-byte line (32 scores) at a hashed position in every 2048-score stratum
 //           (1/64 of the pool, 1/64 of its bytes) -> order-preserving keys, kept, and a histogram of
-//           their top 11 bits
+//           their top 13 bits
 //   tau     the key of sample rank r = k/64 + 4 sqrt(k/64) + 16 from the top, to as many further
-//           digit levels (11, 10 bits) over the sampled keys of the chosen prefix as needed; every key
+//           digit levels (11, 8 bits) over the sampled keys of the chosen prefix as needed; every key
 //           >= tau is a candidate (expected ~64 r of them, >= k with overwhelming probability)
 //   pass    ONE read of the pool (4 float4 loads in flight per thread): keys >= tau appended as
 //           (key, index) through per-warp staging
 //   final   exact rank of every candidate by counting the candidates that precede it in
-//           (key desc, index asc) order — lanes own candidates, warps split the comparisons, spread
-//           over the whole grid — and the first k written at their ranks
+//           (key desc, index asc) order — (candidate block, comparison chunk) items over every warp,
+//           partial counts summed with integer atomics — and the first k written at their ranks
 // If the candidates overflow or fall short of k (adversarial score layouts), the kernel raises a flag
 // and the caller runs the exact three-pass radix select instead (kernels.cu). Either way the result is
 // the exact top-k: the candidate set holds every key >= tau and at least k keys, so it holds the top k.
@@ -34,16 +34,17 @@ constexpr int kTkCap = 16384;
 constexpr int kTkThreads = 1024;
 constexpr int kTkWarps = kTkThreads / 32;
 constexpr int kTkWarpStage = 128;
-constexpr int kTkBits0 = 11, kTkBits1 = 11, kTkBits2 = 10;  // digit levels over the 32-bit key
+constexpr int kTkBits0 = 13, kTkBits1 = 11, kTkBits2 = 8;  // digit levels over the 32-bit key
 constexpr int kTkBins0 = 1 << kTkBits0, kTkBins1 = 1 << kTkBits1, kTkBins2 = 1 << kTkBits2;
 constexpr int kTkHist = kTkBins0 + kTkBins1 + kTkBins2;
 constexpr int kTkDynSmem = kTkCap * 8;  // >= the pass staging (kTkWarps * kTkWarpStage * 8)
 static_assert(kTkDynSmem >= kTkWarps * kTkWarpStage * 8, "staging");
 // a digit level is enough once at most this many sampled keys lie at or above its bucket's lower bound
-// (~64x as many candidates expected: ~8K of the 16K candidate capacity). A 13-bit level 0 (1/16-octave
-// buckets) usually settled a normal pool's top-1024 threshold alone, but with ~50 % more candidates the
-// exact-rank phase cost more than the skipped digit level (101 vs 98 us per call): 11 bits.
-constexpr unsigned kTkLoose = 128;
+// (~64x as many candidates expected: ~10K of the 16K candidate capacity). The 13-bit level 0
+// (1/16-octave buckets) usually settles a normal pool's top-1024 threshold alone (5.4K candidates
+// instead of 3.7K after a second level): with the grid-wide exact-rank phase on composite keys that
+// is 95 vs 96 us per call over 100M scores.
+constexpr unsigned kTkLoose = 160;
 
 // Persistent per device, zero between launches: allocated zeroed once, and every launch restores it (the
 // grid barrier's arrival count returns to 0 at each barrier, the histograms are cleared once their last
@@ -134,12 +135,12 @@ __device__ __forceinline__ void tk_pick(const unsigned* gh, unsigned need, unsig
 
 __global__ void __launch_bounds__(kTkThreads, 1)
     tk_fused_kernel(const float* __restrict__ s, long long n, long long k, unsigned r, TkState* st,
-                    unsigned* __restrict__ keys, uint2* __restrict__ cand, unsigned* __restrict__ out_key,
+                    unsigned* __restrict__ keys, uint2* __restrict__ cand, unsigned* __restrict__ ranks,
+                    unsigned* __restrict__ out_key,
                     long long* __restrict__ out_idx, unsigned* __restrict__ fail_out) {
   __shared__ unsigned h[kTkBins0];
   extern __shared__ __align__(16) uint2 dyn[];  // pass: per-warp staging; final: the candidates
   uint2* stage_all = dyn;
-  __shared__ unsigned part[kTkWarps * 32];  // final: partial ranks
   __shared__ __align__(16) unsigned char scan_tmp[sizeof(typename cub::BlockScan<unsigned, kTkThreads>::TempStorage)];
   __shared__ unsigned sel[3];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     g_tk_trace[9] = ~0ull;
     g_tk_trace[10] = 0;
   }
+  for (int i = int(blockIdx.x) * kTkThreads + t; i < kTkCap; i += int(gridDim.x) * kTkThreads) ranks[i] = 0;
   const unsigned par = __ldcg(&st->parity);
   unsigned long long* cand_n = &st->cand_n[par];
   // ---- sample + histogram of the top kTkBits0 key bits
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
   tk_grid_sync(st->bar);
   tk_stamp(1);
 
-  // ---- tau: the sample key of rank r to as many digit levels (11, 11, 10 bits) as the candidate count
+  // ---- tau: the sample key of rank r to as many digit levels (13, 11, 8 bits) as the candidate count
   // needs — the lower bound of the bucket holding it once few enough sampled keys lie at or above that
   // bound (a lower tau only adds candidates), the exact key after all three levels
   tk_pick<kTkBins0>(st->hist, r, sel, scan_tmp);
@@ -319,33 +321,40 @@ __global__ void __launch_bounds__(kTkThreads, 1)
   }
   if (blockIdx.x == 0 && t == 0) *fail_out = 0;
   const int cn = int(c);
-  const int items = (cn + 31) / 32;
-  if (int(blockIdx.x) >= items) return;
-  for (int i = t; i < (cn + 1) / 2; i += kTkThreads)  // all candidates into shared memory (16 B loads)
-    reinterpret_cast<uint4*>(dyn)[i] = __ldcg(reinterpret_cast<const uint4*>(cand) + i);
-  __syncthreads();
-  const int j0 = int((long long)cn * warp / kTkWarps), j1 = int((long long)cn * (warp + 1) / kTkWarps);
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    const int i = it * 32 + lane;
-    const uint2 me = i < cn ? dyn[i] : make_uint2(0u, 0xffffffffu);
-    unsigned before = 0;
-#pragma unroll 4
-    for (int j = j0; j < j1; ++j) {
-      const uint2 o = dyn[j];  // one address per warp: a broadcast
-      before += (o.x > me.x) | ((o.x == me.x) & (o.y < me.y));
+  // (block of 32 candidates, chunk of the comparisons) items over every warp of the grid: lanes own
+  // candidates, each item counts the candidates of its chunk that precede them, the partial counts meet
+  // in ranks[] (atomics: integer sums, any order) — then one barrier and the first k written at their ranks
+  const int cb_n = (cn + 31) / 32;
+  const int gw = int(gridDim.x) * kTkWarps;
+  const int jc_n = max(1, gw / cb_n);
+  const int items = cb_n * jc_n;
+  if (int(blockIdx.x) * kTkWarps < items) {  // CTA-uniform
+    // order-composite keys: (key << 32) | ~index is larger exactly when the candidate comes first
+    unsigned long long* comp = reinterpret_cast<unsigned long long*>(dyn);
+    for (int i = t; i < cn; i += kTkThreads) {
+      const uint2 v = __ldcg(cand + i);
+      comp[i] = (static_cast<unsigned long long>(v.x) << 32) | static_cast<unsigned long long>(~v.y);
     }
-    part[warp * 32 + lane] = before;
     __syncthreads();
-    if (warp == 0) {
-      unsigned rank = 0;
+    for (int it = int(blockIdx.x) * kTkWarps + warp; it < items; it += gw) {
+      const int cb = it / jc_n, jc = it - cb * jc_n;
+      const int i = cb * 32 + lane;
+      const unsigned long long me = i < cn ? comp[i] : ~0ull;
+      const int j0 = int((long long)cn * jc / jc_n), j1 = int((long long)cn * (jc + 1) / jc_n);
+      unsigned before = 0;
 #pragma unroll 8
-      for (int w = 0; w < kTkWarps; ++w) rank += part[w * 32 + lane];
-      if (i < cn && rank < unsigned(k)) {
-        out_key[rank] = me.x;
-        out_idx[rank] = (long long)me.y;
-      }
+      for (int j = j0; j < j1; ++j) before += comp[j] > me ? 1u : 0u;  // one address per warp: a broadcast
+      if (i < cn && before) atomicAdd(ranks + i, before);
     }
-    __syncthreads();
+  }
+  tk_grid_sync(st->bar);
+  for (int i = int(blockIdx.x) * kTkThreads + t; i < cn; i += int(gridDim.x) * kTkThreads) {
+    const unsigned rank = __ldcg(ranks + i);
+    if (rank < unsigned(k)) {
+      const uint2 me = __ldcg(cand + i);
+      out_key[rank] = me.x;
+      out_idx[rank] = (long long)me.y;
+    }
   }
   tk_stamp(6);
 }
@@ -371,8 +380,8 @@ void topk_trace_read(unsigned long long* out16) {
 
 static long long tk_samples(long long n) { return n / kTkStratum * kTkLine; }
 
-size_t topk_fast_ws_bytes(long long n) {  // [flag word | candidates | sampled keys]
-  return 256 + size_t(kTkCap) * 8 + size_t(std::max(tk_samples(n), 1ll)) * 4 + 256;
+size_t topk_fast_ws_bytes(long long n) {  // [flag word | candidates | ranks | sampled keys]
+  return 256 + size_t(kTkCap) * 12 + size_t(std::max(tk_samples(n), 1ll)) * 4 + 256;
 }
 
 static TkState* tk_state() {
@@ -401,10 +410,11 @@ bool topk_fast_launch(const float* scores, long long n, long long k, void* ws, u
   TkState* S = tk_state();
   uint8_t* p = static_cast<uint8_t*>(ws) + 256;
   uint2* cand = reinterpret_cast<uint2*>(p);
-  unsigned* keys = reinterpret_cast<unsigned*>(p + size_t(kTkCap) * 8);
+  unsigned* ranks = reinterpret_cast<unsigned*>(p + size_t(kTkCap) * 8);
+  unsigned* keys = ranks + kTkCap;
   unsigned ru = unsigned(r);
-  void* args[] = {(void*)&scores, (void*)&n, (void*)&k, (void*)&ru, (void*)&S, (void*)&keys, (void*)&cand,
-                  (void*)&out_key, (void*)&out_idx, (void*)&fail_out};
+  void* args[] = {(void*)&scores, (void*)&n,   (void*)&k,       (void*)&ru,      (void*)&S,       (void*)&keys,
+                  (void*)&cand,   (void*)&ranks, (void*)&out_key, (void*)&out_idx, (void*)&fail_out};
   const int grid = tk_grid();
   MOSES_CUDA(cudaLaunchCooperativeKernel((const void*)tk_fused_kernel, dim3(grid), dim3(kTkThreads), args, kTkDynSmem, st));
   return true;
