@@ -49,6 +49,8 @@ for mode, name in ((2, "ratio 0.5"), (1, "threshold 0.5")):
         torch.cuda.synchronize()
     L.moses_set_async(0)
     evs = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+    if not evs:  # CUPTI taken (e.g. running under ncu): no timeline
+        break
     t0 = evs[0].time_range.start
     print("---", name)
     for e in evs:
